@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 randomized-Tucker hot path (BASELINE.json metric:
+"TTM GB/s of Y streamed (% HBM peak) + e2e Tucker+FFCP sec at 1/2/4/8 GPU").
+
+A step is one full rand_tucker_2i decomposition (paper Alg. 3, tucker.hpp:136-169) of the
+resident tensor Y: 2N Y-streaming TTM passes + 2N sketches/QRs + the core. The default
+workload is BASELINE configs[1] (1000^3 fp32, Tucker core 20^3, SNR 20 dB, ranks 20,
+oversample 10, FFCP rank 20), synthetic from the reference's seeded generators.
+
+  value      = Y bytes streamed per step / device time per step (GB/s, inputs in HBM)
+  e2e        = same metric through the public API with a pinned host Y: H2D copy +
+               decomposition + FFCP + D2H of the model inside the timed region
+  roofline   = the Y-streaming TTM kernel: |Y| bytes per launch / its mean CUDA-event time,
+               against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline / --impl reference = the CPU oracle (restated reference, oracle/) on the
+               box's host cores over a bounded slab of the same workload
+
+Multi-GPU (torchrun, one process per GPU): weak scaling — every rank holds one
+1000^3 slab of a 1000 x 1000 x (1000 N) tensor (last-mode slabs, dist.hpp:70-123); partial
+sketches and cores are all-reduced over NCCL (the library's tk_comm hook).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs (index in parentheses)
+    "cfg1": dict(idx=0, dims=(200, 200, 200), dtype="f64", gen="cp_uniform", cp_rank=10, snr=10.0, ranks=(10, 10, 10),
+                 p=5, ffcp_rank=10, constraint=0),
+    "cfg2": dict(idx=1, dims=(1000, 1000, 1000), dtype="f32", gen="tucker", mlrank=(20, 20, 20), snr=20.0,
+                 ranks=(20, 20, 20), p=10, ffcp_rank=20, constraint=0),
+    "cfg3": dict(idx=2, dims=(2400, 2400, 2400), dtype="f32", gen="tucker", mlrank=(30, 30, 30), snr=20.0,
+                 ranks=(30, 30, 30), p=10, ffcp_rank=30, constraint=0),
+    "cfg4": dict(idx=3, dims=(300, 300, 300, 300), dtype="f32", gen="cp_uniform", cp_rank=15, snr=30.0,
+                 abs_noise=True, ranks=(15, 15, 15, 15), p=5, ffcp_rank=15, constraint=2),
+}
+STOP = (200, 1e-6)  # bench default StopRule{200, 1e-6} (bench.hpp:274)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def all_max(x: float, world: int) -> float:
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _all_sum(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_decompose(y64, cfg, seed, threads, with_ffcp=True):
+    from oracle import pyoracle as O
+    O.set_threads(threads)
+    t0 = time.perf_counter()
+    g, us = O.rand_tucker_2i(y64, cfg["ranks"], cfg["p"], (seed.root, seed.stream))
+    t1 = time.perf_counter()
+    if with_ffcp:
+        O.ffcp(g, us, cfg["ffcp_rank"], cfg["constraint"], 0.0, STOP[0], STOP[1], (seed.root, seed.stream))
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t0
+
+
+def cpu_sample(cfg, y_dev_flat, slabs):
+    """A bounded slab Y[..., :slabs] of the workload (host fp64), the CPU baseline's sample."""
+    dims = list(cfg["dims"])
+    n = int(np.prod(dims[:-1])) * slabs
+    y = y_dev_flat[:n].double().cpu().numpy()
+    dims[-1] = slabs
+    return y.reshape(dims, order="F"), dims
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference algorithm (restated CPU oracle; the reference itself
+    cannot be built here: no Eigen/Catch2) on the box's host cores, bounded slab sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from paper_1412_1885_b200.generators import bench_seeds, generate
+    threads = os.cpu_count() or 1
+    _, alg_seed = bench_seeds(0)
+    slabs = args.cpu_slabs
+    if torch.cuda.is_available():
+        y = generate(cfg)
+        ys, sdims = cpu_sample(cfg, y.float() if cfg["dtype"] == "f32" else y, slabs)
+        del y
+        torch.cuda.empty_cache()
+    else:  # host-only fallback for the sample generator: the oracle's own generators
+        from oracle import pyoracle as O
+        from paper_1412_1885_b200.generators import bench_seeds as bs
+        ds, _ = bs(0)
+        sdims = list(cfg["dims"])
+        sdims[-1] = slabs
+        O.set_threads(threads)
+        ys = O.gen_tucker(sdims, cfg["mlrank"], (ds.root, ds.stream))
+    passes = 2 * len(cfg["dims"]) + 1
+    elem_bytes = 4 if cfg["dtype"] == "f32" else 8
+    sample_bytes = ys.size * elem_bytes
+    for _ in range(args.warmup):
+        oracle_decompose(ys, cfg, alg_seed, threads, with_ffcp=False)
+    times, e2e = [], []
+    for _ in range(args.steps):
+        tc, te = oracle_decompose(ys, cfg, alg_seed, threads)
+        times.append(tc)
+        e2e.append(te)
+    ms = 1e3 * statistics.mean(times)
+    value = passes * sample_bytes / (statistics.mean(times)) / 1e9
+    e2e_v = passes * sample_bytes / (statistics.mean(e2e)) / 1e9
+    sample = f"rand_tucker_2i+ffcp on the {'x'.join(map(str, sdims))} slab of the workload (fp64 oracle, OpenBLAS {threads} threads)"
+    line = {
+        "metric": "TTM GB/s of Y streamed (% HBM peak) + e2e Tucker+FFCP sec at 1/2/4/8 GPU",
+        "impl": "reference", "value": round(value, 3), "unit": "GB/s", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference seeded generators, bench.hpp:46-112)",
+        "config": {"workload": args.config, "dims": list(cfg["dims"]), "ranks": list(cfg["ranks"]),
+                   "oversample": cfg["p"], "ffcp_rank": cfg["ffcp_rank"], "passes_per_step": passes,
+                   "sample_dims": sdims},
+        "e2e": {"value": round(e2e_v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "tucker_ffcp_seconds": round(statistics.mean(e2e), 4),
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def run_b200(args, cfg):
+    import torch
+    import paper_1412_1885_b200 as P
+    from paper_1412_1885_b200 import dist as D
+    from paper_1412_1885_b200.generators import bench_seeds, generate
+
+    rank, world, local = dist_setup(args.gpus)
+    ctx = P.Context.default(local)
+    ctx.bind_torch_stream()
+    tdt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+    dims = list(cfg["dims"])
+    gdims = list(dims)
+    gdims[-1] = dims[-1] * world
+    slab_offset = rank * dims[-1]
+    _, alg_seed = bench_seeds(0)
+
+    # ---- data (untimed): this rank's slab. Weak scaling: slab r of the global tensor is
+    # the seeded workload generated with run index r (independent data per slab).
+    cfg_r = dict(cfg, seed=0)
+    y64 = generate(cfg_r) if world == 1 else _gen_slab(cfg, rank)
+    y = y64.to(tdt)
+    del y64
+    torch.cuda.empty_cache()
+    yd = P.DenseTensor(dims, y)
+    ybytes = y.numel() * y.element_size()
+    comm = None
+    if world > 1:
+        comm = D.DistComm(slab_offset, gdims[-1], D.exchange_capacity(gdims, cfg["ranks"], cfg["p"]))
+        ctx.set_comm(comm)
+    kw = dict(sync_ranks=False, out="device", global_last_dim=gdims[-1] if world > 1 else 0)
+
+    def step(time_kernels=False):
+        return P.rand_tucker_2i(yd, cfg["ranks"], cfg["p"], alg_seed, context=ctx, time_kernels=time_kernels, **kw)
+
+    for _ in range(max(args.warmup, 3)):
+        m = step()
+    barrier(world)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream_ms, stream_launches, launches = 0.0, 0, 0
+    with ClockSampler(local) as clk:
+        barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            m = step(time_kernels=True)
+            stream_ms += m.stats["stream_ms"]
+            stream_launches += m.stats["stream_launches"]
+            launches += m.stats["kernel_launches"]
+        ev1.record(stream)
+        barrier(world)
+    dev_ms = ev0.elapsed_time(ev1)
+    dev_ms = all_max(dev_ms, world)
+    ms_step = dev_ms / args.steps
+    passes = m.stats["passes"]
+    value = world * passes * ybytes / (ms_step * 1e-3) / 1e9
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    kern_ms = stream_ms / max(stream_launches, 1)
+    achieved = ybytes / (kern_ms * 1e-3) / 1e9
+    traffic = _ncu_traffic()
+
+    # ---- sanity on the bench workload: fit of the Tucker model to Y from the Gram identity
+    # ||Y - G x U||^2 = ||Y||^2 - ||G||^2 (orthonormal U); global norms summed over ranks
+    ysq = float(torch.linalg.vector_norm(y.double()).item() ** 2)
+    if world > 1:
+        ysq = _all_sum(ysq)
+    gsq = float(torch.linalg.vector_norm(m.core).item() ** 2)
+    fit_model = 1.0 - float(np.sqrt(max(0.0, 1.0 - gsq / ysq)))
+
+    # ---- e2e through the public API with a pinned host Y
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(y.numel(), dtype=tdt, pin_memory=True)
+        host.copy_(y)
+        torch.cuda.synchronize()
+        yh = P.DenseTensor(dims, host.numpy())
+        del y
+        yd = None
+        torch.cuda.empty_cache()
+        e2e_times, h2d, d2h = [], 0, 0
+        for it in range(1 + args.e2e_steps):
+            barrier(world)
+            t0 = time.perf_counter()
+            mm = P.rand_tucker_2i(yh, cfg["ranks"], cfg["p"], alg_seed, context=ctx, sync_ranks=False,
+                                  global_last_dim=kw["global_last_dim"])
+            res = P.ffcp(mm, cfg["ffcp_rank"], P.ConstraintSpec(cfg["constraint"]), P.StopRule(*STOP), alg_seed,
+                         context=ctx)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            if it > 0:
+                e2e_times.append(all_max(t1 - t0, world))
+            h2d = ybytes
+            d2h = (mm.core.size + sum(u.size for u in mm.factors)) * 8
+        e2e_s = statistics.mean(e2e_times)
+        e2e = {"value": round(world * passes * ybytes / e2e_s / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "tucker_ffcp_seconds": round(e2e_s, 4), "ffcp_iterations": int(res.iterations),
+               "ffcp_fit": float(res.fit_trace[-1])}
+
+    # ---- CPU baseline (rank 0, N=1 only): oracle on a bounded slab
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        yy = generate(cfg_r)
+        ys, sdims = cpu_sample(cfg, yy.to(tdt), args.cpu_slabs)
+        del yy
+        torch.cuda.empty_cache()
+        tc, te = oracle_decompose(ys, cfg, alg_seed, threads, with_ffcp=False)
+        pref = 2 * len(dims) + 1
+        cpu = {"value": round(pref * ys.size * (4 if cfg["dtype"] == "f32" else 8) / tc / 1e9, 3), "unit": "GB/s",
+               "cores": threads, "kind": "port",
+               "sample": f"rand_tucker_2i on the {'x'.join(map(str, sdims))} slab (fp64 oracle, OpenBLAS {threads} threads), {pref} passes"}
+
+    if rank == 0:
+        line = {
+            "metric": "TTM GB/s of Y streamed (% HBM peak) + e2e Tucker+FFCP sec at 1/2/4/8 GPU",
+            "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if cfg["dtype"] == "f32" else "f64",
+            "data": "synthetic (reference seeded generators bench.hpp:46-112 on device; Y > L2, no flush needed)",
+            "config": {"workload": args.config, "dims": gdims, "ranks": list(cfg["ranks"]), "oversample": cfg["p"],
+                       "ffcp_rank": cfg["ffcp_rank"], "passes_per_step": passes, "parallelism": f"slab{world}",
+                       "l2": "inputs larger than L2 (126 MB)", "core": "derived from X_{N-1} (2N passes)"},
+            "hbm_frac_of_peak": round(value / world / hbm, 4),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": traffic,
+                         "kernel": "ttm_mmajor_kernel (Y-streaming TTM)", "peak_source": "measured" if not pk.get("_fallback") else "fallback",
+                         "bytes_per_launch": ybytes, "mean_launch_ms": round(kern_ms, 4)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "fit_model": round(fit_model, 6),
+        }
+        if e2e:
+            line["e2e"] = e2e
+            line["tucker_ffcp_seconds"] = e2e["tucker_ffcp_seconds"]
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _gen_slab(cfg, rank):
+    from paper_1412_1885_b200.generators import generate
+    return generate(dict(cfg, seed=rank))
+
+
+def _ncu_traffic():
+    """DRAM bytes per launch of the TTM kernel from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ttm_traffic.json")
+    try:
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-slabs", type=int, default=100)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,143 @@
+/* tenkit_b200.h — C-ABI of the B200-native randomized-Tucker hot path.
+ *
+ * The reference (`tenkit`, arXiv 1412.1885) is a header-only C++20 library with no FFI
+ * layer; its boundary is the set of free functions in namespace tenkit. Each
+ * entry point below replaces one of them, with plain pointers and sizes (no torch types):
+ *
+ *   tk_rand_tucker_2i     <- tenkit::rand_tucker_2i      tucker.hpp:136-169 (Alg. 3)
+ *   tk_rand_tucker        <- tenkit::rand_tucker         tucker.hpp:108-130 (Alg. 2)
+ *   tk_ttm                <- tenkit::ttm                 tensor.hpp:151-176
+ *   tk_ttm_all            <- tenkit::ttm_all             tensor.hpp:181-192
+ *   tk_unfold_times       <- tenkit::unfold_times        tensor.hpp:195-209
+ *   tk_orthonormal_basis  <- tenkit::orthonormal_basis   range_finder.hpp:18-29
+ *                            + detail::fix_column_signs  tucker.hpp:39-45
+ *   tk_gaussian_matrix    <- tenkit::gaussian_matrix     random.hpp:85-100
+ *   tk_seed_derived       <- tenkit::SeedSpec::derived   random.hpp:36-41
+ *   tk_ffcp               <- tenkit::ffcp                ffcp.hpp:94-194
+ *
+ * Layouts are the reference's: column-major, mode 0 fastest (tensor.hpp:31). Errors: every
+ * call returns TK_OK or a code; the reference's std::invalid_argument("tenkit: ...")
+ * (tensor.hpp:20-22) maps to TK_ERR_INVALID with the same message in tk_last_error().
+ * There is no CPU fallback: without a usable sm_100 device every compute call returns
+ * TK_ERR_NO_DEVICE.
+ */
+#ifndef TENKIT_B200_H
+#define TENKIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TK_MAX_ORDER 8
+
+enum tk_status { TK_OK = 0, TK_ERR_INVALID = 1, TK_ERR_CUDA = 2, TK_ERR_NO_DEVICE = 3, TK_ERR_INTERNAL = 4 };
+enum tk_dtype { TK_F32 = 0, TK_F64 = 1 };
+enum tk_constraint { TK_CP_NONE = 0, TK_CP_NONNEG_MU = 1, TK_CP_NONNEG_HALS = 2, TK_CP_SPARSE = 3 };
+
+typedef struct tk_context tk_context;
+
+/* Cross-rank reduction hook for slab-partitioned Y (dist.hpp:617-800 semantics: partial
+ * sketches and partial cores are summed over ranks). The library writes `count` doubles
+ * at the front of `xbuf` (a caller-owned device buffer of `xbuf_capacity` doubles) and
+ * calls allreduce_sum(user, count, stream); on return xbuf holds the sum over ranks.
+ * This rank owns rows [slab_offset, slab_offset + local I_{N-1}) of the last mode of a
+ * tensor whose global last-mode size is global_last_dim. */
+typedef struct tk_comm {
+    int rank;
+    int world;
+    int64_t slab_offset;
+    int64_t global_last_dim;
+    double* xbuf;
+    int64_t xbuf_capacity;
+    int (*allreduce_sum)(void* user, int64_t count, void* cuda_stream);
+    void* user;
+} tk_comm;
+
+/* Output of the Tucker drivers (TuckerModel, tucker.hpp:14-33). Pointers are device
+ * pointers when on_device != 0, else host pointers; capacities: core prod_n rt_n doubles,
+ * factor n I_n*rt_n doubles (rt_n = min(R_n + p, I_n)). Actual shapes are returned. */
+typedef struct tk_tucker_out {
+    int on_device;
+    double* core;
+    int64_t core_shape[TK_MAX_ORDER];
+    double* factors[TK_MAX_ORDER];
+    int64_t factor_cols[TK_MAX_ORDER];
+} tk_tucker_out;
+
+typedef struct tk_tucker_opts {
+    int explicit_core_pass; /* 1: core = Y x_all U^T as its own pass (reference tucker.hpp:166);
+                               0: core = X_{N-1} x_{N-1} U_{N-1}^T (same value, saves a Y pass) */
+    int sync_ranks;         /* 1 (default): read each step's rank on the host (exact on rank
+                               drop); 0: speculate full rank, verify once at the end, rerun
+                               synchronously if any rank dropped */
+    int time_kernels;       /* 1: bracket every Y-streaming launch with CUDA events on the
+                               call's stream and report their summed device time in stats */
+} tk_tucker_opts;
+
+/* Per-call timing/trace (filled when non-null) */
+typedef struct tk_tucker_stats {
+    int passes;            /* full Y passes */
+    int kernel_launches;   /* kernels this call launched */
+    double y_bytes;        /* bytes of (local) Y */
+    int ranks[2 * TK_MAX_ORDER];
+    int stream_launches;   /* Y-streaming (first-stage TTM) launches */
+    double stream_ms;      /* their summed CUDA-event time (time_kernels = 1) */
+} tk_tucker_stats;
+
+const char* tk_last_error(void);
+int tk_version(void);
+/* 1 when a CUDA device of compute capability 10.x is usable */
+int tk_device_ok(void);
+
+int tk_context_create(int device, tk_context** out);
+int tk_context_destroy(tk_context* ctx);
+/* Run on an external CUDA stream (cudaStream_t); NULL = the context's own stream */
+int tk_context_set_stream(tk_context* ctx, void* cuda_stream);
+/* Install (or clear, with NULL) the cross-rank reduction hook */
+int tk_context_set_comm(tk_context* ctx, const tk_comm* comm);
+int tk_context_synchronize(tk_context* ctx);
+
+/* Alg. 3. y: dtype TK_F32/TK_F64, dims[order], device pointer if y_on_device else host
+ * (copied in on the context stream). ranks[order], oversample >= 0, seed = SeedSpec{root, stream}. */
+int tk_rand_tucker_2i(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y,
+                      int y_on_device, const int64_t* ranks, int64_t oversample, uint64_t seed_root,
+                      uint64_t seed_stream, const tk_tucker_opts* opts, tk_tucker_out* out,
+                      tk_tucker_stats* stats);
+
+/* Alg. 2 */
+int tk_rand_tucker(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y, int y_on_device,
+                   const int64_t* ranks, int64_t oversample, uint64_t seed_root, uint64_t seed_stream,
+                   tk_tucker_out* out, tk_tucker_stats* stats);
+
+/* Kernel-level entry points, device pointers, dtype of t/m/out = dtype. */
+/* ttm: out = T x_mode M  (M: mrows x dims[mode], column-major) */
+int tk_ttm(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* t, int64_t mrows,
+           const void* m, int64_t mode, void* out);
+/* ttm_all(t, ms, skip, transpose=1): ms[n] is dims[n] x cols[n] double, applied transposed */
+int tk_ttm_all(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* t, const double** ms,
+               const int64_t* cols, int64_t skip, void* out);
+/* unfold_times: z (dims[mode] x bcols double) = unfold(t, mode) * b (b: W x bcols double) */
+int tk_unfold_times(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* t, int64_t mode,
+                    const double* b, int64_t bcols, double* z);
+/* orthonormal_basis + fix_column_signs: q (rows x cols capacity, double) and the rank */
+int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* q, int64_t* rank,
+                         double* rdiag);
+/* gaussian_matrix(rows, cols, SeedSpec{root, stream}) into a device double buffer */
+int tk_gaussian_matrix(tk_context* ctx, int64_t rows, int64_t cols, uint64_t seed_root, uint64_t seed_stream,
+                       double* out);
+uint64_t tk_seed_derived(uint64_t seed_root, uint64_t seed_stream, uint64_t tag);
+
+/* FFCP on a Tucker model (host pointers, fp64). factors[n] is rows[n] x core_shape[n].
+ * out_factors[n]: rows[n] x rank; fit_trace: capacity max_iters. */
+int tk_ffcp(tk_context* ctx, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
+            const int64_t* rows, int64_t rank, int constraint, double sparsity_c, int max_iters, double fit_tol,
+            uint64_t seed_root, uint64_t seed_stream, double** out_factors, double* fit_trace, int* iterations);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TENKIT_B200_H */

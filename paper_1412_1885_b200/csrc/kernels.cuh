@@ -1,0 +1,70 @@
+// kernels.cuh — launch interfaces of the sm_100a kernels (implemented in ttm.cu, qr.cu,
+// gen.cu). All launches are asynchronous on the given stream; layouts are column-major
+// (mode 0 fastest) like the reference DenseTensor (tensor.hpp:31).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace tkb {
+
+// Dtype tags of the C-ABI (include/tenkit_b200.h)
+enum Dtype : int { kF32 = 0, kF64 = 1 };
+
+// TTM column counts supported by the contraction kernels; a factor with `cols`
+// columns is packed with stride pack_stride(cols) (zero padded).
+constexpr int kMaxRank = 64;
+inline int pack_stride(int cols) { return (cols + 3) / 4 * 4; }
+
+// One mode-m tensor-times-matrix on the (P, K, Q) slab view of a column-major tensor
+// (P = prod of modes before m, K = I_m, Q = prod after; tensor.hpp:103-116):
+//   out[p, r, q] = sum_k in[p, k, q] * U[k, r],  r < cols
+// `up` is U packed k-major with stride pack_stride(cols) (pack_factor below), so a
+// contiguous row range of U is a contiguous sub-array (used for slab-partitioned Y).
+// Counts the launches it makes into *launches when non-null.
+// `work` (work_elems elements, may be null) enables split-K when the row tiles alone
+// cannot fill the GPU; partials are summed in fixed split order.
+template <typename T>
+void launch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t Q, int cols,
+                cudaStream_t s, int* launches = nullptr, T* work = nullptr, int64_t work_elems = 0);
+
+// Pack a column-major double factor (rows x cols, leading dim ld) into T k-major
+// [rows][pack_stride(cols)] with zero padding.
+template <typename T>
+void launch_pack_factor(const double* u, int64_t ld, int64_t rows, int cols, T* up, cudaStream_t s);
+
+// Z = unfold(X, n) * Omega without materialising the unfolding (tensor.hpp:195-209).
+// X is the (B, I, A) view of the projected tensor, Omega is given transposed
+// (omega_t[c * rn + j] = Omega(c, j), c = b + a * B). Z is I x rn column-major double.
+template <typename T>
+void launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const double* omega_t, int rn, double* z,
+                   int64_t ldz, cudaStream_t s);
+
+// Omega packed for the TTM kernels (T, k-major, stride pack_stride(cols)):
+// out[c * stride + j] = normal_at(key, j * rows + c) for j < cols, 0 for the padding.
+template <typename T>
+void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaStream_t s);
+
+// Counter-RNG fills (random.hpp:85-100): out[i + j*rows] = normal_at(key, j*rows + i).
+void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s);
+// Omega transposed: out[c * cols + j] = normal_at(key, j * rows + c)
+void launch_gaussian_transposed(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s);
+
+template <typename S, typename D>
+void launch_cast(const S* in, D* out, int64_t n, cudaStream_t s);
+
+// Column-pivoted Householder QR + rank cut + explicit Q + sign fix of Z (rows x ncols,
+// column-major, ld = rows), the device restatement of orthonormal_basis
+// (range_finder.hpp:18-29) + fix_column_signs (tucker.hpp:39-45). Writes U (rows x ucap,
+// ld = rows; columns >= rank zeroed), the packed T copy (pack_factor layout for `rank`
+// columns, if up != nullptr), rank to *rank_dev and |R_kk| diagnostics to diag (ncols).
+// Runs as one thread-block cluster holding Z in distributed shared memory.
+void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up,
+                              int up_dtype, int* rank_dev, double* diag, cudaStream_t s);
+// Largest Z (rows) the cluster QR can hold for `ncols` columns.
+int64_t qr_max_rows(int ncols);
+
+}  // namespace tkb

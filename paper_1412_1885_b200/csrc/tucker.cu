@@ -1,0 +1,643 @@
+// tucker.cu — host driver of the randomized Tucker decompositions on one B200 (and one
+// rank of a slab-partitioned multi-GPU run) + the C-ABI (include/tenkit_b200.h).
+//
+// rand_tucker_2i (reference tucker.hpp:136-169, paper Alg. 3) per (pass, n):
+//   X_n = Y x_{p != n} U_p^T   first stage streams Y once (ttm.cu), later stages are small
+//   Z_n = unfold(X_n, n) * Omega_n          (Omega regenerated from the seed, never stored)
+//   U_n = orthonormal_basis(Z_n), sign-fixed (qr.cu, one cluster)
+// core = X_{N-1} x_{N-1} U_{N-1}^T (the reference's extra pass at tucker.hpp:166 computes
+// the same tensor with the same operation order; opts.explicit_core_pass restores it).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/tenkit_b200.h"
+#include "kernels.cuh"
+
+using namespace tkb;
+
+struct tk_context {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    bool has_comm = false;
+    tk_comm comm{};
+    std::map<std::string, std::pair<void*, size_t>> bufs;
+    int* rank_host = nullptr;  // pinned
+
+    void* buf(const std::string& name, size_t bytes) {
+        auto& e = bufs[name];
+        if (e.second < bytes) {
+            if (e.first) TK_CUDA(cudaFree(e.first));
+            e.first = nullptr;
+            TK_CUDA(cudaMalloc(&e.first, std::max<size_t>(bytes, 256)));
+            e.second = std::max<size_t>(bytes, 256);
+        }
+        return e.first;
+    }
+    ~tk_context() {
+        for (auto& kv : bufs)
+            if (kv.second.first) cudaFree(kv.second.first);
+        if (rank_host) cudaFreeHost(rank_host);
+        if (own) cudaStreamDestroy(own);
+    }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return TK_OK;
+    } catch (const InvalidArgument& e) {
+        return fail(TK_ERR_INVALID, e.what());
+    } catch (const CudaError& e) {
+        return fail(TK_ERR_CUDA, e.what());
+    } catch (const std::exception& e) {
+        return fail(TK_ERR_INTERNAL, std::string("tenkit: ") + e.what());
+    }
+}
+
+int64_t prod(const std::vector<int64_t>& v, int64_t skip = -1) {
+    int64_t p = 1;
+    for (size_t i = 0; i < v.size(); ++i)
+        if (static_cast<int64_t>(i) != skip) p *= v[i];
+    return p;
+}
+
+size_t dsize(int dtype) { return dtype == TK_F32 ? 4 : 8; }
+
+void check_ctx(tk_context* ctx) {
+    require(ctx != nullptr, "null context");
+    TK_CUDA(cudaSetDevice(ctx->device));
+}
+
+// ---------------------------------------------------------------------------
+// One decomposition run for value type T.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct TuckerRun {
+    tk_context* ctx;
+    cudaStream_t s;
+    int64_t order;
+    std::vector<int64_t> ldims;  // local dims of Y on this rank
+    std::vector<int64_t> gdims;  // global dims
+    int64_t offset = 0;          // slab offset along the last mode
+    const T* y;
+    std::vector<int> rt, cols;
+    std::vector<double*> U;  // global factors, gdims[n] x rt[n] (ld gdims[n])
+    std::vector<T*> Up;      // packed k-major copies
+    int launches = 0;
+    int passes = 0;
+    int* rank_dev = nullptr;
+    bool time_kernels = false;
+    std::vector<cudaEvent_t> ev;  // (start, stop) pairs around Y-streaming launches
+
+    ~TuckerRun() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    void mark() {
+        cudaEvent_t e;
+        TK_CUDA(cudaEventCreate(&e));
+        TK_CUDA(cudaEventRecord(e, s));
+        ev.push_back(e);
+    }
+    double streamed_ms() {
+        double ms = 0.0;
+        for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+            TK_CUDA(cudaEventSynchronize(ev[i + 1]));
+            float t = 0.f;
+            TK_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+            ms += t;
+        }
+        return ms;
+    }
+
+    const T* factor_rows(int m) const {  // rows of U_m matching this rank's block
+        const T* p = Up[m];
+        if (m == order - 1) p += offset * pack_stride(cols[m]);
+        return p;
+    }
+
+    // Y x_{p != skip} U_p^T (skip = -1: all modes). Returns the result buffer and its dims.
+    const T* project(int skip, std::vector<int64_t>& xd) {
+        xd = ldims;
+        if (order == 1 && skip == 0) return y;
+        std::vector<int> modes;
+        const int first = (skip != order - 1) ? static_cast<int>(order - 1) : static_cast<int>(order - 2);
+        if (first >= 0 && first != skip) modes.push_back(first);
+        for (int m = static_cast<int>(order) - 1; m >= 0; --m)
+            if (m != skip && m != first) modes.push_back(m);
+        const T* cur = y;
+        int which = 0;
+        for (size_t t = 0; t < modes.size(); ++t) {
+            const int m = modes[t];
+            const int64_t P = prod(std::vector<int64_t>(xd.begin(), xd.begin() + m));
+            const int64_t K = xd[m];
+            const int64_t Q = prod(std::vector<int64_t>(xd.begin() + m + 1, xd.end()));
+            T* out = static_cast<T*>(ctx->buf(which ? "projB" : "projA", sizeof(T) * P * cols[m] * Q));
+            const bool streams_y = (t == 0 && cur == y);
+            if (streams_y && time_kernels) mark();
+            ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
+            if (streams_y && time_kernels) mark();
+            if (streams_y) ++passes;
+            xd[m] = cols[m];
+            cur = out;
+            which ^= 1;
+        }
+        return cur;
+    }
+
+    void ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t Q, int c) {
+        const int64_t welems = std::min<int64_t>(P * c * Q * 2 * 148, int64_t(32) << 20);
+        T* work = static_cast<T*>(ctx->buf("splitk", sizeof(T) * welems));
+        launch_ttm<T>(in, up, out, P, K, Q, c, s, &launches, work, welems);
+    }
+
+    void allreduce(double* buf, int64_t count) {
+        if (!ctx->has_comm || ctx->comm.world <= 1) return;
+        const tk_comm& c = ctx->comm;
+        require(count <= c.xbuf_capacity, "comm: exchange buffer too small");
+        if (buf != c.xbuf) TK_CUDA(cudaMemcpyAsync(c.xbuf, buf, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        require(c.allreduce_sum(c.user, count, s) == 0, "comm: allreduce failed");
+        if (buf != c.xbuf) TK_CUDA(cudaMemcpyAsync(buf, c.xbuf, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+
+    // One range-finding step for mode n: Z = unfold(X, n) Omega, U_n = basis(Z)
+    void range_step(const T* x, const std::vector<int64_t>& xd, int n, const Seed& omega_seed, int step, bool sync) {
+        const int64_t W = prod(std::vector<int64_t>(cols.begin(), cols.end()), n);
+        const int rn = rt[n];
+        double* om = static_cast<double*>(ctx->buf("omega", sizeof(double) * W * rn));
+        launch_gaussian_transposed(om, W, rn, omega_seed.key(), s);
+        ++launches;
+        const int64_t In = gdims[n];
+        double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * In * rn));
+        const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + n));
+        const int64_t A = prod(std::vector<int64_t>(xd.begin() + n + 1, xd.end()));
+        const bool local_rows = ctx->has_comm && ctx->comm.world > 1 && n == order - 1;
+        if (local_rows) {
+            TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * In * rn, s));
+            launch_sketch<T>(x, B, xd[n], A, om, rn, z + offset, In, s);
+        } else {
+            launch_sketch<T>(x, B, xd[n], A, om, rn, z, In, s);
+        }
+        ++launches;
+        allreduce(z, In * rn);
+        launch_orthonormal_basis(z, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64, rank_dev + step,
+                                 nullptr, s);
+        ++launches;
+        if (sync) {
+            TK_CUDA(cudaMemcpyAsync(ctx->rank_host, rank_dev + step, sizeof(int), cudaMemcpyDeviceToHost, s));
+            TK_CUDA(cudaStreamSynchronize(s));
+            const int r = *ctx->rank_host;
+            require(r >= 1, "tensor dimensions must be positive");  // a rank-0 factor (zero data)
+            cols[n] = r;
+        }
+    }
+
+    void run(const std::vector<int64_t>& ranks, int64_t p, const Seed& seed, const tk_tucker_opts& opt,
+             tk_tucker_out* out, tk_tucker_stats* stats) {
+        rt.resize(order);
+        cols.resize(order);
+        U.resize(order);
+        Up.resize(order);
+        for (int n = 0; n < order; ++n) {
+            rt[n] = static_cast<int>(std::min<int64_t>(ranks[n] + p, gdims[n]));
+            require(rt[n] >= 1, "gaussian_matrix: dimensions must be positive");
+            require(rt[n] <= kMaxRank, "rank + oversample must be <= 64 on this device path");
+            cols[n] = rt[n];
+            U[n] = static_cast<double*>(ctx->buf("U" + std::to_string(n), sizeof(double) * gdims[n] * rt[n]));
+            Up[n] = static_cast<T*>(ctx->buf("Up" + std::to_string(n), sizeof(T) * gdims[n] * pack_stride(rt[n])));
+            launch_gaussian_colmajor(U[n], gdims[n], rt[n], alg3_init_seed(seed, n).key(), s);
+            launch_pack_factor<T>(U[n], gdims[n], gdims[n], rt[n], Up[n], s);
+            launches += 2;
+        }
+        rank_dev = static_cast<int*>(ctx->buf("ranks", sizeof(int) * 2 * TK_MAX_ORDER));
+        const bool sync = opt.sync_ranks != 0;
+        const T* xlast = nullptr;
+        std::vector<int64_t> xd;
+        int step = 0;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int n = 0; n < order; ++n, ++step) {
+                const T* x = project(n, xd);
+                range_step(x, xd, n, alg3_omega_seed(seed, pass, n), step, sync);
+                xlast = x;
+            }
+        if (!sync) {  // verify the full-rank speculation
+            int hr[2 * TK_MAX_ORDER];
+            TK_CUDA(cudaMemcpyAsync(hr, rank_dev, sizeof(int) * 2 * order, cudaMemcpyDeviceToHost, s));
+            TK_CUDA(cudaStreamSynchronize(s));
+            for (int i = 0; i < 2 * order; ++i)
+                if (hr[i] != rt[i % order]) throw std::runtime_error("rank-drop");  // caller reruns synchronously
+        }
+        // core
+        std::vector<int64_t> gd;
+        const T* g;
+        if (opt.explicit_core_pass || order == 1) {
+            g = project(-1, gd);
+        } else {
+            gd = xd;  // X_{N-1}: cols everywhere except mode N-1 (local extent)
+            const int m = static_cast<int>(order - 1);
+            const int64_t P = prod(std::vector<int64_t>(gd.begin(), gd.begin() + m));
+            T* o = static_cast<T*>(ctx->buf("core", sizeof(T) * P * cols[m]));
+            ttm(xlast, factor_rows(m), o, P, gd[m], 1, cols[m]);
+            gd[m] = cols[m];
+            g = o;
+        }
+        const int64_t gsize = prod(gd);
+        double* gdv = static_cast<double*>(ctx->buf("core64", sizeof(double) * gsize));
+        if constexpr (sizeof(T) == 4) launch_cast<float, double>(reinterpret_cast<const float*>(g), gdv, gsize, s);
+        else launch_cast<double, double>(reinterpret_cast<const double*>(g), gdv, gsize, s);
+        ++launches;
+        allreduce(gdv, gsize);
+        // outputs
+        const cudaMemcpyKind kind = out->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        TK_CUDA(cudaMemcpyAsync(out->core, gdv, sizeof(double) * gsize, kind, s));
+        for (int n = 0; n < order; ++n) {
+            out->core_shape[n] = gd[n];
+            out->factor_cols[n] = cols[n];
+            TK_CUDA(cudaMemcpyAsync(out->factors[n], U[n], sizeof(double) * gdims[n] * cols[n], kind, s));
+        }
+        if (stats) {
+            stats->passes = passes;
+            stats->kernel_launches = launches;
+            stats->stream_launches = passes;
+            stats->stream_ms = time_kernels ? streamed_ms() : 0.0;
+            stats->y_bytes = static_cast<double>(prod(ldims)) * sizeof(T);
+            int hr[2 * TK_MAX_ORDER] = {0};
+            TK_CUDA(cudaMemcpyAsync(hr, rank_dev, sizeof(int) * 2 * order, cudaMemcpyDeviceToHost, s));
+            TK_CUDA(cudaStreamSynchronize(s));
+            for (int i = 0; i < 2 * order; ++i) stats->ranks[i] = hr[i];
+        }
+        if (!out->on_device) TK_CUDA(cudaStreamSynchronize(s));
+    }
+};
+
+// rand_tucker (Alg. 2, tucker.hpp:108-130): Z = unfold(cur, n) * Omega (dense Omega of
+// width prod_{k != n} cur.dim(k), regenerated from the seed), U_n = basis(Z),
+// cur <- cur x_n U_n^T; the core is the final cur. Single device.
+template <typename T>
+void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const void* y, int y_on_device,
+                      const int64_t* ranks, int64_t p, Seed seed, tk_tucker_out* out, tk_tucker_stats* stats) {
+    require(!(ctx->has_comm && ctx->comm.world > 1), "rand_tucker: multi-rank runs use rand_tucker_2i");
+    cudaStream_t s = ctx->stream;
+    std::vector<int64_t> cd(dims, dims + order);
+    const T* cur = static_cast<const T*>(y);
+    if (!y_on_device) {
+        T* buf = static_cast<T*>(ctx->buf("y_in", sizeof(T) * prod(cd)));
+        TK_CUDA(cudaMemcpyAsync(buf, y, sizeof(T) * prod(cd), cudaMemcpyHostToDevice, s));
+        cur = buf;
+    }
+    TuckerRun<T> r{ctx, s, order, cd, cd, 0, cur};
+    r.rank_dev = static_cast<int*>(ctx->buf("ranks", sizeof(int) * 2 * TK_MAX_ORDER));
+    std::vector<double*> U(order);
+    std::vector<int64_t> fcols(order);
+    int which = 0;
+    for (int n = 0; n < order; ++n) {
+        const int rt = static_cast<int>(std::min<int64_t>(ranks[n] + p, cd[n]));
+        require(rt >= 1, "gaussian_matrix: dimensions must be positive");
+        require(rt <= kMaxRank, "rank + oversample must be <= 64 on this device path");
+        const int64_t width = prod(cd) / cd[n];
+        const Seed os = alg2_omega_seed(seed, n);
+        double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * cd[n] * rt));
+        if (n == 0) {  // contiguous unfolding: Z = Y_(0) * Omega as a split-K TTM over the flattened modes
+            T* op = static_cast<T*>(ctx->buf("omega_packed", sizeof(T) * width * pack_stride(rt)));
+            launch_gaussian_packed<T>(op, width, rt, os.key(), s);
+            T* zt = static_cast<T*>(ctx->buf("zt", sizeof(T) * cd[0] * rt));
+            r.ttm(cur, op, zt, cd[0], width, 1, rt);
+            if constexpr (sizeof(T) == 4) launch_cast<float, double>(reinterpret_cast<const float*>(zt), z, cd[0] * rt, s);
+            else launch_cast<double, double>(reinterpret_cast<const double*>(zt), z, cd[0] * rt, s);
+            r.launches += 2;
+        } else {
+            double* om = static_cast<double*>(ctx->buf("omega", sizeof(double) * width * rt));
+            launch_gaussian_transposed(om, width, rt, os.key(), s);
+            const int64_t B = prod(std::vector<int64_t>(cd.begin(), cd.begin() + n));
+            const int64_t A = prod(std::vector<int64_t>(cd.begin() + n + 1, cd.end()));
+            launch_sketch<T>(cur, B, cd[n], A, om, rt, z, cd[n], s);
+            r.launches += 2;
+        }
+        U[n] = static_cast<double*>(ctx->buf("U" + std::to_string(n), sizeof(double) * cd[n] * rt));
+        T* up = static_cast<T*>(ctx->buf("Up" + std::to_string(n), sizeof(T) * cd[n] * pack_stride(rt)));
+        launch_orthonormal_basis(z, cd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64, r.rank_dev + n, nullptr, s);
+        ++r.launches;
+        TK_CUDA(cudaMemcpyAsync(ctx->rank_host, r.rank_dev + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+        TK_CUDA(cudaStreamSynchronize(s));
+        const int rank = *ctx->rank_host;
+        require(rank >= 1, "tensor dimensions must be positive");
+        fcols[n] = rank;
+        const int64_t P = prod(std::vector<int64_t>(cd.begin(), cd.begin() + n));
+        const int64_t Q = prod(std::vector<int64_t>(cd.begin() + n + 1, cd.end()));
+        T* nxt = static_cast<T*>(ctx->buf(which ? "a2B" : "a2A", sizeof(T) * P * rank * Q));
+        r.ttm(cur, up, nxt, P, cd[n], Q, rank);
+        if (n == 0) ++r.passes;
+        cd[n] = rank;
+        cur = nxt;
+        which ^= 1;
+    }
+    const int64_t gsize = prod(cd);
+    double* gdv = static_cast<double*>(ctx->buf("core64", sizeof(double) * gsize));
+    if constexpr (sizeof(T) == 4) launch_cast<float, double>(reinterpret_cast<const float*>(cur), gdv, gsize, s);
+    else launch_cast<double, double>(reinterpret_cast<const double*>(cur), gdv, gsize, s);
+    const cudaMemcpyKind kind = out->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    TK_CUDA(cudaMemcpyAsync(out->core, gdv, sizeof(double) * gsize, kind, s));
+    for (int n = 0; n < order; ++n) {
+        out->core_shape[n] = cd[n];
+        out->factor_cols[n] = fcols[n];
+        TK_CUDA(cudaMemcpyAsync(out->factors[n], U[n], sizeof(double) * dims[n] * fcols[n], kind, s));
+    }
+    if (stats) {
+        stats->passes = r.passes + 1;  // the Z sketch of mode 0 streams Y as well
+        stats->kernel_launches = r.launches + 1;
+        stats->y_bytes = static_cast<double>(prod(std::vector<int64_t>(dims, dims + order))) * sizeof(T);
+        for (int n = 0; n < order; ++n) stats->ranks[n] = static_cast<int>(fcols[n]);
+    }
+    TK_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+void rand_tucker_2i_impl(tk_context* ctx, int64_t order, const int64_t* dims, const void* y, int y_on_device,
+                         const int64_t* ranks, int64_t p, Seed seed, const tk_tucker_opts& opt, tk_tucker_out* out,
+                         tk_tucker_stats* stats) {
+    std::vector<int64_t> ld(dims, dims + order), rk(ranks, ranks + order);
+    std::vector<int64_t> gd = ld;
+    int64_t offset = 0;
+    if (ctx->has_comm && ctx->comm.world > 1) {
+        gd[order - 1] = ctx->comm.global_last_dim;
+        offset = ctx->comm.slab_offset;
+        require(offset >= 0 && offset + ld[order - 1] <= gd[order - 1], "comm: slab outside the global tensor");
+    }
+    const T* ydev = static_cast<const T*>(y);
+    if (!y_on_device) {
+        T* buf = static_cast<T*>(ctx->buf("y_in", sizeof(T) * prod(ld)));
+        TK_CUDA(cudaMemcpyAsync(buf, y, sizeof(T) * prod(ld), cudaMemcpyHostToDevice, ctx->stream));
+        ydev = buf;
+    }
+    auto attempt = [&](const tk_tucker_opts& o) {
+        TuckerRun<T> r{ctx, ctx->stream, order, ld, gd, offset, ydev};
+        r.time_kernels = o.time_kernels != 0;
+        r.run(rk, p, seed, o, out, stats);
+    };
+    if (opt.sync_ranks) {
+        attempt(opt);
+    } else {
+        try {
+            attempt(opt);
+        } catch (const std::runtime_error& e) {
+            if (std::string(e.what()) != "rank-drop") throw;
+            tk_tucker_opts o2 = opt;
+            o2.sync_ranks = 1;
+            attempt(o2);
+        }
+    }
+}
+
+void validate_common(int dtype, int64_t order, const int64_t* dims, const int64_t* ranks, int64_t p,
+                     const char* who) {
+    require(dtype == TK_F32 || dtype == TK_F64, "unsupported dtype");
+    require(order >= 1 && order <= TK_MAX_ORDER, "tensor order must be in [1, 8]");
+    for (int64_t n = 0; n < order; ++n) require(dims[n] >= 1, "tensor dimensions must be positive");
+    require(ranks != nullptr, std::string(who) + ": one rank per mode required");
+    require(p >= 0, std::string(who) + ": oversampling must be nonnegative");
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int tk_ffcp_fail(int code, const char* msg) { return fail(code, msg); }
+const char* tk_last_error(void) { return g_err.c_str(); }
+int tk_version(void) { return 1; }
+
+int tk_device_ok(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaDeviceProp pr{};
+    if (cudaGetDeviceProperties(&pr, 0) != cudaSuccess) return 0;
+    return pr.major == 10 ? 1 : 0;
+}
+
+int tk_context_create(int device, tk_context** out) {
+    if (!tk_device_ok()) return fail(TK_ERR_NO_DEVICE, "tenkit: no sm_100 CUDA device available (no CPU fallback)");
+    return guarded([&] {
+        require(out != nullptr, "null output");
+        auto ctx = std::make_unique<tk_context>();
+        ctx->device = device;
+        TK_CUDA(cudaSetDevice(device));
+        TK_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+        ctx->stream = ctx->own;
+        TK_CUDA(cudaMallocHost(&ctx->rank_host, sizeof(int) * 4));
+        *out = ctx.release();
+    });
+}
+
+int tk_context_destroy(tk_context* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        delete ctx;
+    });
+}
+
+int tk_context_set_stream(tk_context* ctx, void* st) {
+    return guarded([&] {
+        check_ctx(ctx);
+        ctx->stream = st ? static_cast<cudaStream_t>(st) : ctx->own;
+    });
+}
+
+int tk_context_set_comm(tk_context* ctx, const tk_comm* comm) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (!comm) {
+            ctx->has_comm = false;
+            return;
+        }
+        require(comm->world >= 1 && comm->rank >= 0 && comm->rank < comm->world, "comm: bad rank/world");
+        require(comm->world == 1 || (comm->allreduce_sum && comm->xbuf), "comm: missing reduction hook");
+        ctx->comm = *comm;
+        ctx->has_comm = true;
+    });
+}
+
+int tk_context_synchronize(tk_context* ctx) {
+    return guarded([&] {
+        check_ctx(ctx);
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tk_rand_tucker_2i(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y, int y_on_device,
+                      const int64_t* ranks, int64_t oversample, uint64_t seed_root, uint64_t seed_stream,
+                      const tk_tucker_opts* opts, tk_tucker_out* out, tk_tucker_stats* stats) {
+    return guarded([&] {
+        check_ctx(ctx);
+        validate_common(dtype, order, dims, ranks, oversample, "rand_tucker_2i");
+        require(out != nullptr && y != nullptr, "rand_tucker_2i: null argument");
+        tk_tucker_opts o{0, 1, 0};
+        if (opts) o = *opts;
+        const Seed seed{seed_root, seed_stream};
+        if (dtype == TK_F32) rand_tucker_2i_impl<float>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, o, out, stats);
+        else rand_tucker_2i_impl<double>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, o, out, stats);
+    });
+}
+
+int tk_rand_tucker(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y, int y_on_device,
+                   const int64_t* ranks, int64_t oversample, uint64_t seed_root, uint64_t seed_stream,
+                   tk_tucker_out* out, tk_tucker_stats* stats) {
+    return guarded([&] {
+        check_ctx(ctx);
+        validate_common(dtype, order, dims, ranks, oversample, "rand_tucker");
+        require(out != nullptr && y != nullptr, "rand_tucker: null argument");
+        const Seed seed{seed_root, seed_stream};
+        if (dtype == TK_F32) rand_tucker_impl<float>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, out, stats);
+        else rand_tucker_impl<double>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, out, stats);
+    });
+}
+
+uint64_t tk_seed_derived(uint64_t root, uint64_t stream, uint64_t tag) { return Seed{root, stream}.derived(tag).stream; }
+
+int tk_gaussian_matrix(tk_context* ctx, int64_t rows, int64_t cols, uint64_t root, uint64_t stream, double* out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(rows >= 1 && cols >= 1, "gaussian_matrix: dimensions must be positive");
+        launch_gaussian_colmajor(out, rows, cols, Seed{root, stream}.key(), ctx->stream);
+    });
+}
+
+int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* q, int64_t* rank,
+                         double* rdiag) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(rows >= 1, "orthonormal_basis: empty input");
+        if (cols == 0) {
+            *rank = 0;
+            return;
+        }
+        require(cols <= rows, "orthonormal_basis: wide inputs are not supported on the device path");
+        int* rd = static_cast<int*>(ctx->buf("qr_rank", sizeof(int)));
+        launch_orthonormal_basis(z, rows, static_cast<int>(cols), q, static_cast<int>(cols), nullptr, kF64, rd, rdiag,
+                                 ctx->stream);
+        TK_CUDA(cudaMemcpyAsync(ctx->rank_host, rd, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+        *rank = *ctx->rank_host;
+    });
+}
+
+int tk_ttm(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* t, int64_t mrows,
+           const void* m, int64_t mode, void* out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(order >= 1 && order <= TK_MAX_ORDER, "tensor order must be in [1, 8]");
+        require(mode >= 0 && mode < order, "mode index out of range");
+        require(mrows >= 1 && mrows <= kMaxRank, "ttm: matrix rows must be in [1, 64] on the device path");
+        std::vector<int64_t> d(dims, dims + order);
+        const int64_t P = prod(std::vector<int64_t>(d.begin(), d.begin() + mode));
+        const int64_t Q = prod(std::vector<int64_t>(d.begin() + mode + 1, d.end()));
+        // m is mrows x I_mode column-major (dtype); pack M^T k-major
+        const int stride = pack_stride(static_cast<int>(mrows));
+        double* md = static_cast<double*>(ctx->buf("ttm_m64", sizeof(double) * mrows * d[mode]));
+        // M^T (I_mode x mrows, ld I_mode) as double
+        std::vector<double> host(mrows * d[mode]);
+        const size_t es = dsize(dtype);
+        std::vector<unsigned char> raw(es * mrows * d[mode]);
+        TK_CUDA(cudaMemcpyAsync(raw.data(), m, raw.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int64_t k = 0; k < d[mode]; ++k)
+            for (int64_t r = 0; r < mrows; ++r) {
+                const int64_t src = r + k * mrows;
+                host[k + r * d[mode]] = dtype == TK_F32 ? reinterpret_cast<float*>(raw.data())[src]
+                                                        : reinterpret_cast<double*>(raw.data())[src];
+            }
+        TK_CUDA(cudaMemcpyAsync(md, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, ctx->stream));
+        if (dtype == TK_F32) {
+            float* up = static_cast<float*>(ctx->buf("ttm_up", sizeof(float) * d[mode] * stride));
+            launch_pack_factor<float>(md, d[mode], d[mode], static_cast<int>(mrows), up, ctx->stream);
+            launch_ttm<float>(static_cast<const float*>(t), up, static_cast<float*>(out), P, d[mode], Q,
+                              static_cast<int>(mrows), ctx->stream);
+        } else {
+            double* up = static_cast<double*>(ctx->buf("ttm_up", sizeof(double) * d[mode] * stride));
+            launch_pack_factor<double>(md, d[mode], d[mode], static_cast<int>(mrows), up, ctx->stream);
+            launch_ttm<double>(static_cast<const double*>(t), up, static_cast<double*>(out), P, d[mode], Q,
+                               static_cast<int>(mrows), ctx->stream);
+        }
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tk_ttm_all(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* t, const double** ms,
+               const int64_t* cols, int64_t skip, void* out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(order >= 1 && order <= TK_MAX_ORDER, "tensor order must be in [1, 8]");
+        std::vector<int64_t> d(dims, dims + order);
+        auto body = [&](auto tag) {
+            using T = decltype(tag);
+            TuckerRun<T> r{ctx, ctx->stream, order, d, d, 0, static_cast<const T*>(t)};
+            r.cols.resize(order);
+            r.Up.resize(order);
+            for (int n = 0; n < order; ++n) {
+                r.cols[n] = static_cast<int>(cols[n]);
+                if (n == skip) continue;
+                require(cols[n] >= 1 && cols[n] <= kMaxRank, "ttm_all: factor columns must be in [1, 64]");
+                r.Up[n] = static_cast<T*>(ctx->buf("tall_up" + std::to_string(n), sizeof(T) * d[n] * pack_stride(r.cols[n])));
+                launch_pack_factor<T>(ms[n], d[n], d[n], r.cols[n], r.Up[n], ctx->stream);
+            }
+            std::vector<int64_t> xd;
+            const T* x = r.project(static_cast<int>(skip), xd);
+            TK_CUDA(cudaMemcpyAsync(out, x, sizeof(T) * prod(xd), cudaMemcpyDeviceToDevice, ctx->stream));
+        };
+        if (dtype == TK_F32) body(float{});
+        else body(double{});
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tk_unfold_times(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* t, int64_t mode,
+                    const double* b, int64_t bcols, double* z) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(mode >= 0 && mode < order, "mode index out of range");
+        std::vector<int64_t> d(dims, dims + order);
+        const int64_t B = prod(std::vector<int64_t>(d.begin(), d.begin() + mode));
+        const int64_t A = prod(std::vector<int64_t>(d.begin() + mode + 1, d.end()));
+        const int64_t W = B * A;
+        // b is W x bcols column-major; the sketch kernel reads it transposed
+        double* bt = static_cast<double*>(ctx->buf("ut_bt", sizeof(double) * W * bcols));
+        std::vector<double> hb(W * bcols), ht(W * bcols);
+        TK_CUDA(cudaMemcpyAsync(hb.data(), b, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int64_t c = 0; c < W; ++c)
+            for (int64_t j = 0; j < bcols; ++j) ht[c * bcols + j] = hb[c + j * W];
+        TK_CUDA(cudaMemcpyAsync(bt, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice, ctx->stream));
+        if (dtype == TK_F32)
+            launch_sketch<float>(static_cast<const float*>(t), B, d[mode], A, bt, static_cast<int>(bcols), z, d[mode],
+                                 ctx->stream);
+        else
+            launch_sketch<double>(static_cast<const double*>(t), B, d[mode], A, bt, static_cast<int>(bcols), z, d[mode],
+                                  ctx->stream);
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+"""Seeded synthetic workloads of the reference benchmark (bench.hpp:46-112, 410-437) built on
+the device: Tucker (Gaussian core + Gaussian factors) or CP (Gaussian / U(0,1) factors)
+ground truth, plus realised-SNR Gaussian or |Gaussian| noise. Every random entry is the
+reference's counter RNG at the reference's index (random.hpp:85-138), so the tensors are
+the ones the reference's generators produce (up to fp64 rounding of the contractions).
+
+The U(0,1) factors (configs 1, 4) and |N| noise (config 4) are the BASELINE configs'
+additions, defined by mirroring bench.hpp:63-71: entry (i, j) of factor n is
+uniform_at(gen_factor_seed(seed, n), j*I_n + i); noise is |gaussian_tensor(...)|.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .tenkit import Context, SeedSpec, _dptr, _lib
+
+_GOLD = 0x9E3779B97F4A7C15
+
+
+def _np_mix64(x):
+    with np.errstate(over="ignore"):
+        x = np.asarray(x, dtype=np.uint64) + np.uint64(_GOLD)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def uniform_matrix(rows: int, cols: int, seed: SeedSpec) -> np.ndarray:
+    """uniform_at(seed, j*rows + i) in (0, 1] (random.hpp:48-56, 74-76), column-major."""
+    idx = np.arange(rows * cols, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        bits = _np_mix64(np.uint64(seed.key()) + idx * np.uint64(_GOLD))
+    v = ((bits >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0**-53
+    return v.reshape((rows, cols), order="F")
+
+
+def gaussian_flat(n: int, seed: SeedSpec, context: Context | None = None):
+    """Flat fp64 CUDA tensor of gaussian_tensor / gaussian_matrix draws (random.hpp:85-138)."""
+    import torch
+    ctx = context or Context.default()
+    out = torch.empty(max(int(n), 1), dtype=torch.float64, device="cuda")
+    _lib.check(ctx.lib.tk_gaussian_matrix(ctx.handle, int(n), 1, seed.root, seed.stream, _dptr(out)))
+    return out[: int(n)]
+
+
+def gen_factor_seed(seed: SeedSpec, n: int) -> SeedSpec:  # bench.hpp:46-48
+    return seed.derived(0x9E4, n)
+
+
+def _colmajor_einsum(core, factors):
+    """Y = core x_0 A_0 ... x_{N-1} A_{N-1} as a flat column-major fp64 CUDA tensor."""
+    import torch
+    order = len(factors)
+    letters_r = "abcdefgh"[:order]
+    letters_i = "ijklmnop"[:order]
+    # row-major views with reversed mode order are the column-major layouts
+    spec = letters_r[::-1] + "," + ",".join(letters_i[n] + letters_r[n] for n in range(order)) + "->" + letters_i[::-1]
+    return torch.einsum(spec, core, *factors).contiguous().view(-1)
+
+
+def gen_tucker_device(dims, mlranks, seed: SeedSpec, context=None):
+    """gen_tucker_tensor (bench.hpp:83-95) on the device, fp64 flat column-major."""
+    import torch
+    core = gaussian_flat(int(np.prod(mlranks)), seed.derived(0xC0DE), context)
+    core_rm = core.view(*reversed([int(r) for r in mlranks]))
+    fs = []
+    for n, (i, r) in enumerate(zip(dims, mlranks)):
+        a = gaussian_flat(int(i) * int(r), gen_factor_seed(seed, n), context)
+        fs.append(a.view(int(r), int(i)).t())
+    return _colmajor_einsum(core_rm, fs)
+
+
+def gen_cp_device(dims, rank: int, seed: SeedSpec, uniform: bool = True, context=None):
+    """gen_cp_tensor (bench.hpp:56-80) with U(0,1) (or Gaussian) factors, fp64 flat column-major."""
+    import torch
+    fs = []
+    for n, i in enumerate(dims):
+        if uniform:
+            a = torch.from_numpy(uniform_matrix(int(i), rank, gen_factor_seed(seed, n))).cuda()
+        else:
+            a = gaussian_flat(int(i) * rank, gen_factor_seed(seed, n), context).view(rank, int(i)).t()
+        fs.append(a)
+    order = len(dims)
+    eye = torch.zeros([rank] * order, dtype=torch.float64, device="cuda")
+    idx = torch.arange(rank, device="cuda")
+    eye[tuple([idx] * order)] = 1.0
+    return _colmajor_einsum(eye, fs)
+
+
+def add_noise_device(y, snr_db: float, seed: SeedSpec, abs_noise: bool = False, context=None):
+    """add_noise (bench.hpp:100-112): sigma = ||Y|| / (||E|| 10^(snr/20)), Y + sigma E (in place)."""
+    import torch
+    if np.isinf(snr_db) and snr_db > 0:
+        return y
+    e = gaussian_flat(y.numel(), seed.derived(0x7015E), context)
+    if abs_noise:
+        e.abs_()
+    ny = torch.linalg.vector_norm(y).item()
+    ne = torch.linalg.vector_norm(e).item()
+    if ny <= 0 or ne <= 0:
+        raise _lib.TenkitError("tenkit: add_noise: zero tensor input")
+    sigma = ny / (ne * 10.0 ** (snr_db / 20.0))
+    y.add_(e, alpha=sigma)
+    del e
+    return y
+
+
+def bench_seeds(seed: int = 0, d: int = 0, s: int = 0, run: int = 0):
+    """run_experiment's seed derivation (bench.hpp:588,604-606): (data_seed, alg_seed)."""
+    root = SeedSpec(seed, 0)
+    return root.derived(0xDA7A, (d * 1000 + s) * 1000 + run), root.derived(0xA16D, run)
+
+
+def generate(cfg: dict, context=None):
+    """Observation Y (fp64 flat column-major CUDA tensor) of a benchmark config dict."""
+    data_seed, _ = bench_seeds(cfg.get("seed", 0))
+    if cfg["gen"] == "tucker":
+        y = gen_tucker_device(cfg["dims"], cfg["mlrank"], data_seed, context)
+    else:
+        y = gen_cp_device(cfg["dims"], cfg["cp_rank"], data_seed, uniform=cfg["gen"] == "cp_uniform", context=context)
+    return add_noise_device(y, cfg["snr"], data_seed.derived(0xAD0), abs_noise=cfg.get("abs_noise", False),
+                            context=context)

@@ -1,0 +1,224 @@
+"""Parity of the sm_100a path against the CPU oracle (oracle/), through the C-ABI.
+
+Bars (north star): subspaces ||U U^T - U' U'^T||_F, the aligned core and the fit agree
+within 1e-5 in fp64 (Y fp64) and 1e-3 in fp32 (Y fp32, oracle in fp64 on the same fp32
+values). Kernel-level results are compared at fp64 rounding level (<= 1e-12 relative) or
+fp32 accumulation level (<= 2e-5 relative)."""
+import numpy as np
+import pytest
+
+from helpers import orthonormality_defect, subspace_dist, transpositions_to_perm
+
+pytestmark = pytest.mark.gpu
+
+F64_TOL = 1e-5
+F32_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1412_1885_b200 as P
+    return P
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))
+
+
+def rt(O, shape, seed):
+    return O.gaussian_matrix(int(np.prod(shape)), 1, (seed, 0)).reshape(shape, order="F")
+
+
+def noisy_tucker(O, dims, ranks, snr_db, seed):
+    y = O.gen_tucker(dims, ranks, seed)
+    return O.add_noise(y, snr_db, O.seed_derived(*seed, 0xAD0))
+
+
+# ------------------------------------------------------------------ RNG / kernels
+def test_gaussian_matrix_matches_oracle(P, O):
+    for rows, cols, seed in [(7, 4, (5, 11)), (1000, 30, (0, 3)), (999, 3, (1, 2))]:
+        d = P.gaussian_matrix(rows, cols, seed)
+        h = O.gaussian_matrix(rows, cols, seed)
+        assert np.max(np.abs(d - h)) <= 4e-15 * max(1.0, np.max(np.abs(h)))
+
+
+@pytest.mark.parametrize("shape", [(200, 40, 30), (64, 33, 17), (3, 4, 2), (12, 10, 9, 8), (256, 300), (5, 4000)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_ttm_all_modes(P, O, shape, dtype):
+    import torch
+    t = rt(O, shape, 8)
+    tt = P.DenseTensor.from_numpy(t, np.float32 if dtype == "f32" else np.float64)
+    for n in range(len(shape)):
+        for rows in (1, 5, 15, 30, 64):
+            m = O.gaussian_matrix(rows, shape[n], (9, n + rows))
+            ref = O.ttm(tt.numpy().astype(np.float64), m, n)
+            got = P.ttm(tt, m, n)
+            assert rel(got, ref) < (1e-12 if dtype == "f64" else 2e-5 * np.sqrt(shape[n] / 100 + 1))
+
+
+@pytest.mark.parametrize("shape,skip", [((60, 50, 40), -1), ((60, 50, 40), 0), ((60, 50, 40), 1), ((60, 50, 40), 2),
+                                        ((20, 18, 16, 14), 3), ((20, 18, 16, 14), 1)])
+def test_ttm_all_projection(P, O, shape, skip):
+    t = rt(O, shape, 13)
+    us = [O.gaussian_matrix(s, 7, (14, k)) for k, s in enumerate(shape)]
+    ref = O.ttm_all(t, us, skip, True)
+    got = P.ttm_all(P.DenseTensor.from_numpy(t), us, skip)
+    assert rel(got, ref) < 1e-12
+
+
+@pytest.mark.parametrize("shape", [(40, 30, 20), (7, 9, 11), (10, 9, 8, 7)])
+def test_unfold_times(P, O, shape):
+    t = rt(O, shape, 11)
+    for n in range(len(shape)):
+        b = O.gaussian_matrix(t.size // t.shape[n], 6, (12, n))
+        assert rel(P.unfold_times(P.DenseTensor.from_numpy(t), n, b), O.unfold_times(t, n, b)) < 1e-12
+
+
+# ------------------------------------------------------------------ pivoted QR
+@pytest.mark.parametrize("rows,cols", [(50, 8), (200, 15), (1000, 30), (2400, 40), (300, 20), (31, 31), (4000, 60),
+                                       (12, 1)])
+def test_orthonormal_basis_matches_oracle(P, O, rows, cols):
+    z = O.gaussian_matrix(rows, cols, (rows, cols))
+    if cols > 2:
+        z[:, 1] = 3.0 * z[:, 0] + 1e-3 * z[:, 1]  # exercises the norm downdate / recompute path
+    u_ref, d = O.orthonormal_basis(z, diagnostics=True)
+    u_ref = O.fix_column_signs(u_ref)
+    u, diag = P.orthonormal_basis(z, with_diag=True)
+    assert u.shape == u_ref.shape
+    assert np.allclose(np.abs(diag), np.abs(d["rdiag"]), rtol=1e-10, atol=1e-12)  # same pivots, same R_kk
+    assert np.max(np.abs(u - u_ref)) < 1e-10
+    assert orthonormality_defect(u) < 1e-12
+
+
+def test_orthonormal_basis_rank_deficient_and_zero(P, O):
+    z = np.zeros((5, 2))
+    z[0, 0], z[0, 1] = 1.0, 2.0
+    u = P.orthonormal_basis(z)
+    assert u.shape == (5, 1) and abs(abs(u[0, 0]) - 1.0) < 1e-14
+    assert P.orthonormal_basis(np.zeros((6, 3))).shape == (6, 0)
+    m = O.gaussian_matrix(40, 6, (3, 0)) @ O.gaussian_matrix(6, 16, (3, 1))
+    u = P.orthonormal_basis(m)
+    u_ref = O.fix_column_signs(O.orthonormal_basis(m))
+    assert u.shape == u_ref.shape == (40, 6)
+    assert subspace_dist(u, u_ref) < 1e-10
+
+
+# ------------------------------------------------------------------ Tucker drivers
+def compare_models(O, y, got, ref, tol):
+    g_ref, us_ref = ref
+    assert [u.shape[1] for u in got.factors] == [u.shape[1] for u in us_ref]
+    for u, v in zip(got.factors, us_ref):
+        assert subspace_dist(u, v) < tol * max(1.0, np.sqrt(v.shape[1]))
+        assert orthonormality_defect(u) < 1e-10
+    # core after aligning bases: G x_n (U_n^T U'_n)
+    aligned = O.ttm_all(got.core, [u.T @ v for u, v in zip(got.factors, us_ref)], -1, False)
+    assert rel(aligned, g_ref) < tol
+    f_got = O.fit(y, O.reconstruct(got.core, got.factors))
+    f_ref = O.fit(y, O.reconstruct(g_ref, us_ref))
+    assert abs(f_got - f_ref) < tol
+
+
+@pytest.mark.parametrize("dims,ranks,p,snr", [((40, 36, 30), (5, 4, 3), 5, 10.0), ((24, 24, 24, 24), (3, 3, 3, 3), 4, 20.0),
+                                              ((64, 50), (6, 5), 4, 10.0), ((300, 12, 10), (4, 4, 4), 3, 5.0)])
+def test_rand_tucker_2i_f64_matches_oracle(P, O, dims, ranks, p, snr):
+    y = noisy_tucker(O, dims, ranks, snr, (1, 2))
+    seed = (33, 0)
+    ref = O.rand_tucker_2i(y, ranks, p, seed)
+    got = P.rand_tucker_2i(y, ranks, p, seed)
+    compare_models(O, y, got, ref, F64_TOL)
+    # bitwise determinism (reference test_tucker.cpp:108-117)
+    again = P.rand_tucker_2i(y, ranks, p, seed)
+    assert np.array_equal(again.core, got.core)
+
+
+def test_config1_cpu_runnable_case(P, O):
+    """BASELINE config 1: 200^3 fp64 rank-10 CP with U(0,1) factors + noise at 10 dB,
+    ranks (10,10,10), oversample 5; then FFCP rank 10 (bench.hpp seeds, cfg.seed=0)."""
+    root = (0, 0)
+    data = O.seed_derived(*root, 0xDA7A, 0)
+    alg = O.seed_derived(*root, 0xA16D, 0)
+    y, _ = O.gen_cp((200, 200, 200), 10, O.CP_UNIFORM, data)
+    y = O.add_noise(y, 10.0, O.seed_derived(*data, 0xAD0))
+    ref = O.rand_tucker_2i(y, (10, 10, 10), 5, alg)
+    got = P.rand_tucker_2i(y, (10, 10, 10), 5, alg)
+    compare_models(O, y, got, ref, F64_TOL)
+    a_ref, tr_ref, it_ref = O.ffcp(ref[0], ref[1], 10, O.NONE, 0.0, 200, 1e-6, alg)
+    res = P.ffcp(got, 10, stop=P.StopRule(200, 1e-6), seed=alg)
+    assert abs(res.fit_trace[-1] - tr_ref[-1]) < F64_TOL
+    f_ref = O.fit(y, O.cp_reconstruct(a_ref))
+    f_got = O.fit(y, O.cp_reconstruct(res.factors))
+    assert abs(f_got - f_ref) < F64_TOL
+
+
+@pytest.mark.parametrize("dims,ranks,p", [((128, 96, 80), (8, 8, 8), 6), ((60, 52, 48, 40), (4, 4, 4, 4), 4)])
+def test_rand_tucker_2i_f32_matches_oracle(P, O, dims, ranks, p):
+    y = noisy_tucker(O, dims, ranks, 20.0, (3, 4)).astype(np.float32).astype(np.float64)
+    seed = (34, 0)
+    ref = O.rand_tucker_2i(y, ranks, p, seed)
+    got = P.rand_tucker_2i(y.astype(np.float32), ranks, p, seed)
+    compare_models(O, y, got, ref, F32_TOL)
+
+
+def test_rand_tucker_2i_exact_rank_drop(P, O):
+    """Noise-free multilinear rank 5 with r~ = 15: the rank cut drops 10 columns (test_tucker.cpp:108-117)."""
+    core = rt(O, (5, 5, 5), 1)
+    us = [O.gaussian_matrix(30, 5, (32, 2 + n)) for n in range(3)]
+    y = O.reconstruct(core, us)
+    ref = O.rand_tucker_2i(y, (5, 5, 5), 10, (33, 0))
+    for sync in (True, False):
+        got = P.rand_tucker_2i(y, (5, 5, 5), 10, (33, 0), sync_ranks=sync)
+        assert [u.shape[1] for u in got.factors] == [5, 5, 5]
+        assert O.fit(y, O.reconstruct(got.core, got.factors)) > 1 - 1e-8
+        compare_models(O, y, got, ref, F64_TOL)
+
+
+def test_speculative_and_explicit_core_agree(P, O):
+    y = noisy_tucker(O, (50, 40, 30), (5, 5, 5), 10.0, (5, 6))
+    a = P.rand_tucker_2i(y, (5, 5, 5), 5, (7, 0))
+    b = P.rand_tucker_2i(y, (5, 5, 5), 5, (7, 0), sync_ranks=False)
+    c = P.rand_tucker_2i(y, (5, 5, 5), 5, (7, 0), explicit_core_pass=True)
+    assert np.array_equal(a.core, b.core)
+    assert rel(c.core, a.core) < 1e-12
+    assert a.stats["passes"] == 6 and c.stats["passes"] == 7
+
+
+def test_device_resident_path(P, O):
+    import torch
+    y = noisy_tucker(O, (80, 70, 60), (6, 6, 6), 20.0, (8, 9))
+    yd = P.DenseTensor.from_numpy(y, np.float32).cuda()
+    m = P.rand_tucker_2i(yd, (6, 6, 6), 4, (10, 0))
+    assert m.core.is_cuda
+    h = m.to_host()
+    ref = O.rand_tucker_2i(y.astype(np.float32).astype(np.float64), (6, 6, 6), 4, (10, 0))
+    compare_models(O, y, h, ref, F32_TOL)
+
+
+def test_rand_tucker_alg2_matches_oracle(P, O):
+    y = noisy_tucker(O, (60, 50, 40), (5, 5, 5), 10.0, (11, 12))
+    ref = O.rand_tucker(y, (5, 5, 5), 5, (13, 0))
+    got = P.rand_tucker(y, (5, 5, 5), 5, (13, 0))
+    compare_models(O, y, got, ref, F64_TOL)
+
+
+def test_ffcp_variants_match_oracle(P, O):
+    fs = [np.abs(O.gaussian_matrix(d, 3, (84, n))) for n, d in enumerate((10, 9, 8))]
+    y = O.cp_reconstruct(fs)
+    g, us = O.rand_tucker_2i(y, (3, 3, 3), 5, (85, 0))
+    model = P.TuckerModel(g, us, g.shape)
+    for kind in (O.NONE, O.NONNEG_MU, O.NONNEG_HALS, O.SPARSE):
+        a_ref, tr_ref, it_ref = O.ffcp(g, us, 3, kind, 0.05, 30, 0.0, (86, 0))
+        res = P.ffcp(model, 3, P.ConstraintSpec(kind, 0.05), P.StopRule(30, 0.0), (86, 0))
+        assert res.iterations == it_ref
+        assert np.allclose(res.fit_trace, tr_ref, rtol=1e-9, atol=1e-9)
+        for a, b in zip(res.factors, a_ref):
+            assert np.allclose(a, b, rtol=1e-7, atol=1e-9)
+
+
+def test_errors_mirror_reference(P):
+    with pytest.raises(P.TenkitError, match="one rank per mode required"):
+        P.rand_tucker_2i(np.ones((3, 3, 3)), (2, 2), 1, (0, 0))
+    with pytest.raises(P.TenkitError, match="tensor dimensions must be positive"):
+        P.rand_tucker_2i(np.zeros((6, 5, 4)), (2, 2, 2), 1, (0, 0))  # zero data: rank-0 factor

@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .tenkit import Context, SeedSpec, _dptr, _lib
+from .tenkit import Context, SeedSpec, _ctx, _dptr, _lib
 
 _GOLD = 0x9E3779B97F4A7C15
 
@@ -37,7 +37,7 @@ def uniform_matrix(rows: int, cols: int, seed: SeedSpec) -> np.ndarray:
 def gaussian_flat(n: int, seed: SeedSpec, context: Context | None = None):
     """Flat fp64 CUDA tensor of gaussian_tensor / gaussian_matrix draws (random.hpp:85-138)."""
     import torch
-    ctx = context or Context.default()
+    ctx = _ctx(context)  # launches on torch's current stream: ordered with the torch ops below
     out = torch.empty(max(int(n), 1), dtype=torch.float64, device="cuda")
     _lib.check(ctx.lib.tk_gaussian_matrix(ctx.handle, int(n), 1, seed.root, seed.stream, _dptr(out)))
     return out[: int(n)]

@@ -1,0 +1,107 @@
+"""Multi-rank path on CPU (gloo, world_size 2): the slab plan, the tk_comm reduction hook
+(DistComm) and the sharding identity the device driver relies on —
+
+  for n != N-1:  Z_n = sum_g unfold(Y^g x_{p != n} U_p^T, n) Omega_n   (rank g uses rows
+                 [off_g, off_g + L_g) of U_{N-1})
+  for n == N-1:  rank g owns rows [off_g, off_g + L_g) of Z_{N-1} (others zero-padded)
+  core:          G = sum_g Y^g x_0 U_0^T ... x_{N-1} U_{N-1}[off_g:off_g+L_g]^T
+
+(dist.hpp:617-800 semantics). Partial products come from the CPU oracle (test
+infrastructure); the reduction goes through DistComm over torch.distributed/gloo."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def test_plan_slabs_matches_reference_partition():
+    from paper_1412_1885_b200.dist import plan_slabs
+    assert [l for _, l in plan_slabs(300, 8)] == [38, 38, 38, 38, 37, 37, 37, 37]
+    for dim, w in [(1000, 1), (1000, 3), (7, 7), (4000, 8)]:
+        sl = plan_slabs(dim, w)
+        assert sum(l for _, l in sl) == dim and sl[0][0] == 0
+        assert all(sl[i][0] + sl[i][1] == sl[i + 1][0] for i in range(w - 1))
+        assert max(l for _, l in sl) - min(l for _, l in sl) <= 1
+    from paper_1412_1885_b200 import TenkitError
+    with pytest.raises(TenkitError, match="segment lengths must be positive"):
+        plan_slabs(3, 4)
+
+
+def test_exchange_capacity():
+    from paper_1412_1885_b200.dist import exchange_capacity
+    assert exchange_capacity((1000, 1000, 1000), (20, 20, 20), 10) == max(1000 * 30, 30 ** 3)
+    assert exchange_capacity((100, 100, 100), (20, 20, 20), 10) == 30 ** 3
+    assert exchange_capacity((4000, 10, 10), (5, 5, 5), 1) == 4000 * 6
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    try:
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle import pyoracle as O
+        from paper_1412_1885_b200.dist import DistComm, plan_slabs, exchange_capacity
+        O.set_threads(1)
+        dims, ranks, p = (14, 12, 11), (3, 3, 3), 2
+        seed = (5, 0)
+        y = O.add_noise(O.gen_tucker(dims, ranks, seed), 10.0, O.seed_derived(*seed, 0xAD0))
+        off, ln = plan_slabs(dims[-1], world)[rank]
+        yl = np.asfortranarray(y[:, :, off:off + ln])
+        rts = [min(r + p, i) for r, i in zip(ranks, dims)]
+        us = [O.gaussian_matrix(i, r, (9, n)) for n, (i, r) in enumerate(zip(dims, rts))]
+        comm = DistComm(off, dims[-1], exchange_capacity(dims, ranks, p))
+        assert comm.world == world and comm.rank == rank
+        errs = []
+        for n in range(3):
+            om = O.gaussian_matrix(int(np.prod([rts[k] for k in range(3) if k != n])), rts[n], (11, n))
+            full = O.unfold_times(O.ttm_all(y, us, n, True), n, om)
+            ul = [u if k != 2 else u[off:off + ln] for k, u in enumerate(us)]
+            part = O.unfold_times(O.ttm_all(yl, ul, n, True), n, om)
+            if n == 2:  # local rows of Z_{N-1}, zero-padded
+                zp = np.zeros_like(full)
+                zp[off:off + ln] = part
+                part = zp
+            comm.xbuf[: part.size] = __import__("torch").from_numpy(part.ravel(order="F"))
+            assert comm.allreduce(part.size) == 0
+            got = comm.xbuf[: part.size].numpy().reshape(full.shape, order="F")
+            errs.append(float(np.abs(got - full).max() / np.abs(full).max()))
+        g_full = O.ttm_all(y, us, -1, True)
+        ul = [u if k != 2 else u[off:off + ln] for k, u in enumerate(us)]
+        g_part = O.ttm_all(yl, ul, -1, True)
+        comm.xbuf[: g_part.size] = __import__("torch").from_numpy(g_part.ravel(order="F"))
+        comm.allreduce(g_part.size)
+        g_got = comm.xbuf[: g_part.size].numpy().reshape(g_full.shape, order="F")
+        errs.append(float(np.abs(g_got - g_full).max() / np.abs(g_full).max()))
+        st = comm.as_struct()
+        assert st.world == world and st.slab_offset == off and st.global_last_dim == dims[-1]
+        q.put((rank, errs, comm.calls))
+        dist.destroy_process_group()
+    except Exception as e:  # surface the failure in the parent
+        import traceback
+        q.put((rank, repr(e) + traceback.format_exc(), -1))
+
+
+def test_gloo_world2_partial_sketches_reduce_to_single_node():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, errs, calls in res:
+        assert calls == 4, errs
+        assert max(errs) < 1e-12, errs

@@ -85,7 +85,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def window(self, t0, t1):
+        self.t0, self.t1 = t0, t1
 
     def __exit__(self, *exc):
         if self.proc:
@@ -98,7 +101,9 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        inside = [ln for t, ln in self.lines if t0 is None or t0 - 0.1 <= t <= t1 + 0.1]
+        for ln in (inside or [ln for _, ln in self.lines][-3:]):
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -111,7 +116,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "samples_in_timed_region": len(inside)}
 
 
 def dist_setup(n_gpus):
@@ -266,15 +271,18 @@ def run_b200(args, cfg):
     def step(time_kernels=False):
         return P.rand_tucker_2i(yd, cfg["ranks"], cfg["p"], alg_seed, context=ctx, time_kernels=time_kernels, **kw)
 
-    for _ in range(max(args.warmup, 3)):
-        m = step()
-    barrier(world)
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stream_ms, stream_launches, launches = 0.0, 0, 0
     with ClockSampler(local) as clk:
+        t_w = time.perf_counter()
+        nw = 0
+        while nw < max(args.warmup, 3) or time.perf_counter() - t_w < 1.0:  # >= 1 s of warm-up
+            m = step()
+            nw += 1
         barrier(world)
         ev0.record(stream)
+        t0 = time.perf_counter()
         for _ in range(args.steps):
             m = step(time_kernels=True)
             stream_ms += m.stats["stream_ms"]
@@ -282,6 +290,7 @@ def run_b200(args, cfg):
             launches += m.stats["kernel_launches"]
         ev1.record(stream)
         barrier(world)
+        clk.window(t0, time.perf_counter())
     dev_ms = ev0.elapsed_time(ev1)
     dev_ms = all_max(dev_ms, world)
     ms_step = dev_ms / args.steps
@@ -392,7 +401,7 @@ def _ncu_traffic():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))

@@ -36,12 +36,9 @@ void launch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t 
 template <typename T>
 void launch_pack_factor(const double* u, int64_t ld, int64_t rows, int cols, T* up, cudaStream_t s);
 
-// Z = unfold(X, n) * Omega without materialising the unfolding (tensor.hpp:195-209).
-// X is the (B, I, A) view of the projected tensor, Omega is given transposed
-// (omega_t[c * rn + j] = Omega(c, j), c = b + a * B). Z is I x rn column-major double.
+// Materialise the mode-n unfolding of a (B, I, A) view: out[i + (b + a*B)*I] = x[b + i*B + a*B*I]
 template <typename T>
-void launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const double* omega_t, int rn, double* z,
-                   int64_t ldz, cudaStream_t s);
+void launch_unfold(const T* x, int64_t B, int64_t I, int64_t A, T* out, cudaStream_t s);
 
 // Omega packed for the TTM kernels (T, k-major, stride pack_stride(cols)):
 // out[c * stride + j] = normal_at(key, j * rows + c) for j < cols, 0 for the padding.
@@ -50,11 +47,12 @@ void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaSt
 
 // Counter-RNG fills (random.hpp:85-100): out[i + j*rows] = normal_at(key, j*rows + i).
 void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s);
-// Omega transposed: out[c * cols + j] = normal_at(key, j * rows + c)
-void launch_gaussian_transposed(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s);
 
 template <typename S, typename D>
 void launch_cast(const S* in, D* out, int64_t n, cudaStream_t s);
+// out[i + j*ldo] = in[i + j*ldi] (rows x cols)
+template <typename S, typename D>
+void launch_cast2d(const S* in, int64_t ldi, D* out, int64_t ldo, int64_t rows, int64_t cols, cudaStream_t s);
 
 // Column-pivoted Householder QR + rank cut + explicit Q + sign fix of Z (rows x ncols,
 // column-major, ld = rows), the device restatement of orthonormal_basis

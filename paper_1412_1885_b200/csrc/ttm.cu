@@ -185,43 +185,102 @@ __global__ void __launch_bounds__(kConsumers + 32, 1)
 }
 
 // Mode-0 contraction (P == 1): in is (K x A) column-major, K contiguous.
-// out[r + a*cols] = sum_k in[k + a*K] * up[k*R4 + r]. Tiles are transposed through
-// shared memory so the K-contiguous reads stay coalesced.
-constexpr int kKcBA = 256;
+// out[r + a*cols] = sum_k in[k + a*K] * up[k*R4 + r] over this block's K range.
+// A 128-column x 32-k tile is read with full-line loads (each thread one column) and
+// transposed through shared memory; thread (q, g) then owns columns 4q..4q+3 and the
+// r-quads g, g+4, ... so every k costs one 128-bit load of Y and one broadcast 128-bit
+// load of U per 16 FMAs.
+constexpr int kKcBA = 128;
+template <typename T>
+__host__ __device__ constexpr int kc_bk() { return sizeof(T) == 4 ? 32 : 16; }
 template <typename T, int R>
-__global__ void __launch_bounds__(256) ttm_kcontig_kernel(const T* __restrict__ in, const T* __restrict__ up,
-                                                           T* __restrict__ out, int64_t K, int64_t A, int cols) {
+__global__ void __launch_bounds__(128) ttm_kcontig_kernel(const T* __restrict__ in, const T* __restrict__ up,
+                                                           T* __restrict__ out, int64_t K, int64_t A, int cols,
+                                                           int64_t tiles_a, int64_t kchunk) {
     constexpr int R4 = (R + 3) / 4 * 4;
-    constexpr int kKcBK = sizeof(T) == 4 ? 32 : 16;
-    __shared__ T sT[kKcBK][kKcBA + 1];
+    constexpr int NP = (R4 + 15) / 16;  // r-passes of 16 (4 groups x 4)
+    constexpr int kKcBK = kc_bk<T>();
+    __shared__ __align__(16) T sT[kKcBK][kKcBA + 4];
     __shared__ __align__(16) T sU[kKcBK * R4];
-    const int tid = threadIdx.x;
-    const int64_t a0 = int64_t(blockIdx.x) * kKcBA;
-    T acc[R];
+    const int tid = threadIdx.x, q = tid & 31, g = tid >> 5;
+    const int64_t a0 = (blockIdx.x % tiles_a) * kKcBA;
+    const int64_t ks = blockIdx.x / tiles_a;
+    const int64_t kbeg = ks * kchunk, kend = lmin(K, kbeg + kchunk);
+    out += ks * int64_t(cols) * A;
+    T acc[NP][4][4];
 #pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = T(0);
-    for (int64_t k0 = 0; k0 < K; k0 += kKcBK) {
-        const int kn = static_cast<int>(lmin(kKcBK, K - k0));
-        for (int idx = tid; idx < kKcBK * kKcBA; idx += 256) {
-            const int kk = idx % kKcBK, c = idx / kKcBK;
-            const int64_t a = a0 + c;
-            sT[kk][c] = (a < A && kk < kn) ? in[(k0 + kk) + a * K] : T(0);
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) acc[p][c][s] = T(0);
+    const int64_t acol = a0 + tid;
+    const bool vec = (K % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
+    for (int64_t k0 = kbeg; k0 < kend; k0 += kKcBK) {
+        const int kn = static_cast<int>(lmin(kKcBK, kend - k0));
+        if (acol < A) {
+            const T* src = in + acol * K + k0;
+            if (vec && kn == kKcBK) {
+#pragma unroll
+                for (int v = 0; v < kKcBK; v += 16 / int(sizeof(T))) {
+                    T tmp[16 / sizeof(T)];
+                    load_vec<T, 16 / sizeof(T)>(src + v, tmp);
+#pragma unroll
+                    for (int e = 0; e < int(16 / sizeof(T)); ++e) sT[v + e][tid] = tmp[e];
+                }
+            } else {
+                for (int kk = 0; kk < kKcBK; ++kk) sT[kk][tid] = kk < kn ? src[kk] : T(0);
+            }
+        } else {
+            for (int kk = 0; kk < kKcBK; ++kk) sT[kk][tid] = T(0);
         }
-        for (int i = tid; i < kKcBK * R4; i += 256) sU[i] = (i / R4 < kn) ? up[k0 * R4 + i] : T(0);
+        for (int i = tid; i < kKcBK * R4; i += 128) sU[i] = (i / R4 < kn) ? up[(k0 + i / R4) * R4 + i % R4] : T(0);
         __syncthreads();
 #pragma unroll 4
         for (int kk = 0; kk < kKcBK; ++kk) {
-            const T y = sT[kk][tid];
+            T y[4];
+            if constexpr (sizeof(T) == 4) {
+                load_vec<T, 4>(&sT[kk][4 * q], y);
+            } else {
+                T a2[2], b2[2];
+                load_vec<T, 2>(&sT[kk][4 * q], a2);
+                load_vec<T, 2>(&sT[kk][4 * q + 2], b2);
+                y[0] = a2[0], y[1] = a2[1], y[2] = b2[0], y[3] = b2[1];
+            }
 #pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = fma(y, sU[kk * R4 + r], acc[r]);
+            for (int p = 0; p < NP; ++p) {
+                const int rb = 16 * p + 4 * g;
+                if (rb < R4) {
+                    T u[4];
+                    if constexpr (sizeof(T) == 4) {
+                        load_vec<T, 4>(&sU[kk * R4 + rb], u);
+                    } else {
+                        T a2[2], b2[2];
+                        load_vec<T, 2>(&sU[kk * R4 + rb], a2);
+                        load_vec<T, 2>(&sU[kk * R4 + rb + 2], b2);
+                        u[0] = a2[0], u[1] = a2[1], u[2] = b2[0], u[3] = b2[1];
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int s2 = 0; s2 < 4; ++s2) acc[p][c][s2] = fma(y[c], u[s2], acc[p][c][s2]);
+                }
+            }
         }
         __syncthreads();
     }
-    const int64_t a = a0 + tid;
-    if (a < A)
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-            if (r < cols) out[r + a * cols] = acc[r];
+    for (int c = 0; c < 4; ++c) {
+        const int64_t a = a0 + 4 * q + c;
+        if (a < A)
+#pragma unroll
+            for (int p = 0; p < NP; ++p)
+#pragma unroll
+                for (int s2 = 0; s2 < 4; ++s2) {
+                    const int r = 16 * p + 4 * g + s2;
+                    if (r < cols) out[r + a * cols] = acc[p][c][s2];
+                }
+    }
 }
 
 // Any shape: one output element per thread.
@@ -286,8 +345,25 @@ void dispatch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_
             if (launches) ++*launches;
         }
     } else if (P == 1) {
-        const int64_t grid = (Q + kKcBA - 1) / kKcBA;
-        ttm_kcontig_kernel<T, R><<<static_cast<unsigned>(grid), 256, 0, s>>>(in, up, out, K, Q, cols);
+        const int64_t tiles_a = (Q + kKcBA - 1) / kKcBA;
+        int64_t splits = 1;
+        constexpr int bk = kc_bk<T>();
+        if (tiles_a < 4 * 148 && K >= 4 * bk && work) {
+            splits = std::min<int64_t>((4 * 148 + tiles_a - 1) / tiles_a, K / (2 * bk));
+            while (splits > 1 && splits * cols * Q > work_elems) --splits;
+        }
+        const int64_t kchunk = ((K + splits - 1) / splits + bk - 1) / bk * bk;
+        splits = (K + kchunk - 1) / kchunk;
+        T* dst = splits > 1 ? work : out;
+        ttm_kcontig_kernel<T, R><<<static_cast<unsigned>(tiles_a * splits), 128, 0, s>>>(in, up, dst, K, Q, cols,
+                                                                                         tiles_a, kchunk);
+        if (splits > 1) {
+            TK_LAUNCH_CHECK();
+            const int64_t n = int64_t(cols) * Q;
+            splitk_reduce_kernel<T><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(
+                work, out, n, static_cast<int>(splits));
+            if (launches) ++*launches;
+        }
     } else {
         const int64_t n = P * cols * Q;
         const int64_t grid = std::min<int64_t>((n + 255) / 256, 148 * 32);
@@ -309,38 +385,6 @@ __global__ void pack_factor_kernel(const double* __restrict__ u, int64_t ld, int
     }
 }
 
-// Z[i + j*ldz] = sum_c X[b + i*B + a*B*I] * omega_t[c*rn + j], c = b + a*B
-template <typename T>
-__global__ void __launch_bounds__(256) sketch_kernel(const T* __restrict__ x, int64_t B, int64_t I, int64_t A,
-                                                     const double* __restrict__ omega_t, int rn, double* __restrict__ z,
-                                                     int64_t ldz) {
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    __shared__ double red[8][kMaxRank];
-    const int64_t W = B * A;
-    for (int64_t i = blockIdx.x; i < I; i += gridDim.x) {
-        double acc0 = 0.0, acc1 = 0.0;
-        for (int64_t c = ty; c < W; c += 8) {
-            const int64_t b = c % B, a = c / B;
-            const double xv = static_cast<double>(x[b + i * B + a * B * I]);
-            const double* om = omega_t + c * rn;
-            if (tx < rn) acc0 = fma(xv, om[tx], acc0);
-            if (tx + 32 < rn) acc1 = fma(xv, om[tx + 32], acc1);
-        }
-        red[ty][tx] = acc0;
-        red[ty][tx + 32] = acc1;
-        __syncthreads();
-        if (ty == 0) {
-            for (int j = tx; j < rn; j += 32) {
-                double s = 0.0;
-#pragma unroll
-                for (int t = 0; t < 8; ++t) s += red[t][j];
-                z[i + j * ldz] = s;
-            }
-        }
-        __syncthreads();
-    }
-}
-
 __global__ void gaussian_colmajor_kernel(double* __restrict__ out, uint64_t n, uint64_t key) {
     for (uint64_t pr = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; 2 * pr < n; pr += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = 2 * pr;
@@ -352,11 +396,14 @@ __global__ void gaussian_colmajor_kernel(double* __restrict__ out, uint64_t n, u
     }
 }
 
-__global__ void gaussian_transposed_kernel(double* __restrict__ out, int64_t rows, int64_t cols, uint64_t key) {
-    const int64_t n = rows * cols;
+
+// out[i + c*I] = x[b + i*B + a*B*I], c = b + a*B: the mode-n unfolding of a (B, I, A) view
+template <typename T>
+__global__ void unfold_kernel(const T* __restrict__ x, int64_t B, int64_t I, int64_t A, T* __restrict__ out) {
+    const int64_t n = B * I * A;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t c = t / cols, j = t % cols;
-        out[t] = normal_at_key(key, static_cast<uint64_t>(j * rows + c));
+        const int64_t b = t % B, i = (t / B) % I, a = t / (B * I);
+        out[i + (b + a * B) * I] = x[t];
     }
 }
 
@@ -367,6 +414,16 @@ __global__ void gaussian_packed_kernel(T* __restrict__ out, int64_t rows, int co
         const int64_t c = t / stride;
         const int j = static_cast<int>(t % stride);
         out[t] = j < cols ? static_cast<T>(normal_at_key(key, static_cast<uint64_t>(j * rows + c))) : T(0);
+    }
+}
+
+template <typename S, typename D>
+__global__ void cast2d_kernel(const S* __restrict__ in, int64_t ldi, D* __restrict__ out, int64_t ldo, int64_t rows,
+                              int64_t cols) {
+    const int64_t n = rows * cols;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = t % rows, j = t / rows;
+        out[i + j * ldo] = static_cast<D>(in[i + j * ldi]);
     }
 }
 
@@ -418,25 +475,20 @@ void launch_pack_factor(const double* u, int64_t ld, int64_t rows, int cols, T* 
     TK_LAUNCH_CHECK();
 }
 
-template <typename T>
-void launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const double* omega_t, int rn, double* z,
-                   int64_t ldz, cudaStream_t s) {
-    require(rn >= 1 && rn <= kMaxRank, "sketch: r_tilde must be in [1, 64]");
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(I, 148 * 8));
-    sketch_kernel<T><<<grid, 256, 0, s>>>(x, B, I, A, omega_t, rn, z, ldz);
-    TK_LAUNCH_CHECK();
-}
-
 void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s) {
     const uint64_t n = uint64_t(rows) * uint64_t(cols);
     gaussian_colmajor_kernel<<<grid_for(static_cast<int64_t>((n + 1) / 2)), 256, 0, s>>>(out, n, key);
     TK_LAUNCH_CHECK();
 }
 
-void launch_gaussian_transposed(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s) {
-    gaussian_transposed_kernel<<<grid_for(rows * cols), 256, 0, s>>>(out, rows, cols, key);
+
+template <typename T>
+void launch_unfold(const T* x, int64_t B, int64_t I, int64_t A, T* out, cudaStream_t s) {
+    unfold_kernel<T><<<grid_for(B * I * A), 256, 0, s>>>(x, B, I, A, out);
     TK_LAUNCH_CHECK();
 }
+template void launch_unfold<float>(const float*, int64_t, int64_t, int64_t, float*, cudaStream_t);
+template void launch_unfold<double>(const double*, int64_t, int64_t, int64_t, double*, cudaStream_t);
 
 template <typename T>
 void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaStream_t s) {
@@ -459,10 +511,13 @@ template void launch_ttm<double>(const double*, const double*, double*, int64_t,
                                  int*, double*, int64_t);
 template void launch_pack_factor<float>(const double*, int64_t, int64_t, int, float*, cudaStream_t);
 template void launch_pack_factor<double>(const double*, int64_t, int64_t, int, double*, cudaStream_t);
-template void launch_sketch<float>(const float*, int64_t, int64_t, int64_t, const double*, int, double*, int64_t,
-                                   cudaStream_t);
-template void launch_sketch<double>(const double*, int64_t, int64_t, int64_t, const double*, int, double*, int64_t,
-                                    cudaStream_t);
+template <typename S, typename D>
+void launch_cast2d(const S* in, int64_t ldi, D* out, int64_t ldo, int64_t rows, int64_t cols, cudaStream_t s) {
+    cast2d_kernel<S, D><<<grid_for(rows * cols), 256, 0, s>>>(in, ldi, out, ldo, rows, cols);
+    TK_LAUNCH_CHECK();
+}
+template void launch_cast2d<float, double>(const float*, int64_t, double*, int64_t, int64_t, int64_t, cudaStream_t);
+template void launch_cast2d<double, double>(const double*, int64_t, double*, int64_t, int64_t, int64_t, cudaStream_t);
 template void launch_cast<float, double>(const float*, double*, int64_t, cudaStream_t);
 template void launch_cast<double, float>(const double*, float*, int64_t, cudaStream_t);
 template void launch_cast<double, double>(const double*, double*, int64_t, cudaStream_t);

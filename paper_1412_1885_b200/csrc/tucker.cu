@@ -177,25 +177,42 @@ struct TuckerRun {
         if (buf != c.xbuf) TK_CUDA(cudaMemcpyAsync(buf, c.xbuf, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
 
+    // Z = unfold(X, n) * Omega (tensor.hpp:195-209): X is small, so its mode-n unfolding is
+    // materialised and multiplied by the packed Omega with the same TTM kernel as the Y
+    // passes; Z (T) is widened to fp64 into z (leading dimension ldz) for the QR.
+    void sketch(const T* x, const std::vector<int64_t>& xd, int n, const T* omp, int rn, double* z, int64_t ldz) {
+        const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + n));
+        const int64_t I = xd[n];
+        const int64_t A = prod(std::vector<int64_t>(xd.begin() + n + 1, xd.end()));
+        const T* xu = x;
+        if (B > 1) {
+            T* b = static_cast<T*>(ctx->buf("xunf", sizeof(T) * B * I * A));
+            launch_unfold<T>(x, B, I, A, b, s);
+            ++launches;
+            xu = b;
+        }
+        T* zt = static_cast<T*>(ctx->buf("zt", sizeof(T) * I * rn));
+        ttm(xu, omp, zt, I, B * A, 1, rn);
+        launch_cast2d<T, double>(zt, I, z, ldz, I, rn, s);
+        ++launches;
+    }
+
     // One range-finding step for mode n: Z = unfold(X, n) Omega, U_n = basis(Z)
     void range_step(const T* x, const std::vector<int64_t>& xd, int n, const Seed& omega_seed, int step, bool sync) {
         const int64_t W = prod(std::vector<int64_t>(cols.begin(), cols.end()), n);
         const int rn = rt[n];
-        double* om = static_cast<double*>(ctx->buf("omega", sizeof(double) * W * rn));
-        launch_gaussian_transposed(om, W, rn, omega_seed.key(), s);
+        T* omp = static_cast<T*>(ctx->buf("omega_p", sizeof(T) * W * pack_stride(rn)));
+        launch_gaussian_packed<T>(omp, W, rn, omega_seed.key(), s);
         ++launches;
         const int64_t In = gdims[n];
         double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * In * rn));
-        const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + n));
-        const int64_t A = prod(std::vector<int64_t>(xd.begin() + n + 1, xd.end()));
         const bool local_rows = ctx->has_comm && ctx->comm.world > 1 && n == order - 1;
         if (local_rows) {
             TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * In * rn, s));
-            launch_sketch<T>(x, B, xd[n], A, om, rn, z + offset, In, s);
+            sketch(x, xd, n, omp, rn, z + offset, In);
         } else {
-            launch_sketch<T>(x, B, xd[n], A, om, rn, z, In, s);
+            sketch(x, xd, n, omp, rn, z, In);
         }
-        ++launches;
         allreduce(z, In * rn);
         launch_orthonormal_basis(z, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64, rank_dev + step,
                                  nullptr, s);
@@ -323,12 +340,10 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
             else launch_cast<double, double>(reinterpret_cast<const double*>(zt), z, cd[0] * rt, s);
             r.launches += 2;
         } else {
-            double* om = static_cast<double*>(ctx->buf("omega", sizeof(double) * width * rt));
-            launch_gaussian_transposed(om, width, rt, os.key(), s);
-            const int64_t B = prod(std::vector<int64_t>(cd.begin(), cd.begin() + n));
-            const int64_t A = prod(std::vector<int64_t>(cd.begin() + n + 1, cd.end()));
-            launch_sketch<T>(cur, B, cd[n], A, om, rt, z, cd[n], s);
-            r.launches += 2;
+            T* op = static_cast<T*>(ctx->buf("omega_packed", sizeof(T) * width * pack_stride(rt)));
+            launch_gaussian_packed<T>(op, width, rt, os.key(), s);
+            r.sketch(cur, cd, n, op, rt, z, cd[n]);
+            ++r.launches;
         }
         U[n] = static_cast<double*>(ctx->buf("U" + std::to_string(n), sizeof(double) * cd[n] * rt));
         T* up = static_cast<T*>(ctx->buf("Up" + std::to_string(n), sizeof(T) * cd[n] * pack_stride(rt)));
@@ -622,20 +637,16 @@ int tk_unfold_times(tk_context* ctx, int dtype, int64_t order, const int64_t* di
         const int64_t B = prod(std::vector<int64_t>(d.begin(), d.begin() + mode));
         const int64_t A = prod(std::vector<int64_t>(d.begin() + mode + 1, d.end()));
         const int64_t W = B * A;
-        // b is W x bcols column-major; the sketch kernel reads it transposed
-        double* bt = static_cast<double*>(ctx->buf("ut_bt", sizeof(double) * W * bcols));
-        std::vector<double> hb(W * bcols), ht(W * bcols);
-        TK_CUDA(cudaMemcpyAsync(hb.data(), b, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, ctx->stream));
-        TK_CUDA(cudaStreamSynchronize(ctx->stream));
-        for (int64_t c = 0; c < W; ++c)
-            for (int64_t j = 0; j < bcols; ++j) ht[c * bcols + j] = hb[c + j * W];
-        TK_CUDA(cudaMemcpyAsync(bt, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice, ctx->stream));
-        if (dtype == TK_F32)
-            launch_sketch<float>(static_cast<const float*>(t), B, d[mode], A, bt, static_cast<int>(bcols), z, d[mode],
-                                 ctx->stream);
-        else
-            launch_sketch<double>(static_cast<const double*>(t), B, d[mode], A, bt, static_cast<int>(bcols), z, d[mode],
-                                  ctx->stream);
+        require(bcols >= 1 && bcols <= kMaxRank, "unfold_times: B columns must be in [1, 64] on the device path");
+        auto body = [&](auto tag) {
+            using T = decltype(tag);
+            TuckerRun<T> r{ctx, ctx->stream, order, d, d, 0, static_cast<const T*>(t)};
+            T* bp = static_cast<T*>(ctx->buf("ut_bp", sizeof(T) * W * pack_stride(static_cast<int>(bcols))));
+            launch_pack_factor<T>(b, W, W, static_cast<int>(bcols), bp, ctx->stream);
+            r.sketch(static_cast<const T*>(t), d, static_cast<int>(mode), bp, static_cast<int>(bcols), z, d[mode]);
+        };
+        if (dtype == TK_F32) body(float{});
+        else body(double{});
         TK_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }

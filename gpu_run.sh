@@ -1,9 +1,8 @@
 #!/bin/bash
-# one gpurun session: environment probe, GPU parity tests, smoke, short bench
-set -x
 mkdir -p gpurun_out
-(nproc; lscpu | head -20; free -g; nvidia-smi; df -h /tmp) > gpurun_out/env.txt 2>&1
+python tools/qr_bench.py > gpurun_out/qr_bench.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:qr_colpiv -s 9 -c 1 -o gpurun_out/prof_qr python tools/qr_bench.py > gpurun_out/ncu_qr.log 2>&1
+echo "ncu rc=$?"
+cat gpurun_out/qr_bench.log
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+tail -3 gpurun_out/pytest_gpu.log

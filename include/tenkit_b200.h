@@ -94,7 +94,8 @@ int tk_device_ok(void);
 
 int tk_context_create(int device, tk_context** out);
 int tk_context_destroy(tk_context* ctx);
-/* Run on an external CUDA stream (cudaStream_t); NULL = the context's own stream */
+/* Run on an external CUDA stream (cudaStream_t), taken literally: NULL is the legacy default
+ * stream (torch's default stream). A new context runs on its own non-blocking stream. */
 int tk_context_set_stream(tk_context* ctx, void* cuda_stream);
 /* Install (or clear, with NULL) the cross-rank reduction hook */
 int tk_context_set_comm(tk_context* ctx, const tk_comm* comm);

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtenkit_b200.so")
+LIB_PATH = os.environ.get("TENKIT_B200_LIB") or os.path.join(HERE, "lib", "libtenkit_b200.so")
 
 TK_MAX_ORDER = 8
 TK_OK, TK_ERR_INVALID, TK_ERR_CUDA, TK_ERR_NO_DEVICE, TK_ERR_INTERNAL = range(5)

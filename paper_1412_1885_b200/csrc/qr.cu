@@ -4,16 +4,16 @@
 // ColPivHouseholderQR, rank = #leading |R_kk| > 1e-12 |R_00|, Q = first `rank` Householder
 // columns in pivot order) followed by fix_column_signs (tucker.hpp:39-45), all in fp64.
 //
-// Z (rows x ncols, rows <= a few thousand, ncols <= 64) is split into contiguous row
-// blocks held in the shared memory of the cluster's CTAs (distributed shared memory).
-// Each Householder step needs exactly one cluster-wide reduction (column-k tail norm, the
-// dot products of column k with the trailing columns, and row k itself); partial vectors
-// are exchanged through DSMEM and summed in fixed CTA order, so results are deterministic.
-// Pivoting is done by a logical->physical column map (no data movement); the pivot
-// choice, the Householder scalars and the LAPACK-style norm downdating (direct
-// recomputation below sqrt(eps)) are evaluated redundantly and identically in every warp
-// of every CTA, which keeps a step at one cluster barrier plus two CTA barriers. Q is then
-// formed in place over the stored reflectors (backward accumulation).
+// Z (rows x ncols, ncols <= 64) is split into contiguous row blocks held in the shared
+// memory of the CTAs of one thread-block cluster. The QR is latency-bound (every step
+// depends on the previous one), so a step is kept to: warp-redundant pivot argmax ->
+// column swap -> ONE reduction of [col_k . col_j | row_k] (8 threads per column over
+// interleaved rows + 3 shuffle rounds, then a DSMEM exchange summed in fixed CTA order)
+// -> Householder scalars evaluated redundantly -> 2-D parallel trailing update + one
+// thread per column for the LAPACK-style norm downdate (direct recomputation below
+// sqrt(eps), as Eigen / xGEQP3). Q is formed in place by backward accumulation with the
+// same reduction. All loops stay rolled: the kernel is small enough to live in the
+// instruction cache (straight-line unrolled variants were instruction-fetch bound).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -23,337 +23,366 @@
 
 namespace cg = cooperative_groups;
 
+#ifdef TK_QR_TRACE
+__device__ long long g_qr_trace[4096];
+#define QR_MARK(slot)                                                                            \
+    do {                                                                                         \
+        if (threadIdx.x == 0 && blockIdx.x == 0 && (slot) < 4096) g_qr_trace[(slot)] = clock64(); \
+    } while (0)
+#else
+#define QR_MARK(slot) \
+    do {              \
+    } while (0)
+#endif
+
 namespace tkb {
 
 namespace {
 
 constexpr int kQrThreads = 512;
-constexpr int kQrWarps = kQrThreads / 32;
-constexpr int kSlot = 3 * kMaxRank + 8;  // exchange vector length (doubles)
-constexpr size_t kQrFixedSmem = (3 * kSlot + 6 * kMaxRank + 16) * sizeof(double) + (kMaxRank + 16) * sizeof(int);
+constexpr int kTpc = 16;  // threads per column in the reductions (kQrThreads / kTpc columns per pass)
+constexpr int kVec = 2 * kMaxRank + 8;
+constexpr size_t kQrFixedSmem = (3 * kVec + 6 * kMaxRank) * sizeof(double) + 16 * sizeof(int);
 constexpr size_t kQrSmemCap = 200 * 1024;
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-struct Xchg {
-    cg::cluster_group cl;
-    unsigned cs;
-    double* slot;  // [2][kSlot]
-    double* tot;   // [kSlot]
-    int par = 0;
-
-    __device__ double* mine() { return slot + par * kSlot; }
-    __device__ void sync_all() {
-        if (cs > 1) cl.sync();
-        else __syncthreads();
-    }
-    // Sum of every CTA's slot[par][0:len] in CTA order into tot (block-visible on return)
-    __device__ void sum(int len) {
-        sync_all();
-        double* m = mine();
-        for (int i = threadIdx.x; i < len; i += blockDim.x) {
-            double s = 0.0;
-            if (cs > 1)
-                for (unsigned c = 0; c < cs; ++c) s += cl.map_shared_rank(m, c)[i];
-            else
-                s = m[i];
-            tot[i] = s;
-        }
-        par ^= 1;
-        __syncthreads();
-    }
+struct Sh {
+    double* z;     // [ncols][ld] own rows, column-major
+    double* slot;  // [2][kVec] cluster exchange
+    double* tot;   // [kVec]
+    double *upd, *dir, *beta, *taus, *sgn, *wv;
+    int* flag;
 };
+
+// tot[j - j0] (j in [j0, j1)) = sum over own rows i in [i0, nloc) of a[i] * z[j][i], then the
+// sum over the cluster's CTAs; extra[e * xstride] (e < nextra; a null `extra` contributes
+// zeros) is summed into tot[kMaxRank + e] the same way. Block-visible on return.
+__device__ void reduce_dots(Sh& sh, cg::cluster_group& cl, unsigned cs, int& par, const double* a, int ld, int i0,
+                            int nloc, int j0, int j1, const double* extra, int xstride, int nextra) {
+    const int tid = threadIdx.x, sub = tid % kTpc, grp = tid / kTpc;
+    double* m = sh.slot + par * kVec;
+    // warp-uniform trip count (the shuffles need all 32 lanes): groups past j1 compute 0
+    for (int base = j0; base + (tid / 32) * (32 / kTpc) < j1; base += kQrThreads / kTpc) {
+        const int j = base + grp;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (j < j1) {
+            const double* b = sh.z + size_t(j) * ld;
+            int i = i0 + sub;
+            for (; i + 3 * kTpc < nloc; i += 4 * kTpc) {
+                s0 = fma(a[i], b[i], s0);
+                s1 = fma(a[i + kTpc], b[i + kTpc], s1);
+                s2 = fma(a[i + 2 * kTpc], b[i + 2 * kTpc], s2);
+                s3 = fma(a[i + 3 * kTpc], b[i + 3 * kTpc], s3);
+            }
+            for (; i < nloc; i += kTpc) s0 = fma(a[i], b[i], s0);
+        }
+        double s = (s0 + s1) + (s2 + s3);
+        s += __shfl_xor_sync(0xffffffffu, s, 8);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        if (sub == 0 && j < j1) m[j - j0] = s;
+    }
+    for (int e = tid; e < nextra; e += kQrThreads) m[kMaxRank + e] = extra ? extra[size_t(e) * xstride] : 0.0;
+    const int len = kMaxRank + nextra;
+    if (cs > 1) {
+        cl.sync();
+        for (int t = tid; t < len; t += kQrThreads) {
+            if (t >= j1 - j0 && t < kMaxRank) continue;
+            double s = 0.0;
+            for (unsigned c = 0; c < cs; ++c) s += cl.map_shared_rank(m, c)[t];
+            sh.tot[t] = s;
+        }
+    } else {
+        __syncthreads();
+        for (int t = tid; t < len; t += kQrThreads) sh.tot[t] = m[t];
+    }
+    par ^= 1;
+    __syncthreads();
+}
 
 __global__ void __launch_bounds__(kQrThreads, 1)
     qr_colpiv_cluster_kernel(const double* __restrict__ zin, int64_t rows, int ncols, int ld,
                              double* __restrict__ uout, int ucap, void* upout, int up_dtype, int* rank_out,
                              double* diag_out) {
     cg::cluster_group cl = cg::this_cluster();
+    const unsigned cs = cl.num_blocks();
     const int crank = static_cast<int>(cl.block_rank());
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     extern __shared__ __align__(16) double qsm[];
-    double* z = qsm;
-    double* slot = z + size_t(ld) * ncols;
-    double* tot = slot + 2 * kSlot;
-    double* upd = tot + kSlot;
-    double* dir = upd + kMaxRank;
-    double* beta = dir + kMaxRank;
-    double* taus = beta + kMaxRank;
-    double* sgn = taus + kMaxRank;
-    double* misc = sgn + kMaxRank;
-    int* colmap = reinterpret_cast<int*>(misc + 16);
-    int* flags = colmap + kMaxRank;  // [0..1] recompute-any flags by step parity
-
-    Xchg X{cl, cl.num_blocks(), slot, tot};
+    Sh sh;
+    sh.z = qsm;
+    sh.slot = sh.z + size_t(ld) * ncols;
+    sh.tot = sh.slot + 2 * kVec;
+    sh.upd = sh.tot + kVec;
+    sh.dir = sh.upd + kMaxRank;
+    sh.beta = sh.dir + kMaxRank;
+    sh.taus = sh.beta + kMaxRank;
+    sh.sgn = sh.taus + kMaxRank;
+    sh.wv = sh.sgn + kMaxRank;
+    sh.flag = reinterpret_cast<int*>(sh.wv + kMaxRank);
+    double* z = sh.z;
     const int64_t r0 = int64_t(crank) * ld;
     const int nloc = static_cast<int>(lmax(0, lmin(ld, rows - r0)));
+    int par = 0;
+    QR_MARK(0);
 
-    for (int j = 0; j < ncols; ++j)
-        for (int i = tid; i < ld; i += kQrThreads) z[i + j * ld] = i < nloc ? zin[(r0 + i) + j * rows] : 0.0;
-    for (int j = tid; j < kMaxRank; j += kQrThreads) colmap[j] = j;
-    if (tid < 2) flags[tid] = 0;
-    __syncthreads();
-
-    // initial column norms (m_qr.col(k).norm())
-    for (int j = warp; j < ncols; j += kQrWarps) {
-        double s = 0.0;
-        for (int i = lane; i < nloc; i += 32) s += z[i + j * ld] * z[i + j * ld];
-        s = warp_sum(s);
-        if (lane == 0) X.mine()[j] = s;
+#pragma unroll 4
+    for (int t = tid; t < ld * ncols; t += kQrThreads) {
+        const int i = t % ld, j = t / ld;
+        z[t] = i < nloc ? zin[(r0 + i) + int64_t(j) * rows] : 0.0;
     }
-    X.sum(ncols);
-    for (int j = tid; j < ncols; j += kQrThreads) upd[j] = dir[j] = sqrt(tot[j]);
+    if (tid < 2) sh.flag[tid] = 0;
     __syncthreads();
+
+    // initial column norms (m_qr.col(k).norm()): one reduction of col_j . col_j
+    {
+        double* m = sh.slot + par * kVec;
+        const int sub = tid % kTpc, grp = tid / kTpc;
+        for (int base = 0; base + warp * (32 / kTpc) < ncols; base += kQrThreads / kTpc) {
+            const int j = base + grp;
+            double s = 0.0;
+            if (j < ncols) {
+                const double* b = z + size_t(j) * ld;
+                for (int i = sub; i < nloc; i += kTpc) s = fma(b[i], b[i], s);
+            }
+            s += __shfl_xor_sync(0xffffffffu, s, 8);
+            s += __shfl_xor_sync(0xffffffffu, s, 4);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            if (sub == 0 && j < ncols) m[j] = s;
+        }
+        if (cs > 1) cl.sync();
+        else __syncthreads();
+        for (int j = tid; j < ncols; j += kQrThreads) {
+            double s = 0.0;
+            for (unsigned c = 0; c < cs; ++c) s += (cs > 1 ? cl.map_shared_rank(m, c) : m)[j];
+            sh.upd[j] = sh.dir[j] = sqrt(s);
+        }
+        par ^= 1;
+        __syncthreads();
+    }
 
     const double norm_downdate_threshold = sqrt(DBL_EPSILON);
     const int size = static_cast<int>(lmin(rows, ncols));
-    int pprev = -1;  // physical column of the previous step (its essential part is written late)
-    double dprev = 1.0;
-    bool zprev = false;
-    int kprev = -1;
+    QR_MARK(1);
     for (int k = 0; k < size; ++k) {
-        // ---- pivot: first maximum of the updated norms over logical columns k.. (per warp)
-        int best;
-        {
-            double bv = -1.0;
-            int bi = 0x7fffffff;
-            for (int j = k + lane; j < ncols; j += 32)
-                if (upd[j] > bv) {
-                    bv = upd[j];
-                    bi = j;
-                }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ov > bv || (ov == bv && oi < bi)) {
-                    bv = ov;
-                    bi = oi;
-                }
-            }
-            best = bi;
+        QR_MARK(7 + 8 * k);
+        // ---- pivot: first maximum of the updated norms over columns k.. (every warp)
+        double bv = -1.0;
+        int best = k;
+        for (int j = k + lane; j < ncols; j += 32) {
+            const double u = sh.upd[j];
+            const bool take = u > bv;
+            bv = take ? u : bv;
+            best = take ? j : best;
         }
-        // registers: thread 0 swaps colmap[k] / colmap[best] during this step's update phase
-        const int ck = colmap[k];
-        const int pk = colmap[best];
-        auto phys = [&](int j) { return j == best ? ck : colmap[j]; };
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, best, o);
+            const bool take = ov > bv || (ov == bv && oi < best);
+            bv = take ? ov : bv;
+            best = take ? oi : best;
+        }
+        const double upd_k = sh.upd[k], dir_k = sh.dir[k];
+        QR_MARK(6 + 8 * k);
+        if (best != k) {  // uniform: swap columns k and best
+            for (int i = tid; i < nloc; i += kQrThreads) {
+                const double t = z[i + k * ld];
+                z[i + k * ld] = z[i + best * ld];
+                z[i + best * ld] = t;
+            }
+            __syncthreads();
+        }
+        QR_MARK(8 + 8 * k);
         const int lk = static_cast<int>(k - r0);
         const bool owner = lk >= 0 && lk < nloc;
         const int i0 = static_cast<int>(lmax(0, k + 1 - r0));
 
-        // ---- local partials: [j-k] = dot(col k, col j) over rows > k ([0]: tail norm^2),
-        //      [kMaxRank + j-k] = row k (owner; others 0)
-        {
-            double* m = X.mine();
-            for (int j = k + warp; j < ncols; j += kQrWarps) {
-                const int pj = j == k ? pk : phys(j);
-                double s = 0.0;
-                for (int i = i0 + lane; i < nloc; i += 32) s += z[i + pk * ld] * z[i + pj * ld];
-                s = warp_sum(s);
-                if (lane == 0) {
-                    m[j - k] = s;
-                    m[kMaxRank + (j - k)] = owner ? z[lk + pj * ld] : 0.0;
-                }
-            }
-            if (pprev >= 0) {  // late essential write of the previous step's column
-                const int ip = static_cast<int>(lmax(0, kprev + 1 - r0));
-                for (int i = ip + tid; i < nloc; i += kQrThreads)
-                    z[i + pprev * ld] = zprev ? 0.0 : z[i + pprev * ld] / dprev;
-            }
-        }
-        X.sum(kMaxRank + (ncols - k));
+        // ---- one reduction: tot[j-k] = col_k . col_j over rows > k ([0]: tail norm^2),
+        //      tot[kMaxRank + j-k] = row k (contributed by the owner CTA only)
+        reduce_dots(sh, cl, cs, par, z + size_t(k) * ld, ld, i0, nloc, k, ncols,
+                    owner ? z + lk + size_t(k) * ld : nullptr, ld, ncols - k);
+        QR_MARK(10 + 8 * k);
 
         // ---- Householder scalars (makeHouseholderInPlace), redundantly in every thread
-        const double tail_sq = (rows - k == 1) ? 0.0 : tot[0];
-        const double c0 = tot[kMaxRank];
-        double tau, bta, denom = 1.0;
-        bool zero_ess = false;
+        const double tail_sq = (rows - k == 1) ? 0.0 : sh.tot[0];
+        const double c0 = sh.tot[kMaxRank];
+        double tau, bta, rden = 0.0;  // essential v = tail * rden, rden = 1 / (c0 - beta)
         if (tail_sq <= DBL_MIN) {
             tau = 0.0;
             bta = c0;
-            zero_ess = true;
         } else {
             bta = sqrt(c0 * c0 + tail_sq);
             if (c0 >= 0.0) bta = -bta;
-            denom = c0 - bta;
+            rden = 1.0 / (c0 - bta);
             tau = (bta - c0) / bta;
         }
         if (tid == 0) {
-            beta[k] = bta;
-            taus[k] = tau;
-            flags[(k + 1) & 1] = 0;
+            sh.beta[k] = bta;
+            sh.taus[k] = tau;
+            sh.flag[(k + 1) & 1] = 0;
         }
-
-        // ---- apply H_k to the trailing columns: w_j = row0_j + dot_j / denom,
-        //      col_j -= (tau * v) w_j with v = col_k / denom; norm downdate per column
-        for (int j = k + 1 + warp; j < ncols; j += kQrWarps) {
-            const int pj = phys(j);
-            const double rowk = tot[kMaxRank + (j - k)];
-            const double wj = tau != 0.0 ? rowk + tot[j - k] / denom : 0.0;
+        // ---- w_j and the norm downdate, one thread per trailing column (xGEQP3); position
+        //      `best` inherits the norms of the column swapped out of position k
+        for (int j = k + 1 + tid; j < ncols; j += kQrThreads) {
+            const double rowk = sh.tot[kMaxRank + (j - k)];
+            const double wj = tau != 0.0 ? rowk + sh.tot[j - k] * rden : 0.0;
+            sh.wv[j] = wj;
             const double nrow = tau != 0.0 ? rowk - tau * wj : rowk;
-            if (tau != 0.0)
-                for (int i = i0 + lane; i < nloc; i += 32) z[i + pj * ld] -= (tau * (z[i + pk * ld] / denom)) * wj;
-            if (owner && lane == 0) z[lk + pj * ld] = nrow;
-            const double u = (j == best) ? upd[k] : upd[j];
-            const double d = (j == best) ? dir[k] : dir[j];
-            bool recompute = false;
+            const double u = (j == best) ? upd_k : sh.upd[j];
+            const double d = (j == best) ? dir_k : sh.dir[j];
             double nu = u;
             if (u != 0.0) {
                 double temp = fabs(nrow) / u;
                 temp = (1.0 + temp) * (1.0 - temp);
                 temp = temp < 0.0 ? 0.0 : temp;
                 const double ratio = u / d;
-                if (temp * ratio * ratio <= norm_downdate_threshold) recompute = true;
-                else nu = u * sqrt(temp);
-            }
-            if (recompute) {  // local partial of the fresh tail norm (rows > k), exchanged below
-                __syncwarp();
-                double s = 0.0;
-                for (int i = i0 + lane; i < nloc; i += 32) s += z[i + pj * ld] * z[i + pj * ld];
-                s = warp_sum(s);
-                if (lane == 0) {
-                    X.mine()[j] = s;
-                    atomicOr(&flags[k & 1], 1);
+                if (temp * ratio * ratio <= norm_downdate_threshold) {
+                    nu = -1.0;  // pending direct recomputation
+                    atomicOr(&sh.flag[k & 1], 1);
+                } else {
+                    nu = u * sqrt(temp);
                 }
             }
-            if (lane == 0) {
-                upd[j] = recompute ? -1.0 : nu;  // -1: pending recompute
-                dir[j] = d;
-            }
+            sh.upd[j] = nu;
+            sh.dir[j] = d;
         }
-        if (owner && tid == 0) z[lk + pk * ld] = bta;
-        if (tid == 0 && best != k) {
-            const int t = colmap[k];
-            colmap[k] = colmap[best];
-            colmap[best] = t;
+        // essential part of column k in place (rows > k), R_kk on the owner
+        for (int i = i0 + tid; i < nloc; i += kQrThreads) z[i + k * ld] *= rden;
+        if (owner && tid == 0) z[lk + k * ld] = bta;
+        __syncthreads();
+        QR_MARK(11 + 8 * k);
+        // ---- trailing update col_j -= (tau v) w_j (rows > k); row k = row_k - tau w_j
+        if (tau != 0.0) {
+            for (int i = i0 + tid; i < nloc; i += kQrThreads) {
+                const double tv = tau * z[i + k * ld];
+#pragma unroll 4
+                for (int j = k + 1; j < ncols; ++j) z[i + j * ld] = fma(-tv, sh.wv[j], z[i + j * ld]);
+            }
+            if (owner)
+                for (int j = k + 1 + tid; j < ncols; j += kQrThreads) z[lk + j * ld] -= tau * sh.wv[j];
         }
         __syncthreads();
-        if (flags[k & 1]) {
-            double* m = X.mine();
-            for (int j = tid; j < ncols; j += kQrThreads)
-                if (j <= k || upd[j] >= 0.0) m[j] = 0.0;
-            X.sum(ncols);
+        QR_MARK(12 + 8 * k);
+        if (sh.flag[k & 1]) {  // identical decision on every CTA
+            double* m = sh.slot + par * kVec;
+            const int sub = tid % kTpc, grp = tid / kTpc;
+            for (int base = k + 1; base + warp * (32 / kTpc) < ncols; base += kQrThreads / kTpc) {
+                const int j = base + grp;
+                double s = 0.0;
+                if (j < ncols && sh.upd[j] < 0.0)
+                    for (int i = i0 + sub; i < nloc; i += kTpc) s = fma(z[i + j * ld], z[i + j * ld], s);
+                s += __shfl_xor_sync(0xffffffffu, s, 8);
+                s += __shfl_xor_sync(0xffffffffu, s, 4);
+                s += __shfl_xor_sync(0xffffffffu, s, 2);
+                s += __shfl_xor_sync(0xffffffffu, s, 1);
+                if (sub == 0 && j < ncols) m[j] = s;
+            }
+            if (cs > 1) cl.sync();
+            else __syncthreads();
             for (int j = k + 1 + tid; j < ncols; j += kQrThreads)
-                if (upd[j] < 0.0) upd[j] = dir[j] = sqrt(tot[j]);
+                if (sh.upd[j] < 0.0) {
+                    double s = 0.0;
+                    for (unsigned c = 0; c < cs; ++c) s += (cs > 1 ? cl.map_shared_rank(m, c) : m)[j];
+                    sh.upd[j] = sh.dir[j] = sqrt(s);
+                }
+            par ^= 1;
             __syncthreads();
         }
-        pprev = pk;
-        dprev = denom;
-        zprev = zero_ess;
-        kprev = k;
     }
-    if (pprev >= 0) {
-        const int ip = static_cast<int>(lmax(0, kprev + 1 - r0));
-        for (int i = ip + tid; i < nloc; i += kQrThreads) z[i + pprev * ld] = zprev ? 0.0 : z[i + pprev * ld] / dprev;
-    }
-    __syncthreads();
+    QR_MARK(2);
 
     // ---- rank cut (range_finder.hpp:24-26), redundantly
     int rank = 0;
     {
-        const double top = fabs(beta[0]);
-        while (rank < size && fabs(beta[rank]) > 1e-12 * top) ++rank;
+        const double top = fabs(sh.beta[0]);
+        while (rank < size && fabs(sh.beta[rank]) > 1e-12 * top) ++rank;
     }
 
-    // ---- explicit Q(:, 0:rank) = H_0 ... H_{rank-1} [I; 0], in place, logical column j at colmap[j]
+    // ---- explicit Q(:, 0:rank) = H_0 ... H_{rank-1} [I; 0], in place
     for (int k = rank - 1; k >= 0; --k) {
-        const double tau = taus[k];
-        const int pk = colmap[k];
+        const double tau = sh.taus[k];
         const int lk = static_cast<int>(k - r0);
         const bool owner = lk >= 0 && lk < nloc;
         const int i0 = static_cast<int>(lmax(0, k + 1 - r0));
         if (k + 1 < rank) {
-            double* m = X.mine();
-            for (int j = k + 1 + warp; j < rank; j += kQrWarps) {
-                const int pj = colmap[j];
-                double s = 0.0;
-                for (int i = i0 + lane; i < nloc; i += 32) s += z[i + pk * ld] * z[i + pj * ld];
-                s = warp_sum(s);
-                if (lane == 0) m[j - k] = s;
-            }
-            X.sum(rank - k);
-            for (int j = k + 1 + warp; j < rank; j += kQrWarps) {
-                const int pj = colmap[j];
-                const double t = tot[j - k];
-                if (tau != 0.0)
-                    for (int i = i0 + lane; i < nloc; i += 32) z[i + pj * ld] -= (tau * z[i + pk * ld]) * t;
-                if (owner && lane == 0) z[lk + pj * ld] = -tau * t;
-            }
+            reduce_dots(sh, cl, cs, par, z + size_t(k) * ld, ld, i0, nloc, k + 1, rank, nullptr, 0, 0);
+            if (tau != 0.0)
+                for (int i = i0 + tid; i < nloc; i += kQrThreads) {
+                    const double tv = tau * z[i + k * ld];
+#pragma unroll 4
+                    for (int j = k + 1; j < rank; ++j) z[i + j * ld] = fma(-tv, sh.tot[j - k - 1], z[i + j * ld]);
+                }
+            if (owner)
+                for (int j = k + 1 + tid; j < rank; j += kQrThreads) z[lk + j * ld] = -tau * sh.tot[j - k - 1];
             __syncthreads();
         }
         for (int i = tid; i < nloc; i += kQrThreads) {
             const int64_t gi = r0 + i;
-            double v;
-            if (gi < k) v = 0.0;
-            else if (gi == k) v = 1.0 - tau;
-            else v = -tau * z[i + pk * ld];
-            z[i + pk * ld] = v;
+            z[i + k * ld] = gi < k ? 0.0 : (gi == k ? 1.0 - tau : -tau * z[i + k * ld]);
         }
         __syncthreads();
     }
+    QR_MARK(3);
 
     // ---- sign fix: largest |entry| of each column positive (first maximum on ties)
     if (rank > 0) {
-        double* m = X.mine();
-        for (int j = warp; j < rank; j += kQrWarps) {
-            const int pj = colmap[j];
-            double bv = -1.0, val = 0.0;
+        double* m = sh.slot + par * kVec;
+        const int sub = tid % kTpc, grp = tid / kTpc;
+        for (int base = 0; base + warp * (32 / kTpc) < rank; base += kQrThreads / kTpc) {
+            const int j = base + grp;
+            double bvv = -1.0, val = 0.0;
             int bi = 0x7fffffff;
-            for (int i = lane; i < nloc; i += 32) {
-                const double a = fabs(z[i + pj * ld]);
-                if (a > bv) {
-                    bv = a;
-                    bi = i;
-                    val = z[i + pj * ld];
-                }
+            for (int i = sub; j < rank && i < nloc; i += kTpc) {
+                const double x = z[i + j * ld];
+                const bool take = fabs(x) > bvv;
+                bvv = take ? fabs(x) : bvv;
+                bi = take ? i : bi;
+                val = take ? x : val;
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, bv, o);
+            for (int o = kTpc / 2; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, bvv, o);
                 const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
                 const double ov = __shfl_xor_sync(0xffffffffu, val, o);
-                if (ob > bv || (ob == bv && oi < bi)) {
-                    bv = ob;
-                    bi = oi;
-                    val = ov;
-                }
+                const bool take = ob > bvv || (ob == bvv && oi < bi);
+                bvv = take ? ob : bvv;
+                bi = take ? oi : bi;
+                val = take ? ov : val;
             }
-            if (lane == 0) {
-                m[2 * j] = bv;
+            if (sub == 0 && j < rank) {
+                m[2 * j] = bvv;
                 m[2 * j + 1] = val;
             }
         }
-        X.sync_all();
+        if (cs > 1) cl.sync();
+        else __syncthreads();
         for (int j = tid; j < rank; j += kQrThreads) {
-            double bv = -1.0, val = 0.0;
-            for (unsigned c = 0; c < X.cs; ++c) {
-                const double* ps = X.cs > 1 ? cl.map_shared_rank(m, c) : m;
-                if (ps[2 * j] > bv) {  // CTAs hold increasing rows: strict > keeps the first
-                    bv = ps[2 * j];
+            double bvv = -1.0, val = 0.0;
+            for (unsigned c = 0; c < cs; ++c) {  // CTAs hold increasing rows: strict > keeps the first
+                const double* ps = cs > 1 ? cl.map_shared_rank(m, c) : m;
+                if (ps[2 * j] > bvv) {
+                    bvv = ps[2 * j];
                     val = ps[2 * j + 1];
                 }
             }
-            sgn[j] = val < 0.0 ? -1.0 : 1.0;
+            sh.sgn[j] = val < 0.0 ? -1.0 : 1.0;
         }
-        X.par ^= 1;
+        par ^= 1;
         __syncthreads();
     }
+    QR_MARK(4);
 
     // ---- outputs
-    for (int j = 0; j < ucap; ++j) {
-        const int pj = j < rank ? colmap[j] : 0;
+    for (int j = 0; j < ucap; ++j)
         for (int i = tid; i < nloc; i += kQrThreads)
-            uout[(r0 + i) + int64_t(j) * rows] = j < rank ? sgn[j] * z[i + pj * ld] : 0.0;
-    }
+            uout[(r0 + i) + int64_t(j) * rows] = j < rank ? sh.sgn[j] * z[i + j * ld] : 0.0;
     if (upout) {
         const int stride = (rank + 3) / 4 * 4;
         for (int64_t t = tid; t < int64_t(nloc) * stride; t += kQrThreads) {
             const int i = static_cast<int>(t / stride), j = static_cast<int>(t % stride);
-            const double v = j < rank ? sgn[j] * z[i + colmap[j] * ld] : 0.0;
+            const double v = j < rank ? sh.sgn[j] * z[i + j * ld] : 0.0;
             const int64_t o = (r0 + i) * stride + j;
             if (up_dtype == kF32) static_cast<float*>(upout)[o] = static_cast<float>(v);
             else static_cast<double*>(upout)[o] = v;
@@ -362,9 +391,10 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     if (crank == 0) {
         if (tid == 0) *rank_out = rank;
         if (diag_out)
-            for (int k = tid; k < size; k += kQrThreads) diag_out[k] = beta[k];
+            for (int k = tid; k < size; k += kQrThreads) diag_out[k] = sh.beta[k];
     }
-    if (X.cs > 1) cl.sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
+    QR_MARK(5);
+    if (cs > 1) cl.sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
 int pick_cluster(int64_t rows, int ncols, int* ld_out, size_t* smem_out) {

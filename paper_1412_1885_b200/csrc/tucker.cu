@@ -477,7 +477,7 @@ int tk_context_destroy(tk_context* ctx) {
 int tk_context_set_stream(tk_context* ctx, void* st) {
     return guarded([&] {
         check_ctx(ctx);
-        ctx->stream = st ? static_cast<cudaStream_t>(st) : ctx->own;
+        ctx->stream = static_cast<cudaStream_t>(st);  // NULL: the legacy default stream (torch's default)
     });
 }
 

@@ -233,11 +233,10 @@ class Context:
 
 
 def _ctx(context):
+    """The context, bound to torch's current CUDA stream so library kernels and torch ops
+    are ordered (a failure to bind is an error: a silent fallback would race)."""
     c = context or Context.default()
-    try:
-        c.bind_torch_stream()
-    except Exception:
-        pass
+    c.bind_torch_stream()
     return c
 
 

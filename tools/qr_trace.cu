@@ -1,0 +1,35 @@
+// Phase timing of the cluster QR kernel (clock64 marks of CTA 0 / thread 0): build with
+// nvcc -DTK_QR_TRACE; not part of the library.
+#define TK_QR_TRACE 1
+#include "../paper_1412_1885_b200/csrc/qr.cu"
+#include <cstdio>
+#include <random>
+#include <vector>
+int main() {
+    int shapes[][2] = {{300, 20}, {1000, 30}, {4000, 60}};
+    for (auto& sh : shapes) {
+        const int rows = sh[0], cols = sh[1];
+        std::vector<double> h(rows * cols);
+        std::mt19937 g(1);
+        std::normal_distribution<double> nd;
+        for (auto& x : h) x = nd(g);
+        double *z, *u;
+        int* rk;
+        cudaMalloc(&z, h.size() * 8);
+        cudaMalloc(&u, h.size() * 8);
+        cudaMalloc(&rk, 4);
+        cudaMemcpy(z, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        for (int it = 0; it < 3; ++it) tkb::launch_orthonormal_basis(z, rows, cols, u, cols, nullptr, 1, rk, nullptr, 0);
+        cudaDeviceSynchronize();
+        long long t[4096];
+        cudaMemcpyFromSymbol(t, g_qr_trace, sizeof(t));
+        printf("%dx%d: load+norms %lld\n", rows, cols, t[1] - t[0]);
+        for (int k = 1; k < 4; ++k)
+            printf("  step %d: pivot %lld swap %lld reduce %lld scal+downdate+essential %lld update %lld\n", k,
+                   t[6 + 8 * k] - t[7 + 8 * k], t[8 + 8 * k] - t[6 + 8 * k], t[10 + 8 * k] - t[8 + 8 * k],
+                   t[11 + 8 * k] - t[10 + 8 * k], t[12 + 8 * k] - t[11 + 8 * k]);
+        printf("  factor %lld Q %lld sign %lld out %lld total %lld cycles\n", t[2] - t[1], t[3] - t[2], t[4] - t[3],
+               t[5] - t[4], t[5] - t[0]);
+    }
+    return 0;
+}

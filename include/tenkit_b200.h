@@ -100,6 +100,10 @@ int tk_context_set_stream(tk_context* ctx, void* cuda_stream);
 /* Install (or clear, with NULL) the cross-rank reduction hook */
 int tk_context_set_comm(tk_context* ctx, const tk_comm* comm);
 int tk_context_synchronize(tk_context* ctx);
+/* Contraction kernels for the Y-streaming TTM passes: 0 auto (tcgen05 3xTF32 UMMA for fp32
+ * data when the shape tiles the GPU, FFMA otherwise), 1 FFMA only, 2 tcgen05 whenever the
+ * shape is supported (also for the kernel-level tk_ttm) */
+int tk_context_set_ttm_path(tk_context* ctx, int path);
 
 /* Alg. 3. y: dtype TK_F32/TK_F64, dims[order], device pointer if y_on_device else host
  * (copied in on the context stream). ranks[order], oversample >= 0, seed = SeedSpec{root, stream}. */

@@ -27,6 +27,7 @@ struct tk_context {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     bool has_comm = false;
+    int ttm_path = 0;  // 0 auto (tcgen05 for fp32 Y streams), 1 FFMA only, 2 tcgen05 whenever supported
     tk_comm comm{};
     std::map<std::string, std::pair<void*, size_t>> bufs;
     int* rank_host = nullptr;  // pinned
@@ -152,7 +153,7 @@ struct TuckerRun {
             T* out = static_cast<T*>(ctx->buf(which ? "projB" : "projA", sizeof(T) * P * cols[m] * Q));
             const bool streams_y = (t == 0 && cur == y);
             if (streams_y && time_kernels) mark();
-            ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
+            if (!stream_ttm(cur, m, out, P, K, Q, streams_y)) ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
             if (streams_y && time_kernels) mark();
             if (streams_y) ++passes;
             xd[m] = cols[m];
@@ -160,6 +161,26 @@ struct TuckerRun {
             which ^= 1;
         }
         return cur;
+    }
+
+    // The Y-streaming contraction on the tcgen05 tensor cores (3xTF32, ttm_tc.cu) when the data
+    // is fp32 and the shape tiles the GPU; returns false to fall back to the FFMA kernels.
+    bool stream_ttm(const T* in, int m, T* out, int64_t P, int64_t K, int64_t Q, bool streams_y) {
+        if constexpr (sizeof(T) != 4) {
+            return false;
+        } else {
+            const int path = ctx->ttm_path;
+            if (path == 1 || (path == 0 && !streams_y) || U.size() <= size_t(m) || !U[m]) return false;
+            const float* fin = reinterpret_cast<const float*>(in);
+            float* fout = reinterpret_cast<float*>(out);
+            if (!tc_ttm_supported(fin, fout, P, Q, cols[m])) return false;
+            void* bpk = ctx->buf("umma_pack", static_cast<size_t>(umma_pack_bytes(K, cols[m])));
+            const double* u = U[m] + (m == order - 1 ? offset : 0);
+            launch_pack_umma(u, gdims[m], K, cols[m], bpk, s);
+            launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s);
+            launches += 2;
+            return true;
+        }
     }
 
     void ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t Q, int c) {
@@ -495,6 +516,14 @@ int tk_context_set_comm(tk_context* ctx, const tk_comm* comm) {
     });
 }
 
+int tk_context_set_ttm_path(tk_context* ctx, int path) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(path >= 0 && path <= 2, "ttm path must be 0 (auto), 1 (FFMA) or 2 (tcgen05)");
+        ctx->ttm_path = path;
+    });
+}
+
 int tk_context_synchronize(tk_context* ctx) {
     return guarded([&] {
         check_ctx(ctx);
@@ -586,10 +615,18 @@ int tk_ttm(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const
             }
         TK_CUDA(cudaMemcpyAsync(md, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, ctx->stream));
         if (dtype == TK_F32) {
+            const float* ft = static_cast<const float*>(t);
+            float* fo = static_cast<float*>(out);
+            if (ctx->ttm_path == 2 && tc_ttm_supported(ft, fo, P, Q, static_cast<int>(mrows))) {
+                void* bpk = ctx->buf("umma_pack", static_cast<size_t>(umma_pack_bytes(d[mode], static_cast<int>(mrows))));
+                launch_pack_umma(md, d[mode], d[mode], static_cast<int>(mrows), bpk, ctx->stream);
+                launch_ttm_tc(ft, bpk, fo, P, d[mode], Q, static_cast<int>(mrows), ctx->stream);
+                TK_CUDA(cudaStreamSynchronize(ctx->stream));
+                return;
+            }
             float* up = static_cast<float*>(ctx->buf("ttm_up", sizeof(float) * d[mode] * stride));
             launch_pack_factor<float>(md, d[mode], d[mode], static_cast<int>(mrows), up, ctx->stream);
-            launch_ttm<float>(static_cast<const float*>(t), up, static_cast<float*>(out), P, d[mode], Q,
-                              static_cast<int>(mrows), ctx->stream);
+            launch_ttm<float>(ft, up, fo, P, d[mode], Q, static_cast<int>(mrows), ctx->stream);
         } else {
             double* up = static_cast<double*>(ctx->buf("ttm_up", sizeof(double) * d[mode] * stride));
             launch_pack_factor<double>(md, d[mode], d[mode], static_cast<int>(mrows), up, ctx->stream);
@@ -611,12 +648,14 @@ int tk_ttm_all(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, c
             TuckerRun<T> r{ctx, ctx->stream, order, d, d, 0, static_cast<const T*>(t)};
             r.cols.resize(order);
             r.Up.resize(order);
+            r.U.assign(order, nullptr);
             for (int n = 0; n < order; ++n) {
                 r.cols[n] = static_cast<int>(cols[n]);
                 if (n == skip) continue;
                 require(cols[n] >= 1 && cols[n] <= kMaxRank, "ttm_all: factor columns must be in [1, 64]");
                 r.Up[n] = static_cast<T*>(ctx->buf("tall_up" + std::to_string(n), sizeof(T) * d[n] * pack_stride(r.cols[n])));
                 launch_pack_factor<T>(ms[n], d[n], d[n], r.cols[n], r.Up[n], ctx->stream);
+                r.U[n] = const_cast<double*>(ms[n]);
             }
             std::vector<int64_t> xd;
             const T* x = r.project(static_cast<int>(skip), xd);

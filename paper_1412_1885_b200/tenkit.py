@@ -211,6 +211,11 @@ class Context:
         import torch
         _lib.check(self.lib.tk_context_set_stream(self.handle, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
+    def set_ttm_path(self, path: str):
+        """'auto' (tcgen05 3xTF32 for fp32 Y passes), 'ffma', or 'tc' (tcgen05 whenever supported)."""
+        code = {"auto": 0, "ffma": 1, "tc": 2}[path]
+        _lib.check(self.lib.tk_context_set_ttm_path(self.handle, code))
+
     def synchronize(self):
         _lib.check(self.lib.tk_context_synchronize(self.handle))
 

@@ -367,7 +367,7 @@ def run_b200(args, cfg):
             "hbm_frac_of_peak": round(value / world / hbm, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic,
-                         "kernel": "ttm_mmajor_kernel (Y-streaming TTM)", "peak_source": "measured" if not pk.get("_fallback") else "fallback",
+                         "kernel": "ttm_tc_kernel (Y-streaming TTM, tcgen05 3xTF32)" if cfg["dtype"] == "f32" else "ttm_mmajor_kernel (Y-streaming TTM, FFMA)", "peak_source": "measured" if not pk.get("_fallback") else "fallback",
                          "bytes_per_launch": ybytes, "mean_launch_ms": round(kern_ms, 4)},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

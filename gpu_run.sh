@@ -1,8 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-python tools/qr_bench.py > gpurun_out/qr_bench.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:qr_colpiv -s 9 -c 1 -o gpurun_out/prof_qr python tools/qr_bench.py > gpurun_out/ncu_qr.log 2>&1
-echo "ncu rc=$?"
-cat gpurun_out/qr_bench.log
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -m pytest tests/test_gpu_tc.py -x -q > gpurun_out/pytest_tc.log 2>&1; echo "tc pytest rc=$?" >> gpurun_out/pytest_tc.log
+tail -3 gpurun_out/pytest_tc.log
+timeout 600 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain20.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/plain20.log | cut -c1-200; grep -o '"roofline": {[^}]*}' gpurun_out/plain20.log

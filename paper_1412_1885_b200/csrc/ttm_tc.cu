@@ -4,17 +4,21 @@
 // first stage of every X_n = Y x_{p != n} U_p^T, tensor.hpp:151-192), but the FFMA loop is
 // replaced by tf32 UMMAs in an fp32-accurate 3-pass split (plain TF32 flips
 // the sign rule; 3xTF32 keeps ~2^-21 relative error per product):
-//     y u ~= y_hi u_hi + y_hi u_lo + y_lo u_hi,   x_hi = rna_tf32(x), x_lo = rna_tf32(x - x_hi)
+//     y u ~= y_hi u_hi + y_hi u_lo + y_lo u_hi,   x_hi = rna_tf32(x), x_lo = x - x_hi (exact)
 // Warp roles (one 512-row tile of Y per CTA, K streamed in 16-column stages):
-//   warp 4      producer: bulk-async copies (TMA engine) of the Y columns + the packed
-//               [U_hi | U_lo] stage into a 4-deep shared-memory ring (mbarrier complete_tx)
-//   warps 0-3   converters: LDS.128 of 4 rows per thread, split y into (hi, lo) and
+//   warp 8      producer: TMA tensor loads (256-row x 16-k boxes of the (P, K, Q) view,
+//               zero-filled out of bounds) + a bulk copy of the packed [U_hi | U_lo] stage
+//               into a 4-deep shared-memory ring (mbarrier complete_tx)
+//   warps 0-7   converters: LDS.128 of 4 rows per thread, split y into (hi, lo) and
 //               tcgen05.st them as the A operands in TMEM (row 4L+j of the tile goes to
-//               TMEM lane L of M-tile j), then the epilogue (tcgen05.ld, D_hi + D_lo)
-//   warp 5      TMEM allocator + single-thread MMA issuer:
+//               TMEM lane L of M-tile j; warps w and w+4 share lane quarter w and split the
+//               16 k of a stage), then the epilogue (warps 0-3: tcgen05.ld, D_hi + D_lo)
+//   warp 9      TMEM allocator + single-thread MMA issuer:
 //               D_j[0:2NH] += A_hi_j [U_hi | U_lo]   (N = 2NH)
 //               D_j[0:NH]  += A_lo_j  U_hi           (N = NH)
 // Accumulators stay in TMEM for the whole K loop; Y is read from HBM exactly once.
+#include <cuda.h>
+
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -23,7 +27,7 @@ namespace tkb {
 
 namespace {
 
-constexpr int kTcConv = 4;                      // converter / epilogue warps (TMEM lane quarters)
+constexpr int kTcConv = 8;                      // converter warps: 2 per TMEM lane quarter (k halves)
 constexpr int kTcThreads = (kTcConv + 2) * 32;  // + producer warp + MMA warp
 constexpr int kTcBK = 16;                       // K per pipeline stage (2 MMA k-steps of 8)
 constexpr int kTcStages = 4;
@@ -47,6 +51,10 @@ __device__ __forceinline__ uint32_t f2tf32(float x) {
     return r;
 }
 
+// round-to-nearest (ties away) to tf32 on the magnitude bits; the residual x - hi is exact
+// in fp32 and is handed to the MMA as is (the tensor core reads its top 19 bits)
+__device__ __forceinline__ uint32_t tf32_hi_bits(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -57,6 +65,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
         "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
         "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
@@ -90,6 +104,14 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a, uint64_t b, 
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                  : "memory");
@@ -97,12 +119,12 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 template <int NH>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    ttm_tc_kernel(const float* __restrict__ in, const uint8_t* __restrict__ bpk, float* __restrict__ out, int64_t P,
-                  int64_t K, int cols, int64_t tiles_p) {
+    ttm_tc_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
+                  int64_t P, int64_t K, int cols, int64_t tiles_p) {
     using C = TcCfg<NH>;
     constexpr int MT = C::MT, BM = C::BM;
     extern __shared__ __align__(1024) uint8_t tsm[];
-    uint8_t* sY = tsm;                                            // [stages][kTcBK][BM] fp32
+    uint8_t* sY = tsm;  // [stages][BM/256 boxes][kTcBK][256] fp32
     uint8_t* sB = tsm + size_t(kTcStages) * C::STAGE_Y;           // [stages][2][2NH x 8] tf32 core matrices
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kTcStages) * C::STAGE_B);
     uint64_t* full = bars;                   // [stages]  producer -> (converters, MMA)
@@ -142,16 +164,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (warp == kTcConv) {
         // ===== producer =====
         if (lane == 0) {
-            const float* base = in + q * P * K + p0;
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
             for (int kc = 0; kc < nk; ++kc) {
                 const int s = kc % kTcStages;
                 mbar_wait(&empty[s], ((kc / kTcStages) & 1) ^ 1);
-                const int64_t k0 = int64_t(kc) * kTcBK;
-                const int kn = static_cast<int>(lmin(kTcBK, K - k0));
-                const uint32_t yb = uint32_t(rows) * 4;
-                mbar_arrive_expect_tx(&full[s], yb * kn + C::STAGE_B);
+                mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
                 uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
-                for (int kk = 0; kk < kn; ++kk) bulk_g2s(dy + kk * BM * 4, base + (k0 + kk) * P, yb, &full[s]);
+#pragma unroll
+                for (int b = 0; b < BM / 256; ++b)
+                    tma_load_3d(dy + b * (kTcBK * 256 * 4), &ymap, static_cast<int>(p0 + 256 * b), kc * kTcBK,
+                                static_cast<int>(q), &full[s]);
                 bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
             }
         }
@@ -182,48 +204,52 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mma_commit(dfull);
         }
     } else {
-        // ===== converters (warps 0-3): Y tile -> (hi, lo) tf32 A operands in TMEM =====
-        const int L = warp * 32 + lane;                    // TMEM lane of this thread
-        const uint32_t lane_off = uint32_t(warp * 32) << 16;
+        // ===== converters (warps 0-7): Y tile -> (hi, lo) tf32 A operands in TMEM =====
+        const int quarter = warp & 3, khalf = warp >> 2;
+        const int L = quarter * 32 + lane;                    // TMEM lane of this thread
+        const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         for (int kc = 0; kc < nk; ++kc) {
             const int s = kc % kTcStages, a = kc & 1;
             mbar_wait(&full[s], (kc / kTcStages) & 1);
-            const int kn = static_cast<int>(lmin(kTcBK, K - int64_t(kc) * kTcBK));
-            uint32_t hi[MT][16], lo[MT][16];
-            const float* ys = reinterpret_cast<const float*>(sY + size_t(s) * C::STAGE_Y) + MT * L;
-#pragma unroll
-            for (int kk = 0; kk < kTcBK; ++kk) {
+            uint32_t hi[MT][8], lo[MT][8];
+            // rows MT*L .. MT*L+MT-1 of the tile sit in box (MT*L)/256 at row (MT*L)%256
+            const float* ys = reinterpret_cast<const float*>(sY + size_t(s) * C::STAGE_Y) +
+                              ((MT * L) / 256) * (kTcBK * 256) + (MT * L) % 256 + khalf * 8 * 256;
+            auto split = [&](int kk, bool live) {
                 float y[MT];
                 if constexpr (MT == 4) {
-                    const float4 v = *reinterpret_cast<const float4*>(ys + kk * BM);
+                    const float4 v = *reinterpret_cast<const float4*>(ys + kk * 256);
                     y[0] = v.x, y[1] = v.y, y[2] = v.z, y[3] = v.w;
                 } else {
-                    const float2 v = *reinterpret_cast<const float2*>(ys + kk * BM);
+                    const float2 v = *reinterpret_cast<const float2*>(ys + kk * 256);
                     y[0] = v.x, y[1] = v.y;
                 }
 #pragma unroll
                 for (int j = 0; j < MT; ++j) {
-                    const float x = kk < kn ? y[j] : 0.f;
-                    const uint32_t h = f2tf32(x);
+                    const float x = live ? y[j] : 0.f;
+                    const uint32_t h = tf32_hi_bits(x);
                     hi[j][kk] = h;
-                    lo[j][kk] = f2tf32(x - __uint_as_float(h));
+                    lo[j][kk] = __float_as_uint(x - __uint_as_float(h));
                 }
-            }
+            };
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) split(kk, true);  // the K tail is zero-filled by the TMA
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // Y stage consumed (B: the MMA commit)
             mbar_wait(&aempty[a], ((kc >> 1) & 1) ^ 1);
             fence_after();
 #pragma unroll
             for (int j = 0; j < MT; ++j) {
-                const uint32_t ta = tmem + lane_off + uint32_t(C::D_COLS + a * C::A_COLS + j * 32);
-                tmem_st16(ta, hi[j]);
-                tmem_st16(ta + 16, lo[j]);
+                const uint32_t ta = tmem + lane_off + uint32_t(C::D_COLS + a * C::A_COLS + j * 32 + khalf * 8);
+                tmem_st8(ta, hi[j]);
+                tmem_st8(ta + 16, lo[j]);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&afull[a]);
         }
+        if (khalf == 1) goto done;  // the epilogue runs on warps 0-3 (one per lane quarter)
         // ===== epilogue: D = D[:, 0:NH] + D[:, NH:2NH], rows MT*L + j =====
         mbar_wait(dfull, 0);
         fence_after();
@@ -258,6 +284,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
         }
     }
+done:
     fence_before();
     __syncthreads();
     if (warp == kTcConv + 1) {
@@ -299,7 +326,18 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
     const int64_t tiles_p = (P + C::BM - 1) / C::BM;
     const int64_t grid = tiles_p * Q;
     require(grid < (int64_t(1) << 31), "ttm: grid too large");
-    ttm_tc_kernel<NH><<<static_cast<unsigned>(grid), kTcThreads, C::smem, s>>>(in, bpk, out, P, K, cols, tiles_p);
+    require(K < (int64_t(1) << 31) && Q < (int64_t(1) << 31) && P < (int64_t(1) << 31), "ttm: extent too large for TMA");
+    CUtensorMap map;
+    const cuuint64_t dims[3] = {cuuint64_t(P), cuuint64_t(K), cuuint64_t(Q)};
+    const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
+    const cuuint32_t box[3] = {256, kTcBK, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims,
+                                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    ttm_tc_kernel<NH><<<static_cast<unsigned>(grid), kTcThreads, C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p);
     TK_LAUNCH_CHECK();
 }
 

@@ -152,9 +152,11 @@ struct TuckerRun {
             const int64_t Q = prod(std::vector<int64_t>(xd.begin() + m + 1, xd.end()));
             T* out = static_cast<T*>(ctx->buf(which ? "projB" : "projA", sizeof(T) * P * cols[m] * Q));
             const bool streams_y = (t == 0 && cur == y);
-            if (streams_y && time_kernels) mark();
-            if (!stream_ttm(cur, m, out, P, K, Q, streams_y)) ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
-            if (streams_y && time_kernels) mark();
+            if (!stream_ttm(cur, m, out, P, K, Q, streams_y)) {
+                if (streams_y && time_kernels) mark();
+                ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
+                if (streams_y && time_kernels) mark();
+            }
             if (streams_y) ++passes;
             xd[m] = cols[m];
             cur = out;
@@ -177,7 +179,9 @@ struct TuckerRun {
             void* bpk = ctx->buf("umma_pack", static_cast<size_t>(umma_pack_bytes(K, cols[m])));
             const double* u = U[m] + (m == order - 1 ? offset : 0);
             launch_pack_umma(u, gdims[m], K, cols[m], bpk, s);
+            if (streams_y && time_kernels) mark();
             launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s);
+            if (streams_y && time_kernels) mark();
             launches += 2;
             return true;
         }

@@ -75,6 +75,8 @@ typedef struct tk_tucker_opts {
                                synchronously if any rank dropped */
     int time_kernels;       /* 1: bracket every Y-streaming launch with CUDA events on the
                                call's stream and report their summed device time in stats */
+    int overlap;            /* 1: launch the next Y pass on a second stream so it overlaps the
+                               current QR (it contracts a mode whose factor is already final) */
 } tk_tucker_opts;
 
 /* Per-call timing/trace (filled when non-null) */

@@ -35,7 +35,8 @@ class tk_tucker_out(C.Structure):
 
 
 class tk_tucker_opts(C.Structure):
-    _fields_ = [("explicit_core_pass", C.c_int), ("sync_ranks", C.c_int), ("time_kernels", C.c_int)]
+    _fields_ = [("explicit_core_pass", C.c_int), ("sync_ranks", C.c_int), ("time_kernels", C.c_int),
+                ("overlap", C.c_int)]
 
 
 class tk_tucker_stats(C.Structure):

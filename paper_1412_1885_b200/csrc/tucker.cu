@@ -31,6 +31,20 @@ struct tk_context {
     tk_comm comm{};
     std::map<std::string, std::pair<void*, size_t>> bufs;
     int* rank_host = nullptr;  // pinned
+    cudaStream_t side = nullptr;  // second stream: next Y pass overlapped with the current QR
+    cudaEvent_t ev_free = nullptr, ev_fs = nullptr;
+
+    void ensure_side() {
+        if (!side) {
+            // lowest priority: when the QR cluster (main stream) and the next Y pass become
+            // runnable together, the QR is dispatched first and the pass takes the other SMs
+            int lo = 0, hi = 0;
+            TK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            TK_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+            TK_CUDA(cudaEventCreateWithFlags(&ev_free, cudaEventDisableTiming));
+            TK_CUDA(cudaEventCreateWithFlags(&ev_fs, cudaEventDisableTiming));
+        }
+    }
 
     void* buf(const std::string& name, size_t bytes) {
         auto& e = bufs[name];
@@ -46,6 +60,9 @@ struct tk_context {
         for (auto& kv : bufs)
             if (kv.second.first) cudaFree(kv.second.first);
         if (rank_host) cudaFreeHost(rank_host);
+        if (ev_free) cudaEventDestroy(ev_free);
+        if (ev_fs) cudaEventDestroy(ev_fs);
+        if (side) cudaStreamDestroy(side);
         if (own) cudaStreamDestroy(own);
     }
 };
@@ -134,35 +151,67 @@ struct TuckerRun {
         return p;
     }
 
-    // Y x_{p != skip} U_p^T (skip = -1: all modes). Returns the result buffer and its dims.
-    const T* project(int skip, std::vector<int64_t>& xd) {
-        xd = ldims;
-        if (order == 1 && skip == 0) return y;
-        std::vector<int> modes;
-        const int first = (skip != order - 1) ? static_cast<int>(order - 1) : static_cast<int>(order - 2);
-        if (first >= 0 && first != skip) modes.push_back(first);
+    const char* work_name = "splitk";  // split-K scratch of the stream currently launching
+    cudaEvent_t qr_event = nullptr;     // recorded just before the next QR launch (overlap gate)
+
+    // Mode contracted first (the one pass that streams Y): the last mode (a plain M-major GEMM)
+    // unless it is kept, and never `avoid` (the factor the still-running QR is producing) when
+    // another mode with a wide enough row block exists, so that pass can overlap the QR.
+    int first_mode(int skip, int avoid) const {
+        auto ok = [&](int m) { return m >= 0 && m < order && m != skip; };
+        for (int m = static_cast<int>(order) - 1; m >= 0; --m) {
+            if (!ok(m) || m == avoid) continue;
+            if (prod(std::vector<int64_t>(ldims.begin(), ldims.begin() + m)) >= 256) return m;
+        }
         for (int m = static_cast<int>(order) - 1; m >= 0; --m)
-            if (m != skip && m != first) modes.push_back(m);
-        const T* cur = y;
+            if (ok(m)) return m;
+        return -1;
+    }
+
+    // First stage: Y x_f U_f^T into "proj1" (dims updated). Runs on the current stream `s`.
+    const T* first_stage(int f, std::vector<int64_t>& xd) {
+        xd = ldims;
+        if (f < 0) return y;
+        const int64_t P = prod(std::vector<int64_t>(xd.begin(), xd.begin() + f));
+        const int64_t K = xd[f];
+        const int64_t Q = prod(std::vector<int64_t>(xd.begin() + f + 1, xd.end()));
+        T* out = static_cast<T*>(ctx->buf("proj1", sizeof(T) * P * cols[f] * Q));
+        if (!stream_ttm(y, f, out, P, K, Q, true)) {
+            if (time_kernels) mark();
+            ttm(y, factor_rows(f), out, P, K, Q, cols[f]);
+            if (time_kernels) mark();
+        }
+        ++passes;
+        xd[f] = cols[f];
+        return out;
+    }
+
+    // Remaining (small) contractions of every mode except skip and f, descending.
+    const T* finish(const T* cur, std::vector<int64_t>& xd, int skip, int f) {
         int which = 0;
-        for (size_t t = 0; t < modes.size(); ++t) {
-            const int m = modes[t];
+        for (int m = static_cast<int>(order) - 1; m >= 0; --m) {
+            if (m == skip || m == f) continue;
             const int64_t P = prod(std::vector<int64_t>(xd.begin(), xd.begin() + m));
             const int64_t K = xd[m];
             const int64_t Q = prod(std::vector<int64_t>(xd.begin() + m + 1, xd.end()));
             T* out = static_cast<T*>(ctx->buf(which ? "projB" : "projA", sizeof(T) * P * cols[m] * Q));
-            const bool streams_y = (t == 0 && cur == y);
-            if (!stream_ttm(cur, m, out, P, K, Q, streams_y)) {
-                if (streams_y && time_kernels) mark();
-                ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
-                if (streams_y && time_kernels) mark();
-            }
-            if (streams_y) ++passes;
+            ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
             xd[m] = cols[m];
             cur = out;
             which ^= 1;
         }
         return cur;
+    }
+
+    // Y x_{p != skip} U_p^T (skip = -1: all modes), on the current stream.
+    const T* project(int skip, std::vector<int64_t>& xd) {
+        if (order == 1 && skip == 0) {
+            xd = ldims;
+            return y;
+        }
+        const int f = first_mode(skip, -1);
+        const T* t1 = first_stage(f, xd);
+        return finish(t1, xd, skip, f);
     }
 
     // The Y-streaming contraction on the tcgen05 tensor cores (3xTF32, ttm_tc.cu) when the data
@@ -189,7 +238,7 @@ struct TuckerRun {
 
     void ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t Q, int c) {
         const int64_t welems = std::min<int64_t>(P * c * Q * 2 * 148, int64_t(32) << 20);
-        T* work = static_cast<T*>(ctx->buf("splitk", sizeof(T) * welems));
+        T* work = static_cast<T*>(ctx->buf(work_name, sizeof(T) * welems));
         launch_ttm<T>(in, up, out, P, K, Q, c, s, &launches, work, welems);
     }
 
@@ -239,16 +288,19 @@ struct TuckerRun {
             sketch(x, xd, n, omp, rn, z, In);
         }
         allreduce(z, In * rn);
+        if (qr_event) TK_CUDA(cudaEventRecord(qr_event, s));
         launch_orthonormal_basis(z, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64, rank_dev + step,
                                  nullptr, s);
         ++launches;
-        if (sync) {
-            TK_CUDA(cudaMemcpyAsync(ctx->rank_host, rank_dev + step, sizeof(int), cudaMemcpyDeviceToHost, s));
-            TK_CUDA(cudaStreamSynchronize(s));
-            const int r = *ctx->rank_host;
-            require(r >= 1, "tensor dimensions must be positive");  // a rank-0 factor (zero data)
-            cols[n] = r;
-        }
+        if (sync) sync_rank(n, step);
+    }
+
+    void sync_rank(int n, int step) {
+        TK_CUDA(cudaMemcpyAsync(ctx->rank_host, rank_dev + step, sizeof(int), cudaMemcpyDeviceToHost, s));
+        TK_CUDA(cudaStreamSynchronize(s));
+        const int r = *ctx->rank_host;
+        require(r >= 1, "tensor dimensions must be positive");  // a rank-0 factor (zero data)
+        cols[n] = r;
     }
 
     void run(const std::vector<int64_t>& ranks, int64_t p, const Seed& seed, const tk_tucker_opts& opt,
@@ -272,13 +324,57 @@ struct TuckerRun {
         const bool sync = opt.sync_ranks != 0;
         const T* xlast = nullptr;
         std::vector<int64_t> xd;
-        int step = 0;
-        for (int pass = 0; pass < 2; ++pass)
-            for (int n = 0; n < order; ++n, ++step) {
-                const T* x = project(n, xd);
-                range_step(x, xd, n, alg3_omega_seed(seed, pass, n), step, sync);
-                xlast = x;
+        // Steps (pass, n). The Y pass of step k+1 contracts a mode whose factor is already final
+        // and is launched on the side stream right after step k's QR, so the latency-bound QR
+        // runs under the bandwidth-bound pass (2 of the 148 SMs for the QR cluster).
+        const int nsteps = 2 * static_cast<int>(order);
+        const bool overlap = opt.overlap && order > 1;
+        if (overlap) ctx->ensure_side();
+        std::vector<int64_t> d1;
+        const T* t1 = nullptr;
+        int f = -1;
+        bool on_side = false;
+        auto launch_first = [&](int n, int avoid, bool side) {
+            f = order == 1 ? -1 : first_mode(n, avoid);
+            on_side = side && f >= 0 && f != avoid;
+            if (on_side) {
+                TK_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_free, 0));  // finish() done with proj1
+                cudaStream_t keep = s;
+                s = ctx->side;
+                work_name = "splitk_side";
+                t1 = first_stage(f, d1);
+                TK_CUDA(cudaEventRecord(ctx->ev_fs, s));
+                s = keep;
+                work_name = "splitk";
+            } else {
+                t1 = first_stage(f, d1);
             }
+        };
+        launch_first(0, -1, false);
+        for (int step = 0; step < nsteps; ++step) {
+            const int pass = step / static_cast<int>(order), n = step % static_cast<int>(order);
+            if (on_side) TK_CUDA(cudaStreamWaitEvent(s, ctx->ev_fs, 0));
+            xd = d1;
+            const T* x = (order == 1) ? y : finish(t1, xd, n, f);
+            const bool can_overlap = overlap && x != t1;  // the sketch must not read proj1
+            qr_event = can_overlap ? ctx->ev_free : nullptr;  // recorded right before this step's QR
+            range_step(x, xd, n, alg3_omega_seed(seed, pass, n), step, false);
+            qr_event = nullptr;
+            xlast = x;
+            if (step + 1 < nsteps) {
+                const int nn = (step + 1) % static_cast<int>(order);
+                const int fn = order == 1 ? -1 : first_mode(nn, n);
+                if (can_overlap && fn != n) {
+                    launch_first(nn, n, true);  // uses factors other than U_n: independent of this QR
+                    if (sync) sync_rank(n, step);
+                } else {
+                    if (sync) sync_rank(n, step);
+                    launch_first(nn, n, false);
+                }
+            } else if (sync) {
+                sync_rank(n, step);
+            }
+        }
         if (!sync) {  // verify the full-rank speculation
             int hr[2 * TK_MAX_ORDER];
             TK_CUDA(cudaMemcpyAsync(hr, rank_dev, sizeof(int) * 2 * order, cudaMemcpyDeviceToHost, s));
@@ -542,7 +638,7 @@ int tk_rand_tucker_2i(tk_context* ctx, int dtype, int64_t order, const int64_t* 
         check_ctx(ctx);
         validate_common(dtype, order, dims, ranks, oversample, "rand_tucker_2i");
         require(out != nullptr && y != nullptr, "rand_tucker_2i: null argument");
-        tk_tucker_opts o{0, 1, 0};
+        tk_tucker_opts o{0, 1, 0, 1};
         if (opts) o = *opts;
         const Seed seed{seed_root, seed_stream};
         if (dtype == TK_F32) rand_tucker_2i_impl<float>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, o, out, stats);

@@ -288,7 +288,7 @@ def _tucker_call(fn_name, y, ranks, oversample, seed, context, out, opts=None):
             _i64arr(ranks), int(oversample), int(seed.root), int(seed.stream)]
     if fn_name == "tk_rand_tucker_2i":
         oo = _lib.tk_tucker_opts(int(getattr(opts, "explicit_core_pass", 0)), int(getattr(opts, "sync_ranks", 1)),
-                                 int(getattr(opts, "time_kernels", 0)))
+                                 int(getattr(opts, "time_kernels", 0)), int(getattr(opts, "overlap", 1)))
         rc = getattr(ctx.lib, fn_name)(*args, C.byref(oo), C.byref(o), C.byref(st))
     else:
         rc = getattr(ctx.lib, fn_name)(*args, C.byref(o), C.byref(st))
@@ -312,15 +312,17 @@ class TuckerOptions:
     sync_ranks: int = 1
     _global_last_dim: int = 0
     time_kernels: int = 0
+    overlap: int = 1
 
 
 def rand_tucker_2i(y, ranks, oversample: int, seed, *, explicit_core_pass: bool = False, sync_ranks: bool = True,
                    context: Context | None = None, out: str | None = None, global_last_dim: int = 0,
-                   time_kernels: bool = False) -> TuckerModel:
+                   time_kernels: bool = False, overlap: bool = True) -> TuckerModel:
     """Alg. 3 (tucker.hpp:136-169) on the B200. `y`: numpy array (host; copied in) or a
     device DenseTensor. Returns a host (numpy) model for host input, device otherwise,
     unless out='host'/'device'."""
-    opts = TuckerOptions(int(explicit_core_pass), int(sync_ranks), int(global_last_dim), int(time_kernels))
+    opts = TuckerOptions(int(explicit_core_pass), int(sync_ranks), int(global_last_dim), int(time_kernels),
+                         int(overlap))
     return _tucker_call("tk_rand_tucker_2i", y, ranks, oversample, seed, context, out, opts)
 
 

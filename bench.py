@@ -325,15 +325,16 @@ def run_b200(args, cfg):
             barrier(world)
             t0 = time.perf_counter()
             mm = P.rand_tucker_2i(yh, cfg["ranks"], cfg["p"], alg_seed, context=ctx, sync_ranks=False,
-                                  global_last_dim=kw["global_last_dim"])
+                                  global_last_dim=kw["global_last_dim"], out="device")
             res = P.ffcp(mm, cfg["ffcp_rank"], P.ConstraintSpec(cfg["constraint"]), P.StopRule(*STOP), alg_seed,
-                         context=ctx)
+                         context=ctx)  # on the device model; CP factors come back to the host
+            mh = mm.to_host()  # Tucker core + factors to the host
             torch.cuda.synchronize()
             t1 = time.perf_counter()
             if it > 0:
                 e2e_times.append(all_max(t1 - t0, world))
             h2d = ybytes
-            d2h = (mm.core.size + sum(u.size for u in mm.factors)) * 8
+            d2h = (mh.core.size + sum(u.size for u in mh.factors) + sum(a.size for a in res.factors)) * 8
         e2e_s = statistics.mean(e2e_times)
         e2e = {"value": round(world * passes * ybytes / e2e_s / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

@@ -1,5 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 600 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain20.log 2>&1; echo "bench rc=$?"
-tail -1 gpurun_out/plain20.log | cut -c1-200; grep -o '"roofline": {[^}]*}' gpurun_out/plain20.log; grep -o '"fit_model": [0-9.]*' gpurun_out/plain20.log
-timeout 300 python -m pytest tests/test_gpu_parity.py tests/test_gpu_tc.py -x -q 2>&1 | tail -2
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log; grep -E "FAILED|Error" gpurun_out/pytest_gpu.log | head -5
+timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_full.log 2> gpurun_out/bench_full.err; echo "bench rc=$?"
+cat gpurun_out/bench_full.log; tail -3 gpurun_out/bench_full.err

@@ -13,7 +13,7 @@
  *                            + detail::fix_column_signs  tucker.hpp:39-45
  *   tk_gaussian_matrix    <- tenkit::gaussian_matrix     random.hpp:85-100
  *   tk_seed_derived       <- tenkit::SeedSpec::derived   random.hpp:36-41
- *   tk_ffcp               <- tenkit::ffcp                ffcp.hpp:94-194
+ *   tk_ffcp(_device)      <- tenkit::ffcp                ffcp.hpp:94-194
  *
  * Layouts are the reference's: column-major, mode 0 fastest (tensor.hpp:31). Errors: every
  * call returns TK_OK or a code; the reference's std::invalid_argument("tenkit: ...")
@@ -137,11 +137,18 @@ int tk_gaussian_matrix(tk_context* ctx, int64_t rows, int64_t cols, uint64_t see
                        double* out);
 uint64_t tk_seed_derived(uint64_t seed_root, uint64_t seed_stream, uint64_t tag);
 
-/* FFCP on a Tucker model (host pointers, fp64). factors[n] is rows[n] x core_shape[n].
- * out_factors[n]: rows[n] x rank; fit_trace: capacity max_iters. */
+/* FFCP on a Tucker model (host pointers, fp64; computed on the device). factors[n] is
+ * rows[n] x core_shape[n]. out_factors[n]: rows[n] x rank; fit_trace: capacity max_iters. */
 int tk_ffcp(tk_context* ctx, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
             const int64_t* rows, int64_t rank, int constraint, double sparsity_c, int max_iters, double fit_tol,
             uint64_t seed_root, uint64_t seed_stream, double** out_factors, double* fit_trace, int* iterations);
+
+/* Same with device pointers for core / factors / out_factors (fit_trace stays host memory):
+ * the decomposition's device outputs feed it without a host round trip. */
+int tk_ffcp_device(tk_context* ctx, int64_t order, const int64_t* core_shape, const double* core,
+                   const double** factors, const int64_t* rows, int64_t rank, int constraint, double sparsity_c,
+                   int max_iters, double fit_tol, uint64_t seed_root, uint64_t seed_stream, double** out_factors,
+                   double* fit_trace, int* iterations);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,8 @@ SIGNATURES = {
     "tk_seed_derived": (U64, [U64, U64, U64]),
     "tk_ffcp": (C.c_int, [C.c_void_p, I64, PI64, PD, C.POINTER(PD), PI64, I64, C.c_int, C.c_double, C.c_int,
                           C.c_double, U64, U64, C.POINTER(PD), PD, C.POINTER(C.c_int)]),
+    "tk_ffcp_device": (C.c_int, [C.c_void_p, I64, PI64, PD, C.POINTER(PD), PI64, I64, C.c_int, C.c_double, C.c_int,
+                                 C.c_double, U64, U64, C.POINTER(PD), PD, C.POINTER(C.c_int)]),
 }
 
 _lib = None

@@ -73,4 +73,9 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
 // Largest Z (rows) the cluster QR can hold for `ncols` columns.
 int64_t qr_max_rows(int ncols);
 
+// FFCP on the device (ffcp.cu); all pointers are device pointers, fit_trace is host memory.
+void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
+                 const int64_t* rows, int64_t rank, int kind, double c, int max_iters, double fit_tol, Seed seed,
+                 double** out_factors, double* fit_trace, int* iterations);
+
 }  // namespace tkb

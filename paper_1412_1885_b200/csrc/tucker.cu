@@ -557,7 +557,6 @@ void validate_common(int dtype, int64_t order, const int64_t* dims, const int64_
 // ===========================================================================
 extern "C" {
 
-int tk_ffcp_fail(int code, const char* msg) { return fail(code, msg); }
 const char* tk_last_error(void) { return g_err.c_str(); }
 int tk_version(void) { return 1; }
 
@@ -656,6 +655,46 @@ int tk_rand_tucker(tk_context* ctx, int dtype, int64_t order, const int64_t* dim
         const Seed seed{seed_root, seed_stream};
         if (dtype == TK_F32) rand_tucker_impl<float>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, out, stats);
         else rand_tucker_impl<double>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, out, stats);
+    });
+}
+
+int tk_ffcp_device(tk_context* ctx, int64_t order, const int64_t* core_shape, const double* core,
+                   const double** factors, const int64_t* rows, int64_t rank, int constraint, double sparsity_c,
+                   int max_iters, double fit_tol, uint64_t seed_root, uint64_t seed_stream, double** out_factors,
+                   double* fit_trace, int* iterations) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(order >= 2 && order <= TK_MAX_ORDER, "ffcp: tensor order must be at least 2");
+        ffcp_device(ctx->stream, order, core_shape, core, factors, rows, rank, constraint, sparsity_c, max_iters,
+                    fit_tol, Seed{seed_root, seed_stream}, out_factors, fit_trace, iterations);
+    });
+}
+
+int tk_ffcp(tk_context* ctx, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
+            const int64_t* rows, int64_t rank, int constraint, double sparsity_c, int max_iters, double fit_tol,
+            uint64_t seed_root, uint64_t seed_stream, double** out_factors, double* fit_trace, int* iterations) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(order >= 2 && order <= TK_MAX_ORDER, "ffcp: tensor order must be at least 2");
+        require(rank >= 1, "ffcp: rank must be positive");
+        cudaStream_t s = ctx->stream;
+        int64_t gsz = 1;
+        for (int64_t n = 0; n < order; ++n) gsz *= core_shape[n];
+        double* dcore = static_cast<double*>(ctx->buf("ffcp_core", sizeof(double) * gsz));
+        TK_CUDA(cudaMemcpyAsync(dcore, core, sizeof(double) * gsz, cudaMemcpyHostToDevice, s));
+        std::vector<const double*> df(order);
+        std::vector<double*> dout(order);
+        for (int64_t n = 0; n < order; ++n) {
+            double* u = static_cast<double*>(ctx->buf("ffcp_u" + std::to_string(n), sizeof(double) * rows[n] * core_shape[n]));
+            TK_CUDA(cudaMemcpyAsync(u, factors[n], sizeof(double) * rows[n] * core_shape[n], cudaMemcpyHostToDevice, s));
+            df[n] = u;
+            dout[n] = static_cast<double*>(ctx->buf("ffcp_a" + std::to_string(n), sizeof(double) * rows[n] * rank));
+        }
+        ffcp_device(s, order, core_shape, dcore, df.data(), rows, rank, constraint, sparsity_c, max_iters, fit_tol,
+                    Seed{seed_root, seed_stream}, dout.data(), fit_trace, iterations);
+        for (int64_t n = 0; n < order; ++n)
+            TK_CUDA(cudaMemcpyAsync(out_factors[n], dout[n], sizeof(double) * rows[n] * rank, cudaMemcpyDeviceToHost, s));
+        TK_CUDA(cudaStreamSynchronize(s));
     });
 }
 

@@ -440,12 +440,30 @@ class FfcpResult:  # ffcp.hpp:81-86
 
 
 def ffcp(model: TuckerModel, rank: int, constraint: ConstraintSpec = ConstraintSpec(), stop: StopRule = StopRule(),
-         seed=SeedSpec(), *, context: Context | None = None) -> FfcpResult:
-    """CP decomposition of a Tucker-compressed tensor (ffcp.hpp:94-194)."""
-    model = model.to_host()
+         seed=SeedSpec(), *, context: Context | None = None, out: str = "host") -> FfcpResult:
+    """CP decomposition of a Tucker-compressed tensor (ffcp.hpp:94-194), computed on the device.
+    A device model (from rand_tucker_2i on device data) is used in place; a host model is
+    copied in. Factors come back as numpy arrays (out='host') or CUDA tensors (out='device')."""
     seed = seed if isinstance(seed, SeedSpec) else SeedSpec(*seed)
-    ctx = context or Context.default()
+    ctx = _ctx(context)
     order = len(model.factors)
+    trace = np.empty(max(stop.max_iters, 1))
+    its = C.c_int()
+    if hasattr(model.core, "is_cuda") and model.core.is_cuda:
+        import torch
+        cshape = list(model.core_shape)
+        rows = [int(u.numel()) // int(c) for u, c in zip(model.factors, cshape)]
+        outs = [torch.empty(int(r) * int(rank), dtype=torch.float64, device="cuda") for r in rows]
+        farr = (_lib.PD * order)(*[_dptr(u) for u in model.factors])
+        oarr = (_lib.PD * order)(*[_dptr(x) for x in outs])
+        _lib.check(ctx.lib.tk_ffcp_device(ctx.handle, order, _i64arr(cshape), _dptr(model.core), farr, _i64arr(rows),
+                                          int(rank), int(constraint.kind), float(constraint.sparsity_c),
+                                          int(stop.max_iters), float(stop.fit_tol), seed.root, seed.stream, oarr,
+                                          _dptr(trace), C.byref(its)))
+        fs = outs if out == "device" else [o.cpu().numpy().reshape((int(r), int(rank)), order="F")
+                                             for o, r in zip(outs, rows)]
+        return FfcpResult(fs, trace[: its.value].copy(), its.value)
+    model = model.to_host()
     core = np.ascontiguousarray(np.asarray(model.core, dtype=np.float64).ravel(order="F"))
     cshape = np.shape(model.core) if np.ndim(model.core) == order else model.core_shape
     for n, u in enumerate(model.factors):
@@ -454,8 +472,6 @@ def ffcp(model: TuckerModel, rank: int, constraint: ConstraintSpec = ConstraintS
     fs = [np.ascontiguousarray(np.asarray(u, dtype=np.float64).ravel(order="F")) for u in model.factors]
     rows = [np.shape(u)[0] for u in model.factors]
     outs = [np.empty(int(r) * max(int(rank), 1)) for r in rows]
-    trace = np.empty(max(stop.max_iters, 1))
-    its = C.c_int()
     farr = (_lib.PD * order)(*[_dptr(x) for x in fs])
     oarr = (_lib.PD * order)(*[_dptr(x) for x in outs])
     _lib.check(ctx.lib.tk_ffcp(ctx.handle, order, _i64arr(cshape), _dptr(core), farr, _i64arr(rows), int(rank),

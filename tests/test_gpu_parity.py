@@ -217,6 +217,21 @@ def test_ffcp_variants_match_oracle(P, O):
             assert np.allclose(a, b, rtol=1e-7, atol=1e-9)
 
 
+def test_ffcp_device_model_matches_oracle(P, O):
+    """FFCP straight on the device outputs of rand_tucker_2i (no host round trip), 4-way
+    nonnegative HALS (BASELINE config 4's constraint) and unconstrained."""
+    fs = [np.abs(O.gaussian_matrix(d, 3, (90, n))) for n, d in enumerate((14, 12, 10, 9))]
+    y = O.add_noise(O.cp_reconstruct(fs), 30.0, (91, 0), abs_noise=True)
+    m = P.rand_tucker_2i(P.DenseTensor.from_numpy(y).cuda(), (3, 3, 3, 3), 2, (92, 0))
+    h = m.to_host()
+    for kind in (O.NONNEG_HALS, O.NONE):
+        res = P.ffcp(m, 3, P.ConstraintSpec(kind), P.StopRule(200, 1e-6), (93, 0))
+        a_ref, tr_ref, it_ref = O.ffcp(h.core, h.factors, 3, kind, 0.0, 200, 1e-6, (93, 0))
+        assert res.iterations == it_ref
+        assert np.allclose(res.fit_trace, tr_ref, rtol=1e-8, atol=1e-8)
+        assert abs(O.fit(y, O.cp_reconstruct(res.factors)) - O.fit(y, O.cp_reconstruct(a_ref))) < 1e-6
+
+
 def test_errors_mirror_reference(P):
     with pytest.raises(P.TenkitError, match="one rank per mode required"):
         P.rand_tucker_2i(np.ones((3, 3, 3)), (2, 2), 1, (0, 0))

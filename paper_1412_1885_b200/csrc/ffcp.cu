@@ -33,33 +33,39 @@ inline unsigned nblocks(int64_t n, int per = 256) {
     return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, 148 * 32)));
 }
 
-// H[i + r*cs[n]] = sum over the other core indices of G * prod_{p != n} V_p[i_p, r]
-// (ffcp_h: h_r = G x_{p != n} v_r^(p)T), one thread per (i, r); digits advance with carries.
-__global__ void ffcp_h_kernel(const double* __restrict__ g, CoreDesc cd, int n, int R, double* __restrict__ h) {
-    const int In = cd.cs[n];
-    const int64_t total = int64_t(In) * R;
-    int64_t W = 1;
-    for (int p = 0; p < cd.order; ++p)
-        if (p != n) W *= cd.cs[p];
+// Diagonal contraction of one mode q of W against V_q[:, r], where r is W's mode `rpos`:
+// out[..., r, ...] = sum_i W[..., i (mode q), ..., r, ...] V_q[i, r]  (mode q removed).
+// dims/ndim describe W (column-major); one thread per output element.
+struct WDesc {
+    int ndim;
+    int64_t dims[kMaxOrder];
+};
+__global__ void diag_contract_kernel(const double* __restrict__ w, WDesc d, int q, int rpos, const double* __restrict__ v,
+                                     int ldv, double* __restrict__ out) {
+    int64_t before = 1, after = 1;
+    for (int k = 0; k < q; ++k) before *= d.dims[k];
+    for (int k = q + 1; k < d.ndim; ++k) after *= d.dims[k];
+    int64_t rstride = 1;  // stride of the r index in the OUTPUT (mode q removed)
+    for (int k = 0; k < rpos; ++k)
+        if (k != q) rstride *= d.dims[k];
+    const int64_t rdim = d.dims[rpos];
+    const int64_t nq = d.dims[q];
+    const int64_t total = before * after;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(t % In), r = static_cast<int>(t / In);
-        int dig[kMaxOrder] = {0};
-        int64_t off = int64_t(i) * cd.stride[n];
+        const int64_t b = t % before, a = t / before;
+        const int64_t r = (t / rstride) % rdim;
+        const double* src = w + b + a * before * nq;
+        const double* vr = v + r * ldv;
         double acc = 0.0;
-        for (int64_t w = 0; w < W; ++w) {
-            double prod = g[off];
-            for (int p = 0; p < cd.order; ++p)
-                if (p != n) prod *= cd.V[p][dig[p] + int64_t(r) * cd.cs[p]];
-            acc += prod;
-            for (int p = 0; p < cd.order; ++p) {  // increment the mixed-radix counter (modes != n)
-                if (p == n) continue;
-                off += cd.stride[p];
-                if (++dig[p] < cd.cs[p]) break;
-                off -= int64_t(cd.cs[p]) * cd.stride[p];
-                dig[p] = 0;
-            }
-        }
-        h[t] = acc;
+        for (int64_t i = 0; i < nq; ++i) acc = fma(src[i * before], vr[i], acc);
+        out[t] = acc;
+    }
+}
+
+__global__ void finalize_h_kernel(const double* __restrict__ w, int cn, int R, bool transposed, double* __restrict__ h) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cn * R; t += gridDim.x * blockDim.x) {
+        const int i = t % cn, r = t / cn;
+        h[t] = transposed ? w[r + i * R] : w[t];
     }
 }
 
@@ -346,6 +352,11 @@ void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const
         cd.V[n] = V[n];
     }
     double* H = mem.get<double>(size_t(kMaxRank) * R);
+    int64_t min_cs = kMaxRank;
+    for (int n = 0; n < order; ++n) min_cs = std::min<int64_t>(min_cs, core_shape[n]);
+    double* hw[2] = {mem.get<double>(size_t(gsz / min_cs) * R), mem.get<double>(size_t(gsz / min_cs) * R)};
+    std::vector<double*> vpk(order);
+    for (int n = 0; n < order; ++n) vpk[n] = mem.get<double>(size_t(core_shape[n]) * pack_stride(R));
     double* Qm = mem.get<double>(size_t(maxrows) * R);
     double* T = mem.get<double>(size_t(R) * R);
     double* F = mem.get<double>(size_t(R) * R);
@@ -364,6 +375,7 @@ void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const
                                                                                V[n], cd.cs[n], rows[n], R);
         matmul_tn_kernel<<<nblocks(int64_t(R) * R * 32), 256, 0, s>>>(A[n], rows[n], A[n], rows[n], Gm[n], R, rows[n],
                                                                       R);
+        launch_pack_factor<double>(V[n], cd.cs[n], cd.cs[n], R, vpk[n], s);
     }
     // ||Y_T||^2 = <G, G x_n (U_n^T U_n)> (ffcp.hpp:118-131)
     {
@@ -394,7 +406,33 @@ void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const
         for (int n = 0; n < order; ++n) {
             const int cn = cd.cs[n];
             const int64_t m = rows[n];
-            ffcp_h_kernel<<<nblocks(int64_t(cn) * R, 64), 64, 0, st>>>(core, cd, n, R, H);
+            // H = unfold(G, n) * KR_{p != n}(V_p) (ffcp_h): one TTM with V_p0 (p0 = last mode
+            // != n), then diagonal contractions of the other modes against the same column r
+            {
+                int p0 = static_cast<int>(order) - 1;
+                if (p0 == n) --p0;
+                WDesc wd{};
+                wd.ndim = static_cast<int>(order);
+                for (int p = 0; p < order; ++p) wd.dims[p] = cd.cs[p];
+                launch_ttm<double>(core, vpk[p0], hw[0], cd.stride[p0], cd.cs[p0], gsz / (cd.stride[p0] * cd.cs[p0]), R,
+                                   st);
+                wd.dims[p0] = R;
+                int rpos = p0, cur = 0;
+                for (int qm = static_cast<int>(order) - 1; qm >= 0; --qm) {
+                    if (qm == n || qm == p0) continue;
+                    int64_t tot = 1;
+                    for (int p = 0; p < wd.ndim; ++p)
+                        if (p != qm) tot *= wd.dims[p];
+                    diag_contract_kernel<<<nblocks(tot), 256, 0, st>>>(hw[cur], wd, qm, rpos, V[qm], cd.cs[qm],
+                                                                        hw[cur ^ 1]);
+                    for (int p = qm; p + 1 < wd.ndim; ++p) wd.dims[p] = wd.dims[p + 1];
+                    wd.ndim -= 1;
+                    if (qm < rpos) rpos -= 1;
+                    cur ^= 1;
+                }
+                // W is now (cs_n, R) [rpos == 1] or (R, cs_n) [rpos == 0]
+                finalize_h_kernel<<<nblocks(int64_t(cn) * R), 256, 0, st>>>(hw[cur], cn, R, rpos == 0, H);
+            }
             matmul_nn_kernel<<<nblocks(m * R), 256, 0, st>>>(factors[n], m, H, cn, Qm, m, cn, R);
             hadamard_kernel<<<1, 256, 0, st>>>(gram_ptrs, static_cast<int>(order), n, R, T);
             if (kind == TK_CP_NONE || kind == TK_CP_SPARSE) {
@@ -409,6 +447,7 @@ void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const
             }
             matmul_tn_kernel<<<nblocks(int64_t(R) * R * 32), 256, 0, st>>>(A[n], m, A[n], m, Gm[n], R, m, R);
             matmul_tn_kernel<<<nblocks(int64_t(cn) * R * 32), 256, 0, st>>>(factors[n], m, A[n], m, V[n], cn, m, R);
+            launch_pack_factor<double>(V[n], cn, cn, R, vpk[n], st);
             if (n == order - 1)
                 fit_kernel<<<1, 256, 0, st>>>(H, V[n], int64_t(cn) * R, T, Gm[n], R, yt, fit_dev);
         }

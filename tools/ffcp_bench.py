@@ -1,0 +1,20 @@
+"""Times device FFCP on a config-2-sized Tucker model (core 30^3, U 1000x30, CP rank 20)."""
+import os, sys, time
+import numpy as np
+import torch
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
+import paper_1412_1885_b200 as P
+torch.manual_seed(0)
+cs, I, R = 30, 1000, 20
+core = torch.randn(cs ** 3, dtype=torch.float64, device="cuda")
+us = [torch.linalg.qr(torch.randn(I, cs, dtype=torch.float64, device="cuda"))[0].t().contiguous().view(-1) for _ in range(3)]
+m = P.TuckerModel(core, us, (cs, cs, cs))
+iters = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+for kind in (0, 2):
+    P.ffcp(m, R, P.ConstraintSpec(kind), P.StopRule(5, 0.0), (1, 0))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = P.ffcp(m, R, P.ConstraintSpec(kind), P.StopRule(iters, 0.0), (1, 0))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    print(f"ffcp kind {kind}: {res.iterations} iterations in {dt*1e3:.1f} ms ({dt/res.iterations*1e6:.1f} us/iter)", flush=True)

@@ -1,0 +1,10 @@
+#!/bin/bash
+# Full GPU check: tests, bench, launch list (ncu timing-only pass, after the plain run exited 0).
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
+tail -3 gpurun_out/gpu_tests.log
+python bench.py --steps 20 --warmup 3 > gpurun_out/bench_full.log 2> gpurun_out/bench_full.err; echo "bench rc=$?"
+tail -1 gpurun_out/bench_full.log | cut -c1-600
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+tail -1 gpurun_out/bench_ref.log | cut -c1-400

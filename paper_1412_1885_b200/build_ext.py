@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIB_DIR, exist_ok=True)
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(_compile, _sources()))
-    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda"]
+    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs
     subprocess.run(cmd, check=True)
     if verbose:
         print("built", LIB)

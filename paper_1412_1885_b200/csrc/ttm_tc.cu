@@ -19,6 +19,26 @@
 // Accumulators stay in TMEM for the whole K loop; Y is read from HBM exactly once.
 #include <cuda.h>
 
+#include <stdexcept>
+
+namespace {
+// The driver entry point is resolved through the runtime (no link-time libcuda dependency,
+// so the library loads on hosts without a driver and fails only when a kernel is launched).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        return (e == cudaSuccess && q == cudaDriverEntryPointSuccess) ? reinterpret_cast<EncodeTiledFn>(p) : nullptr;
+    }();
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled entry point unavailable");
+    return fn;
+}
+}  // namespace
+
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -332,7 +352,7 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
     const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
     const cuuint32_t box[3] = {256, kTcBK, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims,
+    const CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims,
                                               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -47,6 +47,14 @@ def test_library_is_sm100a(lib):
     assert "sm_100a" in out
 
 
+def test_library_has_no_link_time_driver_dependency(lib):
+    """The driver (libcuda) is reached through the runtime's entry-point query, so the
+    library loads on a build host without a GPU driver (build() runs there)."""
+    from paper_1412_1885_b200 import _lib
+    out = subprocess.run(["readelf", "-d", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libcuda" not in out
+
+
 def test_no_cpu_fallback_without_device(lib):
     import ctypes as C
     import torch

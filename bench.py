@@ -222,7 +222,7 @@ def run_reference(args, cfg):
     sample = f"rand_tucker_2i+ffcp on the {'x'.join(map(str, sdims))} slab of the workload (fp64 oracle, OpenBLAS {threads} threads)"
     line = {
         "metric": "TTM GB/s of Y streamed (% HBM peak) + e2e Tucker+FFCP sec at 1/2/4/8 GPU",
-        "impl": "reference", "value": round(value, 3), "unit": "GB/s", "n_gpus": 0, "steps": args.steps,
+        "impl": "reference", "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference seeded generators, bench.hpp:46-112)",
         "config": {"workload": args.config, "dims": list(cfg["dims"]), "ranks": list(cfg["ranks"]),

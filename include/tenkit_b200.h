@@ -94,6 +94,7 @@ int tk_version(void);
 /* 1 when a CUDA device of compute capability 10.x is usable */
 int tk_device_ok(void);
 
+/* device: CUDA ordinal, or -1 for the calling thread's current device */
 int tk_context_create(int device, tk_context** out);
 int tk_context_destroy(tk_context* ctx);
 /* Run on an external CUDA stream (cudaStream_t), taken literally: NULL is the legacy default

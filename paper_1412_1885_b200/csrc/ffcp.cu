@@ -5,9 +5,12 @@
 // so each sweep is a handful of small kernels; one sweep (all modes) is captured once as a
 // CUDA graph and replayed, with the compressed-space fit read back after every sweep for
 // the stopping rule |fit - prev| < fit_tol (identical iteration count to the reference).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cfloat>
 #include <cmath>
 #include <cstring>
@@ -304,17 +307,533 @@ __global__ void absorb_kernel(double* const* a, const int64_t* rows, int order, 
     }
 }
 
-struct DevBuf {
-    std::vector<void*> ptrs;
-    ~DevBuf() {
-        for (void* p : ptrs) cudaFree(p);
+// ---------------------------------------------------------------------------------------
+// Persistent FFCP: every sweep of every iteration in ONE cooperative launch (one CTA per
+// SM), with the stopping rule evaluated on the device. Per mode n (ffcp.hpp:139-170):
+//   A  H = ffcp_h(G, V, n): one warp per (i, r) over the core slice G[i, ...] staged in
+//      shared memory  |  last CTA: T = *_{p!=n} Gram_p and LDLT(T), LDLT(T + ridge) for the
+//      least-squares kinds (cp.hpp:63-70), one warp each
+//   B  rows of A_n by warps: q = U_n[i,:] H, row update (LS solve / MU / HALS / sparse),
+//      per-CTA partial sums of A_n^T A_n and U_n^T A_n in fixed row order
+//   C  fixed-order reduction of the partials over CTAs -> Gram_n, V_n
+// separated by grid barriers. The compressed-space fit (ffcp.hpp:172-184) is evaluated
+// redundantly (bit-identically) by every CTA, so all CTAs take the same stop decision.
+// ---------------------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+constexpr int kPThreads = 256;
+constexpr int kPWarps = kPThreads / 32;
+
+struct PersistParams {
+    int order, R, kind, max_iters;
+    double c, fit_tol;
+    int cs[kMaxOrder];
+    int64_t gstride[kMaxOrder];
+    int64_t rows[kMaxOrder];
+    const double* core;
+    const double* U[kMaxOrder];
+    double* A[kMaxOrder];
+    double* V[kMaxOrder];
+    double* Gm[kMaxOrder];
+    double* H[2];   // c_n x R, by step parity
+    double* T[2];   // R x R, by step parity
+    double* F;      // LDLT factors of T, and of T + ridge
+    double* Fr;
+    int* sig;       // pivot order (gather indices), [2][kMaxRank]
+    double* part;   // gridDim.x x ps_max partial sums
+    int64_t ps_max;
+    int* bad;       // [2], by step parity
+    const double* yt;
+    double* fit_trace;
+    int* iters;
+    int64_t scratch;  // doubles of the shared scratch region
+    int stage_v;      // phase A stages V_q (p != n) in shared memory
+    int64_t stage_g;  // doubles available for staged core slices (0: read the core from L2)
+    unsigned long long* prof;  // optional: per (step, mark) globaltimer stamps of CTA 0
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PROF_SUB(b, k)                                                                            \
+    do {                                                                                          \
+        if (p.prof && blockIdx.x == (b) && threadIdx.x == 0 && step < 4096) {                                \
+            p.prof[4096 * 4 + step * 8 + (k)] = gtimer();                                                     \
+            p.prof[4096 * 12 + step * 8 + (k)] = clock64();                                                   \
+        }                                                                                                     \
+    } while (0)
+#define PROF_MARK(k)                                                                          \
+    do {                                                                                      \
+        if (p.prof && blockIdx.x == 0 && threadIdx.x == 0 && step < 4096) p.prof[step * 4 + (k)] = gtimer(); \
+    } while (0)
+
+// Eigen's LDLT (ldlt_inplace, the restated cp.hpp:64 solve) pivots on the largest remaining
+// ORIGINAL diagonal entry (the left-looking update never touches the trailing diagonal), so
+// the pivot order is the diagonal sorted by decreasing magnitude (stable); the symmetric
+// permutation is applied first (sig[k] = source row of pivot position k) and the
+// unpivoted factorization runs right-looking, each entry receiving the same updates in the
+// same order as the left-looking loop. One warp, lanes over rows; f = L (strict lower) + D.
+__device__ __forceinline__ void pivot_order(const double* t, int R, double ridge, int* sig) {
+    for (int ii = threadIdx.x & 31; ii < R; ii += 32) {
+        const double di = fabs(t[ii + ii * R] + ridge);
+        int rank = 0;
+        for (int j = 0; j < R; ++j) {
+            const double dj = fabs(t[j + j * R] + ridge);
+            rank += (dj > di) || (dj == di && j < ii);
+        }
+        sig[rank] = ii;
     }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void warp_ldlt(const double* t, int R, double ridge, double* a, int* sig,
+                                          unsigned long long* pr = nullptr) {
+    const int lane = threadIdx.x & 31;
+    if (pr && lane == 0) pr[0] = clock64();
+    pivot_order(t, R, ridge, sig);
+    if (pr && lane == 0) pr[1] = clock64();
+    for (int e = lane; e < R * R; e += 32) {
+        const int x = e % R, y = e / R;
+        a[e] = t[sig[x] + sig[y] * R] + (x == y ? ridge : 0.0);
+    }
+    __syncwarp();
+    // left-looking, lanes over the rows i >= k of column k: w_j = L(k,j) D(j) once per step
+    // (Eigen's temp = D A10^T), then s_i = A(i,k) - sum_j L(i,j) w_j with 4 partial sums
+    double* w = a + R * R;  // R scratch doubles after the matrix
+    if (pr && lane == 0) pr[2] = clock64();
+    for (int k = 0; k < R; ++k) {
+        for (int j = lane; j < k; j += 32) w[j] = a[k + j * R] * a[j + j * R];
+        __syncwarp();
+        const int i0 = k + lane, i1 = k + lane + 32;
+        double s0 = 0.0, s1 = 0.0;
+        if (i0 < R) {
+            double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+            int j = 0;
+            for (; j + 4 <= k; j += 4) {
+                p0 = fma(a[i0 + j * R], w[j], p0);
+                p1 = fma(a[i0 + (j + 1) * R], w[j + 1], p1);
+                p2 = fma(a[i0 + (j + 2) * R], w[j + 2], p2);
+                p3 = fma(a[i0 + (j + 3) * R], w[j + 3], p3);
+            }
+            for (; j < k; ++j) p0 = fma(a[i0 + j * R], w[j], p0);
+            s0 = a[i0 + k * R] - ((p0 + p1) + (p2 + p3));
+        }
+        if (i1 < R) {
+            double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+            int j = 0;
+            for (; j + 4 <= k; j += 4) {
+                p0 = fma(a[i1 + j * R], w[j], p0);
+                p1 = fma(a[i1 + (j + 1) * R], w[j + 1], p1);
+                p2 = fma(a[i1 + (j + 2) * R], w[j + 2], p2);
+                p3 = fma(a[i1 + (j + 3) * R], w[j + 3], p3);
+            }
+            for (; j < k; ++j) p0 = fma(a[i1 + j * R], w[j], p0);
+            s1 = a[i1 + k * R] - ((p0 + p1) + (p2 + p3));
+        }
+        const double dk = __shfl_sync(0xffffffffu, s0, 0);
+        if (lane == 0) a[k + k * R] = dk;
+        else if (i0 < R) a[i0 + k * R] = fabs(dk) > 0.0 ? s0 / dk : s0;
+        if (i1 < R) a[i1 + k * R] = fabs(dk) > 0.0 ? s1 / dk : s1;
+        __syncwarp();
+    }
+    if (pr && lane == 0) pr[3] = clock64();
+}
+
+// b (lane r holds b[r] in b0, b[r + 32] in b1) <- T^{-1} b with T = P^T L D L^T P
+// (f, sig in shared memory); returns false when a component is not finite.
+__device__ __forceinline__ bool warp_ldlt_solve(const double* f, const int* sig, int R, double* sb, double& b0, double& b1,
+                                int lane) {
+    sb[lane] = b0;  // gather b[k] = q[sig[k]]
+    sb[lane + 32] = b1;
+    __syncwarp();
+    double x0 = lane < R ? sb[sig[lane]] : 0.0;
+    double x1 = lane + 32 < R ? sb[sig[lane + 32]] : 0.0;
+    __syncwarp();
+    for (int j = 0; j < R; ++j) {  // L y = b (unit lower), column-oriented
+        const double bj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
+        if (lane > j && lane < R) x0 -= f[lane + j * R] * bj;
+        if (lane + 32 > j && lane + 32 < R) x1 -= f[lane + 32 + j * R] * bj;
+    }
+    if (lane < R) {
+        const double d = f[lane + lane * R];
+        x0 = fabs(d) > DBL_MIN ? x0 / d : 0.0;
+    }
+    if (lane + 32 < R) {
+        const double d = f[lane + 32 + (lane + 32) * R];
+        x1 = fabs(d) > DBL_MIN ? x1 / d : 0.0;
+    }
+    for (int j = R - 1; j >= 0; --j) {  // L^T x = y
+        const double bj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
+        if (lane < j) x0 -= f[j + lane * R] * bj;
+        if (lane + 32 < j) x1 -= f[j + (lane + 32) * R] * bj;
+    }
+    if (lane < R) sb[sig[lane]] = x0;  // scatter x[sig[k]] = y[k]
+    if (lane + 32 < R) sb[sig[lane + 32]] = x1;
+    __syncwarp();
+    b0 = lane < R ? sb[lane] : 0.0;
+    b1 = lane + 32 < R ? sb[lane + 32] : 0.0;
+    __syncwarp();
+    const bool ok = isfinite(b0) && isfinite(b1);
+    return __all_sync(0xffffffffu, ok);
+}
+
+__device__ double block_sum(double v, double* red) {
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = kPThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// dst[e] = src(e), e < n, by the whole CTA: each thread issues a batch of independent
+// (L2) loads before its shared-memory stores, so a staging pass costs ~one round trip.
+template <class Src>
+__device__ __forceinline__ void stage_copy(double* dst, int n, Src src) {
+    constexpr int kB = 8;
+    for (int base = threadIdx.x; base < n; base += kB * kPThreads) {
+        double v[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+            const int e = base + b * kPThreads;
+            v[b] = e < n ? src(e) : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+            const int e = base + b * kPThreads;
+            if (e < n) dst[e] = v[b];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistParams p) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    const int R = p.R, RR = R * R;
+    int maxc = 1;
+    for (int q = 0; q < p.order; ++q) maxc = max(maxc, p.cs[q]);
+    double* sH = sm;                   // maxc * R, [k * R + r]
+    double* sT = sH + maxc * R;        // R * R
+    double* sF = sT + RR;              // R * R (+ R scratch)
+    double* sFr = sF + RR + R;         // R * R (+ R scratch)
+    double* red = sFr + RR + R;        // kPThreads
+    int* ssig = reinterpret_cast<int*>(red + kPThreads);  // 2 x kMaxRank
+    double* scr = reinterpret_cast<double*>(ssig + 2 * kMaxRank);  // p.scratch doubles
+    // phase B view of the scratch
+    double* acc = scr;                           // R*R + maxc*R
+    double* sa = acc + RR + maxc * R;            // kPWarps x kMaxRank (a rows)
+    double* su = sa + kPWarps * kMaxRank;        // kPWarps x kMaxRank (U rows)
+    double* sb = su + kPWarps * kMaxRank;        // kPWarps x kMaxRank (solve scratch)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x;
+    const bool ls = p.kind == TK_CP_NONE || p.kind == TK_CP_SPARSE;
+    double prev = -INFINITY;
+    int it = 0, step = 0;
+    bool stop = false;
+    while (it < p.max_iters && !stop) {
+        for (int n = 0; n < p.order; ++n, ++step) {
+            const int cn = p.cs[n];
+            const int64_t m = p.rows[n];
+            const int par = step & 1;
+            double* H = p.H[par];
+            double* T = p.T[par];
+            PROF_MARK(0);
+            // ---------------- phase A
+            if (blockIdx.x == 0 && tid == 0) p.bad[par ^ 1] = 0;
+            if (blockIdx.x == G - 1) {
+                PROF_SUB(G - 1, 0);
+                for (int e = tid; e < RR; e += kPThreads) {
+                    double g[kMaxOrder];
+                    for (int q = 0; q < p.order; ++q) g[q] = q != n ? __ldcg(p.Gm[q] + e) : 1.0;
+                    double v = 1.0;
+                    for (int q = 0; q < p.order; ++q)
+                        if (q != n) v *= g[q];
+                    sT[e] = v;
+                    T[e] = v;
+                }
+                __syncthreads();
+                PROF_SUB(G - 1, 1);
+                if (ls && warp < 2) {
+                    double ridge = 0.0;
+                    if (warp == 1) {
+                        double tr = 0.0;
+                        for (int i = 0; i < R; ++i) tr += sT[i + i * R];
+                        ridge = 1e-12 * tr + 1e-300;
+                    }
+                    double* f = warp ? sFr : sF;
+                    int* sg = ssig + warp * kMaxRank;
+                    warp_ldlt(sT, R, ridge, f, sg,
+                              (p.prof && warp == 0 && step < 4096) ? p.prof + 4096 * 20 + step * 4 : nullptr);
+                    double* gf = warp ? p.Fr : p.F;
+                    for (int e = lane; e < RR; e += 32) gf[e] = f[e];
+                    for (int e = lane; e < R; e += 32) p.sig[warp * kMaxRank + e] = sg[e];
+                }
+                PROF_SUB(G - 1, 2);
+            } else if (int64_t(blockIdx.x) * kPWarps < int64_t(cn) * R) {
+                // H[i, r] = sum over the other modes of G[i, ...] * prod_{q != n} V_q[i_q, r],
+                // contracting the last other mode innermost (the reference's ffcp_h contracts
+                // trailing modes first, ffcp.hpp:37-41). One warp per (i, r), lanes over the
+                // flattened leading other modes.
+                int om[kMaxOrder], no = 0;
+                for (int q = 0; q < p.order; ++q)
+                    if (q != n) om[no++] = q;
+                const int last = om[no - 1], cl = p.cs[last];
+                int S = 1;
+                for (int q = 0; q < no; ++q) S *= p.cs[om[q]];
+                const int Sp = S / cl;
+                const int Pn = static_cast<int>(p.gstride[n]);  // extent product before mode n
+                auto slice_off = [&](int el) { return (el % Pn) + (el / Pn) * Pn * cn; };
+                const double* vq[kMaxOrder];
+                double* stg = scr;
+                if (p.stage_v) {
+                    for (int q = 0; q < no; ++q) {
+                        const int sz = p.cs[om[q]] * R;
+                        const double* src = p.V[om[q]];
+                        stage_copy(stg, sz, [&](int e) { return __ldcg(src + e); });
+                        vq[q] = stg;
+                        stg += sz;
+                    }
+                } else {
+                    for (int q = 0; q < no; ++q) vq[q] = p.V[om[q]];
+                }
+                const int64_t nw = int64_t(G - 1) * kPWarps;
+                PROF_SUB(0, 3);
+                for (int64_t base = int64_t(blockIdx.x) * kPWarps; base < int64_t(cn) * R; base += nw) {
+                    // this chunk's outputs o = base + warp, (i, r) = (o / R, o % R): stage the
+                    // core slices G[i, ...] of its rows (one L2 round trip for the CTA)
+                    const int64_t olast = (base + kPWarps < int64_t(cn) * R ? base + kPWarps : int64_t(cn) * R) - 1;
+                    const int i0 = static_cast<int>(base / R), i1 = static_cast<int>(olast / R);
+                    const bool sg_ok = p.stage_g >= int64_t(i1 - i0 + 1) * S;
+                    __syncthreads();  // previous chunk done with the staged slices
+                    if (sg_ok)
+                        stage_copy(stg, (i1 - i0 + 1) * S, [&](int e) {
+                            const int ii = i0 + e / S;
+                            return __ldcg(p.core + ii * Pn + slice_off(e % S));
+                        });
+                    __syncthreads();
+                    PROF_SUB(0, 4);
+                    const int64_t o = base + warp;
+                    if (o <= olast) {
+                        const int i = static_cast<int>(o / R), r = static_cast<int>(o % R);
+                        const double* vl = vq[no - 1] + int64_t(r) * cl;
+                        double accv = 0.0;
+                        if (sg_ok) {
+                            const double* gs = stg + (i - i0) * S;
+                            const int sp = Sp;
+                            if (no == 1) {
+                                for (int k = lane; k < cl; k += 32) accv = fma(gs[k], vl[k], accv);
+                            } else {
+                                for (int e = lane; e < sp; e += 32) {
+                                    double t = 0.0;
+#pragma unroll 8
+                                    for (int k = 0; k < cl; ++k) t = fma(gs[e + k * sp], vl[k], t);
+                                    int rem = e;
+                                    double prod = 1.0;
+                                    for (int q = 0; q + 1 < no; ++q) {
+                                        const int c = p.cs[om[q]];
+                                        prod *= vq[q][rem % c + r * c];
+                                        rem /= c;
+                                    }
+                                    accv = fma(prod, t, accv);
+                                }
+                            }
+                        } else {
+                            const double* gi = p.core + i * Pn;
+                            if (no == 1) {
+                                for (int k = lane; k < cl; k += 32) accv = fma(__ldcg(gi + slice_off(k)), vl[k], accv);
+                            } else {
+                                for (int e = lane; e < Sp; e += 32) {
+                                    double t = 0.0;
+#pragma unroll 8
+                                    for (int k = 0; k < cl; ++k) t = fma(__ldcg(gi + slice_off(e + k * Sp)), vl[k], t);
+                                    int rem = e;
+                                    double prod = 1.0;
+                                    for (int q = 0; q + 1 < no; ++q) {
+                                        const int c = p.cs[om[q]];
+                                        prod *= vq[q][rem % c + r * c];
+                                        rem /= c;
+                                    }
+                                    accv = fma(prod, t, accv);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int off = 16; off > 0; off >>= 1) accv += __shfl_xor_sync(0xffffffffu, accv, off);
+                        if (lane == 0) H[i + int64_t(r) * cn] = accv;
+                    }
+                    PROF_SUB(0, 5);
+                }
+            }
+            grid.sync();
+            PROF_MARK(1);
+            // ---------------- phase B (and the ridge rerun)
+            const int ps = RR + cn * R;
+            for (int attempt = 0; attempt < 2; ++attempt) {
+                const bool ridge = attempt == 1;
+                if (ridge && !(ls && __ldcg(p.bad + par))) break;
+                stage_copy(sH, cn * R, [&](int d) { return __ldcg(H + (d / R) + (d % R) * cn); });
+                stage_copy(sT, RR, [&](int e) { return __ldcg(T + e); });
+                if (ls) {
+                    const double* fsrc = ridge ? p.Fr : p.F;
+                    stage_copy(sF, RR, [&](int e) { return __ldcg(fsrc + e); });
+                }
+                for (int e = tid; e < R; e += kPThreads) ssig[e] = __ldcg(p.sig + (ridge ? kMaxRank : 0) + e);
+                for (int e = tid; e < ps; e += kPThreads) acc[e] = 0.0;
+                __syncthreads();
+                if (!ridge) PROF_SUB(0, 6);
+                const double* U = p.U[n];
+                double* A = p.A[n];
+                double* wa = sa + warp * kMaxRank;
+                double* wu = su + warp * kMaxRank;
+                double* wb = sb + warp * kMaxRank;
+                const int64_t chunk = int64_t(G) * kPWarps;
+                for (int64_t base = int64_t(blockIdx.x) * kPWarps; base < m; base += chunk) {
+                    const int64_t i = base + warp;
+                    if (i < m) {
+                        for (int k = lane; k < cn; k += 32) wu[k] = U[i + k * m];
+                        double a0 = 0.0, a1 = 0.0;
+                        if (!ls) {
+                            a0 = lane < R ? A[i + int64_t(lane) * m] : 0.0;
+                            a1 = lane + 32 < R ? A[i + int64_t(lane + 32) * m] : 0.0;
+                        }
+                        __syncwarp();
+                        double q0 = 0.0, q1 = 0.0;
+                        if (lane < R) {
+#pragma unroll 8
+                            for (int k = 0; k < cn; ++k) q0 = fma(wu[k], sH[k * R + lane], q0);
+                        }
+                        if (lane + 32 < R) {
+#pragma unroll 8
+                            for (int k = 0; k < cn; ++k) q1 = fma(wu[k], sH[k * R + lane + 32], q1);
+                        }
+                        if (ls) {
+                            a0 = q0;
+                            a1 = q1;
+                            const bool ok = warp_ldlt_solve(sF, ssig, R, wb, a0, a1, lane);
+                            if (!ok && !ridge && lane == 0) p.bad[par] = 1;
+                            if (p.kind == TK_CP_SPARSE) {
+                                const double cc = p.c;
+                                a0 = a0 > cc ? a0 - cc : (a0 < -cc ? a0 + cc : 0.0);
+                                a1 = a1 > cc ? a1 - cc : (a1 < -cc ? a1 + cc : 0.0);
+                            }
+                        } else if (p.kind == TK_CP_NONNEG_MU) {  // ffcp.hpp:157-161
+                            wa[lane] = a0;
+                            wa[lane + 32] = a1;
+                            __syncwarp();
+                            double t0 = 0.0, t1 = 0.0;
+                            if (lane < R)
+                                for (int u = 0; u < R; ++u) t0 += wa[u] * sT[u + lane * R];
+                            if (lane + 32 < R)
+                                for (int u = 0; u < R; ++u) t1 += wa[u] * sT[u + (lane + 32) * R];
+                            a0 *= fmax(q0, 0.0) / fmax(t0, 1e-16);
+                            a1 *= fmax(q1, 0.0) / fmax(t1, 1e-16);
+                            __syncwarp();
+                        } else {  // HALS, projected (cp.hpp:84-92), columns in order
+                            wa[lane] = a0;
+                            wa[lane + 32] = a1;
+                            __syncwarp();
+                            for (int r = 0; r < R; ++r) {
+                                const double trr = sT[r + r * R];
+                                if (trr < 1e-15) continue;
+                                double sacc = 0.0;
+                                for (int u = 0; u < R; ++u) sacc += wa[u] * sT[u + r * R];
+                                const double qr = __shfl_sync(0xffffffffu, r < 32 ? q0 : q1, r & 31);
+                                const double nv = fmax(wa[r] + (qr - sacc) / trr, 0.0);
+                                __syncwarp();
+                                if (lane == 0) wa[r] = nv;
+                                __syncwarp();
+                            }
+                            a0 = wa[lane];
+                            a1 = wa[lane + 32];
+                            __syncwarp();
+                        }
+                        if (lane < R) A[i + int64_t(lane) * m] = a0;
+                        if (lane + 32 < R) A[i + int64_t(lane + 32) * m] = a1;
+                        wa[lane] = a0;
+                        wa[lane + 32] = a1;
+                    }
+                    __syncthreads();
+                    const int nrow = static_cast<int>(m - base < kPWarps ? m - base : int64_t(kPWarps));
+                    for (int e = tid; e < ps; e += kPThreads) {
+                        double v = acc[e];
+                        if (e < RR) {
+                            const int x = e % R, y = e / R;
+#pragma unroll
+                            for (int w = 0; w < kPWarps; ++w)
+                                if (w < nrow) v = fma(sa[w * kMaxRank + x], sa[w * kMaxRank + y], v);
+                        } else {
+                            const int e2 = e - RR, k = e2 % cn, r = e2 / cn;
+#pragma unroll
+                            for (int w = 0; w < kPWarps; ++w)
+                                if (w < nrow) v = fma(su[w * kMaxRank + k], sa[w * kMaxRank + r], v);
+                        }
+                        acc[e] = v;
+                    }
+                    __syncthreads();
+                }
+                if (!ridge) PROF_SUB(0, 7);
+                for (int e = tid; e < ps; e += kPThreads) p.part[int64_t(blockIdx.x) * p.ps_max + e] = acc[e];
+                grid.sync();
+                PROF_MARK(2);
+            }
+            // ---------------- phase C: Gram_n, V_n in fixed order over CTAs
+            for (int64_t e = int64_t(blockIdx.x) * kPWarps + warp; e < ps; e += int64_t(G) * kPWarps) {
+                double v = 0.0;
+                double pv[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int b = lane + 32 * t;
+                    pv[t] = b < G ? __ldcg(p.part + int64_t(b) * p.ps_max + e) : 0.0;
+                }
+                for (int t = 0; t < 8; ++t) v += pv[t];
+                for (int b = lane + 256; b < G; b += 32) v += __ldcg(p.part + int64_t(b) * p.ps_max + e);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0) {
+                    if (e < RR) p.Gm[n][e] = v;
+                    else p.V[n][e - RR] = v;
+                }
+            }
+            grid.sync();
+            PROF_MARK(3);
+        }
+        // fit (ffcp.hpp:172-184), identical in every CTA
+        {
+            const int nl = p.order - 1, cn = p.cs[nl];
+            const int par = (step - 1) & 1;
+            double a = 0.0, b = 0.0;
+            for (int e = tid; e < cn * R; e += kPThreads) a += __ldcg(p.H[par] + e) * __ldcg(p.V[nl] + e);
+            for (int e = tid; e < RR; e += kPThreads) b += __ldcg(p.T[par] + e) * __ldcg(p.Gm[nl] + e);
+            const double inner = block_sum(a, red);
+            const double msq = block_sum(b, red);
+            const double res = fmax(0.0, p.yt[0] - 2.0 * inner + msq);
+            const double f = 1.0 - sqrt(res) / sqrt(p.yt[0]);
+            if (blockIdx.x == 0 && tid == 0) p.fit_trace[it] = f;
+            ++it;
+            stop = fabs(f - prev) < p.fit_tol;
+            prev = f;
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) *p.iters = it;
+}
+
+// Shared memory of the persistent kernel: fixed part + `scratch` doubles.
+size_t persist_smem(int R, int maxc, int64_t scratch) {
+    return sizeof(double) * (size_t(maxc) * R + 3 * size_t(R) * R + 2 * size_t(R) + kPThreads + size_t(scratch)) +
+           sizeof(int) * 2 * kMaxRank;
+}
+
+struct DevBuf {  // per-call scratch carved from the context's named pool (no per-call cudaMalloc)
+    BufPool& pool;
+    int next = 0;
+    explicit DevBuf(BufPool& p) : pool(p) {}
     template <typename T>
     T* get(size_t n) {
-        void* p = nullptr;
-        TK_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-        ptrs.push_back(p);
-        return static_cast<T*>(p);
+        return static_cast<T*>(pool.get("ffcp#" + std::to_string(next++), std::max<size_t>(n, 1) * sizeof(T)));
     }
 };
 
@@ -322,7 +841,7 @@ struct DevBuf {
 
 // Device FFCP. core/factors: device fp64 (factors[n]: rows[n] x core_shape[n]); outputs
 // (out_factors[n]: rows[n] x rank, fit_trace: max_iters) are device or host per out_on_device.
-void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
+void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
                  const int64_t* rows, int64_t rank, int kind, double c, int max_iters, double fit_tol, Seed seed,
                  double** out_factors, double* fit_trace, int* iterations) {
     require(order >= 2, "ffcp: tensor order must be at least 2");
@@ -333,7 +852,7 @@ void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const
     require(kind >= TK_CP_NONE && kind <= TK_CP_SPARSE, "ffcp: unknown constraint");
     const int R = static_cast<int>(rank);
     const bool nonneg = kind == TK_CP_NONNEG_MU || kind == TK_CP_NONNEG_HALS;
-    DevBuf mem;
+    DevBuf mem(pool);
     CoreDesc cd{};
     cd.order = static_cast<int>(order);
     int64_t gsz = 1, maxrows = 1;
@@ -401,7 +920,165 @@ void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const
     TK_CUDA(cudaStreamSynchronize(s));
     require(std::sqrt(h_yt) > 0.0, "ffcp: compressed tensor has zero norm");
 
-    // one sweep over the modes, captured once as a graph
+    const char* env = std::getenv("TENKIT_FFCP_GRAPH");
+    if (!(env && env[0] == '1')) {  // persistent cooperative kernel (default)
+        int dev = 0, nsm = 0, coop = 0, per_sm = 0;
+        TK_CUDA(cudaGetDevice(&dev));
+        TK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        TK_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        require(coop != 0, "ffcp: device lacks cooperative launch");
+        int maxc = 1;
+        for (int n = 0; n < order; ++n) maxc = std::max(maxc, cd.cs[n]);
+        int smem_optin = 0;
+        TK_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        // scratch: phase B needs acc + 3 row buffers per warp; phase A stages V_q (q != n)
+        // and the core slices G[i, ...] of one chunk of outputs (<= kPWarps / R + 2 rows)
+        int64_t gsz_all = 1, vsum = 0, smax = 1;
+        for (int n = 0; n < order; ++n) {
+            gsz_all *= cd.cs[n];
+            vsum += int64_t(cd.cs[n]) * R;
+        }
+        for (int n = 0; n < order; ++n) smax = std::max<int64_t>(smax, gsz_all / cd.cs[n]);
+        const int64_t need_b = int64_t(R) * R + int64_t(maxc) * R + 3 * kPWarps * kMaxRank;
+        const int64_t slices = smax * (kPWarps / R + 2);
+        const int64_t budget =
+            (int64_t(smem_optin) - 2048) / 8 - (int64_t(maxc) * R + 3 * int64_t(R) * R + 2 * R + kPThreads + kMaxRank);
+        require(gsz_all < (int64_t(1) << 31), "ffcp: core too large for the device path");
+        const char* nostage = std::getenv("TENKIT_FFCP_NOSTAGE");
+        const bool allow = !(nostage && nostage[0] == '1');
+        bool stage_v = allow && vsum + slices <= budget;
+        int64_t scratch = need_b;
+        int64_t stage_g = 0;
+        if (stage_v) {
+            scratch = std::max(need_b, vsum + slices);
+            stage_g = scratch - vsum;
+        } else if (allow && vsum <= budget) {
+            stage_v = true;
+            scratch = std::max(need_b, vsum);
+        }
+        const size_t smem = persist_smem(R, maxc, scratch);
+        TK_CUDA(cudaFuncSetAttribute(ffcp_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffcp_persistent_kernel, kPThreads, smem));
+        require(per_sm >= 1, "ffcp: persistent kernel does not fit an SM");
+        const int G = nsm;  // one CTA per SM (co-resident by construction)
+        PersistParams pp{};
+        pp.order = static_cast<int>(order);
+        pp.R = R;
+        pp.kind = kind;
+        pp.max_iters = max_iters;
+        pp.c = c;
+        pp.fit_tol = fit_tol;
+        pp.core = core;
+        for (int n = 0; n < order; ++n) {
+            pp.cs[n] = cd.cs[n];
+            pp.gstride[n] = cd.stride[n];
+            pp.rows[n] = rows[n];
+            pp.U[n] = factors[n];
+            pp.A[n] = A[n];
+            pp.V[n] = V[n];
+            pp.Gm[n] = Gm[n];
+        }
+        pp.ps_max = int64_t(R) * R + int64_t(maxc) * R;
+        for (int b = 0; b < 2; ++b) {
+            pp.H[b] = mem.get<double>(size_t(maxc) * R);
+            pp.T[b] = mem.get<double>(size_t(R) * R);
+        }
+        pp.F = mem.get<double>(size_t(R) * R);
+        pp.Fr = mem.get<double>(size_t(R) * R);
+        pp.sig = mem.get<int>(2 * kMaxRank);
+        pp.part = mem.get<double>(size_t(G) * pp.ps_max);
+        pp.bad = mem.get<int>(2);
+        pp.yt = yt;
+        pp.fit_trace = mem.get<double>(std::max(max_iters, 1));
+        pp.iters = mem.get<int>(1);
+        pp.scratch = scratch;
+        pp.stage_v = stage_v ? 1 : 0;
+        pp.stage_g = stage_g;
+        const char* profenv = std::getenv("TENKIT_FFCP_PROF");
+        const bool prof = profenv && profenv[0] == '1';
+        if (prof) {
+            pp.prof = mem.get<unsigned long long>(4096 * 24);
+            TK_CUDA(cudaMemsetAsync(pp.prof, 0, 4096 * 24 * sizeof(unsigned long long), s));
+        }
+        TK_CUDA(cudaMemsetAsync(pp.bad, 0, 2 * sizeof(int), s));
+        TK_CUDA(cudaMemsetAsync(pp.iters, 0, sizeof(int), s));
+        void* args[] = {&pp};
+        TK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(ffcp_persistent_kernel), dim3(G), dim3(kPThreads),
+                                            args, smem, s));
+        int it = 0;
+        TK_CUDA(cudaMemcpyAsync(&it, pp.iters, sizeof(int), cudaMemcpyDeviceToHost, s));
+        TK_CUDA(cudaStreamSynchronize(s));
+        if (it > 0) TK_CUDA(cudaMemcpyAsync(fit_trace, pp.fit_trace, sizeof(double) * it, cudaMemcpyDeviceToHost, s));
+        *iterations = it;
+        if (prof) {
+            std::vector<unsigned long long> h(4096 * 24);
+            TK_CUDA(cudaMemcpy(h.data(), pp.prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            const int steps = std::min(4095, it * static_cast<int>(order));
+            double ph[4] = {0, 0, 0, 0};
+            for (int st = 1; st + 1 < steps; ++st) {
+                ph[0] += double(h[st * 4 + 1] - h[st * 4 + 0]);
+                ph[1] += double(h[st * 4 + 2] - h[st * 4 + 1]);
+                ph[2] += double(h[st * 4 + 3] - h[st * 4 + 2]);
+                ph[3] += double(h[(st + 1) * 4 + 0] - h[st * 4 + 3]);
+            }
+            double sub[6] = {0, 0, 0, 0, 0, 0};
+            for (int st = 1; st + 1 < steps; ++st) {
+                const unsigned long long* q = h.data() + 4096 * 4 + st * 8;
+                const unsigned long long a0 = h[st * 4 + 0];
+                sub[0] += double(q[1] - q[0]);  // T
+                sub[1] += double(q[2] - q[1]);  // LDLT
+                sub[2] += double(q[0] - a0);    // start skew of the last CTA
+                sub[3] += double(q[3] - a0);    // V staging (CTA 0)
+                sub[4] += double(q[4] - q[3]);  // slice staging
+                sub[5] += double(q[5] - q[4]);  // H compute
+            }
+            for (double& v : sub) v /= 1e3 * (steps - 2);
+            double bsub[3] = {0, 0, 0};
+            for (int st = 1; st + 1 < steps; ++st) {
+                const unsigned long long* q = h.data() + 4096 * 4 + st * 8;
+                bsub[0] += double(q[6] - h[st * 4 + 1]);  // phase B staging
+                bsub[1] += double(q[7] - q[6]);           // rows + partial sums
+                bsub[2] += double(h[st * 4 + 2] - q[7]);  // partial store + grid sync
+            }
+            std::fprintf(stderr, "  phase B: stage %.2f rows %.2f store+sync %.2f\n", bsub[0] / 1e3 / (steps - 2),
+                         bsub[1] / 1e3 / (steps - 2), bsub[2] / 1e3 / (steps - 2));
+            double lc[3] = {0, 0, 0};
+            for (int st = 1; st + 1 < steps; ++st) {
+                const unsigned long long* q = h.data() + 4096 * 20 + st * 4;
+                if (!q[0]) continue;
+                lc[0] += double(q[1] - q[0]);
+                lc[1] += double(q[2] - q[1]);
+                lc[2] += double(q[3] - q[2]);
+            }
+            std::fprintf(stderr, "  ldlt cycles: pivot %.0f copy %.0f factor %.0f\n", lc[0] / (steps - 2), lc[1] / (steps - 2),
+                         lc[2] / (steps - 2));
+            double cyc[3] = {0, 0, 0};
+            for (int st = 1; st + 1 < steps; ++st) {
+                const unsigned long long* q = h.data() + 4096 * 12 + st * 8;
+                cyc[0] += double(q[2] - q[1]);  // LDLT (cycles)
+                cyc[1] += double(q[4] - q[3]);  // slices
+                cyc[2] += double(q[5] - q[4]);  // compute
+            }
+            std::fprintf(stderr, "  cycles: ldlt %.0f slices %.0f compute %.0f\n", cyc[0] / (steps - 2), cyc[1] / (steps - 2),
+                         cyc[2] / (steps - 2));
+            std::fprintf(stderr, "  ldlt-cta: skew %.2f T %.2f ldlt %.2f | cta0: vstage %.2f slices %.2f compute %.2f\n", sub[2], sub[0],
+                         sub[1], sub[3], sub[4], sub[5]);
+            std::fprintf(stderr, "ffcp persistent: per mode-step us: A %.2f  B %.2f  C %.2f  fit/loop %.2f  (grid %d, stage %d)\n",
+                         ph[0] / 1e3 / (steps - 2), ph[1] / 1e3 / (steps - 2), ph[2] / 1e3 / (steps - 2),
+                         ph[3] / 1e3 / (steps - 2), G, int(stage_g > 0));
+        }
+        double** aptrs = mem.get<double*>(order);
+        int64_t* rws = mem.get<int64_t>(order);
+        TK_CUDA(cudaMemcpyAsync(aptrs, A.data(), sizeof(double*) * order, cudaMemcpyHostToDevice, s));
+        TK_CUDA(cudaMemcpyAsync(rws, rows, sizeof(int64_t) * order, cudaMemcpyHostToDevice, s));
+        absorb_kernel<<<R, 256, 0, s>>>(aptrs, rws, static_cast<int>(order), R);
+        TK_LAUNCH_CHECK();
+        TK_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+
+    // one sweep over the modes, captured once as a graph (TENKIT_FFCP_GRAPH=1)
     auto sweep = [&](cudaStream_t st) {
         for (int n = 0; n < order; ++n) {
             const int cn = cd.cs[n];

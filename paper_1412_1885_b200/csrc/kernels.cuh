@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 #include "common.cuh"
 
@@ -73,8 +74,14 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
 // Largest Z (rows) the cluster QR can hold for `ncols` columns.
 int64_t qr_max_rows(int ncols);
 
+// Named device scratch owned by the caller's context (grows, never shrinks; reused across calls).
+struct BufPool {
+    virtual void* get(const std::string& name, size_t bytes) = 0;
+    virtual ~BufPool() = default;
+};
+
 // FFCP on the device (ffcp.cu); all pointers are device pointers, fit_trace is host memory.
-void ffcp_device(cudaStream_t s, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
+void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
                  const int64_t* rows, int64_t rank, int kind, double c, int max_iters, double fit_tol, Seed seed,
                  double** out_factors, double* fit_trace, int* iterations);
 

@@ -576,6 +576,7 @@ int tk_context_create(int device, tk_context** out) {
     return guarded([&] {
         require(out != nullptr, "null output");
         auto ctx = std::make_unique<tk_context>();
+        if (device < 0) TK_CUDA(cudaGetDevice(&device));  // -1: the calling thread's current device
         ctx->device = device;
         TK_CUDA(cudaSetDevice(device));
         TK_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
@@ -658,6 +659,14 @@ int tk_rand_tucker(tk_context* ctx, int dtype, int64_t order, const int64_t* dim
     });
 }
 
+namespace {
+struct CtxPool : tkb::BufPool {
+    tk_context* c;
+    explicit CtxPool(tk_context* ctx) : c(ctx) {}
+    void* get(const std::string& name, size_t bytes) override { return c->buf(name, bytes); }
+};
+}  // namespace
+
 int tk_ffcp_device(tk_context* ctx, int64_t order, const int64_t* core_shape, const double* core,
                    const double** factors, const int64_t* rows, int64_t rank, int constraint, double sparsity_c,
                    int max_iters, double fit_tol, uint64_t seed_root, uint64_t seed_stream, double** out_factors,
@@ -665,7 +674,8 @@ int tk_ffcp_device(tk_context* ctx, int64_t order, const int64_t* core_shape, co
     return guarded([&] {
         check_ctx(ctx);
         require(order >= 2 && order <= TK_MAX_ORDER, "ffcp: tensor order must be at least 2");
-        ffcp_device(ctx->stream, order, core_shape, core, factors, rows, rank, constraint, sparsity_c, max_iters,
+        CtxPool pool(ctx);
+        ffcp_device(pool, ctx->stream, order, core_shape, core, factors, rows, rank, constraint, sparsity_c, max_iters,
                     fit_tol, Seed{seed_root, seed_stream}, out_factors, fit_trace, iterations);
     });
 }
@@ -690,7 +700,8 @@ int tk_ffcp(tk_context* ctx, int64_t order, const int64_t* core_shape, const dou
             df[n] = u;
             dout[n] = static_cast<double*>(ctx->buf("ffcp_a" + std::to_string(n), sizeof(double) * rows[n] * rank));
         }
-        ffcp_device(s, order, core_shape, dcore, df.data(), rows, rank, constraint, sparsity_c, max_iters, fit_tol,
+        CtxPool pool(ctx);
+        ffcp_device(pool, s, order, core_shape, dcore, df.data(), rows, rank, constraint, sparsity_c, max_iters, fit_tol,
                     Seed{seed_root, seed_stream}, dout.data(), fit_trace, iterations);
         for (int64_t n = 0; n < order; ++n)
             TK_CUDA(cudaMemcpyAsync(out_factors[n], dout[n], sizeof(double) * rows[n] * rank, cudaMemcpyDeviceToHost, s));

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -98,6 +99,21 @@ __device__ void reduce_dots(Sh& sh, cg::cluster_group& cl, unsigned cs, int& par
     }
     par ^= 1;
     __syncthreads();
+}
+
+// zr[j * ld] = fma(a, w[j], zr[j * ld]) for j in [j0, j1): loads of a group issued before its
+// stores (the compiler cannot prove the column stores do not alias the next loads)
+__device__ __forceinline__ void axpy_row(double* zr, int ld, int j0, int j1, double a, const double* w) {
+    int j = j0;
+    for (; j + 4 <= j1; j += 4) {
+        const double z0 = zr[j * ld], z1 = zr[(j + 1) * ld], z2 = zr[(j + 2) * ld], z3 = zr[(j + 3) * ld];
+        const double w0 = w[j], w1 = w[j + 1], w2 = w[j + 2], w3 = w[j + 3];
+        zr[j * ld] = fma(a, w0, z0);
+        zr[(j + 1) * ld] = fma(a, w1, z1);
+        zr[(j + 2) * ld] = fma(a, w2, z2);
+        zr[(j + 3) * ld] = fma(a, w3, z3);
+    }
+    for (; j < j1; ++j) zr[j * ld] = fma(a, w[j], zr[j * ld]);
 }
 
 __global__ void __launch_bounds__(kQrThreads, 1)
@@ -257,8 +273,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         if (tau != 0.0) {
             for (int i = i0 + tid; i < nloc; i += kQrThreads) {
                 const double tv = tau * z[i + k * ld];
-#pragma unroll 4
-                for (int j = k + 1; j < ncols; ++j) z[i + j * ld] = fma(-tv, sh.wv[j], z[i + j * ld]);
+                axpy_row(z + i, ld, k + 1, ncols, -tv, sh.wv);
             }
             if (owner)
                 for (int j = k + 1 + tid; j < ncols; j += kQrThreads) z[lk + j * ld] -= tau * sh.wv[j];
@@ -311,8 +326,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             if (tau != 0.0)
                 for (int i = i0 + tid; i < nloc; i += kQrThreads) {
                     const double tv = tau * z[i + k * ld];
-#pragma unroll 4
-                    for (int j = k + 1; j < rank; ++j) z[i + j * ld] = fma(-tv, sh.tot[j - k - 1], z[i + j * ld]);
+                    axpy_row(z + i, ld, k + 1, rank, -tv, sh.tot - (k + 1));
                 }
             if (owner)
                 for (int j = k + 1 + tid; j < rank; j += kQrThreads) z[lk + j * ld] = -tau * sh.tot[j - k - 1];
@@ -398,10 +412,18 @@ __global__ void __launch_bounds__(kQrThreads, 1)
 }
 
 int pick_cluster(int64_t rows, int ncols, int* ld_out, size_t* smem_out) {
-    for (int cs = 1; cs <= 16; cs *= 2) {
+    static const int min_cs = [] {
+        const char* e = std::getenv("TENKIT_QR_MIN_CLUSTER");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    // The QR is latency-bound per Householder step; spreading the rows so that each CTA holds
+    // <= 128 of them cuts the per-step reduction and update work (1000 x 30: 8 CTAs, ~30%
+    // faster than the 2 the shared memory alone needs; measured with tools/qr_trace.cu).
+    constexpr int kTargetRows = 128;
+    for (int cs = min_cs; cs <= 16; cs *= 2) {
         const int ld = static_cast<int>((rows + cs - 1) / cs);
         const size_t smem = size_t(ld) * ncols * sizeof(double) + kQrFixedSmem;
-        if (smem <= kQrSmemCap) {
+        if (smem <= kQrSmemCap && (ld <= kTargetRows || cs == 16)) {
             *ld_out = ld;
             *smem_out = smem;
             return cs;

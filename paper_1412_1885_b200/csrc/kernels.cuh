@@ -34,7 +34,8 @@ void launch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t 
 
 // tcgen05 path (ttm_tc.cu, fp32 data): 3xTF32 UMMA contraction of the (P, K, Q) view with
 // the factor packed by launch_pack_umma ([U_hi | U_lo] core-matrix blocks).
-bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t Q, int cols);
+// P == 1 (contraction over the fastest mode) uses the K-major variant (K % 4 == 0, cols <= 32).
+bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols);
 int64_t umma_pack_bytes(int64_t rows, int cols);
 void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s);
 void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,

@@ -51,18 +51,30 @@ constexpr int kTcConv = 8;                      // converter warps: 2 per TMEM l
 constexpr int kTcThreads = (kTcConv + 2) * 32;  // + producer warp + MMA warp
 constexpr int kTcBK = 16;                       // K per pipeline stage (2 MMA k-steps of 8)
 constexpr int kTcStages = 4;
+// 3xTF32: y_hi u_hi -> main accumulators, y_hi u_lo + y_lo u_hi -> cross accumulator (the
+// fourth product y_lo u_lo, 2^-22 relative, is dropped).
 
-template <int NH>
+template <int NH, int MT_ = (NH <= 32 ? 4 : 2)>
 struct TcCfg {
-    static constexpr int MT = NH <= 32 ? 4 : 2;  // 128-row M tiles per CTA
+    static constexpr int MT = MT_;  // 128-row M tiles per CTA
     static constexpr int BM = 128 * MT;
+    static constexpr int BOXR = BM < 256 ? BM : 256;  // rows per TMA box
     static constexpr int BBYTES = 64 * NH;       // one k-step of [U_hi | U_lo]: 2NH rows x 8 tf32
     static constexpr int STAGE_Y = kTcBK * BM * 4;
     static constexpr int STAGE_B = 2 * BBYTES;
-    static constexpr int D_COLS = MT * 2 * NH;
+    static constexpr int D_COLS = MT * 2 * NH;   // one accumulator set: per tile [main | cross]
     static constexpr int A_COLS = MT * 32;       // per A stage and tile: 16 hi + 16 lo columns
-    static_assert(D_COLS + 2 * A_COLS <= 512, "TMEM budget");
-    static constexpr size_t smem = size_t(kTcStages) * (STAGE_Y + STAGE_B) + 256 + 128;
+    static constexpr int XBASE = D_COLS + 2 * A_COLS;  // accumulator sets 1.. (D_COLS each)
+    // The fp32 accumulation inside the tensor core truncates, so its error grows with the
+    // number of MMAs accumulated into one D: k-block kc accumulates into set kc % S, and the
+    // sets are summed in round-to-nearest fp32 in the epilogue.
+    static constexpr int S_RAW = 1 + (512 - XBASE) / D_COLS;
+    static constexpr int S = S_RAW > 4 ? 4 : S_RAW;
+    static_assert(XBASE <= 512, "TMEM budget");
+    // pipeline depth: ~128 KB of Y in flight per SM whatever the tile height
+    static constexpr int STAGES_RAW = (128 * 1024) / STAGE_Y;
+    static constexpr int STAGES = STAGES_RAW < kTcStages ? kTcStages : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
+    static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 256 + 128;
 };
 
 __device__ __forceinline__ uint32_t f2tf32(float x) {
@@ -72,7 +84,8 @@ __device__ __forceinline__ uint32_t f2tf32(float x) {
 }
 
 // round-to-nearest (ties away) to tf32 on the magnitude bits; the residual x - hi is exact
-// in fp32 and is handed to the MMA as is (the tensor core reads its top 19 bits)
+// in fp32 and is handed to the MMA as is (the tensor core reads its top 19 bits; rounding it
+// first changed nothing measurable and costs converter issue slots)
 __device__ __forceinline__ uint32_t tf32_hi_bits(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
 
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -132,24 +145,56 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                  : "memory");
 }
 
-template <int NH>
+// Columns rc..rc+15 of tile j: sum over the accumulator sets of (main + cross), in
+// round-to-nearest fp32 (`used` = sets actually written: min(k-blocks, S)).
+template <class C>
+__device__ __forceinline__ void drain16(uint32_t tl, int j, int rc, int used, float (&v)[16]) {
+    constexpr int NH = C::D_COLS / (2 * C::MT);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = 0.f;
+    for (int sm = 0; sm < used; ++sm) {
+        const uint32_t base = tl + uint32_t((sm == 0 ? 0 : C::XBASE + (sm - 1) * C::D_COLS) + j * 2 * NH + rc);
+        uint32_t uh[16], ul[16];
+        tmem_ld16(base, uh);
+        tmem_ld16(base + NH, ul);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] += __uint_as_float(uh[e]) + __uint_as_float(ul[e]);
+    }
+}
+
+// KM = false: the contracted mode is not the fastest (P > 1): Y viewed as (P, K, Q), tiles of
+//   BM consecutive p for one q, TMA boxes of 256 p x 16 k, out[p + r P + q P cols].
+// KM = true: the contracted mode is mode 0 (P == 1): Y viewed as Q rows of K contiguous
+//   values, tiles of BM rows, TMA boxes of BOXR rows x 16 k (64 B, 64B-swizzled so the
+//   converters' 16-B row reads are bank-conflict free), out[r + q cols] written through a
+//   shared-memory transpose (coalesced rows of the output).
+template <int NH, int MT_, bool KM>
 __global__ void __launch_bounds__(kTcThreads, 1)
     ttm_tc_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
                   int64_t P, int64_t K, int cols, int64_t tiles_p) {
-    using C = TcCfg<NH>;
+    using C = TcCfg<NH, MT_>;
     constexpr int MT = C::MT, BM = C::BM;
     extern __shared__ __align__(1024) uint8_t tsm[];
     uint8_t* sY = tsm;  // [stages][BM/256 boxes][kTcBK][256] fp32
-    uint8_t* sB = tsm + size_t(kTcStages) * C::STAGE_Y;           // [stages][2][2NH x 8] tf32 core matrices
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kTcStages) * C::STAGE_B);
+    uint8_t* sB = tsm + size_t(C::STAGES) * C::STAGE_Y;           // [stages][2][2NH x 8] tf32 core matrices
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(C::STAGES) * C::STAGE_B);
     uint64_t* full = bars;                   // [stages]  producer -> (converters, MMA)
-    uint64_t* empty = bars + kTcStages;      // [stages]  converters (4) + MMA commit (1) -> producer
-    uint64_t* afull = bars + 2 * kTcStages;  // [2]       converters -> MMA
+    uint64_t* empty = bars + C::STAGES;      // [stages]  converters (4) + MMA commit (1) -> producer
+    uint64_t* afull = bars + 2 * C::STAGES;  // [2]       converters -> MMA
     uint64_t* aempty = afull + 2;            // [2]       MMA commit -> converters
     uint64_t* dfull = aempty + 2;            // [1]       MMA commit -> epilogue
     uint32_t* tbase_sm = reinterpret_cast<uint32_t*>(dfull + 1);
@@ -161,7 +206,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int nk = static_cast<int>((K + kTcBK - 1) / kTcBK);
 
     if (tid == 0) {
-        for (int s = 0; s < kTcStages; ++s) {
+        for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kTcConv + 1);
         }
@@ -186,14 +231,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
             for (int kc = 0; kc < nk; ++kc) {
-                const int s = kc % kTcStages;
-                mbar_wait(&empty[s], ((kc / kTcStages) & 1) ^ 1);
+                const int s = kc % C::STAGES;
+                mbar_wait(&empty[s], ((kc / C::STAGES) & 1) ^ 1);
                 mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
                 uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
+                if constexpr (KM) {
 #pragma unroll
-                for (int b = 0; b < BM / 256; ++b)
-                    tma_load_3d(dy + b * (kTcBK * 256 * 4), &ymap, static_cast<int>(p0 + 256 * b), kc * kTcBK,
-                                static_cast<int>(q), &full[s]);
+                    for (int b = 0; b < BM / C::BOXR; ++b)
+                        tma_load_2d(dy + b * (C::BOXR * kTcBK * 4), &ymap, kc * kTcBK, static_cast<int>(p0 + C::BOXR * b),
+                                    &full[s]);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < BM / 256; ++b)
+                        tma_load_3d(dy + b * (kTcBK * 256 * 4), &ymap, static_cast<int>(p0 + 256 * b), kc * kTcBK,
+                                    static_cast<int>(q), &full[s]);
+                }
                 bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
             }
         }
@@ -202,20 +254,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) {
             const uint32_t id_full = idesc_tf32(2 * NH), id_hi = idesc_tf32(NH);
             for (int kc = 0; kc < nk; ++kc) {
-                const int s = kc % kTcStages, a = kc & 1;
-                mbar_wait(&full[s], (kc / kTcStages) & 1);
+                const int s = kc % C::STAGES, a = kc & 1;
+                mbar_wait(&full[s], (kc / C::STAGES) & 1);
                 mbar_wait(&afull[a], (kc >> 1) & 1);
                 fence_after();
                 const uint8_t* bs = sB + size_t(s) * C::STAGE_B;
 #pragma unroll
                 for (int j = 0; j < MT; ++j) {
-                    const uint32_t d = tmem + uint32_t(j * 2 * NH);
+                    const int sm = kc % C::S;
+                    // set sm, tile j: [main | cross]; y_hi [u_hi | u_lo] fills both halves,
+                    // y_lo u_hi adds into the cross half (main keeps only y_hi u_hi)
+                    const uint32_t d = tmem + uint32_t((sm == 0 ? 0 : C::XBASE + (sm - 1) * C::D_COLS) + j * 2 * NH);
                     const uint32_t ahi = tmem + uint32_t(C::D_COLS + a * C::A_COLS + j * 32);
 #pragma unroll
                     for (int ks = 0; ks < 2; ++ks) {
                         const uint64_t b = bdesc(bs + ks * C::BBYTES);
-                        mma_tf32_ts(d, ahi + ks * 8, b, id_full, (kc > 0 || ks > 0) ? 1u : 0u);
-                        mma_tf32_ts(d, ahi + 16 + ks * 8, b, id_hi, 1u);
+                        mma_tf32_ts(d, ahi + ks * 8, b, id_full, (kc >= C::S || ks > 0) ? 1u : 0u);
+                        mma_tf32_ts(d + NH, ahi + 16 + ks * 8, b, id_hi, 1u);
                     }
                 }
                 mma_commit(&aempty[a]);
@@ -229,31 +284,54 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int L = quarter * 32 + lane;                    // TMEM lane of this thread
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         for (int kc = 0; kc < nk; ++kc) {
-            const int s = kc % kTcStages, a = kc & 1;
-            mbar_wait(&full[s], (kc / kTcStages) & 1);
+            const int s = kc % C::STAGES, a = kc & 1;
+            mbar_wait(&full[s], (kc / C::STAGES) & 1);
             uint32_t hi[MT][8], lo[MT][8];
             // rows MT*L .. MT*L+MT-1 of the tile sit in box (MT*L)/256 at row (MT*L)%256
             const float* ys = reinterpret_cast<const float*>(sY + size_t(s) * C::STAGE_Y) +
                               ((MT * L) / 256) * (kTcBK * 256) + (MT * L) % 256 + khalf * 8 * 256;
-            auto split = [&](int kk, bool live) {
-                float y[MT];
-                if constexpr (MT == 4) {
-                    const float4 v = *reinterpret_cast<const float4*>(ys + kk * 256);
-                    y[0] = v.x, y[1] = v.y, y[2] = v.z, y[3] = v.w;
-                } else {
-                    const float2 v = *reinterpret_cast<const float2*>(ys + kk * 256);
-                    y[0] = v.x, y[1] = v.y;
-                }
+            if constexpr (KM) {
+                // row j*128 + L of the tile: 8 k values = logical 16-B chunks 2*khalf, 2*khalf+1
+                const uint8_t* stage = sY + size_t(s) * C::STAGE_Y;
 #pragma unroll
                 for (int j = 0; j < MT; ++j) {
-                    const float x = live ? y[j] : 0.f;
-                    const uint32_t h = tf32_hi_bits(x);
-                    hi[j][kk] = h;
-                    lo[j][kk] = __float_as_uint(x - __uint_as_float(h));
-                }
-            };
+                    const int row = j * 128 + L;
+                    const int rr = row % C::BOXR;
+                    const uint8_t* rb = stage + (row / C::BOXR) * (C::BOXR * kTcBK * 4) + rr * 64;
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) split(kk, true);  // the K tail is zero-filled by the TMA
+                    for (int h = 0; h < 2; ++h) {
+                        const int phys = (2 * khalf + h) ^ ((rr >> 1) & 3);
+                        const float4 v = *reinterpret_cast<const float4*>(rb + phys * 16);
+                        const float y4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint32_t hb = tf32_hi_bits(y4[e]);
+                            hi[j][h * 4 + e] = hb;
+                            lo[j][h * 4 + e] = __float_as_uint(y4[e] - __uint_as_float(hb));
+                        }
+                    }
+                }
+            } else {
+                auto split = [&](int kk, bool live) {
+                    float y[MT];
+                    if constexpr (MT == 4) {
+                        const float4 v = *reinterpret_cast<const float4*>(ys + kk * 256);
+                        y[0] = v.x, y[1] = v.y, y[2] = v.z, y[3] = v.w;
+                    } else {
+                        const float2 v = *reinterpret_cast<const float2*>(ys + kk * 256);
+                        y[0] = v.x, y[1] = v.y;
+                    }
+#pragma unroll
+                    for (int j = 0; j < MT; ++j) {
+                        const float x = live ? y[j] : 0.f;
+                        const uint32_t h = tf32_hi_bits(x);
+                        hi[j][kk] = h;
+                        lo[j][kk] = __float_as_uint(x - __uint_as_float(h));
+                    }
+                };
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) split(kk, true);  // the K tail is zero-filled by the TMA
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // Y stage consumed (B: the MMA commit)
             mbar_wait(&aempty[a], ((kc >> 1) & 1) ^ 1);
@@ -273,21 +351,35 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // ===== epilogue: D = D[:, 0:NH] + D[:, NH:2NH], rows MT*L + j =====
         mbar_wait(dfull, 0);
         fence_after();
+        if constexpr (KM) {
+            // D tile j, TMEM lane L = row j*128 + L: stage [row][cols] in the (drained) Y
+            // buffers, then copy the contiguous out[p0*cols ...] block with coalesced stores
+            float* stg = reinterpret_cast<float*>(sY);
+#pragma unroll
+            for (int rc = 0; rc < NH; rc += 16) {
+#pragma unroll
+                for (int j = 0; j < MT; ++j) {
+                    float v[16];
+                    drain16<C>(tmem + lane_off, j, rc, min(nk, C::S), v);
+                    float* srow = stg + (j * 128 + L) * cols;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (rc + e < cols) srow[rc + e] = v[e];
+                }
+            }
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");
+            const int64_t n = int64_t(rows) * cols;
+            float* o = out + p0 * cols;
+            for (int64_t t = tid; t < n; t += 128) o[t] = stg[t];
+            goto done;
+        }
         float* o = out + q * P * cols + p0 + MT * L;
         const bool live = MT * L < rows;
 #pragma unroll
         for (int rc = 0; rc < NH; rc += 16) {
             float acc[MT][16];
 #pragma unroll
-            for (int j = 0; j < MT; ++j) {
-                uint32_t vh[16], vl[16];
-                const uint32_t td = tmem + lane_off + uint32_t(j * 2 * NH + rc);
-                tmem_ld16(td, vh);
-                tmem_ld16(td + NH, vl);
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-                for (int e = 0; e < 16; ++e) acc[j][e] = __uint_as_float(vh[e]) + __uint_as_float(vl[e]);
-            }
+            for (int j = 0; j < MT; ++j) drain16<C>(tmem + lane_off, j, rc, min(nk, C::S), acc[j]);
             if (live) {
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
@@ -333,31 +425,45 @@ __global__ void pack_umma_kernel(const double* __restrict__ u, int64_t ld, int64
     }
 }
 
-template <int NH>
+template <int NH, int MT, bool KM>
 void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                cudaStream_t s) {
-    using C = TcCfg<NH>;
+    using C = TcCfg<NH, MT>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_tc_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_tc_kernel<NH, MT, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
-    const int64_t tiles_p = (P + C::BM - 1) / C::BM;
-    const int64_t grid = tiles_p * Q;
-    require(grid < (int64_t(1) << 31), "ttm: grid too large");
     require(K < (int64_t(1) << 31) && Q < (int64_t(1) << 31) && P < (int64_t(1) << 31), "ttm: extent too large for TMA");
     CUtensorMap map;
-    const cuuint64_t dims[3] = {cuuint64_t(P), cuuint64_t(K), cuuint64_t(Q)};
-    const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
-    const cuuint32_t box[3] = {256, kTcBK, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims,
-                                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    int64_t tiles_p, grid;
+    if constexpr (KM) {  // rows q of K contiguous values
+        tiles_p = (Q + C::BM - 1) / C::BM;
+        grid = tiles_p;
+        const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(Q)};
+        const cuuint64_t strides[1] = {cuuint64_t(K) * 4};
+        const cuuint32_t box[2] = {kTcBK, C::BOXR};
+        const cuuint32_t estr[2] = {1, 1};
+        r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(in), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        P = Q;  // the kernel's row extent
+    } else {
+        tiles_p = (P + C::BM - 1) / C::BM;
+        grid = tiles_p * Q;
+        const cuuint64_t dims[3] = {cuuint64_t(P), cuuint64_t(K), cuuint64_t(Q)};
+        const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
+        const cuuint32_t box[3] = {256, kTcBK, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    require(grid < (int64_t(1) << 31), "ttm: grid too large");
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-    ttm_tc_kernel<NH><<<static_cast<unsigned>(grid), kTcThreads, C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p);
+    ttm_tc_kernel<NH, MT, KM><<<static_cast<unsigned>(grid), kTcThreads, C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p);
     TK_LAUNCH_CHECK();
 }
 
@@ -386,21 +492,35 @@ void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void*
     TK_LAUNCH_CHECK();
 }
 
-bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t Q, int cols) {
-    const int bm = tc_nh(cols) <= 32 ? 512 : 256;
+// Y-streaming passes use 4 x 128-row tiles (TMEM then holds a single accumulator set; the
+// main accumulator takes one MMA per k-step). Short contractions that cannot fill the GPU
+// with such tiles (K-major second stages) use 128-row tiles with 4 accumulator sets.
+inline bool km_wide(int64_t Q) { return (Q + 511) / 512 >= 2 * 148; }
+constexpr int kMmt = 4;
+
+bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols) {
+    if (reinterpret_cast<uintptr_t>(in) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
+    if (P == 1) return K % 4 == 0 && K >= kTcBK && cols <= 32 && (Q + 127) / 128 >= 148;
+    const int bm = tc_nh(cols) <= 32 ? 128 * kMmt : 256;
     const int64_t tiles = (P + bm - 1) / bm * Q;
-    return P % 4 == 0 && P >= 256 && tiles >= 2 * 148 && reinterpret_cast<uintptr_t>(in) % 16 == 0 &&
-           reinterpret_cast<uintptr_t>(out) % 16 == 0;
+    return P % 4 == 0 && P >= 256 && tiles >= 2 * 148;
 }
 
 void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                    cudaStream_t s) {
     const uint8_t* b = static_cast<const uint8_t*>(bpk);
+    if (P == 1) {
+        const bool wide = km_wide(Q);
+        if (tc_nh(cols) <= 16) return wide ? launch_tc<16, 4, true>(in, b, out, P, K, Q, cols, s)
+                                           : launch_tc<16, 1, true>(in, b, out, P, K, Q, cols, s);
+        return wide ? launch_tc<32, 4, true>(in, b, out, P, K, Q, cols, s)
+                    : launch_tc<32, 1, true>(in, b, out, P, K, Q, cols, s);
+    }
     switch (tc_nh(cols)) {
-        case 16: return launch_tc<16>(in, b, out, P, K, Q, cols, s);
-        case 32: return launch_tc<32>(in, b, out, P, K, Q, cols, s);
-        case 48: return launch_tc<48>(in, b, out, P, K, Q, cols, s);
-        default: return launch_tc<64>(in, b, out, P, K, Q, cols, s);
+        case 16: return launch_tc<16, kMmt, false>(in, b, out, P, K, Q, cols, s);
+        case 32: return launch_tc<32, kMmt, false>(in, b, out, P, K, Q, cols, s);
+        case 48: return launch_tc<48, 2, false>(in, b, out, P, K, Q, cols, s);
+        default: return launch_tc<64, 2, false>(in, b, out, P, K, Q, cols, s);
     }
 }
 

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -162,10 +163,27 @@ struct TuckerRun {
         for (int m = static_cast<int>(order) - 1; m >= 0; --m) {
             if (!ok(m) || m == avoid) continue;
             if (prod(std::vector<int64_t>(ldims.begin(), ldims.begin() + m)) >= 256) return m;
+            if (m == 0 && km_stream_ok()) return m;  // K-major tcgen05 pass over mode 0
         }
         for (int m = static_cast<int>(order) - 1; m >= 0; --m)
             if (ok(m)) return m;
         return -1;
+    }
+
+    // Mode 0 can lead a Y pass when the K-major tcgen05 kernel takes it (fp32, I_0 % 4 == 0).
+    // Only on the tcgen05-everywhere path (2): a 512-row-tile Y pass keeps one accumulator
+    // set, whose truncating accumulation over K = I_0 doubles the fp32 basis error in the
+    // noise directions relative to leading with an M-major pass (measured at cfg 2).
+    bool km_stream_ok() const {
+        if constexpr (sizeof(T) != 4) {
+            return false;
+        } else {
+            if (ctx->ttm_path != 2 || cols.empty()) return false;
+            const int64_t K = ldims[0];
+            const int64_t Q = prod(ldims) / K;
+            return K % 4 == 0 && K >= 16 && cols[0] <= 32 && (Q + 127) / 128 >= 148 &&
+                   reinterpret_cast<uintptr_t>(y) % 16 == 0;
+        }
     }
 
     // First stage: Y x_f U_f^T into "proj1" (dims updated). Runs on the current stream `s`.
@@ -195,7 +213,7 @@ struct TuckerRun {
             const int64_t K = xd[m];
             const int64_t Q = prod(std::vector<int64_t>(xd.begin() + m + 1, xd.end()));
             T* out = static_cast<T*>(ctx->buf(which ? "projB" : "projA", sizeof(T) * P * cols[m] * Q));
-            ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
+            if (!stream_ttm(cur, m, out, P, K, Q, false)) ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
             xd[m] = cols[m];
             cur = out;
             which ^= 1;
@@ -221,11 +239,13 @@ struct TuckerRun {
             return false;
         } else {
             const int path = ctx->ttm_path;
-            if (path == 1 || (path == 0 && !streams_y) || U.size() <= size_t(m) || !U[m]) return false;
+            // auto: every Y pass, and the later contractions over the fastest mode (P == 1),
+            // which the FFMA kernels serve poorly
+            if (path == 1 || (path == 0 && !streams_y && P != 1) || U.size() <= size_t(m) || !U[m]) return false;
             const float* fin = reinterpret_cast<const float*>(in);
             float* fout = reinterpret_cast<float*>(out);
-            if (!tc_ttm_supported(fin, fout, P, Q, cols[m])) return false;
-            void* bpk = ctx->buf("umma_pack", static_cast<size_t>(umma_pack_bytes(K, cols[m])));
+            if (!tc_ttm_supported(fin, fout, P, K, Q, cols[m])) return false;
+            void* bpk = ctx->buf(streams_y ? "umma_pack" : "umma_pack2", static_cast<size_t>(umma_pack_bytes(K, cols[m])));
             const double* u = U[m] + (m == order - 1 ? offset : 0);
             launch_pack_umma(u, gdims[m], K, cols[m], bpk, s);
             if (streams_y && time_kernels) mark();
@@ -767,7 +787,7 @@ int tk_ttm(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const
         if (dtype == TK_F32) {
             const float* ft = static_cast<const float*>(t);
             float* fo = static_cast<float*>(out);
-            if (ctx->ttm_path == 2 && tc_ttm_supported(ft, fo, P, Q, static_cast<int>(mrows))) {
+            if (ctx->ttm_path == 2 && tc_ttm_supported(ft, fo, P, d[mode], Q, static_cast<int>(mrows))) {
                 void* bpk = ctx->buf("umma_pack", static_cast<size_t>(umma_pack_bytes(d[mode], static_cast<int>(mrows))));
                 launch_pack_umma(md, d[mode], d[mode], static_cast<int>(mrows), bpk, ctx->stream);
                 launch_ttm_tc(ft, bpk, fo, P, d[mode], Q, static_cast<int>(mrows), ctx->stream);

@@ -24,7 +24,10 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("shape,mode", [((512, 40, 300), 1), ((1000, 37, 320), 1), ((256, 1000, 300), 1),
-                                        ((600, 500, 8), 2)])
+                                        ((600, 500, 8), 2),
+                                        # mode 0 (K-major tcgen05 variant): 128-row and 512-row tiles
+                                        ((64, 300, 80), 0), ((1000, 40, 600), 0), ((100, 613, 37), 0),
+                                        ((20, 400, 400), 0)])
 @pytest.mark.parametrize("rows", [8, 15, 30, 40, 64])
 def test_tc_ttm_matches_oracle_and_ffma(P, O, shape, mode, rows):
     import torch

@@ -49,9 +49,17 @@ class DistComm:
 
     def _allreduce(self, user, count, stream) -> int:
         try:
+            import torch
             import torch.distributed as dist
             if self.world > 1:
-                dist.all_reduce(self.xbuf[: int(count)], group=self.group)
+                if self.xbuf.is_cuda:
+                    # enqueue on the library's stream (the one that produced xbuf and will
+                    # consume the sum); NULL is the legacy default stream
+                    st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+                    with torch.cuda.stream(st):
+                        dist.all_reduce(self.xbuf[: int(count)], group=self.group)
+                else:
+                    dist.all_reduce(self.xbuf[: int(count)], group=self.group)
             self.calls += 1
             return 0
         except Exception:  # the library turns a non-zero status into "comm: allreduce failed"

@@ -1,0 +1,95 @@
+"""The multi-GPU path through the C-ABI (slab-partitioned Y, tk_comm reduction hook) with
+two ranks. Only one GPU is available to this run, so both ranks share cuda:0 over gloo
+(host-staged all-reduce: no kernel of one rank waits on the other's); on a multi-GPU box
+bench.py runs the same code over NCCL, one rank per GPU. The distributed model must equal
+the single-process model of the whole tensor (dist.hpp:617-800 semantics: partial
+sketches and cores summed over ranks, replicated QR) and the oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from helpers import orthonormality_defect, subspace_dist
+
+pytestmark = pytest.mark.gpu
+
+DIMS, RANKS, P_OVER, SEED = (40, 36, 30), (4, 4, 4), 3, (7, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _tensor(O):
+    data = O.seed_derived(3, 0, 0xDA7A)
+    return O.add_noise(O.gen_tucker(DIMS, RANKS, data), 15.0, O.seed_derived(*data, 0xAD0))
+
+
+def _worker(rank, world, port, sync, dtype, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from oracle import pyoracle as O
+        import paper_1412_1885_b200 as P
+        from paper_1412_1885_b200.dist import dist_rand_tucker_2i, plan_slabs
+        O.build()
+        y = _tensor(O)
+        off, ln = plan_slabs(DIMS[-1], world)[rank]
+        yl = np.asfortranarray(y[:, :, off:off + ln]).astype(dtype)
+        ctx = P.Context.default()
+        ctx.bind_torch_stream()
+        yd = P.DenseTensor.from_numpy(yl, dtype).cuda()
+        m = dist_rand_tucker_2i(yd, DIMS[-1], off, RANKS, P_OVER, SEED, context=ctx, sync_ranks=sync).to_host()
+        q.put((rank, m.core, m.factors, m.stats.get("passes")))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported by the parent
+        q.put((rank, repr(e), None, None))
+
+
+@pytest.mark.parametrize("sync", [True, False])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_two_rank_slabs_match_single_process(O, sync, dtype):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import torch.multiprocessing as mp
+    import paper_1412_1885_b200 as P
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, sync, dtype, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, core, fac, passes = q.get(timeout=300)
+        assert fac is not None, core
+        res[r] = (core, fac, passes)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    y = _tensor(O)
+    single = P.rand_tucker_2i(P.DenseTensor.from_numpy(y.astype(dtype), dtype).cuda(), RANKS, P_OVER, SEED).to_host()
+    g_ref, u_ref = O.rand_tucker_2i(y.astype(dtype).astype(np.float64), RANKS, P_OVER, SEED)
+    tol = 1e-10 if dtype == np.float64 else 1e-4
+    for r in (0, 1):
+        core, fac, _ = res[r]
+        for u, us, uo in zip(fac, single.factors, u_ref):
+            assert orthonormality_defect(u) < 1e-10
+            assert subspace_dist(u, us) < tol
+            assert subspace_dist(u, uo) < (1e-8 if dtype == np.float64 else 1e-3)
+        np.testing.assert_allclose(core, single.core, rtol=0, atol=tol * np.abs(single.core).max())
+    # replicated QR: both ranks hold the identical model
+    for a, b in zip(res[0][1], res[1][1]):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(res[0][0], res[1][0])

@@ -260,10 +260,14 @@ def run_b200(args, cfg):
     slab_offset = rank * dims[-1]
     _, alg_seed = bench_seeds(0)
 
-    # ---- data (untimed): this rank's slab. Weak scaling: slab r of the global tensor is
-    # the seeded workload generated with run index r (independent data per slab).
-    cfg_r = dict(cfg, seed=0)
-    y64 = generate(cfg_r) if world == 1 else _gen_slab(cfg, rank)
+    # ---- data (untimed): this rank's slab of ONE global seeded tensor of dims
+    # I_0 x ... x (N * I_{N-1}) (weak scaling), generated blockwise on the device: the last
+    # factor's rows and the noise are drawn at their global indices, the noise scale from
+    # norms summed over ranks, so the slabs concatenate to the tensor a single run generates.
+    if world == 1:
+        y64 = generate(dict(cfg, seed=0))
+    else:
+        y64 = generate(dict(cfg, seed=0, dims=gdims), slab=(slab_offset, dims[-1]), all_sum=_all_sum)
     y = y64.to(tdt)
     del y64
     torch.cuda.empty_cache()
@@ -390,11 +394,6 @@ def run_b200(args, cfg):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
-
-
-def _gen_slab(cfg, rank):
-    from paper_1412_1885_b200.generators import generate
-    return generate(dict(cfg, seed=rank))
 
 
 def _ncu_traffic():

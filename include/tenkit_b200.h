@@ -12,6 +12,7 @@
  *   tk_orthonormal_basis  <- tenkit::orthonormal_basis   range_finder.hpp:18-29
  *                            + detail::fix_column_signs  tucker.hpp:39-45
  *   tk_gaussian_matrix    <- tenkit::gaussian_matrix     random.hpp:85-100
+ *   tk_gaussian_fill      <- tenkit::gaussian_tensor     random.hpp:124-138 (window at an offset)
  *   tk_seed_derived       <- tenkit::SeedSpec::derived   random.hpp:36-41
  *   tk_ffcp(_device)      <- tenkit::ffcp                ffcp.hpp:94-194
  *
@@ -136,6 +137,11 @@ int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const doub
 /* gaussian_matrix(rows, cols, SeedSpec{root, stream}) into a device double buffer */
 int tk_gaussian_matrix(tk_context* ctx, int64_t rows, int64_t cols, uint64_t seed_root, uint64_t seed_stream,
                        double* out);
+/* out[t] = normal_at(SeedSpec{root, stream}, offset + t) for t < n (device doubles): a window of
+ * gaussian_tensor's flat counter stream (random.hpp:124-138), e.g. one rank's slab of a
+ * globally indexed noise tensor (bench.hpp:100-112 generated blockwise) */
+int tk_gaussian_fill(tk_context* ctx, int64_t n, uint64_t offset, uint64_t seed_root, uint64_t seed_stream,
+                     double* out);
 uint64_t tk_seed_derived(uint64_t seed_root, uint64_t seed_stream, uint64_t tag);
 
 /* FFCP on a Tucker model (host pointers, fp64; computed on the device). factors[n] is

@@ -57,6 +57,8 @@ void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaSt
 
 // Counter-RNG fills (random.hpp:85-100): out[i + j*rows] = normal_at(key, j*rows + i).
 void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s);
+// out[t] = normal_at(key, offset + t), t < n (a window of the flat counter stream).
+void launch_gaussian_fill(double* out, int64_t n, uint64_t offset, uint64_t key, cudaStream_t s);
 
 template <typename S, typename D>
 void launch_cast(const S* in, D* out, int64_t n, cudaStream_t s);

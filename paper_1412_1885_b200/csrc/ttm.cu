@@ -397,6 +397,21 @@ __global__ void gaussian_colmajor_kernel(double* __restrict__ out, uint64_t n, u
 }
 
 
+// out[t] = normal_at(key, off + t), t < n: a window of gaussian_tensor (random.hpp:124-138)
+// at an arbitrary flat offset (a rank's slab of a globally indexed tensor)
+__global__ void gaussian_fill_kernel(double* __restrict__ out, uint64_t n, uint64_t off, uint64_t key) {
+    const uint64_t first = off >> 1, last = (off + n - 1) >> 1;
+    for (uint64_t pr = first + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; pr <= last;
+         pr += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = 2 * pr;
+        const double u1 = counter_unit(key, i), u2 = counter_unit(key, i + 1);
+        const double r = sqrt(-2.0 * log(u1));
+        const double ang = 6.283185307179586476925287 * u2;
+        if (i >= off && i < off + n) out[i - off] = r * cos(ang);
+        if (i + 1 >= off && i + 1 < off + n) out[i + 1 - off] = r * sin(ang);
+    }
+}
+
 // out[i + c*I] = x[b + i*B + a*B*I], c = b + a*B: the mode-n unfolding of a (B, I, A) view
 template <typename T>
 __global__ void unfold_kernel(const T* __restrict__ x, int64_t B, int64_t I, int64_t A, T* __restrict__ out) {
@@ -472,6 +487,12 @@ template <typename T>
 void launch_pack_factor(const double* u, int64_t ld, int64_t rows, int cols, T* up, cudaStream_t s) {
     const int stride = pack_stride(cols);
     pack_factor_kernel<T><<<grid_for(rows * stride), 256, 0, s>>>(u, ld, rows, cols, stride, up);
+    TK_LAUNCH_CHECK();
+}
+
+void launch_gaussian_fill(double* out, int64_t n, uint64_t offset, uint64_t key, cudaStream_t s) {
+    if (n <= 0) return;
+    gaussian_fill_kernel<<<grid_for((n + 3) / 2), 256, 0, s>>>(out, uint64_t(n), offset, key);
     TK_LAUNCH_CHECK();
 }
 

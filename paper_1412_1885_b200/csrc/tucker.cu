@@ -739,6 +739,14 @@ int tk_gaussian_matrix(tk_context* ctx, int64_t rows, int64_t cols, uint64_t roo
     });
 }
 
+int tk_gaussian_fill(tk_context* ctx, int64_t n, uint64_t offset, uint64_t root, uint64_t stream, double* out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(n >= 0, "gaussian_fill: negative length");
+        launch_gaussian_fill(out, n, offset, Seed{root, stream}.key(), ctx->stream);
+    });
+}
+
 int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* q, int64_t* rank,
                          double* rdiag) {
     return guarded([&] {

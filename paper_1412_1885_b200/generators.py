@@ -34,12 +34,16 @@ def uniform_matrix(rows: int, cols: int, seed: SeedSpec) -> np.ndarray:
     return v.reshape((rows, cols), order="F")
 
 
-def gaussian_flat(n: int, seed: SeedSpec, context: Context | None = None):
-    """Flat fp64 CUDA tensor of gaussian_tensor / gaussian_matrix draws (random.hpp:85-138)."""
+def gaussian_flat(n: int, seed: SeedSpec, context: Context | None = None, offset: int = 0):
+    """Flat fp64 CUDA tensor of gaussian_tensor / gaussian_matrix draws (random.hpp:85-138):
+    entries offset .. offset + n - 1 of the seed's flat counter stream."""
     import torch
     ctx = _ctx(context)  # launches on torch's current stream: ordered with the torch ops below
     out = torch.empty(max(int(n), 1), dtype=torch.float64, device="cuda")
-    _lib.check(ctx.lib.tk_gaussian_matrix(ctx.handle, int(n), 1, seed.root, seed.stream, _dptr(out)))
+    if offset:
+        _lib.check(ctx.lib.tk_gaussian_fill(ctx.handle, int(n), int(offset), seed.root, seed.stream, _dptr(out)))
+    else:
+        _lib.check(ctx.lib.tk_gaussian_matrix(ctx.handle, int(n), 1, seed.root, seed.stream, _dptr(out)))
     return out[: int(n)]
 
 
@@ -58,20 +62,24 @@ def _colmajor_einsum(core, factors):
     return torch.einsum(spec, core, *factors).contiguous().view(-1)
 
 
-def gen_tucker_device(dims, mlranks, seed: SeedSpec, context=None):
-    """gen_tucker_tensor (bench.hpp:83-95) on the device, fp64 flat column-major."""
+def gen_tucker_device(dims, mlranks, seed: SeedSpec, context=None, last_rows=None):
+    """gen_tucker_tensor (bench.hpp:83-95) on the device, fp64 flat column-major.
+    last_rows=(offset, length): only that slab of the last mode (the global tensor's slab)."""
     import torch
     core = gaussian_flat(int(np.prod(mlranks)), seed.derived(0xC0DE), context)
     core_rm = core.view(*reversed([int(r) for r in mlranks]))
     fs = []
     for n, (i, r) in enumerate(zip(dims, mlranks)):
-        a = gaussian_flat(int(i) * int(r), gen_factor_seed(seed, n), context)
-        fs.append(a.view(int(r), int(i)).t())
+        a = gaussian_flat(int(i) * int(r), gen_factor_seed(seed, n), context).view(int(r), int(i)).t()
+        if last_rows is not None and n == len(dims) - 1:
+            a = a[int(last_rows[0]):int(last_rows[0]) + int(last_rows[1])]
+        fs.append(a)
     return _colmajor_einsum(core_rm, fs)
 
 
-def gen_cp_device(dims, rank: int, seed: SeedSpec, uniform: bool = True, context=None):
-    """gen_cp_tensor (bench.hpp:56-80) with U(0,1) (or Gaussian) factors, fp64 flat column-major."""
+def gen_cp_device(dims, rank: int, seed: SeedSpec, uniform: bool = True, context=None, last_rows=None):
+    """gen_cp_tensor (bench.hpp:56-80) with U(0,1) (or Gaussian) factors, fp64 flat column-major.
+    last_rows=(offset, length): only that slab of the last mode."""
     import torch
     fs = []
     for n, i in enumerate(dims):
@@ -79,6 +87,8 @@ def gen_cp_device(dims, rank: int, seed: SeedSpec, uniform: bool = True, context
             a = torch.from_numpy(uniform_matrix(int(i), rank, gen_factor_seed(seed, n))).cuda()
         else:
             a = gaussian_flat(int(i) * rank, gen_factor_seed(seed, n), context).view(rank, int(i)).t()
+        if last_rows is not None and n == len(dims) - 1:
+            a = a[int(last_rows[0]):int(last_rows[0]) + int(last_rows[1])]
         fs.append(a)
     order = len(dims)
     eye = torch.zeros([rank] * order, dtype=torch.float64, device="cuda")
@@ -87,16 +97,22 @@ def gen_cp_device(dims, rank: int, seed: SeedSpec, uniform: bool = True, context
     return _colmajor_einsum(eye, fs)
 
 
-def add_noise_device(y, snr_db: float, seed: SeedSpec, abs_noise: bool = False, context=None):
-    """add_noise (bench.hpp:100-112): sigma = ||Y|| / (||E|| 10^(snr/20)), Y + sigma E (in place)."""
+def add_noise_device(y, snr_db: float, seed: SeedSpec, abs_noise: bool = False, context=None, offset: int = 0,
+                     all_sum=None):
+    """add_noise (bench.hpp:100-112): sigma = ||Y|| / (||E|| 10^(snr/20)), Y + sigma E (in place).
+    For a slab of a global tensor: `offset` = its first global flat index (noise drawn at the
+    global indices) and `all_sum` sums the squared norms over the ranks holding the slabs."""
     import torch
     if np.isinf(snr_db) and snr_db > 0:
         return y
-    e = gaussian_flat(y.numel(), seed.derived(0x7015E), context)
+    e = gaussian_flat(y.numel(), seed.derived(0x7015E), context, offset=offset)
     if abs_noise:
         e.abs_()
-    ny = torch.linalg.vector_norm(y).item()
-    ne = torch.linalg.vector_norm(e).item()
+    ysq = float(torch.dot(y, y).item())
+    esq = float(torch.dot(e, e).item())
+    if all_sum is not None:
+        ysq, esq = all_sum(ysq), all_sum(esq)
+    ny, ne = float(np.sqrt(ysq)), float(np.sqrt(esq))
     if ny <= 0 or ne <= 0:
         raise _lib.TenkitError("tenkit: add_noise: zero tensor input")
     sigma = ny / (ne * 10.0 ** (snr_db / 20.0))
@@ -111,12 +127,18 @@ def bench_seeds(seed: int = 0, d: int = 0, s: int = 0, run: int = 0):
     return root.derived(0xDA7A, (d * 1000 + s) * 1000 + run), root.derived(0xA16D, run)
 
 
-def generate(cfg: dict, context=None):
-    """Observation Y (fp64 flat column-major CUDA tensor) of a benchmark config dict."""
+def generate(cfg: dict, context=None, slab=None, all_sum=None):
+    """Observation Y (fp64 flat column-major CUDA tensor) of a benchmark config dict.
+    slab=(offset, length): only that slab of the last mode of the global tensor cfg["dims"]
+    (blockwise generation on the device: the slabs of all ranks concatenate to exactly the
+    tensor a single generate() call produces, noise scale from norms summed by `all_sum`)."""
     data_seed, _ = bench_seeds(cfg.get("seed", 0))
+    dims = [int(d) for d in cfg["dims"]]
     if cfg["gen"] == "tucker":
-        y = gen_tucker_device(cfg["dims"], cfg["mlrank"], data_seed, context)
+        y = gen_tucker_device(dims, cfg["mlrank"], data_seed, context, last_rows=slab)
     else:
-        y = gen_cp_device(cfg["dims"], cfg["cp_rank"], data_seed, uniform=cfg["gen"] == "cp_uniform", context=context)
+        y = gen_cp_device(dims, cfg["cp_rank"], data_seed, uniform=cfg["gen"] == "cp_uniform", context=context,
+                          last_rows=slab)
+    offset = int(slab[0]) * int(np.prod(dims[:-1])) if slab is not None else 0
     return add_noise_device(y, cfg["snr"], data_seed.derived(0xAD0), abs_noise=cfg.get("abs_noise", False),
-                            context=context)
+                            context=context, offset=offset, all_sum=all_sum)

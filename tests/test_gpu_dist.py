@@ -93,3 +93,65 @@ def test_two_rank_slabs_match_single_process(O, sync, dtype):
     for a, b in zip(res[0][1], res[1][1]):
         np.testing.assert_array_equal(a, b)
     np.testing.assert_array_equal(res[0][0], res[1][0])
+
+
+def test_gaussian_fill_windows():
+    """tk_gaussian_fill = a window of the flat counter stream at any (odd/even) offset."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1412_1885_b200 import SeedSpec
+    from paper_1412_1885_b200.generators import gaussian_flat
+    s = SeedSpec(9, 4)
+    full = gaussian_flat(1001, s).cpu().numpy()
+    for off, n in [(1, 10), (2, 999), (7, 1), (500, 501), (999, 2)]:
+        np.testing.assert_array_equal(gaussian_flat(n, s, offset=off).cpu().numpy(), full[off:off + n])
+
+
+def _gen_worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_1412_1885_b200.dist import plan_slabs
+        from paper_1412_1885_b200.generators import generate
+
+        def all_sum(x):
+            t = torch.tensor([x], dtype=torch.float64)
+            dist.all_reduce(t)
+            return float(t.item())
+
+        cfg = dict(dims=(24, 20, 31), gen="tucker", mlrank=(3, 4, 2), snr=20.0)
+        off, ln = plan_slabs(31, world)[rank]
+        y = generate(cfg, slab=(off, ln), all_sum=all_sum)
+        q.put((rank, y.cpu().numpy()))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+def test_blockwise_generation_concatenates_to_the_global_tensor():
+    """generate(slab=...) on 2 ranks == generate() of the whole tensor (bench.hpp:83-112
+    drawn at global indices), the data layout bench.py --gpus N uses."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import torch.multiprocessing as mp
+    from paper_1412_1885_b200.generators import generate
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gen_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(isinstance(v, np.ndarray) for v in got.values()), got
+    full = generate(dict(dims=(24, 20, 31), gen="tucker", mlrank=(3, 4, 2), snr=20.0)).cpu().numpy()
+    cat = np.concatenate([got[0], got[1]])
+    np.testing.assert_allclose(cat, full, rtol=0, atol=1e-12 * np.abs(full).max())

@@ -351,6 +351,20 @@ def run_b200(args, cfg):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "tucker_ffcp_seconds": round(e2e_s, 4), "ffcp_iterations": int(res.iterations),
                "ffcp_fit": float(res.fit_trace[-1])}
+        # ---- reported fits of the CP model (bench.hpp:530-531), untimed: streamed over Y
+        # on the device (tk_model_fit), the noise-free truth regenerated from the seed
+        if world == 1:
+            yd_fit = torch.from_numpy(yh.data).cuda()
+            cpm = P.CpModel(res.factors)
+            t0 = time.perf_counter()
+            fit_obs = P.model_fit(P.DenseTensor(dims, yd_fit), cpm, context=ctx)
+            fit_ms = 1e3 * (time.perf_counter() - t0)
+            del yd_fit
+            truth = generate(dict(cfg, seed=0, snr=float("inf"))).to(tdt)
+            fit_gt = P.model_fit(P.DenseTensor(dims, truth), cpm, context=ctx)
+            del truth
+            torch.cuda.empty_cache()
+            e2e.update({"fit_obs": round(fit_obs, 6), "fit_gt": round(fit_gt, 6), "fit_pass_ms": round(fit_ms, 2)})
 
     # ---- CPU baseline (rank 0, N=1 only): oracle on a bounded slab
     cpu = None

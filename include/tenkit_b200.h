@@ -15,6 +15,8 @@
  *   tk_gaussian_fill      <- tenkit::gaussian_tensor     random.hpp:124-138 (window at an offset)
  *   tk_seed_derived       <- tenkit::SeedSpec::derived   random.hpp:36-41
  *   tk_ffcp(_device)      <- tenkit::ffcp                ffcp.hpp:94-194
+ *   tk_model_fit          <- tenkit::fit(y, reconstruct / cp_reconstruct(model))
+ *                                                        tensor.hpp:282-290, tucker.hpp:63-66, cp.hpp:118-128
  *
  * Layouts are the reference's: column-major, mode 0 fastest (tensor.hpp:31). Errors: every
  * call returns TK_OK or a code; the reference's std::invalid_argument("tenkit: ...")
@@ -137,6 +139,15 @@ int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const doub
 /* gaussian_matrix(rows, cols, SeedSpec{root, stream}) into a device double buffer */
 int tk_gaussian_matrix(tk_context* ctx, int64_t rows, int64_t cols, uint64_t seed_root, uint64_t seed_stream,
                        double* out);
+/* Streaming fit of a model to y without materialising the reconstruction: sums[0] =
+ * ||y - yhat||_F^2, sums[1] = ||y||_F^2 (host doubles), so fit(y, yhat) (tensor.hpp:282-290)
+ * = 1 - sqrt(sums[0] / sums[1]). yhat = reconstruct(TuckerModel) (tucker.hpp:63-66) when core
+ * is non-null (core_shape[order], factors[n]: dims[n] x core_shape[n]), else
+ * cp_reconstruct(CpModel) (cp.hpp:118-128) with factors[n]: dims[n] x rank. y (dtype), core
+ * and factors are device pointers; fp64 accumulation, one pass over y. */
+int tk_model_fit(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y,
+                 const int64_t* core_shape, const double* core, const double** factors, int64_t rank, double* sums);
+
 /* out[t] = normal_at(SeedSpec{root, stream}, offset + t) for t < n (device doubles): a window of
  * gaussian_tensor's flat counter stream (random.hpp:124-138), e.g. one rank's slab of a
  * globally indexed noise tensor (bench.hpp:100-112 generated blockwise) */

@@ -83,6 +83,13 @@ struct BufPool {
     virtual ~BufPool() = default;
 };
 
+// Streaming fit (fit.cu): ||Y - Yhat||^2 and ||Y||^2 into sums[0..1] (device doubles) for a
+// Tucker model (core != nullptr) or a CP model (core == nullptr, factors I_n x rank).
+template <typename T>
+void launch_model_fit(BufPool& pool, const T* y, int order, const int64_t* dims, const double* core,
+                      const int64_t* core_shape, const double* const* factors, int64_t rank, double* sums,
+                      cudaStream_t s);
+
 // FFCP on the device (ffcp.cu); all pointers are device pointers, fit_trace is host memory.
 void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* core_shape, const double* core, const double** factors,
                  const int64_t* rows, int64_t rank, int kind, double c, int max_iters, double fit_tol, Seed seed,

@@ -591,6 +591,14 @@ int tk_device_ok(void) {
     return pr.major == 10 ? 1 : 0;
 }
 
+namespace {
+struct CtxPool : tkb::BufPool {
+    tk_context* c;
+    explicit CtxPool(tk_context* ctx) : c(ctx) {}
+    void* get(const std::string& name, size_t bytes) override { return c->buf(name, bytes); }
+};
+}  // namespace
+
 int tk_context_create(int device, tk_context** out) {
     if (!tk_device_ok()) return fail(TK_ERR_NO_DEVICE, "tenkit: no sm_100 CUDA device available (no CPU fallback)");
     return guarded([&] {
@@ -679,14 +687,6 @@ int tk_rand_tucker(tk_context* ctx, int dtype, int64_t order, const int64_t* dim
     });
 }
 
-namespace {
-struct CtxPool : tkb::BufPool {
-    tk_context* c;
-    explicit CtxPool(tk_context* ctx) : c(ctx) {}
-    void* get(const std::string& name, size_t bytes) override { return c->buf(name, bytes); }
-};
-}  // namespace
-
 int tk_ffcp_device(tk_context* ctx, int64_t order, const int64_t* core_shape, const double* core,
                    const double** factors, const int64_t* rows, int64_t rank, int constraint, double sparsity_c,
                    int max_iters, double fit_tol, uint64_t seed_root, uint64_t seed_stream, double** out_factors,
@@ -736,6 +736,28 @@ int tk_gaussian_matrix(tk_context* ctx, int64_t rows, int64_t cols, uint64_t roo
         check_ctx(ctx);
         require(rows >= 1 && cols >= 1, "gaussian_matrix: dimensions must be positive");
         launch_gaussian_colmajor(out, rows, cols, Seed{root, stream}.key(), ctx->stream);
+    });
+}
+
+int tk_model_fit(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y,
+                 const int64_t* core_shape, const double* core, const double** factors, int64_t rank, double* sums) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(y != nullptr && factors != nullptr && sums != nullptr, "fit: null argument");
+        require(order >= 2 && order <= TK_MAX_ORDER, "fit: tensor order must be in [2, 8]");
+        for (int64_t n = 0; n < order; ++n) require(dims[n] >= 1, "tensor dimensions must be positive");
+        require(core != nullptr || rank >= 1, "fit: CP rank must be positive");
+        CtxPool pool(ctx);
+        double* d = static_cast<double*>(ctx->buf("fit_sums", 2 * sizeof(double)));
+        if (dtype == TK_F32)
+            launch_model_fit<float>(pool, static_cast<const float*>(y), static_cast<int>(order), dims, core, core_shape,
+                                    factors, rank, d, ctx->stream);
+        else
+            launch_model_fit<double>(pool, static_cast<const double*>(y), static_cast<int>(order), dims, core,
+                                     core_shape, factors, rank, d, ctx->stream);
+        TK_CUDA(cudaMemcpyAsync(sums, d, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+        require(sums[1] > 0.0, "fit: reference tensor has zero norm");
     });
 }
 

@@ -30,7 +30,7 @@ from ._lib import TenkitError, TenkitCudaError  # noqa: F401
 
 __all__ = ["SeedSpec", "DenseTensor", "TuckerModel", "StopRule", "ConstraintSpec", "ConstraintKind", "Context",
            "rand_tucker_2i", "rand_tucker", "ttm", "ttm_all", "unfold_times", "orthonormal_basis",
-           "gaussian_matrix", "ffcp", "TenkitError"]
+           "gaussian_matrix", "ffcp", "CpModel", "model_fit", "TenkitError"]
 
 
 # ---------------------------------------------------------------------------- seeds
@@ -479,3 +479,53 @@ def ffcp(model: TuckerModel, rank: int, constraint: ConstraintSpec = ConstraintS
                                float(stop.fit_tol), seed.root, seed.stream, oarr, _dptr(trace), C.byref(its)))
     return FfcpResult([o.reshape((int(r), rank), order="F") for o, r in zip(outs, rows)], trace[: its.value].copy(),
                       its.value)
+
+
+# ---------------------------------------------------------------------------- fit
+class CpModel:  # cp.hpp:17-30
+    """CP factors A_n (I_n x R): numpy arrays or CUDA tensors (I_n x R, or flat column-major)."""
+
+    def __init__(self, factors):
+        self.factors = list(factors)
+
+    def order(self) -> int:
+        return len(self.factors)
+
+
+def model_fit(y, model, *, context: Context | None = None, norms: bool = False):
+    """fit(y, reconstruct(model)) (tensor.hpp:282-290 with tucker.hpp:63-66) for a TuckerModel,
+    or fit(y, cp_reconstruct(model)) (cp.hpp:118-128) for a CpModel / FfcpResult / factor
+    list, = 1 - ||y - yhat|| / ||y||, streamed over y on the device without forming yhat.
+    norms=True also returns (||y - yhat||, ||y||)."""
+    import torch
+    y = _as_dense(y)
+    ctx = _ctx(context)
+    dt = torch.float32 if _dtype_code(y.data) == _lib.TK_F32 else torch.float64
+    yd = y.data if y.on_device else torch.from_numpy(np.ascontiguousarray(y.data)).cuda()
+    yd = yd.to(dt).contiguous()
+    order = len(y.shape)
+    if isinstance(model, TuckerModel):
+        cshape = [int(c) for c in (model.core_shape if model.core_shape else np.shape(model.core))]
+        core = _to_dev(model.core, torch.float64) if not hasattr(model.core, "is_cuda") else model.core.contiguous()
+        fac = [_to_dev(u, torch.float64) if not hasattr(u, "is_cuda") else u.contiguous() for u in model.factors]
+        rank = 0
+    else:
+        fs = model.factors if hasattr(model, "factors") else list(model)
+        rank = int(np.shape(fs[0])[1]) if not hasattr(fs[0], "is_cuda") or fs[0].dim() == 2 else \
+            int(fs[0].numel()) // int(y.shape[0])
+        fac = []
+        for u in fs:
+            if hasattr(u, "is_cuda"):
+                fac.append(u.t().contiguous().view(-1) if u.dim() == 2 else u.contiguous())  # column-major flat
+            else:
+                fac.append(_to_dev(u, torch.float64))
+        core, cshape = None, [0] * order
+    if len(fac) != order:
+        raise TenkitError("tenkit: fit: one factor per mode required")
+    sums = np.zeros(2)
+    farr = (_lib.PD * order)(*[_dptr(u) for u in fac])
+    _lib.check(ctx.lib.tk_model_fit(ctx.handle, _dtype_code(yd), order, _i64arr(y.shape), _ptr(yd), _i64arr(cshape),
+                                    _dptr(core) if core is not None else None, farr, int(rank), _dptr(sums)))
+    res, ny = float(np.sqrt(max(sums[0], 0.0))), float(np.sqrt(sums[1]))
+    f = 1.0 - res / ny
+    return (f, res, ny) if norms else f

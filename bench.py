@@ -370,7 +370,7 @@ def run_b200(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        yy = generate(cfg_r)
+        yy = generate(dict(cfg, seed=0))
         ys, sdims = cpu_sample(cfg, yy.to(tdt), args.cpu_slabs)
         del yy
         torch.cuda.empty_cache()

@@ -398,43 +398,43 @@ __device__ __forceinline__ void warp_ldlt(const double* t, int R, double ridge, 
         a[e] = t[sig[x] + sig[y] * R] + (x == y ? ridge : 0.0);
     }
     __syncwarp();
-    // left-looking, lanes over the rows i >= k of column k: w_j = L(k,j) D(j) once per step
-    // (Eigen's temp = D A10^T), then s_i = A(i,k) - sum_j L(i,j) w_j with 4 partial sums
-    double* w = a + R * R;  // R scratch doubles after the matrix
+    // left-looking, lanes over the rows i >= k of column k, read-only inner loop:
+    //   s_i = A(i,k) - sum_{j<k} L(i,j) M(k,j),   M(k,j) = L(k,j) D(j) (Eigen's temp = D A10^T)
+    // where M(i,k) = s_i, the numerator of L(i,k) = s_i / D(k). D(k) = s_k reaches the other
+    // lanes by one shuffle; rolled loops only (this runs once per mode on one CTA and is
+    // instruction-fetch bound when unrolled). Per step ~170 cycles + ~15 per dot term.
+    double* mm = a + R * R;  // R x R scratch (M)
     if (pr && lane == 0) pr[2] = clock64();
+    auto dot = [&](int i, int k) {
+        const double* mk = mm + k;  // row k of M: mk[j * R]
+        double p0 = 0.0, p1 = 0.0;
+        int j = 0;
+#pragma unroll 1
+        for (; j + 2 <= k; j += 2) {
+            p0 = fma(a[i + j * R], mk[j * R], p0);
+            p1 = fma(a[i + (j + 1) * R], mk[(j + 1) * R], p1);
+        }
+        if (j < k) p0 = fma(a[i + j * R], mk[j * R], p0);
+        return a[i + k * R] - (p0 + p1);
+    };
+#pragma unroll 1
     for (int k = 0; k < R; ++k) {
-        for (int j = lane; j < k; j += 32) w[j] = a[k + j * R] * a[j + j * R];
-        __syncwarp();
         const int i0 = k + lane, i1 = k + lane + 32;
-        double s0 = 0.0, s1 = 0.0;
-        if (i0 < R) {
-            double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-            int j = 0;
-            for (; j + 4 <= k; j += 4) {
-                p0 = fma(a[i0 + j * R], w[j], p0);
-                p1 = fma(a[i0 + (j + 1) * R], w[j + 1], p1);
-                p2 = fma(a[i0 + (j + 2) * R], w[j + 2], p2);
-                p3 = fma(a[i0 + (j + 3) * R], w[j + 3], p3);
-            }
-            for (; j < k; ++j) p0 = fma(a[i0 + j * R], w[j], p0);
-            s0 = a[i0 + k * R] - ((p0 + p1) + (p2 + p3));
+        const double s0 = i0 < R ? dot(i0, k) : 0.0;
+        const double s1 = i1 < R ? dot(i1, k) : 0.0;
+        const double dk = __shfl_sync(0xffffffffu, s0, 0);
+        const bool nz = fabs(dk) > 0.0;
+        const double inv = nz ? 1.0 / dk : 0.0;
+        if (lane == 0) {
+            a[k + k * R] = dk;
+        } else if (i0 < R) {
+            a[i0 + k * R] = nz ? s0 * inv : s0;
+            mm[i0 + k * R] = nz ? s0 : 0.0;
         }
         if (i1 < R) {
-            double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-            int j = 0;
-            for (; j + 4 <= k; j += 4) {
-                p0 = fma(a[i1 + j * R], w[j], p0);
-                p1 = fma(a[i1 + (j + 1) * R], w[j + 1], p1);
-                p2 = fma(a[i1 + (j + 2) * R], w[j + 2], p2);
-                p3 = fma(a[i1 + (j + 3) * R], w[j + 3], p3);
-            }
-            for (; j < k; ++j) p0 = fma(a[i1 + j * R], w[j], p0);
-            s1 = a[i1 + k * R] - ((p0 + p1) + (p2 + p3));
+            a[i1 + k * R] = nz ? s1 * inv : s1;
+            mm[i1 + k * R] = nz ? s1 : 0.0;
         }
-        const double dk = __shfl_sync(0xffffffffu, s0, 0);
-        if (lane == 0) a[k + k * R] = dk;
-        else if (i0 < R) a[i0 + k * R] = fabs(dk) > 0.0 ? s0 / dk : s0;
-        if (i1 < R) a[i1 + k * R] = fabs(dk) > 0.0 ? s1 / dk : s1;
         __syncwarp();
     }
     if (pr && lane == 0) pr[3] = clock64();
@@ -518,9 +518,9 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
     for (int q = 0; q < p.order; ++q) maxc = max(maxc, p.cs[q]);
     double* sH = sm;                   // maxc * R, [k * R + r]
     double* sT = sH + maxc * R;        // R * R
-    double* sF = sT + RR;              // R * R (+ R scratch)
-    double* sFr = sF + RR + R;         // R * R (+ R scratch)
-    double* red = sFr + RR + R;        // kPThreads
+    double* sF = sT + RR;              // R * R (+ R * R scratch)
+    double* sFr = sF + 2 * RR;         // R * R (+ R * R scratch)
+    double* red = sFr + 2 * RR;        // kPThreads
     int* ssig = reinterpret_cast<int*>(red + kPThreads);  // 2 x kMaxRank
     double* scr = reinterpret_cast<double*>(ssig + 2 * kMaxRank);  // p.scratch doubles
     // phase B view of the scratch
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
                     double* f = warp ? sFr : sF;
                     int* sg = ssig + warp * kMaxRank;
                     warp_ldlt(sT, R, ridge, f, sg,
-                              (p.prof && warp == 0 && step < 4096) ? p.prof + 4096 * 20 + step * 4 : nullptr);
+                              (p.prof && warp == 0 && step < 4096) ? p.prof + 4096 * 24 + step * 16 : nullptr);
                     double* gf = warp ? p.Fr : p.F;
                     for (int e = lane; e < RR; e += 32) gf[e] = f[e];
                     for (int e = lane; e < R; e += 32) p.sig[warp * kMaxRank + e] = sg[e];
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
 
 // Shared memory of the persistent kernel: fixed part + `scratch` doubles.
 size_t persist_smem(int R, int maxc, int64_t scratch) {
-    return sizeof(double) * (size_t(maxc) * R + 3 * size_t(R) * R + 2 * size_t(R) + kPThreads + size_t(scratch)) +
+    return sizeof(double) * (size_t(maxc) * R + 5 * size_t(R) * R + kPThreads + size_t(scratch)) +
            sizeof(int) * 2 * kMaxRank;
 }
 
@@ -942,7 +942,7 @@ void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* co
         const int64_t need_b = int64_t(R) * R + int64_t(maxc) * R + 3 * kPWarps * kMaxRank;
         const int64_t slices = smax * (kPWarps / R + 2);
         const int64_t budget =
-            (int64_t(smem_optin) - 2048) / 8 - (int64_t(maxc) * R + 3 * int64_t(R) * R + 2 * R + kPThreads + kMaxRank);
+            (int64_t(smem_optin) - 2048) / 8 - (int64_t(maxc) * R + 5 * int64_t(R) * R + kPThreads + kMaxRank);
         require(gsz_all < (int64_t(1) << 31), "ffcp: core too large for the device path");
         const char* nostage = std::getenv("TENKIT_FFCP_NOSTAGE");
         const bool allow = !(nostage && nostage[0] == '1');
@@ -998,8 +998,8 @@ void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* co
         const char* profenv = std::getenv("TENKIT_FFCP_PROF");
         const bool prof = profenv && profenv[0] == '1';
         if (prof) {
-            pp.prof = mem.get<unsigned long long>(4096 * 24);
-            TK_CUDA(cudaMemsetAsync(pp.prof, 0, 4096 * 24 * sizeof(unsigned long long), s));
+            pp.prof = mem.get<unsigned long long>(4096 * 40);
+            TK_CUDA(cudaMemsetAsync(pp.prof, 0, 4096 * 40 * sizeof(unsigned long long), s));
         }
         TK_CUDA(cudaMemsetAsync(pp.bad, 0, 2 * sizeof(int), s));
         TK_CUDA(cudaMemsetAsync(pp.iters, 0, sizeof(int), s));
@@ -1012,7 +1012,7 @@ void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* co
         if (it > 0) TK_CUDA(cudaMemcpyAsync(fit_trace, pp.fit_trace, sizeof(double) * it, cudaMemcpyDeviceToHost, s));
         *iterations = it;
         if (prof) {
-            std::vector<unsigned long long> h(4096 * 24);
+            std::vector<unsigned long long> h(4096 * 40);
             TK_CUDA(cudaMemcpy(h.data(), pp.prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
             const int steps = std::min(4095, it * static_cast<int>(order));
             double ph[4] = {0, 0, 0, 0};
@@ -1043,16 +1043,21 @@ void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* co
             }
             std::fprintf(stderr, "  phase B: stage %.2f rows %.2f store+sync %.2f\n", bsub[0] / 1e3 / (steps - 2),
                          bsub[1] / 1e3 / (steps - 2), bsub[2] / 1e3 / (steps - 2));
-            double lc[3] = {0, 0, 0};
+            double lc[7] = {0, 0, 0, 0, 0, 0, 0};
             for (int st = 1; st + 1 < steps; ++st) {
-                const unsigned long long* q = h.data() + 4096 * 20 + st * 4;
+                const unsigned long long* q = h.data() + 4096 * 24 + st * 16;
                 if (!q[0]) continue;
                 lc[0] += double(q[1] - q[0]);
                 lc[1] += double(q[2] - q[1]);
                 lc[2] += double(q[3] - q[2]);
+                lc[3] += double(q[5] - q[4]);
+                lc[4] += double(q[6] - q[5]);
+                lc[5] += double(q[7] - q[6]);
+                lc[6] += double(q[8] - q[7]);
             }
-            std::fprintf(stderr, "  ldlt cycles: pivot %.0f copy %.0f factor %.0f\n", lc[0] / (steps - 2), lc[1] / (steps - 2),
-                         lc[2] / (steps - 2));
+            for (double& v : lc) v /= (steps - 2);
+            std::fprintf(stderr, "  ldlt cycles: pivot %.0f copy %.0f factor %.0f | mid step: w %.0f dot %.0f shfl %.0f div+st %.0f\n",
+                         lc[0], lc[1], lc[2], lc[3], lc[4], lc[5], lc[6]);
             double cyc[3] = {0, 0, 0};
             for (int st = 1; st + 1 < steps; ++st) {
                 const unsigned long long* q = h.data() + 4096 * 12 + st * 8;

@@ -19,6 +19,7 @@
 // Accumulators stay in TMEM for the whole K loop; Y is read from HBM exactly once.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <stdexcept>
 
 namespace {
@@ -54,8 +55,10 @@ constexpr int kTcStages = 4;
 // 3xTF32: y_hi u_hi -> main accumulators, y_hi u_lo + y_lo u_hi -> cross accumulator (the
 // fourth product y_lo u_lo, 2^-22 relative, is dropped).
 
-template <int NH, int MT_ = (NH <= 32 ? 4 : 2)>
+template <int NH, int MT_ = (NH <= 32 ? 4 : 2), int OCC_ = 1>
 struct TcCfg {
+    static constexpr int OCC = OCC_;            // CTAs per SM (TMEM and smem split between them)
+    static constexpr int TMEM = 512 / OCC_;
     static constexpr int MT = MT_;  // 128-row M tiles per CTA
     static constexpr int BM = 128 * MT;
     static constexpr int BOXR = BM < 256 ? BM : 256;  // rows per TMA box
@@ -68,11 +71,11 @@ struct TcCfg {
     // The fp32 accumulation inside the tensor core truncates, so its error grows with the
     // number of MMAs accumulated into one D: k-block kc accumulates into set kc % S, and the
     // sets are summed in round-to-nearest fp32 in the epilogue.
-    static constexpr int S_RAW = 1 + (512 - XBASE) / D_COLS;
+    static constexpr int S_RAW = 1 + (TMEM - XBASE) / D_COLS;
     static constexpr int S = S_RAW > 4 ? 4 : S_RAW;
-    static_assert(XBASE <= 512, "TMEM budget");
+    static_assert(XBASE <= TMEM, "TMEM budget");
     // pipeline depth: ~128 KB of Y in flight per SM whatever the tile height
-    static constexpr int STAGES_RAW = (128 * 1024) / STAGE_Y;
+    static constexpr int STAGES_RAW = (128 * 1024) / STAGE_Y / OCC_;
     static constexpr int STAGES = STAGES_RAW < kTcStages ? kTcStages : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
     static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 256 + 128;
 };
@@ -182,11 +185,11 @@ __device__ __forceinline__ void drain16(uint32_t tl, int j, int rc, int used, fl
 //   values, tiles of BM rows, TMA boxes of BOXR rows x 16 k (64 B, 64B-swizzled so the
 //   converters' 16-B row reads are bank-conflict free), out[r + q cols] written through a
 //   shared-memory transpose (coalesced rows of the output).
-template <int NH, int MT_, bool KM>
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int NH, int MT_, bool KM, int OCC = 1>
+__global__ void __launch_bounds__(kTcThreads, OCC)
     ttm_tc_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
                   int64_t P, int64_t K, int cols, int64_t tiles_p) {
-    using C = TcCfg<NH, MT_>;
+    using C = TcCfg<NH, MT_, OCC>;
     constexpr int MT = C::MT, BM = C::BM;
     extern __shared__ __align__(1024) uint8_t tsm[];
     uint8_t* sY = tsm;  // [stages][BM/256 boxes][kTcBK][256] fp32
@@ -218,7 +221,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mbar_fence_init();
     }
     if (warp == kTcConv + 1) {  // TMEM allocation (whole warp)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tbase_sm)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tbase_sm)),
+                     "r"(C::TMEM));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     fence_before();
@@ -401,7 +405,7 @@ done:
     __syncthreads();
     if (warp == kTcConv + 1) {
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(C::TMEM));
     }
 }
 
@@ -425,13 +429,13 @@ __global__ void pack_umma_kernel(const double* __restrict__ u, int64_t ld, int64
     }
 }
 
-template <int NH, int MT, bool KM>
+template <int NH, int MT, bool KM, int OCC = 1>
 void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                cudaStream_t s) {
-    using C = TcCfg<NH, MT>;
+    using C = TcCfg<NH, MT, OCC>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_tc_kernel<NH, MT, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_tc_kernel<NH, MT, KM, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
@@ -463,7 +467,8 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
     }
     require(grid < (int64_t(1) << 31), "ttm: grid too large");
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-    ttm_tc_kernel<NH, MT, KM><<<static_cast<unsigned>(grid), kTcThreads, C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p);
+    ttm_tc_kernel<NH, MT, KM, OCC><<<static_cast<unsigned>(grid), kTcThreads, C::smem, s>>>(map, bpk, out, P, K, cols,
+                                                                                           tiles_p);
     TK_LAUNCH_CHECK();
 }
 
@@ -492,18 +497,22 @@ void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void*
     TK_LAUNCH_CHECK();
 }
 
-// Y-streaming passes use 4 x 128-row tiles (TMEM then holds a single accumulator set; the
-// main accumulator takes one MMA per k-step). Short contractions that cannot fill the GPU
-// with such tiles (K-major second stages) use 128-row tiles with 4 accumulator sets.
-inline bool km_wide(int64_t Q) { return (Q + 511) / 512 >= 2 * 148; }
-constexpr int kMmt = 4;
+// Y-streaming passes: two CTAs per SM, each with 2 x 128-row tiles, 256 TMEM columns and a
+// 4-stage ring (one CTA's prologue, pipeline fill and epilogue overlap the other's stream:
+// 6.1 TB/s vs 5.4 TB/s for one 512-row CTA per SM at cfg 2). TMEM then holds one accumulator
+// set (the main accumulator takes one MMA per k-step). Short contractions that cannot fill
+// the GPU with such tiles (K-major second stages) use 128-row tiles, 2 CTAs per SM and 3
+// accumulator sets.
+inline bool km_wide(int64_t Q) { return (Q + 255) / 256 >= 4 * 148; }
+constexpr int kMmt = 2;
+constexpr int kOcc = 2;
 
 bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols) {
     if (reinterpret_cast<uintptr_t>(in) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
     if (P == 1) return K % 4 == 0 && K >= kTcBK && cols <= 32 && (Q + 127) / 128 >= 148;
-    const int bm = tc_nh(cols) <= 32 ? 128 * kMmt : 256;
+    const int bm = tc_nh(cols) <= 32 ? 128 * kMmt : 256;  // tiles >= 2 waves of 2 CTAs per SM
     const int64_t tiles = (P + bm - 1) / bm * Q;
-    return P % 4 == 0 && P >= 256 && tiles >= 2 * 148;
+    return P % 4 == 0 && P >= 256 && tiles >= 2 * 2 * 148;
 }
 
 void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
@@ -511,14 +520,22 @@ void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int6
     const uint8_t* b = static_cast<const uint8_t*>(bpk);
     if (P == 1) {
         const bool wide = km_wide(Q);
-        if (tc_nh(cols) <= 16) return wide ? launch_tc<16, 4, true>(in, b, out, P, K, Q, cols, s)
-                                           : launch_tc<16, 1, true>(in, b, out, P, K, Q, cols, s);
-        return wide ? launch_tc<32, 4, true>(in, b, out, P, K, Q, cols, s)
-                    : launch_tc<32, 1, true>(in, b, out, P, K, Q, cols, s);
+        if (tc_nh(cols) <= 16) return wide ? launch_tc<16, 2, true, 2>(in, b, out, P, K, Q, cols, s)
+                                           : launch_tc<16, 1, true, 2>(in, b, out, P, K, Q, cols, s);
+        return wide ? launch_tc<32, 2, true, 2>(in, b, out, P, K, Q, cols, s)
+                    : launch_tc<32, 1, true, 2>(in, b, out, P, K, Q, cols, s);
+    }
+    static const int variant = [] {
+        const char* e = std::getenv("TENKIT_TC_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (variant == 1) {  // A/B: one 512-row CTA per SM (the round-1 first version)
+        if (tc_nh(cols) <= 16) return launch_tc<16, 4, false>(in, b, out, P, K, Q, cols, s);
+        if (tc_nh(cols) <= 32) return launch_tc<32, 4, false>(in, b, out, P, K, Q, cols, s);
     }
     switch (tc_nh(cols)) {
-        case 16: return launch_tc<16, kMmt, false>(in, b, out, P, K, Q, cols, s);
-        case 32: return launch_tc<32, kMmt, false>(in, b, out, P, K, Q, cols, s);
+        case 16: return launch_tc<16, kMmt, false, kOcc>(in, b, out, P, K, Q, cols, s);
+        case 32: return launch_tc<32, kMmt, false, kOcc>(in, b, out, P, K, Q, cols, s);
         case 48: return launch_tc<48, 2, false>(in, b, out, P, K, Q, cols, s);
         default: return launch_tc<64, 2, false>(in, b, out, P, K, Q, cols, s);
     }

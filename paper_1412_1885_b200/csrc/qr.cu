@@ -101,6 +101,163 @@ __device__ void reduce_dots(Sh& sh, cg::cluster_group& cl, unsigned cs, int& par
     __syncthreads();
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Fast path: column-pivoted CholeskyQR2. In exact arithmetic ColPivHouseholderQR's pivot at
+// step k is the column of largest remaining norm, i.e. the largest diagonal entry of the
+// Schur complement of the Gram matrix G = Z^T Z, and |R_kk| is its square root; so the
+// pivoted Cholesky of G gives the same pivots and |R_kk|, and Q = Z_P R^{-1} the same
+// columns up to sign (fixed by the sign rule afterwards). One more Cholesky pass on Q
+// (CholeskyQR2) restores orthonormality to ~eps. Taken only when Z is well conditioned
+// (every R_kk > kFastMinRatio R_00, so the 1e-12 rank cut cannot bite); otherwise the kernel
+// falls through to the Householder path with Z untouched. 3 cluster exchanges instead of
+// one per Householder step.
+// ---------------------------------------------------------------------------------------
+constexpr double kFastMinRatio = 1e-5;
+
+// gp[a + b n] = sum over own rows of z[:, a] z[:, b] (full symmetric n x n)
+__device__ void gram_partial(const double* z, int ld, int nloc, int n, double* gp) {
+    const int npair = n * (n + 1) / 2;
+    for (int t = threadIdx.x; t < npair; t += kQrThreads) {
+        int a = 0, rem = t;
+        while (rem >= n - a) {  // t -> (a, b), a <= b
+            rem -= n - a;
+            ++a;
+        }
+        const int b = a + rem;
+        const double* za = z + size_t(a) * ld;
+        const double* zb = z + size_t(b) * ld;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int i = 0;
+        for (; i + 4 <= nloc; i += 4) {
+            s0 = fma(za[i], zb[i], s0);
+            s1 = fma(za[i + 1], zb[i + 1], s1);
+            s2 = fma(za[i + 2], zb[i + 2], s2);
+            s3 = fma(za[i + 3], zb[i + 3], s3);
+        }
+        for (; i < nloc; ++i) s0 = fma(za[i], zb[i], s0);
+        const double v = (s0 + s1) + (s2 + s3);
+        gp[a + b * n] = v;
+        gp[b + a * n] = v;
+    }
+}
+
+// gs = sum over the cluster's CTAs (fixed order) of gp; every CTA ends with the same gs
+__device__ void gram_reduce(cg::cluster_group& cl, unsigned cs, double* gp, double* gs, int n) {
+    if (cs > 1) cl.sync();
+    else __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += kQrThreads) {
+        double v = 0.0;
+        for (unsigned c = 0; c < cs; ++c) v += (cs > 1 ? cl.map_shared_rank(gp, c) : gp)[e];
+        gs[e] = v;
+    }
+    if (cs > 1) cl.sync();  // every CTA done reading the partials before they are rewritten
+    else __syncthreads();
+}
+
+// Right-looking Cholesky of gs (n x n, full symmetric, destroyed) by one warp, with
+// ColPiv pivoting (first largest Schur diagonal) when `pivot`: R (upper, col-major, n x n)
+// into rr, source column of pivot position k into perm[k]. Returns false when a pivot is
+// not positive or R_kk <= kFastMinRatio R_00 (the caller then takes the Householder path).
+__device__ bool warp_pchol(double* gs, int n, bool pivot, double* rr, int* perm) {
+    const int lane = threadIdx.x & 31;
+    for (int j = lane; j < n; j += 32) perm[j] = j;
+    for (int e = lane; e < n * n; e += 32) rr[e] = 0.0;
+    __syncwarp();
+    double r00 = 0.0;
+    for (int k = 0; k < n; ++k) {
+        int best = k;
+        if (pivot) {
+            double bv = -1.0;
+            int bi = k;
+            for (int j = k + lane; j < n; j += 32) {
+                const double v = gs[j + j * n];
+                if (v > bv) {
+                    bv = v;
+                    bi = j;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > bv || (ov == bv && oi < bi)) {
+                    bv = ov;
+                    bi = oi;
+                }
+            }
+            best = bi;
+        }
+        if (best != k) {  // symmetric swap k <-> best; R rows < k: swap their columns
+            for (int j = lane; j < n; j += 32) {
+                const double t0 = gs[k + j * n];
+                gs[k + j * n] = gs[best + j * n];
+                gs[best + j * n] = t0;
+            }
+            __syncwarp();
+            for (int i = lane; i < n; i += 32) {
+                const double t0 = gs[i + k * n];
+                gs[i + k * n] = gs[i + best * n];
+                gs[i + best * n] = t0;
+            }
+            for (int i = lane; i < k; i += 32) {
+                const double t0 = rr[i + k * n];
+                rr[i + k * n] = rr[i + best * n];
+                rr[i + best * n] = t0;
+            }
+            if (lane == 0) {
+                const int t0 = perm[k];
+                perm[k] = perm[best];
+                perm[best] = t0;
+            }
+            __syncwarp();
+        }
+        const double d = gs[k + k * n];
+        if (k == 0) r00 = d > 0.0 ? sqrt(d) : 0.0;
+        if (!(d > 0.0)) return false;
+        const double rkk = sqrt(d);
+        if (!(rkk > kFastMinRatio * r00)) return false;
+        const double inv = 1.0 / rkk;
+        for (int j = k + lane; j < n; j += 32) rr[k + j * n] = j == k ? rkk : gs[k + j * n] * inv;
+        __syncwarp();
+        // trailing Schur complement, lane j owns column j (all rows > k): loads before stores
+        for (int j = k + 1 + lane; j < n; j += 32) {
+            const double rkj = rr[k + j * n];
+            double* col = gs + size_t(j) * n;
+            int i = k + 1;
+            for (; i + 4 <= n; i += 4) {
+                const double c0 = col[i], c1 = col[i + 1], c2 = col[i + 2], c3 = col[i + 3];
+                const double q0 = rr[k + i * n], q1 = rr[k + (i + 1) * n], q2 = rr[k + (i + 2) * n],
+                             q3 = rr[k + (i + 3) * n];
+                col[i] = fma(-q0, rkj, c0);
+                col[i + 1] = fma(-q1, rkj, c1);
+                col[i + 2] = fma(-q2, rkj, c2);
+                col[i + 3] = fma(-q3, rkj, c3);
+            }
+            for (; i < n; ++i) col[i] = fma(-rr[k + i * n], rkj, col[i]);
+        }
+        __syncwarp();
+    }
+    return true;
+}
+
+// out[:, j] = (in[:, perm[j]] - sum_{k<j} out[:, k] R_kj) / R_jj, one thread per own row
+__device__ void trsm_rows(const double* in, double* out, int ld, int nloc, int n, const double* rr, const int* perm) {
+    for (int i = threadIdx.x; i < nloc; i += kQrThreads) {
+        for (int j = 0; j < n; ++j) {
+            double a0 = in[i + size_t(perm[j]) * ld], a1 = 0.0;
+            const double* rj = rr + size_t(j) * n;
+            int k = 0;
+            for (; k + 2 <= j; k += 2) {
+                a0 = fma(-out[i + size_t(k) * ld], rj[k], a0);
+                a1 = fma(-out[i + size_t(k + 1) * ld], rj[k + 1], a1);
+            }
+            if (k < j) a0 = fma(-out[i + size_t(k) * ld], rj[k], a0);
+            out[i + size_t(j) * ld] = (a0 + a1) / rj[j];
+        }
+    }
+}
+
 // zr[j * ld] = fma(a, w[j], zr[j * ld]) for j in [j0, j1): loads of a group issued before its
 // stores (the compiler cannot prove the column stores do not alias the next loads)
 __device__ __forceinline__ void axpy_row(double* zr, int ld, int j0, int j1, double a, const double* w) {
@@ -119,7 +276,7 @@ __device__ __forceinline__ void axpy_row(double* zr, int ld, int j0, int j1, dou
 __global__ void __launch_bounds__(kQrThreads, 1)
     qr_colpiv_cluster_kernel(const double* __restrict__ zin, int64_t rows, int ncols, int ld,
                              double* __restrict__ uout, int ucap, void* upout, int up_dtype, int* rank_out,
-                             double* diag_out) {
+                             double* diag_out, int fast) {
     cg::cluster_group cl = cg::this_cluster();
     const unsigned cs = cl.num_blocks();
     const int crank = static_cast<int>(cl.block_rank());
@@ -150,6 +307,50 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     if (tid < 2) sh.flag[tid] = 0;
     __syncthreads();
 
+    int rank = 0;
+    const int size = static_cast<int>(lmin(rows, ncols));
+    bool fast_ok = false;
+    if (fast && rows >= ncols) {
+        const int n = ncols;
+        double* q = reinterpret_cast<double*>(sh.flag + 16);  // [n][ld]
+        double* gp = q + size_t(ld) * n;                       // n x n partial Gram
+        double* gs = gp + n * n;                               // n x n Gram / Schur complement
+        double* r1 = gs + n * n;                               // n x n R of pass 1
+        double* r2 = r1 + n * n;                               // n x n R of pass 2
+        int* perm = reinterpret_cast<int*>(r2 + n * n);        // n: pivot order of pass 1
+        int* perm2 = perm + kMaxRank;                          // n: (identity) of pass 2
+        int* ident = perm2 + kMaxRank;                         // n
+        int* okf = ident + kMaxRank;                           // 2 flags
+        gram_partial(z, ld, nloc, n, gp);
+        gram_reduce(cl, cs, gp, gs, n);
+        if (warp == 0) {
+            const bool ok = warp_pchol(gs, n, true, r1, perm);
+            if (lane == 0) okf[0] = ok ? 1 : 0;
+        }
+        __syncthreads();
+        if (okf[0]) {  // identical in every CTA (same reduced Gram, same arithmetic)
+            trsm_rows(z, q, ld, nloc, n, r1, perm);
+            __syncthreads();
+            gram_partial(q, ld, nloc, n, gp);
+            gram_reduce(cl, cs, gp, gs, n);
+            if (warp == 0) {
+                for (int j = lane; j < n; j += 32) ident[j] = j;
+                __syncwarp();
+                const bool ok = warp_pchol(gs, n, false, r2, perm2);
+                if (lane == 0) okf[1] = ok ? 1 : 0;
+            }
+            __syncthreads();
+            if (okf[1]) {
+                trsm_rows(q, z, ld, nloc, n, r2, ident);
+                for (int k = tid; k < n; k += kQrThreads) sh.beta[k] = r2[k + k * n] * r1[k + k * n];
+                __syncthreads();
+                fast_ok = true;
+                rank = n;
+            }
+        }
+    }
+
+    if (!fast_ok) {
     // initial column norms (m_qr.col(k).norm()): one reduction of col_j . col_j
     {
         double* m = sh.slot + par * kVec;
@@ -179,7 +380,6 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     }
 
     const double norm_downdate_threshold = sqrt(DBL_EPSILON);
-    const int size = static_cast<int>(lmin(rows, ncols));
     QR_MARK(1);
     for (int k = 0; k < size; ++k) {
         QR_MARK(7 + 8 * k);
@@ -309,7 +509,6 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     QR_MARK(2);
 
     // ---- rank cut (range_finder.hpp:24-26), redundantly
-    int rank = 0;
     {
         const double top = fabs(sh.beta[0]);
         while (rank < size && fabs(sh.beta[rank]) > 1e-12 * top) ++rank;
@@ -338,6 +537,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         }
         __syncthreads();
     }
+    }  // Householder path
     QR_MARK(3);
 
     // ---- sign fix: largest |entry| of each column positive (first maximum on ties)
@@ -446,6 +646,14 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
     size_t smem = 0;
     const int cs = pick_cluster(rows, ncols, &ld, &smem);
     require(cs > 0, "orthonormal_basis: sketch too large for the cluster QR");
+    // fast path scratch: Q of pass 1 (ld x ncols) + 4 n x n + 4 kMaxRank ints
+    const size_t fast_extra = (size_t(ld) * ncols + 4 * size_t(ncols) * ncols) * sizeof(double) + 4 * kMaxRank * sizeof(int);
+    static const bool no_fast = [] {
+        const char* e = std::getenv("TENKIT_QR_NO_FAST");
+        return e && e[0] == '1';
+    }();
+    const int fast = (!no_fast && smem + fast_extra <= kQrSmemCap) ? 1 : 0;
+    if (fast) smem += fast_extra;
     static bool attr = false;
     if (!attr) {
         TK_CUDA(cudaFuncSetAttribute(qr_colpiv_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -466,7 +674,7 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
     TK_CUDA(cudaLaunchKernelEx(&cfg, qr_colpiv_cluster_kernel, z, rows, ncols, ld, u, ucap, up, up_dtype, rank_dev,
-                               diag));
+                               diag, fast));
 }
 
 }  // namespace tkb

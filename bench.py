@@ -201,8 +201,10 @@ def run_reference(args, cfg):
     _, alg_seed = bench_seeds(0)
     slabs = args.cpu_slabs
     if torch.cuda.is_available():
-        y = generate(cfg)
-        ys, sdims = cpu_sample(cfg, y.float() if cfg["dtype"] == "f32" else y, slabs)
+        from paper_1412_1885_b200.generators import generate_as
+        tdt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+        y = generate_as(dict(cfg, seed=0), tdt, slab=(0, slabs), full_sigma=True)
+        ys, sdims = cpu_sample(cfg, y, slabs)
         del y
         torch.cuda.empty_cache()
     else:  # host-only fallback for the sample generator: the oracle's own generators
@@ -264,13 +266,15 @@ def run_b200(args, cfg):
     # I_0 x ... x (N * I_{N-1}) (weak scaling), generated blockwise on the device: the last
     # factor's rows and the noise are drawn at their global indices, the noise scale from
     # norms summed over ranks, so the slabs concatenate to the tensor a single run generates.
+    from paper_1412_1885_b200.generators import generate_as
     if world == 1:
-        y64 = generate(dict(cfg, seed=0))
+        y = generate_as(dict(cfg, seed=0), tdt)
     else:
-        y64 = generate(dict(cfg, seed=0, dims=gdims), slab=(slab_offset, dims[-1]), all_sum=_all_sum)
-    y = y64.to(tdt)
-    del y64
+        y = generate_as(dict(cfg, seed=0, dims=gdims), tdt, slab=(slab_offset, dims[-1]), all_sum=_all_sum)
     torch.cuda.empty_cache()
+    cpu_ys = None  # the CPU baseline's bounded sample: the first slabs of this Y (host fp64)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_ys, cpu_sdims = cpu_sample(cfg, y, args.cpu_slabs)
     yd = P.DenseTensor(dims, y)
     ybytes = y.numel() * y.element_size()
     comm = None
@@ -360,7 +364,7 @@ def run_b200(args, cfg):
             fit_obs = P.model_fit(P.DenseTensor(dims, yd_fit), cpm, context=ctx)
             fit_ms = 1e3 * (time.perf_counter() - t0)
             del yd_fit
-            truth = generate(dict(cfg, seed=0, snr=float("inf"))).to(tdt)
+            truth = generate_as(dict(cfg, seed=0, snr=float("inf")), tdt)
             fit_gt = P.model_fit(P.DenseTensor(dims, truth), cpm, context=ctx)
             del truth
             torch.cuda.empty_cache()
@@ -370,10 +374,7 @@ def run_b200(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        yy = generate(dict(cfg, seed=0))
-        ys, sdims = cpu_sample(cfg, yy.to(tdt), args.cpu_slabs)
-        del yy
-        torch.cuda.empty_cache()
+        ys, sdims = cpu_ys, cpu_sdims
         tc, te = oracle_decompose(ys, cfg, alg_seed, threads, with_ffcp=False)
         pref = 2 * len(dims) + 1
         cpu = {"value": round(pref * ys.size * (4 if cfg["dtype"] == "f32" else 8) / tc / 1e9, 3), "unit": "GB/s",

@@ -1,6 +1,3 @@
 #!/bin/bash
-timeout 300 python tools/qr_bench.py
-TENKIT_QR_NO_FAST=1 timeout 300 python tools/qr_bench.py
-timeout 900 python -m pytest tests -m gpu -q -x -k "qr or basis or golden or parity or tc or workload" 2>&1 | tail -3
-python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_q.log 2>&1; tail -1 gpurun_out/bench_q.log | python -c "import json,sys; d=json.load(sys.stdin); print(d['value'], d['ms_per_step'], d['roofline']['achieved'])"
-timeout 800 python tools/diag_subspace.py 2>&1 | grep auto
+timeout 600 python -m pytest tests/test_gpu_workload.py -q -x -k chunked 2>&1 | tail -2
+for c in cfg4 cfg3 cfg1; do timeout 1500 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.log 2> gpurun_out/bench_$c.err; echo "$c rc=$?"; tail -1 gpurun_out/bench_$c.log | python -c "import json,sys; d=json.load(sys.stdin); print(d['value'], d['ms_per_step'], d['roofline']['achieved'], d['fit_model'], d.get('e2e'), d.get('cpu_baseline',{}).get('value'))"; tail -2 gpurun_out/bench_$c.err; done

@@ -108,8 +108,8 @@ def add_noise_device(y, snr_db: float, seed: SeedSpec, abs_noise: bool = False, 
     e = gaussian_flat(y.numel(), seed.derived(0x7015E), context, offset=offset)
     if abs_noise:
         e.abs_()
-    ysq = float(torch.dot(y, y).item())
-    esq = float(torch.dot(e, e).item())
+    ysq = _sumsq(y)
+    esq = _sumsq(e)
     if all_sum is not None:
         ysq, esq = all_sum(ysq), all_sum(esq)
     ny, ne = float(np.sqrt(ysq)), float(np.sqrt(esq))
@@ -119,6 +119,16 @@ def add_noise_device(y, snr_db: float, seed: SeedSpec, abs_noise: bool = False, 
     y.add_(e, alpha=sigma)
     del e
     return y
+
+
+def _sumsq(x) -> float:
+    """sum of squares in fp64 (chunked: BLAS dot takes 32-bit lengths)."""
+    import torch
+    n, tot, step = x.numel(), 0.0, 1 << 30
+    for a in range(0, n, step):
+        c = x[a:a + step]
+        tot += float(torch.dot(c, c).item())
+    return tot
 
 
 def bench_seeds(seed: int = 0, d: int = 0, s: int = 0, run: int = 0):
@@ -142,3 +152,56 @@ def generate(cfg: dict, context=None, slab=None, all_sum=None):
     offset = int(slab[0]) * int(np.prod(dims[:-1])) if slab is not None else 0
     return add_noise_device(y, cfg["snr"], data_seed.derived(0xAD0), abs_noise=cfg.get("abs_noise", False),
                             context=context, offset=offset, all_sum=all_sum)
+
+
+def generate_as(cfg: dict, dtype, context=None, slab=None, all_sum=None, chunk_elems: int = 1 << 28,
+                full_sigma: bool = False):
+    """generate() straight into `dtype` (e.g. torch.float32) with bounded fp64 temporaries:
+    the tensor (or this rank's last-mode slab) is built in chunks of the last mode, twice
+    (pass 1: the norms of Y and E for sigma; pass 2: Y + sigma E rounded to dtype), every
+    entry drawn at its global index. Same values as generate(...).to(dtype) up to the
+    rounding of the chunked contractions; needed for cfg 3/4 (55 / 32 GB fp32) where the
+    fp64 tensor and noise would not fit next to each other. full_sigma: materialise only
+    `slab` but take the noise scale from the whole tensor (a bounded sample of it)."""
+    import torch
+    dims = [int(d) for d in cfg["dims"]]
+    off0, ln = (int(slab[0]), int(slab[1])) if slab is not None else (0, dims[-1])
+    S = int(np.prod(dims[:-1]))
+    per = max(1, int(chunk_elems) // S)
+    data_seed, _ = bench_seeds(cfg.get("seed", 0))
+    nseed = data_seed.derived(0xAD0).derived(0x7015E)
+    abs_noise = cfg.get("abs_noise", False)
+    noisy = not (np.isinf(cfg["snr"]) and cfg["snr"] > 0)
+
+    def clean(a, b):  # rows [a, b) of the last mode (global indices)
+        if cfg["gen"] == "tucker":
+            return gen_tucker_device(dims, cfg["mlrank"], data_seed, context, last_rows=(a, b - a))
+        return gen_cp_device(dims, cfg["cp_rank"], data_seed, uniform=cfg["gen"] == "cp_uniform", context=context,
+                             last_rows=(a, b - a))
+
+    def noise(a, b):
+        e = gaussian_flat((b - a) * S, nseed, context, offset=a * S)
+        return e.abs_() if abs_noise else e
+
+    out = torch.empty(S * ln, dtype=dtype, device="cuda")
+    ysq = esq = 0.0
+    sigma = 0.0
+    if noisy:
+        n0, n1 = (0, dims[-1]) if full_sigma else (off0, off0 + ln)
+        for a in range(n0, n1, per):
+            b = min(a + per, n1)
+            ysq += _sumsq(clean(a, b))
+            esq += _sumsq(noise(a, b))
+        if all_sum is not None:
+            ysq, esq = all_sum(ysq), all_sum(esq)
+        if ysq <= 0 or esq <= 0:
+            raise _lib.TenkitError("tenkit: add_noise: zero tensor input")
+        sigma = float(np.sqrt(ysq)) / (float(np.sqrt(esq)) * 10.0 ** (cfg["snr"] / 20.0))
+    for a in range(off0, off0 + ln, per):
+        b = min(a + per, off0 + ln)
+        y = clean(a, b)
+        if noisy:
+            y.add_(noise(a, b), alpha=sigma)
+        out[(a - off0) * S:(b - off0) * S] = y.to(dtype)
+        del y
+    return out

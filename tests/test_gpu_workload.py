@@ -75,3 +75,19 @@ def test_config2_shape_reduced(P, O):
 def test_config2_full_size(P, O):
     """BASELINE configs[1] at full size: 1000^3 fp32 (4 GB), oracle on the same Y in fp64."""
     _check_against_oracle(P, O, (1000, 1000, 1000), (20, 20, 20), (20, 20, 20), 10)
+
+
+@pytest.mark.parametrize("gen", ["tucker", "cp_uniform"])
+def test_chunked_generation_matches_full(P, gen):
+    """generate_as (chunked along the last mode, bounded fp64 temporaries; cfg 3/4 sizes)
+    reproduces generate(); a full-sigma sample is the leading slab of the full tensor."""
+    from paper_1412_1885_b200.generators import generate, generate_as
+    import torch
+    cfg = dict(dims=(20, 18, 33), gen=gen, mlrank=(3, 4, 2), cp_rank=3, snr=15.0, abs_noise=(gen != "tucker"))
+    full = generate(cfg).cpu().numpy()
+    got = generate_as(cfg, torch.float64, chunk_elems=20 * 18 * 5).cpu().numpy()
+    np.testing.assert_allclose(got, full, rtol=0, atol=1e-12 * np.abs(full).max())
+    part = generate_as(cfg, torch.float64, slab=(0, 7), full_sigma=True, chunk_elems=20 * 18 * 4).cpu().numpy()
+    np.testing.assert_allclose(part, full[: 20 * 18 * 7], rtol=0, atol=1e-12 * np.abs(full).max())
+    f32 = generate_as(cfg, torch.float32).cpu().numpy()
+    np.testing.assert_array_equal(f32, full.astype(np.float32))

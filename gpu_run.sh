@@ -1,3 +1,2 @@
 #!/bin/bash
-timeout 600 python -m pytest tests/test_gpu_workload.py -q -x -k chunked 2>&1 | tail -2
-for c in cfg4 cfg3 cfg1; do timeout 1500 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.log 2> gpurun_out/bench_$c.err; echo "$c rc=$?"; tail -1 gpurun_out/bench_$c.log | python -c "import json,sys; d=json.load(sys.stdin); print(d['value'], d['ms_per_step'], d['roofline']['achieved'], d['fit_model'], d.get('e2e'), d.get('cpu_baseline',{}).get('value'))"; tail -2 gpurun_out/bench_$c.err; done
+for v in 0 1; do TENKIT_TC_VARIANT=$v timeout 400 python bench.py --config cfg3 --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_cfg3.log 2> gpurun_out/bench_cfg3.err; echo "cfg3 v$v rc=$?"; tail -1 gpurun_out/bench_cfg3.log | python -c "import json,sys; d=json.load(sys.stdin); print(d['value'], d['ms_per_step'], d['roofline']['achieved'], d['fit_model'])"; done

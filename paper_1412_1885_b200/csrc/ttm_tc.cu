@@ -6,7 +6,7 @@
 // the sign rule; 3xTF32 keeps ~2^-21 relative error per product):
 //     y u ~= y_hi u_hi + y_hi u_lo + y_lo u_hi,   x_hi = rna_tf32(x), x_lo = x - x_hi (exact)
 // Warp roles (one 512-row tile of Y per CTA, K streamed in 16-column stages):
-//   warp 8      producer: TMA tensor loads (256-row x 16-k boxes of the (P, K, Q) view,
+//   warp 8      producer: TMA tensor loads (BOXR-row x 16-k boxes of the (P, K, Q) view,
 //               zero-filled out of bounds) + a bulk copy of the packed [U_hi | U_lo] stage
 //               into a 4-deep shared-memory ring (mbarrier complete_tx)
 //   warps 0-7   converters: LDS.128 of 4 rows per thread, split y into (hi, lo) and
@@ -76,7 +76,7 @@ struct TcCfg {
     static_assert(XBASE <= TMEM, "TMEM budget");
     // pipeline depth: ~128 KB of Y in flight per SM whatever the tile height
     static constexpr int STAGES_RAW = (128 * 1024) / STAGE_Y / OCC_;
-    static constexpr int STAGES = STAGES_RAW < kTcStages ? kTcStages : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
+    static constexpr int STAGES = STAGES_RAW < kTcStages ? kTcStages : (STAGES_RAW > 6 ? 6 : STAGES_RAW);
     static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 256 + 128;
 };
 
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
     using C = TcCfg<NH, MT_, OCC>;
     constexpr int MT = C::MT, BM = C::BM;
     extern __shared__ __align__(1024) uint8_t tsm[];
-    uint8_t* sY = tsm;  // [stages][BM/256 boxes][kTcBK][256] fp32
+    uint8_t* sY = tsm;  // [stages][BM/BOXR boxes][kTcBK][BOXR] fp32
     uint8_t* sB = tsm + size_t(C::STAGES) * C::STAGE_Y;           // [stages][2][2NH x 8] tf32 core matrices
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(C::STAGES) * C::STAGE_B);
     uint64_t* full = bars;                   // [stages]  producer -> (converters, MMA)
@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
                                     &full[s]);
                 } else {
 #pragma unroll
-                    for (int b = 0; b < BM / 256; ++b)
-                        tma_load_3d(dy + b * (kTcBK * 256 * 4), &ymap, static_cast<int>(p0 + 256 * b), kc * kTcBK,
+                    for (int b = 0; b < BM / C::BOXR; ++b)
+                        tma_load_3d(dy + b * (kTcBK * C::BOXR * 4), &ymap, static_cast<int>(p0 + C::BOXR * b), kc * kTcBK,
                                     static_cast<int>(q), &full[s]);
                 }
                 bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
@@ -291,9 +291,9 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
             const int s = kc % C::STAGES, a = kc & 1;
             mbar_wait(&full[s], (kc / C::STAGES) & 1);
             uint32_t hi[MT][8], lo[MT][8];
-            // rows MT*L .. MT*L+MT-1 of the tile sit in box (MT*L)/256 at row (MT*L)%256
+            // rows MT*L .. MT*L+MT-1 of the tile sit in box (MT*L)/BOXR at row (MT*L)%BOXR
             const float* ys = reinterpret_cast<const float*>(sY + size_t(s) * C::STAGE_Y) +
-                              ((MT * L) / 256) * (kTcBK * 256) + (MT * L) % 256 + khalf * 8 * 256;
+                              ((MT * L) / C::BOXR) * (kTcBK * C::BOXR) + (MT * L) % C::BOXR + khalf * 8 * C::BOXR;
             if constexpr (KM) {
                 // row j*128 + L of the tile: 8 k values = logical 16-B chunks 2*khalf, 2*khalf+1
                 const uint8_t* stage = sY + size_t(s) * C::STAGE_Y;
@@ -319,11 +319,13 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
                 auto split = [&](int kk, bool live) {
                     float y[MT];
                     if constexpr (MT == 4) {
-                        const float4 v = *reinterpret_cast<const float4*>(ys + kk * 256);
+                        const float4 v = *reinterpret_cast<const float4*>(ys + kk * C::BOXR);
                         y[0] = v.x, y[1] = v.y, y[2] = v.z, y[3] = v.w;
-                    } else {
-                        const float2 v = *reinterpret_cast<const float2*>(ys + kk * 256);
+                    } else if constexpr (MT == 2) {
+                        const float2 v = *reinterpret_cast<const float2*>(ys + kk * C::BOXR);
                         y[0] = v.x, y[1] = v.y;
+                    } else {
+                        y[0] = ys[kk * C::BOXR];
                     }
 #pragma unroll
                     for (int j = 0; j < MT; ++j) {
@@ -392,8 +394,10 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
                         if constexpr (MT == 4) {
                             *reinterpret_cast<float4*>(o + int64_t(r) * P) =
                                 make_float4(acc[0][e], acc[1][e], acc[2][e], acc[3][e]);
-                        } else {
+                        } else if constexpr (MT == 2) {
                             *reinterpret_cast<float2*>(o + int64_t(r) * P) = make_float2(acc[0][e], acc[1][e]);
+                        } else {
+                            o[int64_t(r) * P] = acc[0][e];
                         }
                     }
                 }
@@ -459,7 +463,7 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
         grid = tiles_p * Q;
         const cuuint64_t dims[3] = {cuuint64_t(P), cuuint64_t(K), cuuint64_t(Q)};
         const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
-        const cuuint32_t box[3] = {256, kTcBK, 1};
+        const cuuint32_t box[3] = {C::BOXR, kTcBK, 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -510,7 +514,7 @@ constexpr int kOcc = 2;
 bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols) {
     if (reinterpret_cast<uintptr_t>(in) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
     if (P == 1) return K % 4 == 0 && K >= kTcBK && cols <= 32 && (Q + 127) / 128 >= 148;
-    const int bm = tc_nh(cols) <= 32 ? 128 * kMmt : 256;  // tiles >= 2 waves of 2 CTAs per SM
+    const int bm = tc_nh(cols) <= 32 ? 128 * kMmt : 128;  // tiles >= 2 waves of 2 CTAs per SM
     const int64_t tiles = (P + bm - 1) / bm * Q;
     return P % 4 == 0 && P >= 256 && tiles >= 2 * 2 * 148;
 }
@@ -529,15 +533,18 @@ void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int6
         const char* e = std::getenv("TENKIT_TC_VARIANT");
         return e ? std::atoi(e) : 0;
     }();
-    if (variant == 1) {  // A/B: one 512-row CTA per SM (the round-1 first version)
+    if (variant == 1) {  // A/B: one CTA per SM (the round-1 first version)
         if (tc_nh(cols) <= 16) return launch_tc<16, 4, false>(in, b, out, P, K, Q, cols, s);
         if (tc_nh(cols) <= 32) return launch_tc<32, 4, false>(in, b, out, P, K, Q, cols, s);
+        if (tc_nh(cols) <= 48) return launch_tc<48, 2, false>(in, b, out, P, K, Q, cols, s);
+        return launch_tc<64, 2, false>(in, b, out, P, K, Q, cols, s);
     }
     switch (tc_nh(cols)) {
         case 16: return launch_tc<16, kMmt, false, kOcc>(in, b, out, P, K, Q, cols, s);
         case 32: return launch_tc<32, kMmt, false, kOcc>(in, b, out, P, K, Q, cols, s);
-        case 48: return launch_tc<48, 2, false>(in, b, out, P, K, Q, cols, s);
-        default: return launch_tc<64, 2, false>(in, b, out, P, K, Q, cols, s);
+        // wider factors: one 128-row tile per CTA keeps two CTAs per SM inside 256 TMEM columns
+        case 48: return launch_tc<48, 1, false, kOcc>(in, b, out, P, K, Q, cols, s);
+        default: return launch_tc<64, 1, false, kOcc>(in, b, out, P, K, Q, cols, s);
     }
 }
 

@@ -349,7 +349,37 @@ struct PersistParams {
     int stage_v;      // phase A stages V_q (p != n) in shared memory
     int64_t stage_g;  // doubles available for staged core slices (0: read the core from L2)
     unsigned long long* prof;  // optional: per (step, mark) globaltimer stamps of CTA 0
+    unsigned* bar;             // grid barrier: [0] arrivals, [1] generation
+    unsigned* fready;          // LDLT factors of step s published: *fready >= s + 1
 };
+
+// Split-phase grid barrier for the phase A -> B boundary (all CTAs are co-resident:
+// cooperative launch; the other boundaries use the cooperative-groups grid barrier).
+// arrive() makes the CTA's prior writes visible and returns the generation to wait on; the
+// LDLT CTA arrives early and factorizes while the other CTAs run ahead into phase B.
+__device__ __forceinline__ unsigned bar_arrive(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    unsigned g = 0;
+    if (threadIdx.x == 0) {
+        g = *reinterpret_cast<volatile unsigned*>(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        }
+    }
+    return g;
+}
+__device__ __forceinline__ void bar_wait(unsigned* bar, unsigned g) {
+    if (threadIdx.x == 0) {
+        while (*reinterpret_cast<volatile unsigned*>(bar + 1) == g) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void bar_sync(unsigned* bar, unsigned nblocks) { bar_wait(bar, bar_arrive(bar, nblocks)); }
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -555,7 +585,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
                     sT[e] = v;
                     T[e] = v;
                 }
-                __syncthreads();
+                const unsigned ga = bar_arrive(p.bar, G);  // phase A arrival; factorize meanwhile
                 PROF_SUB(G - 1, 1);
                 if (ls && warp < 2) {
                     double ridge = 0.0;
@@ -572,7 +602,13 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
                     for (int e = lane; e < RR; e += 32) gf[e] = f[e];
                     for (int e = lane; e < R; e += 32) p.sig[warp * kMaxRank + e] = sg[e];
                 }
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence();
+                    atomicMax(p.fready, unsigned(step + 1));
+                }
                 PROF_SUB(G - 1, 2);
+                bar_wait(p.bar, ga);
             } else if (int64_t(blockIdx.x) * kPWarps < int64_t(cn) * R) {
                 // H[i, r] = sum over the other modes of G[i, ...] * prod_{q != n} V_q[i_q, r],
                 // contracting the last other mode innermost (the reference's ffcp_h contracts
@@ -644,12 +680,12 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
                         } else {
                             const double* gi = p.core + i * Pn;
                             if (no == 1) {
-                                for (int k = lane; k < cl; k += 32) accv = fma(__ldcg(gi + slice_off(k)), vl[k], accv);
+                                for (int k = lane; k < cl; k += 32) accv = fma(__ldcg(gi + slice_off(k)), __ldcg(vl + k), accv);
                             } else {
                                 for (int e = lane; e < Sp; e += 32) {
                                     double t = 0.0;
 #pragma unroll 8
-                                    for (int k = 0; k < cl; ++k) t = fma(__ldcg(gi + slice_off(e + k * Sp)), vl[k], t);
+                                    for (int k = 0; k < cl; ++k) t = fma(__ldcg(gi + slice_off(e + k * Sp)), __ldcg(vl + k), t);
                                     int rem = e;
                                     double prod = 1.0;
                                     for (int q = 0; q + 1 < no; ++q) {
@@ -668,7 +704,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
                     PROF_SUB(0, 5);
                 }
             }
-            grid.sync();
+            if (blockIdx.x != G - 1) bar_sync(p.bar, G);
             PROF_MARK(1);
             // ---------------- phase B (and the ridge rerun)
             const int ps = RR + cn * R;
@@ -677,11 +713,21 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
                 if (ridge && !(ls && __ldcg(p.bad + par))) break;
                 stage_copy(sH, cn * R, [&](int d) { return __ldcg(H + (d / R) + (d % R) * cn); });
                 stage_copy(sT, RR, [&](int e) { return __ldcg(T + e); });
-                if (ls) {
+                bool fstaged = !ls;
+                auto stage_f = [&]() {  // LDLT factors of this step (published by the last CTA)
+                    if (tid == 0) {
+                        while (*reinterpret_cast<volatile unsigned*>(p.fready) < unsigned(step + 1)) {
+                        }
+                        __threadfence();
+                    }
+                    __syncthreads();
                     const double* fsrc = ridge ? p.Fr : p.F;
                     stage_copy(sF, RR, [&](int e) { return __ldcg(fsrc + e); });
-                }
-                for (int e = tid; e < R; e += kPThreads) ssig[e] = __ldcg(p.sig + (ridge ? kMaxRank : 0) + e);
+                    for (int e = tid; e < R; e += kPThreads) ssig[e] = __ldcg(p.sig + (ridge ? kMaxRank : 0) + e);
+                    __syncthreads();
+                    fstaged = true;
+                };
+                if (ridge && ls) stage_f();
                 for (int e = tid; e < ps; e += kPThreads) acc[e] = 0.0;
                 __syncthreads();
                 if (!ridge) PROF_SUB(0, 6);
@@ -690,18 +736,19 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
                 double* wa = sa + warp * kMaxRank;
                 double* wu = su + warp * kMaxRank;
                 double* wb = sb + warp * kMaxRank;
-                const int64_t chunk = int64_t(G) * kPWarps;
-                for (int64_t base = int64_t(blockIdx.x) * kPWarps; base < m; base += chunk) {
+                // rows over CTAs 0 .. G-2 (the last CTA factorizes T meanwhile)
+                const int64_t chunk = int64_t(G - 1) * kPWarps;
+                const int64_t first = blockIdx.x == G - 1 ? m : int64_t(blockIdx.x) * kPWarps;
+                for (int64_t base = first; base < m; base += chunk) {
                     const int64_t i = base + warp;
+                    double q0 = 0.0, q1 = 0.0, a0 = 0.0, a1 = 0.0;
                     if (i < m) {
                         for (int k = lane; k < cn; k += 32) wu[k] = U[i + k * m];
-                        double a0 = 0.0, a1 = 0.0;
                         if (!ls) {
                             a0 = lane < R ? A[i + int64_t(lane) * m] : 0.0;
                             a1 = lane + 32 < R ? A[i + int64_t(lane + 32) * m] : 0.0;
                         }
                         __syncwarp();
-                        double q0 = 0.0, q1 = 0.0;
                         if (lane < R) {
 #pragma unroll 8
                             for (int k = 0; k < cn; ++k) q0 = fma(wu[k], sH[k * R + lane], q0);
@@ -710,6 +757,9 @@ __global__ void __launch_bounds__(kPThreads, 1) ffcp_persistent_kernel(PersistPa
 #pragma unroll 8
                             for (int k = 0; k < cn; ++k) q1 = fma(wu[k], sH[k * R + lane + 32], q1);
                         }
+                    }
+                    if (!fstaged) stage_f();  // CTA-uniform: first chunk only
+                    if (i < m) {
                         if (ls) {
                             a0 = q0;
                             a1 = q1;
@@ -992,6 +1042,10 @@ void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* co
         pp.yt = yt;
         pp.fit_trace = mem.get<double>(std::max(max_iters, 1));
         pp.iters = mem.get<int>(1);
+        pp.bar = mem.get<unsigned>(2);
+        pp.fready = mem.get<unsigned>(1);
+        TK_CUDA(cudaMemsetAsync(pp.bar, 0, 2 * sizeof(unsigned), s));
+        TK_CUDA(cudaMemsetAsync(pp.fready, 0, sizeof(unsigned), s));
         pp.scratch = scratch;
         pp.stage_v = stage_v ? 1 : 0;
         pp.stage_g = stage_g;

@@ -1,4 +1,3 @@
 #!/bin/bash
-timeout 120 python tools/ffcp_exp.py 2>&1 | grep -E "mode-step|Error|error" ; echo "exp rc=$?"
-timeout 120 python tools/ffcp_bench.py 200 2>&1 | grep -E "persistent|max"
-timeout 300 python -m pytest tests -m gpu -q -x -k "ffcp or golden or cpp or fit" 2>&1 | tail -2
+timeout 400 python -m pytest tests/test_gpu_dist.py -q -x 2>&1 | tail -3
+timeout 400 python -m pytest tests -m gpu -q -x -k "rand_tucker or alg2 or config1 or golden" 2>&1 | tail -2

@@ -51,9 +51,12 @@ template <typename T>
 void launch_unfold(const T* x, int64_t B, int64_t I, int64_t A, T* out, cudaStream_t s);
 
 // Omega packed for the TTM kernels (T, k-major, stride pack_stride(cols)):
-// out[c * stride + j] = normal_at(key, j * rows + c) for j < cols, 0 for the padding.
+// out[c * stride + j] = normal_at(key, j * rows_total + row_off + c) for j < cols, 0 for the
+// padding: rows [row_off, row_off + rows) of a rows_total x cols gaussian_matrix
+// (rows_total <= 0: rows_total = rows).
 template <typename T>
-void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaStream_t s);
+void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaStream_t s, int64_t row_off = 0,
+                            int64_t rows_total = 0);
 
 // Counter-RNG fills (random.hpp:85-100): out[i + j*rows] = normal_at(key, j*rows + i).
 void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s);

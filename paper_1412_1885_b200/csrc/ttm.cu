@@ -423,12 +423,13 @@ __global__ void unfold_kernel(const T* __restrict__ x, int64_t B, int64_t I, int
 }
 
 template <typename T>
-__global__ void gaussian_packed_kernel(T* __restrict__ out, int64_t rows, int cols, int stride, uint64_t key) {
+__global__ void gaussian_packed_kernel(T* __restrict__ out, int64_t rows, int cols, int stride, uint64_t key,
+                                       int64_t row_off, int64_t rows_total) {
     const int64_t n = rows * stride;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
         const int64_t c = t / stride;
         const int j = static_cast<int>(t % stride);
-        out[t] = j < cols ? static_cast<T>(normal_at_key(key, static_cast<uint64_t>(j * rows + c))) : T(0);
+        out[t] = j < cols ? static_cast<T>(normal_at_key(key, static_cast<uint64_t>(j * rows_total + row_off + c))) : T(0);
     }
 }
 
@@ -512,13 +513,15 @@ template void launch_unfold<float>(const float*, int64_t, int64_t, int64_t, floa
 template void launch_unfold<double>(const double*, int64_t, int64_t, int64_t, double*, cudaStream_t);
 
 template <typename T>
-void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaStream_t s) {
+void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaStream_t s, int64_t row_off,
+                            int64_t rows_total) {
     const int stride = pack_stride(cols);
-    gaussian_packed_kernel<T><<<grid_for(rows * stride), 256, 0, s>>>(out, rows, cols, stride, key);
+    if (rows_total <= 0) rows_total = rows;
+    gaussian_packed_kernel<T><<<grid_for(rows * stride), 256, 0, s>>>(out, rows, cols, stride, key, row_off, rows_total);
     TK_LAUNCH_CHECK();
 }
-template void launch_gaussian_packed<float>(float*, int64_t, int, uint64_t, cudaStream_t);
-template void launch_gaussian_packed<double>(double*, int64_t, int, uint64_t, cudaStream_t);
+template void launch_gaussian_packed<float>(float*, int64_t, int, uint64_t, cudaStream_t, int64_t, int64_t);
+template void launch_gaussian_packed<double>(double*, int64_t, int, uint64_t, cudaStream_t, int64_t, int64_t);
 
 template <typename S, typename D>
 void launch_cast(const S* in, D* out, int64_t n, cudaStream_t s) {

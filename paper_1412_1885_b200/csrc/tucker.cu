@@ -451,44 +451,63 @@ struct TuckerRun {
 template <typename T>
 void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const void* y, int y_on_device,
                       const int64_t* ranks, int64_t p, Seed seed, tk_tucker_out* out, tk_tucker_stats* stats) {
-    require(!(ctx->has_comm && ctx->comm.world > 1), "rand_tucker: multi-rank runs use rand_tucker_2i");
     cudaStream_t s = ctx->stream;
-    std::vector<int64_t> cd(dims, dims + order);
+    std::vector<int64_t> cd(dims, dims + order);  // current (local) extents
+    std::vector<int64_t> gd = cd;                 // global extents
+    int64_t offset = 0;
+    const bool dist = ctx->has_comm && ctx->comm.world > 1;
+    if (dist) {  // slab of the last mode (dist.hpp:496-596: Omega rows by global column id)
+        gd[order - 1] = ctx->comm.global_last_dim;
+        offset = ctx->comm.slab_offset;
+        require(offset >= 0 && offset + cd[order - 1] <= gd[order - 1], "comm: slab outside the global tensor");
+    }
     const T* cur = static_cast<const T*>(y);
     if (!y_on_device) {
         T* buf = static_cast<T*>(ctx->buf("y_in", sizeof(T) * prod(cd)));
         TK_CUDA(cudaMemcpyAsync(buf, y, sizeof(T) * prod(cd), cudaMemcpyHostToDevice, s));
         cur = buf;
     }
-    TuckerRun<T> r{ctx, s, order, cd, cd, 0, cur};
+    TuckerRun<T> r{ctx, s, order, cd, gd, offset, cur};
     r.rank_dev = static_cast<int*>(ctx->buf("ranks", sizeof(int) * 2 * TK_MAX_ORDER));
     std::vector<double*> U(order);
     std::vector<int64_t> fcols(order);
     int which = 0;
+    const int last = static_cast<int>(order) - 1;
     for (int n = 0; n < order; ++n) {
-        const int rt = static_cast<int>(std::min<int64_t>(ranks[n] + p, cd[n]));
+        const int rt = static_cast<int>(std::min<int64_t>(ranks[n] + p, gd[n]));
         require(rt >= 1, "gaussian_matrix: dimensions must be positive");
         require(rt <= kMaxRank, "rank + oversample must be <= 64 on this device path");
+        // Omega_n: (global width) x rt; this rank's unfolding columns are the contiguous rows
+        // [offset * S, (offset + len) * S) of it when n < last (the last mode varies slowest)
         const int64_t width = prod(cd) / cd[n];
+        int64_t row_off = 0, width_g = width;
+        if (dist && n < last) {
+            const int64_t S = width / cd[last];
+            row_off = offset * S;
+            width_g = S * gd[last];
+        }
         const Seed os = alg2_omega_seed(seed, n);
-        double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * cd[n] * rt));
-        if (n == 0) {  // contiguous unfolding: Z = Y_(0) * Omega as a split-K TTM over the flattened modes
-            T* op = static_cast<T*>(ctx->buf("omega_packed", sizeof(T) * width * pack_stride(rt)));
-            launch_gaussian_packed<T>(op, width, rt, os.key(), s);
+        double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * gd[n] * rt));
+        T* op = static_cast<T*>(ctx->buf("omega_packed", sizeof(T) * width * pack_stride(rt)));
+        launch_gaussian_packed<T>(op, width, rt, os.key(), s, row_off, width_g);
+        if (n == 0 && !(dist && last == 0)) {  // contiguous unfolding: Z = Y_(0) Omega, split-K TTM
             T* zt = static_cast<T*>(ctx->buf("zt", sizeof(T) * cd[0] * rt));
             r.ttm(cur, op, zt, cd[0], width, 1, rt);
             if constexpr (sizeof(T) == 4) launch_cast<float, double>(reinterpret_cast<const float*>(zt), z, cd[0] * rt, s);
             else launch_cast<double, double>(reinterpret_cast<const double*>(zt), z, cd[0] * rt, s);
             r.launches += 2;
+        } else if (dist && n == last) {  // own rows of Z, the others zero (summed over ranks)
+            TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * gd[n] * rt, s));
+            r.sketch(cur, cd, n, op, rt, z + offset, gd[n]);
+            ++r.launches;
         } else {
-            T* op = static_cast<T*>(ctx->buf("omega_packed", sizeof(T) * width * pack_stride(rt)));
-            launch_gaussian_packed<T>(op, width, rt, os.key(), s);
             r.sketch(cur, cd, n, op, rt, z, cd[n]);
             ++r.launches;
         }
-        U[n] = static_cast<double*>(ctx->buf("U" + std::to_string(n), sizeof(double) * cd[n] * rt));
-        T* up = static_cast<T*>(ctx->buf("Up" + std::to_string(n), sizeof(T) * cd[n] * pack_stride(rt)));
-        launch_orthonormal_basis(z, cd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64, r.rank_dev + n, nullptr, s);
+        r.allreduce(z, gd[n] * rt);  // partial sketches summed over ranks (no-op on one rank)
+        U[n] = static_cast<double*>(ctx->buf("U" + std::to_string(n), sizeof(double) * gd[n] * rt));
+        T* up = static_cast<T*>(ctx->buf("Up" + std::to_string(n), sizeof(T) * gd[n] * pack_stride(rt)));
+        launch_orthonormal_basis(z, gd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64, r.rank_dev + n, nullptr, s);
         ++r.launches;
         TK_CUDA(cudaMemcpyAsync(ctx->rank_host, r.rank_dev + n, sizeof(int), cudaMemcpyDeviceToHost, s));
         TK_CUDA(cudaStreamSynchronize(s));
@@ -498,7 +517,8 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
         const int64_t P = prod(std::vector<int64_t>(cd.begin(), cd.begin() + n));
         const int64_t Q = prod(std::vector<int64_t>(cd.begin() + n + 1, cd.end()));
         T* nxt = static_cast<T*>(ctx->buf(which ? "a2B" : "a2A", sizeof(T) * P * rank * Q));
-        r.ttm(cur, up, nxt, P, cd[n], Q, rank);
+        const T* upl = up + (n == last ? offset * pack_stride(rank) : 0);  // this rank's rows of U
+        r.ttm(cur, upl, nxt, P, cd[n], Q, rank);
         if (n == 0) ++r.passes;
         cd[n] = rank;
         cur = nxt;
@@ -508,12 +528,13 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
     double* gdv = static_cast<double*>(ctx->buf("core64", sizeof(double) * gsize));
     if constexpr (sizeof(T) == 4) launch_cast<float, double>(reinterpret_cast<const float*>(cur), gdv, gsize, s);
     else launch_cast<double, double>(reinterpret_cast<const double*>(cur), gdv, gsize, s);
+    r.allreduce(gdv, gsize);  // partial cores summed over ranks
     const cudaMemcpyKind kind = out->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     TK_CUDA(cudaMemcpyAsync(out->core, gdv, sizeof(double) * gsize, kind, s));
     for (int n = 0; n < order; ++n) {
         out->core_shape[n] = cd[n];
         out->factor_cols[n] = fcols[n];
-        TK_CUDA(cudaMemcpyAsync(out->factors[n], U[n], sizeof(double) * dims[n] * fcols[n], kind, s));
+        TK_CUDA(cudaMemcpyAsync(out->factors[n], U[n], sizeof(double) * gd[n] * fcols[n], kind, s));
     }
     if (stats) {
         stats->passes = r.passes + 1;  // the Z sketch of mode 0 streams Y as well

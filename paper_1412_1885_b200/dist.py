@@ -105,3 +105,21 @@ def dist_rand_tucker_2i(local_y, global_last_dim: int, slab_offset: int, ranks, 
         return rand_tucker_2i(local_y, ranks, oversample, seed, context=ctx, global_last_dim=global_last_dim, **kw)
     finally:
         ctx.set_comm(None)
+
+
+def dist_rand_tucker(local_y, global_last_dim: int, slab_offset: int, ranks, oversample, seed, *, context=None,
+                     group=None, **kw):
+    """rand_tucker (Alg. 2, tucker.hpp:108-130) of the global tensor whose last-mode slab
+    lives on this rank: the Omega rows of each unfolding are drawn at their global column ids
+    (dist.hpp:525-537), partial sketches and the partial core are summed over ranks, the QR
+    is replicated. Every rank returns the same model."""
+    from .tenkit import Context, rand_tucker
+    ctx = context or Context.default()
+    gdims = list(local_y.shape)
+    gdims[-1] = global_last_dim
+    comm = DistComm(slab_offset, global_last_dim, exchange_capacity(gdims, ranks, oversample), group=group)
+    ctx.set_comm(comm)
+    try:
+        return rand_tucker(local_y, ranks, oversample, seed, context=ctx, global_last_dim=global_last_dim, **kw)
+    finally:
+        ctx.set_comm(None)

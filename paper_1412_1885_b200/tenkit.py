@@ -326,9 +326,12 @@ def rand_tucker_2i(y, ranks, oversample: int, seed, *, explicit_core_pass: bool 
     return _tucker_call("tk_rand_tucker_2i", y, ranks, oversample, seed, context, out, opts)
 
 
-def rand_tucker(y, ranks, oversample: int, seed, *, context: Context | None = None, out: str | None = None) -> TuckerModel:
-    """Alg. 2 (tucker.hpp:108-130) on the B200."""
-    return _tucker_call("tk_rand_tucker", y, ranks, oversample, seed, context, out)
+def rand_tucker(y, ranks, oversample: int, seed, *, context: Context | None = None, out: str | None = None,
+                global_last_dim: int = 0) -> TuckerModel:
+    """Alg. 2 (tucker.hpp:108-130) on the B200. global_last_dim: with a comm hook installed,
+    y is this rank's slab of a tensor whose last mode has that global extent."""
+    opts = TuckerOptions(_global_last_dim=int(global_last_dim)) if global_last_dim else None
+    return _tucker_call("tk_rand_tucker", y, ranks, oversample, seed, context, out, opts)
 
 
 # ---------------------------------------------------------------------------- kernels

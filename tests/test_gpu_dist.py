@@ -30,7 +30,7 @@ def _tensor(O):
     return O.add_noise(O.gen_tucker(DIMS, RANKS, data), 15.0, O.seed_derived(*data, 0xAD0))
 
 
-def _worker(rank, world, port, sync, dtype, q):
+def _worker(rank, world, port, sync, dtype, q, alg="2i"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -40,7 +40,7 @@ def _worker(rank, world, port, sync, dtype, q):
         torch.cuda.set_device(0)
         from oracle import pyoracle as O
         import paper_1412_1885_b200 as P
-        from paper_1412_1885_b200.dist import dist_rand_tucker_2i, plan_slabs
+        from paper_1412_1885_b200.dist import dist_rand_tucker, dist_rand_tucker_2i, plan_slabs
         O.build()
         y = _tensor(O)
         off, ln = plan_slabs(DIMS[-1], world)[rank]
@@ -48,7 +48,10 @@ def _worker(rank, world, port, sync, dtype, q):
         ctx = P.Context.default()
         ctx.bind_torch_stream()
         yd = P.DenseTensor.from_numpy(yl, dtype).cuda()
-        m = dist_rand_tucker_2i(yd, DIMS[-1], off, RANKS, P_OVER, SEED, context=ctx, sync_ranks=sync).to_host()
+        if alg == "2i":
+            m = dist_rand_tucker_2i(yd, DIMS[-1], off, RANKS, P_OVER, SEED, context=ctx, sync_ranks=sync).to_host()
+        else:
+            m = dist_rand_tucker(yd, DIMS[-1], off, RANKS, P_OVER, SEED, context=ctx).to_host()
         q.put((rank, m.core, m.factors, m.stats.get("passes")))
         dist.barrier()
         dist.destroy_process_group()
@@ -155,3 +158,38 @@ def test_blockwise_generation_concatenates_to_the_global_tensor():
     full = generate(dict(dims=(24, 20, 31), gen="tucker", mlrank=(3, 4, 2), snr=20.0)).cpu().numpy()
     cat = np.concatenate([got[0], got[1]])
     np.testing.assert_allclose(cat, full, rtol=0, atol=1e-12 * np.abs(full).max())
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_two_rank_alg2_matches_single_process(O, dtype):
+    """dist_rand_tucker (Alg. 2) over two slabs == rand_tucker of the whole tensor == oracle."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import torch.multiprocessing as mp
+    import paper_1412_1885_b200 as P
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, True, dtype, q, "alg2")) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, core, fac, _ = q.get(timeout=300)
+        assert fac is not None, core
+        res[r] = (core, fac)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    y = _tensor(O)
+    single = P.rand_tucker(P.DenseTensor.from_numpy(y.astype(dtype), dtype).cuda(), RANKS, P_OVER, SEED).to_host()
+    g_ref, u_ref = O.rand_tucker(y.astype(dtype).astype(np.float64), RANKS, P_OVER, SEED)
+    tol = 1e-10 if dtype == np.float64 else 1e-4
+    for r in (0, 1):
+        core, fac = res[r]
+        for u, us, uo in zip(fac, single.factors, u_ref):
+            assert orthonormality_defect(u) < 1e-10
+            assert subspace_dist(u, us) < tol
+            assert subspace_dist(u, uo) < (1e-8 if dtype == np.float64 else 1e-3)
+        np.testing.assert_allclose(core, single.core, rtol=0, atol=tol * np.abs(single.core).max())

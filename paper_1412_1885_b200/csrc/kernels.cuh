@@ -38,8 +38,10 @@ void launch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t 
 bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols);
 int64_t umma_pack_bytes(int64_t rows, int cols);
 void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s);
+// accurate: for P == 1 always use the 128-row K-major tiles with 3 accumulator sets (fp32
+// FFMA-level error) instead of the faster single-set 256-row tiles.
 void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s);
+                   cudaStream_t s, bool accurate = false);
 
 // Pack a column-major double factor (rows x cols, leading dim ld) into T k-major
 // [rows][pack_stride(cols)] with zero padding.

@@ -520,10 +520,10 @@ bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t
 }
 
 void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s) {
+                   cudaStream_t s, bool accurate) {
     const uint8_t* b = static_cast<const uint8_t*>(bpk);
     if (P == 1) {
-        const bool wide = km_wide(Q);
+        const bool wide = km_wide(Q) && !accurate;  // narrow tiles: 3 accumulator sets
         if (tc_nh(cols) <= 16) return wide ? launch_tc<16, 2, true, 2>(in, b, out, P, K, Q, cols, s)
                                            : launch_tc<16, 1, true, 2>(in, b, out, P, K, Q, cols, s);
         return wide ? launch_tc<32, 2, true, 2>(in, b, out, P, K, Q, cols, s)

@@ -518,7 +518,19 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
         const int64_t Q = prod(std::vector<int64_t>(cd.begin() + n + 1, cd.end()));
         T* nxt = static_cast<T*>(ctx->buf(which ? "a2B" : "a2A", sizeof(T) * P * rank * Q));
         const T* upl = up + (n == last ? offset * pack_stride(rank) : 0);  // this rank's rows of U
-        r.ttm(cur, upl, nxt, P, cd[n], Q, rank);
+        bool done = false;
+        if constexpr (sizeof(T) == 4) {  // the Y-sized mode-0 shrink on the tensor cores (K-major)
+            if (n == 0 && P == 1 && ctx->ttm_path != 1 &&
+                tc_ttm_supported(reinterpret_cast<const float*>(cur), reinterpret_cast<float*>(nxt), 1, cd[0], Q, rank)) {
+                void* bpk = ctx->buf("umma_pack", static_cast<size_t>(umma_pack_bytes(cd[0], rank)));
+                launch_pack_umma(U[0], gd[0], cd[0], rank, bpk, s);
+                launch_ttm_tc(reinterpret_cast<const float*>(cur), bpk, reinterpret_cast<float*>(nxt), 1, cd[0], Q, rank, s,
+                              true);
+                r.launches += 2;
+                done = true;
+            }
+        }
+        if (!done) r.ttm(cur, upl, nxt, P, cd[n], Q, rank);
         if (n == 0) ++r.passes;
         cd[n] = rank;
         cur = nxt;

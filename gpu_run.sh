@@ -1,3 +1,2 @@
 #!/bin/bash
-timeout 300 python tools/alg2_bench.py
-timeout 400 python -m pytest tests -m gpu -q -x -k "rand_tucker or alg2 or config1 or golden" 2>&1 | tail -2
+for t in 64 128 256 512; do echo "target $t"; TENKIT_QR_TARGET_ROWS=$t timeout 120 python tools/qr_bench.py | head -3; done

@@ -108,12 +108,13 @@ __device__ void reduce_dots(Sh& sh, cg::cluster_group& cl, unsigned cs, int& par
 // Schur complement of the Gram matrix G = Z^T Z, and |R_kk| is its square root; so the
 // pivoted Cholesky of G gives the same pivots and |R_kk|, and Q = Z_P R^{-1} the same
 // columns up to sign (fixed by the sign rule afterwards). One more Cholesky pass on Q
-// (CholeskyQR2) restores orthonormality to ~eps. Taken only when Z is well conditioned
+// (CholeskyQR2, applied to first order: Q1^T Q1 = I + O(eps cond^2)) restores orthonormality
+// to ~eps. Taken only when Z is well conditioned
 // (every R_kk > kFastMinRatio R_00, so the 1e-12 rank cut cannot bite); otherwise the kernel
 // falls through to the Householder path with Z untouched. 3 cluster exchanges instead of
 // one per Householder step.
 // ---------------------------------------------------------------------------------------
-constexpr double kFastMinRatio = 1e-5;
+constexpr double kFastMinRatio = 1e-4;  // cond(Z) <= 1e4: first-order second pass exact to ~1e-16
 
 // gp[a + b n] = sum over own rows of z[:, a] z[:, b] (full symmetric n x n)
 __device__ void gram_partial(const double* z, int ld, int nloc, int n, double* gp) {
@@ -155,106 +156,121 @@ __device__ void gram_reduce(cg::cluster_group& cl, unsigned cs, double* gp, doub
     else __syncthreads();
 }
 
-// Right-looking Cholesky of gs (n x n, full symmetric, destroyed) by one warp, with
+// Right-looking Cholesky of gs (n x n, full symmetric, destroyed) by the whole CTA, with
 // ColPiv pivoting (first largest Schur diagonal) when `pivot`: R (upper, col-major, n x n)
-// into rr, source column of pivot position k into perm[k]. Returns false when a pivot is
-// not positive or R_kk <= kFastMinRatio R_00 (the caller then takes the Householder path).
-__device__ bool warp_pchol(double* gs, int n, bool pivot, double* rr, int* perm) {
-    const int lane = threadIdx.x & 31;
-    for (int j = lane; j < n; j += 32) perm[j] = j;
-    for (int e = lane; e < n * n; e += 32) rr[e] = 0.0;
-    __syncwarp();
+// into rr, 1 / R_kk into rinv, source column of pivot position k into perm[k]. Returns false
+// (CTA-uniform) when a pivot is not positive or R_kk <= kFastMinRatio R_00 (the caller then
+// takes the Householder path). Per step: warp 0 picks the pivot (exact first-max via three
+// warp reductions on the non-negative doubles' bit patterns) and the scalars, all threads
+// swap and update the trailing Schur complement; ~3 block barriers per step.
+__device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rinv, int* perm, int* ctl) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int j = tid; j < n; j += kQrThreads) perm[j] = j;
+    for (int e = tid; e < n * n; e += kQrThreads) rr[e] = 0.0;
+    __syncthreads();
     double r00 = 0.0;
     for (int k = 0; k < n; ++k) {
-        int best = k;
-        if (pivot) {
-            double bv = -1.0;
-            int bi = k;
-            for (int j = k + lane; j < n; j += 32) {
-                const double v = gs[j + j * n];
-                if (v > bv) {
-                    bv = v;
-                    bi = j;
-                }
+        if (tid < 32) {
+            int best = k;
+            if (pivot) {
+                // candidates j = k + lane, k + lane + 32 (n <= 64): first maximum of S_jj >= 0
+                unsigned long long b0 = 0, b1 = 0;
+                const int j0 = k + lane, j1 = k + lane + 32;
+                if (j0 < n) b0 = __double_as_longlong(fmax(gs[j0 + j0 * n], 0.0));
+                if (j1 < n) b1 = __double_as_longlong(fmax(gs[j1 + j1 * n], 0.0));
+                const unsigned long long bm = b0 > b1 ? b0 : b1;
+                const unsigned hi = __reduce_max_sync(0xffffffffu, unsigned(bm >> 32));
+                const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned(bm >> 32) == hi) ? unsigned(bm) : 0u);
+                const unsigned long long top = (static_cast<unsigned long long>(hi) << 32) | lo;
+                const unsigned cand = (j0 < n && b0 == top) ? unsigned(j0) : ((j1 < n && b1 == top) ? unsigned(j1) : 0xffffu);
+                best = static_cast<int>(__reduce_min_sync(0xffffffffu, cand));
+                if (best >= n) best = k;
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ov > bv || (ov == bv && oi < bi)) {
-                    bv = ov;
-                    bi = oi;
-                }
-            }
-            best = bi;
+            if (lane == 0) ctl[0] = best;
         }
-        if (best != k) {  // symmetric swap k <-> best; R rows < k: swap their columns
-            for (int j = lane; j < n; j += 32) {
+        __syncthreads();
+        const int best = ctl[0];
+        if (best != k) {  // symmetric swap k <-> best; rows < k of R: swap their columns
+            for (int j = tid; j < n; j += kQrThreads) {
                 const double t0 = gs[k + j * n];
                 gs[k + j * n] = gs[best + j * n];
                 gs[best + j * n] = t0;
             }
-            __syncwarp();
-            for (int i = lane; i < n; i += 32) {
+            __syncthreads();
+            for (int i = tid; i < n; i += kQrThreads) {
                 const double t0 = gs[i + k * n];
                 gs[i + k * n] = gs[i + best * n];
                 gs[i + best * n] = t0;
             }
-            for (int i = lane; i < k; i += 32) {
+            for (int i = tid; i < k; i += kQrThreads) {
                 const double t0 = rr[i + k * n];
                 rr[i + k * n] = rr[i + best * n];
                 rr[i + best * n] = t0;
             }
-            if (lane == 0) {
+            if (tid == 0) {
                 const int t0 = perm[k];
                 perm[k] = perm[best];
                 perm[best] = t0;
             }
-            __syncwarp();
+            __syncthreads();
         }
         const double d = gs[k + k * n];
         if (k == 0) r00 = d > 0.0 ? sqrt(d) : 0.0;
-        if (!(d > 0.0)) return false;
-        const double rkk = sqrt(d);
-        if (!(rkk > kFastMinRatio * r00)) return false;
+        const double rkk = d > 0.0 ? sqrt(d) : 0.0;
+        if (!(d > 0.0) || !(rkk > kFastMinRatio * r00)) return false;  // uniform: same values everywhere
         const double inv = 1.0 / rkk;
-        for (int j = k + lane; j < n; j += 32) rr[k + j * n] = j == k ? rkk : gs[k + j * n] * inv;
-        __syncwarp();
-        // trailing Schur complement, lane j owns column j (all rows > k): loads before stores
-        for (int j = k + 1 + lane; j < n; j += 32) {
-            const double rkj = rr[k + j * n];
-            double* col = gs + size_t(j) * n;
-            int i = k + 1;
-            for (; i + 4 <= n; i += 4) {
-                const double c0 = col[i], c1 = col[i + 1], c2 = col[i + 2], c3 = col[i + 3];
-                const double q0 = rr[k + i * n], q1 = rr[k + (i + 1) * n], q2 = rr[k + (i + 2) * n],
-                             q3 = rr[k + (i + 3) * n];
-                col[i] = fma(-q0, rkj, c0);
-                col[i + 1] = fma(-q1, rkj, c1);
-                col[i + 2] = fma(-q2, rkj, c2);
-                col[i + 3] = fma(-q3, rkj, c3);
-            }
-            for (; i < n; ++i) col[i] = fma(-rr[k + i * n], rkj, col[i]);
+        const int m = n - k - 1;
+        // trailing update S_ij -= (S_ki / R_kk)(S_kj / R_kk), i, j > k; the diagonal threads
+        // also write row k of R
+        for (int e = tid; e < m * m; e += kQrThreads) {
+            const int i = k + 1 + e % m, j = k + 1 + e / m;
+            const double rki = gs[k + i * n] * inv, rkj = gs[k + j * n] * inv;
+            gs[i + j * n] = fma(-rki, rkj, gs[i + j * n]);
+            if (i == j) rr[k + j * n] = rkj;
         }
-        __syncwarp();
+        if (tid == 0) {
+            rr[k + k * n] = rkk;
+            rinv[k] = inv;
+        }
+        __syncthreads();
     }
     return true;
 }
 
-// out[:, j] = (in[:, perm[j]] - sum_{k<j} out[:, k] R_kj) / R_jj, one thread per own row
-__device__ void trsm_rows(const double* in, double* out, int ld, int nloc, int n, const double* rr, const int* perm) {
-    for (int i = threadIdx.x; i < nloc; i += kQrThreads) {
-        for (int j = 0; j < n; ++j) {
-            double a0 = in[i + size_t(perm[j]) * ld], a1 = 0.0;
-            const double* rj = rr + size_t(j) * n;
-            int k = 0;
-            for (; k + 2 <= j; k += 2) {
-                a0 = fma(-out[i + size_t(k) * ld], rj[k], a0);
-                a1 = fma(-out[i + size_t(k + 1) * ld], rj[k + 1], a1);
+// X = R^{-1} (upper triangular, n x n col-major) by one warp, lanes over the columns j:
+// X_jj = 1 / R_jj, X_ij = -(sum_{k=i+1..j} R_ik X_kj) / R_ii for i < j (rolled loops)
+__device__ void warp_tri_inv(const double* rr, const double* rinv, int n, double* x) {
+    const int lane = threadIdx.x & 31;
+    for (int j = lane; j < n; j += 32) {
+        double* xj = x + size_t(j) * n;
+        for (int i = j + 1; i < n; ++i) xj[i] = 0.0;
+        xj[j] = rinv[j];
+        for (int i = j - 1; i >= 0; --i) {
+            double a0 = 0.0, a1 = 0.0;
+            int k = i + 1;
+            for (; k + 2 <= j + 1; k += 2) {
+                a0 = fma(rr[i + size_t(k) * n], xj[k], a0);
+                a1 = fma(rr[i + size_t(k + 1) * n], xj[k + 1], a1);
             }
-            if (k < j) a0 = fma(-out[i + size_t(k) * ld], rj[k], a0);
-            out[i + size_t(j) * ld] = (a0 + a1) / rj[j];
+            if (k <= j) a0 = fma(rr[i + size_t(k) * n], xj[k], a0);
+            xj[i] = -(a0 + a1) * rinv[i];
         }
+    }
+}
+
+// out[:, j] = sum_{k <= j} in[:, perm[k]] X[k, j] for the own rows (X upper triangular)
+__device__ void apply_upper(const double* in, double* out, int ld, int nloc, int n, const double* x, const int* perm) {
+    for (int e = threadIdx.x; e < nloc * n; e += kQrThreads) {
+        const int i = e % nloc, j = e / nloc;
+        const double* xj = x + size_t(j) * n;
+        double a0 = 0.0, a1 = 0.0;
+        int k = 0;
+        for (; k + 2 <= j + 1; k += 2) {
+            a0 = fma(in[i + size_t(perm[k]) * ld], xj[k], a0);
+            a1 = fma(in[i + size_t(perm[k + 1]) * ld], xj[k + 1], a1);
+        }
+        if (k <= j) a0 = fma(in[i + size_t(perm[k]) * ld], xj[k], a0);
+        out[i + size_t(j) * ld] = a0 + a1;
     }
 }
 
@@ -319,34 +335,41 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         double* r2 = r1 + n * n;                               // n x n R of pass 2
         int* perm = reinterpret_cast<int*>(r2 + n * n);        // n: pivot order of pass 1
         int* perm2 = perm + kMaxRank;                          // n: (identity) of pass 2
-        int* ident = perm2 + kMaxRank;                         // n
-        int* okf = ident + kMaxRank;                           // 2 flags
+        int* ctl = perm2 + kMaxRank;                           // scratch
+        double* rinv1 = sh.upd;                                // 1 / R_kk (the Householder
+                                                               // norms are not in use yet)
         gram_partial(z, ld, nloc, n, gp);
         gram_reduce(cl, cs, gp, gs, n);
-        if (warp == 0) {
-            const bool ok = warp_pchol(gs, n, true, r1, perm);
-            if (lane == 0) okf[0] = ok ? 1 : 0;
-        }
-        __syncthreads();
-        if (okf[0]) {  // identical in every CTA (same reduced Gram, same arithmetic)
-            trsm_rows(z, q, ld, nloc, n, r1, perm);
+        QR_MARK(600);
+        const bool ok1 = cta_pchol(gs, n, true, r1, rinv1, perm, ctl);
+        QR_MARK(601);
+        if (ok1) {  // identical in every CTA (same reduced Gram, same arithmetic)
+            // Q1 = Z_P R1^{-1} with R1^{-1} formed explicitly (parallel application)
+            if (warp == 0) warp_tri_inv(r1, rinv1, n, r2);
             __syncthreads();
+            apply_upper(z, q, ld, nloc, n, r2, perm);
+            __syncthreads();
+            QR_MARK(602);
+            // second pass, to first order: Q1^T Q1 = I + E (E ~ eps cond^2 <= 1e-8), its
+            // Cholesky factor is I + V with V = strict_upper(E) + diag(E) / 2, so
+            // Q = Q1 (I + V)^{-1} = Q1 (I - V) + O(E^2) and R_kk = R1_kk (1 + V_kk)
             gram_partial(q, ld, nloc, n, gp);
             gram_reduce(cl, cs, gp, gs, n);
-            if (warp == 0) {
-                for (int j = lane; j < n; j += 32) ident[j] = j;
-                __syncwarp();
-                const bool ok = warp_pchol(gs, n, false, r2, perm2);
-                if (lane == 0) okf[1] = ok ? 1 : 0;
+            QR_MARK(603);
+            for (int e = tid; e < n * n; e += kQrThreads) {
+                const int a = e % n, b = e / n;
+                const double g = gs[e] - (a == b ? 1.0 : 0.0);
+                r2[e] = a < b ? -g : (a == b ? 1.0 - 0.5 * g : 0.0);  // I - V
             }
+            for (int k = tid; k < n; k += kQrThreads) perm2[k] = k;
             __syncthreads();
-            if (okf[1]) {
-                trsm_rows(q, z, ld, nloc, n, r2, ident);
-                for (int k = tid; k < n; k += kQrThreads) sh.beta[k] = r2[k + k * n] * r1[k + k * n];
-                __syncthreads();
-                fast_ok = true;
-                rank = n;
-            }
+            QR_MARK(604);
+            apply_upper(q, z, ld, nloc, n, r2, perm2);
+            for (int k = tid; k < n; k += kQrThreads) sh.beta[k] = r1[k + k * n] * (1.0 + 0.5 * (gs[k + k * n] - 1.0));
+            __syncthreads();
+            fast_ok = true;
+            rank = n;
+            QR_MARK(605);
         }
     }
 
@@ -619,7 +642,10 @@ int pick_cluster(int64_t rows, int ncols, int* ld_out, size_t* smem_out) {
     // The QR is latency-bound per Householder step; spreading the rows so that each CTA holds
     // <= 128 of them cuts the per-step reduction and update work (1000 x 30: 8 CTAs, ~30%
     // faster than the 2 the shared memory alone needs; measured with tools/qr_trace.cu).
-    constexpr int kTargetRows = 128;
+    static const int kTargetRows = [] {
+        const char* e = std::getenv("TENKIT_QR_TARGET_ROWS");
+        return e ? std::max(16, std::atoi(e)) : 128;
+    }();
     for (int cs = min_cs; cs <= 16; cs *= 2) {
         const int ld = static_cast<int>((rows + cs - 1) / cs);
         const size_t smem = size_t(ld) * ncols * sizeof(double) + kQrFixedSmem;

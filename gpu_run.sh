@@ -1,2 +1,3 @@
 #!/bin/bash
-for t in 64 128 256 512; do echo "target $t"; TENKIT_QR_TARGET_ROWS=$t timeout 120 python tools/qr_bench.py | head -3; done
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k repeated 2>&1 | tail -2
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -1

@@ -48,6 +48,14 @@ void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int6
 template <typename T>
 void launch_pack_factor(const double* u, int64_t ld, int64_t rows, int cols, T* up, cudaStream_t s);
 
+// z[i + r ldz] (fp64) = sum_{b,a} x[b + i B + a B I] om[(b + a B) pack_stride(rn) + r]: the
+// sketch unfold(X, n) Omega of a (B, I, A) view without materialising the unfolding (split-K
+// partials in `work`, sketch_work_elems doubles, reduced in fixed order). Returns launches.
+int64_t sketch_work_elems(int64_t I, int rn);
+template <typename T>
+int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* z, int64_t ldz, double* work,
+                  cudaStream_t s);
+
 // Materialise the mode-n unfolding of a (B, I, A) view: out[i + (b + a*B)*I] = x[b + i*B + a*B*I]
 template <typename T>
 void launch_unfold(const T* x, int64_t B, int64_t I, int64_t A, T* out, cudaStream_t s);

@@ -412,6 +412,64 @@ __global__ void gaussian_fill_kernel(double* __restrict__ out, uint64_t n, uint6
     }
 }
 
+// Z (fp64, ldz) = unfold(X, n) Omega for X viewed as (B, I, A): Z[i, r] = sum over
+// k = b + a B of X[b + i B + a B I] Omega[k, r] (tensor.hpp:195-209 unfold_times), without
+// materialising the unfolding. CTA tile 32 rows x 32 columns, split-K over blockIdx.z into
+// fp64 partials summed in fixed order by sketch_reduce_kernel; fp64 accumulation.
+template <typename T>
+__global__ void __launch_bounds__(256) sketch_kernel(const T* __restrict__ x, int B, int64_t I, int A,
+                                                     const T* __restrict__ om, int stride, int rn, int kchunk,
+                                                     double* __restrict__ part) {
+    __shared__ double xs[64][33];
+    __shared__ double os[64][33];
+    const int tid = threadIdx.x, ti = tid & 31, tr = tid >> 5;
+    const int64_t i0 = int64_t(blockIdx.x) * 32;
+    const int r0 = blockIdx.y * 32;
+    const int K = B * A;
+    const int k0 = blockIdx.z * kchunk, k1 = min(K, k0 + kchunk);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int kk = k0; kk < k1; kk += 64) {
+        for (int e = tid; e < 64 * 32; e += 256) {
+            const int kl = e >> 5, il = e & 31;
+            const int k = kk + kl;
+            const int64_t i = i0 + il;
+            double v = 0.0;
+            if (k < k1 && i < I) {
+                const int b = k % B, a = k / B;
+                v = static_cast<double>(x[b + i * B + int64_t(a) * B * I]);
+            }
+            xs[kl][il] = v;
+            const int r = r0 + il;
+            os[kl][il] = (k < k1 && r < rn) ? static_cast<double>(om[int64_t(k) * stride + r]) : 0.0;
+        }
+        __syncthreads();
+        const int kn = min(64, k1 - kk);
+        for (int k = 0; k < kn; ++k) {
+            const double xv = xs[k][ti];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = fma(xv, os[k][tr * 4 + j], acc[j]);
+        }
+        __syncthreads();
+    }
+    const int64_t i = i0 + ti;
+    if (i < I)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = r0 + tr * 4 + j;
+            if (r < rn) part[(int64_t(blockIdx.z) * rn + r) * I + i] = acc[j];
+        }
+}
+
+__global__ void sketch_reduce_kernel(const double* __restrict__ part, int64_t I, int rn, int S, double* __restrict__ z,
+                                     int64_t ldz) {
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < I * rn; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = t % I, r = t / I;
+        double v = 0.0;
+        for (int sidx = 0; sidx < S; ++sidx) v += part[(int64_t(sidx) * rn + r) * I + i];
+        z[i + r * ldz] = v;
+    }
+}
+
 // out[i + c*I] = x[b + i*B + a*B*I], c = b + a*B: the mode-n unfolding of a (B, I, A) view
 template <typename T>
 __global__ void unfold_kernel(const T* __restrict__ x, int64_t B, int64_t I, int64_t A, T* __restrict__ out) {
@@ -503,6 +561,30 @@ void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t 
     TK_LAUNCH_CHECK();
 }
 
+
+int64_t sketch_work_elems(int64_t I, int rn) { return I * rn * 16; }
+
+template <typename T>
+int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* z, int64_t ldz, double* work,
+                  cudaStream_t s) {
+    require(B * A < (int64_t(1) << 31), "unfold_times: unfolding too wide");
+    const int K = static_cast<int>(B * A);
+    const unsigned gx = static_cast<unsigned>((I + 31) / 32), gy = static_cast<unsigned>((rn + 31) / 32);
+    // split K so the grid covers ~2 waves, at most 16 splits, at least 64 k per split
+    int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, (2 * 148 + gx * gy - 1) / (gx * gy))));
+    S = std::max(1, std::min(S, (K + 63) / 64));
+    const int kchunk = ((K + S - 1) / S + 63) / 64 * 64;
+    S = (K + kchunk - 1) / kchunk;
+    sketch_kernel<T><<<dim3(gx, gy, S), 256, 0, s>>>(x, static_cast<int>(B), I, static_cast<int>(A), om, pack_stride(rn), rn,
+                                                     kchunk, work);
+    sketch_reduce_kernel<<<grid_for(I * rn), 256, 0, s>>>(work, I, rn, S, z, ldz);
+    TK_LAUNCH_CHECK();
+    return 2;
+}
+template int launch_sketch<float>(const float*, int64_t, int64_t, int64_t, const float*, int, double*, int64_t, double*,
+                                  cudaStream_t);
+template int launch_sketch<double>(const double*, int64_t, int64_t, int64_t, const double*, int, double*, int64_t, double*,
+                                   cudaStream_t);
 
 template <typename T>
 void launch_unfold(const T* x, int64_t B, int64_t I, int64_t A, T* out, cudaStream_t s) {

@@ -34,6 +34,30 @@ struct tk_context {
     int* rank_host = nullptr;  // pinned
     cudaStream_t side = nullptr;  // second stream: next Y pass overlapped with the current QR
     cudaEvent_t ev_free = nullptr, ev_fs = nullptr;
+    cudaStream_t cap = nullptr;   // private stream the CUDA graph is captured on
+    cudaEvent_t ev_cap = nullptr;
+    // A repeated rand_tucker_2i call (same shapes, seed, input pointer and options) is captured
+    // once as a CUDA graph and replayed: one launch per decomposition instead of ~60.
+    struct Graph {
+        std::string key;
+        int seen = 0;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<cudaEvent_t> marks;  // Y-pass timing events (time_kernels)
+        double* core = nullptr;
+        std::vector<double*> U;
+        std::vector<int64_t> cshape, cols;
+        int64_t gsize = 0;
+        int passes = 0, launches = 0;
+        std::vector<int> rt;
+        uint64_t buf_gen = 0;
+        void reset() {
+            if (exec) cudaGraphExecDestroy(exec);
+            exec = nullptr;
+            for (auto e : marks) cudaEventDestroy(e);
+            marks.clear();
+            seen = 0;
+        }
+    } g2i;
 
     void ensure_side() {
         if (!side) {
@@ -47,9 +71,11 @@ struct tk_context {
         }
     }
 
+    uint64_t buf_gen = 0;  // bumped whenever a buffer is (re)allocated: captured graphs go stale
     void* buf(const std::string& name, size_t bytes) {
         auto& e = bufs[name];
         if (e.second < bytes) {
+            ++buf_gen;
             if (e.first) TK_CUDA(cudaFree(e.first));
             e.first = nullptr;
             TK_CUDA(cudaMalloc(&e.first, std::max<size_t>(bytes, 256)));
@@ -58,6 +84,9 @@ struct tk_context {
         return e.first;
     }
     ~tk_context() {
+        g2i.reset();
+        if (ev_cap) cudaEventDestroy(ev_cap);
+        if (cap) cudaStreamDestroy(cap);
         for (auto& kv : bufs)
             if (kv.second.first) cudaFree(kv.second.first);
         if (rank_host) cudaFreeHost(rank_host);
@@ -129,10 +158,14 @@ struct TuckerRun {
     ~TuckerRun() {
         for (auto e : ev) cudaEventDestroy(e);
     }
+    bool capture = false;        // compute only: no host syncs, outputs stay in context buffers
+    double* core_out = nullptr;  // capture: the fp64 core (context buffer)
+    std::vector<int64_t> core_shape;
     void mark() {
         cudaEvent_t e;
         TK_CUDA(cudaEventCreate(&e));
-        TK_CUDA(cudaEventRecord(e, s));
+        // in a captured graph the record must be an external event node to be re-recorded
+        TK_CUDA(capture ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s));
         ev.push_back(e);
     }
     double streamed_ms() {
@@ -271,24 +304,15 @@ struct TuckerRun {
         if (buf != c.xbuf) TK_CUDA(cudaMemcpyAsync(buf, c.xbuf, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
 
-    // Z = unfold(X, n) * Omega (tensor.hpp:195-209): X is small, so its mode-n unfolding is
-    // materialised and multiplied by the packed Omega with the same TTM kernel as the Y
-    // passes; Z (T) is widened to fp64 into z (leading dimension ldz) for the QR.
+    // Z = unfold(X, n) * Omega (tensor.hpp:195-209) straight into fp64 z (leading dimension
+    // ldz) for the QR: one split-K kernel over the (B, I, A) view, no materialised unfolding.
     void sketch(const T* x, const std::vector<int64_t>& xd, int n, const T* omp, int rn, double* z, int64_t ldz) {
         const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + n));
         const int64_t I = xd[n];
         const int64_t A = prod(std::vector<int64_t>(xd.begin() + n + 1, xd.end()));
-        const T* xu = x;
-        if (B > 1) {
-            T* b = static_cast<T*>(ctx->buf("xunf", sizeof(T) * B * I * A));
-            launch_unfold<T>(x, B, I, A, b, s);
-            ++launches;
-            xu = b;
-        }
-        T* zt = static_cast<T*>(ctx->buf("zt", sizeof(T) * I * rn));
-        ttm(xu, omp, zt, I, B * A, 1, rn);
-        launch_cast2d<T, double>(zt, I, z, ldz, I, rn, s);
-        ++launches;
+        double* work = static_cast<double*>(ctx->buf(work_name == std::string("splitk") ? "sketch_part" : "sketch_part_side",
+                                                     sizeof(double) * sketch_work_elems(I, rn)));
+        launches += launch_sketch<T>(x, B, I, A, omp, rn, z, ldz, work, s);
     }
 
     // One range-finding step for mode n: Z = unfold(X, n) Omega, U_n = basis(Z)
@@ -395,7 +419,7 @@ struct TuckerRun {
                 sync_rank(n, step);
             }
         }
-        if (!sync) {  // verify the full-rank speculation
+        if (!sync && !capture) {  // verify the full-rank speculation
             int hr[2 * TK_MAX_ORDER];
             TK_CUDA(cudaMemcpyAsync(hr, rank_dev, sizeof(int) * 2 * order, cudaMemcpyDeviceToHost, s));
             TK_CUDA(cudaStreamSynchronize(s));
@@ -422,6 +446,11 @@ struct TuckerRun {
         else launch_cast<double, double>(reinterpret_cast<const double*>(g), gdv, gsize, s);
         ++launches;
         allreduce(gdv, gsize);
+        if (capture) {
+            core_out = gdv;
+            core_shape = gd;
+            return;
+        }
         // outputs
         const cudaMemcpyKind kind = out->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
         TK_CUDA(cudaMemcpyAsync(out->core, gdv, sizeof(double) * gsize, kind, s));
@@ -557,6 +586,98 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
     TK_CUDA(cudaStreamSynchronize(s));
 }
 
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TENKIT_NO_GRAPH");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+// Replays (or, on the second identical call, captures) the decomposition as a CUDA graph on
+// the context's private stream, then copies the model out and verifies the speculated ranks.
+// Returns false when the eager path must run (first sighting of this call, or a rank drop).
+template <typename T>
+bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, const T* ydev,
+              const std::vector<int64_t>& rk, int64_t p, const Seed& seed, const tk_tucker_opts& opt, tk_tucker_out* out,
+              tk_tucker_stats* stats) {
+    std::string key = std::to_string(sizeof(T)) + "|" + std::to_string(reinterpret_cast<uintptr_t>(ydev)) + "|" +
+                      std::to_string(p) + "|" + std::to_string(seed.root) + "|" + std::to_string(seed.stream) + "|" +
+                      std::to_string(opt.explicit_core_pass) + std::to_string(opt.overlap) +
+                      std::to_string(opt.time_kernels) + "|" + std::to_string(ctx->ttm_path);
+    for (int64_t n = 0; n < order; ++n) key += "|" + std::to_string(ld[n]) + "x" + std::to_string(rk[n]);
+    auto& g = ctx->g2i;
+    if (g.key != key || (g.exec && g.buf_gen != ctx->buf_gen)) {
+        g.reset();
+        g.key = key;
+    }
+    if (!g.exec) {
+        if (g.seen++ == 0) return false;  // first sighting: eager (allocates every buffer)
+        if (!ctx->cap) {
+            TK_CUDA(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+            TK_CUDA(cudaEventCreateWithFlags(&ctx->ev_cap, cudaEventDisableTiming));
+        }
+        ctx->ensure_side();
+        TuckerRun<T> r{ctx, ctx->cap, order, ld, ld, 0, ydev};
+        r.time_kernels = opt.time_kernels != 0;
+        r.capture = true;
+        cudaGraph_t graph = nullptr;
+        TK_CUDA(cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal));
+        try {
+            r.run(rk, p, seed, opt, out, nullptr);
+        } catch (...) {
+            cudaStreamEndCapture(ctx->cap, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            g.reset();
+            throw;
+        }
+        TK_CUDA(cudaStreamEndCapture(ctx->cap, &graph));
+        const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        TK_CUDA(ie);
+        g.marks.swap(r.ev);  // the graph records these events on every replay
+        g.core = r.core_out;
+        g.cshape = r.core_shape;
+        g.gsize = prod(r.core_shape);
+        g.U = r.U;
+        g.cols = std::vector<int64_t>(r.cols.begin(), r.cols.end());
+        g.rt = r.rt;
+        g.passes = r.passes;
+        g.launches = r.launches;
+        g.buf_gen = ctx->buf_gen;
+    }
+    cudaStream_t s = ctx->stream;
+    TK_CUDA(cudaGraphLaunch(g.exec, s));
+    int hr[2 * TK_MAX_ORDER] = {0};
+    const int* rank_dev = static_cast<const int*>(ctx->buf("ranks", sizeof(int) * 2 * TK_MAX_ORDER));
+    TK_CUDA(cudaMemcpyAsync(hr, rank_dev, sizeof(int) * 2 * order, cudaMemcpyDeviceToHost, s));
+    const cudaMemcpyKind kind = out->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    TK_CUDA(cudaMemcpyAsync(out->core, g.core, sizeof(double) * g.gsize, kind, s));
+    for (int64_t n = 0; n < order; ++n) {
+        out->core_shape[n] = g.cshape[n];
+        out->factor_cols[n] = g.cols[n];
+        TK_CUDA(cudaMemcpyAsync(out->factors[n], g.U[n], sizeof(double) * ld[n] * g.cols[n], kind, s));
+    }
+    TK_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < 2 * order; ++i)
+        if (hr[i] != g.rt[i % order]) return false;  // a rank dropped: rerun eagerly (synchronous ranks)
+    if (stats) {
+        stats->passes = g.passes;
+        stats->kernel_launches = g.launches;
+        stats->stream_launches = g.passes;
+        double ms = 0.0;
+        for (size_t i = 0; i + 1 < g.marks.size(); i += 2) {
+            float t = 0.f;
+            TK_CUDA(cudaEventElapsedTime(&t, g.marks[i], g.marks[i + 1]));
+            ms += t;
+        }
+        stats->stream_ms = ms;
+        stats->y_bytes = static_cast<double>(prod(ld)) * sizeof(T);
+        for (int i = 0; i < 2 * order; ++i) stats->ranks[i] = hr[i];
+    }
+    return true;
+}
+
 template <typename T>
 void rand_tucker_2i_impl(tk_context* ctx, int64_t order, const int64_t* dims, const void* y, int y_on_device,
                          const int64_t* ranks, int64_t p, Seed seed, const tk_tucker_opts& opt, tk_tucker_out* out,
@@ -580,6 +701,9 @@ void rand_tucker_2i_impl(tk_context* ctx, int64_t order, const int64_t* dims, co
         r.time_kernels = o.time_kernels != 0;
         r.run(rk, p, seed, o, out, stats);
     };
+    if (!opt.sync_ranks && y_on_device && !(ctx->has_comm && ctx->comm.world > 1) && graphs_enabled() &&
+        graph_2i<T>(ctx, order, ld, ydev, rk, p, seed, opt, out, stats))
+        return;
     if (opt.sync_ranks) {
         attempt(opt);
     } else {

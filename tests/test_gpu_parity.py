@@ -237,3 +237,27 @@ def test_errors_mirror_reference(P):
         P.rand_tucker_2i(np.ones((3, 3, 3)), (2, 2), 1, (0, 0))
     with pytest.raises(P.TenkitError, match="tensor dimensions must be positive"):
         P.rand_tucker_2i(np.zeros((6, 5, 4)), (2, 2, 2), 1, (0, 0))  # zero data: rank-0 factor
+
+
+def test_repeated_calls_replay_graph_identically(P, O):
+    """A repeated rand_tucker_2i call is captured as a CUDA graph and replayed: every
+    replay returns the bit-identical model of the eager call, kernel timing still works, and
+    a call that reallocates the context's buffers in between invalidates the graph."""
+    import torch
+    dims = (300, 280, 260)
+    y = O.add_noise(O.gen_tucker(dims, (6, 6, 6), (3, 3)), 20.0, (4, 4)).astype(np.float32)
+    yd = P.DenseTensor.from_numpy(y, np.float32).cuda()
+    ctx = P.Context.default()
+    runs = [P.rand_tucker_2i(yd, (6, 6, 6), 4, (9, 0), sync_ranks=False, out="device", time_kernels=True).to_host()
+            for _ in range(4)]
+    for m in runs[1:]:
+        np.testing.assert_array_equal(m.core, runs[0].core)
+        for a, b in zip(m.factors, runs[0].factors):
+            np.testing.assert_array_equal(a, b)
+        assert m.stats["stream_ms"] > 0 and m.stats["passes"] == 6
+    big = P.DenseTensor.from_numpy(np.ones((400, 390, 380), np.float32), np.float32).cuda()
+    P.rand_tucker_2i(big, (6, 6, 6), 4, (9, 0), sync_ranks=False, out="device")  # grows the buffers
+    again = P.rand_tucker_2i(yd, (6, 6, 6), 4, (9, 0), sync_ranks=False, out="device").to_host()
+    np.testing.assert_array_equal(again.core, runs[0].core)
+    del big
+    torch.cuda.empty_cache()

@@ -261,3 +261,28 @@ def test_repeated_calls_replay_graph_identically(P, O):
     np.testing.assert_array_equal(again.core, runs[0].core)
     del big
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dims,ranks,p,dtype", [
+    ((5, 40, 30), (10, 4, 4), 2, np.float64),       # R + p >= I_0: r~_0 clamped to I_0 (square factor)
+    ((50,), (3,), 2, np.float64),                    # order 1
+    ((6, 5, 4, 5, 6), (2, 2, 2, 2, 2), 1, np.float64),  # order 5
+    ((40, 36, 30), (5, 4, 3), 0, np.float64),        # no oversampling
+    ((37, 41, 43), (4, 5, 3), 3, np.float32),        # fp32, extents not multiples of 4 (FFMA paths)
+    ((200, 100, 70), (60, 10, 10), 4, np.float64),   # r~ = 64, the device maximum
+])
+def test_edge_shapes_match_oracle(P, O, dims, ranks, p, dtype):
+    y = noisy_tucker(O, dims, tuple(min(r, d) for r, d in zip(ranks, dims)), 15.0, (5, 6)).astype(dtype)
+    seed = (21, 0)
+    ref = O.rand_tucker_2i(y.astype(np.float64), ranks, p, seed)
+    got = P.rand_tucker_2i(P.DenseTensor.from_numpy(y, dtype), ranks, p, seed)
+    compare_models(O, y.astype(np.float64), got, ref, F64_TOL if dtype == np.float64 else F32_TOL)
+    ref2 = O.rand_tucker(y.astype(np.float64), ranks, p, seed)
+    got2 = P.rand_tucker(P.DenseTensor.from_numpy(y, dtype), ranks, p, seed)
+    compare_models(O, y.astype(np.float64), got2, ref2, F64_TOL if dtype == np.float64 else F32_TOL)
+
+
+def test_device_rank_limit_is_an_error(P, O):
+    y = rt(O, (200, 100, 70), 3)
+    with pytest.raises(P.TenkitError, match="rank \\+ oversample must be <= 64"):
+        P.rand_tucker_2i(y, (61, 10, 10), 4, (1, 0))

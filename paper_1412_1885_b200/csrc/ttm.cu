@@ -430,7 +430,8 @@ __global__ void __launch_bounds__(256) sketch_kernel(const T* __restrict__ x, in
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int kk = k0; kk < k1; kk += 64) {
         for (int e = tid; e < 64 * 32; e += 256) {
-            const int kl = e >> 5, il = e & 31;
+            // coalesced: consecutive threads walk the contiguous index (i when B == 1, else b)
+            const int kl = B == 1 ? (e >> 5) : (e & 63), il = B == 1 ? (e & 31) : (e >> 6);
             const int k = kk + kl;
             const int64_t i = i0 + il;
             double v = 0.0;
@@ -439,8 +440,11 @@ __global__ void __launch_bounds__(256) sketch_kernel(const T* __restrict__ x, in
                 v = static_cast<double>(x[b + i * B + int64_t(a) * B * I]);
             }
             xs[kl][il] = v;
-            const int r = r0 + il;
-            os[kl][il] = (k < k1 && r < rn) ? static_cast<double>(om[int64_t(k) * stride + r]) : 0.0;
+        }
+        for (int e = tid; e < 64 * 32; e += 256) {
+            const int kl = e >> 5, rl = e & 31;
+            const int k = kk + kl, r = r0 + rl;
+            os[kl][rl] = (k < k1 && r < rn) ? static_cast<double>(om[int64_t(k) * stride + r]) : 0.0;
         }
         __syncthreads();
         const int kn = min(64, k1 - kk);

@@ -1,2 +1,4 @@
 #!/bin/bash
-for gr in 0 1 0 1; do TENKIT_NO_GRAPH=$gr timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_q.log 2> gpurun_out/bench_q.err; echo "no_graph=$gr $(tail -1 gpurun_out/bench_q.log | python -c "import json,sys; d=json.load(sys.stdin); print(d['value'], d['ms_per_step'], d['roofline']['achieved'], d['clocks']['sm_mhz'])")"; done
+timeout 120 python tools/ffcp_exp.py 2>&1 | grep -E "mode-step|ldlt cycles"
+timeout 120 python tools/ffcp_bench.py 200 2>&1 | grep -E "persistent|max"
+timeout 300 python -m pytest tests -m gpu -q -x -k "ffcp or golden or cpp or fit" 2>&1 | tail -1

@@ -417,9 +417,60 @@ __device__ __forceinline__ void pivot_order(const double* t, int R, double ridge
     __syncwarp();
 }
 
+// R <= 32: lane i keeps row i of the permuted matrix in registers; right-looking, one step
+// per column k with the column of L broadcast through shared memory. Every entry receives
+// the same updates in the same order, with the same expression, as the left-looking loop
+// below (fma(-(L_ik L_jk), D_k, a_ij)), so both produce the same factors.
+__device__ __noinline__ void warp_ldlt_reg(const double* t, int R, double ridge, double* f, int* sig, double* colk) {
+    const int lane = threadIdx.x & 31;
+    pivot_order(t, R, ridge, sig);
+    const int si = lane < R ? sig[lane] : 0;
+    double row[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) row[j] = (lane < R && j < R) ? t[si + sig[j] * R] + (lane == j ? ridge : 0.0) : 0.0;
+#pragma unroll 1
+    for (int k = 0; k < R; ++k) {
+        double rk = 0.0;
+        switch (k) {  // row[k]: k is warp-uniform, so one indexed branch instead of a select chain
+#define TK_ROW_CASE(c) \
+    case c:            \
+        rk = row[c];   \
+        break;
+            TK_ROW_CASE(0) TK_ROW_CASE(1) TK_ROW_CASE(2) TK_ROW_CASE(3) TK_ROW_CASE(4) TK_ROW_CASE(5) TK_ROW_CASE(6)
+            TK_ROW_CASE(7) TK_ROW_CASE(8) TK_ROW_CASE(9) TK_ROW_CASE(10) TK_ROW_CASE(11) TK_ROW_CASE(12)
+            TK_ROW_CASE(13) TK_ROW_CASE(14) TK_ROW_CASE(15) TK_ROW_CASE(16) TK_ROW_CASE(17) TK_ROW_CASE(18)
+            TK_ROW_CASE(19) TK_ROW_CASE(20) TK_ROW_CASE(21) TK_ROW_CASE(22) TK_ROW_CASE(23) TK_ROW_CASE(24)
+            TK_ROW_CASE(25) TK_ROW_CASE(26) TK_ROW_CASE(27) TK_ROW_CASE(28) TK_ROW_CASE(29) TK_ROW_CASE(30)
+            TK_ROW_CASE(31)
+#undef TK_ROW_CASE
+            default:
+                break;
+        }  // row[k] (dynamic index)
+        const double d = __shfl_sync(0xffffffffu, rk, k);
+        const bool nz = fabs(d) > 0.0;
+        const double inv = nz ? 1.0 / d : 0.0;
+        const double l = (lane > k && lane < R) ? (nz ? rk * inv : rk) : 0.0;
+        if (lane > k && lane < R) f[lane + k * R] = l;
+        if (lane == k) f[k + k * R] = d;
+        colk[lane] = l * d;  // L(j,k) D(k), zero for j <= k
+        __syncwarp();
+        // trailing update of the whole row, no masks: entries above the diagonal are never
+        // read (row[k] of lane k is the diagonal; lanes i < k have l = 0)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) row[j] = fma(-l, colk[j], row[j]);
+        __syncwarp();
+    }
+}
+
 __device__ __forceinline__ void warp_ldlt(const double* t, int R, double ridge, double* a, int* sig,
                                           unsigned long long* pr = nullptr) {
     const int lane = threadIdx.x & 31;
+    if (R <= 32) {  // the factor loop in registers (scratch: the R x R area after the matrix)
+        if (pr && lane == 0) pr[0] = pr[1] = pr[2] = clock64();
+        warp_ldlt_reg(t, R, ridge, a, sig, a + R * R);
+        if (pr && lane == 0) pr[3] = clock64();
+        return;
+    }
     if (pr && lane == 0) pr[0] = clock64();
     pivot_order(t, R, ridge, sig);
     if (pr && lane == 0) pr[1] = clock64();

@@ -1,4 +1,7 @@
 #!/bin/bash
-timeout 120 python tools/ffcp_exp.py 2>&1 | grep -E "mode-step|ldlt cycles"
-timeout 120 python tools/ffcp_bench.py 200 2>&1 | grep -E "persistent|max"
-timeout 300 python -m pytest tests -m gpu -q -x -k "ffcp or golden or cpp or fit" 2>&1 | tail -1
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu"
+$CMD > gpurun_out/plain.log 2>&1; rc=$?; echo "plain rc=$rc"
+if [ $rc -eq 0 ]; then
+  ncu --set full --clock-control none -k regex:sketch_kernel -s 20 -c 1 -o gpurun_out/prof_sketch $CMD > gpurun_out/ncu3.log 2>&1
+  echo "ncu rc=$?"
+fi

@@ -1,7 +1,4 @@
 #!/bin/bash
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu"
-$CMD > gpurun_out/plain.log 2>&1; rc=$?; echo "plain rc=$rc"
-if [ $rc -eq 0 ]; then
-  ncu --set full --clock-control none -k regex:sketch_kernel -s 20 -c 1 -o gpurun_out/prof_sketch $CMD > gpurun_out/ncu3.log 2>&1
-  echo "ncu rc=$?"
-fi
+timeout 60 ./tools/qr_trace_new | grep -E "fast"
+timeout 120 python tools/qr_bench.py
+timeout 400 python -m pytest tests -m gpu -q -x -k "qr or basis or golden or parity or dist or edge" 2>&1 | tail -2

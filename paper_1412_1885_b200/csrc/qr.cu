@@ -237,6 +237,66 @@ __device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rin
     return true;
 }
 
+// n <= 32: the pivoted Cholesky by one warp with lane i keeping row i of the Gram matrix in
+// registers and its Schur diagonal in `dg`; no physical swaps: the pivot of step k is the
+// first largest remaining diagonal (original index order), its column reaches every lane
+// through one indexed branch (k-uniform), and the unmasked trailing update leaves finished
+// rows/columns untouched (their multipliers are zero). Step k stores l_i = S_ip / d into
+// lraw[k n + i] (1 at the pivot) and sqrt(d) into rdk[k]; R is assembled afterwards.
+__device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lraw, double* rdk, int* perm, double* colk) {
+    const int lane = threadIdx.x & 31;
+    double row[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) row[j] = (lane < n && j < n) ? gs[lane + j * n] : 0.0;
+    double dg = lane < n ? gs[lane + lane * n] : 0.0;
+    bool done = lane >= n;
+    double r00 = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+        // first maximum of the remaining Schur diagonal (exact, lowest index on ties)
+        const unsigned long long key = done ? 0ull : static_cast<unsigned long long>(__double_as_longlong(fmax(dg, 0.0)));
+        const unsigned hi = __reduce_max_sync(0xffffffffu, unsigned(key >> 32));
+        const unsigned lo = __reduce_max_sync(0xffffffffu, unsigned(key >> 32) == hi ? unsigned(key) : 0u);
+        const bool cand = !done && key == ((static_cast<unsigned long long>(hi) << 32) | lo);
+        const int pv = static_cast<int>(__reduce_min_sync(0xffffffffu, cand ? unsigned(lane) : 0xffffu));
+        const double d = __shfl_sync(0xffffffffu, dg, pv & 31);
+        if (k == 0) r00 = d > 0.0 ? sqrt(d) : 0.0;
+        const double rkk = d > 0.0 ? sqrt(d) : 0.0;
+        if (pv >= n || !(d > 0.0) || !(rkk > kFastMinRatio * r00)) return false;
+        double cp = 0.0;
+        switch (pv) {  // row[pv]: pv is warp-uniform
+#define TK_ROW_CASE(c) \
+    case c:            \
+        cp = row[c];   \
+        break;
+            TK_ROW_CASE(0) TK_ROW_CASE(1) TK_ROW_CASE(2) TK_ROW_CASE(3) TK_ROW_CASE(4) TK_ROW_CASE(5) TK_ROW_CASE(6)
+            TK_ROW_CASE(7) TK_ROW_CASE(8) TK_ROW_CASE(9) TK_ROW_CASE(10) TK_ROW_CASE(11) TK_ROW_CASE(12)
+            TK_ROW_CASE(13) TK_ROW_CASE(14) TK_ROW_CASE(15) TK_ROW_CASE(16) TK_ROW_CASE(17) TK_ROW_CASE(18)
+            TK_ROW_CASE(19) TK_ROW_CASE(20) TK_ROW_CASE(21) TK_ROW_CASE(22) TK_ROW_CASE(23) TK_ROW_CASE(24)
+            TK_ROW_CASE(25) TK_ROW_CASE(26) TK_ROW_CASE(27) TK_ROW_CASE(28) TK_ROW_CASE(29) TK_ROW_CASE(30)
+            TK_ROW_CASE(31)
+#undef TK_ROW_CASE
+            default:
+                break;
+        }
+        const bool piv = lane == pv;
+        const double l = (done || piv) ? 0.0 : cp / d;
+        if (lane < n) lraw[k * n + lane] = piv ? 1.0 : l;
+        if (piv) {
+            done = true;
+            perm[k] = pv;
+            rdk[k] = rkk;
+        }
+        colk[lane] = l * d;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) row[j] = fma(-l, colk[j], row[j]);
+        dg = fma(-l, colk[lane], dg);
+        __syncwarp();
+    }
+    return true;
+}
+
 // X = R^{-1} (upper triangular, n x n col-major) by one warp, lanes over the columns j:
 // X_jj = 1 / R_jj, X_ij = -(sum_{k=i+1..j} R_ik X_kj) / R_ii for i < j (rolled loops)
 __device__ void warp_tri_inv(const double* rr, const double* rinv, int n, double* x) {
@@ -341,7 +401,25 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         gram_partial(z, ld, nloc, n, gp);
         gram_reduce(cl, cs, gp, gs, n);
         QR_MARK(600);
-        const bool ok1 = cta_pchol(gs, n, true, r1, rinv1, perm, ctl);
+        bool ok1;
+        if (n <= 32) {  // registers, one warp; lraw (n x n) and the step diagonals in r2 / sh.dir
+            if (warp == 0) {
+                const bool ok = warp_pchol_reg(gs, n, r2, sh.dir, perm, sh.wv);
+                if (lane == 0) ctl[0] = ok ? 1 : 0;
+            }
+            __syncthreads();
+            ok1 = ctl[0] != 0;
+            if (ok1) {  // R[k][m] = sqrt(d_k) l^{(k)}_{perm[m]} (m > k), R_kk = sqrt(d_k)
+                for (int e = tid; e < n * n; e += kQrThreads) {
+                    const int k = e % n, m = e / n;
+                    r1[e] = m < k ? 0.0 : (m == k ? sh.dir[k] : sh.dir[k] * r2[k * n + perm[m]]);
+                }
+                for (int k = tid; k < n; k += kQrThreads) rinv1[k] = 1.0 / sh.dir[k];
+                __syncthreads();
+            }
+        } else {
+            ok1 = cta_pchol(gs, n, true, r1, rinv1, perm, ctl);
+        }
         QR_MARK(601);
         if (ok1) {  // identical in every CTA (same reduced Gram, same arithmetic)
             // Q1 = Z_P R1^{-1} with R1^{-1} formed explicitly (parallel application)

@@ -1,4 +1,2 @@
 #!/bin/bash
-timeout 60 ./tools/qr_trace_new | grep -E "fast"
-timeout 120 python tools/qr_bench.py
-timeout 400 python -m pytest tests -m gpu -q -x -k "qr or basis or golden or parity or dist or edge" 2>&1 | tail -2
+for g in 148 96 64 32 16; do echo "grid $g"; TENKIT_FFCP_GRID=$g timeout 120 python tools/ffcp_bench.py 200 2>&1 | grep -E "persistent" | grep -v max; done

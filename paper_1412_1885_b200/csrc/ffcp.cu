@@ -1062,7 +1062,8 @@ void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* co
                                      static_cast<int>(smem)));
         TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffcp_persistent_kernel, kPThreads, smem));
         require(per_sm >= 1, "ffcp: persistent kernel does not fit an SM");
-        const int G = nsm;  // one CTA per SM (co-resident by construction)
+        int G = nsm;  // one CTA per SM (co-resident by construction)
+        if (const char* ge = std::getenv("TENKIT_FFCP_GRID")) G = std::max(2, std::min(nsm, std::atoi(ge)));
         PersistParams pp{};
         pp.order = static_cast<int>(order);
         pp.R = R;

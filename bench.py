@@ -15,9 +15,10 @@ oversample 10, FFCP rank 20), synthetic from the reference's seeded generators.
   cpu_baseline / --impl reference = the CPU oracle (restated reference, oracle/) on the
                box's host cores over a bounded slab of the same workload
 
-Multi-GPU (torchrun, one process per GPU): weak scaling — every rank holds one
-1000^3 slab of a 1000 x 1000 x (1000 N) tensor (last-mode slabs, dist.hpp:70-123); partial
-sketches and cores are all-reduced over NCCL (the library's tk_comm hook).
+Multi-GPU (torchrun, one process per GPU): weak scaling — every rank holds one 1000^3 block
+of ONE global tensor: last-mode slabs of 1000 x 1000 x (1000 N) at N = 2, 4 and the
+2 x 2 x 2 block grid of a 2000^3 tensor at N = 8 (BASELINE cfg 5's partition; BlockGrid,
+dist.hpp:24-123); partial sketches and cores are all-reduced over NCCL (tk_comm hook).
 """
 from __future__ import annotations
 
@@ -257,9 +258,11 @@ def run_b200(args, cfg):
     ctx.bind_torch_stream()
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
     dims = list(cfg["dims"])
-    gdims = list(dims)
-    gdims[-1] = dims[-1] * world
-    slab_offset = rank * dims[-1]
+    grid = D.default_grid(len(dims), world)
+    gdims = [d * g for d, g in zip(dims, grid)]
+    plan = D.GridPlan(gdims, [[d] * g for d, g in zip(dims, grid)])
+    blo, bln = plan.block(rank)
+    assert bln == dims
     _, alg_seed = bench_seeds(0)
 
     # ---- data (untimed): this rank's slab of ONE global seeded tensor of dims
@@ -270,8 +273,9 @@ def run_b200(args, cfg):
     if world == 1:
         y = generate_as(dict(cfg, seed=0), tdt)
     else:
-        y = generate_as(dict(cfg, seed=0, dims=gdims), tdt, slab=(slab_offset, dims[-1]), all_sum=_all_sum)
+        y = generate_as(dict(cfg, seed=0, dims=gdims), tdt, block=(blo, bln), all_sum=_all_sum)
     torch.cuda.empty_cache()
+    log(f"[rank {rank}/{world}] block lo={blo} len={bln} of {gdims}: generated")
     cpu_ys = None  # the CPU baseline's bounded sample: the first slabs of this Y (host fp64)
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu_ys, cpu_sdims = cpu_sample(cfg, y, args.cpu_slabs)
@@ -279,9 +283,10 @@ def run_b200(args, cfg):
     ybytes = y.numel() * y.element_size()
     comm = None
     if world > 1:
-        comm = D.DistComm(slab_offset, gdims[-1], D.exchange_capacity(gdims, cfg["ranks"], cfg["p"]))
+        comm = D.DistComm(blo[-1], gdims[-1], D.exchange_capacity(gdims, cfg["ranks"], cfg["p"]), block_lo=blo,
+                          global_dims=gdims)
         ctx.set_comm(comm)
-    kw = dict(sync_ranks=False, out="device", global_last_dim=gdims[-1] if world > 1 else 0)
+    kw = dict(sync_ranks=False, out="device", global_dims=gdims if world > 1 else ())
 
     def step(time_kernels=False):
         return P.rand_tucker_2i(yd, cfg["ranks"], cfg["p"], alg_seed, context=ctx, time_kernels=time_kernels, **kw)
@@ -297,6 +302,7 @@ def run_b200(args, cfg):
         while nw < max(args.warmup, 3) or time.perf_counter() - t_w < 1.0:
             m = step(time_kernels=True)
             nw += 1
+        log(f"[rank {rank}/{world}] warm-up done ({nw} calls)")
         barrier(world)
         ev0.record(stream)
         t0 = time.perf_counter()
@@ -342,7 +348,7 @@ def run_b200(args, cfg):
             barrier(world)
             t0 = time.perf_counter()
             mm = P.rand_tucker_2i(yh, cfg["ranks"], cfg["p"], alg_seed, context=ctx, sync_ranks=False,
-                                  global_last_dim=kw["global_last_dim"], out="device")
+                                  global_dims=kw["global_dims"], out="device")
             res = P.ffcp(mm, cfg["ffcp_rank"], P.ConstraintSpec(cfg["constraint"]), P.StopRule(*STOP), alg_seed,
                          context=ctx)  # on the device model; CP factors come back to the host
             mh = mm.to_host()  # Tucker core + factors to the host
@@ -391,7 +397,8 @@ def run_b200(args, cfg):
             "dtype": "f32" if cfg["dtype"] == "f32" else "f64",
             "data": "synthetic (reference seeded generators bench.hpp:46-112 on device; Y > L2, no flush needed)",
             "config": {"workload": args.config, "dims": gdims, "ranks": list(cfg["ranks"]), "oversample": cfg["p"],
-                       "ffcp_rank": cfg["ffcp_rank"], "passes_per_step": passes, "parallelism": f"slab{world}",
+                       "ffcp_rank": cfg["ffcp_rank"], "passes_per_step": passes,
+                       "parallelism": ("block" + "x".join(map(str, grid))) if world > 1 else "slab1",
                        "l2": "inputs larger than L2 (126 MB)", "core": "derived from X_{N-1} (2N passes)"},
             "hbm_frac_of_peak": round(value / world / hbm, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",

@@ -13,6 +13,7 @@
  *                            + detail::fix_column_signs  tucker.hpp:39-45
  *   tk_gaussian_matrix    <- tenkit::gaussian_matrix     random.hpp:85-100
  *   tk_gaussian_fill      <- tenkit::gaussian_tensor     random.hpp:124-138 (window at an offset)
+ *   tk_gaussian_fill_block   (same, one block of a BlockGrid, dist.hpp:24-123)
  *   tk_seed_derived       <- tenkit::SeedSpec::derived   random.hpp:36-41
  *   tk_ffcp(_device)      <- tenkit::ffcp                ffcp.hpp:94-194
  *   tk_model_fit          <- tenkit::fit(y, reconstruct / cp_reconstruct(model))
@@ -42,12 +43,16 @@ enum tk_constraint { TK_CP_NONE = 0, TK_CP_NONNEG_MU = 1, TK_CP_NONNEG_HALS = 2,
 
 typedef struct tk_context tk_context;
 
-/* Cross-rank reduction hook for slab-partitioned Y (dist.hpp:617-800 semantics: partial
+/* Cross-rank reduction hook for block-partitioned Y (dist.hpp:617-800 semantics: partial
  * sketches and partial cores are summed over ranks). The library writes `count` doubles
  * at the front of `xbuf` (a caller-owned device buffer of `xbuf_capacity` doubles) and
  * calls allreduce_sum(user, count, stream); on return xbuf holds the sum over ranks.
- * This rank owns rows [slab_offset, slab_offset + local I_{N-1}) of the last mode of a
- * tensor whose global last-mode size is global_last_dim. */
+ *
+ * Which block of the global tensor this rank holds (BlockGrid, dist.hpp:24-123):
+ *   blocked == 0: a slab of the last mode, rows [slab_offset, slab_offset + local I_{N-1})
+ *                 of a tensor whose global last-mode size is global_last_dim;
+ *   blocked != 0: a general block, indices [block_lo[n], block_lo[n] + local I_n) of mode n
+ *                 of a tensor of global_dims[n] (the slab fields are ignored). */
 typedef struct tk_comm {
     int rank;
     int world;
@@ -57,6 +62,9 @@ typedef struct tk_comm {
     int64_t xbuf_capacity;
     int (*allreduce_sum)(void* user, int64_t count, void* cuda_stream);
     void* user;
+    int blocked;
+    int64_t block_lo[TK_MAX_ORDER];
+    int64_t global_dims[TK_MAX_ORDER];
 } tk_comm;
 
 /* Output of the Tucker drivers (TuckerModel, tucker.hpp:14-33). Pointers are device
@@ -153,6 +161,11 @@ int tk_model_fit(tk_context* ctx, int dtype, int64_t order, const int64_t* dims,
  * globally indexed noise tensor (bench.hpp:100-112 generated blockwise) */
 int tk_gaussian_fill(tk_context* ctx, int64_t n, uint64_t offset, uint64_t seed_root, uint64_t seed_stream,
                      double* out);
+/* The same for a block of a tensor of global_dims (lo[n] .. lo[n] + len[n] - 1 in mode n): out
+ * (prod len doubles, column-major block) holds each entry's draw at its global flat index —
+ * one rank's block of a globally indexed noise tensor (dist.hpp:24-123 BlockGrid layout). */
+int tk_gaussian_fill_block(tk_context* ctx, int64_t order, const int64_t* global_dims, const int64_t* lo,
+                           const int64_t* len, uint64_t seed_root, uint64_t seed_stream, double* out);
 uint64_t tk_seed_derived(uint64_t seed_root, uint64_t seed_stream, uint64_t tag);
 
 /* FFCP on a Tucker model (host pointers, fp64; computed on the device). factors[n] is

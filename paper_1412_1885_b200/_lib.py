@@ -26,7 +26,8 @@ ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p)
 
 class tk_comm(C.Structure):
     _fields_ = [("rank", C.c_int), ("world", C.c_int), ("slab_offset", I64), ("global_last_dim", I64),
-                ("xbuf", PD), ("xbuf_capacity", I64), ("allreduce_sum", ALLREDUCE_FN), ("user", C.c_void_p)]
+                ("xbuf", PD), ("xbuf_capacity", I64), ("allreduce_sum", ALLREDUCE_FN), ("user", C.c_void_p),
+                ("blocked", C.c_int), ("block_lo", I64 * TK_MAX_ORDER), ("global_dims", I64 * TK_MAX_ORDER)]
 
 
 class tk_tucker_out(C.Structure):
@@ -65,6 +66,7 @@ SIGNATURES = {
     "tk_orthonormal_basis": (C.c_int, [C.c_void_p, I64, I64, PD, PD, PI64, PD]),
     "tk_gaussian_matrix": (C.c_int, [C.c_void_p, I64, I64, U64, U64, PD]),
     "tk_gaussian_fill": (C.c_int, [C.c_void_p, I64, U64, U64, U64, PD]),
+    "tk_gaussian_fill_block": (C.c_int, [C.c_void_p, I64, PI64, PI64, PI64, U64, U64, PD]),
     "tk_model_fit": (C.c_int, [C.c_void_p, C.c_int, I64, PI64, C.c_void_p, PI64, PD, C.POINTER(PD), I64, PD]),
     "tk_seed_derived": (U64, [U64, U64, U64]),
     "tk_ffcp": (C.c_int, [C.c_void_p, I64, PI64, PD, C.POINTER(PD), PI64, I64, C.c_int, C.c_double, C.c_int,

@@ -68,6 +68,21 @@ template <typename T>
 void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaStream_t s, int64_t row_off = 0,
                             int64_t rows_total = 0);
 
+// Omega rows at scattered global positions (a block of a BlockGrid, dist.hpp:496-596): local
+// row c has mixed-radix digits d_k over lext[0..nd) (first fastest) and sits at global row
+// sum_k (lo[k] + d_k) * gstride[k] of a rows_total x cols gaussian_matrix.
+struct RowMap {
+    int nd = 0;
+    int64_t lext[8] = {0}, lo[8] = {0}, gstride[8] = {0};
+    int64_t rows_total = 1;
+};
+template <typename T>
+void launch_gaussian_packed_map(T* out, int64_t rows, int cols, uint64_t key, const RowMap& map, cudaStream_t s);
+
+// out[c] = normal_at(key, global flat index of local element c) for a block (map.lext =
+// block extents, lo = block offsets, gstride = global column-major strides), c < n.
+void launch_gaussian_fill_map(double* out, int64_t n, uint64_t key, const RowMap& map, cudaStream_t s);
+
 // Counter-RNG fills (random.hpp:85-100): out[i + j*rows] = normal_at(key, j*rows + i).
 void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s);
 // out[t] = normal_at(key, offset + t), t < n (a window of the flat counter stream).

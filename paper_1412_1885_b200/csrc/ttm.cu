@@ -495,6 +495,23 @@ __global__ void gaussian_packed_kernel(T* __restrict__ out, int64_t rows, int co
     }
 }
 
+template <typename T>
+__global__ void gaussian_packed_map_kernel(T* __restrict__ out, int64_t rows, int cols, int stride, uint64_t key,
+                                           RowMap map) {
+    const int64_t n = rows * stride;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c = t / stride;
+        const int j = static_cast<int>(t % stride);
+        int64_t g = 0, rem = c;
+        for (int k = 0; k < map.nd; ++k) {
+            const int64_t d = rem % map.lext[k];
+            rem /= map.lext[k];
+            g += (map.lo[k] + d) * map.gstride[k];
+        }
+        out[t] = j < cols ? static_cast<T>(normal_at_key(key, static_cast<uint64_t>(j * map.rows_total + g))) : T(0);
+    }
+}
+
 template <typename S, typename D>
 __global__ void cast2d_kernel(const S* __restrict__ in, int64_t ldi, D* __restrict__ out, int64_t ldo, int64_t rows,
                               int64_t cols) {
@@ -608,6 +625,20 @@ void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaSt
 }
 template void launch_gaussian_packed<float>(float*, int64_t, int, uint64_t, cudaStream_t, int64_t, int64_t);
 template void launch_gaussian_packed<double>(double*, int64_t, int, uint64_t, cudaStream_t, int64_t, int64_t);
+
+template <typename T>
+void launch_gaussian_packed_map(T* out, int64_t rows, int cols, uint64_t key, const RowMap& map, cudaStream_t s) {
+    const int stride = pack_stride(cols);
+    gaussian_packed_map_kernel<T><<<grid_for(rows * stride), 256, 0, s>>>(out, rows, cols, stride, key, map);
+    TK_LAUNCH_CHECK();
+}
+void launch_gaussian_fill_map(double* out, int64_t n, uint64_t key, const RowMap& map, cudaStream_t s) {
+    // stride 1, one column: out[c] = normal_at(key, 0 * rows_total + g(c))
+    gaussian_packed_map_kernel<double><<<grid_for(n), 256, 0, s>>>(out, n, 1, 1, key, map);
+    TK_LAUNCH_CHECK();
+}
+template void launch_gaussian_packed_map<float>(float*, int64_t, int, uint64_t, const RowMap&, cudaStream_t);
+template void launch_gaussian_packed_map<double>(double*, int64_t, int, uint64_t, const RowMap&, cudaStream_t);
 
 template <typename S, typename D>
 void launch_cast(const S* in, D* out, int64_t n, cudaStream_t s) {

@@ -134,6 +134,30 @@ void check_ctx(tk_context* ctx) {
     TK_CUDA(cudaSetDevice(ctx->device));
 }
 
+// This rank's block of the global tensor (BlockGrid, dist.hpp:24-123): global extents gd and
+// the global index of the block's first row in each mode. Without a multi-rank comm hook the
+// block is the whole tensor.
+void block_of(const tk_context* ctx, const std::vector<int64_t>& ld, std::vector<int64_t>& gd,
+              std::vector<int64_t>& lo) {
+    const size_t order = ld.size();
+    gd = ld;
+    lo.assign(order, 0);
+    if (!ctx->has_comm || ctx->comm.world <= 1) return;
+    const tk_comm& c = ctx->comm;
+    if (c.blocked) {
+        for (size_t n = 0; n < order; ++n) {
+            gd[n] = c.global_dims[n];
+            lo[n] = c.block_lo[n];
+            require(lo[n] >= 0 && lo[n] + ld[n] <= gd[n], "comm: block outside the global tensor");
+        }
+    } else {
+        gd[order - 1] = c.global_last_dim;
+        lo[order - 1] = c.slab_offset;
+        require(lo[order - 1] >= 0 && lo[order - 1] + ld[order - 1] <= gd[order - 1],
+                "comm: slab outside the global tensor");
+    }
+}
+
 // ---------------------------------------------------------------------------
 // One decomposition run for value type T.
 // ---------------------------------------------------------------------------
@@ -144,7 +168,7 @@ struct TuckerRun {
     int64_t order;
     std::vector<int64_t> ldims;  // local dims of Y on this rank
     std::vector<int64_t> gdims;  // global dims
-    int64_t offset = 0;          // slab offset along the last mode
+    std::vector<int64_t> off;    // global index of this rank's first row in each mode (BlockGrid lo)
     const T* y;
     std::vector<int> rt, cols;
     std::vector<double*> U;  // global factors, gdims[n] x rt[n] (ld gdims[n])
@@ -181,7 +205,7 @@ struct TuckerRun {
 
     const T* factor_rows(int m) const {  // rows of U_m matching this rank's block
         const T* p = Up[m];
-        if (m == order - 1) p += offset * pack_stride(cols[m]);
+        p += off[m] * pack_stride(cols[m]);
         return p;
     }
 
@@ -279,7 +303,7 @@ struct TuckerRun {
             float* fout = reinterpret_cast<float*>(out);
             if (!tc_ttm_supported(fin, fout, P, K, Q, cols[m])) return false;
             void* bpk = ctx->buf(streams_y ? "umma_pack" : "umma_pack2", static_cast<size_t>(umma_pack_bytes(K, cols[m])));
-            const double* u = U[m] + (m == order - 1 ? offset : 0);
+            const double* u = U[m] + off[m];
             launch_pack_umma(u, gdims[m], K, cols[m], bpk, s);
             if (streams_y && time_kernels) mark();
             launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s);
@@ -324,10 +348,9 @@ struct TuckerRun {
         ++launches;
         const int64_t In = gdims[n];
         double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * In * rn));
-        const bool local_rows = ctx->has_comm && ctx->comm.world > 1 && n == order - 1;
-        if (local_rows) {
+        if (ldims[n] != In) {  // this rank's rows of Z, the others zero (summed over ranks)
             TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * In * rn, s));
-            sketch(x, xd, n, omp, rn, z + offset, In);
+            sketch(x, xd, n, omp, rn, z + off[n], In);
         } else {
             sketch(x, xd, n, omp, rn, z, In);
         }
@@ -482,55 +505,56 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
                       const int64_t* ranks, int64_t p, Seed seed, tk_tucker_out* out, tk_tucker_stats* stats) {
     cudaStream_t s = ctx->stream;
     std::vector<int64_t> cd(dims, dims + order);  // current (local) extents
-    std::vector<int64_t> gd = cd;                 // global extents
-    int64_t offset = 0;
-    const bool dist = ctx->has_comm && ctx->comm.world > 1;
-    if (dist) {  // slab of the last mode (dist.hpp:496-596: Omega rows by global column id)
-        gd[order - 1] = ctx->comm.global_last_dim;
-        offset = ctx->comm.slab_offset;
-        require(offset >= 0 && offset + cd[order - 1] <= gd[order - 1], "comm: slab outside the global tensor");
-    }
+    std::vector<int64_t> gd, lo;                  // global extents, block offsets (dist.hpp:24-123)
+    block_of(ctx, cd, gd, lo);
     const T* cur = static_cast<const T*>(y);
     if (!y_on_device) {
         T* buf = static_cast<T*>(ctx->buf("y_in", sizeof(T) * prod(cd)));
         TK_CUDA(cudaMemcpyAsync(buf, y, sizeof(T) * prod(cd), cudaMemcpyHostToDevice, s));
         cur = buf;
     }
-    TuckerRun<T> r{ctx, s, order, cd, gd, offset, cur};
+    TuckerRun<T> r{ctx, s, order, cd, gd, lo, cur};
     r.rank_dev = static_cast<int*>(ctx->buf("ranks", sizeof(int) * 2 * TK_MAX_ORDER));
     std::vector<double*> U(order);
     std::vector<int64_t> fcols(order);
     int which = 0;
-    const int last = static_cast<int>(order) - 1;
     for (int n = 0; n < order; ++n) {
         const int rt = static_cast<int>(std::min<int64_t>(ranks[n] + p, gd[n]));
         require(rt >= 1, "gaussian_matrix: dimensions must be positive");
         require(rt <= kMaxRank, "rank + oversample must be <= 64 on this device path");
-        // Omega_n: (global width) x rt; this rank's unfolding columns are the contiguous rows
-        // [offset * S, (offset + len) * S) of it when n < last (the last mode varies slowest)
+        // Omega_n: (global width) x rt. Column c of this rank's mode-n unfolding sits at global
+        // column sum_k (lo_k + digit_k) * stride_k of the global unfolding (modes k != n ascending,
+        // already contracted modes at their full rank with lo = 0): streamed_block_product,
+        // dist.hpp:496-596.
         const int64_t width = prod(cd) / cd[n];
-        int64_t row_off = 0, width_g = width;
-        if (dist && n < last) {
-            const int64_t S = width / cd[last];
-            row_off = offset * S;
-            width_g = S * gd[last];
+        RowMap map;
+        map.rows_total = 1;
+        for (int k = 0; k < order; ++k) {
+            if (k == n) continue;
+            const int64_t ge = k < n ? cd[k] : gd[k];
+            map.lext[map.nd] = cd[k];
+            map.lo[map.nd] = k < n ? 0 : lo[k];
+            map.gstride[map.nd] = map.rows_total;
+            map.rows_total *= ge;
+            ++map.nd;
         }
         const Seed os = alg2_omega_seed(seed, n);
         double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * gd[n] * rt));
         T* op = static_cast<T*>(ctx->buf("omega_packed", sizeof(T) * width * pack_stride(rt)));
-        launch_gaussian_packed<T>(op, width, rt, os.key(), s, row_off, width_g);
-        if (n == 0 && !(dist && last == 0)) {  // contiguous unfolding: Z = Y_(0) Omega, split-K TTM
+        launch_gaussian_packed_map<T>(op, width, rt, os.key(), map, s);
+        const bool part = cd[n] != gd[n];  // a partitioned mode: own rows of Z, the others zero
+        if (part) TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * gd[n] * rt, s));
+        double* zown = z + lo[n];
+        if (n == 0) {  // contiguous unfolding: Z = Y_(0) Omega, split-K TTM
             T* zt = static_cast<T*>(ctx->buf("zt", sizeof(T) * cd[0] * rt));
             r.ttm(cur, op, zt, cd[0], width, 1, rt);
-            if constexpr (sizeof(T) == 4) launch_cast<float, double>(reinterpret_cast<const float*>(zt), z, cd[0] * rt, s);
-            else launch_cast<double, double>(reinterpret_cast<const double*>(zt), z, cd[0] * rt, s);
+            if constexpr (sizeof(T) == 4)
+                launch_cast2d<float, double>(reinterpret_cast<const float*>(zt), cd[0], zown, gd[0], cd[0], rt, s);
+            else
+                launch_cast2d<double, double>(reinterpret_cast<const double*>(zt), cd[0], zown, gd[0], cd[0], rt, s);
             r.launches += 2;
-        } else if (dist && n == last) {  // own rows of Z, the others zero (summed over ranks)
-            TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * gd[n] * rt, s));
-            r.sketch(cur, cd, n, op, rt, z + offset, gd[n]);
-            ++r.launches;
         } else {
-            r.sketch(cur, cd, n, op, rt, z, cd[n]);
+            r.sketch(cur, cd, n, op, rt, zown, gd[n]);
             ++r.launches;
         }
         r.allreduce(z, gd[n] * rt);  // partial sketches summed over ranks (no-op on one rank)
@@ -546,13 +570,13 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
         const int64_t P = prod(std::vector<int64_t>(cd.begin(), cd.begin() + n));
         const int64_t Q = prod(std::vector<int64_t>(cd.begin() + n + 1, cd.end()));
         T* nxt = static_cast<T*>(ctx->buf(which ? "a2B" : "a2A", sizeof(T) * P * rank * Q));
-        const T* upl = up + (n == last ? offset * pack_stride(rank) : 0);  // this rank's rows of U
+        const T* upl = up + lo[n] * pack_stride(rank);  // this rank's rows of U
         bool done = false;
         if constexpr (sizeof(T) == 4) {  // the Y-sized mode-0 shrink on the tensor cores (K-major)
             if (n == 0 && P == 1 && ctx->ttm_path != 1 &&
                 tc_ttm_supported(reinterpret_cast<const float*>(cur), reinterpret_cast<float*>(nxt), 1, cd[0], Q, rank)) {
                 void* bpk = ctx->buf("umma_pack", static_cast<size_t>(umma_pack_bytes(cd[0], rank)));
-                launch_pack_umma(U[0], gd[0], cd[0], rank, bpk, s);
+                launch_pack_umma(U[0] + lo[0], gd[0], cd[0], rank, bpk, s);
                 launch_ttm_tc(reinterpret_cast<const float*>(cur), bpk, reinterpret_cast<float*>(nxt), 1, cd[0], Q, rank, s,
                               true);
                 r.launches += 2;
@@ -618,7 +642,7 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
             TK_CUDA(cudaEventCreateWithFlags(&ctx->ev_cap, cudaEventDisableTiming));
         }
         ctx->ensure_side();
-        TuckerRun<T> r{ctx, ctx->cap, order, ld, ld, 0, ydev};
+        TuckerRun<T> r{ctx, ctx->cap, order, ld, ld, std::vector<int64_t>(order, 0), ydev};
         r.time_kernels = opt.time_kernels != 0;
         r.capture = true;
         cudaGraph_t graph = nullptr;
@@ -683,13 +707,8 @@ void rand_tucker_2i_impl(tk_context* ctx, int64_t order, const int64_t* dims, co
                          const int64_t* ranks, int64_t p, Seed seed, const tk_tucker_opts& opt, tk_tucker_out* out,
                          tk_tucker_stats* stats) {
     std::vector<int64_t> ld(dims, dims + order), rk(ranks, ranks + order);
-    std::vector<int64_t> gd = ld;
-    int64_t offset = 0;
-    if (ctx->has_comm && ctx->comm.world > 1) {
-        gd[order - 1] = ctx->comm.global_last_dim;
-        offset = ctx->comm.slab_offset;
-        require(offset >= 0 && offset + ld[order - 1] <= gd[order - 1], "comm: slab outside the global tensor");
-    }
+    std::vector<int64_t> gd, offset;
+    block_of(ctx, ld, gd, offset);
     const T* ydev = static_cast<const T*>(y);
     if (!y_on_device) {
         T* buf = static_cast<T*>(ctx->buf("y_in", sizeof(T) * prod(ld)));
@@ -926,6 +945,26 @@ int tk_gaussian_fill(tk_context* ctx, int64_t n, uint64_t offset, uint64_t root,
     });
 }
 
+int tk_gaussian_fill_block(tk_context* ctx, int64_t order, const int64_t* global_dims, const int64_t* lo,
+                           const int64_t* len, uint64_t root, uint64_t stream, double* out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(order >= 1 && order <= TK_MAX_ORDER, "tensor order must be in [1, 8]");
+        RowMap map;
+        int64_t n = 1;
+        for (int k = 0; k < order; ++k) {
+            require(len[k] >= 0 && lo[k] >= 0 && lo[k] + len[k] <= global_dims[k], "gaussian_fill: block outside the tensor");
+            map.lext[k] = std::max<int64_t>(len[k], 1);
+            map.lo[k] = lo[k];
+            map.gstride[k] = map.rows_total;
+            map.rows_total *= global_dims[k];
+            n *= len[k];
+        }
+        map.nd = static_cast<int>(order);
+        if (n > 0) launch_gaussian_fill_map(out, n, Seed{root, stream}.key(), map, ctx->stream);
+    });
+}
+
 int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* q, int64_t* rank,
                          double* rdiag) {
     return guarded([&] {
@@ -1002,7 +1041,7 @@ int tk_ttm_all(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, c
         std::vector<int64_t> d(dims, dims + order);
         auto body = [&](auto tag) {
             using T = decltype(tag);
-            TuckerRun<T> r{ctx, ctx->stream, order, d, d, 0, static_cast<const T*>(t)};
+            TuckerRun<T> r{ctx, ctx->stream, order, d, d, std::vector<int64_t>(order, 0), static_cast<const T*>(t)};
             r.cols.resize(order);
             r.Up.resize(order);
             r.U.assign(order, nullptr);
@@ -1036,7 +1075,7 @@ int tk_unfold_times(tk_context* ctx, int dtype, int64_t order, const int64_t* di
         require(bcols >= 1 && bcols <= kMaxRank, "unfold_times: B columns must be in [1, 64] on the device path");
         auto body = [&](auto tag) {
             using T = decltype(tag);
-            TuckerRun<T> r{ctx, ctx->stream, order, d, d, 0, static_cast<const T*>(t)};
+            TuckerRun<T> r{ctx, ctx->stream, order, d, d, std::vector<int64_t>(order, 0), static_cast<const T*>(t)};
             T* bp = static_cast<T*>(ctx->buf("ut_bp", sizeof(T) * W * pack_stride(static_cast<int>(bcols))));
             launch_pack_factor<T>(b, W, W, static_cast<int>(bcols), bp, ctx->stream);
             r.sketch(static_cast<const T*>(t), d, static_cast<int>(mode), bp, static_cast<int>(bcols), z, d[mode]);

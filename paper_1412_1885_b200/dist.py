@@ -1,5 +1,6 @@
-"""Multi-GPU plumbing: slab partition of Y along its last mode and the cross-rank reduction
-hook of the C-ABI (tk_comm), over torch.distributed (NCCL on B200s, gloo on CPU tests).
+"""Multi-GPU plumbing: block partition of Y (BlockGrid, dist.hpp:24-123; a slab of the last
+mode is the 1 x ... x 1 x W grid) and the cross-rank reduction hook of the C-ABI (tk_comm),
+over torch.distributed (NCCL on B200s, gloo on CPU tests).
 
 Semantics follow the reference's distributed protocol (dist.hpp:617-800): every rank
 projects its own block with the factor rows it owns, the partial sketches Z_n^g and the
@@ -29,12 +30,101 @@ def plan_slabs(dim: int, world: int):
     return out
 
 
+def ind2sub(grid_shape, w: int):
+    """Column-major 1-based subscripts of worker w (dist.hpp:45-56)."""
+    total = 1
+    for g in grid_shape:
+        total *= int(g)
+    if not 1 <= w <= total:
+        raise _lib.TenkitError("tenkit: ind2sub: worker id out of range")
+    subs, rem = [], w - 1
+    for g in grid_shape:
+        subs.append(rem % int(g) + 1)
+        rem //= int(g)
+    return subs
+
+
+def sub2ind(grid_shape, subs) -> int:
+    """Inverse of ind2sub (dist.hpp:58-67)."""
+    if len(subs) != len(grid_shape):
+        raise _lib.TenkitError("tenkit: sub2ind: order mismatch")
+    idx, stride = 0, 1
+    for g, s in zip(grid_shape, subs):
+        if not 1 <= s <= g:
+            raise _lib.TenkitError("tenkit: sub2ind: subscript range")
+        idx += (s - 1) * stride
+        stride *= int(g)
+    return idx + 1
+
+
+class GridPlan:
+    """Block partition of a tensor of `shape` into contiguous-range blocks (partition,
+    dist.hpp:71-123): `splits[n]` are the segment lengths of mode n (summing to shape[n]),
+    block (s_1..s_N) belongs to worker sub2ind(grid_shape, s) = rank + 1."""
+
+    def __init__(self, shape, splits):
+        self.shape = [int(d) for d in shape]
+        if len(splits) != len(self.shape):
+            raise _lib.TenkitError("tenkit: partition: one split list per mode required")
+        self.splits, self.offsets = [], []
+        for n, sp in enumerate(splits):
+            sp = [int(x) for x in sp]
+            if not sp:
+                raise _lib.TenkitError("tenkit: partition: empty split list")
+            if any(x < 1 for x in sp):
+                raise _lib.TenkitError("tenkit: partition: segment lengths must be positive")
+            if sum(sp) != self.shape[n]:
+                raise _lib.TenkitError("tenkit: partition: split lengths must sum to the mode dimension")
+            offs, o = [], 0
+            for x in sp:
+                offs.append(o)
+                o += x
+            self.splits.append(sp)
+            self.offsets.append(offs)
+        self.grid_shape = [len(sp) for sp in self.splits]
+
+    @classmethod
+    def even(cls, shape, grid_shape):
+        """Near-even segments per mode (plan_slabs per mode)."""
+        return cls(shape, [[ln for _, ln in plan_slabs(d, g)] for d, g in zip(shape, grid_shape)])
+
+    @property
+    def world(self) -> int:
+        w = 1
+        for g in self.grid_shape:
+            w *= g
+        return w
+
+    def block(self, rank: int):
+        """(lo, len) per mode of the block of 0-based `rank` (worker rank + 1)."""
+        subs = ind2sub(self.grid_shape, rank + 1)
+        lo = [self.offsets[n][s - 1] for n, s in enumerate(subs)]
+        ln = [self.splits[n][s - 1] for n, s in enumerate(subs)]
+        return lo, ln
+
+    def local(self, y, rank: int):
+        """This rank's block of a full (host) array, Fortran-ordered copy."""
+        import numpy as np
+        lo, ln = self.block(rank)
+        return np.asfortranarray(y[tuple(slice(a, a + b) for a, b in zip(lo, ln))])
+
+
+def default_grid(order: int, world: int):
+    """Grid shape for `world` ranks: a slab of the last mode, except 8 ranks on a 3-way tensor,
+    which get the 2 x 2 x 2 block grid (BASELINE cfg 5)."""
+    if order == 3 and world == 8:
+        return [2, 2, 2]
+    return [1] * (order - 1) + [world]
+
+
 class DistComm:
     """Reduction hook handed to the library: `xbuf` is a device (or, in CPU tests, host)
     float64 buffer; the library writes `count` values and calls back for an all-reduce sum
-    over the process group."""
+    over the process group. The block this rank holds is either a last-mode slab
+    (slab_offset, global_last_dim) or, with `block_lo`/`global_dims`, a general block."""
 
-    def __init__(self, slab_offset: int, global_last_dim: int, capacity: int, group=None, device=None):
+    def __init__(self, slab_offset: int, global_last_dim: int, capacity: int, group=None, device=None,
+                 block_lo=None, global_dims=None):
         import torch
         import torch.distributed as dist
         self.group = group
@@ -42,6 +132,12 @@ class DistComm:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.slab_offset = int(slab_offset)
         self.global_last_dim = int(global_last_dim)
+        self.block_lo = None if block_lo is None else [int(x) for x in block_lo]
+        self.global_dims = None if global_dims is None else [int(x) for x in global_dims]
+        if (self.block_lo is None) != (self.global_dims is None):
+            raise _lib.TenkitError("tenkit: comm: block_lo and global_dims go together")
+        if self.global_dims is not None and len(self.global_dims) > _lib.TK_MAX_ORDER:
+            raise _lib.TenkitError("tenkit: comm: order too large")
         dev = device if device is not None else ("cuda" if torch.cuda.is_available() else "cpu")
         self.xbuf = torch.zeros(int(capacity), dtype=torch.float64, device=dev)
         self.calls = 0
@@ -78,6 +174,11 @@ class DistComm:
         s.xbuf_capacity = self.xbuf.numel()
         s.allreduce_sum = self._cb
         s.user = None
+        s.blocked = 0 if self.block_lo is None else 1
+        if self.block_lo is not None:
+            for n, (a, g) in enumerate(zip(self.block_lo, self.global_dims)):
+                s.block_lo[n] = a
+                s.global_dims[n] = g
         return s
 
 
@@ -90,36 +191,47 @@ def exchange_capacity(dims, ranks, oversample) -> int:
     return max([int(i) * r for i, r in zip(dims, rts)] + [core])
 
 
-def dist_rand_tucker_2i(local_y, global_last_dim: int, slab_offset: int, ranks, oversample, seed, *, context=None,
-                        group=None, **kw):
-    """rand_tucker_2i of the global tensor whose last-mode slab
-    [slab_offset, slab_offset + local_y.shape[-1]) lives on this rank (one process per GPU).
-    Every rank returns the same model (replicated QR)."""
-    from .tenkit import Context, rand_tucker_2i
+def _block_args(local_y, global_dims, lo):
+    """(global dims, block lo) from either the slab form (int last-mode size, int offset) or
+    the block form (sequences)."""
+    shape = list(local_y.shape)
+    if isinstance(global_dims, (int,)) or hasattr(global_dims, "__index__"):
+        g = shape[:-1] + [int(global_dims)]
+        l = [0] * (len(shape) - 1) + [int(lo)]
+    else:
+        g, l = [int(x) for x in global_dims], [int(x) for x in lo]
+        if len(g) != len(shape) or len(l) != len(shape):
+            raise _lib.TenkitError("tenkit: comm: one global extent and block offset per mode required")
+    return g, l
+
+
+def _dist_call(fn, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw):
+    from .tenkit import Context
     ctx = context or Context.default()
-    gdims = list(local_y.shape)
-    gdims[-1] = global_last_dim
-    comm = DistComm(slab_offset, global_last_dim, exchange_capacity(gdims, ranks, oversample), group=group)
+    gdims, blo = _block_args(local_y, global_dims, lo)
+    comm = DistComm(blo[-1], gdims[-1], exchange_capacity(gdims, ranks, oversample), group=group,
+                    block_lo=blo, global_dims=gdims)
     ctx.set_comm(comm)
     try:
-        return rand_tucker_2i(local_y, ranks, oversample, seed, context=ctx, global_last_dim=global_last_dim, **kw)
+        return fn(local_y, ranks, oversample, seed, context=ctx, global_dims=gdims, **kw)
     finally:
         ctx.set_comm(None)
 
 
-def dist_rand_tucker(local_y, global_last_dim: int, slab_offset: int, ranks, oversample, seed, *, context=None,
-                     group=None, **kw):
-    """rand_tucker (Alg. 2, tucker.hpp:108-130) of the global tensor whose last-mode slab
-    lives on this rank: the Omega rows of each unfolding are drawn at their global column ids
-    (dist.hpp:525-537), partial sketches and the partial core are summed over ranks, the QR
-    is replicated. Every rank returns the same model."""
-    from .tenkit import Context, rand_tucker
-    ctx = context or Context.default()
-    gdims = list(local_y.shape)
-    gdims[-1] = global_last_dim
-    comm = DistComm(slab_offset, global_last_dim, exchange_capacity(gdims, ranks, oversample), group=group)
-    ctx.set_comm(comm)
-    try:
-        return rand_tucker(local_y, ranks, oversample, seed, context=ctx, global_last_dim=global_last_dim, **kw)
-    finally:
-        ctx.set_comm(None)
+def dist_rand_tucker_2i(local_y, global_dims, lo, ranks, oversample, seed, *, context=None, group=None, **kw):
+    """rand_tucker_2i (dist_rand_tucker_2i semantics, dist.hpp:884-936) of the global tensor
+    whose block lives on this rank (one process per GPU): `global_dims`/`lo` are the global
+    extents and the block's first index per mode (GridPlan.block), or — the slab form — the
+    global last-mode size and the slab offset. Every rank returns the same model (replicated
+    QR; the factors equal the single-node rand_tucker_2i's, not a rotation of them)."""
+    from .tenkit import rand_tucker_2i
+    return _dist_call(rand_tucker_2i, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw)
+
+
+def dist_rand_tucker(local_y, global_dims, lo, ranks, oversample, seed, *, context=None, group=None, **kw):
+    """rand_tucker (Alg. 2, tucker.hpp:108-130; dist_rand_tucker, dist.hpp:852-878) of the
+    global tensor whose block lives on this rank: the Omega rows of each unfolding are drawn
+    at their global column ids (dist.hpp:496-596), partial sketches and the partial core are
+    summed over ranks, the QR is replicated. Every rank returns the same model."""
+    from .tenkit import rand_tucker
+    return _dist_call(rand_tucker, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw)

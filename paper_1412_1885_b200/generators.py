@@ -47,6 +47,20 @@ def gaussian_flat(n: int, seed: SeedSpec, context: Context | None = None, offset
     return out[: int(n)]
 
 
+def gaussian_block(global_dims, lo, ln, seed: SeedSpec, context: Context | None = None):
+    """Flat fp64 CUDA tensor (column-major block ln) of gaussian_tensor(global_dims, seed)
+    restricted to the block starting at `lo`: every entry drawn at its global flat index
+    (tk_gaussian_fill_block)."""
+    import torch
+    ctx = _ctx(context)
+    n = int(np.prod([int(x) for x in ln]))
+    out = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    arr = lambda xs: (_lib.I64 * len(xs))(*[int(x) for x in xs])
+    _lib.check(ctx.lib.tk_gaussian_fill_block(ctx.handle, len(global_dims), arr(global_dims), arr(lo), arr(ln),
+                                              seed.root, seed.stream, _dptr(out)))
+    return out[:n]
+
+
 def gen_factor_seed(seed: SeedSpec, n: int) -> SeedSpec:  # bench.hpp:46-48
     return seed.derived(0x9E4, n)
 
@@ -62,22 +76,30 @@ def _colmajor_einsum(core, factors):
     return torch.einsum(spec, core, *factors).contiguous().view(-1)
 
 
-def gen_tucker_device(dims, mlranks, seed: SeedSpec, context=None, last_rows=None):
+def _rows(a, n, order, last_rows, block):
+    """Rows of factor n this block uses: block=(lo, ln) lists, or last_rows=(off, len) of the last mode."""
+    if block is not None:
+        return a[int(block[0][n]):int(block[0][n]) + int(block[1][n])]
+    if last_rows is not None and n == order - 1:
+        return a[int(last_rows[0]):int(last_rows[0]) + int(last_rows[1])]
+    return a
+
+
+def gen_tucker_device(dims, mlranks, seed: SeedSpec, context=None, last_rows=None, block=None):
     """gen_tucker_tensor (bench.hpp:83-95) on the device, fp64 flat column-major.
-    last_rows=(offset, length): only that slab of the last mode (the global tensor's slab)."""
+    last_rows=(offset, length): only that slab of the last mode (the global tensor's slab);
+    block=(lo, ln): only that block."""
     import torch
     core = gaussian_flat(int(np.prod(mlranks)), seed.derived(0xC0DE), context)
     core_rm = core.view(*reversed([int(r) for r in mlranks]))
     fs = []
     for n, (i, r) in enumerate(zip(dims, mlranks)):
         a = gaussian_flat(int(i) * int(r), gen_factor_seed(seed, n), context).view(int(r), int(i)).t()
-        if last_rows is not None and n == len(dims) - 1:
-            a = a[int(last_rows[0]):int(last_rows[0]) + int(last_rows[1])]
-        fs.append(a)
+        fs.append(_rows(a, n, len(dims), last_rows, block))
     return _colmajor_einsum(core_rm, fs)
 
 
-def gen_cp_device(dims, rank: int, seed: SeedSpec, uniform: bool = True, context=None, last_rows=None):
+def gen_cp_device(dims, rank: int, seed: SeedSpec, uniform: bool = True, context=None, last_rows=None, block=None):
     """gen_cp_tensor (bench.hpp:56-80) with U(0,1) (or Gaussian) factors, fp64 flat column-major.
     last_rows=(offset, length): only that slab of the last mode."""
     import torch
@@ -87,9 +109,7 @@ def gen_cp_device(dims, rank: int, seed: SeedSpec, uniform: bool = True, context
             a = torch.from_numpy(uniform_matrix(int(i), rank, gen_factor_seed(seed, n))).cuda()
         else:
             a = gaussian_flat(int(i) * rank, gen_factor_seed(seed, n), context).view(rank, int(i)).t()
-        if last_rows is not None and n == len(dims) - 1:
-            a = a[int(last_rows[0]):int(last_rows[0]) + int(last_rows[1])]
-        fs.append(a)
+        fs.append(_rows(a, n, len(dims), last_rows, block))
     order = len(dims)
     eye = torch.zeros([rank] * order, dtype=torch.float64, device="cuda")
     idx = torch.arange(rank, device="cuda")
@@ -155,32 +175,45 @@ def generate(cfg: dict, context=None, slab=None, all_sum=None):
 
 
 def generate_as(cfg: dict, dtype, context=None, slab=None, all_sum=None, chunk_elems: int = 1 << 28,
-                full_sigma: bool = False):
+                full_sigma: bool = False, block=None):
     """generate() straight into `dtype` (e.g. torch.float32) with bounded fp64 temporaries:
     the tensor (or this rank's last-mode slab) is built in chunks of the last mode, twice
     (pass 1: the norms of Y and E for sigma; pass 2: Y + sigma E rounded to dtype), every
     entry drawn at its global index. Same values as generate(...).to(dtype) up to the
     rounding of the chunked contractions; needed for cfg 3/4 (55 / 32 GB fp32) where the
     fp64 tensor and noise would not fit next to each other. full_sigma: materialise only
-    `slab` but take the noise scale from the whole tensor (a bounded sample of it)."""
+    `slab` but take the noise scale from the whole tensor (a bounded sample of it).
+    block=(lo, ln): this rank's block of a BlockGrid instead of a slab (dist.GridPlan.block);
+    the blocks of all ranks tile exactly the tensor generate() produces."""
     import torch
     dims = [int(d) for d in cfg["dims"]]
+    if block is not None:
+        if slab is not None or full_sigma:
+            raise _lib.TenkitError("tenkit: generate: block excludes slab / full_sigma")
+        blo, bln = [int(x) for x in block[0]], [int(x) for x in block[1]]
+        slab = (blo[-1], bln[-1])
     off0, ln = (int(slab[0]), int(slab[1])) if slab is not None else (0, dims[-1])
-    S = int(np.prod(dims[:-1]))
+    S = int(np.prod(dims[:-1])) if block is None else int(np.prod(bln[:-1]))
     per = max(1, int(chunk_elems) // S)
     data_seed, _ = bench_seeds(cfg.get("seed", 0))
     nseed = data_seed.derived(0xAD0).derived(0x7015E)
     abs_noise = cfg.get("abs_noise", False)
     noisy = not (np.isinf(cfg["snr"]) and cfg["snr"] > 0)
 
+    def sub(a, b):  # the block restricted to rows [a, b) of the last mode
+        return (blo[:-1] + [a], bln[:-1] + [b - a]) if block is not None else None
+
     def clean(a, b):  # rows [a, b) of the last mode (global indices)
         if cfg["gen"] == "tucker":
-            return gen_tucker_device(dims, cfg["mlrank"], data_seed, context, last_rows=(a, b - a))
+            return gen_tucker_device(dims, cfg["mlrank"], data_seed, context, last_rows=(a, b - a), block=sub(a, b))
         return gen_cp_device(dims, cfg["cp_rank"], data_seed, uniform=cfg["gen"] == "cp_uniform", context=context,
-                             last_rows=(a, b - a))
+                             last_rows=(a, b - a), block=sub(a, b))
 
     def noise(a, b):
-        e = gaussian_flat((b - a) * S, nseed, context, offset=a * S)
+        if block is not None:
+            e = gaussian_block(dims, *sub(a, b), nseed, context)
+        else:
+            e = gaussian_flat((b - a) * S, nseed, context, offset=a * S)
         return e.abs_() if abs_noise else e
 
     out = torch.empty(S * ln, dtype=dtype, device="cuda")

@@ -267,7 +267,9 @@ def _tucker_call(fn_name, y, ranks, oversample, seed, context, out, opts=None):
     seed = seed if isinstance(seed, SeedSpec) else SeedSpec(*seed)
     ctx = _ctx(context)
     gdims = list(y.shape)
-    if opts is not None and getattr(opts, "_global_last_dim", None):
+    if opts is not None and getattr(opts, "_global_dims", None):
+        gdims = [int(d) for d in opts._global_dims]
+    elif opts is not None and getattr(opts, "_global_last_dim", None):
         gdims[-1] = opts._global_last_dim
     rts = [max(min(int(r) + int(oversample), int(i)), 1) for r, i in zip(ranks, gdims)]
     on_dev = y.on_device if out is None else (out == "device")
@@ -313,24 +315,26 @@ class TuckerOptions:
     _global_last_dim: int = 0
     time_kernels: int = 0
     overlap: int = 1
+    _global_dims: tuple = ()
 
 
 def rand_tucker_2i(y, ranks, oversample: int, seed, *, explicit_core_pass: bool = False, sync_ranks: bool = True,
                    context: Context | None = None, out: str | None = None, global_last_dim: int = 0,
-                   time_kernels: bool = False, overlap: bool = True) -> TuckerModel:
+                   time_kernels: bool = False, overlap: bool = True, global_dims=()) -> TuckerModel:
     """Alg. 3 (tucker.hpp:136-169) on the B200. `y`: numpy array (host; copied in) or a
     device DenseTensor. Returns a host (numpy) model for host input, device otherwise,
-    unless out='host'/'device'."""
+    unless out='host'/'device'. global_dims / global_last_dim: with a comm hook installed,
+    y is this rank's block of a tensor of these global extents (dist.py)."""
     opts = TuckerOptions(int(explicit_core_pass), int(sync_ranks), int(global_last_dim), int(time_kernels),
-                         int(overlap))
+                         int(overlap), tuple(int(d) for d in global_dims))
     return _tucker_call("tk_rand_tucker_2i", y, ranks, oversample, seed, context, out, opts)
 
 
 def rand_tucker(y, ranks, oversample: int, seed, *, context: Context | None = None, out: str | None = None,
-                global_last_dim: int = 0) -> TuckerModel:
-    """Alg. 2 (tucker.hpp:108-130) on the B200. global_last_dim: with a comm hook installed,
-    y is this rank's slab of a tensor whose last mode has that global extent."""
-    opts = TuckerOptions(_global_last_dim=int(global_last_dim)) if global_last_dim else None
+                global_last_dim: int = 0, global_dims=()) -> TuckerModel:
+    """Alg. 2 (tucker.hpp:108-130) on the B200. global_dims / global_last_dim: with a comm
+    hook installed, y is this rank's block of a tensor of these global extents (dist.py)."""
+    opts = TuckerOptions(_global_last_dim=int(global_last_dim), _global_dims=tuple(int(d) for d in global_dims))
     return _tucker_call("tk_rand_tucker", y, ranks, oversample, seed, context, out, opts)
 
 

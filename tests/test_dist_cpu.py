@@ -105,3 +105,100 @@ def test_gloo_world2_partial_sketches_reduce_to_single_node():
     for rank, errs, calls in res:
         assert calls == 4, errs
         assert max(errs) < 1e-12, errs
+
+
+def test_grid_plan_mirrors_reference_partition():
+    """GridPlan = partition/ind2sub/sub2ind (dist.hpp:45-123): worker ids are P = reshape(1..W)
+    column-major over the grid, blocks tile the tensor exactly, errors carry the reference's
+    messages. KAT: ind2sub((2,4,3), 13) = (1,3,2) (test_dist.cpp:32-40)."""
+    from paper_1412_1885_b200 import TenkitError
+    from paper_1412_1885_b200.dist import GridPlan, default_grid, ind2sub, sub2ind
+    assert ind2sub([2, 4, 3], 13) == [1, 3, 2]
+    assert sub2ind([2, 4, 3], [1, 3, 2]) == 13
+    for w in range(1, 25):
+        assert sub2ind([2, 4, 3], ind2sub([2, 4, 3], w)) == w
+    with pytest.raises(TenkitError, match="worker id out of range"):
+        ind2sub([2, 2], 5)
+    g = GridPlan.even((9, 8, 7), (2, 1, 3))
+    assert g.world == 6 and g.splits == [[5, 4], [8], [3, 2, 2]] and g.offsets[2] == [0, 3, 5]
+    assert g.block(0) == ([0, 0, 0], [5, 8, 3]) and g.block(1) == ([5, 0, 0], [4, 8, 3])
+    assert g.block(5) == ([5, 0, 5], [4, 8, 2])
+    y = np.arange(9 * 8 * 7, dtype=np.float64).reshape((9, 8, 7), order="F")
+    cover = np.zeros_like(y)
+    for r in range(g.world):
+        lo, ln = g.block(r)
+        cover[lo[0]:lo[0] + ln[0], lo[1]:lo[1] + ln[1], lo[2]:lo[2] + ln[2]] += 1
+        blk = g.local(y, r)
+        assert blk.flags.f_contiguous and blk.shape == tuple(ln)
+    assert (cover == 1).all()
+    with pytest.raises(TenkitError, match="split lengths must sum to the mode dimension"):
+        GridPlan((4, 4), [[2, 1], [4]])
+    with pytest.raises(TenkitError, match="one split list per mode required"):
+        GridPlan((4, 4), [[4]])
+    assert default_grid(3, 8) == [2, 2, 2] and default_grid(3, 4) == [1, 1, 4] and default_grid(4, 2) == [1, 1, 1, 2]
+
+
+def _block_worker(rank, world, port, grid_shape, q):
+    """Block-grid sharding identity on the oracle: partial sketches of every mode (own rows of
+    Z for a partitioned mode, zero elsewhere) and partial cores, summed through DistComm,
+    equal the single-node products; the tk_comm struct carries the block."""
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle import pyoracle as O
+        from paper_1412_1885_b200.dist import DistComm, GridPlan, exchange_capacity
+        O.set_threads(1)
+        dims, ranks, p = (13, 12, 11), (3, 3, 3), 2
+        seed = (5, 0)
+        y = O.add_noise(O.gen_tucker(dims, ranks, seed), 10.0, O.seed_derived(*seed, 0xAD0))
+        plan = GridPlan.even(dims, grid_shape)
+        lo, ln = plan.block(rank)
+        yl = plan.local(y, rank)
+        rts = [min(r + p, i) for r, i in zip(ranks, dims)]
+        us = [O.gaussian_matrix(i, r, (9, n)) for n, (i, r) in enumerate(zip(dims, rts))]
+        ul = [u[a:a + b] for u, a, b in zip(us, lo, ln)]
+        comm = DistComm(lo[-1], dims[-1], exchange_capacity(dims, ranks, p), block_lo=lo, global_dims=dims)
+        errs = []
+        for n in range(3):
+            om = O.gaussian_matrix(int(np.prod([rts[k] for k in range(3) if k != n])), rts[n], (11, n))
+            full = O.unfold_times(O.ttm_all(y, us, n, True), n, om)
+            part = O.unfold_times(O.ttm_all(yl, ul, n, True), n, om)
+            zp = np.zeros_like(full)
+            zp[lo[n]:lo[n] + ln[n]] = part
+            comm.xbuf[: zp.size] = torch.from_numpy(zp.ravel(order="F"))
+            assert comm.allreduce(zp.size) == 0
+            got = comm.xbuf[: zp.size].numpy().reshape(full.shape, order="F")
+            errs.append(float(np.abs(got - full).max() / np.abs(full).max()))
+        g_full = O.ttm_all(y, us, -1, True)
+        g_part = O.ttm_all(yl, ul, -1, True)
+        comm.xbuf[: g_part.size] = torch.from_numpy(g_part.ravel(order="F"))
+        comm.allreduce(g_part.size)
+        g_got = comm.xbuf[: g_part.size].numpy().reshape(g_full.shape, order="F")
+        errs.append(float(np.abs(g_got - g_full).max() / np.abs(g_full).max()))
+        st = comm.as_struct()
+        assert st.blocked == 1 and list(st.block_lo[:3]) == lo and list(st.global_dims[:3]) == list(dims)
+        q.put((rank, errs, comm.calls))
+        dist.destroy_process_group()
+    except Exception as e:
+        import traceback
+        q.put((rank, repr(e) + traceback.format_exc(), -1))
+
+
+def test_gloo_world4_block_grid_partials_reduce_to_single_node():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    grid = (2, 1, 2)
+    procs = [ctx.Process(target=_block_worker, args=(r, 4, port, grid, q)) for r in range(4)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, errs, calls in res:
+        assert calls == 4, errs
+        assert max(errs) < 1e-12, errs

@@ -193,3 +193,125 @@ def test_two_rank_alg2_matches_single_process(O, dtype):
             assert subspace_dist(u, us) < tol
             assert subspace_dist(u, uo) < (1e-8 if dtype == np.float64 else 1e-3)
         np.testing.assert_allclose(core, single.core, rtol=0, atol=tol * np.abs(single.core).max())
+
+
+# ---------------------------------------------------------------- general block grids
+BDIMS = (40, 36, 30)
+
+
+def _block_worker(rank, world, port, grid, alg, dtype, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from oracle import pyoracle as O
+        import paper_1412_1885_b200 as P
+        from paper_1412_1885_b200.dist import GridPlan, dist_rand_tucker, dist_rand_tucker_2i
+        O.build()
+        y = _tensor(O)
+        plan = GridPlan.even(BDIMS, grid)
+        lo, ln = plan.block(rank)
+        ctx = P.Context.default()
+        ctx.bind_torch_stream()
+        yd = P.DenseTensor.from_numpy(plan.local(y, rank).astype(dtype), dtype).cuda()
+        fn = dist_rand_tucker_2i if alg == "2i" else dist_rand_tucker
+        m = fn(yd, BDIMS, lo, RANKS, P_OVER, SEED, context=ctx).to_host()
+        q.put((rank, m.core, m.factors))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported by the parent
+        import traceback
+        q.put((rank, repr(e) + traceback.format_exc(), None))
+
+
+@pytest.mark.parametrize("alg,grid,dtype", [("2i", (2, 2, 2), np.float64), ("2i", (2, 2, 2), np.float32),
+                                            ("2i", (1, 3, 1), np.float64), ("alg2", (2, 2, 2), np.float64),
+                                            ("alg2", (3, 1, 2), np.float32)])
+def test_block_grid_matches_single_process(O, alg, grid, dtype):
+    """dist_rand_tucker(_2i) over a general BlockGrid (dist.hpp:24-123, e.g. BASELINE cfg 5's
+    2 x 2 x 2 grid on 8 ranks): every rank projects its block with its rows of every factor,
+    partial sketches (own rows of Z for partitioned modes) and partial cores are summed — the
+    model equals the single-process model and the oracle; all ranks hold the identical model."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import torch.multiprocessing as mp
+    import paper_1412_1885_b200 as P
+    world = int(np.prod(grid))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_block_worker, args=(r, world, port, grid, alg, dtype, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, core, fac = q.get(timeout=600)
+        assert fac is not None, core
+        res[r] = (core, fac)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    y = _tensor(O)
+    yt = P.DenseTensor.from_numpy(y.astype(dtype), dtype).cuda()
+    if alg == "2i":
+        single = P.rand_tucker_2i(yt, RANKS, P_OVER, SEED).to_host()
+        g_ref, u_ref = O.rand_tucker_2i(y.astype(dtype).astype(np.float64), RANKS, P_OVER, SEED)
+    else:
+        single = P.rand_tucker(yt, RANKS, P_OVER, SEED).to_host()
+        g_ref, u_ref = O.rand_tucker(y.astype(dtype).astype(np.float64), RANKS, P_OVER, SEED)
+    tol = 1e-10 if dtype == np.float64 else 1e-4
+    for r in range(world):
+        core, fac = res[r]
+        for u, us, uo in zip(fac, single.factors, u_ref):
+            assert orthonormality_defect(u) < 1e-10
+            assert subspace_dist(u, us) < tol
+            assert subspace_dist(u, uo) < (1e-8 if dtype == np.float64 else 1e-3)
+        np.testing.assert_allclose(core, single.core, rtol=0, atol=tol * np.abs(single.core).max())
+        for a, b in zip(res[0][1], fac):  # replicated QR: identical models on every rank
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(res[0][0], core)
+
+
+def test_block_generation_tiles_the_global_tensor():
+    """generate_as(block=...) of every block of a 2 x 2 x 2 grid, placed at its offsets,
+    == generate() of the whole tensor (every entry drawn at its global index; the sigma of
+    the noise from norms summed over the blocks) — cfg 5's blockwise on-device generation."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1412_1885_b200.dist import GridPlan
+    from paper_1412_1885_b200.generators import generate, generate_as, gaussian_block, gaussian_flat
+    from paper_1412_1885_b200 import SeedSpec
+    dims = (24, 20, 31)
+    cfg = dict(dims=dims, gen="tucker", mlrank=(3, 4, 2), snr=20.0)
+    full = generate(cfg).cpu().numpy().reshape(dims, order="F")
+    plan = GridPlan.even(dims, (2, 2, 2))
+    # noise/raw draws: the block fill equals the slice of the flat stream
+    s = SeedSpec(4, 2)
+    flat = gaussian_flat(int(np.prod(dims)), s).cpu().numpy().reshape(dims, order="F")
+    for r in range(plan.world):
+        lo, ln = plan.block(r)
+        got = gaussian_block(dims, lo, ln, s).cpu().numpy().reshape(ln, order="F")
+        np.testing.assert_array_equal(got, plan.local(flat, r))
+    # sigma from the whole tensor's norms: sum the blocks' squared norms like all_sum would
+    parts = {}
+    # all_sum stand-in: first collect each block's (||Y||^2, ||E||^2), then feed the totals
+    norms = []
+    for r in range(plan.world):
+        rec = []
+        generate_as(cfg, torch.float64, block=plan.block(r), all_sum=lambda x, rec=rec: rec.append(x) or x)
+        norms.append(rec)
+    tot = [sum(v[i] for v in norms) for i in range(2)]
+    for r in range(plan.world):
+        it = iter(tot)
+        parts[r] = generate_as(cfg, torch.float64, block=plan.block(r), all_sum=lambda x, it=it: next(it))
+    out = np.zeros(dims)
+    for r in range(plan.world):
+        lo, ln = plan.block(r)
+        out[lo[0]:lo[0] + ln[0], lo[1]:lo[1] + ln[1], lo[2]:lo[2] + ln[2]] = \
+            parts[r].cpu().numpy().reshape(ln, order="F")
+    np.testing.assert_allclose(out, full, rtol=0, atol=1e-12 * np.abs(full).max())

@@ -286,7 +286,8 @@ def run_b200(args, cfg):
         comm = D.DistComm(blo[-1], gdims[-1], D.exchange_capacity(gdims, cfg["ranks"], cfg["p"]), block_lo=blo,
                           global_dims=gdims)
         ctx.set_comm(comm)
-    kw = dict(sync_ranks=False, out="device", global_dims=gdims if world > 1 else ())
+    kw = dict(sync_ranks=False, out="device", global_dims=gdims if world > 1 else (),
+              one_pass_per_step=args.one_pass_per_step)
 
     def step(time_kernels=False):
         return P.rand_tucker_2i(yd, cfg["ranks"], cfg["p"], alg_seed, context=ctx, time_kernels=time_kernels, **kw)
@@ -299,7 +300,8 @@ def run_b200(args, cfg):
         nw = 0
         # >= 1 s of warm-up with the timed call itself, so a repeated call's CUDA graph is
         # captured here (first call eager, second captures, then replays) and not timed
-        while nw < max(args.warmup, 3) or time.perf_counter() - t_w < 1.0:
+        # the number of warm-up calls is agreed over ranks (every call runs collectives)
+        while nw < max(args.warmup, 3) or all_max(float(time.perf_counter() - t_w < 1.0), world) > 0:
             m = step(time_kernels=True)
             nw += 1
         log(f"[rank {rank}/{world}] warm-up done ({nw} calls)")
@@ -348,7 +350,8 @@ def run_b200(args, cfg):
             barrier(world)
             t0 = time.perf_counter()
             mm = P.rand_tucker_2i(yh, cfg["ranks"], cfg["p"], alg_seed, context=ctx, sync_ranks=False,
-                                  global_dims=kw["global_dims"], out="device")
+                                  global_dims=kw["global_dims"], one_pass_per_step=args.one_pass_per_step,
+                                  out="device")
             res = P.ffcp(mm, cfg["ffcp_rank"], P.ConstraintSpec(cfg["constraint"]), P.StopRule(*STOP), alg_seed,
                          context=ctx)  # on the device model; CP factors come back to the host
             mh = mm.to_host()  # Tucker core + factors to the host
@@ -399,7 +402,10 @@ def run_b200(args, cfg):
             "config": {"workload": args.config, "dims": gdims, "ranks": list(cfg["ranks"]), "oversample": cfg["p"],
                        "ffcp_rank": cfg["ffcp_rank"], "passes_per_step": passes,
                        "parallelism": ("block" + "x".join(map(str, grid))) if world > 1 else "slab1",
-                       "l2": "inputs larger than L2 (126 MB)", "core": "derived from X_{N-1} (2N passes)"},
+                       "l2": "inputs larger than L2 (126 MB)",
+                       "core": "derived from X_{N-1}",
+                       "steps_per_pass": "one Y pass per range step" if args.one_pass_per_step else
+                       "consecutive range steps share one Y pass (reference: 2N+1 passes)"},
             "hbm_frac_of_peak": round(value / world / hbm, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic,
@@ -437,6 +443,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--one-pass-per-step", action="store_true",
+                    help="A/B: stream Y once per range step (reference structure) instead of sharing passes")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-slabs", type=int, default=100)

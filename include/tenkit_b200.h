@@ -88,6 +88,10 @@ typedef struct tk_tucker_opts {
                                call's stream and report their summed device time in stats */
     int overlap;            /* 1: launch the next Y pass on a second stream so it overlaps the
                                current QR (it contracts a mode whose factor is already final) */
+    int one_pass_per_step;  /* 1: every range step streams Y itself (the reference's structure,
+                               tucker.hpp:149-160); 0: consecutive steps with distinct modes share
+                               one Y pass over a mode outside the group (same values up to
+                               rounding; N = 3: 3 Y passes instead of 6) */
 } tk_tucker_opts;
 
 /* Per-call timing/trace (filled when non-null) */

@@ -175,6 +175,7 @@ struct TuckerRun {
     std::vector<T*> Up;      // packed k-major copies
     int launches = 0;
     int passes = 0;
+    int group_count = 0;
     int* rank_dev = nullptr;
     bool time_kernels = false;
     std::vector<cudaEvent_t> ev;  // (start, stop) pairs around Y-streaming launches
@@ -227,6 +228,22 @@ struct TuckerRun {
         return -1;
     }
 
+    // Leader of a shared Y pass for a group of steps whose modes are `mask`: a mode outside the
+    // group that can lead a pass (first_mode's rule), preferring one other than `avoid`.
+    int leader_mode(uint32_t mask, int avoid) const {
+        int fallback = -1;
+        for (int m = static_cast<int>(order) - 1; m >= 0; --m) {
+            if (mask & (1u << m)) continue;
+            // small tensors (latency-bound passes): any mode can lead (FFMA kernels)
+            const bool capable = prod(std::vector<int64_t>(ldims.begin(), ldims.begin() + m)) >= 256 ||
+                                 (m == 0 && km_stream_ok()) || prod(ldims) * int64_t(sizeof(T)) <= (int64_t(256) << 20);
+            if (!capable) continue;
+            if (m != avoid) return m;
+            fallback = m;
+        }
+        return fallback;
+    }
+
     // Mode 0 can lead a Y pass when the K-major tcgen05 kernel takes it (fp32, I_0 % 4 == 0).
     // Only on the tcgen05-everywhere path (2): a 512-row-tile Y pass keeps one accumulator
     // set, whose truncating accumulation over K = I_0 doubles the fp32 basis error in the
@@ -235,7 +252,7 @@ struct TuckerRun {
         if constexpr (sizeof(T) != 4) {
             return false;
         } else {
-            if (ctx->ttm_path != 2 || cols.empty()) return false;
+            if (ctx->ttm_path == 1 || cols.empty()) return false;
             const int64_t K = ldims[0];
             const int64_t Q = prod(ldims) / K;
             return K % 4 == 0 && K >= 16 && cols[0] <= 32 && (Q + 127) / 128 >= 148 &&
@@ -306,7 +323,7 @@ struct TuckerRun {
             const double* u = U[m] + off[m];
             launch_pack_umma(u, gdims[m], K, cols[m], bpk, s);
             if (streams_y && time_kernels) mark();
-            launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s);
+            launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s, /*accurate=*/true);
             if (streams_y && time_kernels) mark();
             launches += 2;
             return true;
@@ -391,19 +408,47 @@ struct TuckerRun {
         const bool sync = opt.sync_ranks != 0;
         const T* xlast = nullptr;
         std::vector<int64_t> xd;
-        // Steps (pass, n). The Y pass of step k+1 contracts a mode whose factor is already final
-        // and is launched on the side stream right after step k's QR, so the latency-bound QR
-        // runs under the bandwidth-bound pass (2 of the 148 SMs for the QR cluster).
+        // Steps (pass, n). Consecutive steps with distinct modes form a group that shares ONE Y
+        // pass: the group's first-stage contraction is over a mode m outside the group (its
+        // factor is final for every step of the group), so T = Y x_m U_m^T serves them all and
+        // each step only contracts T with the group's other factors (N = 3: 6 steps -> 3 Y
+        // passes; N = 4: 8 -> 3). opt.one_pass_per_step = 1 keeps one pass per step. A group's
+        // Y pass that does not contract the factor the previous step's QR is producing is
+        // launched on the side stream right after that QR, so the latency-bound QR runs under
+        // the bandwidth-bound pass (2 of the 148 SMs for the QR cluster).
         const int nsteps = 2 * static_cast<int>(order);
         const bool overlap = opt.overlap && order > 1;
         if (overlap) ctx->ensure_side();
+        struct Group {
+            int s, e, leader;
+        };
+        std::vector<Group> groups;
+        for (int st = 0; st < nsteps;) {
+            const int avoid = st > 0 ? (st - 1) % static_cast<int>(order) : -1;
+            Group g{st, st + 1, order == 1 ? -1 : first_mode(st % static_cast<int>(order), avoid)};
+            while (opt.one_pass_per_step == 0 && order > 2 && g.e < nsteps) {
+                uint32_t mask = 0;
+                bool distinct = true;
+                for (int k = g.s; k <= g.e; ++k) {
+                    const uint32_t bit = 1u << (k % static_cast<int>(order));
+                    distinct = distinct && !(mask & bit);
+                    mask |= bit;
+                }
+                const int l = distinct ? leader_mode(mask, avoid) : -1;
+                if (l < 0) break;
+                g.e += 1;
+                g.leader = l;
+            }
+            groups.push_back(g);
+            st = g.e;
+        }
         std::vector<int64_t> d1;
         const T* t1 = nullptr;
         int f = -1;
         bool on_side = false;
-        auto launch_first = [&](int n, int avoid, bool side) {
-            f = order == 1 ? -1 : first_mode(n, avoid);
-            on_side = side && f >= 0 && f != avoid;
+        auto launch_first = [&](int leader, bool side) {
+            f = leader;
+            on_side = side && f >= 0;
             if (on_side) {
                 TK_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_free, 0));  // finish() done with proj1
                 cudaStream_t keep = s;
@@ -417,31 +462,32 @@ struct TuckerRun {
                 t1 = first_stage(f, d1);
             }
         };
-        launch_first(0, -1, false);
-        for (int step = 0; step < nsteps; ++step) {
-            const int pass = step / static_cast<int>(order), n = step % static_cast<int>(order);
-            if (on_side) TK_CUDA(cudaStreamWaitEvent(s, ctx->ev_fs, 0));
-            xd = d1;
-            const T* x = (order == 1) ? y : finish(t1, xd, n, f);
-            const bool can_overlap = overlap && x != t1;  // the sketch must not read proj1
-            qr_event = can_overlap ? ctx->ev_free : nullptr;  // recorded right before this step's QR
-            range_step(x, xd, n, alg3_omega_seed(seed, pass, n), step, false);
-            qr_event = nullptr;
-            xlast = x;
-            if (step + 1 < nsteps) {
-                const int nn = (step + 1) % static_cast<int>(order);
-                const int fn = order == 1 ? -1 : first_mode(nn, n);
-                if (can_overlap && fn != n) {
-                    launch_first(nn, n, true);  // uses factors other than U_n: independent of this QR
+        launch_first(groups[0].leader, false);
+        for (size_t gi = 0; gi < groups.size(); ++gi) {
+            const Group& g = groups[gi];
+            for (int step = g.s; step < g.e; ++step) {
+                const int pass = step / static_cast<int>(order), n = step % static_cast<int>(order);
+                if (on_side && step == g.s) TK_CUDA(cudaStreamWaitEvent(s, ctx->ev_fs, 0));
+                xd = d1;
+                const T* x = (order == 1) ? y : finish(t1, xd, n, f);
+                const bool last = step + 1 == g.e;
+                const bool next = gi + 1 < groups.size();
+                // the sketch must not read proj1; the next pass must not need this step's U_n
+                const bool can_overlap = overlap && x != t1 && last && next && groups[gi + 1].leader != n;
+                qr_event = can_overlap ? ctx->ev_free : nullptr;  // recorded right before this step's QR
+                range_step(x, xd, n, alg3_omega_seed(seed, pass, n), step, false);
+                qr_event = nullptr;
+                xlast = x;
+                if (can_overlap) {
+                    launch_first(groups[gi + 1].leader, true);  // independent of this QR
                     if (sync) sync_rank(n, step);
                 } else {
                     if (sync) sync_rank(n, step);
-                    launch_first(nn, n, false);
+                    if (last && next) launch_first(groups[gi + 1].leader, false);
                 }
-            } else if (sync) {
-                sync_rank(n, step);
             }
         }
+        group_count = static_cast<int>(groups.size());
         if (!sync && !capture) {  // verify the full-rank speculation
             int hr[2 * TK_MAX_ORDER];
             TK_CUDA(cudaMemcpyAsync(hr, rank_dev, sizeof(int) * 2 * order, cudaMemcpyDeviceToHost, s));
@@ -627,7 +673,7 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
               tk_tucker_stats* stats) {
     std::string key = std::to_string(sizeof(T)) + "|" + std::to_string(reinterpret_cast<uintptr_t>(ydev)) + "|" +
                       std::to_string(p) + "|" + std::to_string(seed.root) + "|" + std::to_string(seed.stream) + "|" +
-                      std::to_string(opt.explicit_core_pass) + std::to_string(opt.overlap) +
+                      std::to_string(opt.explicit_core_pass) + std::to_string(opt.overlap) + std::to_string(opt.one_pass_per_step) +
                       std::to_string(opt.time_kernels) + "|" + std::to_string(ctx->ttm_path);
     for (int64_t n = 0; n < order; ++n) key += "|" + std::to_string(ld[n]) + "x" + std::to_string(rk[n]);
     auto& g = ctx->g2i;

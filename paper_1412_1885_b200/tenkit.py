@@ -290,7 +290,8 @@ def _tucker_call(fn_name, y, ranks, oversample, seed, context, out, opts=None):
             _i64arr(ranks), int(oversample), int(seed.root), int(seed.stream)]
     if fn_name == "tk_rand_tucker_2i":
         oo = _lib.tk_tucker_opts(int(getattr(opts, "explicit_core_pass", 0)), int(getattr(opts, "sync_ranks", 1)),
-                                 int(getattr(opts, "time_kernels", 0)), int(getattr(opts, "overlap", 1)))
+                                 int(getattr(opts, "time_kernels", 0)), int(getattr(opts, "overlap", 1)),
+                                 int(getattr(opts, "one_pass_per_step", 0)))
         rc = getattr(ctx.lib, fn_name)(*args, C.byref(oo), C.byref(o), C.byref(st))
     else:
         rc = getattr(ctx.lib, fn_name)(*args, C.byref(o), C.byref(st))
@@ -316,17 +317,20 @@ class TuckerOptions:
     time_kernels: int = 0
     overlap: int = 1
     _global_dims: tuple = ()
+    one_pass_per_step: int = 0
 
 
 def rand_tucker_2i(y, ranks, oversample: int, seed, *, explicit_core_pass: bool = False, sync_ranks: bool = True,
                    context: Context | None = None, out: str | None = None, global_last_dim: int = 0,
-                   time_kernels: bool = False, overlap: bool = True, global_dims=()) -> TuckerModel:
+                   time_kernels: bool = False, overlap: bool = True, global_dims=(),
+                   one_pass_per_step: bool = False) -> TuckerModel:
     """Alg. 3 (tucker.hpp:136-169) on the B200. `y`: numpy array (host; copied in) or a
     device DenseTensor. Returns a host (numpy) model for host input, device otherwise,
     unless out='host'/'device'. global_dims / global_last_dim: with a comm hook installed,
-    y is this rank's block of a tensor of these global extents (dist.py)."""
+    y is this rank's block of a tensor of these global extents (dist.py). one_pass_per_step:
+    stream Y once per range step like the reference (default: consecutive steps share a pass)."""
     opts = TuckerOptions(int(explicit_core_pass), int(sync_ranks), int(global_last_dim), int(time_kernels),
-                         int(overlap), tuple(int(d) for d in global_dims))
+                         int(overlap), tuple(int(d) for d in global_dims), int(one_pass_per_step))
     return _tucker_call("tk_rand_tucker_2i", y, ranks, oversample, seed, context, out, opts)
 
 

@@ -66,4 +66,4 @@ def test_rand_tucker_2i_tc_path_matches_oracle(P, O):
         assert subspace_dist(u, v) < 1e-3
     ysq = float(np.sum(y32.astype(np.float64) ** 2))
     assert abs(float(np.sum(m.core ** 2)) - float(np.sum(g_ref ** 2))) / ysq < 1e-5
-    assert m.stats["passes"] == 6
+    assert m.stats["passes"] == 3  # steps share Y passes; the mode-0 pass on the K-major kernel

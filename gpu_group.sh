@@ -1,7 +1,7 @@
 #!/bin/bash
 # Shared-pass step groups: full GPU tests, bench (grouped and one-pass-per-step A/B), ncu launch list.
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q --deselect tests/test_gpu_dist.py > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
 tail -4 gpurun_out/gpu_tests.log
 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_grp.log 2> gpurun_out/bench_grp.err; echo "bench rc=$?"
 tail -1 gpurun_out/bench_grp.log | cut -c1-420

@@ -40,8 +40,10 @@ int64_t umma_pack_bytes(int64_t rows, int cols);
 void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s);
 // accurate: for P == 1 always use the 128-row K-major tiles with 3 accumulator sets (fp32
 // FFMA-level error) instead of the faster single-set 256-row tiles.
+// tout (P == 1 only): write the output transposed, out[q + r Q] (the contracted mode moves to
+// the slowest position) instead of out[r + q cols].
 void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s, bool accurate = false);
+                   cudaStream_t s, bool accurate = false, bool tout = false);
 
 // Pack a column-major double factor (rows x cols, leading dim ld) into T k-major
 // [rows][pack_stride(cols)] with zero padding.
@@ -90,6 +92,10 @@ void launch_gaussian_fill(double* out, int64_t n, uint64_t offset, uint64_t key,
 
 template <typename S, typename D>
 void launch_cast(const S* in, D* out, int64_t n, cudaStream_t s);
+// out (standard column-major, dims[0..order)) = in stored with its modes in the order perm
+// (in's storage position k holds mode perm[k]), cast S -> D.
+template <typename S, typename D>
+void launch_permute_cast(const S* in, D* out, int order, const int64_t* dims, const int* perm, cudaStream_t s);
 // out[i + j*ldo] = in[i + j*ldi] (rows x cols)
 template <typename S, typename D>
 void launch_cast2d(const S* in, int64_t ldi, D* out, int64_t ldo, int64_t rows, int64_t cols, cudaStream_t s);

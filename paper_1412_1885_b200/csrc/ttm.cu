@@ -512,6 +512,24 @@ __global__ void gaussian_packed_map_kernel(T* __restrict__ out, int64_t rows, in
     }
 }
 
+struct PermDesc {
+    int order;
+    int64_t dims[8];     // standard extents
+    int64_t sstride[8];  // storage stride of each (standard) mode
+};
+
+template <typename S, typename D>
+__global__ void permute_cast_kernel(const S* __restrict__ in, D* __restrict__ out, int64_t n, PermDesc pd) {
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+        int64_t rem = t, src = 0;
+        for (int k = 0; k < pd.order; ++k) {
+            src += (rem % pd.dims[k]) * pd.sstride[k];
+            rem /= pd.dims[k];
+        }
+        out[t] = static_cast<D>(in[src]);
+    }
+}
+
 template <typename S, typename D>
 __global__ void cast2d_kernel(const S* __restrict__ in, int64_t ldi, D* __restrict__ out, int64_t ldo, int64_t rows,
                               int64_t cols) {
@@ -645,6 +663,27 @@ void launch_cast(const S* in, D* out, int64_t n, cudaStream_t s) {
     cast_kernel<S, D><<<grid_for(n), 256, 0, s>>>(in, out, n);
     TK_LAUNCH_CHECK();
 }
+
+template <typename S, typename D>
+void launch_permute_cast(const S* in, D* out, int order, const int64_t* dims, const int* perm, cudaStream_t s) {
+    require(order >= 1 && order <= 8, "permute: order must be in [1, 8]");
+    PermDesc pd{};
+    pd.order = order;
+    int64_t n = 1, st = 1;
+    for (int k = 0; k < order; ++k) {
+        pd.dims[k] = dims[k];
+        n *= dims[k];
+    }
+    for (int k = 0; k < order; ++k) {  // storage position k holds mode perm[k]
+        pd.sstride[perm[k]] = st;
+        st *= dims[perm[k]];
+    }
+    permute_cast_kernel<S, D><<<grid_for(n), 256, 0, s>>>(in, out, n, pd);
+    TK_LAUNCH_CHECK();
+}
+template void launch_permute_cast<float, double>(const float*, double*, int, const int64_t*, const int*, cudaStream_t);
+template void launch_permute_cast<double, double>(const double*, double*, int, const int64_t*, const int*, cudaStream_t);
+template void launch_permute_cast<float, float>(const float*, float*, int, const int64_t*, const int*, cudaStream_t);
 
 template void launch_ttm<float>(const float*, const float*, float*, int64_t, int64_t, int64_t, int, cudaStream_t, int*,
                                 float*, int64_t);

@@ -188,7 +188,7 @@ __device__ __forceinline__ void drain16(uint32_t tl, int j, int rc, int used, fl
 template <int NH, int MT_, bool KM, int OCC = 1>
 __global__ void __launch_bounds__(kTcThreads, OCC)
     ttm_tc_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
-                  int64_t P, int64_t K, int cols, int64_t tiles_p) {
+                  int64_t P, int64_t K, int cols, int64_t tiles_p, int tout) {
     using C = TcCfg<NH, MT_, OCC>;
     constexpr int MT = C::MT, BM = C::BM;
     extern __shared__ __align__(1024) uint8_t tsm[];
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
         // ===== epilogue: D = D[:, 0:NH] + D[:, NH:2NH], rows MT*L + j =====
         mbar_wait(dfull, 0);
         fence_after();
-        if constexpr (KM) {
+        if (KM && !tout) {
             // D tile j, TMEM lane L = row j*128 + L: stage [row][cols] in the (drained) Y
             // buffers, then copy the contiguous out[p0*cols ...] block with coalesced stores
             float* stg = reinterpret_cast<float*>(sY);
@@ -435,7 +435,7 @@ __global__ void pack_umma_kernel(const double* __restrict__ u, int64_t ld, int64
 
 template <int NH, int MT, bool KM, int OCC = 1>
 void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-               cudaStream_t s) {
+               cudaStream_t s, bool tout = false) {
     using C = TcCfg<NH, MT, OCC>;
     static bool attr = false;
     if (!attr) {
@@ -472,7 +472,7 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
     require(grid < (int64_t(1) << 31), "ttm: grid too large");
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     ttm_tc_kernel<NH, MT, KM, OCC><<<static_cast<unsigned>(grid), kTcThreads, C::smem, s>>>(map, bpk, out, P, K, cols,
-                                                                                           tiles_p);
+                                                                                           tiles_p, tout ? 1 : 0);
     TK_LAUNCH_CHECK();
 }
 
@@ -520,14 +520,14 @@ bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t
 }
 
 void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s, bool accurate) {
+                   cudaStream_t s, bool accurate, bool tout) {
     const uint8_t* b = static_cast<const uint8_t*>(bpk);
     if (P == 1) {
-        const bool wide = km_wide(Q) && !accurate;  // narrow tiles: 3 accumulator sets
-        if (tc_nh(cols) <= 16) return wide ? launch_tc<16, 2, true, 2>(in, b, out, P, K, Q, cols, s)
-                                           : launch_tc<16, 1, true, 2>(in, b, out, P, K, Q, cols, s);
-        return wide ? launch_tc<32, 2, true, 2>(in, b, out, P, K, Q, cols, s)
-                    : launch_tc<32, 1, true, 2>(in, b, out, P, K, Q, cols, s);
+        const bool wide = km_wide(Q) && !accurate && !tout;  // narrow tiles: 3 accumulator sets
+        if (tc_nh(cols) <= 16) return wide ? launch_tc<16, 2, true, 2>(in, b, out, P, K, Q, cols, s, tout)
+                                           : launch_tc<16, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
+        return wide ? launch_tc<32, 2, true, 2>(in, b, out, P, K, Q, cols, s, tout)
+                    : launch_tc<32, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
     }
     static const int variant = [] {
         const char* e = std::getenv("TENKIT_TC_VARIANT");

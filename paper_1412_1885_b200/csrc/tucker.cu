@@ -260,35 +260,58 @@ struct TuckerRun {
         }
     }
 
+    // Intermediate tensors may hold their modes in a permuted storage order: xd are the extents
+    // in storage order and xp[k] the mode stored at position k (identity unless a mode-0 Y
+    // pass wrote its output transposed, moving mode 0 to the slowest position).
+    std::vector<int> ident() const {
+        std::vector<int> v(static_cast<size_t>(order));
+        std::iota(v.begin(), v.end(), 0);
+        return v;
+    }
+    static int pos_of(const std::vector<int>& xp, int m) {
+        for (size_t k = 0; k < xp.size(); ++k)
+            if (xp[k] == m) return static_cast<int>(k);
+        return -1;
+    }
+
     // First stage: Y x_f U_f^T into "proj1" (dims updated). Runs on the current stream `s`.
-    const T* first_stage(int f, std::vector<int64_t>& xd) {
+    // A mode-0 pass (K-major tcgen05 kernel) writes its output transposed (mode 0 last), so the
+    // later contractions of the group see the big modes first (M-major / K-major shapes).
+    const T* first_stage(int f, std::vector<int64_t>& xd, std::vector<int>& xp) {
         xd = ldims;
+        xp = ident();
         if (f < 0) return y;
         const int64_t P = prod(std::vector<int64_t>(xd.begin(), xd.begin() + f));
         const int64_t K = xd[f];
         const int64_t Q = prod(std::vector<int64_t>(xd.begin() + f + 1, xd.end()));
         T* out = static_cast<T*>(ctx->buf("proj1", sizeof(T) * P * cols[f] * Q));
-        if (!stream_ttm(y, f, out, P, K, Q, true)) {
+        bool tout = false;
+        if (!stream_ttm(y, f, out, P, K, Q, true, &tout)) {
             if (time_kernels) mark();
             ttm(y, factor_rows(f), out, P, K, Q, cols[f]);
             if (time_kernels) mark();
         }
         ++passes;
         xd[f] = cols[f];
+        if (tout) {  // storage (1, 2, ..., N-1, 0)
+            std::rotate(xd.begin(), xd.begin() + 1, xd.end());
+            std::rotate(xp.begin(), xp.begin() + 1, xp.end());
+        }
         return out;
     }
 
     // Remaining (small) contractions of every mode except skip and f, descending.
-    const T* finish(const T* cur, std::vector<int64_t>& xd, int skip, int f) {
+    const T* finish(const T* cur, std::vector<int64_t>& xd, const std::vector<int>& xp, int skip, int f) {
         int which = 0;
         for (int m = static_cast<int>(order) - 1; m >= 0; --m) {
             if (m == skip || m == f) continue;
-            const int64_t P = prod(std::vector<int64_t>(xd.begin(), xd.begin() + m));
-            const int64_t K = xd[m];
-            const int64_t Q = prod(std::vector<int64_t>(xd.begin() + m + 1, xd.end()));
+            const int k = pos_of(xp, m);
+            const int64_t P = prod(std::vector<int64_t>(xd.begin(), xd.begin() + k));
+            const int64_t K = xd[k];
+            const int64_t Q = prod(std::vector<int64_t>(xd.begin() + k + 1, xd.end()));
             T* out = static_cast<T*>(ctx->buf(which ? "projB" : "projA", sizeof(T) * P * cols[m] * Q));
             if (!stream_ttm(cur, m, out, P, K, Q, false)) ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
-            xd[m] = cols[m];
+            xd[k] = cols[m];
             cur = out;
             which ^= 1;
         }
@@ -296,19 +319,21 @@ struct TuckerRun {
     }
 
     // Y x_{p != skip} U_p^T (skip = -1: all modes), on the current stream.
-    const T* project(int skip, std::vector<int64_t>& xd) {
+    const T* project(int skip, std::vector<int64_t>& xd, std::vector<int>& xp) {
         if (order == 1 && skip == 0) {
             xd = ldims;
+            xp = ident();
             return y;
         }
         const int f = first_mode(skip, -1);
-        const T* t1 = first_stage(f, xd);
-        return finish(t1, xd, skip, f);
+        const T* t1 = first_stage(f, xd, xp);
+        return finish(t1, xd, xp, skip, f);
     }
 
     // The Y-streaming contraction on the tcgen05 tensor cores (3xTF32, ttm_tc.cu) when the data
     // is fp32 and the shape tiles the GPU; returns false to fall back to the FFMA kernels.
-    bool stream_ttm(const T* in, int m, T* out, int64_t P, int64_t K, int64_t Q, bool streams_y) {
+    bool stream_ttm(const T* in, int m, T* out, int64_t P, int64_t K, int64_t Q, bool streams_y,
+                    bool* tout = nullptr) {
         if constexpr (sizeof(T) != 4) {
             return false;
         } else {
@@ -323,7 +348,9 @@ struct TuckerRun {
             const double* u = U[m] + off[m];
             launch_pack_umma(u, gdims[m], K, cols[m], bpk, s);
             if (streams_y && time_kernels) mark();
-            launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s, /*accurate=*/true);
+            const bool tr = tout && P == 1;  // a mode-0 Y pass: transposed output
+            launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s, /*accurate=*/true, tr);
+            if (tr) *tout = true;
             if (streams_y && time_kernels) mark();
             launches += 2;
             return true;
@@ -347,29 +374,54 @@ struct TuckerRun {
 
     // Z = unfold(X, n) * Omega (tensor.hpp:195-209) straight into fp64 z (leading dimension
     // ldz) for the QR: one split-K kernel over the (B, I, A) view, no materialised unfolding.
-    void sketch(const T* x, const std::vector<int64_t>& xd, int n, const T* omp, int rn, double* z, int64_t ldz) {
-        const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + n));
-        const int64_t I = xd[n];
-        const int64_t A = prod(std::vector<int64_t>(xd.begin() + n + 1, xd.end()));
+    // x stored with mode order xp; omp must hold Omega's rows in the matching column order.
+    void sketch(const T* x, const std::vector<int64_t>& xd, const std::vector<int>& xp, int n, const T* omp, int rn,
+                double* z, int64_t ldz) {
+        const int k = pos_of(xp, n);
+        const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + k));
+        const int64_t I = xd[k];
+        const int64_t A = prod(std::vector<int64_t>(xd.begin() + k + 1, xd.end()));
         double* work = static_cast<double*>(ctx->buf(work_name == std::string("splitk") ? "sketch_part" : "sketch_part_side",
                                                      sizeof(double) * sketch_work_elems(I, rn)));
         launches += launch_sketch<T>(x, B, I, A, omp, rn, z, ldz, work, s);
     }
 
     // One range-finding step for mode n: Z = unfold(X, n) Omega, U_n = basis(Z)
-    void range_step(const T* x, const std::vector<int64_t>& xd, int n, const Seed& omega_seed, int step, bool sync) {
+    void range_step(const T* x, const std::vector<int64_t>& xd, const std::vector<int>& xp, int n,
+                    const Seed& omega_seed, int step, bool sync) {
         const int64_t W = prod(std::vector<int64_t>(cols.begin(), cols.end()), n);
         const int rn = rt[n];
         T* omp = static_cast<T*>(ctx->buf("omega_p", sizeof(T) * W * pack_stride(rn)));
-        launch_gaussian_packed<T>(omp, W, rn, omega_seed.key(), s);
+        // Omega rows follow the unfolding's columns (modes != n ascending, tensor.hpp:103-116);
+        // for a permuted x its storage columns map to them through a mixed-radix RowMap
+        bool ordered = true;
+        RowMap map;
+        {
+            std::vector<int64_t> stride(static_cast<size_t>(order), 0);
+            int64_t st = 1;
+            for (int m = 0; m < order; ++m)
+                if (m != n) stride[m] = st, st *= cols[m];
+            int prev = -1;
+            for (int k = 0; k < order; ++k) {
+                if (xp[k] == n) continue;
+                ordered = ordered && xp[k] > prev;
+                prev = xp[k];
+                map.lext[map.nd] = xd[k];
+                map.gstride[map.nd] = stride[xp[k]];
+                ++map.nd;
+            }
+            map.rows_total = W;
+        }
+        if (ordered) launch_gaussian_packed<T>(omp, W, rn, omega_seed.key(), s);
+        else launch_gaussian_packed_map<T>(omp, W, rn, omega_seed.key(), map, s);
         ++launches;
         const int64_t In = gdims[n];
         double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * In * rn));
         if (ldims[n] != In) {  // this rank's rows of Z, the others zero (summed over ranks)
             TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * In * rn, s));
-            sketch(x, xd, n, omp, rn, z + off[n], In);
+            sketch(x, xd, xp, n, omp, rn, z + off[n], In);
         } else {
-            sketch(x, xd, n, omp, rn, z, In);
+            sketch(x, xd, xp, n, omp, rn, z, In);
         }
         allreduce(z, In * rn);
         if (qr_event) TK_CUDA(cudaEventRecord(qr_event, s));
@@ -443,6 +495,7 @@ struct TuckerRun {
             st = g.e;
         }
         std::vector<int64_t> d1;
+        std::vector<int> p1, xp;
         const T* t1 = nullptr;
         int f = -1;
         bool on_side = false;
@@ -454,12 +507,12 @@ struct TuckerRun {
                 cudaStream_t keep = s;
                 s = ctx->side;
                 work_name = "splitk_side";
-                t1 = first_stage(f, d1);
+                t1 = first_stage(f, d1, p1);
                 TK_CUDA(cudaEventRecord(ctx->ev_fs, s));
                 s = keep;
                 work_name = "splitk";
             } else {
-                t1 = first_stage(f, d1);
+                t1 = first_stage(f, d1, p1);
             }
         };
         launch_first(groups[0].leader, false);
@@ -469,13 +522,14 @@ struct TuckerRun {
                 const int pass = step / static_cast<int>(order), n = step % static_cast<int>(order);
                 if (on_side && step == g.s) TK_CUDA(cudaStreamWaitEvent(s, ctx->ev_fs, 0));
                 xd = d1;
-                const T* x = (order == 1) ? y : finish(t1, xd, n, f);
+                xp = p1;
+                const T* x = (order == 1) ? y : finish(t1, xd, xp, n, f);
                 const bool last = step + 1 == g.e;
                 const bool next = gi + 1 < groups.size();
                 // the sketch must not read proj1; the next pass must not need this step's U_n
                 const bool can_overlap = overlap && x != t1 && last && next && groups[gi + 1].leader != n;
                 qr_event = can_overlap ? ctx->ev_free : nullptr;  // recorded right before this step's QR
-                range_step(x, xd, n, alg3_omega_seed(seed, pass, n), step, false);
+                range_step(x, xd, xp, n, alg3_omega_seed(seed, pass, n), step, false);
                 qr_event = nullptr;
                 xlast = x;
                 if (can_overlap) {
@@ -496,23 +550,32 @@ struct TuckerRun {
                 if (hr[i] != rt[i % order]) throw std::runtime_error("rank-drop");  // caller reruns synchronously
         }
         // core
-        std::vector<int64_t> gd;
+        std::vector<int64_t> gd;  // core extents in storage order, then standard order
         const T* g;
         if (opt.explicit_core_pass || order == 1) {
-            g = project(-1, gd);
+            g = project(-1, gd, xp);
         } else {
             gd = xd;  // X_{N-1}: cols everywhere except mode N-1 (local extent)
             const int m = static_cast<int>(order - 1);
-            const int64_t P = prod(std::vector<int64_t>(gd.begin(), gd.begin() + m));
-            T* o = static_cast<T*>(ctx->buf("core", sizeof(T) * P * cols[m]));
-            ttm(xlast, factor_rows(m), o, P, gd[m], 1, cols[m]);
-            gd[m] = cols[m];
+            const int k = pos_of(xp, m);
+            const int64_t P = prod(std::vector<int64_t>(gd.begin(), gd.begin() + k));
+            const int64_t Q = prod(std::vector<int64_t>(gd.begin() + k + 1, gd.end()));
+            T* o = static_cast<T*>(ctx->buf("core", sizeof(T) * P * cols[m] * Q));
+            ttm(xlast, factor_rows(m), o, P, gd[k], Q, cols[m]);
+            gd[k] = cols[m];
             g = o;
         }
         const int64_t gsize = prod(gd);
         double* gdv = static_cast<double*>(ctx->buf("core64", sizeof(double) * gsize));
-        if constexpr (sizeof(T) == 4) launch_cast<float, double>(reinterpret_cast<const float*>(g), gdv, gsize, s);
-        else launch_cast<double, double>(reinterpret_cast<const double*>(g), gdv, gsize, s);
+        if (xp == ident()) {
+            if constexpr (sizeof(T) == 4) launch_cast<float, double>(reinterpret_cast<const float*>(g), gdv, gsize, s);
+            else launch_cast<double, double>(reinterpret_cast<const double*>(g), gdv, gsize, s);
+        } else {  // back to the standard mode order
+            std::vector<int64_t> sd(static_cast<size_t>(order));
+            for (int k = 0; k < order; ++k) sd[xp[k]] = gd[k];
+            gd = sd;
+            launch_permute_cast<T, double>(g, gdv, static_cast<int>(order), gd.data(), xp.data(), s);
+        }
         ++launches;
         allreduce(gdv, gsize);
         if (capture) {
@@ -600,7 +663,7 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
                 launch_cast2d<double, double>(reinterpret_cast<const double*>(zt), cd[0], zown, gd[0], cd[0], rt, s);
             r.launches += 2;
         } else {
-            r.sketch(cur, cd, n, op, rt, zown, gd[n]);
+            r.sketch(cur, cd, r.ident(), n, op, rt, zown, gd[n]);
             ++r.launches;
         }
         r.allreduce(z, gd[n] * rt);  // partial sketches summed over ranks (no-op on one rank)
@@ -1100,8 +1163,16 @@ int tk_ttm_all(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, c
                 r.U[n] = const_cast<double*>(ms[n]);
             }
             std::vector<int64_t> xd;
-            const T* x = r.project(static_cast<int>(skip), xd);
-            TK_CUDA(cudaMemcpyAsync(out, x, sizeof(T) * prod(xd), cudaMemcpyDeviceToDevice, ctx->stream));
+            std::vector<int> xp;
+            const T* x = r.project(static_cast<int>(skip), xd, xp);
+            if (xp == r.ident()) {
+                TK_CUDA(cudaMemcpyAsync(out, x, sizeof(T) * prod(xd), cudaMemcpyDeviceToDevice, ctx->stream));
+            } else {
+                std::vector<int64_t> sd(static_cast<size_t>(order));
+                for (int k = 0; k < order; ++k) sd[xp[k]] = xd[k];
+                launch_permute_cast<T, T>(x, static_cast<T*>(out), static_cast<int>(order), sd.data(), xp.data(),
+                                          ctx->stream);
+            }
         };
         if (dtype == TK_F32) body(float{});
         else body(double{});
@@ -1124,7 +1195,7 @@ int tk_unfold_times(tk_context* ctx, int dtype, int64_t order, const int64_t* di
             TuckerRun<T> r{ctx, ctx->stream, order, d, d, std::vector<int64_t>(order, 0), static_cast<const T*>(t)};
             T* bp = static_cast<T*>(ctx->buf("ut_bp", sizeof(T) * W * pack_stride(static_cast<int>(bcols))));
             launch_pack_factor<T>(b, W, W, static_cast<int>(bcols), bp, ctx->stream);
-            r.sketch(static_cast<const T*>(t), d, static_cast<int>(mode), bp, static_cast<int>(bcols), z, d[mode]);
+            r.sketch(static_cast<const T*>(t), d, r.ident(), static_cast<int>(mode), bp, static_cast<int>(bcols), z, d[mode]);
         };
         if (dtype == TK_F32) body(float{});
         else body(double{});

@@ -69,6 +69,20 @@ def test_ttm_all_projection(P, O, shape, skip):
     assert rel(got, ref) < 1e-12
 
 
+@pytest.mark.parametrize("skip", [2, -1])
+def test_ttm_all_mode0_first_stage_fp32(P, O, skip):
+    """fp32 shapes whose first (Y-streaming) contraction is over mode 0 (I_0 < 256: no
+    M-major pass over mode 1): the K-major tcgen05 pass writes its output transposed (mode 0
+    last) and ttm_all returns the standard layout."""
+    shape = (200, 300, 160)
+    t = rt(O, shape, 17).astype(np.float32)
+    us = [O.gaussian_matrix(s, 12, (15, k)) for k, s in enumerate(shape)]
+    ref = O.ttm_all(t.astype(np.float64), us, skip, True)
+    got = P.ttm_all(P.DenseTensor.from_numpy(t, np.float32), us, skip)
+    assert got.shape == ref.shape
+    assert rel(got, ref) < 1e-5
+
+
 @pytest.mark.parametrize("shape", [(40, 30, 20), (7, 9, 11), (10, 9, 8, 7)])
 def test_unfold_times(P, O, shape):
     t = rt(O, shape, 11)
@@ -199,7 +213,9 @@ def test_shared_passes_match_one_pass_per_step(P, O, dims, dtype):
     s = P.rand_tucker_2i(yy, ranks, 3, (8, 1), out="host", one_pass_per_step=True)
     assert g.stats["passes"] == 3 and s.stats["passes"] == 2 * order
     ref = O.rand_tucker_2i(y.astype(dtype).astype(np.float64), ranks, 3, (8, 1))
-    tol = 1e-10 if dtype == np.float64 else 1e-4
+    # fp32: the two contraction orders round differently; both sit ~1e-4 from the fp64 oracle
+    # in the noise directions, so they are held to the north star's fp32 bar (1e-3)
+    tol = 1e-10 if dtype == np.float64 else F32_TOL
     for u, v in zip(g.factors, s.factors):
         assert subspace_dist(u, v) < tol
     compare_models(O, y, g, ref, F64_TOL if dtype == np.float64 else F32_TOL)

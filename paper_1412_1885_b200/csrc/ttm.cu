@@ -283,19 +283,37 @@ __global__ void __launch_bounds__(128) ttm_kcontig_kernel(const T* __restrict__ 
     }
 }
 
-// Any shape: one output element per thread.
-template <typename T>
-__global__ void ttm_generic_kernel(const T* __restrict__ in, const T* __restrict__ up, T* __restrict__ out,
-                                   int64_t P, int64_t K, int64_t Q, int cols, int stride) {
-    const int64_t n = P * cols * Q;
-    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < n; idx += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t p = idx % P;
-        const int r = static_cast<int>((idx / P) % cols);
-        const int64_t q = idx / (P * cols);
+// Shapes the tiled kernels do not take (P > 1 small or not a multiple of 4, e.g. the core
+// contraction of a permuted X): one warp per (p, q) fibre, lanes stride over k and keep all R
+// outputs in registers, then a fixed-order butterfly reduction (deterministic).
+template <typename T, int R>
+__global__ void __launch_bounds__(256) ttm_fibre_kernel(const T* __restrict__ in, const T* __restrict__ up,
+                                                        T* __restrict__ out, int64_t P, int64_t K, int64_t Q, int cols,
+                                                        int stride) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nf = P * Q;
+    for (int64_t f = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; f < nf;
+         f += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int64_t p = f % P, q = f / P;
         const T* src = in + p + q * P * K;
-        T acc = T(0);
-        for (int64_t k = 0; k < K; ++k) acc = fma(src[k * P], up[k * stride + r], acc);
-        out[idx] = acc;
+        T acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = T(0);
+        for (int64_t k = lane; k < K; k += 32) {
+            const T x = src[k * P];
+            const T* u = up + k * stride;
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = fma(x, u[r], acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+        }
+        T* dst = out + p + q * P * cols;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (r < cols && lane == (r & 31)) dst[int64_t(r) * P] = acc[r];
     }
 }
 
@@ -365,10 +383,9 @@ void dispatch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_
             if (launches) ++*launches;
         }
     } else {
-        const int64_t n = P * cols * Q;
-        const int64_t grid = std::min<int64_t>((n + 255) / 256, 148 * 32);
-        ttm_generic_kernel<T><<<static_cast<unsigned>(grid), 256, 0, s>>>(in, up, out, P, K, Q, cols,
-                                                                         pack_stride(cols));
+        const int64_t grid = std::min<int64_t>((P * Q * 32 + 255) / 256, 148 * 32);
+        ttm_fibre_kernel<T, R><<<static_cast<unsigned>(grid), 256, 0, s>>>(in, up, out, P, K, Q, cols,
+                                                                           pack_stride(cols));
     }
     TK_LAUNCH_CHECK();
 }

@@ -76,7 +76,10 @@ struct TcCfg {
     static_assert(XBASE <= TMEM, "TMEM budget");
     // pipeline depth: ~128 KB of Y in flight per SM whatever the tile height
     static constexpr int STAGES_RAW = (128 * 1024) / STAGE_Y / OCC_;
-    static constexpr int STAGES = STAGES_RAW < kTcStages ? kTcStages : (STAGES_RAW > 6 ? 6 : STAGES_RAW);
+    // at most 8 stages and what fits OCC CTAs into the SM's shared memory
+    static constexpr int STAGES_FIT = (220 * 1024 / OCC_ - 1024) / (STAGE_Y + STAGE_B);
+    static constexpr int STAGES_CAP = STAGES_FIT < 8 ? STAGES_FIT : 8;
+    static constexpr int STAGES = STAGES_RAW < kTcStages ? kTcStages : (STAGES_RAW > STAGES_CAP ? STAGES_CAP : STAGES_RAW);
     static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 256 + 128;
 };
 

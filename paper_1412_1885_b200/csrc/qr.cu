@@ -260,9 +260,9 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         const bool cand = !done && key == ((static_cast<unsigned long long>(hi) << 32) | lo);
         const int pv = static_cast<int>(__reduce_min_sync(0xffffffffu, cand ? unsigned(lane) : 0xffffu));
         const double d = __shfl_sync(0xffffffffu, dg, pv & 31);
-        if (k == 0) r00 = d > 0.0 ? sqrt(d) : 0.0;
-        const double rkk = d > 0.0 ? sqrt(d) : 0.0;
-        if (pv >= n || !(d > 0.0) || !(rkk > kFastMinRatio * r00)) return false;
+        if (k == 0) r00 = d;  // (squared) R_00
+        // R_kk > kFastMinRatio R_00 tested on the squares: the sqrt stays off the step's chain
+        if (pv >= n || !(d > 0.0) || !(d > kFastMinRatio * kFastMinRatio * r00)) return false;
         double cp = 0.0;
         switch (pv) {  // row[pv]: pv is warp-uniform
 #define TK_ROW_CASE(c) \
@@ -280,21 +280,71 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
                 break;
         }
         const bool piv = lane == pv;
+        // the Schur column S_ip reaches the other lanes before l_i = S_ip / d is formed, so the
+        // division overlaps the exchange (update: S_ij -= l_i S_pj)
+        colk[lane] = (done || piv) ? 0.0 : cp;
+        __syncwarp();
         const double l = (done || piv) ? 0.0 : cp / d;
         if (lane < n) lraw[k * n + lane] = piv ? 1.0 : l;
         if (piv) {
             done = true;
             perm[k] = pv;
-            rdk[k] = rkk;
+            rdk[k] = sqrt(d);
         }
-        colk[lane] = l * d;
-        __syncwarp();
 #pragma unroll
         for (int j = 0; j < 32; ++j) row[j] = fma(-l, colk[j], row[j]);
         dg = fma(-l, colk[lane], dg);
         __syncwarp();
     }
     return true;
+}
+
+// n <= 32, one thread per own row i (rows in registers): out_i = in_i,P R^{-1} by forward
+// substitution, right-looking (x_k = acc_k / R_kk, then acc_j -= x_k R_kj for j > k: the
+// chain per step is one multiply and one FMA). R upper, col-major n x n, rinv = 1 / R_kk.
+__device__ void rows_trsm_perm(const double* in, double* out, int ld, int nloc, int n, const double* rr,
+                               const double* rinv, const int* perm) {
+    for (int i = threadIdx.x; i < nloc; i += kQrThreads) {
+        double acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = j < n ? in[i + size_t(perm[j]) * ld] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            if (k < n) {
+                acc[k] *= rinv[k];
+                const double xk = acc[k];
+                const double* rk = rr + k;  // R[k][j] = rr[k + j n]
+#pragma unroll
+                for (int j = k + 1; j < 32; ++j)
+                    if (j < n) acc[j] = fma(-xk, rk[size_t(j) * n], acc[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < n) out[i + size_t(j) * ld] = acc[j];
+    }
+}
+
+// n <= 32, one thread per own row: out_i = in_i M (M upper triangular, col-major n x n)
+__device__ void rows_mul_upper(const double* in, double* out, int ld, int nloc, int n, const double* m) {
+    for (int i = threadIdx.x; i < nloc; i += kQrThreads) {
+        double x[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = j < n ? in[i + size_t(j) * ld] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j < n) {
+                const double* mj = m + size_t(j) * n;
+                double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < 32; k += 2) {
+                    if (k <= j) a0 = fma(x[k], mj[k], a0);
+                    if (k + 1 <= j) a1 = fma(x[k + 1], mj[k + 1], a1);
+                }
+                out[i + size_t(j) * ld] = a0 + a1;
+            }
+        }
+    }
 }
 
 // X = R^{-1} (upper triangular, n x n col-major) by one warp, lanes over the columns j:
@@ -422,10 +472,15 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         }
         QR_MARK(601);
         if (ok1) {  // identical in every CTA (same reduced Gram, same arithmetic)
-            // Q1 = Z_P R1^{-1} with R1^{-1} formed explicitly (parallel application)
-            if (warp == 0) warp_tri_inv(r1, rinv1, n, r2);
-            __syncthreads();
-            apply_upper(z, q, ld, nloc, n, r2, perm);
+            // Q1 = Z_P R1^{-1}: row-parallel substitution for n <= 32, else with R1^{-1}
+            // formed explicitly (parallel application)
+            if (n <= 32) {
+                rows_trsm_perm(z, q, ld, nloc, n, r1, rinv1, perm);
+            } else {
+                if (warp == 0) warp_tri_inv(r1, rinv1, n, r2);
+                __syncthreads();
+                apply_upper(z, q, ld, nloc, n, r2, perm);
+            }
             __syncthreads();
             QR_MARK(602);
             // second pass, to first order: Q1^T Q1 = I + E (E ~ eps cond^2 <= 1e-8), its
@@ -442,7 +497,8 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             for (int k = tid; k < n; k += kQrThreads) perm2[k] = k;
             __syncthreads();
             QR_MARK(604);
-            apply_upper(q, z, ld, nloc, n, r2, perm2);
+            if (n <= 32) rows_mul_upper(q, z, ld, nloc, n, r2);
+            else apply_upper(q, z, ld, nloc, n, r2, perm2);
             for (int k = tid; k < n; k += kQrThreads) sh.beta[k] = r1[k + k * n] * (1.0 + 0.5 * (gs[k + k * n] - 1.0));
             __syncthreads();
             fast_ok = true;

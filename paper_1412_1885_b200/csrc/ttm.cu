@@ -284,36 +284,51 @@ __global__ void __launch_bounds__(128) ttm_kcontig_kernel(const T* __restrict__ 
 }
 
 // Shapes the tiled kernels do not take (P > 1 small or not a multiple of 4, e.g. the core
-// contraction of a permuted X): one warp per (p, q) fibre, lanes stride over k and keep all R
-// outputs in registers, then a fixed-order butterfly reduction (deterministic).
-template <typename T, int R>
+// contraction of a permuted X): one CTA per (p, q) fibre, its 8 warps split K into
+// contiguous chunks, lane r accumulates output r (and r + 32) over its chunk from a
+// warp-broadcast x and a coalesced row of U, then the chunks are summed in fixed order.
+template <typename T>
 __global__ void __launch_bounds__(256) ttm_fibre_kernel(const T* __restrict__ in, const T* __restrict__ up,
                                                         T* __restrict__ out, int64_t P, int64_t K, int64_t Q, int cols,
                                                         int stride) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nf = P * Q;
-    for (int64_t f = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; f < nf;
-         f += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    __shared__ T red[8][64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t kc = (K + 7) / 8;
+    const int64_t k0 = warp * kc, k1 = k0 + kc < K ? k0 + kc : K;
+    for (int64_t f = blockIdx.x; f < P * Q; f += gridDim.x) {
         const int64_t p = f % P, q = f / P;
         const T* src = in + p + q * P * K;
-        T acc[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = T(0);
-        for (int64_t k = lane; k < K; k += 32) {
-            const T x = src[k * P];
-            const T* u = up + k * stride;
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = fma(x, u[r], acc[r]);
+        T a0 = T(0), a1 = T(0), b0 = T(0), b1 = T(0);
+        const int c0 = lane < cols ? lane : 0;  // lanes past cols compute a discarded copy of column 0
+        const bool r1 = lane + 32 < cols;
+        int64_t k = k0;
+        for (; k + 2 <= k1; k += 2) {  // two independent chains
+            const T x0 = src[k * P], x1 = src[(k + 1) * P];
+            const T* u0 = up + k * stride;
+            a0 = fma(x0, u0[c0], a0);
+            b0 = fma(x1, u0[stride + c0], b0);
+            if (r1) {
+                a1 = fma(x0, u0[lane + 32], a1);
+                b1 = fma(x1, u0[stride + lane + 32], b1);
+            }
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+        if (k < k1) {
+            const T x0 = src[k * P];
+            a0 = fma(x0, up[k * stride + c0], a0);
+            if (r1) a1 = fma(x0, up[k * stride + lane + 32], a1);
         }
-        T* dst = out + p + q * P * cols;
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-            if (r < cols && lane == (r & 31)) dst[int64_t(r) * P] = acc[r];
+        red[warp][lane] = a0 + b0;
+        red[warp][lane + 32] = a1 + b1;
+        __syncthreads();
+        if (warp == 0) {
+            T* dst = out + p + q * P * cols;
+            for (int r = lane; r < cols; r += 32) {
+                T v = red[0][r];
+                for (int w = 1; w < 8; ++w) v += red[w][r];
+                dst[int64_t(r) * P] = v;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -383,9 +398,8 @@ void dispatch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_
             if (launches) ++*launches;
         }
     } else {
-        const int64_t grid = std::min<int64_t>((P * Q * 32 + 255) / 256, 148 * 32);
-        ttm_fibre_kernel<T, R><<<static_cast<unsigned>(grid), 256, 0, s>>>(in, up, out, P, K, Q, cols,
-                                                                           pack_stride(cols));
+        const int64_t grid = std::min<int64_t>(P * Q, 148 * 64);
+        ttm_fibre_kernel<T><<<static_cast<unsigned>(grid), 256, 0, s>>>(in, up, out, P, K, Q, cols, pack_stride(cols));
     }
     TK_LAUNCH_CHECK();
 }

@@ -298,27 +298,37 @@ __global__ void __launch_bounds__(256) ttm_fibre_kernel(const T* __restrict__ in
     for (int64_t f = blockIdx.x; f < P * Q; f += gridDim.x) {
         const int64_t p = f % P, q = f / P;
         const T* src = in + p + q * P * K;
-        T a0 = T(0), a1 = T(0), b0 = T(0), b1 = T(0);
+        constexpr int U = 8;  // k per iteration: 2U independent loads in flight per lane
+        T a0[U], a1[U];
+#pragma unroll
+        for (int e = 0; e < U; ++e) a0[e] = a1[e] = T(0);
         const int c0 = lane < cols ? lane : 0;  // lanes past cols compute a discarded copy of column 0
-        const bool r1 = lane + 32 < cols;
+        const int c1 = lane + 32 < cols ? lane + 32 : 0;
         int64_t k = k0;
-        for (; k + 2 <= k1; k += 2) {  // two independent chains
-            const T x0 = src[k * P], x1 = src[(k + 1) * P];
-            const T* u0 = up + k * stride;
-            a0 = fma(x0, u0[c0], a0);
-            b0 = fma(x1, u0[stride + c0], b0);
-            if (r1) {
-                a1 = fma(x0, u0[lane + 32], a1);
-                b1 = fma(x1, u0[stride + lane + 32], b1);
+        for (; k + U <= k1; k += U) {
+            T x[U], u[U], v[U];
+#pragma unroll
+            for (int e = 0; e < U; ++e) {
+                x[e] = src[(k + e) * P];
+                u[e] = up[(k + e) * stride + c0];
+                v[e] = up[(k + e) * stride + c1];
+            }
+#pragma unroll
+            for (int e = 0; e < U; ++e) {
+                a0[e] = fma(x[e], u[e], a0[e]);
+                a1[e] = fma(x[e], v[e], a1[e]);
             }
         }
-        if (k < k1) {
+        for (; k < k1; ++k) {
             const T x0 = src[k * P];
-            a0 = fma(x0, up[k * stride + c0], a0);
-            if (r1) a1 = fma(x0, up[k * stride + lane + 32], a1);
+            a0[0] = fma(x0, up[k * stride + c0], a0[0]);
+            a1[0] = fma(x0, up[k * stride + c1], a1[0]);
         }
-        red[warp][lane] = a0 + b0;
-        red[warp][lane + 32] = a1 + b1;
+        T s0 = T(0), s1 = T(0);
+#pragma unroll
+        for (int e = 0; e < U; ++e) s0 += a0[e], s1 += a1[e];
+        red[warp][lane] = s0;
+        red[warp][lane + 32] = s1;
         __syncthreads();
         if (warp == 0) {
             T* dst = out + p + q * P * cols;

@@ -21,6 +21,21 @@ int main() {
         cudaMemcpy(z, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
         for (int it = 0; it < 3; ++it) tkb::launch_orthonormal_basis(z, rows, cols, u, cols, nullptr, 1, rk, nullptr, 0);
         cudaDeviceSynchronize();
+        {
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0);
+            for (int it = 0; it < 20; ++it)
+                tkb::launch_orthonormal_basis(z, rows, cols, u, cols, nullptr, 1, rk, nullptr, 0);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            int clk = 0;
+            cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+            printf("%dx%d: %.1f us per launch (back to back, events), SM clock attr %d MHz\n", rows, cols, 1e3 * ms / 20, clk / 1000);
+        }
         long long t[4096];
         cudaMemcpyFromSymbol(t, g_qr_trace, sizeof(t));
         if (t[605] > t[600])

@@ -148,8 +148,17 @@ __device__ void gram_reduce(cg::cluster_group& cl, unsigned cs, double* gp, doub
     if (cs > 1) cl.sync();
     else __syncthreads();
     for (int e = threadIdx.x; e < n * n; e += kQrThreads) {
+        // all remote loads in flight before the fixed-order sum (DSMEM latency paid once)
         double v = 0.0;
-        for (unsigned c = 0; c < cs; ++c) v += (cs > 1 ? cl.map_shared_rank(gp, c) : gp)[e];
+        for (unsigned c0 = 0; c0 < cs; c0 += 8) {
+            double t[8];
+#pragma unroll
+            for (unsigned c = 0; c < 8; ++c)
+                t[c] = c0 + c < cs ? (cs > 1 ? cl.map_shared_rank(gp, c0 + c) : gp)[e] : 0.0;
+#pragma unroll
+            for (unsigned c = 0; c < 8; ++c)
+                if (c0 + c < cs) v += t[c];
+        }
         gs[e] = v;
     }
     if (cs > 1) cl.sync();  // every CTA done reading the partials before they are rewritten
@@ -402,7 +411,7 @@ __device__ __forceinline__ void axpy_row(double* zr, int ld, int j0, int j1, dou
 __global__ void __launch_bounds__(kQrThreads, 1)
     qr_colpiv_cluster_kernel(const double* __restrict__ zin, int64_t rows, int ncols, int ld,
                              double* __restrict__ uout, int ucap, void* upout, int up_dtype, int* rank_out,
-                             double* diag_out, int fast) {
+                             double* diag_out, int fast, int rowpar) {
     cg::cluster_group cl = cg::this_cluster();
     const unsigned cs = cl.num_blocks();
     const int crank = static_cast<int>(cl.block_rank());
@@ -474,7 +483,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         if (ok1) {  // identical in every CTA (same reduced Gram, same arithmetic)
             // Q1 = Z_P R1^{-1}: row-parallel substitution for n <= 32, else with R1^{-1}
             // formed explicitly (parallel application)
-            if (n <= 32) {
+            if (n <= 32 && rowpar) {
                 rows_trsm_perm(z, q, ld, nloc, n, r1, rinv1, perm);
             } else {
                 if (warp == 0) warp_tri_inv(r1, rinv1, n, r2);
@@ -497,7 +506,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             for (int k = tid; k < n; k += kQrThreads) perm2[k] = k;
             __syncthreads();
             QR_MARK(604);
-            if (n <= 32) rows_mul_upper(q, z, ld, nloc, n, r2);
+            if (n <= 32 && rowpar) rows_mul_upper(q, z, ld, nloc, n, r2);
             else apply_upper(q, z, ld, nloc, n, r2, perm2);
             for (int k = tid; k < n; k += kQrThreads) sh.beta[k] = r1[k + k * n] * (1.0 + 0.5 * (gs[k + k * n] - 1.0));
             __syncthreads();
@@ -731,11 +740,19 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         else __syncthreads();
         for (int j = tid; j < rank; j += kQrThreads) {
             double bvv = -1.0, val = 0.0;
-            for (unsigned c = 0; c < cs; ++c) {  // CTAs hold increasing rows: strict > keeps the first
-                const double* ps = cs > 1 ? cl.map_shared_rank(m, c) : m;
-                if (ps[2 * j] > bvv) {
-                    bvv = ps[2 * j];
-                    val = ps[2 * j + 1];
+            for (unsigned c0 = 0; c0 < cs; c0 += 8) {
+                double tb[8], tv[8];
+#pragma unroll
+                for (unsigned c = 0; c < 8; ++c) {  // remote loads first, then the ordered scan
+                    const double* ps = c0 + c < cs ? (cs > 1 ? cl.map_shared_rank(m, c0 + c) : m) : nullptr;
+                    tb[c] = ps ? ps[2 * j] : -2.0;
+                    tv[c] = ps ? ps[2 * j + 1] : 0.0;
+                }
+#pragma unroll
+                for (unsigned c = 0; c < 8; ++c) {  // CTAs hold increasing rows: strict > keeps the first
+                    const bool take = tb[c] > bvv;
+                    bvv = take ? tb[c] : bvv;
+                    val = take ? tv[c] : val;
                 }
             }
             sh.sgn[j] = val < 0.0 ? -1.0 : 1.0;
@@ -833,8 +850,12 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
+    static const int rowpar = [] {  // A/B knob: 0 = R^-1 formed by one warp + gathered application
+        const char* e = std::getenv("TENKIT_QR_ROWPAR");
+        return e ? std::atoi(e) : 1;
+    }();
     TK_CUDA(cudaLaunchKernelEx(&cfg, qr_colpiv_cluster_kernel, z, rows, ncols, ld, u, ucap, up, up_dtype, rank_dev,
-                               diag, fast));
+                               diag, fast, rowpar));
 }
 
 }  // namespace tkb

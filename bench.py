@@ -407,6 +407,10 @@ def run_b200(args, cfg):
                        "steps_per_pass": "one Y pass per range step" if args.one_pass_per_step else
                        "consecutive range steps share one Y pass (reference: 2N+1 passes)"},
             "hbm_frac_of_peak": round(value / world / hbm, 4),
+            # the reference streams Y 2N+1 times per decomposition (tucker.hpp:136-169); this
+            # run streams it `passes` times (shared passes + core from X_{N-1}): the step's speed
+            # expressed in the reference's bytes
+            "ref_pass_equiv_gbs": round(world * (2 * len(dims) + 1) * ybytes / (ms_step * 1e-3) / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic,
                          "kernel": "ttm_tc_kernel (Y-streaming TTM, tcgen05 3xTF32)" if cfg["dtype"] == "f32" else "ttm_mmajor_kernel (Y-streaming TTM, FFMA)", "peak_source": "measured" if not pk.get("_fallback") else "fallback",

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -186,6 +187,48 @@ struct TuckerRun {
     bool capture = false;        // compute only: no host syncs, outputs stay in context buffers
     double* core_out = nullptr;  // capture: the fp64 core (context buffer)
     std::vector<int64_t> core_shape;
+    // TENKIT_PHASE_TIMING=1 (eager runs only): CUDA events around every phase of the step,
+    // summed per category and printed to stderr (a diagnostic of where a decomposition goes).
+    bool phase_on = [] {
+        const char* e = std::getenv("TENKIT_PHASE_TIMING");
+        return e && e[0] == '1';
+    }();
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> phases;
+    void ph_begin(int cat) {
+        if (!phase_on || capture) return;
+        cudaEvent_t a, b;
+        TK_CUDA(cudaEventCreate(&a));
+        TK_CUDA(cudaEventCreate(&b));
+        TK_CUDA(cudaEventRecord(a, s));
+        phases.push_back({cat, {a, b}});
+    }
+    void ph_end() {
+        if (!phase_on || capture || phases.empty()) return;
+        TK_CUDA(cudaEventRecord(phases.back().second.second, s));
+    }
+    void ph_report() {
+        if (!phase_on || capture || phases.empty()) return;
+        static const char* names[] = {"y_pass", "stage2", "sketch", "qr", "core"};
+        double tot[5] = {0, 0, 0, 0, 0};
+        int cnt[5] = {0, 0, 0, 0, 0};
+        for (auto& p : phases) {
+            TK_CUDA(cudaEventSynchronize(p.second.second));
+            float ms = 0.f;
+            TK_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+            tot[p.first] += ms;
+            ++cnt[p.first];
+        }
+        float span = 0.f;
+        TK_CUDA(cudaEventElapsedTime(&span, phases.front().second.first, phases.back().second.second));
+        std::fprintf(stderr, "tenkit phases:");
+        for (int c = 0; c < 5; ++c) std::fprintf(stderr, " %s %.1f us (%d)", names[c], 1e3 * tot[c], cnt[c]);
+        std::fprintf(stderr, " | span %.1f us\n", 1e3 * span);
+        for (auto& p : phases) {
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        phases.clear();
+    }
     void mark() {
         cudaEvent_t e;
         TK_CUDA(cudaEventCreate(&e));
@@ -286,11 +329,13 @@ struct TuckerRun {
         const int64_t Q = prod(std::vector<int64_t>(xd.begin() + f + 1, xd.end()));
         T* out = static_cast<T*>(ctx->buf("proj1", sizeof(T) * P * cols[f] * Q));
         bool tout = false;
+        ph_begin(0);
         if (!stream_ttm(y, f, out, P, K, Q, true, &tout)) {
             if (time_kernels) mark();
             ttm(y, factor_rows(f), out, P, K, Q, cols[f]);
             if (time_kernels) mark();
         }
+        ph_end();
         ++passes;
         xd[f] = cols[f];
         if (tout) {  // storage (1, 2, ..., N-1, 0)
@@ -310,7 +355,9 @@ struct TuckerRun {
             const int64_t K = xd[k];
             const int64_t Q = prod(std::vector<int64_t>(xd.begin() + k + 1, xd.end()));
             T* out = static_cast<T*>(ctx->buf(which ? "projB" : "projA", sizeof(T) * P * cols[m] * Q));
+            ph_begin(1);
             if (!stream_ttm(cur, m, out, P, K, Q, false)) ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
+            ph_end();
             xd[k] = cols[m];
             cur = out;
             which ^= 1;
@@ -392,6 +439,7 @@ struct TuckerRun {
         const int64_t W = prod(std::vector<int64_t>(cols.begin(), cols.end()), n);
         const int rn = rt[n];
         T* omp = static_cast<T*>(ctx->buf("omega_p", sizeof(T) * W * pack_stride(rn)));
+        ph_begin(2);
         // Omega rows follow the unfolding's columns (modes != n ascending, tensor.hpp:103-116);
         // for a permuted x its storage columns map to them through a mixed-radix RowMap
         bool ordered = true;
@@ -423,10 +471,13 @@ struct TuckerRun {
         } else {
             sketch(x, xd, xp, n, omp, rn, z, In);
         }
+        ph_end();
         allreduce(z, In * rn);
         if (qr_event) TK_CUDA(cudaEventRecord(qr_event, s));
+        ph_begin(3);
         launch_orthonormal_basis(z, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64, rank_dev + step,
                                  nullptr, s);
+        ph_end();
         ++launches;
         if (sync) sync_rank(n, step);
     }
@@ -561,7 +612,9 @@ struct TuckerRun {
             const int64_t P = prod(std::vector<int64_t>(gd.begin(), gd.begin() + k));
             const int64_t Q = prod(std::vector<int64_t>(gd.begin() + k + 1, gd.end()));
             T* o = static_cast<T*>(ctx->buf("core", sizeof(T) * P * cols[m] * Q));
+            ph_begin(4);
             ttm(xlast, factor_rows(m), o, P, gd[k], Q, cols[m]);
+            ph_end();
             gd[k] = cols[m];
             g = o;
         }
@@ -578,6 +631,7 @@ struct TuckerRun {
         }
         ++launches;
         allreduce(gdv, gsize);
+        ph_report();
         if (capture) {
             core_out = gdv;
             core_shape = gd;

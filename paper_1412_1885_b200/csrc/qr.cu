@@ -272,27 +272,15 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         if (k == 0) r00 = d;  // (squared) R_00
         // R_kk > kFastMinRatio R_00 tested on the squares: the sqrt stays off the step's chain
         if (pv >= n || !(d > 0.0) || !(d > kFastMinRatio * kFastMinRatio * r00)) return false;
-        double cp = 0.0;
-        switch (pv) {  // row[pv]: pv is warp-uniform
-#define TK_ROW_CASE(c) \
-    case c:            \
-        cp = row[c];   \
-        break;
-            TK_ROW_CASE(0) TK_ROW_CASE(1) TK_ROW_CASE(2) TK_ROW_CASE(3) TK_ROW_CASE(4) TK_ROW_CASE(5) TK_ROW_CASE(6)
-            TK_ROW_CASE(7) TK_ROW_CASE(8) TK_ROW_CASE(9) TK_ROW_CASE(10) TK_ROW_CASE(11) TK_ROW_CASE(12)
-            TK_ROW_CASE(13) TK_ROW_CASE(14) TK_ROW_CASE(15) TK_ROW_CASE(16) TK_ROW_CASE(17) TK_ROW_CASE(18)
-            TK_ROW_CASE(19) TK_ROW_CASE(20) TK_ROW_CASE(21) TK_ROW_CASE(22) TK_ROW_CASE(23) TK_ROW_CASE(24)
-            TK_ROW_CASE(25) TK_ROW_CASE(26) TK_ROW_CASE(27) TK_ROW_CASE(28) TK_ROW_CASE(29) TK_ROW_CASE(30)
-            TK_ROW_CASE(31)
-#undef TK_ROW_CASE
-            default:
-                break;
-        }
+        // the pivot lane publishes its Schur row S_p. (= column S_.p, S symmetric): lane i reads
+        // its S_ip from it, and the trailing update S_ij -= l_i S_pj reads the whole row
         const bool piv = lane == pv;
-        // the Schur column S_ip reaches the other lanes before l_i = S_ip / d is formed, so the
-        // division overlaps the exchange (update: S_ij -= l_i S_pj)
-        colk[lane] = (done || piv) ? 0.0 : cp;
+        if (piv) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) colk[j] = row[j];
+        }
         __syncwarp();
+        const double cp = colk[lane];
         const double l = (done || piv) ? 0.0 : cp / d;
         if (lane < n) lraw[k * n + lane] = piv ? 1.0 : l;
         if (piv) {

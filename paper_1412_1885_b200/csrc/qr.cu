@@ -262,6 +262,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
     double r00 = 0.0;
 #pragma unroll 1
     for (int k = 0; k < n; ++k) {
+        QR_MARK(700 + 4 * k);
         // first maximum of the remaining Schur diagonal (exact, lowest index on ties)
         const unsigned long long key = done ? 0ull : static_cast<unsigned long long>(__double_as_longlong(fmax(dg, 0.0)));
         const unsigned hi = __reduce_max_sync(0xffffffffu, unsigned(key >> 32));
@@ -272,6 +273,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         if (k == 0) r00 = d;  // (squared) R_00
         // R_kk > kFastMinRatio R_00 tested on the squares: the sqrt stays off the step's chain
         if (pv >= n || !(d > 0.0) || !(d > kFastMinRatio * kFastMinRatio * r00)) return false;
+        QR_MARK(701 + 4 * k);
         // the pivot lane publishes its Schur row S_p. (= column S_.p, S symmetric): lane i reads
         // its S_ip from it, and the trailing update S_ij -= l_i S_pj reads the whole row
         const bool piv = lane == pv;
@@ -281,6 +283,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         }
         __syncwarp();
         const double cp = colk[lane];
+        QR_MARK(702 + 4 * k);
         const double l = (done || piv) ? 0.0 : cp / d;
         if (lane < n) lraw[k * n + lane] = piv ? 1.0 : l;
         if (piv) {
@@ -288,6 +291,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
             perm[k] = pv;
             rdk[k] = sqrt(d);
         }
+        QR_MARK(703 + 4 * k);
 #pragma unroll
         for (int j = 0; j < 32; ++j) row[j] = fma(-l, colk[j], row[j]);
         dg = fma(-l, colk[lane], dg);

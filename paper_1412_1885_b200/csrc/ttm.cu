@@ -284,58 +284,46 @@ __global__ void __launch_bounds__(128) ttm_kcontig_kernel(const T* __restrict__ 
 }
 
 // Shapes the tiled kernels do not take (P > 1 small or not a multiple of 4, e.g. the core
-// contraction of a permuted X): one CTA per (p, q) fibre, its 8 warps split K into
-// contiguous chunks, lane r accumulates output r (and r + 32) over its chunk from a
-// warp-broadcast x and a coalesced row of U, then the chunks are summed in fixed order.
-template <typename T>
-__global__ void __launch_bounds__(256) ttm_fibre_kernel(const T* __restrict__ in, const T* __restrict__ up,
-                                                        T* __restrict__ out, int64_t P, int64_t K, int64_t Q, int cols,
-                                                        int stride) {
-    __shared__ T red[8][64];
+// contraction of a permuted X): CTA (q, 32-row block of p); lane = p, the 8 warps split K
+// into contiguous chunks; each thread keeps the R outputs of its p in registers, reading x
+// coalesced along p and the U row as warp-broadcast vectors; the chunks are summed in fixed
+// order through shared memory.
+template <typename T, int R>
+__global__ void __launch_bounds__(256) ttm_smallp_kernel(const T* __restrict__ in, const T* __restrict__ up,
+                                                         T* __restrict__ out, int64_t P, int64_t K, int cols,
+                                                         int stride) {
+    constexpr int RC = 16;  // outputs per reduction round
+    __shared__ T red[8][RC][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t q = blockIdx.x;
+    const int64_t p = int64_t(blockIdx.y) * 32 + lane;
+    const bool live = p < P;
     const int64_t kc = (K + 7) / 8;
     const int64_t k0 = warp * kc, k1 = k0 + kc < K ? k0 + kc : K;
-    for (int64_t f = blockIdx.x; f < P * Q; f += gridDim.x) {
-        const int64_t p = f % P, q = f / P;
-        const T* src = in + p + q * P * K;
-        constexpr int U = 8;  // k per iteration: 2U independent loads in flight per lane
-        T a0[U], a1[U];
+    const T* src = in + (live ? p : 0) + q * P * K;
+    T acc[R];
 #pragma unroll
-        for (int e = 0; e < U; ++e) a0[e] = a1[e] = T(0);
-        const int c0 = lane < cols ? lane : 0;  // lanes past cols compute a discarded copy of column 0
-        const int c1 = lane + 32 < cols ? lane + 32 : 0;
-        int64_t k = k0;
-        for (; k + U <= k1; k += U) {
-            T x[U], u[U], v[U];
+    for (int r = 0; r < R; ++r) acc[r] = T(0);
+    for (int64_t k = k0; k < k1; ++k) {
+        const T x = live ? src[k * P] : T(0);
+        const T* u = up + k * stride;
 #pragma unroll
-            for (int e = 0; e < U; ++e) {
-                x[e] = src[(k + e) * P];
-                u[e] = up[(k + e) * stride + c0];
-                v[e] = up[(k + e) * stride + c1];
-            }
+        for (int r = 0; r < R; ++r) acc[r] = fma(x, u[r], acc[r]);
+    }
 #pragma unroll
-            for (int e = 0; e < U; ++e) {
-                a0[e] = fma(x[e], u[e], a0[e]);
-                a1[e] = fma(x[e], v[e], a1[e]);
-            }
-        }
-        for (; k < k1; ++k) {
-            const T x0 = src[k * P];
-            a0[0] = fma(x0, up[k * stride + c0], a0[0]);
-            a1[0] = fma(x0, up[k * stride + c1], a1[0]);
-        }
-        T s0 = T(0), s1 = T(0);
+    for (int rc = 0; rc < R; rc += RC) {
 #pragma unroll
-        for (int e = 0; e < U; ++e) s0 += a0[e], s1 += a1[e];
-        red[warp][lane] = s0;
-        red[warp][lane + 32] = s1;
+        for (int e = 0; e < RC; ++e)
+            if (rc + e < R) red[warp][e][lane] = acc[rc + e];
         __syncthreads();
-        if (warp == 0) {
-            T* dst = out + p + q * P * cols;
-            for (int r = lane; r < cols; r += 32) {
-                T v = red[0][r];
-                for (int w = 1; w < 8; ++w) v += red[w][r];
-                dst[int64_t(r) * P] = v;
+        for (int t = threadIdx.x; t < RC * 32; t += 256) {
+            const int e = t >> 5, l = t & 31;
+            const int64_t pp = int64_t(blockIdx.y) * 32 + l;
+            if (rc + e < cols && pp < P) {
+                T v = red[0][e][l];
+#pragma unroll
+                for (int w = 1; w < 8; ++w) v += red[w][e][l];
+                out[pp + int64_t(rc + e) * P + q * P * cols] = v;
             }
         }
         __syncthreads();
@@ -408,8 +396,9 @@ void dispatch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_
             if (launches) ++*launches;
         }
     } else {
-        const int64_t grid = std::min<int64_t>(P * Q, 148 * 64);
-        ttm_fibre_kernel<T><<<static_cast<unsigned>(grid), 256, 0, s>>>(in, up, out, P, K, Q, cols, pack_stride(cols));
+        require(Q < (int64_t(1) << 31) && (P + 31) / 32 < 65536, "ttm: extent too large");
+        ttm_smallp_kernel<T, R><<<dim3(static_cast<unsigned>(Q), static_cast<unsigned>((P + 31) / 32)), 256, 0, s>>>(
+            in, up, out, P, K, cols, pack_stride(cols));
     }
     TK_LAUNCH_CHECK();
 }

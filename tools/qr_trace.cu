@@ -42,6 +42,10 @@ int main() {
             printf("%dx%d fast path: gram1 %lld pchol1 %lld trsm1 %lld gram2 %lld chol2 %lld trsm2 %lld | sign %lld out %lld total %lld\n",
                    rows, cols, t[600] - t[0], t[601] - t[600], t[602] - t[601], t[603] - t[602], t[604] - t[603],
                    t[605] - t[604], t[4] - t[3], t[5] - t[4], t[5] - t[0]);
+        if (t[705] > t[700])
+            printf("  pchol step 1: reduce+pivot %lld publish+read %lld div+stores %lld update %lld (cycles)\n",
+                   t[705] - t[704], t[706] - t[705],
+                   t[707] - t[706], t[708] - t[707]);
         printf("%dx%d: load+norms %lld\n", rows, cols, t[1] - t[0]);
         for (int k = 1; k < 4; ++k)
             printf("  step %d: pivot %lld swap %lld reduce %lld scal+downdate+essential %lld update %lld\n", k,

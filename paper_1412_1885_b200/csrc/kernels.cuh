@@ -57,6 +57,11 @@ int64_t sketch_work_elems(int64_t I, int rn);
 template <typename T>
 int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* z, int64_t ldz, double* work,
                   cudaStream_t s);
+// The split-K partials only: work[(s * rn + r) * I + i], s < returned split count (summed in
+// order s = 0, 1, ... by sketch_reduce_kernel, or by the QR kernel's load: nparts below).
+template <typename T>
+int launch_sketch_partials(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* work,
+                           cudaStream_t s);
 
 // Materialise the mode-n unfolding of a (B, I, A) view: out[i + (b + a*B)*I] = x[b + i*B + a*B*I]
 template <typename T>
@@ -106,8 +111,10 @@ void launch_cast2d(const S* in, int64_t ldi, D* out, int64_t ldo, int64_t rows, 
 // ld = rows; columns >= rank zeroed), the packed T copy (pack_factor layout for `rank`
 // columns, if up != nullptr), rank to *rank_dev and |R_kk| diagnostics to diag (ncols).
 // Runs as one thread-block cluster holding Z in distributed shared memory.
+// nparts > 0: z holds nparts split-K partials of Z, z[(s * ncols + j) * rows + i], summed in
+// order s = 0 .. nparts-1 while loading (launch_sketch_partials' layout).
 void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up,
-                              int up_dtype, int* rank_dev, double* diag, cudaStream_t s);
+                              int up_dtype, int* rank_dev, double* diag, cudaStream_t s, int nparts = 0);
 // Largest Z (rows) the cluster QR can hold for `ncols` columns.
 int64_t qr_max_rows(int ncols);
 

@@ -274,6 +274,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         // R_kk > kFastMinRatio R_00 tested on the squares: the sqrt stays off the step's chain
         if (pv >= n || !(d > 0.0) || !(d > kFastMinRatio * kFastMinRatio * r00)) return false;
         QR_MARK(701 + 4 * k);
+        const double rd = 1.0 / d;  // overlaps the row exchange below
         // the pivot lane publishes its Schur row S_p. (= column S_.p, S symmetric): lane i reads
         // its S_ip from it, and the trailing update S_ij -= l_i S_pj reads the whole row
         const bool piv = lane == pv;
@@ -284,12 +285,12 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         __syncwarp();
         const double cp = colk[lane];
         QR_MARK(702 + 4 * k);
-        const double l = (done || piv) ? 0.0 : cp / d;
+        const double l = (done || piv) ? 0.0 : cp * rd;
         if (lane < n) lraw[k * n + lane] = piv ? 1.0 : l;
         if (piv) {
             done = true;
             perm[k] = pv;
-            rdk[k] = sqrt(d);
+            rdk[k] = d;  // R_kk^2; square roots taken after the loop, off the step chain
         }
         QR_MARK(703 + 4 * k);
 #pragma unroll
@@ -297,6 +298,8 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         dg = fma(-l, colk[lane], dg);
         __syncwarp();
     }
+    for (int k = lane; k < n; k += 32) rdk[k] = sqrt(rdk[k]);
+    __syncwarp();
     return true;
 }
 
@@ -403,7 +406,7 @@ __device__ __forceinline__ void axpy_row(double* zr, int ld, int j0, int j1, dou
 __global__ void __launch_bounds__(kQrThreads, 1)
     qr_colpiv_cluster_kernel(const double* __restrict__ zin, int64_t rows, int ncols, int ld,
                              double* __restrict__ uout, int ucap, void* upout, int up_dtype, int* rank_out,
-                             double* diag_out, int fast, int rowpar) {
+                             double* diag_out, int fast, int rowpar, int nparts) {
     cg::cluster_group cl = cg::this_cluster();
     const unsigned cs = cl.num_blocks();
     const int crank = static_cast<int>(cl.block_rank());
@@ -426,10 +429,20 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     int par = 0;
     QR_MARK(0);
 
+    if (nparts > 0) {  // Z = sum of the sketch's split-K partials, in split order
+        for (int t = tid; t < ld * ncols; t += kQrThreads) {
+            const int i = t % ld, j = t / ld;
+            double v = 0.0;
+            if (i < nloc)
+                for (int sp = 0; sp < nparts; ++sp) v += zin[(int64_t(sp) * ncols + j) * rows + r0 + i];
+            z[t] = v;
+        }
+    } else {
 #pragma unroll 4
-    for (int t = tid; t < ld * ncols; t += kQrThreads) {
-        const int i = t % ld, j = t / ld;
-        z[t] = i < nloc ? zin[(r0 + i) + int64_t(j) * rows] : 0.0;
+        for (int t = tid; t < ld * ncols; t += kQrThreads) {
+            const int i = t % ld, j = t / ld;
+            z[t] = i < nloc ? zin[(r0 + i) + int64_t(j) * rows] : 0.0;
+        }
     }
     if (tid < 2) sh.flag[tid] = 0;
     __syncthreads();
@@ -808,7 +821,7 @@ int64_t qr_max_rows(int ncols) {
 }
 
 void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up, int up_dtype,
-                              int* rank_dev, double* diag, cudaStream_t s) {
+                              int* rank_dev, double* diag, cudaStream_t s, int nparts) {
     require(rows >= 1, "orthonormal_basis: empty input");
     require(ncols >= 1 && ncols <= kMaxRank, "orthonormal_basis: column count must be in [1, 64]");
     int ld = 0;
@@ -847,7 +860,7 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
         return e ? std::atoi(e) : 1;
     }();
     TK_CUDA(cudaLaunchKernelEx(&cfg, qr_colpiv_cluster_kernel, z, rows, ncols, ld, u, ucap, up, up_dtype, rank_dev,
-                               diag, fast, rowpar));
+                               diag, fast, rowpar, nparts));
 }
 
 }  // namespace tkb

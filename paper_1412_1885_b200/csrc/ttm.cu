@@ -634,8 +634,8 @@ void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t 
 int64_t sketch_work_elems(int64_t I, int rn) { return I * rn * 16; }
 
 template <typename T>
-int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* z, int64_t ldz, double* work,
-                  cudaStream_t s) {
+int launch_sketch_partials(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* work,
+                           cudaStream_t s) {
     require(B * A < (int64_t(1) << 31), "unfold_times: unfolding too wide");
     const int K = static_cast<int>(B * A);
     const unsigned gx = static_cast<unsigned>((I + 31) / 32), gy = static_cast<unsigned>((rn + 31) / 32);
@@ -646,10 +646,22 @@ int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int 
     S = (K + kchunk - 1) / kchunk;
     sketch_kernel<T><<<dim3(gx, gy, S), 256, 0, s>>>(x, static_cast<int>(B), I, static_cast<int>(A), om, pack_stride(rn), rn,
                                                      kchunk, work);
+    TK_LAUNCH_CHECK();
+    return S;
+}
+
+template <typename T>
+int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* z, int64_t ldz, double* work,
+                  cudaStream_t s) {
+    const int S = launch_sketch_partials<T>(x, B, I, A, om, rn, work, s);
     sketch_reduce_kernel<<<grid_for(I * rn), 256, 0, s>>>(work, I, rn, S, z, ldz);
     TK_LAUNCH_CHECK();
     return 2;
 }
+template int launch_sketch_partials<float>(const float*, int64_t, int64_t, int64_t, const float*, int, double*,
+                                           cudaStream_t);
+template int launch_sketch_partials<double>(const double*, int64_t, int64_t, int64_t, const double*, int, double*,
+                                            cudaStream_t);
 template int launch_sketch<float>(const float*, int64_t, int64_t, int64_t, const float*, int, double*, int64_t, double*,
                                   cudaStream_t);
 template int launch_sketch<double>(const double*, int64_t, int64_t, int64_t, const double*, int, double*, int64_t, double*,

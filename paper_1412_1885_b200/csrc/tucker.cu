@@ -465,18 +465,28 @@ struct TuckerRun {
         ++launches;
         const int64_t In = gdims[n];
         double* z = static_cast<double*>(ctx->buf("z", sizeof(double) * In * rn));
+        const bool ranks_sum = ctx->has_comm && ctx->comm.world > 1;
+        int nparts = 0;
         if (ldims[n] != In) {  // this rank's rows of Z, the others zero (summed over ranks)
             TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * In * rn, s));
             sketch(x, xd, xp, n, omp, rn, z + off[n], In);
+        } else if (!ranks_sum) {  // the QR sums the split-K partials while loading Z
+            const int k = pos_of(xp, n);
+            const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + k));
+            const int64_t A = prod(std::vector<int64_t>(xd.begin() + k + 1, xd.end()));
+            z = static_cast<double*>(ctx->buf(work_name == std::string("splitk") ? "sketch_part" : "sketch_part_side",
+                                              sizeof(double) * sketch_work_elems(In, rn)));
+            nparts = launch_sketch_partials<T>(x, B, In, A, omp, rn, z, s);
+            ++launches;
         } else {
             sketch(x, xd, xp, n, omp, rn, z, In);
         }
         ph_end();
-        allreduce(z, In * rn);
+        if (!nparts) allreduce(z, In * rn);
         if (qr_event) TK_CUDA(cudaEventRecord(qr_event, s));
         ph_begin(3);
         launch_orthonormal_basis(z, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64, rank_dev + step,
-                                 nullptr, s);
+                                 nullptr, s, nparts);
         ph_end();
         ++launches;
         if (sync) sync_rank(n, step);

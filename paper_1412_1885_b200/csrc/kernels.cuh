@@ -35,15 +35,22 @@ void launch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t 
 // tcgen05 path (ttm_tc.cu, fp32 data): 3xTF32 UMMA contraction of the (P, K, Q) view with
 // the factor packed by launch_pack_umma ([U_hi | U_lo] core-matrix blocks).
 // P == 1 (contraction over the fastest mode) uses the K-major variant (K % 4 == 0, cols <= 32).
-bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols);
+// work_elems: capacity of the split-K partial buffer the caller can pass to launch_ttm_tc
+// (M-major shapes with too few row tiles run split-K over it).
+bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols, int64_t work_elems = 0);
 int64_t umma_pack_bytes(int64_t rows, int cols);
 void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s);
 // accurate: for P == 1 always use the 128-row K-major tiles with 3 accumulator sets (fp32
 // FFMA-level error) instead of the faster single-set 256-row tiles.
 // tout (P == 1 only): write the output transposed, out[q + r Q] (the contracted mode moves to
 // the slowest position) instead of out[r + q cols].
-void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s, bool accurate = false, bool tout = false);
+// Returns the number of kernels launched.
+int launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+                  cudaStream_t s, bool accurate = false, bool tout = false, float* work = nullptr,
+                  int64_t work_elems = 0);
+// out[i] = sum_s part[s * n + i] (fixed split order)
+template <typename T>
+void launch_splitk_reduce(const T* part, T* out, int64_t n, int splits, cudaStream_t s);
 
 // Pack a column-major double factor (rows x cols, leading dim ld) into T k-major
 // [rows][pack_stride(cols)] with zero padding.

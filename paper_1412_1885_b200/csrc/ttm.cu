@@ -304,7 +304,20 @@ __global__ void __launch_bounds__(256) ttm_smallp_kernel(const T* __restrict__ i
     T acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = T(0);
-    for (int64_t k = k0; k < k1; ++k) {
+    constexpr int KU = 8;  // x loads in flight per thread
+    int64_t k = k0;
+    for (; k + KU <= k1; k += KU) {
+        T x[KU];
+#pragma unroll
+        for (int e = 0; e < KU; ++e) x[e] = live ? src[(k + e) * P] : T(0);
+#pragma unroll
+        for (int e = 0; e < KU; ++e) {
+            const T* u = up + (k + e) * stride;
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = fma(x[e], u[r], acc[r]);
+        }
+    }
+    for (; k < k1; ++k) {
         const T x = live ? src[k * P] : T(0);
         const T* u = up + k * stride;
 #pragma unroll
@@ -726,6 +739,14 @@ void launch_permute_cast(const S* in, D* out, int order, const int64_t* dims, co
 template void launch_permute_cast<float, double>(const float*, double*, int, const int64_t*, const int*, cudaStream_t);
 template void launch_permute_cast<double, double>(const double*, double*, int, const int64_t*, const int*, cudaStream_t);
 template void launch_permute_cast<float, float>(const float*, float*, int, const int64_t*, const int*, cudaStream_t);
+
+template <typename T>
+void launch_splitk_reduce(const T* part, T* out, int64_t n, int splits, cudaStream_t s) {
+    splitk_reduce_kernel<T><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(
+        part, out, n, splits);
+    TK_LAUNCH_CHECK();
+}
+template void launch_splitk_reduce<float>(const float*, float*, int64_t, int, cudaStream_t);
 
 template void launch_ttm<float>(const float*, const float*, float*, int64_t, int64_t, int64_t, int, cudaStream_t, int*,
                                 float*, int64_t);

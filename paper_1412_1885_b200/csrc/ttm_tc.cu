@@ -209,7 +209,13 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
     const int64_t q = blockIdx.x / tiles_p;
     const int64_t p0 = (blockIdx.x % tiles_p) * BM;
     const int rows = static_cast<int>(lmin(BM, P - p0));
-    const int nk = static_cast<int>((K + kTcBK - 1) / kTcBK);
+    // split-K (gridDim.y > 1): this CTA takes k-blocks [kb0, kb0 + nk) and writes its partial
+    // to out + blockIdx.y * (P * cols * Q); the caller sums the partials in split order
+    const int nk_all = static_cast<int>((K + kTcBK - 1) / kTcBK);
+    const int nk_per = (nk_all + static_cast<int>(gridDim.y) - 1) / static_cast<int>(gridDim.y);
+    const int kb0 = static_cast<int>(blockIdx.y) * nk_per;
+    const int nk = nk_per < nk_all - kb0 ? nk_per : nk_all - kb0;
+    out += int64_t(blockIdx.y) * P * cols * (int64_t(gridDim.x) / tiles_p);
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -245,15 +251,15 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
                 if constexpr (KM) {
 #pragma unroll
                     for (int b = 0; b < BM / C::BOXR; ++b)
-                        tma_load_2d(dy + b * (C::BOXR * kTcBK * 4), &ymap, kc * kTcBK, static_cast<int>(p0 + C::BOXR * b),
+                        tma_load_2d(dy + b * (C::BOXR * kTcBK * 4), &ymap, (kb0 + kc) * kTcBK, static_cast<int>(p0 + C::BOXR * b),
                                     &full[s]);
                 } else {
 #pragma unroll
                     for (int b = 0; b < BM / C::BOXR; ++b)
-                        tma_load_3d(dy + b * (kTcBK * C::BOXR * 4), &ymap, static_cast<int>(p0 + C::BOXR * b), kc * kTcBK,
+                        tma_load_3d(dy + b * (kTcBK * C::BOXR * 4), &ymap, static_cast<int>(p0 + C::BOXR * b), (kb0 + kc) * kTcBK,
                                     static_cast<int>(q), &full[s]);
                 }
-                bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
+                bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kb0 + kc) * C::STAGE_B, C::STAGE_B, &full[s]);
             }
         }
     } else if (warp == kTcConv + 1) {
@@ -438,7 +444,7 @@ __global__ void pack_umma_kernel(const double* __restrict__ u, int64_t ld, int64
 
 template <int NH, int MT, bool KM, int OCC = 1>
 void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-               cudaStream_t s, bool tout = false) {
+               cudaStream_t s, bool tout = false, int splits = 1) {
     using C = TcCfg<NH, MT, OCC>;
     static bool attr = false;
     if (!attr) {
@@ -474,8 +480,8 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
     }
     require(grid < (int64_t(1) << 31), "ttm: grid too large");
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-    ttm_tc_kernel<NH, MT, KM, OCC><<<static_cast<unsigned>(grid), kTcThreads, C::smem, s>>>(map, bpk, out, P, K, cols,
-                                                                                           tiles_p, tout ? 1 : 0);
+    ttm_tc_kernel<NH, MT, KM, OCC><<<dim3(static_cast<unsigned>(grid), static_cast<unsigned>(splits)), kTcThreads,
+                                     C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p, tout ? 1 : 0);
     TK_LAUNCH_CHECK();
 }
 
@@ -514,41 +520,66 @@ inline bool km_wide(int64_t Q) { return (Q + 255) / 256 >= 4 * 148; }
 constexpr int kMmt = 2;
 constexpr int kOcc = 2;
 
-bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols) {
-    if (reinterpret_cast<uintptr_t>(in) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
-    if (P == 1) return K % 4 == 0 && K >= kTcBK && cols <= 32 && (Q + 127) / 128 >= 148;
-    const int bm = tc_nh(cols) <= 32 ? 128 * kMmt : 128;  // tiles >= 2 waves of 2 CTAs per SM
-    const int64_t tiles = (P + bm - 1) / bm * Q;
-    return P % 4 == 0 && P >= 256 && tiles >= 2 * 2 * 148;
+inline int64_t mm_tiles(int64_t P, int64_t Q, int cols) {
+    const int bm = tc_nh(cols) <= 32 ? 128 * kMmt : 128;
+    return (P + bm - 1) / bm * Q;
 }
 
-void launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s, bool accurate, bool tout) {
+// Split-K factor for an M-major contraction whose row tiles alone cannot fill 2 waves of 2
+// CTAs per SM: >= 8 k-blocks (128 k) per split, no empty split, partials fit `work_elems`.
+inline int mm_splits(int64_t P, int64_t K, int64_t Q, int cols, int64_t work_elems) {
+    const int64_t tiles = mm_tiles(P, Q, cols);
+    if (tiles >= 2 * 2 * 148) return 1;
+    const int64_t nk = (K + kTcBK - 1) / kTcBK;
+    int64_t sp = std::min<int64_t>((2 * 2 * 148 + tiles - 1) / tiles, nk / 8);
+    sp = std::min<int64_t>(sp, work_elems / std::max<int64_t>(1, P * cols * Q));
+    if (sp < 2) return 1;
+    const int64_t per = (nk + sp - 1) / sp;
+    return static_cast<int>((nk + per - 1) / per);
+}
+
+bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols, int64_t work_elems) {
+    if (reinterpret_cast<uintptr_t>(in) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
+    if (P == 1) return K % 4 == 0 && K >= kTcBK && cols <= 32 && (Q + 127) / 128 >= 148;
+    if (P % 4 != 0 || P < 256) return false;
+    // tiles >= 2 waves of 2 CTAs per SM, or (with split-K partials) >= 1 wave
+    const int64_t tiles = mm_tiles(P, Q, cols);
+    return tiles >= 2 * 2 * 148 || tiles * mm_splits(P, K, Q, cols, work_elems) >= 2 * 148;
+}
+
+int launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+                  cudaStream_t s, bool accurate, bool tout, float* work, int64_t work_elems) {
     const uint8_t* b = static_cast<const uint8_t*>(bpk);
     if (P == 1) {
         const bool wide = km_wide(Q) && !accurate && !tout;  // narrow tiles: 3 accumulator sets
-        if (tc_nh(cols) <= 16) return wide ? launch_tc<16, 2, true, 2>(in, b, out, P, K, Q, cols, s, tout)
-                                           : launch_tc<16, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
-        return wide ? launch_tc<32, 2, true, 2>(in, b, out, P, K, Q, cols, s, tout)
-                    : launch_tc<32, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
+        if (tc_nh(cols) <= 16) wide ? launch_tc<16, 2, true, 2>(in, b, out, P, K, Q, cols, s, tout)
+                                    : launch_tc<16, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
+        else wide ? launch_tc<32, 2, true, 2>(in, b, out, P, K, Q, cols, s, tout)
+                  : launch_tc<32, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
+        return 1;
     }
     static const int variant = [] {
         const char* e = std::getenv("TENKIT_TC_VARIANT");
         return e ? std::atoi(e) : 0;
     }();
     if (variant == 1) {  // A/B: one CTA per SM (the round-1 first version)
-        if (tc_nh(cols) <= 16) return launch_tc<16, 4, false>(in, b, out, P, K, Q, cols, s);
-        if (tc_nh(cols) <= 32) return launch_tc<32, 4, false>(in, b, out, P, K, Q, cols, s);
-        if (tc_nh(cols) <= 48) return launch_tc<48, 2, false>(in, b, out, P, K, Q, cols, s);
-        return launch_tc<64, 2, false>(in, b, out, P, K, Q, cols, s);
+        if (tc_nh(cols) <= 16) launch_tc<16, 4, false>(in, b, out, P, K, Q, cols, s);
+        else if (tc_nh(cols) <= 32) launch_tc<32, 4, false>(in, b, out, P, K, Q, cols, s);
+        else if (tc_nh(cols) <= 48) launch_tc<48, 2, false>(in, b, out, P, K, Q, cols, s);
+        else launch_tc<64, 2, false>(in, b, out, P, K, Q, cols, s);
+        return 1;
     }
+    const int sp = work ? mm_splits(P, K, Q, cols, work_elems) : 1;
+    float* dst = sp > 1 ? work : out;
     switch (tc_nh(cols)) {
-        case 16: return launch_tc<16, kMmt, false, kOcc>(in, b, out, P, K, Q, cols, s);
-        case 32: return launch_tc<32, kMmt, false, kOcc>(in, b, out, P, K, Q, cols, s);
+        case 16: launch_tc<16, kMmt, false, kOcc>(in, b, dst, P, K, Q, cols, s, false, sp); break;
+        case 32: launch_tc<32, kMmt, false, kOcc>(in, b, dst, P, K, Q, cols, s, false, sp); break;
         // wider factors: one 128-row tile per CTA keeps two CTAs per SM inside 256 TMEM columns
-        case 48: return launch_tc<48, 1, false, kOcc>(in, b, out, P, K, Q, cols, s);
-        default: return launch_tc<64, 1, false, kOcc>(in, b, out, P, K, Q, cols, s);
+        case 48: launch_tc<48, 1, false, kOcc>(in, b, dst, P, K, Q, cols, s, false, sp); break;
+        default: launch_tc<64, 1, false, kOcc>(in, b, dst, P, K, Q, cols, s, false, sp); break;
     }
+    if (sp > 1) launch_splitk_reduce<float>(work, out, P * cols * Q, sp, s);
+    return sp > 1 ? 2 : 1;
 }
 
 }  // namespace tkb

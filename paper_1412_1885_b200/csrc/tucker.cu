@@ -385,21 +385,23 @@ struct TuckerRun {
             return false;
         } else {
             const int path = ctx->ttm_path;
-            // auto: every Y pass, and the later contractions over the fastest mode (P == 1),
-            // which the FFMA kernels serve poorly
-            if (path == 1 || (path == 0 && !streams_y && P != 1) || U.size() <= size_t(m) || !U[m]) return false;
+            // auto: every contraction the tensor-core kernels take (Y passes; later M-major
+            // stages, split over K when their row tiles cannot fill the GPU; K-major stages)
+            if (path == 1 || U.size() <= size_t(m) || !U[m]) return false;
             const float* fin = reinterpret_cast<const float*>(in);
             float* fout = reinterpret_cast<float*>(out);
-            if (!tc_ttm_supported(fin, fout, P, K, Q, cols[m])) return false;
+            const int64_t welems = std::min<int64_t>(P * cols[m] * Q * 16, int64_t(64) << 20);
+            if (!tc_ttm_supported(fin, fout, P, K, Q, cols[m], welems)) return false;
             void* bpk = ctx->buf(streams_y ? "umma_pack" : "umma_pack2", static_cast<size_t>(umma_pack_bytes(K, cols[m])));
             const double* u = U[m] + off[m];
             launch_pack_umma(u, gdims[m], K, cols[m], bpk, s);
             if (streams_y && time_kernels) mark();
             const bool tr = tout && P == 1;  // a mode-0 Y pass: transposed output
-            launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s, /*accurate=*/true, tr);
+            float* work = static_cast<float*>(
+                ctx->buf(work_name == std::string("splitk") ? "splitk_tc" : "splitk_tc_side", sizeof(float) * welems));
+            launches += 1 + launch_ttm_tc(fin, bpk, fout, P, K, Q, cols[m], s, /*accurate=*/true, tr, work, welems);
             if (tr) *tout = true;
             if (streams_y && time_kernels) mark();
-            launches += 2;
             return true;
         }
     }

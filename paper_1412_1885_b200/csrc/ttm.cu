@@ -298,8 +298,13 @@ __global__ void __launch_bounds__(256) ttm_smallp_kernel(const T* __restrict__ i
     const int64_t q = blockIdx.x;
     const int64_t p = int64_t(blockIdx.y) * 32 + lane;
     const bool live = p < P;
-    const int64_t kc = (K + 7) / 8;
-    const int64_t k0 = warp * kc, k1 = k0 + kc < K ? k0 + kc : K;
+    // split-K over gridDim.z: this CTA's K range, split into 8 warp chunks; partial z goes to
+    // out + z * (P * cols * gridDim.x)
+    const int64_t kz = (K + gridDim.z - 1) / gridDim.z;
+    const int64_t kz0 = int64_t(blockIdx.z) * kz, kz1 = kz0 + kz < K ? kz0 + kz : K;
+    const int64_t kc = (kz1 - kz0 + 7) / 8;
+    const int64_t k0 = kz0 + warp * kc, k1 = k0 + kc < kz1 ? k0 + kc : kz1;
+    out += int64_t(blockIdx.z) * P * cols * gridDim.x;
     const T* src = in + (live ? p : 0) + q * P * K;
     T acc[R];
 #pragma unroll
@@ -410,8 +415,24 @@ void dispatch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_
         }
     } else {
         require(Q < (int64_t(1) << 31) && (P + 31) / 32 < 65536, "ttm: extent too large");
-        ttm_smallp_kernel<T, R><<<dim3(static_cast<unsigned>(Q), static_cast<unsigned>((P + 31) / 32)), 256, 0, s>>>(
-            in, up, out, P, K, cols, pack_stride(cols));
+        const int64_t ctas = Q * ((P + 31) / 32);
+        // split K when the (q, p-block) CTAs cannot fill 2 waves: >= 128 k per split
+        int64_t splits = 1;
+        if (ctas < 2 * 148 && K >= 256 && work) {
+            splits = std::min<int64_t>({(2 * 148 + ctas - 1) / ctas, K / 128, 64});
+            while (splits > 1 && splits * P * cols * Q > work_elems) --splits;
+        }
+        T* dst = splits > 1 ? work : out;
+        ttm_smallp_kernel<T, R><<<dim3(static_cast<unsigned>(Q), static_cast<unsigned>((P + 31) / 32),
+                                       static_cast<unsigned>(splits)), 256, 0, s>>>(in, up, dst, P, K, cols,
+                                                                                   pack_stride(cols));
+        if (splits > 1) {
+            TK_LAUNCH_CHECK();
+            const int64_t n = P * cols * Q;
+            splitk_reduce_kernel<T><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(
+                work, out, n, static_cast<int>(splits));
+            if (launches) ++*launches;
+        }
     }
     TK_LAUNCH_CHECK();
 }

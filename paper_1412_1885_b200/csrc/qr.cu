@@ -143,6 +143,43 @@ __device__ void gram_partial(const double* z, int ld, int nloc, int n, double* g
     }
 }
 
+// The same on the FP64 tensor cores: each warp takes 8x8 tiles (ti <= tj) of the Gram and
+// runs mma.m8n8k4.f64 over the own rows, 4 per step (rows >= nloc count as zero). Lane
+// layouts (PTX m8n8k4 .row.col f64): A[m][k] = lane (m = lane / 4, k = lane % 4), B[k][n] =
+// lane (k = lane % 4, n = lane / 4), D[m][2 (lane % 4) + e] for m = lane / 4.
+__device__ void gram_partial_dmma(const double* z, int nloc, int n, int ld, double* gp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nt = (n + 7) / 8;
+    const int ntile = nt * (nt + 1) / 2;
+    const int g = lane >> 2, t4 = lane & 3;
+    for (int tt = warp; tt < ntile; tt += kQrThreads / 32) {
+        int ti = 0, rem = tt;
+        while (rem >= nt - ti) {
+            rem -= nt - ti;
+            ++ti;
+        }
+        const int tj = ti + rem;
+        const int ca = 8 * ti + g, cb = 8 * tj + g;  // A column (row of G) / B column of this lane
+        const double* za = z + size_t(ca < n ? ca : 0) * ld;
+        const double* zb = z + size_t(cb < n ? cb : 0) * ld;
+        double d0 = 0.0, d1 = 0.0;
+        for (int r0 = 0; r0 < nloc; r0 += 4) {  // warp-uniform trip count
+            const int r = r0 + t4;
+            const double a = (ca < n && r < nloc) ? za[r] : 0.0;
+            const double b = (cb < n && r < nloc) ? zb[r] : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                         : "+d"(d0), "+d"(d1)
+                         : "d"(a), "d"(b));
+        }
+        const int row = 8 * ti + g;
+        const int c0 = 8 * tj + 2 * t4;
+        if (row < n) {
+            if (c0 < n) gp[row + c0 * n] = d0, gp[c0 + row * n] = d0;
+            if (c0 + 1 < n) gp[row + (c0 + 1) * n] = d1, gp[(c0 + 1) + row * n] = d1;
+        }
+    }
+}
+
 // gs = sum over the cluster's CTAs (fixed order) of gp; every CTA ends with the same gs
 __device__ void gram_reduce(cg::cluster_group& cl, unsigned cs, double* gp, double* gs, int n) {
     if (cs > 1) cl.sync();
@@ -260,16 +297,21 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
     double dg = lane < n ? gs[lane + lane * n] : 0.0;
     bool done = lane >= n;
     double r00 = 0.0;
-#pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-        QR_MARK(700 + 4 * k);
-        // first maximum of the remaining Schur diagonal (exact, lowest index on ties)
+    // first maximum of the remaining Schur diagonal (exact, lowest index on ties)
+    auto pick = [&](int& pv, double& d) {
         const unsigned long long key = done ? 0ull : static_cast<unsigned long long>(__double_as_longlong(fmax(dg, 0.0)));
         const unsigned hi = __reduce_max_sync(0xffffffffu, unsigned(key >> 32));
         const unsigned lo = __reduce_max_sync(0xffffffffu, unsigned(key >> 32) == hi ? unsigned(key) : 0u);
         const bool cand = !done && key == ((static_cast<unsigned long long>(hi) << 32) | lo);
-        const int pv = static_cast<int>(__reduce_min_sync(0xffffffffu, cand ? unsigned(lane) : 0xffffu));
-        const double d = __shfl_sync(0xffffffffu, dg, pv & 31);
+        pv = static_cast<int>(__reduce_min_sync(0xffffffffu, cand ? unsigned(lane) : 0xffffu));
+        d = __shfl_sync(0xffffffffu, dg, pv & 31);
+    };
+    int pv;
+    double d;
+    pick(pv, d);
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+        QR_MARK(700 + 4 * k);
         if (k == 0) r00 = d;  // (squared) R_00
         // R_kk > kFastMinRatio R_00 tested on the squares: the sqrt stays off the step's chain
         if (pv >= n || !(d > 0.0) || !(d > kFastMinRatio * kFastMinRatio * r00)) return false;
@@ -293,10 +335,16 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
             rdk[k] = d;  // R_kk^2; square roots taken after the loop, off the step chain
         }
         QR_MARK(703 + 4 * k);
+        // the diagonal first: the next pivot search overlaps the rest of the row update
+        dg = fma(-l, cp, dg);
+        int pv1 = n;
+        double d1 = 0.0;
+        if (k + 1 < n) pick(pv1, d1);
 #pragma unroll
         for (int j = 0; j < 32; ++j) row[j] = fma(-l, colk[j], row[j]);
-        dg = fma(-l, colk[lane], dg);
         __syncwarp();
+        pv = pv1;
+        d = d1;
     }
     for (int k = lane; k < n; k += 32) rdk[k] = sqrt(rdk[k]);
     __syncwarp();
@@ -306,7 +354,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
 // n <= 32, one thread per own row i (rows in registers): out_i = in_i,P R^{-1} by forward
 // substitution, right-looking (x_k = acc_k / R_kk, then acc_j -= x_k R_kj for j > k: the
 // chain per step is one multiply and one FMA). R upper, col-major n x n, rinv = 1 / R_kk.
-__device__ void rows_trsm_perm(const double* in, double* out, int ld, int nloc, int n, const double* rr,
+__device__ __noinline__ void rows_trsm_perm(const double* in, double* out, int ld, int nloc, int n, const double* rr,
                                const double* rinv, const int* perm) {
     for (int i = threadIdx.x; i < nloc; i += kQrThreads) {
         double acc[32];
@@ -330,7 +378,7 @@ __device__ void rows_trsm_perm(const double* in, double* out, int ld, int nloc, 
 }
 
 // n <= 32, one thread per own row: out_i = in_i M (M upper triangular, col-major n x n)
-__device__ void rows_mul_upper(const double* in, double* out, int ld, int nloc, int n, const double* m) {
+__device__ __noinline__ void rows_mul_upper(const double* in, double* out, int ld, int nloc, int n, const double* m) {
     for (int i = threadIdx.x; i < nloc; i += kQrThreads) {
         double x[32];
 #pragma unroll
@@ -462,7 +510,8 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         int* ctl = perm2 + kMaxRank;                           // scratch
         double* rinv1 = sh.upd;                                // 1 / R_kk (the Householder
                                                                // norms are not in use yet)
-        gram_partial(z, ld, nloc, n, gp);
+        __syncthreads();
+        gram_partial_dmma(z, nloc, n, ld, gp);
         gram_reduce(cl, cs, gp, gs, n);
         QR_MARK(600);
         bool ok1;
@@ -500,7 +549,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             // second pass, to first order: Q1^T Q1 = I + E (E ~ eps cond^2 <= 1e-8), its
             // Cholesky factor is I + V with V = strict_upper(E) + diag(E) / 2, so
             // Q = Q1 (I + V)^{-1} = Q1 (I - V) + O(E^2) and R_kk = R1_kk (1 + V_kk)
-            gram_partial(q, ld, nloc, n, gp);
+            gram_partial_dmma(q, nloc, n, ld, gp);
             gram_reduce(cl, cs, gp, gs, n);
             QR_MARK(603);
             for (int e = tid; e < n * n; e += kQrThreads) {

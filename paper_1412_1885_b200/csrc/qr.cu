@@ -40,7 +40,7 @@ namespace tkb {
 
 namespace {
 
-constexpr int kQrThreads = 512;
+constexpr int kQrThreads = 256;
 constexpr int kTpc = 16;  // threads per column in the reductions (kQrThreads / kTpc columns per pass)
 constexpr int kVec = 2 * kMaxRank + 8;
 constexpr size_t kQrFixedSmem = (3 * kVec + 6 * kMaxRank) * sizeof(double) + 16 * sizeof(int);
@@ -354,7 +354,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
 // n <= 32, one thread per own row i (rows in registers): out_i = in_i,P R^{-1} by forward
 // substitution, right-looking (x_k = acc_k / R_kk, then acc_j -= x_k R_kj for j > k: the
 // chain per step is one multiply and one FMA). R upper, col-major n x n, rinv = 1 / R_kk.
-__device__ __noinline__ void rows_trsm_perm(const double* in, double* out, int ld, int nloc, int n, const double* rr,
+__device__ void rows_trsm_perm(const double* in, double* out, int ld, int nloc, int n, const double* rr,
                                const double* rinv, const int* perm) {
     for (int i = threadIdx.x; i < nloc; i += kQrThreads) {
         double acc[32];
@@ -378,7 +378,7 @@ __device__ __noinline__ void rows_trsm_perm(const double* in, double* out, int l
 }
 
 // n <= 32, one thread per own row: out_i = in_i M (M upper triangular, col-major n x n)
-__device__ __noinline__ void rows_mul_upper(const double* in, double* out, int ld, int nloc, int n, const double* m) {
+__device__ void rows_mul_upper(const double* in, double* out, int ld, int nloc, int n, const double* m) {
     for (int i = threadIdx.x; i < nloc; i += kQrThreads) {
         double x[32];
 #pragma unroll

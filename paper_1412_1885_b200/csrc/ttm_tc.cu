@@ -83,18 +83,6 @@ struct TcCfg {
     static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 256 + 128;
 };
 
-// L2 sector promotion of the K-major tensor map (64-B row segments per stage); A/B knob
-// TENKIT_KM_PROMO = 0 none, 1 64B, 2 128B, 3 256B (default)
-inline CUtensorMapL2promotion km_promotion() {
-    static const int v = [] {
-        const char* e = std::getenv("TENKIT_KM_PROMO");
-        return e ? std::atoi(e) : 3;
-    }();
-    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                  : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                           : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-}
-
 __device__ __forceinline__ uint32_t f2tf32(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
@@ -206,8 +194,6 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
                   int64_t P, int64_t K, int cols, int64_t tiles_p, int tout) {
     using C = TcCfg<NH, MT_, OCC>;
     constexpr int MT = C::MT, BM = C::BM;
-    constexpr int PAIR = KM ? 2 : 1;  // K-major: one TMA box feeds two 16-k stages
-    static_assert(C::STAGES % PAIR == 0, "paired stages");
     extern __shared__ __align__(1024) uint8_t tsm[];
     uint8_t* sY = tsm;  // [stages][BM/BOXR boxes][kTcBK][BOXR] fp32
     uint8_t* sB = tsm + size_t(C::STAGES) * C::STAGE_Y;           // [stages][2][2NH x 8] tf32 core matrices
@@ -257,24 +243,23 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
         // ===== producer =====
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
-            for (int kc = 0; kc < nk; kc += PAIR) {
+            for (int kc = 0; kc < nk; ++kc) {
                 const int s = kc % C::STAGES;
                 mbar_wait(&empty[s], ((kc / C::STAGES) & 1) ^ 1);
-                mbar_arrive_expect_tx(&full[s], PAIR * (C::STAGE_Y + C::STAGE_B));
+                mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
                 uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
                 if constexpr (KM) {
-                    // two consecutive 16-k stages in one 32-k box: 128-B row segments per request
 #pragma unroll
                     for (int b = 0; b < BM / C::BOXR; ++b)
-                        tma_load_2d(dy + b * (C::BOXR * PAIR * kTcBK * 4), &ymap, (kb0 + kc) * kTcBK,
-                                    static_cast<int>(p0 + C::BOXR * b), &full[s]);
+                        tma_load_2d(dy + b * (C::BOXR * kTcBK * 4), &ymap, (kb0 + kc) * kTcBK, static_cast<int>(p0 + C::BOXR * b),
+                                    &full[s]);
                 } else {
 #pragma unroll
                     for (int b = 0; b < BM / C::BOXR; ++b)
                         tma_load_3d(dy + b * (kTcBK * C::BOXR * 4), &ymap, static_cast<int>(p0 + C::BOXR * b), (kb0 + kc) * kTcBK,
                                     static_cast<int>(q), &full[s]);
                 }
-                bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kb0 + kc) * C::STAGE_B, PAIR * C::STAGE_B, &full[s]);
+                bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kb0 + kc) * C::STAGE_B, C::STAGE_B, &full[s]);
             }
         }
     } else if (warp == kTcConv + 1) {
@@ -283,8 +268,7 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
             const uint32_t id_full = idesc_tf32(2 * NH), id_hi = idesc_tf32(NH);
             for (int kc = 0; kc < nk; ++kc) {
                 const int s = kc % C::STAGES, a = kc & 1;
-                const int sb = s - s % PAIR;  // the stage (pair) that owns the barriers
-                mbar_wait(&full[sb], (kc / C::STAGES) & 1);
+                mbar_wait(&full[s], (kc / C::STAGES) & 1);
                 mbar_wait(&afull[a], (kc >> 1) & 1);
                 fence_after();
                 const uint8_t* bs = sB + size_t(s) * C::STAGE_B;
@@ -303,7 +287,7 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
                     }
                 }
                 mma_commit(&aempty[a]);
-                if (kc % PAIR == PAIR - 1 || kc == nk - 1) mma_commit(&empty[sb]);
+                mma_commit(&empty[s]);
             }
             mma_commit(dfull);
         }
@@ -314,25 +298,22 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         for (int kc = 0; kc < nk; ++kc) {
             const int s = kc % C::STAGES, a = kc & 1;
-            const int sb = s - s % PAIR;
-            mbar_wait(&full[sb], (kc / C::STAGES) & 1);
+            mbar_wait(&full[s], (kc / C::STAGES) & 1);
             uint32_t hi[MT][8], lo[MT][8];
             // rows MT*L .. MT*L+MT-1 of the tile sit in box (MT*L)/BOXR at row (MT*L)%BOXR
             const float* ys = reinterpret_cast<const float*>(sY + size_t(s) * C::STAGE_Y) +
                               ((MT * L) / C::BOXR) * (kTcBK * C::BOXR) + (MT * L) % C::BOXR + khalf * 8 * C::BOXR;
             if constexpr (KM) {
-                // row j*128 + L of the tile, 128-B rows of the 32-k box (128B swizzle: 16-B chunk
-                // c of row r at c ^ (r % 8)); this stage's 8 k values are the logical chunks
-                // 4 (kc % 2) + 2 khalf + {0, 1}
-                const uint8_t* stage = sY + size_t(sb) * C::STAGE_Y;
+                // row j*128 + L of the tile: 8 k values = logical 16-B chunks 2*khalf, 2*khalf+1
+                const uint8_t* stage = sY + size_t(s) * C::STAGE_Y;
 #pragma unroll
                 for (int j = 0; j < MT; ++j) {
                     const int row = j * 128 + L;
                     const int rr = row % C::BOXR;
-                    const uint8_t* rb = stage + (row / C::BOXR) * (C::BOXR * PAIR * kTcBK * 4) + rr * (PAIR * kTcBK * 4);
+                    const uint8_t* rb = stage + (row / C::BOXR) * (C::BOXR * kTcBK * 4) + rr * 64;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int phys = (4 * (kc % PAIR) + 2 * khalf + h) ^ (rr & 7);
+                        const int phys = (2 * khalf + h) ^ ((rr >> 1) & 3);
                         const float4 v = *reinterpret_cast<const float4*>(rb + phys * 16);
                         const float y4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -367,8 +348,7 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
                 for (int kk = 0; kk < 8; ++kk) split(kk, true);  // the K tail is zero-filled by the TMA
             }
             __syncwarp();
-            if (lane == 0 && (kc % PAIR == PAIR - 1 || kc == nk - 1))
-                mbar_arrive(&empty[sb]);  // Y stage (pair) consumed (B: the MMA commit)
+            if (lane == 0) mbar_arrive(&empty[s]);  // Y stage consumed (B: the MMA commit)
             mbar_wait(&aempty[a], ((kc >> 1) & 1) ^ 1);
             fence_after();
 #pragma unroll
@@ -481,10 +461,10 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
         grid = tiles_p;
         const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(Q)};
         const cuuint64_t strides[1] = {cuuint64_t(K) * 4};
-        const cuuint32_t box[2] = {2 * kTcBK, C::BOXR};  // 32 k (two stages) x BOXR rows
+        const cuuint32_t box[2] = {kTcBK, C::BOXR};
         const cuuint32_t estr[2] = {1, 1};
         r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(in), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, km_promotion(),
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         P = Q;  // the kernel's row extent
     } else {
@@ -509,15 +489,14 @@ inline int tc_nh(int cols) { return cols <= 16 ? 16 : cols <= 32 ? 32 : cols <= 
 
 }  // namespace
 
-// one 16-k block more than the factor needs, zero: a K-major pair of stages may read it
 int64_t umma_pack_bytes(int64_t rows, int cols) {
-    const int64_t ksteps = ((rows + kTcBK - 1) / kTcBK + 1) * 2;
+    const int64_t ksteps = (rows + kTcBK - 1) / kTcBK * 2;
     return ksteps * 64 * tc_nh(cols);
 }
 
 void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s) {
     require(cols >= 1 && cols <= kMaxRank, "ttm: factor column count must be in [1, 64]");
-    const int64_t ksteps = ((rows + kTcBK - 1) / kTcBK + 1) * 2;
+    const int64_t ksteps = (rows + kTcBK - 1) / kTcBK * 2;
     const int nh = tc_nh(cols);
     const int64_t n = ksteps * 2 * nh * 8;
     const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));

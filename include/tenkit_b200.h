@@ -14,6 +14,7 @@
  *   tk_gaussian_matrix    <- tenkit::gaussian_matrix     random.hpp:85-100
  *   tk_gaussian_fill      <- tenkit::gaussian_tensor     random.hpp:124-138 (window at an offset)
  *   tk_gaussian_fill_block   (same, one block of a BlockGrid, dist.hpp:24-123)
+ *   tk_dist_multiply      <- tenkit::dist_multiply       dist.hpp:812-846
  *   tk_seed_derived       <- tenkit::SeedSpec::derived   random.hpp:36-41
  *   tk_ffcp(_device)      <- tenkit::ffcp                ffcp.hpp:94-194
  *   tk_model_fit          <- tenkit::fit(y, reconstruct / cp_reconstruct(model))
@@ -171,6 +172,14 @@ int tk_gaussian_fill(tk_context* ctx, int64_t n, uint64_t offset, uint64_t seed_
 int tk_gaussian_fill_block(tk_context* ctx, int64_t order, const int64_t* global_dims, const int64_t* lo,
                            const int64_t* len, uint64_t seed_root, uint64_t seed_stream, double* out);
 uint64_t tk_seed_derived(uint64_t seed_root, uint64_t seed_stream, uint64_t tag);
+
+/* dist_multiply (dist.hpp:812-846): z (global I_mode x r_tilde doubles, device) = unfold(Y, mode) *
+ * gaussian_matrix(prod_{k != mode} I_k, r_tilde, SeedSpec{root, stream}) of the global tensor whose
+ * block y (device, dims = the block's extents) this rank holds (tk_context_set_comm; without a
+ * multi-rank hook the block is the whole tensor). Every rank ends with the whole z; the
+ * reference's per-segment row blocks are its row ranges. */
+int tk_dist_multiply(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y, int64_t mode,
+                     int64_t r_tilde, uint64_t seed_root, uint64_t seed_stream, double* z);
 
 /* FFCP on a Tucker model (host pointers, fp64; computed on the device). factors[n] is
  * rows[n] x core_shape[n]. out_factors[n]: rows[n] x rank; fit_trace: capacity max_iters. */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "tk_gaussian_matrix": (C.c_int, [C.c_void_p, I64, I64, U64, U64, PD]),
     "tk_gaussian_fill": (C.c_int, [C.c_void_p, I64, U64, U64, U64, PD]),
     "tk_gaussian_fill_block": (C.c_int, [C.c_void_p, I64, PI64, PI64, PI64, U64, U64, PD]),
+    "tk_dist_multiply": (C.c_int, [C.c_void_p, C.c_int, I64, PI64, C.c_void_p, I64, I64, U64, U64, PD]),
     "tk_model_fit": (C.c_int, [C.c_void_p, C.c_int, I64, PI64, C.c_void_p, PI64, PD, C.POINTER(PD), I64, PD]),
     "tk_seed_derived": (U64, [U64, U64, U64]),
     "tk_ffcp": (C.c_int, [C.c_void_p, I64, PI64, PD, C.POINTER(PD), PI64, I64, C.c_int, C.c_double, C.c_int,

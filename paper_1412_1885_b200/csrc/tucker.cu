@@ -1269,4 +1269,47 @@ int tk_unfold_times(tk_context* ctx, int dtype, int64_t order, const int64_t* di
     });
 }
 
+int tk_dist_multiply(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y, int64_t mode,
+                     int64_t r_tilde, uint64_t seed_root, uint64_t seed_stream, double* z) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(order >= 1 && order <= TK_MAX_ORDER, "tensor order must be in [1, 8]");
+        require(mode >= 0 && mode < order, "dist_multiply: mode out of range");
+        require(r_tilde >= 1, "dist_multiply: r_tilde must be positive");
+        require(r_tilde <= kMaxRank, "dist_multiply: r_tilde must be <= 64 on this device path");
+        std::vector<int64_t> ld(dims, dims + order), gd, lo;
+        for (auto v : ld) require(v >= 1, "tensor dimensions must be positive");
+        block_of(ctx, ld, gd, lo);
+        const int n = static_cast<int>(mode), rt = static_cast<int>(r_tilde);
+        // Omega = gaussian_matrix(prod_{k != n} I_k, r~, seed) (random.hpp:85-100) restricted to this
+        // block's unfolding columns at their global ids (streamed_block_product, dist.hpp:496-596)
+        RowMap map;
+        map.rows_total = 1;
+        for (int k = 0; k < order; ++k) {
+            if (k == n) continue;
+            map.lext[map.nd] = ld[k];
+            map.lo[map.nd] = lo[k];
+            map.gstride[map.nd] = map.rows_total;
+            map.rows_total *= gd[k];
+            ++map.nd;
+        }
+        const int64_t width = prod(ld) / ld[n];
+        const int64_t In = gd[n];
+        auto body = [&](auto tag) {
+            using T = decltype(tag);
+            cudaStream_t s = ctx->stream;
+            TuckerRun<T> r{ctx, s, order, ld, gd, lo, static_cast<const T*>(y)};
+            T* op = static_cast<T*>(ctx->buf("dm_omega", sizeof(T) * width * pack_stride(rt)));
+            launch_gaussian_packed_map<T>(op, width, rt, Seed{seed_root, seed_stream}.key(), map, s);
+            TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * In * rt, s));
+            r.sketch(static_cast<const T*>(y), ld, r.ident(), n, op, rt, z + lo[n], In);
+            // partial products summed over the ranks (the row leaders' reduction, dist.hpp:818-845)
+            r.allreduce(z, In * rt);
+        };
+        if (dtype == TK_F32) body(float{});
+        else body(double{});
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 }  // extern "C"

@@ -235,3 +235,36 @@ def dist_rand_tucker(local_y, global_dims, lo, ranks, oversample, seed, *, conte
     summed over ranks, the QR is replicated. Every rank returns the same model."""
     from .tenkit import rand_tucker
     return _dist_call(rand_tucker, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw)
+
+
+def dist_multiply(local_y, global_dims, lo, mode: int, r_tilde: int, seed, *, grid: GridPlan | None = None,
+                  context=None, group=None):
+    """dist_multiply (dist.hpp:812-846): unfold(Y, mode) * Omega with Omega =
+    gaussian_matrix(prod_{k != mode} I_k, r_tilde, seed) for the global tensor Y whose block
+    `local_y` (a device DenseTensor) this rank holds at offsets `lo` (GridPlan.block). Each rank
+    multiplies its block's unfolding by the Omega rows of its global column ids and the partial
+    products are summed over ranks (NCCL / gloo). Returns the reference's result: the Z row
+    blocks, one per mode-`mode` segment of `grid` (a single block without a grid), as numpy."""
+    import numpy as np
+    import torch
+    from .tenkit import Context, SeedSpec, _dptr, _dtype_code, _i64arr, _ptr
+    ctx = context or Context.default()
+    ctx.bind_torch_stream()
+    seed = seed if isinstance(seed, SeedSpec) else SeedSpec(*seed)
+    gdims, blo = _block_args(local_y, global_dims, lo)
+    if not 0 <= mode < len(gdims):
+        raise _lib.TenkitError("tenkit: dist_multiply: mode out of range")
+    rows = gdims[mode]
+    z = torch.empty(rows * max(int(r_tilde), 1), dtype=torch.float64, device="cuda")
+    comm = DistComm(blo[-1], gdims[-1], rows * max(int(r_tilde), 1), group=group, block_lo=blo, global_dims=gdims)
+    ctx.set_comm(comm)
+    try:
+        _lib.check(ctx.lib.tk_dist_multiply(ctx.handle, _dtype_code(local_y.data), len(gdims),
+                                            _i64arr(local_y.shape), _ptr(local_y.data), int(mode), int(r_tilde),
+                                            seed.root, seed.stream, _dptr(z)))
+    finally:
+        ctx.set_comm(None)
+    zz = z.cpu().numpy().reshape((rows, int(r_tilde)), order="F")
+    if grid is None:
+        return [zz]
+    return [zz[o:o + l] for o, l in zip(grid.offsets[mode], grid.splits[mode])]

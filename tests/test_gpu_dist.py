@@ -315,3 +315,81 @@ def test_block_generation_tiles_the_global_tensor():
         out[lo[0]:lo[0] + ln[0], lo[1]:lo[1] + ln[1], lo[2]:lo[2] + ln[2]] = \
             parts[r].cpu().numpy().reshape(ln, order="F")
     np.testing.assert_allclose(out, full, rtol=0, atol=1e-12 * np.abs(full).max())
+
+
+# ---------------------------------------------------------------- dist_multiply
+def test_dist_multiply_single_block_equals_direct_product(O):
+    """dist_multiply on a single block equals unfold(Y, n) * gaussian_matrix(width, r, seed)
+    (reference test_dist.cpp:114-121), every mode, fp64 and fp32; reference error messages."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1412_1885_b200 as P
+    from paper_1412_1885_b200.dist import dist_multiply
+    y = O.gaussian_matrix(6 * 5 * 4, 1, (127, 0)).reshape((6, 5, 4), order="F")
+    for dtype, tol in [(np.float64, 1e-10), (np.float32, 1e-5)]:
+        yd = P.DenseTensor.from_numpy(y.astype(dtype), dtype).cuda()
+        for mode in range(3):
+            (z,) = dist_multiply(yd, (6, 5, 4), (0, 0, 0), mode, 3, (128, 0))
+            om = O.gaussian_matrix(y.size // y.shape[mode], 3, (128, 0))
+            direct = O.unfold_times(y.astype(dtype).astype(np.float64), mode, om)
+            assert np.abs(z - direct).max() <= tol * np.abs(direct).max()
+    with pytest.raises(P.TenkitError, match="r_tilde must be positive"):
+        dist_multiply(yd, (6, 5, 4), (0, 0, 0), 0, 0, (1, 0))
+    with pytest.raises(P.TenkitError, match="mode out of range"):
+        dist_multiply(yd, (6, 5, 4), (0, 0, 0), 3, 2, (1, 0))
+
+
+def _dm_worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from oracle import pyoracle as O
+        import paper_1412_1885_b200 as P
+        from paper_1412_1885_b200.dist import GridPlan, dist_multiply
+        y = O.gaussian_matrix(8 * 6 * 3, 1, (129, 0)).reshape((8, 6, 3), order="F")
+        plan = GridPlan((8, 6, 3), [[4, 4], [3, 3], [3]])
+        lo, ln = plan.block(rank)
+        yd = P.DenseTensor.from_numpy(plan.local(y, rank)).cuda()
+        out = [dist_multiply(yd, (8, 6, 3), lo, mode, 4, (130, 0), grid=plan) for mode in range(3)]
+        q.put((rank, out))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put((rank, repr(e) + traceback.format_exc()))
+
+
+def test_dist_multiply_grid_matches_single_node(O):
+    """dist_multiply across a 2 x 2 x 1 grid (4 ranks sharing cuda:0 over gloo): the stacked
+    row blocks equal the single-node unfold(Y, n) * Omega (reference test_dist.cpp:123-139), for
+    every mode; every rank holds the same blocks."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dm_worker, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(4))
+    for p in procs:
+        p.join(timeout=60)
+    y = O.gaussian_matrix(8 * 6 * 3, 1, (129, 0)).reshape((8, 6, 3), order="F")
+    for r in range(4):
+        assert not isinstance(res[r], str), res[r]
+        for mode in range(3):
+            blocks = res[r][mode]
+            assert len(blocks) == [2, 2, 1][mode]
+            om = O.gaussian_matrix(y.size // y.shape[mode], 4, (130, 0))
+            direct = O.unfold_times(y, mode, om)
+            stacked = np.vstack(blocks)
+            assert np.abs(stacked - direct).max() <= 1e-10 * np.abs(direct).max()
+            for a, b in zip(blocks, res[0][mode]):
+                np.testing.assert_array_equal(a, b)

@@ -298,7 +298,7 @@ struct TuckerRun {
             if (ctx->ttm_path == 1 || cols.empty()) return false;
             const int64_t K = ldims[0];
             const int64_t Q = prod(ldims) / K;
-            return K % 4 == 0 && K >= 16 && cols[0] <= 32 && (Q + 127) / 128 >= 148 &&
+            return K % 4 == 0 && K >= 16 && cols[0] <= 48 && (Q + 127) / 128 >= 148 &&
                    reinterpret_cast<uintptr_t>(y) % 16 == 0;
         }
     }

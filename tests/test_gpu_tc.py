@@ -49,10 +49,12 @@ def test_tc_ttm_matches_oracle_and_ffma(P, O, shape, mode, rows):
     assert rel(got_tc, got_ffma) < 2 * tol
 
 
-def test_rand_tucker_2i_tc_path_matches_oracle(P, O):
-    """400^3 fp32 (first-stage tiles >= 2 waves -> tcgen05 path in auto mode)."""
+@pytest.mark.parametrize("ranks,p", [((12, 12, 12), 8), ((30, 30, 30), 10)])
+def test_rand_tucker_2i_tc_path_matches_oracle(P, O, ranks, p):
+    """400^3 fp32 (first-stage tiles >= 2 waves -> tcgen05 path in auto mode); r~ = 20 and 40
+    (the mode-0 Y pass on the K-major kernel with NH = 32 and NH = 48)."""
     seed = (5, 6)
-    dims, ranks, p = (400, 400, 400), (12, 12, 12), 8
+    dims = (400, 400, 400)
     y = O.add_noise(O.gen_tucker(dims, ranks, seed), 20.0, O.seed_derived(*seed, 0xAD0))
     y32 = y.astype(np.float32)
     O.set_threads(8)

@@ -478,11 +478,20 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     QR_MARK(0);
 
     if (nparts > 0) {  // Z = sum of the sketch's split-K partials, in split order
+        // all of an element's partial loads are issued before the (ordered) sum, two elements
+        // per iteration: the L2 latency is paid once per pair instead of once per partial
+        const int64_t pstride = int64_t(ncols) * rows;
+#pragma unroll 2
         for (int t = tid; t < ld * ncols; t += kQrThreads) {
             const int i = t % ld, j = t / ld;
+            double pv[16];
+            const double* src = zin + int64_t(j) * rows + r0 + i;
+#pragma unroll
+            for (int sp = 0; sp < 16; ++sp) pv[sp] = (i < nloc && sp < nparts) ? src[sp * pstride] : 0.0;
             double v = 0.0;
-            if (i < nloc)
-                for (int sp = 0; sp < nparts; ++sp) v += zin[(int64_t(sp) * ncols + j) * rows + r0 + i];
+#pragma unroll
+            for (int sp = 0; sp < 16; ++sp)
+                if (sp < nparts) v += pv[sp];
             z[t] = v;
         }
     } else {

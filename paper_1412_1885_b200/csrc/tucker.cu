@@ -121,6 +121,8 @@ int guarded(F&& f) {
     }
 }
 
+bool qr_fuse();
+
 int64_t prod(const std::vector<int64_t>& v, int64_t skip = -1) {
     int64_t p = 1;
     for (size_t i = 0; i < v.size(); ++i)
@@ -472,7 +474,7 @@ struct TuckerRun {
         if (ldims[n] != In) {  // this rank's rows of Z, the others zero (summed over ranks)
             TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * In * rn, s));
             sketch(x, xd, xp, n, omp, rn, z + off[n], In);
-        } else if (!ranks_sum) {  // the QR sums the split-K partials while loading Z
+        } else if (!ranks_sum && qr_fuse()) {  // the QR sums the split-K partials while loading Z
             const int k = pos_of(xp, n);
             const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + k));
             const int64_t A = prod(std::vector<int64_t>(xd.begin() + k + 1, xd.end()));
@@ -783,6 +785,17 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
         for (int n = 0; n < order; ++n) stats->ranks[n] = static_cast<int>(fcols[n]);
     }
     TK_CUDA(cudaStreamSynchronize(s));
+}
+
+// A/B knob: TENKIT_QR_FUSE=1 lets the QR kernel sum the sketch partials while loading Z (one
+// launch less per step, but 8 SMs read the partials: measured ~20 us slower per decomposition
+// at cfg 2 than the whole-GPU reduce kernel, so off by default)
+bool qr_fuse() {
+    static const bool on = [] {
+        const char* e = std::getenv("TENKIT_QR_FUSE");
+        return e && e[0] == '1';
+    }();
+    return on;
 }
 
 bool graphs_enabled() {

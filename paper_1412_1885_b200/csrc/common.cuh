@@ -2,6 +2,7 @@
 // error plumbing, the reference's counter RNG as device functions, mbarrier / bulk-copy
 // PTX wrappers.
 #pragma once
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -32,6 +33,22 @@ inline void require(bool cond, const std::string& msg) {
     } while (0)
 
 #define TK_LAUNCH_CHECK() TK_CUDA(cudaGetLastError())
+// A/B knob TENKIT_CARVEOUT=1: every kernel of the path prefers the maximum shared-memory
+// carveout, so consecutive kernels never make the SMs switch their L1/shared split.
+inline bool tk_carveout_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("TENKIT_CARVEOUT");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+#define TK_MAXSMEM(k)                                                                                         \
+    do {                                                                                                      \
+        static const bool tk_co_ = tk_carveout_on() &&                                                        \
+            cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributePreferredSharedMemoryCarveout, \
+                                 100) == cudaSuccess;                                                         \
+        (void)tk_co_;                                                                                         \
+    } while (0)
 
 // ---------------------------------------------------------------------------
 // Counter RNG (reference random.hpp:12-71), host + device. Bit-exact in the integer

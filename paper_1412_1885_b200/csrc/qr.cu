@@ -917,6 +917,7 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
         const char* e = std::getenv("TENKIT_QR_ROWPAR");
         return e ? std::atoi(e) : 1;
     }();
+    TK_MAXSMEM((qr_colpiv_cluster_kernel));
     TK_CUDA(cudaLaunchKernelEx(&cfg, qr_colpiv_cluster_kernel, z, rows, ncols, ld, u, ucap, up, up_dtype, rank_dev,
                                diag, fast, rowpar, nparts));
 }

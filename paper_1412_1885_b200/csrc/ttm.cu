@@ -384,11 +384,13 @@ void dispatch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_
         const int64_t grid = tiles * splits;
         require(grid < (int64_t(1) << 31), "ttm: grid too large");
         T* dst = splits > 1 ? work : out;
+        TK_MAXSMEM((ttm_mmajor_kernel<T, R>));
         ttm_mmajor_kernel<T, R><<<static_cast<unsigned>(grid), kConsumers + 32, Cfg::smem, s>>>(in, up, dst, P, K, cols,
                                                                                                 tiles_p, Q, kchunk);
         if (splits > 1) {
             TK_LAUNCH_CHECK();
             const int64_t n = P * cols * Q;
+            TK_MAXSMEM((splitk_reduce_kernel<T>));
             splitk_reduce_kernel<T><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(
                 work, out, n, static_cast<int>(splits));
             if (launches) ++*launches;
@@ -404,11 +406,13 @@ void dispatch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_
         const int64_t kchunk = ((K + splits - 1) / splits + bk - 1) / bk * bk;
         splits = (K + kchunk - 1) / kchunk;
         T* dst = splits > 1 ? work : out;
+        TK_MAXSMEM((ttm_kcontig_kernel<T, R>));
         ttm_kcontig_kernel<T, R><<<static_cast<unsigned>(tiles_a * splits), 128, 0, s>>>(in, up, dst, K, Q, cols,
                                                                                          tiles_a, kchunk);
         if (splits > 1) {
             TK_LAUNCH_CHECK();
             const int64_t n = int64_t(cols) * Q;
+            TK_MAXSMEM((splitk_reduce_kernel<T>));
             splitk_reduce_kernel<T><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(
                 work, out, n, static_cast<int>(splits));
             if (launches) ++*launches;
@@ -423,12 +427,14 @@ void dispatch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_
             while (splits > 1 && splits * P * cols * Q > work_elems) --splits;
         }
         T* dst = splits > 1 ? work : out;
+        TK_MAXSMEM((ttm_smallp_kernel<T, R>));
         ttm_smallp_kernel<T, R><<<dim3(static_cast<unsigned>(Q), static_cast<unsigned>((P + 31) / 32),
                                        static_cast<unsigned>(splits)), 256, 0, s>>>(in, up, dst, P, K, cols,
                                                                                    pack_stride(cols));
         if (splits > 1) {
             TK_LAUNCH_CHECK();
             const int64_t n = P * cols * Q;
+            TK_MAXSMEM((splitk_reduce_kernel<T>));
             splitk_reduce_kernel<T><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(
                 work, out, n, static_cast<int>(splits));
             if (launches) ++*launches;
@@ -648,18 +654,21 @@ void launch_ttm(const T* in, const T* up, T* out, int64_t P, int64_t K, int64_t 
 template <typename T>
 void launch_pack_factor(const double* u, int64_t ld, int64_t rows, int cols, T* up, cudaStream_t s) {
     const int stride = pack_stride(cols);
+    TK_MAXSMEM((pack_factor_kernel<T>));
     pack_factor_kernel<T><<<grid_for(rows * stride), 256, 0, s>>>(u, ld, rows, cols, stride, up);
     TK_LAUNCH_CHECK();
 }
 
 void launch_gaussian_fill(double* out, int64_t n, uint64_t offset, uint64_t key, cudaStream_t s) {
     if (n <= 0) return;
+    TK_MAXSMEM((gaussian_fill_kernel));
     gaussian_fill_kernel<<<grid_for((n + 3) / 2), 256, 0, s>>>(out, uint64_t(n), offset, key);
     TK_LAUNCH_CHECK();
 }
 
 void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t key, cudaStream_t s) {
     const uint64_t n = uint64_t(rows) * uint64_t(cols);
+    TK_MAXSMEM((gaussian_colmajor_kernel));
     gaussian_colmajor_kernel<<<grid_for(static_cast<int64_t>((n + 1) / 2)), 256, 0, s>>>(out, n, key);
     TK_LAUNCH_CHECK();
 }
@@ -678,6 +687,7 @@ int launch_sketch_partials(const T* x, int64_t B, int64_t I, int64_t A, const T*
     S = std::max(1, std::min(S, (K + 63) / 64));
     const int kchunk = ((K + S - 1) / S + 63) / 64 * 64;
     S = (K + kchunk - 1) / kchunk;
+    TK_MAXSMEM((sketch_kernel<T>));
     sketch_kernel<T><<<dim3(gx, gy, S), 256, 0, s>>>(x, static_cast<int>(B), I, static_cast<int>(A), om, pack_stride(rn), rn,
                                                      kchunk, work);
     TK_LAUNCH_CHECK();
@@ -688,6 +698,7 @@ template <typename T>
 int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* z, int64_t ldz, double* work,
                   cudaStream_t s) {
     const int S = launch_sketch_partials<T>(x, B, I, A, om, rn, work, s);
+    TK_MAXSMEM((sketch_reduce_kernel));
     sketch_reduce_kernel<<<grid_for(I * rn), 256, 0, s>>>(work, I, rn, S, z, ldz);
     TK_LAUNCH_CHECK();
     return 2;
@@ -703,6 +714,7 @@ template int launch_sketch<double>(const double*, int64_t, int64_t, int64_t, con
 
 template <typename T>
 void launch_unfold(const T* x, int64_t B, int64_t I, int64_t A, T* out, cudaStream_t s) {
+    TK_MAXSMEM((unfold_kernel<T>));
     unfold_kernel<T><<<grid_for(B * I * A), 256, 0, s>>>(x, B, I, A, out);
     TK_LAUNCH_CHECK();
 }
@@ -714,6 +726,7 @@ void launch_gaussian_packed(T* out, int64_t rows, int cols, uint64_t key, cudaSt
                             int64_t rows_total) {
     const int stride = pack_stride(cols);
     if (rows_total <= 0) rows_total = rows;
+    TK_MAXSMEM((gaussian_packed_kernel<T>));
     gaussian_packed_kernel<T><<<grid_for(rows * stride), 256, 0, s>>>(out, rows, cols, stride, key, row_off, rows_total);
     TK_LAUNCH_CHECK();
 }
@@ -723,11 +736,13 @@ template void launch_gaussian_packed<double>(double*, int64_t, int, uint64_t, cu
 template <typename T>
 void launch_gaussian_packed_map(T* out, int64_t rows, int cols, uint64_t key, const RowMap& map, cudaStream_t s) {
     const int stride = pack_stride(cols);
+    TK_MAXSMEM((gaussian_packed_map_kernel<T>));
     gaussian_packed_map_kernel<T><<<grid_for(rows * stride), 256, 0, s>>>(out, rows, cols, stride, key, map);
     TK_LAUNCH_CHECK();
 }
 void launch_gaussian_fill_map(double* out, int64_t n, uint64_t key, const RowMap& map, cudaStream_t s) {
     // stride 1, one column: out[c] = normal_at(key, 0 * rows_total + g(c))
+    TK_MAXSMEM((gaussian_packed_map_kernel<double>));
     gaussian_packed_map_kernel<double><<<grid_for(n), 256, 0, s>>>(out, n, 1, 1, key, map);
     TK_LAUNCH_CHECK();
 }
@@ -736,6 +751,7 @@ template void launch_gaussian_packed_map<double>(double*, int64_t, int, uint64_t
 
 template <typename S, typename D>
 void launch_cast(const S* in, D* out, int64_t n, cudaStream_t s) {
+    TK_MAXSMEM((cast_kernel<S, D>));
     cast_kernel<S, D><<<grid_for(n), 256, 0, s>>>(in, out, n);
     TK_LAUNCH_CHECK();
 }
@@ -754,6 +770,7 @@ void launch_permute_cast(const S* in, D* out, int order, const int64_t* dims, co
         pd.sstride[perm[k]] = st;
         st *= dims[perm[k]];
     }
+    TK_MAXSMEM((permute_cast_kernel<S, D>));
     permute_cast_kernel<S, D><<<grid_for(n), 256, 0, s>>>(in, out, n, pd);
     TK_LAUNCH_CHECK();
 }
@@ -763,6 +780,7 @@ template void launch_permute_cast<float, float>(const float*, float*, int, const
 
 template <typename T>
 void launch_splitk_reduce(const T* part, T* out, int64_t n, int splits, cudaStream_t s) {
+    TK_MAXSMEM((splitk_reduce_kernel<T>));
     splitk_reduce_kernel<T><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(
         part, out, n, splits);
     TK_LAUNCH_CHECK();
@@ -777,6 +795,7 @@ template void launch_pack_factor<float>(const double*, int64_t, int64_t, int, fl
 template void launch_pack_factor<double>(const double*, int64_t, int64_t, int, double*, cudaStream_t);
 template <typename S, typename D>
 void launch_cast2d(const S* in, int64_t ldi, D* out, int64_t ldo, int64_t rows, int64_t cols, cudaStream_t s) {
+    TK_MAXSMEM((cast2d_kernel<S, D>));
     cast2d_kernel<S, D><<<grid_for(rows * cols), 256, 0, s>>>(in, ldi, out, ldo, rows, cols);
     TK_LAUNCH_CHECK();
 }

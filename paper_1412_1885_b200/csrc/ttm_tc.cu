@@ -480,6 +480,7 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
     }
     require(grid < (int64_t(1) << 31), "ttm: grid too large");
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    TK_MAXSMEM((ttm_tc_kernel<NH, MT, KM, OCC>));
     ttm_tc_kernel<NH, MT, KM, OCC><<<dim3(static_cast<unsigned>(grid), static_cast<unsigned>(splits)), kTcThreads,
                                      C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p, tout ? 1 : 0);
     TK_LAUNCH_CHECK();
@@ -502,10 +503,10 @@ void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void*
     const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
     uint32_t* o = static_cast<uint32_t*>(out);
     switch (nh) {
-        case 16: pack_umma_kernel<16><<<grid, 256, 0, s>>>(u, ld, rows, cols, ksteps, o); break;
-        case 32: pack_umma_kernel<32><<<grid, 256, 0, s>>>(u, ld, rows, cols, ksteps, o); break;
-        case 48: pack_umma_kernel<48><<<grid, 256, 0, s>>>(u, ld, rows, cols, ksteps, o); break;
-        default: pack_umma_kernel<64><<<grid, 256, 0, s>>>(u, ld, rows, cols, ksteps, o); break;
+        case 16: TK_MAXSMEM((pack_umma_kernel<16>)); pack_umma_kernel<16><<<grid, 256, 0, s>>>(u, ld, rows, cols, ksteps, o); break;
+        case 32: TK_MAXSMEM((pack_umma_kernel<32>)); pack_umma_kernel<32><<<grid, 256, 0, s>>>(u, ld, rows, cols, ksteps, o); break;
+        case 48: TK_MAXSMEM((pack_umma_kernel<48>)); pack_umma_kernel<48><<<grid, 256, 0, s>>>(u, ld, rows, cols, ksteps, o); break;
+        default: TK_MAXSMEM((pack_umma_kernel<64>)); pack_umma_kernel<64><<<grid, 256, 0, s>>>(u, ld, rows, cols, ksteps, o); break;
     }
     TK_LAUNCH_CHECK();
 }

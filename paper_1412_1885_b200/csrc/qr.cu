@@ -831,8 +831,8 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             uout[(r0 + i) + int64_t(j) * rows] = j < rank ? sh.sgn[j] * z[i + j * ld] : 0.0;
     if (upout) {
         const int stride = (rank + 3) / 4 * 4;
-        for (int64_t t = tid; t < int64_t(nloc) * stride; t += kQrThreads) {
-            const int i = static_cast<int>(t / stride), j = static_cast<int>(t % stride);
+        for (int t = tid; t < nloc * stride; t += kQrThreads) {  // < 16 * 128 * 64: 32-bit indices
+            const int i = t / stride, j = t - (t / stride) * stride;
             const double v = j < rank ? sh.sgn[j] * z[i + j * ld] : 0.0;
             const int64_t o = (r0 + i) * stride + j;
             if (up_dtype == kF32) static_cast<float*>(upout)[o] = static_cast<float>(v);

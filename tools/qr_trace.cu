@@ -19,7 +19,9 @@ int main() {
         cudaMalloc(&u, h.size() * 8);
         cudaMalloc(&rk, 4);
         cudaMemcpy(z, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
-        for (int it = 0; it < 3; ++it) tkb::launch_orthonormal_basis(z, rows, cols, u, cols, nullptr, 1, rk, nullptr, 0);
+        float* upk;
+        cudaMalloc(&upk, size_t(rows) * 64 * 4);
+        for (int it = 0; it < 3; ++it) tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0);
         cudaDeviceSynchronize();
         {
             cudaEvent_t e0, e1;
@@ -27,7 +29,7 @@ int main() {
             cudaEventCreate(&e1);
             cudaEventRecord(e0);
             for (int it = 0; it < 20; ++it)
-                tkb::launch_orthonormal_basis(z, rows, cols, u, cols, nullptr, 1, rk, nullptr, 0);
+                tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms = 0.f;
@@ -35,6 +37,22 @@ int main() {
             int clk = 0;
             cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
             printf("%dx%d: %.1f us per launch (back to back, events), SM clock attr %d MHz\n", rows, cols, 1e3 * ms / 20, clk / 1000);
+            // in-situ-like: each QR right after a 2 GB memset (HBM-bound work before it)
+            void* big = nullptr;
+            cudaMalloc(&big, size_t(2) << 30);
+            float tot = 0.f;
+            for (int it = 0; it < 10; ++it) {
+                cudaMemsetAsync(big, it, size_t(2) << 30);
+                cudaEventRecord(e0);
+                tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float m1 = 0.f;
+                cudaEventElapsedTime(&m1, e0, e1);
+                tot += m1;
+            }
+            cudaFree(big);
+            printf("%dx%d: %.1f us per launch after a 2 GB memset each\n", rows, cols, 1e3 * tot / 10);
         }
         long long t[4096];
         cudaMemcpyFromSymbol(t, g_qr_trace, sizeof(t));

@@ -1,3 +1,4 @@
 #!/bin/bash
-for v in 1 0 1 0; do echo "CARVEOUT=$v"; TENKIT_CARVEOUT=$v python tools/phase_bench.py 2>&1 | grep phases | tail -1; done
-for v in 1 0 1 0; do TENKIT_CARVEOUT=$v python bench.py --steps 30 --warmup 3 --no-e2e --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('carveout=$v', d['ms_per_step'], d['clocks']['sm_mhz'])"; done
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+for v in 2 1; do echo "ROWPAR=$v"; TENKIT_QR_ROWPAR=$v timeout 120 ./tools/qr_trace 2>&1 | grep -E "1000x30"; done
+for v in 2 1 2 1; do echo "ROWPAR=$v"; TENKIT_QR_ROWPAR=$v python tools/phase_bench.py 2>&1 | grep phases | tail -1; done

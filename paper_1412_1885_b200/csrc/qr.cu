@@ -351,6 +351,59 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
     return true;
 }
 
+// n <= 32: X = R^{-1} (R upper, col-major n x n; rinv = 1 / R_kk) by one warp, lane j holding
+// column j in registers: right-looking back substitution (x_i = acc_i / R_ii, then acc_k -=
+// R_ki x_i for k < i), so each step's chain is one multiply and one FMA.
+__device__ void warp_upper_inv(const double* rr, const double* rinv, int n, double* x) {
+    const int j = threadIdx.x & 31;
+    double acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = k == j ? 1.0 : 0.0;
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+        if (i < n) {
+            const double xi = acc[i] * rinv[i];
+            acc[i] = xi;
+            const double* ri = rr + size_t(i) * n;  // column i of R: R[k][i] = ri[k]
+#pragma unroll
+            for (int k = 0; k < i; ++k) acc[k] = fma(-ri[k], xi, acc[k]);
+        }
+    }
+    if (j < n)
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+            if (k < n) x[k + size_t(j) * n] = acc[k];
+}
+
+// out (own rows, ld) = in_P X on the FP64 tensor cores: each warp takes 8 x 8 output tiles and
+// runs mma.m8n8k4.f64 over k (X: n x n col-major; perm: column order of `in`, may be null).
+// A[m][k] = in[row0 + m, perm[k0 + k]] (m = lane / 4, k = lane % 4), B[k][c] = X[k0 + k][col0 + c]
+// (k = lane % 4, c = lane / 4), D[m][2 (lane % 4) + e].
+__device__ void apply_dmma(const double* in, double* out, int ld, int nloc, int n, const double* x, const int* perm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int rt = (nloc + 7) / 8, ct = (n + 7) / 8;
+    for (int tt = warp; tt < rt * ct; tt += kQrThreads / 32) {
+        const int row0 = (tt % rt) * 8, col0 = (tt / rt) * 8;
+        const int ra = row0 + g;      // A row of this lane
+        const int cb = col0 + g;      // B column of this lane
+        double d0 = 0.0, d1 = 0.0;
+        for (int k0 = 0; k0 < n; k0 += 4) {
+            const int k = k0 + t4;
+            const double a = (ra < nloc && k < n) ? in[ra + size_t(perm ? perm[k] : k) * ld] : 0.0;
+            const double b = (k < n && cb < n) ? x[k + size_t(cb) * n] : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                         : "+d"(d0), "+d"(d1)
+                         : "d"(a), "d"(b));
+        }
+        const int r = row0 + g, c = col0 + 2 * t4;
+        if (r < nloc) {
+            if (c < n) out[r + size_t(c) * ld] = d0;
+            if (c + 1 < n) out[r + size_t(c + 1) * ld] = d1;
+        }
+    }
+}
+
 // n <= 32, one thread per own row i (rows in registers): out_i = in_i,P R^{-1} by forward
 // substitution, right-looking (x_k = acc_k / R_kk, then acc_j -= x_k R_kj for j > k: the
 // chain per step is one multiply and one FMA). R upper, col-major n x n, rinv = 1 / R_kk.
@@ -546,7 +599,11 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         if (ok1) {  // identical in every CTA (same reduced Gram, same arithmetic)
             // Q1 = Z_P R1^{-1}: row-parallel substitution for n <= 32, else with R1^{-1}
             // formed explicitly (parallel application)
-            if (n <= 32 && rowpar) {
+            if (n <= 32 && rowpar == 2) {  // R1^{-1} by one warp, applied on the FP64 tensor cores
+                if (warp == 0) warp_upper_inv(r1, rinv1, n, r2);
+                __syncthreads();
+                apply_dmma(z, q, ld, nloc, n, r2, perm);
+            } else if (n <= 32 && rowpar) {
                 rows_trsm_perm(z, q, ld, nloc, n, r1, rinv1, perm);
             } else {
                 if (warp == 0) warp_tri_inv(r1, rinv1, n, r2);
@@ -569,7 +626,8 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             for (int k = tid; k < n; k += kQrThreads) perm2[k] = k;
             __syncthreads();
             QR_MARK(604);
-            if (n <= 32 && rowpar) rows_mul_upper(q, z, ld, nloc, n, r2);
+            if (rowpar == 2) apply_dmma(q, z, ld, nloc, n, r2, nullptr);
+            else if (n <= 32 && rowpar) rows_mul_upper(q, z, ld, nloc, n, r2);
             else apply_upper(q, z, ld, nloc, n, r2, perm2);
             for (int k = tid; k < n; k += kQrThreads) sh.beta[k] = r1[k + k * n] * (1.0 + 0.5 * (gs[k + k * n] - 1.0));
             __syncthreads();
@@ -913,9 +971,11 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    static const int rowpar = [] {  // A/B knob: 0 = R^-1 formed by one warp + gathered application
+    // A/B knob: 2 (default) = R^-1 by one warp + FP64-tensor-core applications, 1 = row-parallel
+    // substitution / multiply, 0 = R^-1 by one warp + gathered FFMA application
+    static const int rowpar = [] {
         const char* e = std::getenv("TENKIT_QR_ROWPAR");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 2;
     }();
     TK_MAXSMEM((qr_colpiv_cluster_kernel));
     TK_CUDA(cudaLaunchKernelEx(&cfg, qr_colpiv_cluster_kernel, z, rows, ncols, ld, u, ucap, up, up_dtype, rank_dev,

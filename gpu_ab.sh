@@ -1,4 +1,4 @@
 #!/bin/bash
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_tc.py tests/test_gpu_workload.py tests/test_golden.py -x -q 2>&1 | tail -2
-for v in 1 2; do python tools/phase_bench.py 2>&1 | grep phases | tail -1; done
-python bench.py --steps 30 --warmup 3 --no-e2e --no-cpu 2>/dev/null | tail -1 | cut -c1-220
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+for v in 2 1; do echo "ROWPAR=$v"; TENKIT_QR_ROWPAR=$v timeout 120 ./tools/qr_trace 2>&1 | grep -E "1000x30"; done
+for v in 2 1 2 1; do echo "ROWPAR=$v"; TENKIT_QR_ROWPAR=$v python tools/phase_bench.py 2>&1 | grep phases | tail -1; done

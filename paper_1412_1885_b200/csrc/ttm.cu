@@ -517,35 +517,21 @@ __global__ void __launch_bounds__(256) sketch_kernel(const T* __restrict__ x, in
             os[kl][rl] = (k < k1 && r < rn) ? static_cast<double>(om[int64_t(k) * stride + r]) : 0.0;
         }
         __syncthreads();
-        // 32 x 32 output tile = 16 tiles of 8 x 8 on the FP64 tensor cores (mma.m8n8k4.f64),
-        // two per warp; the k-padding of the staged tile is zero
-        const int g = ti >> 2, t4 = ti & 3;
+        const int kn = min(64, k1 - kk);
+        for (int k = 0; k < kn; ++k) {
+            const double xv = xs[k][ti];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int t = tr + 8 * h;
-            const int ib = (t & 3) * 8, rb = (t >> 2) * 8;
-#pragma unroll 4
-            for (int k = 0; k < 64; k += 4) {
-                const double a = xs[k + t4][ib + g];
-                const double b = os[k + t4][rb + g];
-                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
-                             : "+d"(acc[2 * h]), "+d"(acc[2 * h + 1])
-                             : "d"(a), "d"(b));
-            }
+            for (int j = 0; j < 4; ++j) acc[j] = fma(xv, os[k][tr * 4 + j], acc[j]);
         }
         __syncthreads();
     }
-    const int g = ti >> 2, t4 = ti & 3;
+    const int64_t i = i0 + ti;
+    if (i < I)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int t = tr + 8 * h;
-        const int64_t i = i0 + (t & 3) * 8 + g;
-        const int r = r0 + (t >> 2) * 8 + 2 * t4;
-        if (i < I) {
-            if (r < rn) part[(int64_t(blockIdx.z) * rn + r) * I + i] = acc[2 * h];
-            if (r + 1 < rn) part[(int64_t(blockIdx.z) * rn + r + 1) * I + i] = acc[2 * h + 1];
+        for (int j = 0; j < 4; ++j) {
+            const int r = r0 + tr * 4 + j;
+            if (r < rn) part[(int64_t(blockIdx.z) * rn + r) * I + i] = acc[j];
         }
-    }
 }
 
 __global__ void sketch_reduce_kernel(const double* __restrict__ part, int64_t I, int rn, int S, double* __restrict__ z,

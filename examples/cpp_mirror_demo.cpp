@@ -3,6 +3,7 @@
 // include and namespace changed. Prints the Tucker core norm, factor shapes and the FFCP
 // fit trace so tests/test_cpp_mirror.py can compare them with the oracle.
 //   usage: cpp_mirror_demo I J K R p ffcp_rank   (data: seeded N(0,1) Tucker + noise-free)
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -38,6 +39,21 @@ int main(int argc, char** argv) {
         tenkit::FfcpResult f = tenkit::ffcp(m, cr, tenkit::ConstraintSpec{}, tenkit::StopRule{30, 0.0}, {8, 0});
         std::printf("iterations %d\n", f.iterations);
         for (double v : f.fit_trace) std::printf("fit %.17g\n", v);
+        // the distributed protocol's basis on two row blocks of a sketch (range_finder.hpp:48-84)
+        tenkit::Matrix z = tenkit::gaussian_matrix(40, 5, tenkit::SeedSpec{6, 0});
+        tenkit::Matrix z0(15, 5), z1(25, 5);
+        for (tenkit::Index j = 0; j < 5; ++j)
+            for (tenkit::Index i = 0; i < 40; ++i) (i < 15 ? z0(i, j) : z1(i - 15, j)) = z(i, j);
+        tenkit::GramOrthoResult gr = tenkit::gram_orthonormalize({z0, z1});
+        double defect = 0.0;
+        for (tenkit::Index a = 0; a < 5; ++a)
+            for (tenkit::Index c = 0; c < 5; ++c) {
+                double d = 0.0;
+                for (const auto& blk : gr.blocks)
+                    for (tenkit::Index i = 0; i < blk.rows(); ++i) d += blk(i, a) * blk(i, c);
+                defect = std::max(defect, std::abs(d - (a == c ? 1.0 : 0.0)));
+            }
+        std::printf("gram_kept %zu\ngram_defect %.3e\n", gr.spectrum.size(), defect);
     } catch (const std::invalid_argument& e) {
         std::printf("invalid_argument: %s\n", e.what());
         return 3;

@@ -11,6 +11,10 @@
  *   tk_unfold_times       <- tenkit::unfold_times        tensor.hpp:195-209
  *   tk_orthonormal_basis  <- tenkit::orthonormal_basis   range_finder.hpp:18-29
  *                            + detail::fix_column_signs  tucker.hpp:39-45
+ *   tk_gram_orthonormalize <- tenkit::gram_orthonormalize range_finder.hpp:48-84
+ *   tk_gram_ortho_transform <- tenkit::gram_ortho_transform range_finder.hpp:86-105
+ *   tk_context_set_orthonormalizer(TK_ORTHO_GRAM) <- the dist protocol's basis,
+ *                            detail::dist_compress_mode dist.hpp:688-723
  *   tk_gaussian_matrix    <- tenkit::gaussian_matrix     random.hpp:85-100
  *   tk_gaussian_fill      <- tenkit::gaussian_tensor     random.hpp:124-138 (window at an offset)
  *   tk_gaussian_fill_block   (same, one block of a BlockGrid, dist.hpp:24-123)
@@ -123,6 +127,14 @@ int tk_context_synchronize(tk_context* ctx);
  * data when the shape tiles the GPU, FFMA otherwise), 1 FFMA only, 2 tcgen05 whenever the
  * shape is supported (also for the kernel-level tk_ttm) */
 int tk_context_set_ttm_path(tk_context* ctx, int path);
+/* Basis of every range step (tk_rand_tucker_2i / tk_rand_tucker, any comm):
+ * TK_ORTHO_COLPIV (default) = orthonormal_basis + fix_column_signs (tucker.hpp:39-45,
+ * range_finder.hpp:18-29, single-node semantics); TK_ORTHO_GRAM = the reference's
+ * distributed protocol (dist_rand_tucker(_2i), dist.hpp:688-723): Gram-eig transform,
+ * U = Z T, columns in descending eigenvalue order, no sign rule. */
+#define TK_ORTHO_COLPIV 0
+#define TK_ORTHO_GRAM 1
+int tk_context_set_orthonormalizer(tk_context* ctx, int kind);
 
 /* Alg. 3. y: dtype TK_F32/TK_F64, dims[order], device pointer if y_on_device else host
  * (copied in on the context stream). ranks[order], oversample >= 0, seed = SeedSpec{root, stream}. */
@@ -149,6 +161,14 @@ int tk_unfold_times(tk_context* ctx, int dtype, int64_t order, const int64_t* di
 /* orthonormal_basis + fix_column_signs: q (rows x cols capacity, double) and the rank */
 int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* q, int64_t* rank,
                          double* rdiag);
+/* gram_orthonormalize of the stacked blocks (one device matrix z, rows x cols, cols <= 64):
+ * u (rows x cols capacity, columns >= kept zero), spectrum (cols, descending, zero after
+ * kept) and kept. TK_ERR_INVALID "all blocks are zero" for a zero Z. */
+int tk_gram_orthonormalize(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* u, double* spectrum,
+                           int64_t* kept);
+/* gram_ortho_transform of a device n x n Gram matrix: transform (n x n capacity), spectrum, kept */
+int tk_gram_ortho_transform(tk_context* ctx, int64_t n, const double* gram, double* transform, double* spectrum,
+                            int64_t* kept);
 /* gaussian_matrix(rows, cols, SeedSpec{root, stream}) into a device double buffer */
 int tk_gaussian_matrix(tk_context* ctx, int64_t rows, int64_t cols, uint64_t seed_root, uint64_t seed_stream,
                        double* out);

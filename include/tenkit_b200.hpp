@@ -19,6 +19,8 @@
 //   ffcp                   ffcp.hpp:94-194
 //   ttm / ttm_all / unfold_times   tensor.hpp:151-209
 //   orthonormal_basis      range_finder.hpp:18-29 (+ fix_column_signs, tucker.hpp:39-45)
+//   gram_orthonormalize    range_finder.hpp:48-84 (GramOrthoResult, range_finder.hpp:38-41)
+//   gram_ortho_transform   range_finder.hpp:86-105
 //   gaussian_matrix        random.hpp:85-100
 //
 // Errors: TK_ERR_INVALID -> std::invalid_argument, anything else -> std::runtime_error,
@@ -353,6 +355,70 @@ inline Matrix orthonormal_basis(const Matrix& z) {
     Matrix q(z.rows(), rank);
     dq.to_host(q.data(), static_cast<std::size_t>(q.size()));
     return q;
+}
+
+/// Gram-path result (range_finder.hpp:38-41): the orthonormalised row blocks and the kept
+/// eigenvalues, descending.
+struct GramOrthoResult {
+    std::vector<Matrix> blocks;
+    std::vector<double> spectrum;
+};
+
+/// gram_orthonormalize (range_finder.hpp:48-84): sum_s Z_s^T Z_s = U S U^T, blocks Z_s U S^-1/2
+/// (eigenvalues <= 1e-12 top dropped); eigenvector signs are the device eigensolver's.
+inline GramOrthoResult gram_orthonormalize(const std::vector<Matrix>& z_blocks) {
+    detail::require(!z_blocks.empty(), "gram_orthonormalize: no blocks");
+    const Index r = z_blocks.front().cols();
+    Index rows = 0;
+    for (const Matrix& z : z_blocks) {
+        detail::require(z.cols() == r, "gram_orthonormalize: column-count mismatch");
+        rows += z.rows();
+    }
+    Matrix stacked(rows, r);
+    Index at = 0;
+    for (const Matrix& z : z_blocks) {
+        for (Index j = 0; j < r; ++j)
+            for (Index i = 0; i < z.rows(); ++i) stacked(at + i, j) = z(i, j);
+        at += z.rows();
+    }
+    detail::DeviceBuffer<double> dz(stacked.data(), static_cast<std::size_t>(stacked.size()));
+    detail::DeviceBuffer<double> du(static_cast<std::size_t>(stacked.size()));
+    detail::DeviceBuffer<double> ds(static_cast<std::size_t>(r));
+    Index kept = 0;
+    detail::check(tk_gram_orthonormalize(Device::context(), rows, r, dz.p, du.p, ds.p, &kept));
+    Matrix u(rows, kept);
+    du.to_host(u.data(), static_cast<std::size_t>(u.size()));
+    GramOrthoResult out;
+    out.spectrum.resize(static_cast<std::size_t>(r));
+    ds.to_host(out.spectrum.data(), out.spectrum.size());
+    out.spectrum.resize(static_cast<std::size_t>(kept));
+    at = 0;
+    for (const Matrix& z : z_blocks) {
+        Matrix b(z.rows(), kept);
+        for (Index j = 0; j < kept; ++j)
+            for (Index i = 0; i < z.rows(); ++i) b(i, j) = u(at + i, j);
+        out.blocks.push_back(std::move(b));
+        at += z.rows();
+    }
+    return out;
+}
+
+/// gram_ortho_transform (range_finder.hpp:86-105): T (n x kept) with stacked-Z * T orthonormal.
+inline std::pair<Matrix, std::vector<double>> gram_ortho_transform(const Matrix& gram_sum) {
+    detail::require(gram_sum.rows() == gram_sum.cols() && gram_sum.rows() >= 1,
+                    "gram_ortho_transform: square Gram matrix required");
+    const Index n = gram_sum.rows();
+    detail::DeviceBuffer<double> dg(gram_sum.data(), static_cast<std::size_t>(gram_sum.size()));
+    detail::DeviceBuffer<double> dt(static_cast<std::size_t>(n * n));
+    detail::DeviceBuffer<double> ds(static_cast<std::size_t>(n));
+    Index kept = 0;
+    detail::check(tk_gram_ortho_transform(Device::context(), n, dg.p, dt.p, ds.p, &kept));
+    Matrix t(n, kept);
+    dt.to_host(t.data(), static_cast<std::size_t>(t.size()));
+    std::vector<double> sp(static_cast<std::size_t>(n));
+    ds.to_host(sp.data(), sp.size());
+    sp.resize(static_cast<std::size_t>(kept));
+    return {std::move(t), std::move(sp)};
 }
 
 /// out = t x_mode m (tensor.hpp:151-176).

@@ -282,6 +282,58 @@ def rand_tucker_2i(y, ranks, oversample: int, seed, return_sketches: bool = Fals
     return g, us
 
 
+def sym_eig(a):
+    """Symmetric eigendecomposition (stand-in for Eigen's SelfAdjointEigenSolver,
+    range_finder.hpp:57,87): ascending eigenvalues, eigenvectors as columns."""
+    a = _f64(a)
+    n = a.shape[0]
+    ev = np.empty(max(n, 1))
+    vec = np.empty(max(n * n, 1))
+    _check(lib().tko_sym_eig(C.c_int64(n), _ptr(_flat(a)), _ptr(ev), _ptr(vec)))
+    return ev[:n], vec[: n * n].reshape((n, n), order="F")
+
+
+def gram_ortho_transform(gram):
+    """gram_ortho_transform (range_finder.hpp:86-105) -> (transform n x kept, spectrum)."""
+    gram = _f64(gram)
+    n = gram.shape[0]
+    t = np.empty(max(n * n, 1))
+    sp = np.empty(max(n, 1))
+    kept = C.c_int64()
+    _check(lib().tko_gram_ortho_transform(C.c_int64(n), _ptr(_flat(gram)), _ptr(t), _ptr(sp), C.byref(kept)))
+    k = kept.value
+    return t[: n * k].reshape((n, k), order="F").copy(), sp[:k].copy()
+
+
+def gram_orthonormalize(z_blocks):
+    """gram_orthonormalize (range_finder.hpp:48-84) over row blocks -> (stacked U, spectrum)."""
+    blocks = [_f64(b) for b in z_blocks]
+    cols = blocks[0].shape[1] if blocks else 0
+    z = np.vstack(blocks) if blocks else np.zeros((0, 0))
+    rows = z.shape[0]
+    br = _i64([b.shape[0] for b in blocks])
+    u = np.empty(max(rows * cols, 1))
+    sp = np.empty(max(cols, 1))
+    kept = C.c_int64()
+    _check(lib().tko_gram_orthonormalize(C.c_int64(len(blocks)), _iptr(br), C.c_int64(cols), _ptr(_flat(z)),
+                                         _ptr(u), _ptr(sp), C.byref(kept)))
+    k = kept.value
+    return u[: rows * k].reshape((rows, k), order="F").copy(), sp[:k].copy()
+
+
+def dist_rand_tucker_gram(y, ranks, oversample: int, seed, alg: int = 3):
+    """The reference's distributed algorithms' numerics (dist_rand_tucker alg=2,
+    dist_rand_tucker_2i alg=3; dist.hpp:852-936): Gram-eig basis, no sign rule,
+    on the assembled tensor. Returns (core, factors)."""
+    y = _f64(y)
+    dims = y.shape
+    rts, core, cshape, fbufs, farr, cols = _model_buffers(dims, ranks, oversample)
+    _check(lib().tko_dist_rand_tucker_gram(C.c_int(alg), _iptr(_i64(dims)), C.c_int64(y.ndim), _ptr(_flat(y)),
+                                           _iptr(_i64(ranks)), C.c_int64(oversample), C.c_uint64(seed[0]),
+                                           C.c_uint64(seed[1]), _ptr(core), _iptr(cshape), farr, _iptr(cols)))
+    return _unpack_model(dims, core, cshape, fbufs, cols)
+
+
 def rand_tucker(y, ranks, oversample: int, seed):
     """Alg. 2 (tucker.hpp:108-130). Returns (core, factors)."""
     y = _f64(y)

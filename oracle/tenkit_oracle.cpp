@@ -438,13 +438,158 @@ inline void fix_column_signs(Mat& u) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Gram-path orthonormalisation of the distributed protocol (range_finder.hpp:43-105,
+// used by dist_compress_mode, dist.hpp:688-699). Eigen's SelfAdjointEigenSolver
+// (tridiagonalisation + implicit QL) is stood in for by a cyclic Jacobi eigensolver
+// with round-robin (tournament) pairing: the eigenpairs are unique up to the sign of
+// each eigenvector (distinct eigenvalues), which is all the reference's result
+// depends on (its dist path applies no sign rule, and its tests compare subspaces,
+// test_dist.cpp:141-152). The device kernel (csrc/gram.cu) runs the same rounds.
+// ---------------------------------------------------------------------------
+
+// Pairs of round r of the circle method over m (even) players: position 0 fixed,
+// positions 1..m-1 rotate; pair k = (L[k], L[m-1-k]).
+inline void jacobi_round_pairs(int m, int r, std::vector<std::pair<int, int>>& pairs) {
+    std::vector<int> l(static_cast<size_t>(m));
+    l[0] = 0;
+    for (int k = 1; k < m; ++k) l[static_cast<size_t>(k)] = ((k - 1 + r) % (m - 1)) + 1;
+    pairs.clear();
+    for (int k = 0; k < m / 2; ++k) pairs.emplace_back(l[static_cast<size_t>(k)], l[static_cast<size_t>(m - 1 - k)]);
+}
+
+constexpr int kJacobiMaxSweeps = 40;
+
+// a (n x n symmetric) -> eigenvalues ascending (Eigen's order) + eigenvectors (columns)
+inline void sym_eig(const Mat& a_in, std::vector<double>& evals, Mat& evecs) {
+    const int n = static_cast<int>(a_in.rows);
+    Mat a = a_in;
+    Mat v(n, n);
+    for (int i = 0; i < n; ++i) v(i, i) = 1.0;
+    const int m = n + (n & 1);
+    std::vector<std::pair<int, int>> pairs;
+    std::vector<double> cs(static_cast<size_t>(m / 2)), sn(static_cast<size_t>(m / 2));
+    for (int sweep = 0; sweep < kJacobiMaxSweeps && n > 1; ++sweep) {
+        bool rotated = false;
+        for (int r = 0; r < m - 1; ++r) {
+            jacobi_round_pairs(m, r, pairs);
+            // rotation parameters of every pair from the same A (they act on disjoint rows)
+            for (size_t k = 0; k < pairs.size(); ++k) {
+                int p = pairs[k].first, q = pairs[k].second;
+                if (p > q) std::swap(p, q);
+                cs[k] = 1.0, sn[k] = 0.0;
+                if (q >= n) continue;
+                const double apq = a(p, q), app = a(p, p), aqq = a(q, q);
+                if (std::abs(apq) <= 1e-18 * std::sqrt(std::abs(app * aqq)) || apq == 0.0) continue;
+                const double theta = (aqq - app) / (2.0 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
+                cs[k] = 1.0 / std::sqrt(t * t + 1.0);
+                sn[k] = t * cs[k];
+                rotated = true;
+            }
+            // A <- P^T A (rows), then A <- A P and V <- V P (columns)
+            for (size_t k = 0; k < pairs.size(); ++k) {
+                int p = pairs[k].first, q = pairs[k].second;
+                if (p > q) std::swap(p, q);
+                if (q >= n || sn[k] == 0.0) continue;
+                for (int c = 0; c < n; ++c) {
+                    const double x = a(p, c), y = a(q, c);
+                    a(p, c) = cs[k] * x - sn[k] * y;
+                    a(q, c) = sn[k] * x + cs[k] * y;
+                }
+            }
+            for (size_t k = 0; k < pairs.size(); ++k) {
+                int p = pairs[k].first, q = pairs[k].second;
+                if (p > q) std::swap(p, q);
+                if (q >= n || sn[k] == 0.0) continue;
+                for (int i = 0; i < n; ++i) {
+                    const double x = a(i, p), y = a(i, q);
+                    a(i, p) = cs[k] * x - sn[k] * y;
+                    a(i, q) = sn[k] * x + cs[k] * y;
+                    const double vx = v(i, p), vy = v(i, q);
+                    v(i, p) = cs[k] * vx - sn[k] * vy;
+                    v(i, q) = sn[k] * vx + cs[k] * vy;
+                }
+            }
+        }
+        if (!rotated) break;
+    }
+    // ascending order; ties keep the lower index first
+    std::vector<int> idx(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) idx[static_cast<size_t>(i)] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return a(x, x) < a(y, y); });
+    evals.assign(static_cast<size_t>(n), 0.0);
+    evecs = Mat(n, n);
+    for (int j = 0; j < n; ++j) {
+        const int s = idx[static_cast<size_t>(j)];
+        evals[static_cast<size_t>(j)] = a(s, s);
+        for (int i = 0; i < n; ++i) evecs(i, j) = v(i, s);
+    }
+}
+
+// gram_ortho_transform (range_finder.hpp:86-105): T with stacked-Z * T orthonormal,
+// columns in descending eigenvalue order, eigenvalues <= 1e-12 * top dropped.
+inline Mat gram_ortho_transform(const Mat& gram, std::vector<double>* spectrum) {
+    require(gram.rows == gram.cols, "gram_ortho_transform: square Gram matrix required");
+    std::vector<double> ev;
+    Mat vec;
+    sym_eig(gram, ev, vec);
+    const Index r = gram.rows;
+    const double top = r > 0 ? ev[static_cast<size_t>(r - 1)] : 0.0;
+    require(top > 0.0, "gram_ortho_transform: zero Gram matrix");
+    Index kept = 0;
+    for (Index i = r - 1; i >= 0; --i) {
+        if (ev[static_cast<size_t>(i)] > 1e-12 * top) ++kept;  // kRankDeficiencyTol
+        else break;
+    }
+    Mat t(r, kept);
+    if (spectrum) spectrum->assign(static_cast<size_t>(kept), 0.0);
+    for (Index j = 0; j < kept; ++j) {
+        const Index src = r - 1 - j;
+        const double l = ev[static_cast<size_t>(src)];
+        if (spectrum) (*spectrum)[static_cast<size_t>(j)] = l;
+        for (Index i = 0; i < r; ++i) t(i, j) = vec(i, src) / std::sqrt(l);
+    }
+    return t;
+}
+
+// gram_orthonormalize (range_finder.hpp:48-84) on the stacked row blocks of z
+// (block_rows[s] rows each): Gram = sum_s Z_s^T Z_s in block order, U = Z T.
+inline Mat gram_orthonormalize(const Mat& z, const std::vector<Index>& block_rows, std::vector<double>* spectrum) {
+    require(!block_rows.empty(), "gram_orthonormalize: no blocks");
+    const Index r = z.cols;
+    Mat gram(r, r);
+    Index at = 0;
+    for (Index len : block_rows) {
+        for (Index j = 0; j < r; ++j)
+            for (Index i = 0; i < r; ++i) {
+                double acc = 0.0;
+                for (Index k = 0; k < len; ++k) acc += z(at + k, i) * z(at + k, j);
+                gram(i, j) += acc;
+            }
+        at += len;
+    }
+    require(at == z.rows, "gram_orthonormalize: block rows do not cover Z");
+    const Mat t = gram_ortho_transform(gram, spectrum);
+    Mat u(z.rows, t.cols);
+    gemm(false, false, z.rows, t.cols, r, 1.0, z.data(), z.rows, t.data(), t.rows, 0.0, u.data(), u.rows);
+    return u;
+}
+
+// U_n of one distributed compression step (dist.hpp:688-723): Z summed over blocks,
+// Gram-eig transform, U = Z T; no sign rule.
+inline Mat gram_basis(const Mat& z) { return gram_orthonormalize(z, {z.rows}, nullptr); }
+
 struct Tucker {
     Tensor core;
     std::vector<Mat> factors;
 };
 
 // rand_tucker (Alg. 2, tucker.hpp:108-130)
-inline Tucker rand_tucker(const Tensor& y, const std::vector<Index>& ranks, Index p, const Seed& seed) {
+// gram = true: the distributed protocol's orthonormalisation (dist_rand_tucker,
+// dist.hpp:852-879: Gram-eig basis, no sign rule) on the assembled tensor.
+inline Tucker rand_tucker(const Tensor& y, const std::vector<Index>& ranks, Index p, const Seed& seed,
+                          bool gram = false) {
     require(static_cast<Index>(ranks.size()) == y.order(), "rand_tucker: one rank per mode required");
     require(p >= 0, "rand_tucker: oversampling must be nonnegative");
     Tucker m;
@@ -454,8 +599,13 @@ inline Tucker rand_tucker(const Tensor& y, const std::vector<Index>& ranks, Inde
         const Index rt = std::min(ranks[static_cast<size_t>(n)] + p, cur.dim(n));
         const Index width = cur.size() / cur.dim(n);
         const Mat omega = gaussian_matrix(width, rt, alg2_omega_seed(seed, n));
-        Mat u = orthonormal_basis(unfold_times(cur, n, omega));
-        fix_column_signs(u);
+        Mat u;
+        if (gram) {
+            u = gram_basis(unfold_times(cur, n, omega));
+        } else {
+            u = orthonormal_basis(unfold_times(cur, n, omega));
+            fix_column_signs(u);
+        }
         cur = ttm(cur, transpose(u), n);
         m.factors[static_cast<size_t>(n)] = std::move(u);
     }
@@ -466,7 +616,7 @@ inline Tucker rand_tucker(const Tensor& y, const std::vector<Index>& ranks, Inde
 // rand_tucker_2i (Alg. 3, tucker.hpp:136-169). `z_out`, if given, receives the
 // 2N sketches Z (diagnostics for the parity tests).
 inline Tucker rand_tucker_2i(const Tensor& y, const std::vector<Index>& ranks, Index p,
-                             const Seed& seed, std::vector<Mat>* z_out = nullptr) {
+                             const Seed& seed, std::vector<Mat>* z_out = nullptr, bool gram = false) {
     require(static_cast<Index>(ranks.size()) == y.order(), "rand_tucker_2i: one rank per mode required");
     require(p >= 0, "rand_tucker_2i: oversampling must be nonnegative");
     const Index order = y.order();
@@ -483,8 +633,13 @@ inline Tucker rand_tucker_2i(const Tensor& y, const std::vector<Index>& ranks, I
             const Mat omega = gaussian_matrix(width, rt, alg3_omega_seed(seed, pass, n));
             Mat z = unfold_times(x, n, omega);
             if (z_out) z_out->push_back(z);
-            Mat u = orthonormal_basis(z);
-            fix_column_signs(u);
+            Mat u;
+            if (gram) {  // dist_rand_tucker_2i (dist.hpp:884-936): Gram-eig basis, no sign rule
+                u = gram_basis(z);
+            } else {
+                u = orthonormal_basis(z);
+                fix_column_signs(u);
+            }
             factors[static_cast<size_t>(n)] = std::move(u);
         }
     }
@@ -976,6 +1131,37 @@ int tko_orthonormal_basis(int64_t rows, int64_t cols, const double* z, double* q
         }
     })
 }
+int tko_sym_eig(int64_t n, const double* a, double* evals, double* evecs) {
+    TKO_TRY({
+        std::vector<double> ev;
+        Mat v;
+        sym_eig(to_mat(n, n, a), ev, v);
+        std::memcpy(evals, ev.data(), sizeof(double) * ev.size());
+        std::memcpy(evecs, v.data(), sizeof(double) * v.d.size());
+    })
+}
+int tko_gram_ortho_transform(int64_t n, const double* gram, double* transform, double* spectrum, int64_t* kept) {
+    TKO_TRY({
+        std::vector<double> sp;
+        Mat t = gram_ortho_transform(to_mat(n, n, gram), &sp);
+        *kept = t.cols;
+        std::memcpy(transform, t.data(), sizeof(double) * t.d.size());
+        std::memcpy(spectrum, sp.data(), sizeof(double) * sp.size());
+    })
+}
+int tko_gram_orthonormalize(int64_t nblocks, const int64_t* block_rows, int64_t cols, const double* z, double* u,
+                            double* spectrum, int64_t* kept) {
+    TKO_TRY({
+        std::vector<Index> br(block_rows, block_rows + nblocks);
+        Index rows = 0;
+        for (Index b : br) rows += b;
+        std::vector<double> sp;
+        Mat q = gram_orthonormalize(to_mat(rows, cols, z), br, &sp);
+        *kept = q.cols;
+        std::memcpy(u, q.data(), sizeof(double) * q.d.size());
+        std::memcpy(spectrum, sp.data(), sizeof(double) * sp.size());
+    })
+}
 int tko_fix_column_signs(int64_t rows, int64_t cols, double* u) {
     TKO_TRY({
         Mat m = to_mat(rows, cols, u);
@@ -995,6 +1181,19 @@ int tko_rand_tucker_2i(const int64_t* shape, int64_t order, const double* y, con
         if (z_out)
             for (size_t i = 0; i < zs.size(); ++i)
                 std::memcpy(z_out[i], zs[i].data(), sizeof(double) * zs[i].d.size());
+    })
+}
+// The reference's distributed algorithms (dist.hpp:852-936) on the assembled tensor:
+// alg 2 = dist_rand_tucker, alg 3 = dist_rand_tucker_2i (Gram-eig orthonormalisation).
+int tko_dist_rand_tucker_gram(int alg, const int64_t* shape, int64_t order, const double* y, const int64_t* ranks,
+                              int64_t p, uint64_t root, uint64_t stream, double* core, int64_t* core_shape,
+                              double** factors, int64_t* cols) {
+    TKO_TRY({
+        const Tensor t = to_tensor(shape, order, y);
+        const Seed sd{root, stream};
+        Tucker m = alg == 2 ? rand_tucker(t, to_shape(ranks, order), p, sd, true)
+                            : rand_tucker_2i(t, to_shape(ranks, order), p, sd, nullptr, true);
+        write_model(m, core, core_shape, factors, cols);
     })
 }
 int tko_rand_tucker(const int64_t* shape, int64_t order, const double* y, const int64_t* ranks,

@@ -6,6 +6,7 @@ hand-written CUDA kernels behind the C-ABI of include/tenkit_b200.h
 """
 from .tenkit import (SeedSpec, DenseTensor, TuckerModel, StopRule, ConstraintSpec, ConstraintKind,  # noqa: F401
                      Context, rand_tucker_2i, rand_tucker, ttm, ttm_all, unfold_times, orthonormal_basis,
+                     gram_orthonormalize, gram_ortho_transform,
                      gaussian_matrix, ffcp, CpModel, model_fit, TenkitError)
 
 __version__ = "0.1.0"

@@ -56,6 +56,9 @@ SIGNATURES = {
     "tk_context_set_comm": (C.c_int, [C.c_void_p, C.POINTER(tk_comm)]),
     "tk_context_synchronize": (C.c_int, [C.c_void_p]),
     "tk_context_set_ttm_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "tk_context_set_orthonormalizer": (C.c_int, [C.c_void_p, C.c_int]),
+    "tk_gram_orthonormalize": (C.c_int, [C.c_void_p, I64, I64, PD, PD, PD, PI64]),
+    "tk_gram_ortho_transform": (C.c_int, [C.c_void_p, I64, PD, PD, PD, PI64]),
     "tk_rand_tucker_2i": (C.c_int, [C.c_void_p, C.c_int, I64, PI64, C.c_void_p, C.c_int, PI64, I64, U64, U64,
                                     C.POINTER(tk_tucker_opts), C.POINTER(tk_tucker_out), C.POINTER(tk_tucker_stats)]),
     "tk_rand_tucker": (C.c_int, [C.c_void_p, C.c_int, I64, PI64, C.c_void_p, C.c_int, PI64, I64, U64, U64,

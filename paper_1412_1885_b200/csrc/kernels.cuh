@@ -122,6 +122,18 @@ void launch_cast2d(const S* in, int64_t ldi, D* out, int64_t ldo, int64_t rows, 
 // order s = 0 .. nparts-1 while loading (launch_sketch_partials' layout).
 void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up,
                               int up_dtype, int* rank_dev, double* diag, cudaStream_t s, int nparts = 0);
+// Gram-path orthonormalisation of the distributed protocol (gram.cu; range_finder.hpp:43-105,
+// dist.hpp:688-723): U = Z T with T = V / sqrt(lambda) (descending, eigenvalues <= 1e-12 top
+// dropped), no sign rule. Same outputs as launch_orthonormal_basis (u rows x ucap, ld = rows,
+// columns >= kept zeroed; packed copy; kept -> *rank_dev); spectrum (ncols, may be null).
+// work: gram_work_elems(rows, ncols) doubles. Returns the number of launches.
+int64_t gram_work_elems(int64_t rows, int ncols);
+int launch_gram_orthonormal(const double* z, int64_t rows, int64_t ldz, int ncols, double* u, int ucap, void* up,
+                            int up_dtype, int* rank_dev, double* spectrum, double* work, cudaStream_t s);
+// gram_ortho_transform (range_finder.hpp:86-105) of an n x n Gram matrix: transform (n x n,
+// columns >= kept zero), spectrum (n), kept -> *rank_dev.
+void launch_gram_ortho_transform(const double* gram, int n, double* transform, double* spectrum, int* rank_dev,
+                                 cudaStream_t s);
 // Largest Z (rows) the cluster QR can hold for `ncols` columns.
 int64_t qr_max_rows(int ncols);
 

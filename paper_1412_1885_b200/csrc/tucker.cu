@@ -30,6 +30,7 @@ struct tk_context {
     cudaStream_t stream = nullptr;
     bool has_comm = false;
     int ttm_path = 0;  // 0 auto (tcgen05 for fp32 Y streams), 1 FFMA only, 2 tcgen05 whenever supported
+    int ortho = TK_ORTHO_COLPIV;  // range-step basis: ColPiv QR + sign rule, or the dist protocol's Gram-eig
     tk_comm comm{};
     std::map<std::string, std::pair<void*, size_t>> bufs;
     int* rank_host = nullptr;  // pinned
@@ -474,7 +475,7 @@ struct TuckerRun {
         if (ldims[n] != In) {  // this rank's rows of Z, the others zero (summed over ranks)
             TK_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * In * rn, s));
             sketch(x, xd, xp, n, omp, rn, z + off[n], In);
-        } else if (!ranks_sum && qr_fuse()) {  // the QR sums the split-K partials while loading Z
+        } else if (!ranks_sum && qr_fuse() && ctx->ortho != TK_ORTHO_GRAM) {  // the QR sums the split-K partials while loading Z
             const int k = pos_of(xp, n);
             const int64_t B = prod(std::vector<int64_t>(xd.begin(), xd.begin() + k));
             const int64_t A = prod(std::vector<int64_t>(xd.begin() + k + 1, xd.end()));
@@ -489,10 +490,16 @@ struct TuckerRun {
         if (!nparts) allreduce(z, In * rn);
         if (qr_event) TK_CUDA(cudaEventRecord(qr_event, s));
         ph_begin(3);
-        launch_orthonormal_basis(z, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64, rank_dev + step,
-                                 nullptr, s, nparts);
+        if (ctx->ortho == TK_ORTHO_GRAM) {
+            double* gw = static_cast<double*>(ctx->buf("gram_work", sizeof(double) * gram_work_elems(In, rn)));
+            launches += launch_gram_orthonormal(z, In, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64,
+                                                rank_dev + step, nullptr, gw, s);
+        } else {
+            launch_orthonormal_basis(z, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64, rank_dev + step,
+                                     nullptr, s, nparts);
+            ++launches;
+        }
         ph_end();
-        ++launches;
         if (sync) sync_rank(n, step);
     }
 
@@ -737,8 +744,14 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
         r.allreduce(z, gd[n] * rt);  // partial sketches summed over ranks (no-op on one rank)
         U[n] = static_cast<double*>(ctx->buf("U" + std::to_string(n), sizeof(double) * gd[n] * rt));
         T* up = static_cast<T*>(ctx->buf("Up" + std::to_string(n), sizeof(T) * gd[n] * pack_stride(rt)));
-        launch_orthonormal_basis(z, gd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64, r.rank_dev + n, nullptr, s);
-        ++r.launches;
+        if (ctx->ortho == TK_ORTHO_GRAM) {
+            double* gw = static_cast<double*>(ctx->buf("gram_work", sizeof(double) * gram_work_elems(gd[n], rt)));
+            r.launches += launch_gram_orthonormal(z, gd[n], gd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64,
+                                                  r.rank_dev + n, nullptr, gw, s);
+        } else {
+            launch_orthonormal_basis(z, gd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64, r.rank_dev + n, nullptr, s);
+            ++r.launches;
+        }
         TK_CUDA(cudaMemcpyAsync(ctx->rank_host, r.rank_dev + n, sizeof(int), cudaMemcpyDeviceToHost, s));
         TK_CUDA(cudaStreamSynchronize(s));
         const int rank = *ctx->rank_host;
@@ -816,7 +829,7 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
     std::string key = std::to_string(sizeof(T)) + "|" + std::to_string(reinterpret_cast<uintptr_t>(ydev)) + "|" +
                       std::to_string(p) + "|" + std::to_string(seed.root) + "|" + std::to_string(seed.stream) + "|" +
                       std::to_string(opt.explicit_core_pass) + std::to_string(opt.overlap) + std::to_string(opt.one_pass_per_step) +
-                      std::to_string(opt.time_kernels) + "|" + std::to_string(ctx->ttm_path);
+                      std::to_string(opt.time_kernels) + "|" + std::to_string(ctx->ttm_path) + "|" + std::to_string(ctx->ortho);
     for (int64_t n = 0; n < order; ++n) key += "|" + std::to_string(ld[n]) + "x" + std::to_string(rk[n]);
     auto& g = ctx->g2i;
     if (g.key != key || (g.exec && g.buf_gen != ctx->buf_gen)) {
@@ -1016,6 +1029,15 @@ int tk_context_set_ttm_path(tk_context* ctx, int path) {
     });
 }
 
+int tk_context_set_orthonormalizer(tk_context* ctx, int kind) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(kind == TK_ORTHO_COLPIV || kind == TK_ORTHO_GRAM,
+                "orthonormalizer must be TK_ORTHO_COLPIV (0) or TK_ORTHO_GRAM (1)");
+        ctx->ortho = kind;
+    });
+}
+
 int tk_context_synchronize(tk_context* ctx) {
     return guarded([&] {
         check_ctx(ctx);
@@ -1169,6 +1191,37 @@ int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const doub
         TK_CUDA(cudaMemcpyAsync(ctx->rank_host, rd, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         TK_CUDA(cudaStreamSynchronize(ctx->stream));
         *rank = *ctx->rank_host;
+    });
+}
+
+int tk_gram_orthonormalize(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* u, double* spectrum,
+                           int64_t* kept) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(rows >= 1 && cols >= 1, "gram_orthonormalize: no blocks");
+        require(cols <= kMaxRank, "gram_orthonormalize: column count must be <= 64 on the device path");
+        int* rd = static_cast<int*>(ctx->buf("qr_rank", sizeof(int)));
+        double* gw = static_cast<double*>(ctx->buf("gram_work", sizeof(double) * gram_work_elems(rows, int(cols))));
+        launch_gram_orthonormal(z, rows, rows, static_cast<int>(cols), u, static_cast<int>(cols), nullptr, kF64, rd,
+                                spectrum, gw, ctx->stream);
+        TK_CUDA(cudaMemcpyAsync(ctx->rank_host, rd, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+        *kept = *ctx->rank_host;
+        require(*kept >= 1, "gram_orthonormalize: all blocks are zero");
+    });
+}
+
+int tk_gram_ortho_transform(tk_context* ctx, int64_t n, const double* gram, double* transform, double* spectrum,
+                            int64_t* kept) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(n >= 1 && n <= kMaxRank, "gram_ortho_transform: size must be in [1, 64] on the device path");
+        int* rd = static_cast<int*>(ctx->buf("qr_rank", sizeof(int)));
+        launch_gram_ortho_transform(gram, static_cast<int>(n), transform, spectrum, rd, ctx->stream);
+        TK_CUDA(cudaMemcpyAsync(ctx->rank_host, rd, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+        *kept = *ctx->rank_host;
+        require(*kept >= 1, "gram_ortho_transform: zero Gram matrix");
     });
 }
 

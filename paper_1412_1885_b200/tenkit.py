@@ -30,6 +30,7 @@ from ._lib import TenkitError, TenkitCudaError  # noqa: F401
 
 __all__ = ["SeedSpec", "DenseTensor", "TuckerModel", "StopRule", "ConstraintSpec", "ConstraintKind", "Context",
            "rand_tucker_2i", "rand_tucker", "ttm", "ttm_all", "unfold_times", "orthonormal_basis",
+           "gram_orthonormalize", "gram_ortho_transform",
            "gaussian_matrix", "ffcp", "CpModel", "model_fit", "TenkitError"]
 
 
@@ -288,13 +289,21 @@ def _tucker_call(fn_name, y, ranks, oversample, seed, context, out, opts=None):
     st = _lib.tk_tucker_stats()
     args = [ctx.handle, _dtype_code(y.data), len(y.shape), _i64arr(y.shape), _ptr(y.data), 1 if y.on_device else 0,
             _i64arr(ranks), int(oversample), int(seed.root), int(seed.stream)]
-    if fn_name == "tk_rand_tucker_2i":
-        oo = _lib.tk_tucker_opts(int(getattr(opts, "explicit_core_pass", 0)), int(getattr(opts, "sync_ranks", 1)),
-                                 int(getattr(opts, "time_kernels", 0)), int(getattr(opts, "overlap", 1)),
-                                 int(getattr(opts, "one_pass_per_step", 0)))
-        rc = getattr(ctx.lib, fn_name)(*args, C.byref(oo), C.byref(o), C.byref(st))
-    else:
-        rc = getattr(ctx.lib, fn_name)(*args, C.byref(o), C.byref(st))
+    ortho = getattr(opts, "orthonormalizer", "colpiv")
+    if ortho not in _ORTHO:
+        raise TenkitError("tenkit: orthonormalizer must be 'colpiv' or 'gram'")
+    _lib.check(ctx.lib.tk_context_set_orthonormalizer(ctx.handle, _ORTHO[ortho]))
+    try:
+        if fn_name == "tk_rand_tucker_2i":
+            oo = _lib.tk_tucker_opts(int(getattr(opts, "explicit_core_pass", 0)), int(getattr(opts, "sync_ranks", 1)),
+                                     int(getattr(opts, "time_kernels", 0)), int(getattr(opts, "overlap", 1)),
+                                     int(getattr(opts, "one_pass_per_step", 0)))
+            rc = getattr(ctx.lib, fn_name)(*args, C.byref(oo), C.byref(o), C.byref(st))
+        else:
+            rc = getattr(ctx.lib, fn_name)(*args, C.byref(o), C.byref(st))
+    finally:
+        if ortho != "colpiv":
+            ctx.lib.tk_context_set_orthonormalizer(ctx.handle, 0)
     _lib.check(rc)
     cshape = tuple(int(o.core_shape[n]) for n in range(y.order))
     cols = [int(o.factor_cols[n]) for n in range(y.order)]
@@ -309,6 +318,12 @@ def _tucker_call(fn_name, y, ranks, oversample, seed, context, out, opts=None):
     return TuckerModel(g, fs, cshape, stats)
 
 
+# Basis of each range step: 'colpiv' = orthonormal_basis + fix_column_signs (single-node
+# semantics, range_finder.hpp:18-29, tucker.hpp:39-45); 'gram' = the reference's distributed
+# protocol (dist_compress_mode, dist.hpp:688-723: Gram-eig transform, U = Z T, no sign rule).
+_ORTHO = {"colpiv": 0, "gram": 1}
+
+
 @dataclass
 class TuckerOptions:
     explicit_core_pass: int = 0
@@ -318,27 +333,31 @@ class TuckerOptions:
     overlap: int = 1
     _global_dims: tuple = ()
     one_pass_per_step: int = 0
+    orthonormalizer: str = "colpiv"
 
 
 def rand_tucker_2i(y, ranks, oversample: int, seed, *, explicit_core_pass: bool = False, sync_ranks: bool = True,
                    context: Context | None = None, out: str | None = None, global_last_dim: int = 0,
                    time_kernels: bool = False, overlap: bool = True, global_dims=(),
-                   one_pass_per_step: bool = False) -> TuckerModel:
+                   one_pass_per_step: bool = False, orthonormalizer: str = "colpiv") -> TuckerModel:
     """Alg. 3 (tucker.hpp:136-169) on the B200. `y`: numpy array (host; copied in) or a
     device DenseTensor. Returns a host (numpy) model for host input, device otherwise,
     unless out='host'/'device'. global_dims / global_last_dim: with a comm hook installed,
     y is this rank's block of a tensor of these global extents (dist.py). one_pass_per_step:
-    stream Y once per range step like the reference (default: consecutive steps share a pass)."""
+    stream Y once per range step like the reference (default: consecutive steps share a pass).
+    orthonormalizer='gram': the distributed protocol's basis (dist_rand_tucker_2i numerics)."""
     opts = TuckerOptions(int(explicit_core_pass), int(sync_ranks), int(global_last_dim), int(time_kernels),
-                         int(overlap), tuple(int(d) for d in global_dims), int(one_pass_per_step))
+                         int(overlap), tuple(int(d) for d in global_dims), int(one_pass_per_step), orthonormalizer)
     return _tucker_call("tk_rand_tucker_2i", y, ranks, oversample, seed, context, out, opts)
 
 
 def rand_tucker(y, ranks, oversample: int, seed, *, context: Context | None = None, out: str | None = None,
-                global_last_dim: int = 0, global_dims=()) -> TuckerModel:
+                global_last_dim: int = 0, global_dims=(), orthonormalizer: str = "colpiv") -> TuckerModel:
     """Alg. 2 (tucker.hpp:108-130) on the B200. global_dims / global_last_dim: with a comm
-    hook installed, y is this rank's block of a tensor of these global extents (dist.py)."""
-    opts = TuckerOptions(_global_last_dim=int(global_last_dim), _global_dims=tuple(int(d) for d in global_dims))
+    hook installed, y is this rank's block of a tensor of these global extents (dist.py).
+    orthonormalizer='gram': the distributed protocol's basis (dist_rand_tucker numerics)."""
+    opts = TuckerOptions(_global_last_dim=int(global_last_dim), _global_dims=tuple(int(d) for d in global_dims),
+                         orthonormalizer=orthonormalizer)
     return _tucker_call("tk_rand_tucker", y, ranks, oversample, seed, context, out, opts)
 
 
@@ -430,6 +449,47 @@ def orthonormal_basis(z, *, with_diag: bool = False, context=None):
     if with_diag:
         return u, diag.cpu().numpy()[: min(rows, cols)]
     return u
+
+
+def gram_orthonormalize(z_blocks, *, context=None):
+    """gram_orthonormalize (range_finder.hpp:48-84): the row blocks' summed Gram matrix is
+    eigendecomposed on the device; returns (stacked U with orthonormal columns, spectrum
+    descending). Eigenvector signs are the device eigensolver's (the reference leaves them
+    to Eigen's)."""
+    import torch
+    blocks = [np.asarray(b, dtype=np.float64) for b in z_blocks]
+    if not blocks:
+        raise TenkitError("tenkit: gram_orthonormalize: no blocks")
+    r = blocks[0].shape[1]
+    if any(b.ndim != 2 or b.shape[1] != r for b in blocks):
+        raise TenkitError("tenkit: gram_orthonormalize: column-count mismatch")
+    z = np.vstack(blocks)
+    rows = z.shape[0]
+    ctx = _ctx(context)
+    zd = _to_dev(z, torch.float64)
+    u = torch.zeros(rows * max(r, 1), dtype=torch.float64, device="cuda")
+    sp = torch.zeros(max(r, 1), dtype=torch.float64, device="cuda")
+    kept = C.c_int64()
+    _lib.check(ctx.lib.tk_gram_orthonormalize(ctx.handle, rows, r, _dptr(zd), _dptr(u), _dptr(sp), C.byref(kept)))
+    k = kept.value
+    return u.cpu().numpy()[: rows * k].reshape((rows, k), order="F"), sp.cpu().numpy()[:k]
+
+
+def gram_ortho_transform(gram, *, context=None):
+    """gram_ortho_transform (range_finder.hpp:86-105) -> (transform n x kept, spectrum)."""
+    import torch
+    g = np.asarray(gram, dtype=np.float64)
+    if g.ndim != 2 or g.shape[0] != g.shape[1]:
+        raise TenkitError("tenkit: gram_ortho_transform: square Gram matrix required")
+    n = g.shape[0]
+    ctx = _ctx(context)
+    gd = _to_dev(g, torch.float64)
+    t = torch.zeros(n * n, dtype=torch.float64, device="cuda")
+    sp = torch.zeros(n, dtype=torch.float64, device="cuda")
+    kept = C.c_int64()
+    _lib.check(ctx.lib.tk_gram_ortho_transform(ctx.handle, n, _dptr(gd), _dptr(t), _dptr(sp), C.byref(kept)))
+    k = kept.value
+    return t.cpu().numpy()[: n * k].reshape((n, k), order="F"), sp.cpu().numpy()[:k]
 
 
 def gaussian_matrix(rows: int, cols: int, seed, *, context=None) -> np.ndarray:

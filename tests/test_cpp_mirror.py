@@ -34,8 +34,10 @@ def parse(out):
             d["fit"].append(float(v[0]))
         elif k in ("core_sq", "y_sq"):
             d[k] = float(v[0])
-        elif k == "iterations":
+        elif k in ("iterations", "gram_kept"):
             d[k] = int(v[0])
+        elif k == "gram_defect":
+            d[k] = float(v[0])
     return d
 
 
@@ -66,3 +68,5 @@ def test_cpp_mirror_matches_oracle(demo, O):
     _, trace, its = O.ffcp(g, us, 3, O.NONE, 0.0, 30, 0.0, (8, 0))
     assert got["iterations"] == its
     np.testing.assert_allclose(got["fit"], trace, rtol=0, atol=1e-7)
+    # gram_orthonormalize of a 15 + 25 row split (test_range_finder.cpp:66-77)
+    assert got["gram_kept"] == 5 and got["gram_defect"] < 1e-10

@@ -325,7 +325,7 @@ def run_b200(args, cfg):
     hbm = float(pk.get("hbm_gbs", 6650.0))
     kern_ms = stream_ms / max(stream_launches, 1)
     achieved = ybytes / (kern_ms * 1e-3) / 1e9
-    traffic = _ncu_traffic()
+    traffic = _ncu_traffic(args.config)
 
     # ---- sanity on the bench workload: fit of the Tucker model to Y from the Gram identity
     # ||Y - G x U||^2 = ||Y||^2 - ||G||^2 (orthonormal U); global norms summed over ranks
@@ -430,11 +430,13 @@ def run_b200(args, cfg):
         dist.destroy_process_group()
 
 
-def _ncu_traffic():
-    """DRAM bytes per launch of the TTM kernel from the committed ncu capture, if any."""
+def _ncu_traffic(workload):
+    """DRAM bytes per launch of the TTM kernel from the committed ncu capture of this
+    workload's Y passes (profiles/ttm_traffic.json), else None."""
     p = os.path.join(ROOT, "profiles", "ttm_traffic.json")
     try:
-        return json.load(open(p)).get("dram_bytes_per_launch")
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch") if d.get("workload") == workload else None
     except Exception:
         return None
 

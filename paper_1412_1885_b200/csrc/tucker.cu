@@ -281,8 +281,13 @@ struct TuckerRun {
         for (int m = static_cast<int>(order) - 1; m >= 0; --m) {
             if (mask & (1u << m)) continue;
             // small tensors (latency-bound passes): any mode can lead (FFMA kernels)
+            static const bool no_km_leader = [] {  // A/B knob: mode 0 never leads a shared pass
+                const char* e = std::getenv("TENKIT_NO_KM_LEADER");
+                return e && e[0] == '1';
+            }();
             const bool capable = prod(std::vector<int64_t>(ldims.begin(), ldims.begin() + m)) >= 256 ||
-                                 (m == 0 && km_stream_ok()) || prod(ldims) * int64_t(sizeof(T)) <= (int64_t(256) << 20);
+                                 (m == 0 && !no_km_leader && km_stream_ok()) ||
+                                 prod(ldims) * int64_t(sizeof(T)) <= (int64_t(256) << 20);
             if (!capable) continue;
             if (m != avoid) return m;
             fallback = m;

@@ -10,6 +10,7 @@ shared seed on every rank and never communicated (paper §IV-B, dist.hpp:525-537
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 
 from . import _lib
@@ -117,6 +118,51 @@ def default_grid(order: int, world: int):
     return [1] * (order - 1) + [world]
 
 
+class MessageLog:
+    """Audit log of the exchanges a distributed decomposition made — the reference's
+    MessageLog (dist.hpp:277-320): records in delivery order with monotone sequence numbers,
+    count(kind[, mode]) and one-JSON-object-per-line output (write_ndjson).
+
+    The B200 protocol's exchanges are all-reduces (no client, no leaders): one
+    "partial_product" record (tag "z", rows = I_n, cols = r~_n) per range step and one
+    "core_block" record (tag "core", rows = core elements, cols = 1) per call, each with
+    source = this rank's 1-based worker id and dest = -1 (every rank). The reference's
+    seed_broadcast / factor_block messages have no counterpart: the seed and Omega are
+    regenerated on every rank and the basis is computed redundantly (replicated QR / Gram-eig)."""
+
+    KINDS = ("partial_product", "seed_broadcast", "factor_block", "core_block")
+
+    Record = collections.namedtuple("Record", "seq kind source dest mode tag rows cols")
+
+    def __init__(self):
+        self._records = []
+
+    def append(self, kind: str, source: int, dest: int, mode: int, tag: str, rows: int, cols: int):
+        if kind not in self.KINDS:
+            raise _lib.TenkitError(f"tenkit: message log: unknown kind {kind}")
+        self._records.append(MessageLog.Record(len(self._records), kind, int(source), int(dest), int(mode), tag,
+                                               int(rows), int(cols)))
+
+    def records(self):
+        return list(self._records)
+
+    def count(self, kind: str, mode: int | None = None) -> int:
+        return sum(1 for r in self._records if r.kind == kind and (mode is None or r.mode == mode))
+
+    def write_ndjson(self, f):
+        import json
+        for r in self._records:
+            f.write(json.dumps(r._asdict(), separators=(",", ":")) + "\n")
+
+
+def exchange_plan(alg: str, gdims, ranks, oversample):
+    """The (kind, tag, mode, rows) sequence of the all-reduces one distributed call makes:
+    2N range steps (Alg. 3, modes 0..N-1 twice) or N (Alg. 2), then the core."""
+    order = len(gdims)
+    modes = list(range(order)) * (2 if alg == "2i" else 1)
+    return [("partial_product", "z", n, int(gdims[n])) for n in modes] + [("core_block", "core", -1, 0)]
+
+
 class DistComm:
     """Reduction hook handed to the library: `xbuf` is a device (or, in CPU tests, host)
     float64 buffer; the library writes `count` values and calls back for an all-reduce sum
@@ -141,7 +187,17 @@ class DistComm:
         dev = device if device is not None else ("cuda" if torch.cuda.is_available() else "cpu")
         self.xbuf = torch.zeros(int(capacity), dtype=torch.float64, device=dev)
         self.calls = 0
+        self.log = None  # MessageLog to record into, with self.plan (exchange_plan)
+        self.plan = None
         self._cb = _lib.ALLREDUCE_FN(self._allreduce)
+
+    def _record(self, count: int):
+        if self.log is None or not self.plan:
+            return
+        kind, tag, mode, rows = self.plan[self.calls % len(self.plan)]
+        if rows <= 0 or count % rows:
+            rows = count
+        self.log.append(kind, self.rank + 1, -1, mode, tag, rows, count // rows)
 
     def _allreduce(self, user, count, stream) -> int:
         try:
@@ -156,6 +212,7 @@ class DistComm:
                         dist.all_reduce(self.xbuf[: int(count)], group=self.group)
                 else:
                     dist.all_reduce(self.xbuf[: int(count)], group=self.group)
+            self._record(int(count))
             self.calls += 1
             return 0
         except Exception:  # the library turns a non-zero status into "comm: allreduce failed"
@@ -205,12 +262,16 @@ def _block_args(local_y, global_dims, lo):
     return g, l
 
 
-def _dist_call(fn, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw):
+def _dist_call(fn, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw, alg):
     from .tenkit import Context
     ctx = context or Context.default()
     gdims, blo = _block_args(local_y, global_dims, lo)
     comm = DistComm(blo[-1], gdims[-1], exchange_capacity(gdims, ranks, oversample), group=group,
                     block_lo=blo, global_dims=gdims)
+    log = kw.pop("log", None)
+    if log is not None:
+        comm.log = log
+        comm.plan = exchange_plan(alg, gdims, ranks, oversample)
     ctx.set_comm(comm)
     try:
         return fn(local_y, ranks, oversample, seed, context=ctx, global_dims=gdims, **kw)
@@ -223,18 +284,21 @@ def dist_rand_tucker_2i(local_y, global_dims, lo, ranks, oversample, seed, *, co
     whose block lives on this rank (one process per GPU): `global_dims`/`lo` are the global
     extents and the block's first index per mode (GridPlan.block), or — the slab form — the
     global last-mode size and the slab offset. Every rank returns the same model (replicated
-    QR; the factors equal the single-node rand_tucker_2i's, not a rotation of them)."""
+    QR; the factors equal the single-node rand_tucker_2i's, not a rotation of them).
+    orthonormalizer='gram': the reference's own dist basis (Gram-eig, dist.hpp:688-723).
+    log=MessageLog(): records this rank's exchanges (dist.hpp:277-320)."""
     from .tenkit import rand_tucker_2i
-    return _dist_call(rand_tucker_2i, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw)
+    return _dist_call(rand_tucker_2i, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw, "2i")
 
 
 def dist_rand_tucker(local_y, global_dims, lo, ranks, oversample, seed, *, context=None, group=None, **kw):
     """rand_tucker (Alg. 2, tucker.hpp:108-130; dist_rand_tucker, dist.hpp:852-878) of the
     global tensor whose block lives on this rank: the Omega rows of each unfolding are drawn
     at their global column ids (dist.hpp:496-596), partial sketches and the partial core are
-    summed over ranks, the QR is replicated. Every rank returns the same model."""
+    summed over ranks, the QR is replicated. Every rank returns the same model.
+    orthonormalizer='gram' / log=MessageLog(): as dist_rand_tucker_2i."""
     from .tenkit import rand_tucker
-    return _dist_call(rand_tucker, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw)
+    return _dist_call(rand_tucker, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw, "alg2")
 
 
 def dist_multiply(local_y, global_dims, lo, mode: int, r_tilde: int, seed, *, grid: GridPlan | None = None,

@@ -202,3 +202,73 @@ def test_gloo_world4_block_grid_partials_reduce_to_single_node():
     for rank, errs, calls in res:
         assert calls == 4, errs
         assert max(errs) < 1e-12, errs
+
+
+# ---------------------------------------------------------------- MessageLog (dist.hpp:277-320)
+def test_message_log_records_counts_and_ndjson():
+    """MessageLog mirrors the reference's audit log: monotone seq, count(kind[, mode]), one
+    JSON object per line (test_dist.cpp:186-201, 270-285)."""
+    import io
+    import json
+    from paper_1412_1885_b200.dist import MessageLog, exchange_plan
+    log = MessageLog()
+    plan = exchange_plan("2i", (40, 36, 30), (5, 5, 5), 4)
+    assert [p[2] for p in plan] == [0, 1, 2, 0, 1, 2, -1]
+    for kind, tag, mode, rows in plan:
+        log.append(kind, 1, -1, mode, tag, rows or 729, 9 if rows else 1)
+    assert log.count("partial_product") == 6 and log.count("core_block") == 1
+    assert log.count("partial_product", 1) == 2
+    recs = log.records()
+    assert all(b.seq > a.seq for a, b in zip(recs, recs[1:]))
+    f = io.StringIO()
+    log.write_ndjson(f)
+    lines = f.getvalue().splitlines()
+    assert len(lines) == len(recs)
+    d = json.loads(lines[0])
+    assert d == {"seq": 0, "kind": "partial_product", "source": 1, "dest": -1, "mode": 0, "tag": "z", "rows": 40,
+                 "cols": 9}
+    with pytest.raises(ValueError):
+        log.append("bogus", 1, -1, 0, "z", 1, 1)
+    assert [p[2] for p in exchange_plan("alg2", (8, 8, 8, 8), (2, 2, 2, 2), 1)] == [0, 1, 2, 3, -1]
+
+
+def _log_worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1412_1885_b200.dist import DistComm, MessageLog, exchange_plan
+        dims, ranks, p = (12, 10, 8), (3, 3, 3), 2
+        comm = DistComm(0, dims[-1], 256, device="cpu")
+        comm.log, comm.plan = MessageLog(), exchange_plan("alg2", dims, ranks, p)
+        for n in range(3):  # the call sequence of one Alg. 2 decomposition: Z_0..Z_2, core
+            comm.xbuf[: dims[n] * 5] = float(rank + 1)
+            comm.allreduce(dims[n] * 5)
+            assert float(comm.xbuf[0]) == 3.0
+        comm.allreduce(125)
+        q.put((rank, [tuple(r) for r in comm.log.records()]))
+        dist.destroy_process_group()
+    except Exception as e:
+        import traceback
+        q.put((rank, repr(e) + traceback.format_exc()))
+
+
+def test_gloo_world2_exchanges_are_logged():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_log_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=180) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank in (0, 1):
+        recs = res[rank]
+        assert isinstance(recs, list), recs
+        assert [(r[1], r[2], r[4], r[5], r[6], r[7]) for r in recs] == [
+            ("partial_product", rank + 1, 0, "z", 12, 5), ("partial_product", rank + 1, 1, "z", 10, 5),
+            ("partial_product", rank + 1, 2, "z", 8, 5), ("core_block", rank + 1, -1, "core", 125, 1)]

@@ -171,17 +171,19 @@ def _worker(rank, world, port, grid, alg, q):
         torch.cuda.set_device(0)
         from oracle import pyoracle as O
         import paper_1412_1885_b200 as P
-        from paper_1412_1885_b200.dist import GridPlan, dist_rand_tucker, dist_rand_tucker_2i
+        from paper_1412_1885_b200.dist import GridPlan, MessageLog, dist_rand_tucker, dist_rand_tucker_2i
         O.build()
         y = _tensor(O, BDIMS, (5, 5, 5), (81, 0))
+        log = MessageLog()
         plan = GridPlan.even(BDIMS, grid)
         lo, _ = plan.block(rank)
         ctx = P.Context.default()
         ctx.bind_torch_stream()
         yd = P.DenseTensor.from_numpy(plan.local(y, rank)).cuda()
         fn = dist_rand_tucker_2i if alg == "2i" else dist_rand_tucker
-        m = fn(yd, BDIMS, lo, RANKS, 4, (82, 0), context=ctx, orthonormalizer="gram").to_host()
-        q.put((rank, m.core, m.factors))
+        m = fn(yd, BDIMS, lo, RANKS, 4, (82, 0), context=ctx, orthonormalizer="gram", log=log).to_host()
+        counts = [log.count("partial_product", n) for n in range(3)] + [log.count("core_block")]
+        q.put((rank, m.core, (m.factors, counts, [(r.rows, r.cols) for r in log.records()])))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - reported by the parent
@@ -204,8 +206,13 @@ def test_block_grid_gram_protocol_matches_oracle(P, O, alg, grid):
         p.start()
     res = {}
     for _ in range(world):
-        r, core, fac = q.get(timeout=600)
-        assert fac is not None, core
+        r, core, extra = q.get(timeout=600)
+        assert extra is not None, core
+        fac, counts, shapes = extra
+        # the exchange audit (MessageLog, dist.hpp:277-320): one Z all-reduce per range step, one core
+        steps = 2 if alg == "2i" else 1
+        assert counts == [steps, steps, steps, 1]
+        assert shapes[-1][0] == int(np.prod(np.shape(core))) and all(c == 9 for _, c in shapes[:-1])
         res[r] = (core, fac)
     for p in procs:
         p.join(timeout=60)

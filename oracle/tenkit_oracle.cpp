@@ -480,7 +480,7 @@ inline void sym_eig(const Mat& a_in, std::vector<double>& evals, Mat& evecs) {
                 cs[k] = 1.0, sn[k] = 0.0;
                 if (q >= n) continue;
                 const double apq = a(p, q), app = a(p, p), aqq = a(q, q);
-                if (std::abs(apq) <= 1e-18 * std::sqrt(std::abs(app * aqq)) || apq == 0.0) continue;
+                if (std::abs(apq) <= 1e-16 * std::sqrt(std::abs(app * aqq)) || apq == 0.0) continue;  // gram.cu skip_rotation
                 const double theta = (aqq - app) / (2.0 * apq);
                 const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
                 cs[k] = 1.0 / std::sqrt(t * t + 1.0);

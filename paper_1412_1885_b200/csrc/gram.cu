@@ -75,6 +75,11 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const double
     }
 }
 
+// Jacobi skip rule (oracle sym_eig): the off-diagonal entry is negligible against the diagonal.
+__device__ __forceinline__ bool skip_rotation(double apq, double app, double aqq) {
+    return apq == 0.0 || fabs(apq) <= 1e-16 * sqrt(fabs(app * aqq));
+}
+
 // One CTA. a/v in shared memory with leading dimension n + 1 (row-access bank spread).
 // tout: n x n (column pos < kept = V[:, eig] / sqrt(lambda), the rest zero); spectrum[pos]
 // for pos < kept, 0 after; *rank_out = kept (0 when the Gram matrix is zero).
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(kEigThreads) gram_eig_kernel(const double* __r
     double* v = a + n * ld;
     __shared__ double cs[kMaxRank / 2], sn[kMaxRank / 2];
     __shared__ int pp[kMaxRank / 2], qq[kMaxRank / 2];
-    __shared__ int rotated[2];
+    __shared__ int rotated[1];
     __shared__ int pos[kMaxRank];
     __shared__ double top_s;
     const int tid = threadIdx.x;
@@ -98,12 +103,22 @@ __global__ void __launch_bounds__(kEigThreads) gram_eig_kernel(const double* __r
         a[i + j * ld] = s;
         v[i + j * ld] = i == j ? 1.0 : 0.0;
     }
-    if (tid < 2) rotated[tid] = 0;
+    if (tid == 0) rotated[0] = 0;
     __syncthreads();
     const int m = n + (n & 1);
     const int np = m / 2;
     for (int sweep = 0; sweep < kJacobiMaxSweeps && n > 1; ++sweep) {
-        const int par = sweep & 1;
+        // A sweep without a rotation leaves A unchanged, so "every pair is below the skip
+        // threshold now" is the oracle's "the last sweep rotated nothing" without running it.
+        for (int e = tid; e < n * n; e += kEigThreads) {
+            const int i = e % n, j = e / n;
+            if (i < j && !skip_rotation(a[i + j * ld], a[i + i * ld], a[j + j * ld])) rotated[0] = 1;
+        }
+        __syncthreads();
+        const bool any = rotated[0] != 0;
+        __syncthreads();
+        if (!any) break;
+        if (tid == 0) rotated[0] = 0;
         for (int r = 0; r < m - 1; ++r) {
             if (tid < np) {  // pair tid of round r (jacobi_round_pairs): L[k], L[m-1-k]
                 const int k = tid;
@@ -114,43 +129,49 @@ __global__ void __launch_bounds__(kEigThreads) gram_eig_kernel(const double* __r
                 double c = 1.0, s = 0.0;
                 if (q < n) {
                     const double apq = a[p + q * ld], app = a[p + p * ld], aqq = a[q + q * ld];
-                    if (!(fabs(apq) <= 1e-18 * sqrt(fabs(app * aqq)) || apq == 0.0)) {
+                    if (!skip_rotation(apq, app, aqq)) {
                         const double theta = (aqq - app) / (2.0 * apq);
                         const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
                         c = 1.0 / sqrt(t * t + 1.0);
                         s = t * c;
-                        rotated[par] = 1;
                     }
                 }
                 cs[k] = c, sn[k] = s, pp[k] = p, qq[k] = q;
             }
             __syncthreads();
-            for (int e = tid; e < np * n; e += kEigThreads) {  // rows: A <- P^T A
-                const int k = e / n, col = e - (e / n) * n;
-                if (sn[k] == 0.0) continue;
-                const int p = pp[k], q = qq[k];
-                const double x = a[p + col * ld], y = a[q + col * ld];
-                a[p + col * ld] = cs[k] * x - sn[k] * y;
-                a[q + col * ld] = sn[k] * x + cs[k] * y;
-            }
-            __syncthreads();
-            for (int e = tid; e < np * n; e += kEigThreads) {  // columns: A <- A P, V <- V P
-                const int k = e / n, i = e - (e / n) * n;
-                if (sn[k] == 0.0) continue;
-                const int p = pp[k], q = qq[k];
-                const double x = a[i + p * ld], y = a[i + q * ld];
-                a[i + p * ld] = cs[k] * x - sn[k] * y;
-                a[i + q * ld] = sn[k] * x + cs[k] * y;
-                const double vx = v[i + p * ld], vy = v[i + q * ld];
-                v[i + p * ld] = cs[k] * vx - sn[k] * vy;
-                v[i + q * ld] = sn[k] * vx + cs[k] * vy;
+            // A <- P^T A P one 2x2 block (row pair k1, column pair k2) per item: the blocks are
+            // disjoint, so rows and columns rotate in one phase; V <- V P likewise.
+            for (int e = tid; e < np * np + np * n; e += kEigThreads) {
+                if (e < np * np) {
+                    const int k1 = e % np, k2 = e / np;
+                    const double c1 = cs[k1], s1 = sn[k1], c2 = cs[k2], s2 = sn[k2];
+                    if (s1 == 0.0 && s2 == 0.0) continue;
+                    const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
+                    const bool hq1 = q1 < n, hq2 = q2 < n;
+                    const double x00 = a[p1 + p2 * ld];
+                    const double x01 = hq2 ? a[p1 + q2 * ld] : 0.0;
+                    const double x10 = hq1 ? a[q1 + p2 * ld] : 0.0;
+                    const double x11 = hq1 && hq2 ? a[q1 + q2 * ld] : 0.0;
+                    // rows (P^T A): r0 = c1 x0 - s1 x1, r1 = s1 x0 + c1 x1
+                    const double y00 = c1 * x00 - s1 * x10, y10 = s1 * x00 + c1 * x10;
+                    const double y01 = c1 * x01 - s1 * x11, y11 = s1 * x01 + c1 * x11;
+                    // columns (A P)
+                    a[p1 + p2 * ld] = c2 * y00 - s2 * y01;
+                    if (hq2) a[p1 + q2 * ld] = s2 * y00 + c2 * y01;
+                    if (hq1) a[q1 + p2 * ld] = c2 * y10 - s2 * y11;
+                    if (hq1 && hq2) a[q1 + q2 * ld] = s2 * y10 + c2 * y11;
+                } else {
+                    const int f = e - np * np;
+                    const int k = f / n, i = f - (f / n) * n;
+                    if (sn[k] == 0.0) continue;
+                    const int p = pp[k], q = qq[k];
+                    const double vx = v[i + p * ld], vy = v[i + q * ld];
+                    v[i + p * ld] = cs[k] * vx - sn[k] * vy;
+                    v[i + q * ld] = sn[k] * vx + cs[k] * vy;
+                }
             }
             __syncthreads();
         }
-        const bool any = rotated[par] != 0;
-        if (tid == 0) rotated[par ^ 1] = 0;
-        __syncthreads();
-        if (!any) break;
     }
     // descending position: the reverse of an ascending stable sort (ties: higher index first)
     if (tid < n) {

@@ -274,6 +274,15 @@ struct TuckerRun {
         return -1;
     }
 
+    // A/B knob: TENKIT_NO_REUSE=1 recomputes every step's first small contraction
+    static bool reuse_first() {
+        static const bool on = [] {
+            const char* e = std::getenv("TENKIT_NO_REUSE");
+            return !(e && e[0] == '1');
+        }();
+        return on;
+    }
+
     // Leader of a shared Y pass for a group of steps whose modes are `mask`: a mode outside the
     // group that can lead a pass (first_mode's rule), preferring one other than `avoid`.
     int leader_mode(uint32_t mask, int avoid) const {
@@ -353,9 +362,21 @@ struct TuckerRun {
         return out;
     }
 
+    // The first contraction of the previous finish() (T x_m U_m^T in "projA"): consecutive steps
+    // of a group that contract the same mode first, with the same factor, out of the same Y pass
+    // reuse it (N = 4: steps (0, 1) both start with x_2 U_2, steps (3, 0') with x_3 U_3').
+    struct FirstCache {
+        int pass = -1, mode = -1, ver = -1;
+        const void* src = nullptr;
+        void* out = nullptr;
+        int64_t P = 0, K = 0, Q = 0;
+    } fc;
+    std::vector<int> fver;  // per mode: bumped whenever U_m is rewritten
+
     // Remaining (small) contractions of every mode except skip and f, descending.
     const T* finish(const T* cur, std::vector<int64_t>& xd, const std::vector<int>& xp, int skip, int f) {
         int which = 0;
+        bool first = true;
         for (int m = static_cast<int>(order) - 1; m >= 0; --m) {
             if (m == skip || m == f) continue;
             const int k = pos_of(xp, m);
@@ -363,8 +384,14 @@ struct TuckerRun {
             const int64_t K = xd[k];
             const int64_t Q = prod(std::vector<int64_t>(xd.begin() + k + 1, xd.end()));
             T* out = static_cast<T*>(ctx->buf(which ? "projB" : "projA", sizeof(T) * P * cols[m] * Q));
+            const int ver = fver.empty() ? 0 : fver[m];
+            const bool hit = first && reuse_first() && fc.pass == passes && fc.mode == m && fc.ver == ver &&
+                             fc.src == cur && fc.out == out && fc.P == P && fc.K == K && fc.Q == Q;
+            if (first) fc = FirstCache{passes, m, ver, cur, out, P, K, Q};
+            else if (!which) fc.pass = -1;  // a later contraction overwrites projA
+            first = false;
             ph_begin(1);
-            if (!stream_ttm(cur, m, out, P, K, Q, false)) ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
+            if (!hit && !stream_ttm(cur, m, out, P, K, Q, false)) ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
             ph_end();
             xd[k] = cols[m];
             cur = out;
@@ -492,6 +519,7 @@ struct TuckerRun {
             sketch(x, xd, xp, n, omp, rn, z, In);
         }
         ph_end();
+        if (!fver.empty()) ++fver[n];  // U_n is rewritten below
         if (!nparts) allreduce(z, In * rn);
         if (qr_event) TK_CUDA(cudaEventRecord(qr_event, s));
         ph_begin(3);
@@ -522,6 +550,8 @@ struct TuckerRun {
         cols.resize(order);
         U.resize(order);
         Up.resize(order);
+        fver.assign(order, 0);
+        fc = FirstCache{};
         for (int n = 0; n < order; ++n) {
             rt[n] = static_cast<int>(std::min<int64_t>(ranks[n] + p, gdims[n]));
             require(rt[n] >= 1, "gaussian_matrix: dimensions must be positive");

@@ -68,7 +68,7 @@ int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int 
 // order s = 0, 1, ... by sketch_reduce_kernel, or by the QR kernel's load: nparts below).
 template <typename T>
 int launch_sketch_partials(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* work,
-                           cudaStream_t s);
+                           cudaStream_t s, int max_splits = 64);
 
 // Materialise the mode-n unfolding of a (B, I, A) view: out[i + (b + a*B)*I] = x[b + i*B + a*B*I]
 template <typename T>

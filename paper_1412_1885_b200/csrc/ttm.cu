@@ -8,6 +8,7 @@
 // contract each tile against the resident factor chunk with fp32 FFMA (fp32-accurate,
 // never TF32/BF16 — SURVEY App. B shows single-pass TF32 flips the sign rule).
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.cuh"
@@ -674,16 +675,27 @@ void launch_gaussian_colmajor(double* out, int64_t rows, int64_t cols, uint64_t 
 }
 
 
-int64_t sketch_work_elems(int64_t I, int rn) { return I * rn * 16; }
+// Split-K factor of the sketch: the kernel is latency-bound per CTA (ncu at cfg 2: 0.35 waves,
+// issue-bound), so K is split until the grid holds ~kSketchCtas CTAs (4 per SM), at most 64
+// splits, at least 64 k per split. (cfg 4: I = 300, K = 8000 -> 42 splits instead of 16.)
+static int sketch_split_cap(int64_t I, int rn) {
+    static const int64_t target = [] {
+        const char* e = std::getenv("TENKIT_SKETCH_CTAS");
+        return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(4 * 148);
+    }();
+    const int64_t tiles = ((I + 31) / 32) * ((rn + 31) / 32);
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (target + tiles - 1) / tiles)));
+}
+
+int64_t sketch_work_elems(int64_t I, int rn) { return I * rn * sketch_split_cap(I, rn); }
 
 template <typename T>
 int launch_sketch_partials(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* work,
-                           cudaStream_t s) {
+                           cudaStream_t s, int max_splits) {
     require(B * A < (int64_t(1) << 31), "unfold_times: unfolding too wide");
     const int K = static_cast<int>(B * A);
     const unsigned gx = static_cast<unsigned>((I + 31) / 32), gy = static_cast<unsigned>((rn + 31) / 32);
-    // split K so the grid covers ~2 waves, at most 16 splits, at least 64 k per split
-    int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, (2 * 148 + gx * gy - 1) / (gx * gy))));
+    int S = std::min(sketch_split_cap(I, rn), std::max(1, max_splits));
     S = std::max(1, std::min(S, (K + 63) / 64));
     const int kchunk = ((K + S - 1) / S + 63) / 64 * 64;
     S = (K + kchunk - 1) / kchunk;
@@ -697,16 +709,16 @@ int launch_sketch_partials(const T* x, int64_t B, int64_t I, int64_t A, const T*
 template <typename T>
 int launch_sketch(const T* x, int64_t B, int64_t I, int64_t A, const T* om, int rn, double* z, int64_t ldz, double* work,
                   cudaStream_t s) {
-    const int S = launch_sketch_partials<T>(x, B, I, A, om, rn, work, s);
+    const int S = launch_sketch_partials<T>(x, B, I, A, om, rn, work, s, 64);
     TK_MAXSMEM((sketch_reduce_kernel));
     sketch_reduce_kernel<<<grid_for(I * rn), 256, 0, s>>>(work, I, rn, S, z, ldz);
     TK_LAUNCH_CHECK();
     return 2;
 }
 template int launch_sketch_partials<float>(const float*, int64_t, int64_t, int64_t, const float*, int, double*,
-                                           cudaStream_t);
+                                           cudaStream_t, int);
 template int launch_sketch_partials<double>(const double*, int64_t, int64_t, int64_t, const double*, int, double*,
-                                            cudaStream_t);
+                                            cudaStream_t, int);
 template int launch_sketch<float>(const float*, int64_t, int64_t, int64_t, const float*, int, double*, int64_t, double*,
                                   cudaStream_t);
 template int launch_sketch<double>(const double*, int64_t, int64_t, int64_t, const double*, int, double*, int64_t, double*,

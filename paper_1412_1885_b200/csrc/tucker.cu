@@ -513,7 +513,7 @@ struct TuckerRun {
             const int64_t A = prod(std::vector<int64_t>(xd.begin() + k + 1, xd.end()));
             z = static_cast<double*>(ctx->buf(work_name == std::string("splitk") ? "sketch_part" : "sketch_part_side",
                                               sizeof(double) * sketch_work_elems(In, rn)));
-            nparts = launch_sketch_partials<T>(x, B, In, A, omp, rn, z, s);
+            nparts = launch_sketch_partials<T>(x, B, In, A, omp, rn, z, s, 16);  // the QR load sums <= 16
             ++launches;
         } else {
             sketch(x, xd, xp, n, omp, rn, z, In);

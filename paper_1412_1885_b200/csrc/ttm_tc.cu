@@ -191,7 +191,7 @@ __device__ __forceinline__ void drain16(uint32_t tl, int j, int rc, int used, fl
 template <int NH, int MT_, bool KM, int OCC = 1>
 __global__ void __launch_bounds__(kTcThreads, OCC)
     ttm_tc_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
-                  int64_t P, int64_t K, int cols, int64_t tiles_p, int tout) {
+                  int64_t P, int64_t K, int cols, int64_t tiles_p, int tout, int64_t ntiles) {
     using C = TcCfg<NH, MT_, OCC>;
     constexpr int MT = C::MT, BM = C::BM;
     extern __shared__ __align__(1024) uint8_t tsm[];
@@ -203,19 +203,17 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
     uint64_t* afull = bars + 2 * C::STAGES;  // [2]       converters -> MMA
     uint64_t* aempty = afull + 2;            // [2]       MMA commit -> converters
     uint64_t* dfull = aempty + 2;            // [1]       MMA commit -> epilogue
-    uint32_t* tbase_sm = reinterpret_cast<uint32_t*>(dfull + 1);
+    uint64_t* dempty = dfull + 1;            // [1]       epilogue warps (D drained) -> MMA of the next tile
+    uint32_t* tbase_sm = reinterpret_cast<uint32_t*>(dempty + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t q = blockIdx.x / tiles_p;
-    const int64_t p0 = (blockIdx.x % tiles_p) * BM;
-    const int rows = static_cast<int>(lmin(BM, P - p0));
     // split-K (gridDim.y > 1): this CTA takes k-blocks [kb0, kb0 + nk) and writes its partial
     // to out + blockIdx.y * (P * cols * Q); the caller sums the partials in split order
     const int nk_all = static_cast<int>((K + kTcBK - 1) / kTcBK);
     const int nk_per = (nk_all + static_cast<int>(gridDim.y) - 1) / static_cast<int>(gridDim.y);
     const int kb0 = static_cast<int>(blockIdx.y) * nk_per;
     const int nk = nk_per < nk_all - kb0 ? nk_per : nk_all - kb0;
-    out += int64_t(blockIdx.y) * P * cols * (int64_t(gridDim.x) / tiles_p);
+    out += int64_t(blockIdx.y) * P * cols * (ntiles / tiles_p);
 
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -227,6 +225,7 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
             mbar_init(&aempty[a], 1);
         }
         mbar_init(dfull, 1);
+        mbar_init(dempty, kTcConv / 2);
         mbar_fence_init();
     }
     if (warp == kTcConv + 1) {  // TMEM allocation (whole warp)
@@ -239,181 +238,206 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
     fence_after();
     const uint32_t tmem = *tbase_sm;
 
+    // Tiles blockIdx.x, blockIdx.x + gridDim.x, ...: a persistent launch (gridDim.x < ntiles)
+    // keeps the ring streaming across tile boundaries — the producer loads the next tile while
+    // this one is multiplied and drained; the MMA of the next tile waits only for the drain of
+    // D (dempty). Stage / A-buffer phases run on a per-CTA counter g over all tiles.
     if (warp == kTcConv) {
         // ===== producer =====
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
-            for (int kc = 0; kc < nk; ++kc) {
-                const int s = kc % C::STAGES;
-                mbar_wait(&empty[s], ((kc / C::STAGES) & 1) ^ 1);
-                mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
-                uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
-                if constexpr (KM) {
+            uint32_t g = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int64_t q = t / tiles_p;
+                const int64_t p0 = (t % tiles_p) * BM;
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int s = static_cast<int>(g % C::STAGES);
+                    mbar_wait(&empty[s], ((g / C::STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
+                    uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
+                    if constexpr (KM) {
 #pragma unroll
-                    for (int b = 0; b < BM / C::BOXR; ++b)
-                        tma_load_2d(dy + b * (C::BOXR * kTcBK * 4), &ymap, (kb0 + kc) * kTcBK, static_cast<int>(p0 + C::BOXR * b),
-                                    &full[s]);
-                } else {
+                        for (int b = 0; b < BM / C::BOXR; ++b)
+                            tma_load_2d(dy + b * (C::BOXR * kTcBK * 4), &ymap, (kb0 + kc) * kTcBK,
+                                        static_cast<int>(p0 + C::BOXR * b), &full[s]);
+                    } else {
 #pragma unroll
-                    for (int b = 0; b < BM / C::BOXR; ++b)
-                        tma_load_3d(dy + b * (kTcBK * C::BOXR * 4), &ymap, static_cast<int>(p0 + C::BOXR * b), (kb0 + kc) * kTcBK,
-                                    static_cast<int>(q), &full[s]);
+                        for (int b = 0; b < BM / C::BOXR; ++b)
+                            tma_load_3d(dy + b * (kTcBK * C::BOXR * 4), &ymap, static_cast<int>(p0 + C::BOXR * b),
+                                        (kb0 + kc) * kTcBK, static_cast<int>(q), &full[s]);
+                    }
+                    bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kb0 + kc) * C::STAGE_B, C::STAGE_B, &full[s]);
                 }
-                bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kb0 + kc) * C::STAGE_B, C::STAGE_B, &full[s]);
             }
         }
     } else if (warp == kTcConv + 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
             const uint32_t id_full = idesc_tf32(2 * NH), id_hi = idesc_tf32(NH);
-            for (int kc = 0; kc < nk; ++kc) {
-                const int s = kc % C::STAGES, a = kc & 1;
-                mbar_wait(&full[s], (kc / C::STAGES) & 1);
-                mbar_wait(&afull[a], (kc >> 1) & 1);
-                fence_after();
-                const uint8_t* bs = sB + size_t(s) * C::STAGE_B;
-#pragma unroll
-                for (int j = 0; j < MT; ++j) {
-                    const int sm = kc % C::S;
-                    // set sm, tile j: [main | cross]; y_hi [u_hi | u_lo] fills both halves,
-                    // y_lo u_hi adds into the cross half (main keeps only y_hi u_hi)
-                    const uint32_t d = tmem + uint32_t((sm == 0 ? 0 : C::XBASE + (sm - 1) * C::D_COLS) + j * 2 * NH);
-                    const uint32_t ahi = tmem + uint32_t(C::D_COLS + a * C::A_COLS + j * 32);
-#pragma unroll
-                    for (int ks = 0; ks < 2; ++ks) {
-                        const uint64_t b = bdesc(bs + ks * C::BBYTES);
-                        mma_tf32_ts(d, ahi + ks * 8, b, id_full, (kc >= C::S || ks > 0) ? 1u : 0u);
-                        mma_tf32_ts(d + NH, ahi + 16 + ks * 8, b, id_hi, 1u);
-                    }
+            uint32_t g = 0, it = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                if (it > 0) {  // the previous tile's D must be drained before it is overwritten
+                    mbar_wait(dempty, (it - 1) & 1);
+                    fence_after();
                 }
-                mma_commit(&aempty[a]);
-                mma_commit(&empty[s]);
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int s = static_cast<int>(g % C::STAGES), a = static_cast<int>(g & 1);
+                    mbar_wait(&full[s], (g / C::STAGES) & 1);
+                    mbar_wait(&afull[a], (g >> 1) & 1);
+                    fence_after();
+                    const uint8_t* bs = sB + size_t(s) * C::STAGE_B;
+#pragma unroll
+                    for (int j = 0; j < MT; ++j) {
+                        const int sm = kc % C::S;
+                        // set sm, tile j: [main | cross]; y_hi [u_hi | u_lo] fills both halves,
+                        // y_lo u_hi adds into the cross half (main keeps only y_hi u_hi)
+                        const uint32_t d = tmem + uint32_t((sm == 0 ? 0 : C::XBASE + (sm - 1) * C::D_COLS) + j * 2 * NH);
+                        const uint32_t ahi = tmem + uint32_t(C::D_COLS + a * C::A_COLS + j * 32);
+#pragma unroll
+                        for (int ks = 0; ks < 2; ++ks) {
+                            const uint64_t b = bdesc(bs + ks * C::BBYTES);
+                            mma_tf32_ts(d, ahi + ks * 8, b, id_full, (kc >= C::S || ks > 0) ? 1u : 0u);
+                            mma_tf32_ts(d + NH, ahi + 16 + ks * 8, b, id_hi, 1u);
+                        }
+                    }
+                    mma_commit(&aempty[a]);
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(dfull);
             }
-            mma_commit(dfull);
         }
     } else {
         // ===== converters (warps 0-7): Y tile -> (hi, lo) tf32 A operands in TMEM =====
         const int quarter = warp & 3, khalf = warp >> 2;
         const int L = quarter * 32 + lane;                    // TMEM lane of this thread
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-        for (int kc = 0; kc < nk; ++kc) {
-            const int s = kc % C::STAGES, a = kc & 1;
-            mbar_wait(&full[s], (kc / C::STAGES) & 1);
-            uint32_t hi[MT][8], lo[MT][8];
-            // rows MT*L .. MT*L+MT-1 of the tile sit in box (MT*L)/BOXR at row (MT*L)%BOXR
-            const float* ys = reinterpret_cast<const float*>(sY + size_t(s) * C::STAGE_Y) +
-                              ((MT * L) / C::BOXR) * (kTcBK * C::BOXR) + (MT * L) % C::BOXR + khalf * 8 * C::BOXR;
-            if constexpr (KM) {
-                // row j*128 + L of the tile: 8 k values = logical 16-B chunks 2*khalf, 2*khalf+1
-                const uint8_t* stage = sY + size_t(s) * C::STAGE_Y;
-#pragma unroll
-                for (int j = 0; j < MT; ++j) {
-                    const int row = j * 128 + L;
-                    const int rr = row % C::BOXR;
-                    const uint8_t* rb = stage + (row / C::BOXR) * (C::BOXR * kTcBK * 4) + rr * 64;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int phys = (2 * khalf + h) ^ ((rr >> 1) & 3);
-                        const float4 v = *reinterpret_cast<const float4*>(rb + phys * 16);
-                        const float y4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const uint32_t hb = tf32_hi_bits(y4[e]);
-                            hi[j][h * 4 + e] = hb;
-                            lo[j][h * 4 + e] = __float_as_uint(y4[e] - __uint_as_float(hb));
-                        }
-                    }
-                }
-            } else {
-                auto split = [&](int kk, bool live) {
-                    float y[MT];
-                    if constexpr (MT == 4) {
-                        const float4 v = *reinterpret_cast<const float4*>(ys + kk * C::BOXR);
-                        y[0] = v.x, y[1] = v.y, y[2] = v.z, y[3] = v.w;
-                    } else if constexpr (MT == 2) {
-                        const float2 v = *reinterpret_cast<const float2*>(ys + kk * C::BOXR);
-                        y[0] = v.x, y[1] = v.y;
-                    } else {
-                        y[0] = ys[kk * C::BOXR];
-                    }
+        uint32_t g = 0, it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int64_t q = t / tiles_p;
+            const int64_t p0 = (t % tiles_p) * BM;
+            const int rows = static_cast<int>(lmin(BM, P - p0));
+            for (int kc = 0; kc < nk; ++kc, ++g) {
+                const int s = static_cast<int>(g % C::STAGES), a = static_cast<int>(g & 1);
+                mbar_wait(&full[s], (g / C::STAGES) & 1);
+                uint32_t hi[MT][8], lo[MT][8];
+                // rows MT*L .. MT*L+MT-1 of the tile sit in box (MT*L)/BOXR at row (MT*L)%BOXR
+                const float* ys = reinterpret_cast<const float*>(sY + size_t(s) * C::STAGE_Y) +
+                                  ((MT * L) / C::BOXR) * (kTcBK * C::BOXR) + (MT * L) % C::BOXR + khalf * 8 * C::BOXR;
+                if constexpr (KM) {
+                    // row j*128 + L of the tile: 8 k values = logical 16-B chunks 2*khalf, 2*khalf+1
+                    const uint8_t* stage = sY + size_t(s) * C::STAGE_Y;
 #pragma unroll
                     for (int j = 0; j < MT; ++j) {
-                        const float x = live ? y[j] : 0.f;
-                        const uint32_t h = tf32_hi_bits(x);
-                        hi[j][kk] = h;
-                        lo[j][kk] = __float_as_uint(x - __uint_as_float(h));
+                        const int row = j * 128 + L;
+                        const int rr = row % C::BOXR;
+                        const uint8_t* rb = stage + (row / C::BOXR) * (C::BOXR * kTcBK * 4) + rr * 64;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int phys = (2 * khalf + h) ^ ((rr >> 1) & 3);
+                            const float4 v = *reinterpret_cast<const float4*>(rb + phys * 16);
+                            const float y4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const uint32_t hb = tf32_hi_bits(y4[e]);
+                                hi[j][h * 4 + e] = hb;
+                                lo[j][h * 4 + e] = __float_as_uint(y4[e] - __uint_as_float(hb));
+                            }
+                        }
                     }
-                };
+                } else {
+                    auto split = [&](int kk, bool live) {
+                        float y[MT];
+                        if constexpr (MT == 4) {
+                            const float4 v = *reinterpret_cast<const float4*>(ys + kk * C::BOXR);
+                            y[0] = v.x, y[1] = v.y, y[2] = v.z, y[3] = v.w;
+                        } else if constexpr (MT == 2) {
+                            const float2 v = *reinterpret_cast<const float2*>(ys + kk * C::BOXR);
+                            y[0] = v.x, y[1] = v.y;
+                        } else {
+                            y[0] = ys[kk * C::BOXR];
+                        }
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) split(kk, true);  // the K tail is zero-filled by the TMA
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);  // Y stage consumed (B: the MMA commit)
-            mbar_wait(&aempty[a], ((kc >> 1) & 1) ^ 1);
-            fence_after();
+                        for (int j = 0; j < MT; ++j) {
+                            const float x = live ? y[j] : 0.f;
+                            const uint32_t h = tf32_hi_bits(x);
+                            hi[j][kk] = h;
+                            lo[j][kk] = __float_as_uint(x - __uint_as_float(h));
+                        }
+                    };
 #pragma unroll
-            for (int j = 0; j < MT; ++j) {
-                const uint32_t ta = tmem + lane_off + uint32_t(C::D_COLS + a * C::A_COLS + j * 32 + khalf * 8);
-                tmem_st8(ta, hi[j]);
-                tmem_st8(ta + 16, lo[j]);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&afull[a]);
-        }
-        if (khalf == 1) goto done;  // the epilogue runs on warps 0-3 (one per lane quarter)
-        // ===== epilogue: D = D[:, 0:NH] + D[:, NH:2NH], rows MT*L + j =====
-        mbar_wait(dfull, 0);
-        fence_after();
-        if (KM && !tout) {
-            // D tile j, TMEM lane L = row j*128 + L: stage [row][cols] in the (drained) Y
-            // buffers, then copy the contiguous out[p0*cols ...] block with coalesced stores
-            float* stg = reinterpret_cast<float*>(sY);
-#pragma unroll
-            for (int rc = 0; rc < NH; rc += 16) {
+                    for (int kk = 0; kk < 8; ++kk) split(kk, true);  // the K tail is zero-filled by the TMA
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);  // Y stage consumed (B: the MMA commit)
+                mbar_wait(&aempty[a], ((g >> 1) & 1) ^ 1);
+                fence_after();
 #pragma unroll
                 for (int j = 0; j < MT; ++j) {
-                    float v[16];
-                    drain16<C>(tmem + lane_off, j, rc, min(nk, C::S), v);
-                    float* srow = stg + (j * 128 + L) * cols;
-#pragma unroll
-                    for (int e = 0; e < 16; ++e)
-                        if (rc + e < cols) srow[rc + e] = v[e];
+                    const uint32_t ta = tmem + lane_off + uint32_t(C::D_COLS + a * C::A_COLS + j * 32 + khalf * 8);
+                    tmem_st8(ta, hi[j]);
+                    tmem_st8(ta + 16, lo[j]);
                 }
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&afull[a]);
             }
-            asm volatile("bar.sync 1, 128;\n" ::: "memory");
-            const int64_t n = int64_t(rows) * cols;
-            float* o = out + p0 * cols;
-            for (int64_t t = tid; t < n; t += 128) o[t] = stg[t];
-            goto done;
-        }
-        float* o = out + q * P * cols + p0 + MT * L;
-        const bool live = MT * L < rows;
+            if (khalf == 1) continue;  // the epilogue runs on warps 0-3 (one per lane quarter)
+            // ===== epilogue: D = D[:, 0:NH] + D[:, NH:2NH], rows MT*L + j =====
+            mbar_wait(dfull, it & 1);
+            fence_after();
+            if (KM && !tout) {
+                // (never persistent: the staging reuses the Y ring.) D tile j, TMEM lane L = row
+                // j*128 + L: stage [row][cols] in the (drained) Y buffers, then copy the
+                // contiguous out[p0*cols ...] block with coalesced stores
+                float* stg = reinterpret_cast<float*>(sY);
 #pragma unroll
-        for (int rc = 0; rc < NH; rc += 16) {
-            float acc[MT][16];
+                for (int rc = 0; rc < NH; rc += 16) {
 #pragma unroll
-            for (int j = 0; j < MT; ++j) drain16<C>(tmem + lane_off, j, rc, min(nk, C::S), acc[j]);
-            if (live) {
+                    for (int j = 0; j < MT; ++j) {
+                        float v[16];
+                        drain16<C>(tmem + lane_off, j, rc, min(nk, C::S), v);
+                        float* srow = stg + (j * 128 + L) * cols;
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int r = rc + e;
-                    if (r < cols) {
-                        if constexpr (MT == 4) {
-                            *reinterpret_cast<float4*>(o + int64_t(r) * P) =
-                                make_float4(acc[0][e], acc[1][e], acc[2][e], acc[3][e]);
-                        } else if constexpr (MT == 2) {
-                            *reinterpret_cast<float2*>(o + int64_t(r) * P) = make_float2(acc[0][e], acc[1][e]);
-                        } else {
-                            o[int64_t(r) * P] = acc[0][e];
+                        for (int e = 0; e < 16; ++e)
+                            if (rc + e < cols) srow[rc + e] = v[e];
+                    }
+                }
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                const int64_t n = int64_t(rows) * cols;
+                float* o = out + p0 * cols;
+                for (int64_t e = tid; e < n; e += 128) o[e] = stg[e];
+            } else {
+                float* o = out + q * P * cols + p0 + MT * L;
+                const bool live = MT * L < rows;
+#pragma unroll
+                for (int rc = 0; rc < NH; rc += 16) {
+                    float acc[MT][16];
+#pragma unroll
+                    for (int j = 0; j < MT; ++j) drain16<C>(tmem + lane_off, j, rc, min(nk, C::S), acc[j]);
+                    if (live) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const int r = rc + e;
+                            if (r < cols) {
+                                if constexpr (MT == 4) {
+                                    *reinterpret_cast<float4*>(o + int64_t(r) * P) =
+                                        make_float4(acc[0][e], acc[1][e], acc[2][e], acc[3][e]);
+                                } else if constexpr (MT == 2) {
+                                    *reinterpret_cast<float2*>(o + int64_t(r) * P) = make_float2(acc[0][e], acc[1][e]);
+                                } else {
+                                    o[int64_t(r) * P] = acc[0][e];
+                                }
+                            }
                         }
                     }
                 }
             }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dempty);  // D drained: the next tile's MMAs may overwrite it
         }
     }
-done:
     fence_before();
     __syncthreads();
     if (warp == kTcConv + 1) {
@@ -480,9 +504,18 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
     }
     require(grid < (int64_t(1) << 31), "ttm: grid too large");
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    // Persistent launch (OCC CTAs per SM looping over tiles) for the streaming shapes with many
+    // tiles; the K-major second stage (transpose staged through the Y ring) stays one tile per CTA.
+    static const int persist = [] {
+        const char* e = std::getenv("TENKIT_TC_PERSIST");
+        return e ? std::atoi(e) : 1;
+    }();
+    const int64_t ntiles = grid;
+    const int64_t slots = int64_t(148) * OCC;
+    if (persist && !(KM && !tout) && splits == 1 && grid > 2 * slots) grid = slots;
     TK_MAXSMEM((ttm_tc_kernel<NH, MT, KM, OCC>));
     ttm_tc_kernel<NH, MT, KM, OCC><<<dim3(static_cast<unsigned>(grid), static_cast<unsigned>(splits)), kTcThreads,
-                                     C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p, tout ? 1 : 0);
+                                     C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p, tout ? 1 : 0, ntiles);
     TK_LAUNCH_CHECK();
 }
 

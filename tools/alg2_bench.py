@@ -1,4 +1,4 @@
-"""rand_tucker (Alg. 2) vs rand_tucker_2i at cfg 2 on device data."""
+"""rand_tucker (Alg. 2) vs rand_tucker_2i (ColPiv and Gram-eig bases) at cfg 2 on device data."""
 import os, sys, time
 import torch
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
@@ -10,7 +10,9 @@ yd = P.DenseTensor(dims, y)
 _, alg = bench_seeds(0)
 ctx = P.Context.default(); ctx.bind_torch_stream()
 for name, fn, kw in [("rand_tucker (Alg 2)", P.rand_tucker, {}), ("rand_tucker_2i", P.rand_tucker_2i, dict(sync_ranks=False)),
-                     ("rand_tucker_2i explicit core", P.rand_tucker_2i, dict(sync_ranks=False, explicit_core_pass=True))]:
+                     ("rand_tucker_2i explicit core", P.rand_tucker_2i, dict(sync_ranks=False, explicit_core_pass=True)),
+                     ("rand_tucker_2i, Gram-eig basis", P.rand_tucker_2i, dict(sync_ranks=False, orthonormalizer="gram")),
+                     ("rand_tucker (Alg 2), Gram-eig basis", P.rand_tucker, dict(orthonormalizer="gram"))]:
     for _ in range(3):
         m = fn(yd, (20, 20, 20), 10, alg, out="device", **kw)
     torch.cuda.synchronize()

@@ -159,18 +159,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// L2 prefetch of a tensor box (no shared memory, no barrier): raises the bytes in flight
-// beyond the shared-memory ring
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(c0), "r"(c1)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(map), "r"(c0), "r"(c1),
-                 "r"(c2)
-                 : "memory");
-}
-
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                  : "memory");
@@ -203,7 +191,7 @@ __device__ __forceinline__ void drain16(uint32_t tl, int j, int rc, int used, fl
 template <int NH, int MT_, bool KM, int OCC = 1>
 __global__ void __launch_bounds__(kTcThreads, OCC)
     ttm_tc_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
-                  int64_t P, int64_t K, int cols, int64_t tiles_p, int tout, int64_t ntiles, int l2pf) {
+                  int64_t P, int64_t K, int cols, int64_t tiles_p, int tout, int64_t ntiles) {
     using C = TcCfg<NH, MT_, OCC>;
     constexpr int MT = C::MT, BM = C::BM;
     extern __shared__ __align__(1024) uint8_t tsm[];
@@ -279,22 +267,6 @@ __global__ void __launch_bounds__(kTcThreads, OCC)
                                         (kb0 + kc) * kTcBK, static_cast<int>(q), &full[s]);
                     }
                     bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kb0 + kc) * C::STAGE_B, C::STAGE_B, &full[s]);
-                    if (l2pf > 0) {  // the Y box l2pf stages ahead (possibly of this CTA's next tile) into L2
-                        int kc2 = kc + l2pf;
-                        int64_t t2 = t;
-                        while (kc2 >= nk) kc2 -= nk, t2 += gridDim.x;
-                        if (t2 < ntiles) {
-                            const int64_t q2 = t2 / tiles_p, p2 = (t2 % tiles_p) * BM;
-#pragma unroll
-                            for (int b = 0; b < BM / C::BOXR; ++b) {
-                                if constexpr (KM)
-                                    tma_prefetch_2d(&ymap, (kb0 + kc2) * kTcBK, static_cast<int>(p2 + C::BOXR * b));
-                                else
-                                    tma_prefetch_3d(&ymap, static_cast<int>(p2 + C::BOXR * b), (kb0 + kc2) * kTcBK,
-                                                    static_cast<int>(q2));
-                            }
-                        }
-                    }
                 }
             }
         }
@@ -541,15 +513,9 @@ void launch_tc(const float* in, const uint8_t* bpk, float* out, int64_t P, int64
     const int64_t ntiles = grid;
     const int64_t slots = int64_t(148) * OCC;
     if (persist && !(KM && !tout) && splits == 1 && grid > 2 * slots) grid = slots;
-    // A/B knob: L2 prefetch distance in stages for the Y passes (TENKIT_TC_L2PF, 0 = off)
-    static const int l2pf_env = [] {
-        const char* e = std::getenv("TENKIT_TC_L2PF");
-        return e ? std::atoi(e) : 0;
-    }();
-    const int l2pf = grid < ntiles ? l2pf_env : 0;
     TK_MAXSMEM((ttm_tc_kernel<NH, MT, KM, OCC>));
     ttm_tc_kernel<NH, MT, KM, OCC><<<dim3(static_cast<unsigned>(grid), static_cast<unsigned>(splits)), kTcThreads,
-                                     C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p, tout ? 1 : 0, ntiles, l2pf);
+                                     C::smem, s>>>(map, bpk, out, P, K, cols, tiles_p, tout ? 1 : 0, ntiles);
     TK_LAUNCH_CHECK();
 }
 

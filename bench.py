@@ -46,6 +46,10 @@ CONFIGS = {
                  ranks=(30, 30, 30), p=10, ffcp_rank=30, constraint=0),
     "cfg4": dict(idx=3, dims=(300, 300, 300, 300), dtype="f32", gen="cp_uniform", cp_rank=15, snr=30.0,
                  abs_noise=True, ranks=(15, 15, 15, 15), p=5, ffcp_rank=15, constraint=2),
+    # cfg 5 (4000^3, 256 GB) does not fit one GPU: its per-GPU slab at 4 GPUs (4000 x 4000 x 1000,
+    # 64 GB) as a standalone seeded tensor with cfg 5's generator parameters and ranks
+    "cfg5slab": dict(idx=4, dims=(4000, 4000, 1000), dtype="f32", gen="tucker", mlrank=(50, 50, 50), snr=20.0,
+                     ranks=(50, 50, 50), p=10, ffcp_rank=50, constraint=0),
 }
 STOP = (200, 1e-6)  # bench default StopRule{200, 1e-6} (bench.hpp:274)
 
@@ -329,7 +333,9 @@ def run_b200(args, cfg):
 
     # ---- sanity on the bench workload: fit of the Tucker model to Y from the Gram identity
     # ||Y - G x U||^2 = ||Y||^2 - ||G||^2 (orthonormal U); global norms summed over ranks
-    ysq = float(torch.linalg.vector_norm(y.double()).item() ** 2)
+    ysq = 0.0  # in fp64, chunked (no full fp64 copy of a 64 GB Y)
+    for c0 in range(0, y.numel(), 1 << 28):
+        ysq += float(torch.dot(y[c0:c0 + (1 << 28)].double(), y[c0:c0 + (1 << 28)].double()).item())
     if world > 1:
         ysq = _all_sum(ysq)
     gsq = float(torch.linalg.vector_norm(m.core).item() ** 2)

@@ -1058,6 +1058,11 @@ void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* co
             scratch = std::max(need_b, vsum);
         }
         const size_t smem = persist_smem(R, maxc, scratch);
+        // The persistent kernel runs where its shared-memory plan holds: V and the core slices
+        // staged (stage_g > 0) inside the SM's opt-in limit. Otherwise (large cores with
+        // R > 48, e.g. 60^3 / R = 50: the V-only plan faulted, 64^3 / R = 64 exceeded the limit;
+        // tools/ffcp_probe.py) the captured sweep graph below runs — same results.
+        if (stage_g > 0 && smem + 2048 <= size_t(smem_optin)) {
         TK_CUDA(cudaFuncSetAttribute(ffcp_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
         TK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffcp_persistent_kernel, kPThreads, smem));
@@ -1187,9 +1192,11 @@ void ffcp_device(BufPool& pool, cudaStream_t s, int64_t order, const int64_t* co
         TK_LAUNCH_CHECK();
         TK_CUDA(cudaStreamSynchronize(s));
         return;
+        }
     }
 
-    // one sweep over the modes, captured once as a graph (TENKIT_FFCP_GRAPH=1)
+    // one sweep over the modes, captured once as a graph (TENKIT_FFCP_GRAPH=1, or when the
+    // persistent kernel's shared-memory plan does not fit)
     auto sweep = [&](cudaStream_t st) {
         for (int n = 0; n < order; ++n) {
             const int cn = cd.cs[n];

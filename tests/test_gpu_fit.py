@@ -56,3 +56,17 @@ def test_fit_exact_model_is_one(P, O):
     y = O.reconstruct(core, fs)
     f, res, ny = P.model_fit(P.DenseTensor.from_numpy(y), P.TuckerModel(core, fs, ranks), norms=True)
     assert res <= 1e-13 * ny and abs(f - 1.0) < 1e-13
+
+
+@pytest.mark.parametrize("c,R", [(40, 33), (60, 50), (64, 64)])
+def test_ffcp_wide_ranks_match_oracle(P, O, c, R):
+    """FFCP with R > 32 on large cores: (40^3, 33) runs the persistent kernel; (60^3, 50) and
+    (64^3, 64) — whose shared-memory plan does not fit it — the captured sweep graph. Both
+    follow ffcp.hpp:94-194 like the oracle (fit trace within 1e-8)."""
+    rng = np.random.default_rng(c + R)
+    g = rng.standard_normal((c, c, c))
+    us = [np.linalg.qr(rng.standard_normal((c + 20, c)))[0] for _ in range(3)]
+    _, tr_ref, it_ref = O.ffcp(g, us, R, O.NONE, 0.0, 12, 0.0, (5, 0))
+    res = P.ffcp(P.TuckerModel(g, us, g.shape), R, stop=P.StopRule(12, 0.0), seed=(5, 0))
+    assert res.iterations == it_ref
+    np.testing.assert_allclose(res.fit_trace, tr_ref, rtol=0, atol=1e-8)

@@ -1,5 +1,5 @@
-"""BASELINE configs 3 and 4 at their FULL sizes (2400^3 fp32 = 55 GB, 300^4 fp32 = 32 GB) on one
-B200, checked through size-independent properties (the oracle cannot run at these sizes in
+"""BASELINE configs 3 and 4 at their FULL sizes (2400^3 fp32 = 55 GB, 300^4 fp32 = 32 GB) and cfg 5's
+per-GPU slab at 4 GPUs (4000 x 4000 x 1000 fp32 = 64 GB, ranks 50, r~ 60) on one B200, checked through size-independent properties (the oracle cannot run at these sizes in
 test time; cfg 2 at full size is compared with the oracle in test_gpu_workload.py):
 
 * determinism: two decompositions of the same Y are bit-identical (tucker.hpp's contract,
@@ -42,7 +42,7 @@ def _true_factors(cfg):
     return out
 
 
-@pytest.mark.parametrize("name,capture_tol", [("cfg3", 0.05), ("cfg4", 0.05)])
+@pytest.mark.parametrize("name,capture_tol", [("cfg3", 0.05), ("cfg4", 0.05), ("cfg5slab", 0.05)])
 def test_full_size_config_properties(P, name, capture_tol):
     import torch
     import bench
@@ -55,7 +55,7 @@ def test_full_size_config_properties(P, name, capture_tol):
     ranks, p = list(cfg["ranks"]), int(cfg["p"])
     runs = [P.rand_tucker_2i(yd, ranks, p, alg, sync_ranks=False, out="device") for _ in range(3)]
     a, b = runs[1].to_host(), runs[2].to_host()  # runs[2] replays the graph captured by runs[1]
-    assert a.stats["passes"] == 3
+    assert a.stats["passes"] == (4 if max(ranks) + p > 48 else 3)  # R~ = 60: no mode-0 leader (K-major <= 48)
     np.testing.assert_array_equal(a.core, b.core)
     for u, v in zip(a.factors, b.factors):
         np.testing.assert_array_equal(u, v)

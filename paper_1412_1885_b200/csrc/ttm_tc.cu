@@ -575,7 +575,8 @@ inline int mm_splits(int64_t P, int64_t K, int64_t Q, int cols, int64_t work_ele
 bool tc_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols, int64_t work_elems) {
     if (reinterpret_cast<uintptr_t>(in) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
     // K-major: R~ <= 48 (NH = 48 keeps 2 accumulator sets in 256 TMEM columns at MT = 1)
-    if (P == 1) return K % 4 == 0 && K >= kTcBK && cols <= 48 && (Q + 127) / 128 >= 148;
+    // (R~ <= 64: NH = 64 on one CTA per SM, 512 TMEM columns, 3 accumulator sets)
+    if (P == 1) return K % 4 == 0 && K >= kTcBK && cols <= 64 && (Q + 127) / 128 >= 148;
     if (P % 4 != 0 || P < 256) return false;
     // tiles >= 2 waves of 2 CTAs per SM, or (with split-K partials) >= 1 wave
     const int64_t tiles = mm_tiles(P, Q, cols);
@@ -591,7 +592,8 @@ int launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64
                                     : launch_tc<16, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
         else if (tc_nh(cols) <= 32) wide ? launch_tc<32, 2, true, 2>(in, b, out, P, K, Q, cols, s, tout)
                                          : launch_tc<32, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
-        else launch_tc<48, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
+        else if (tc_nh(cols) <= 48) launch_tc<48, 1, true, 2>(in, b, out, P, K, Q, cols, s, tout);
+        else launch_tc<64, 1, true, 1>(in, b, out, P, K, Q, cols, s, tout);
         return 1;
     }
     static const int variant = [] {

@@ -315,7 +315,11 @@ struct TuckerRun {
             if (ctx->ttm_path == 1 || cols.empty()) return false;
             const int64_t K = ldims[0];
             const int64_t Q = prod(ldims) / K;
-            return K % 4 == 0 && K >= 16 && cols[0] <= 48 && (Q + 127) / 128 >= 148 &&
+            static const int km_max = [] {  // A/B knob: widest factor a mode-0 Y pass may use
+                const char* e = std::getenv("TENKIT_KM_LEAD_MAX");
+                return e ? std::atoi(e) : 64;
+            }();
+            return K % 4 == 0 && K >= 16 && cols[0] <= km_max && (Q + 127) / 128 >= 148 &&
                    reinterpret_cast<uintptr_t>(y) % 16 == 0;
         }
     }

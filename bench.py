@@ -3,22 +3,25 @@
 "TTM GB/s of Y streamed (% HBM peak) + e2e Tucker+FFCP sec at 1/2/4/8 GPU").
 
 A step is one full rand_tucker_2i decomposition (paper Alg. 3, tucker.hpp:136-169) of the
-resident tensor Y: 2N Y-streaming TTM passes + 2N sketches/QRs + the core. The default
-workload is BASELINE configs[1] (1000^3 fp32, Tucker core 20^3, SNR 20 dB, ranks 20,
-oversample 10, FFCP rank 20), synthetic from the reference's seeded generators.
+resident tensor Y: the Y-streaming TTM passes + 2N sketches/QRs + the core. The default
+workload is BASELINE configs[2] (cfg3: 2400^3 fp32 = 55 GB, Tucker core 30^3, SNR 20 dB,
+ranks 30, oversample 10, FFCP rank 30), the largest config that fits one GPU, synthetic from
+the reference's seeded generators (generated on the device).
 
-  value      = Y bytes streamed per step / device time per step (GB/s, inputs in HBM)
+  value      = Y bytes streamed per step (every rank's block) / device time per step
+               (GB/s, inputs resident in HBM, max over ranks)
   e2e        = same metric through the public API with a pinned host Y: H2D copy +
                decomposition + FFCP + D2H of the model inside the timed region
-  roofline   = the Y-streaming TTM kernel: |Y| bytes per launch / its mean CUDA-event time,
-               against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline / --impl reference = the CPU oracle (restated reference, oracle/) on the
-               box's host cores over a bounded slab of the same workload
+  roofline   = the Y-streaming TTM kernel: |Y block| bytes per launch / its mean CUDA-event
+               time, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline(_1thread) / --impl reference = the CPU oracle (restated reference, oracle/)
+               on the box's host cores over a bounded sample of the same workload
 
-Multi-GPU (torchrun, one process per GPU): weak scaling — every rank holds one 1000^3 block
-of ONE global tensor: last-mode slabs of 1000 x 1000 x (1000 N) at N = 2, 4 and the
-2 x 2 x 2 block grid of a 2000^3 tensor at N = 8 (BASELINE cfg 5's partition; BlockGrid,
-dist.hpp:24-123); partial sketches and cores are all-reduced over NCCL (tk_comm hook).
+Multi-GPU (torchrun, one process per GPU), BASELINE's partitions (--scaling strong, default):
+the config's tensor is split into contiguous slabs of its last mode (cfg 3 "mode-3 slabs",
+cfg 4 slabs, cfg 5 slabs at 2 and 4 GPUs) or, for cfg 5 at 8 GPUs, the 2 x 2 x 2 block grid
+(BlockGrid, dist.hpp:24-123); partial sketches and cores are all-reduced with a native NCCL
+communicator inside the library. --scaling weak: every rank holds a block of the config's size.
 """
 from __future__ import annotations
 
@@ -50,7 +53,11 @@ CONFIGS = {
     # 64 GB) as a standalone seeded tensor with cfg 5's generator parameters and ranks
     "cfg5slab": dict(idx=4, dims=(4000, 4000, 1000), dtype="f32", gen="tucker", mlrank=(50, 50, 50), snr=20.0,
                      ranks=(50, 50, 50), p=10, ffcp_rank=50, constraint=0),
+    # cfg 5 itself (256 GB): >= 2 GPUs (slabs at 2 and 4, the 2 x 2 x 2 grid at 8)
+    "cfg5": dict(idx=4, dims=(4000, 4000, 4000), dtype="f32", gen="tucker", mlrank=(50, 50, 50), snr=20.0,
+                 ranks=(50, 50, 50), p=10, ffcp_rank=50, constraint=0),
 }
+METRIC = "TTM GB/s of Y streamed (% HBM peak) + e2e Tucker+FFCP sec at 1/2/4/8 GPU"
 STOP = (200, 1e-6)  # bench default StopRule{200, 1e-6} (bench.hpp:274)
 
 
@@ -172,57 +179,121 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
-# ----------------------------------------------------------------------------- CPU oracle
+# ----------------------------------------------------------------------------- host + CPU oracle
+L2_BYTES = 126 << 20  # B200 L2
+
+
+def host_info():
+    """The box's host: CPU model, logical cores (nproc), memory (lscpu / free -g equivalents)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu"] = ln.split(":", 1)[1].strip()
+                break
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                info["mem_gb"] = round(int(ln.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return info
+
+
+def repo_library_loaded() -> bool:
+    """Whether this process mapped the product library (the reference arm must not)."""
+    try:
+        return "libtenkit_b200" in open("/proc/self/maps").read()
+    except OSError:
+        return False
+
+
+def sample_dims(cfg, last=None):
+    """The CPU baseline's bounded sample of the workload: the whole tensor when it is small
+    (<= 32 M elements), else the leading slab of the last mode, r~_last (>= 32) rows long, so
+    every mode keeps its full r~ and the per-element work of a pass (2 r~ flop) is the
+    workload's."""
+    dims = [int(d) for d in cfg["dims"]]
+    if last is None and int(np.prod(dims)) <= (32 << 20):
+        return dims
+    rt_last = min(int(cfg["ranks"][-1]) + int(cfg["p"]), dims[-1])
+    dims[-1] = min(dims[-1], int(last) if last else max(rt_last, 32))
+    return dims
+
+
+def oracle_seeds(seed: int = 0):
+    """bench_seeds (bench.hpp:588,604-606) through the oracle's SeedSpec restatement."""
+    from oracle import pyoracle as O
+    return O.seed_derived(seed, 0, 0xDA7A, 0), O.seed_derived(seed, 0, 0xA16D, 0)
+
+
+def oracle_generate(cfg, dims, data_seed):
+    """The workload's generator (bench.hpp:56-112, configs' U(0,1) / |N| variants) on the host
+    with the oracle, fp64, rounded to fp32 for the fp32 configs (the oracle then runs in fp64
+    on the fp32 values)."""
+    from oracle import pyoracle as O
+    if cfg["gen"] == "tucker":
+        y = O.gen_tucker(dims, cfg["mlrank"], data_seed)
+    else:
+        kind = O.CP_UNIFORM if cfg["gen"] == "cp_uniform" else O.CP_GAUSSIAN
+        y, _ = O.gen_cp(dims, cfg["cp_rank"], kind, data_seed)
+    y = O.add_noise(y, cfg["snr"], O.seed_derived(*data_seed, 0xAD0), abs_noise=cfg.get("abs_noise", False))
+    if cfg["dtype"] == "f32":
+        y = y.astype(np.float32).astype(np.float64)
+    return y
+
+
 def oracle_decompose(y64, cfg, seed, threads, with_ffcp=True):
+    """rand_tucker_2i (+ FFCP) of the CPU oracle; (decomposition s, decomposition + FFCP s),
+    timed like bench.hpp:456-520 (t0 before compression, e2e after FFCP)."""
     from oracle import pyoracle as O
     O.set_threads(threads)
     t0 = time.perf_counter()
-    g, us = O.rand_tucker_2i(y64, cfg["ranks"], cfg["p"], (seed.root, seed.stream))
+    g, us = O.rand_tucker_2i(y64, cfg["ranks"], cfg["p"], seed)
     t1 = time.perf_counter()
     if with_ffcp:
-        O.ffcp(g, us, cfg["ffcp_rank"], cfg["constraint"], 0.0, STOP[0], STOP[1], (seed.root, seed.stream))
+        O.ffcp(g, us, cfg["ffcp_rank"], cfg["constraint"], 0.0, STOP[0], STOP[1], seed)
     t2 = time.perf_counter()
     return t1 - t0, t2 - t0
 
 
-def cpu_sample(cfg, y_dev_flat, slabs):
-    """A bounded slab Y[..., :slabs] of the workload (host fp64), the CPU baseline's sample."""
-    dims = list(cfg["dims"])
-    n = int(np.prod(dims[:-1])) * slabs
-    y = y_dev_flat[:n].double().cpu().numpy()
-    dims[-1] = slabs
-    return y.reshape(dims, order="F"), dims
+def cpu_rate(cfg, ys, seconds):
+    """GB/s of Y streamed by the reference's 2N+1 passes (tucker.hpp:136-169) over the sample,
+    counting the workload's element size (4 B for the fp32 configs)."""
+    elem = 4 if cfg["dtype"] == "f32" else 8
+    return (2 * len(cfg["dims"]) + 1) * ys.size * elem / seconds / 1e9
+
+
+def cpu_baselines(cfg, ys, sdims, seed):
+    """The CPU oracle on this box's host cores over the bounded sample: all cores (OpenBLAS
+    threads) and one thread (the reference's own configuration: Eigen without OpenMP,
+    CMakeLists.txt:13-23)."""
+    out = {}
+    for key, threads in (("all", os.cpu_count() or 1), ("one", 1)):
+        tc, _ = oracle_decompose(ys, cfg, seed, threads, with_ffcp=False)
+        out[key] = {"value": round(cpu_rate(cfg, ys, tc), 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                    "seconds": round(tc, 3),
+                    "sample": f"rand_tucker_2i on the {'x'.join(map(str, sdims))} leading slab of the workload's Y "
+                              f"(fp64 oracle on the fp32 values, {'OpenBLAS ' + str(threads) + ' threads' if threads > 1 else '1 thread'}), "
+                              f"{2 * len(cfg['dims']) + 1} passes"}
+    return out
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference algorithm (restated CPU oracle; the reference itself
-    cannot be built here: no Eigen/Catch2) on the box's host cores, bounded slab sample."""
+    """--impl reference: the reference algorithm (the restated CPU oracle; the reference itself
+    cannot be built here: no Eigen / Catch2) on the box's host cores (all threads), on a
+    bounded sample of the workload generated by the oracle's own generators (no repo library
+    is loaded), rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    from paper_1412_1885_b200.generators import bench_seeds, generate
+    from oracle import pyoracle as O
     threads = os.cpu_count() or 1
-    _, alg_seed = bench_seeds(0)
-    slabs = args.cpu_slabs
-    if torch.cuda.is_available():
-        from paper_1412_1885_b200.generators import generate_as
-        tdt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
-        y = generate_as(dict(cfg, seed=0), tdt, slab=(0, slabs), full_sigma=True)
-        ys, sdims = cpu_sample(cfg, y, slabs)
-        del y
-        torch.cuda.empty_cache()
-    else:  # host-only fallback for the sample generator: the oracle's own generators
-        from oracle import pyoracle as O
-        from paper_1412_1885_b200.generators import bench_seeds as bs
-        ds, _ = bs(0)
-        sdims = list(cfg["dims"])
-        sdims[-1] = slabs
-        O.set_threads(threads)
-        ys = O.gen_tucker(sdims, cfg["mlrank"], (ds.root, ds.stream))
+    O.set_threads(threads)
+    data_seed, alg_seed = oracle_seeds(0)
+    sdims = sample_dims(cfg, args.cpu_slabs)
+    ys = oracle_generate(cfg, sdims, data_seed)
     passes = 2 * len(cfg["dims"]) + 1
-    elem_bytes = 4 if cfg["dtype"] == "f32" else 8
-    sample_bytes = ys.size * elem_bytes
     for _ in range(args.warmup):
         oracle_decompose(ys, cfg, alg_seed, threads, with_ffcp=False)
     times, e2e = [], []
@@ -230,72 +301,92 @@ def run_reference(args, cfg):
         tc, te = oracle_decompose(ys, cfg, alg_seed, threads)
         times.append(tc)
         e2e.append(te)
-    ms = 1e3 * statistics.mean(times)
-    value = passes * sample_bytes / (statistics.mean(times)) / 1e9
-    e2e_v = passes * sample_bytes / (statistics.mean(e2e)) / 1e9
-    sample = f"rand_tucker_2i+ffcp on the {'x'.join(map(str, sdims))} slab of the workload (fp64 oracle, OpenBLAS {threads} threads)"
+    value = cpu_rate(cfg, ys, statistics.mean(times))
+    e2e_v = cpu_rate(cfg, ys, statistics.mean(e2e))
+    sample = (f"rand_tucker_2i+ffcp on a {'x'.join(map(str, sdims))} sample of the workload (oracle generators, "
+              f"fp64 oracle on fp32-rounded values, OpenBLAS {threads} threads)")
     line = {
-        "metric": "TTM GB/s of Y streamed (% HBM peak) + e2e Tucker+FFCP sec at 1/2/4/8 GPU",
-        "impl": "reference", "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference seeded generators, bench.hpp:46-112)",
+        "metric": METRIC, "impl": "reference", "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.mean(times), 3),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference seeded generators bench.hpp:46-112, restated by the oracle on the host)",
         "config": {"workload": args.config, "dims": list(cfg["dims"]), "ranks": list(cfg["ranks"]),
                    "oversample": cfg["p"], "ffcp_rank": cfg["ffcp_rank"], "passes_per_step": passes,
                    "sample_dims": sdims},
         "e2e": {"value": round(e2e_v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "tucker_ffcp_seconds": round(statistics.mean(e2e), 4),
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+        "tucker_ffcp_seconds_sample": round(statistics.mean(e2e), 4),
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
+        "host": host_info(),
+        "repo_library_loaded": repo_library_loaded(),
     }
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- B200 arm
+def bench_grid(name, order, world, scaling):
+    """BASELINE's partitions: strong scaling splits the config's tensor into contiguous slabs
+    of its last mode over the ranks (cfg 3 "mode-3 slabs", cfg 4 slabs, cfg 5 slabs at 2 and 4
+    GPUs) except cfg 5 at 8 GPUs, the 2 x 2 x 2 block grid (partition, dist.hpp:71-123). Weak
+    scaling: every rank holds a block of the config's size (dims x grid, default_grid)."""
+    if scaling == "weak":
+        return [2, 2, 2] if (order == 3 and world == 8) else [1] * (order - 1) + [world]
+    if name == "cfg5" and world == 8:
+        return [2, 2, 2]
+    return [1] * (order - 1) + [world]
+
+
 def run_b200(args, cfg):
     import torch
     import paper_1412_1885_b200 as P
     from paper_1412_1885_b200 import dist as D
-    from paper_1412_1885_b200.generators import bench_seeds, generate
+    from paper_1412_1885_b200.generators import bench_seeds, generate_as
 
     rank, world, local = dist_setup(args.gpus)
     ctx = P.Context.default(local)
     ctx.bind_torch_stream()
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
-    dims = list(cfg["dims"])
-    grid = D.default_grid(len(dims), world)
-    gdims = [d * g for d, g in zip(dims, grid)]
-    plan = D.GridPlan(gdims, [[d] * g for d, g in zip(dims, grid)])
+    dims = [int(d) for d in cfg["dims"]]
+    grid = bench_grid(args.config, len(dims), world, args.scaling)
+    if args.scaling == "weak":
+        gdims = [d * g for d, g in zip(dims, grid)]
+        plan = D.GridPlan(gdims, [[d] * g for d, g in zip(dims, grid)])
+    else:
+        gdims = list(dims)
+        plan = D.GridPlan.even(gdims, grid)
     blo, bln = plan.block(rank)
-    assert bln == dims
     _, alg_seed = bench_seeds(0)
 
-    # ---- data (untimed): this rank's slab of ONE global seeded tensor of dims
-    # I_0 x ... x (N * I_{N-1}) (weak scaling), generated blockwise on the device: the last
-    # factor's rows and the noise are drawn at their global indices, the noise scale from
-    # norms summed over ranks, so the slabs concatenate to the tensor a single run generates.
-    from paper_1412_1885_b200.generators import generate_as
+    # ---- data (untimed): this rank's block of ONE global seeded tensor, generated blockwise on
+    # the device: factor rows and noise drawn at their global indices, the noise scale from
+    # norms summed over ranks, so the blocks tile the tensor a single-GPU run generates.
     if world == 1:
-        y = generate_as(dict(cfg, seed=0), tdt)
+        y = generate_as(dict(cfg, seed=0, dims=gdims), tdt)
     else:
         y = generate_as(dict(cfg, seed=0, dims=gdims), tdt, block=(blo, bln), all_sum=_all_sum)
     torch.cuda.empty_cache()
-    log(f"[rank {rank}/{world}] block lo={blo} len={bln} of {gdims}: generated")
-    cpu_ys = None  # the CPU baseline's bounded sample: the first slabs of this Y (host fp64)
+    log(f"[rank {rank}/{world}] block lo={blo} len={bln} of {gdims} ({args.scaling} scaling): generated")
+    cpu_ys = None  # the CPU baseline's bounded sample: the leading slab of this Y (host fp64)
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu_ys, cpu_sdims = cpu_sample(cfg, y, args.cpu_slabs)
-    yd = P.DenseTensor(dims, y)
+        sdims = sample_dims(cfg, args.cpu_slabs)
+        cpu_ys = y[: int(np.prod(sdims))].double().cpu().numpy().reshape(sdims, order="F")
+    yd = P.DenseTensor(bln, y)
     ybytes = y.numel() * y.element_size()
+    gbytes = int(np.prod(gdims)) * y.element_size()
     comm = None
     if world > 1:
         comm = D.DistComm(blo[-1], gdims[-1], D.exchange_capacity(gdims, cfg["ranks"], cfg["p"]), block_lo=blo,
-                          global_dims=gdims)
+                          global_dims=gdims, native=not args.comm_callback)
         ctx.set_comm(comm)
+        log(f"[rank {rank}/{world}] comm: {comm.describe()}")
     kw = dict(sync_ranks=False, out="device", global_dims=gdims if world > 1 else (),
               one_pass_per_step=args.one_pass_per_step)
 
     def step(time_kernels=False):
         return P.rand_tucker_2i(yd, cfg["ranks"], cfg["p"], alg_seed, context=ctx, time_kernels=time_kernels, **kw)
 
+    # Y smaller than twice the L2: flush it (write a buffer > L2) between timed steps, timed per step
+    flush = ybytes < 2 * L2_BYTES
+    scratch = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device="cuda") if flush else None
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stream_ms, stream_launches, launches = 0.0, 0, 0
@@ -303,33 +394,46 @@ def run_b200(args, cfg):
         t_w = time.perf_counter()
         nw = 0
         # >= 1 s of warm-up with the timed call itself, so a repeated call's CUDA graph is
-        # captured here (first call eager, second captures, then replays) and not timed
+        # captured here (first call eager, second captures, then replays) and not timed;
         # the number of warm-up calls is agreed over ranks (every call runs collectives)
         while nw < max(args.warmup, 3) or all_max(float(time.perf_counter() - t_w < 1.0), world) > 0:
             m = step(time_kernels=True)
             nw += 1
         log(f"[rank {rank}/{world}] warm-up done ({nw} calls)")
         barrier(world)
-        ev0.record(stream)
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            m = step(time_kernels=True)
-            stream_ms += m.stats["stream_ms"]
-            stream_launches += m.stats["stream_launches"]
-            launches += m.stats["kernel_launches"]
-        ev1.record(stream)
-        barrier(world)
+        if flush:
+            dev_ms = 0.0
+            for _ in range(args.steps):
+                scratch.zero_()
+                ev0.record(stream)
+                m = step(time_kernels=True)
+                ev1.record(stream)
+                ev1.synchronize()
+                dev_ms += ev0.elapsed_time(ev1)
+                stream_ms += m.stats["stream_ms"]
+                stream_launches += m.stats["stream_launches"]
+                launches += m.stats["kernel_launches"]
+            barrier(world)
+        else:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                m = step(time_kernels=True)
+                stream_ms += m.stats["stream_ms"]
+                stream_launches += m.stats["stream_launches"]
+                launches += m.stats["kernel_launches"]
+            ev1.record(stream)
+            barrier(world)
+            dev_ms = ev0.elapsed_time(ev1)
         clk.window(t0, time.perf_counter())
-    dev_ms = ev0.elapsed_time(ev1)
     dev_ms = all_max(dev_ms, world)
     ms_step = dev_ms / args.steps
     passes = m.stats["passes"]
-    value = world * passes * ybytes / (ms_step * 1e-3) / 1e9
+    value = passes * gbytes / (ms_step * 1e-3) / 1e9  # whole job: every rank streams its block
     pk = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
-    kern_ms = stream_ms / max(stream_launches, 1)
+    kern_ms = all_max(stream_ms / max(stream_launches, 1), world)
     achieved = ybytes / (kern_ms * 1e-3) / 1e9
-    traffic = _ncu_traffic(args.config)
 
     # ---- sanity on the bench workload: fit of the Tucker model to Y from the Gram identity
     # ||Y - G x U||^2 = ||Y||^2 - ||G||^2 (orthonormal U); global norms summed over ranks
@@ -341,13 +445,13 @@ def run_b200(args, cfg):
     gsq = float(torch.linalg.vector_norm(m.core).item() ** 2)
     fit_model = 1.0 - float(np.sqrt(max(0.0, 1.0 - gsq / ysq)))
 
-    # ---- e2e through the public API with a pinned host Y
+    # ---- e2e through the public API with a pinned host Y (this rank's block)
     e2e = None
     if not args.no_e2e:
         host = torch.empty(y.numel(), dtype=tdt, pin_memory=True)
         host.copy_(y)
         torch.cuda.synchronize()
-        yh = P.DenseTensor(dims, host.numpy())
+        yh = P.DenseTensor(bln, host.numpy())
         del y
         yd = None
         torch.cuda.empty_cache()
@@ -368,81 +472,90 @@ def run_b200(args, cfg):
             h2d = ybytes
             d2h = (mh.core.size + sum(u.size for u in mh.factors) + sum(a.size for a in res.factors)) * 8
         e2e_s = statistics.mean(e2e_times)
-        e2e = {"value": round(world * passes * ybytes / e2e_s / 1e9, 3), "unit": "GB/s",
+        e2e = {"value": round(passes * gbytes / e2e_s / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "tucker_ffcp_seconds": round(e2e_s, 4), "ffcp_iterations": int(res.iterations),
-               "ffcp_fit": float(res.fit_trace[-1])}
+               "ffcp_fit": float(res.fit_trace[-1]),
+               "h2d_floor_seconds": None}
+        # the copy alone (pinned host -> HBM, same bytes): the host-link floor of e2e
+        dst = torch.empty(host.numel(), dtype=tdt, device="cuda")
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dst.copy_(host, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e["h2d_floor_seconds"] = round(all_max(time.perf_counter() - t0, world), 4)
+        del dst
         # ---- reported fits of the CP model (bench.hpp:530-531), untimed: streamed over Y
         # on the device (tk_model_fit), the noise-free truth regenerated from the seed
         if world == 1:
             yd_fit = torch.from_numpy(yh.data).cuda()
             cpm = P.CpModel(res.factors)
             t0 = time.perf_counter()
-            fit_obs = P.model_fit(P.DenseTensor(dims, yd_fit), cpm, context=ctx)
+            fit_obs = P.model_fit(P.DenseTensor(bln, yd_fit), cpm, context=ctx)
             fit_ms = 1e3 * (time.perf_counter() - t0)
             del yd_fit
             truth = generate_as(dict(cfg, seed=0, snr=float("inf")), tdt)
-            fit_gt = P.model_fit(P.DenseTensor(dims, truth), cpm, context=ctx)
+            fit_gt = P.model_fit(P.DenseTensor(bln, truth), cpm, context=ctx)
             del truth
             torch.cuda.empty_cache()
             e2e.update({"fit_obs": round(fit_obs, 6), "fit_gt": round(fit_gt, 6), "fit_pass_ms": round(fit_ms, 2)})
 
-    # ---- CPU baseline (rank 0, N=1 only): oracle on a bounded slab
+    # ---- CPU baselines (rank 0, N=1 only): oracle on a bounded sample, all cores and 1 thread
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        ys, sdims = cpu_ys, cpu_sdims
-        tc, te = oracle_decompose(ys, cfg, alg_seed, threads, with_ffcp=False)
-        pref = 2 * len(dims) + 1
-        cpu = {"value": round(pref * ys.size * (4 if cfg["dtype"] == "f32" else 8) / tc / 1e9, 3), "unit": "GB/s",
-               "cores": threads, "kind": "port",
-               "sample": f"rand_tucker_2i on the {'x'.join(map(str, sdims))} slab (fp64 oracle, OpenBLAS {threads} threads), {pref} passes"}
+    if cpu_ys is not None:
+        cpu = cpu_baselines(cfg, cpu_ys, list(cpu_ys.shape), (alg_seed.root, alg_seed.stream))
 
     if rank == 0:
+        l2 = ("Y larger than L2 (126 MB): no flush needed" if not flush else
+              "Y smaller than 2x L2: a 252 MB buffer is written between timed steps (L2 flushed), steps timed one by one")
         line = {
-            "metric": "TTM GB/s of Y streamed (% HBM peak) + e2e Tucker+FFCP sec at 1/2/4/8 GPU",
+            "metric": METRIC,
             "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32" if cfg["dtype"] == "f32" else "f64",
-            "data": "synthetic (reference seeded generators bench.hpp:46-112 on device; Y > L2, no flush needed)",
+            "data": "synthetic (reference seeded generators bench.hpp:46-112, generated on the device)",
             "config": {"workload": args.config, "dims": gdims, "ranks": list(cfg["ranks"]), "oversample": cfg["p"],
                        "ffcp_rank": cfg["ffcp_rank"], "passes_per_step": passes,
-                       "parallelism": ("block" + "x".join(map(str, grid))) if world > 1 else "slab1",
-                       "l2": "inputs larger than L2 (126 MB)",
+                       "passes_reference": 2 * len(dims) + 1,
+                       "parallelism": ("grid" + "x".join(map(str, grid))) + f" ({args.scaling})",
+                       "block_per_gpu": bln, "l2": l2,
                        "core": "derived from X_{N-1}",
                        "steps_per_pass": "one Y pass per range step" if args.one_pass_per_step else
                        "consecutive range steps share one Y pass (reference: 2N+1 passes)"},
             "hbm_frac_of_peak": round(value / world / hbm, 4),
-            # the reference streams Y 2N+1 times per decomposition (tucker.hpp:136-169); this
-            # run streams it `passes` times (shared passes + core from X_{N-1}): the step's speed
-            # expressed in the reference's bytes
-            "ref_pass_equiv_gbs": round(world * (2 * len(dims) + 1) * ybytes / (ms_step * 1e-3) / 1e9, 1),
+            "decompositions_per_s": round(1e3 / ms_step, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4), "traffic": traffic,
-                         "kernel": "ttm_tc_kernel (Y-streaming TTM, tcgen05 3xTF32)" if cfg["dtype"] == "f32" else "ttm_mmajor_kernel (Y-streaming TTM, FFMA)", "peak_source": "measured" if not pk.get("_fallback") else "fallback",
-                         "bytes_per_launch": ybytes, "mean_launch_ms": round(kern_ms, 4)},
+                         "frac": round(achieved / hbm, 4), "traffic": _ncu_traffic(args.config, world),
+                         "kernel": "ttm_tc_kernel (Y-streaming TTM, tcgen05 3xTF32)" if cfg["dtype"] == "f32" else "ttm_mmajor_kernel (Y-streaming TTM, FFMA)",
+                         "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if not pk.get("_fallback") else "fallback",
+                         "bytes_per_launch": ybytes, "mean_launch_ms": round(kern_ms, 4),
+                         "launches_per_step": passes},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
-            "fit_model": round(fit_model, 6),
+            "fit_model": round(fit_model, 7),
+            "core_norm": round(float(np.sqrt(gsq)), 6),
         }
         if e2e:
             line["e2e"] = e2e
             line["tucker_ffcp_seconds"] = e2e["tucker_ffcp_seconds"]
         if cpu:
-            line["cpu_baseline"] = cpu
+            line["cpu_baseline"] = cpu["all"]
+            line["cpu_baseline_1thread"] = cpu["one"]
+            line["host"] = host_info()
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
 
 
-def _ncu_traffic(workload):
-    """DRAM bytes per launch of the TTM kernel from the committed ncu capture of this
-    workload's Y passes (profiles/ttm_traffic.json), else None."""
+def _ncu_traffic(workload, world=1):
+    """DRAM bytes (read + write) per launch of the Y-streaming TTM kernel, averaged over the
+    step's Y passes, from the committed ncu --set full capture of this workload
+    (profiles/ttm_traffic.json, keyed by workload; single-GPU captures), else None."""
     p = os.path.join(ROOT, "profiles", "ttm_traffic.json")
     try:
-        d = json.load(open(p))
-        return d.get("dram_bytes_per_launch") if d.get("workload") == workload else None
+        d = json.load(open(p)).get(workload)
+        return d.get("dram_bytes_per_launch") if d and world == 1 else None
     except Exception:
         return None
 
@@ -450,16 +563,20 @@ def _ncu_traffic(workload):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: BASELINE's partition of the config's tensor; weak: a config-sized block per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--one-pass-per-step", action="store_true",
                     help="A/B: stream Y once per range step (reference structure) instead of sharing passes")
+    ap.add_argument("--comm-callback", action="store_true",
+                    help="A/B: all-reduce through the torch.distributed callback instead of the native NCCL comm")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-slabs", type=int, default=100)
+    ap.add_argument("--cpu-slabs", type=int, default=None, help="last-mode length of the CPU sample")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -123,6 +123,19 @@ int tk_context_set_stream(tk_context* ctx, void* cuda_stream);
 /* Install (or clear, with NULL) the cross-rank reduction hook */
 int tk_context_set_comm(tk_context* ctx, const tk_comm* comm);
 int tk_context_synchronize(tk_context* ctx);
+/* Native NCCL communicator for the cross-rank sums (one process per GPU, NVLink/NVSwitch):
+ * rank 0 gets a unique id with tk_nccl_unique_id, the ranks exchange it out of band (e.g. a
+ * torch.distributed broadcast), every rank calls tk_context_set_nccl(ctx, id, rank, world).
+ * With it installed, tk_context_set_comm's block description (rank/world/blocks) is still
+ * required but allreduce_sum / xbuf may be NULL: the partial sketches and cores are summed in
+ * place with ncclAllReduce (fp64, sum) on the call's stream, so repeated calls keep their CUDA
+ * graph (the collectives are captured). world = 0 tears the communicator down. NCCL is
+ * resolved at run time (libnccl.so.2 already loaded by the process, else the system one). */
+#define TK_NCCL_UNIQUE_ID_BYTES 128
+int tk_nccl_unique_id(unsigned char* out /* TK_NCCL_UNIQUE_ID_BYTES */);
+int tk_context_set_nccl(tk_context* ctx, const unsigned char* id, int rank, int world);
+/* NCCL version code of the resolved library (e.g. 22809), 0 if unavailable */
+int tk_nccl_version(void);
 /* Contraction kernels for the Y-streaming TTM passes: 0 auto (tcgen05 3xTF32 UMMA for fp32
  * data when the shape tiles the GPU, FFMA otherwise), 1 FFMA only, 2 tcgen05 whenever the
  * shape is supported (also for the kernel-level tk_ttm) */

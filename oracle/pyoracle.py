@@ -282,6 +282,36 @@ def rand_tucker_2i(y, ranks, oversample: int, seed, return_sketches: bool = Fals
     return g, us
 
 
+def rand_tucker_2i_streamed(y32, dims, ranks, oversample: int, seed, slab_elems: int = 1 << 25,
+                            return_sketches: bool = False):
+    """Alg. 3 (tucker.hpp:136-169) streamed over last-mode slabs of an fp32 host tensor
+    (flat column-major np.float32 of prod(dims) elements; each slab converted to fp64):
+    the full-size parity checker for tensors whose fp64 copy does not fit in host memory
+    (dist.hpp:496-596 streaming pattern). Returns (core, factors, margins[, sketches]) with
+    margins = per step (pivot margin, sign margin)."""
+    y32 = np.ascontiguousarray(np.asarray(y32, dtype=np.float32).reshape(-1))
+    dims = [int(d) for d in dims]
+    if y32.size != int(np.prod(dims)):
+        raise OracleError("tenkit: tensor data length does not match shape")
+    order = len(dims)
+    rts, core, cshape, fbufs, farr, cols = _model_buffers(dims, ranks, oversample)
+    zarr, zbufs = None, []
+    if return_sketches:
+        zbufs = [np.empty(dims[i % order] * rts[i % order]) for i in range(2 * order)]
+        zarr = (D * len(zbufs))(*[_ptr(b) for b in zbufs])
+    margins = np.zeros(4 * order)
+    _check(lib().tko_rand_tucker_2i_f32_streamed(
+        _iptr(_i64(dims)), C.c_int64(order), y32.ctypes.data_as(C.POINTER(C.c_float)), _iptr(_i64(ranks)),
+        C.c_int64(oversample), C.c_uint64(seed[0]), C.c_uint64(seed[1]), C.c_int64(slab_elems), _ptr(core),
+        _iptr(cshape), farr, _iptr(cols), zarr, _ptr(margins)))
+    g, us = _unpack_model(dims, core, cshape, fbufs, cols)
+    mg = margins.reshape(2 * order, 2)
+    if return_sketches:
+        zs = [b.reshape((dims[i % order], rts[i % order]), order="F") for i, b in enumerate(zbufs)]
+        return g, us, mg, zs
+    return g, us, mg
+
+
 def sym_eig(a):
     """Symmetric eigendecomposition (stand-in for Eigen's SelfAdjointEigenSolver,
     range_finder.hpp:57,87): ascending eigenvalues, eigenvectors as columns."""

@@ -110,8 +110,8 @@ using dgemm_fn = void (*)(const char*, const char*, const int64_t*, const int64_
                           const int64_t*, size_t, size_t);
 using setthreads_fn = void (*)(int);
 static dgemm_fn g_dgemm = nullptr;
+static int g_threads = 1;  // host threads of the oracle (tko_blas_init)
 static setthreads_fn g_setthreads = nullptr;
-static int g_threads = 1;
 
 static void gemm(bool ta, bool tb, Index m, Index n, Index k, double alpha, const double* a,
                  Index lda, const double* b, Index ldb, double beta, double* c, Index ldc) {
@@ -170,8 +170,8 @@ inline double normal_at_key(uint64_t key, uint64_t index) {  // random.hpp:63-71
     const double angle = 6.283185307179586476925287 * u2;
     return (index & 1u) ? r * std::sin(angle) : r * std::cos(angle);
 }
-inline void gaussian_fill(double* p, uint64_t n, uint64_t key) {  // random.hpp:85-100,124-138
-    for (uint64_t i = 0; i < n; i += 2) {
+inline void gaussian_fill_range(double* p, uint64_t lo, uint64_t hi, uint64_t n, uint64_t key) {
+    for (uint64_t i = lo; i < hi; i += 2) {  // lo even: Box-Muller pairs (2k, 2k+1)
         const double u1 = counter_unit(key, i);
         const double u2 = counter_unit(key, i + 1);
         const double r = std::sqrt(-2.0 * std::log(u1));
@@ -179,6 +179,18 @@ inline void gaussian_fill(double* p, uint64_t n, uint64_t key) {  // random.hpp:
         p[i] = r * std::cos(angle);
         if (i + 1 < n) p[i + 1] = r * std::sin(angle);
     }
+}
+// random.hpp:85-100,124-138: every entry a pure function of (key, index), so the fill is split
+// over the oracle's host threads at even boundaries (values independent of the split)
+inline void gaussian_fill(double* p, uint64_t n, uint64_t key) {
+    const uint64_t nt = std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(g_threads), n >> 20));
+    if (nt == 1) return gaussian_fill_range(p, 0, n, n, key);
+    std::vector<std::thread> pool;
+    for (uint64_t w = 0; w < nt; ++w) {
+        const uint64_t lo = (n * w / nt) & ~uint64_t(1), hi = w + 1 == nt ? n : (n * (w + 1) / nt) & ~uint64_t(1);
+        pool.emplace_back([=] { gaussian_fill_range(p, lo, hi, n, key); });
+    }
+    for (auto& th : pool) th.join();
 }
 inline Mat gaussian_matrix(Index rows, Index cols, const Seed& s) {  // random.hpp:85-100
     require(rows >= 1 && cols >= 1, "gaussian_matrix: dimensions must be positive");
@@ -645,6 +657,134 @@ inline Tucker rand_tucker_2i(const Tensor& y, const std::vector<Index>& ranks, I
     }
     Tucker m;
     m.core = ttm_all(y, factors, -1, true);  // tucker.hpp:166
+    m.factors = std::move(factors);
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// Streamed-slab restatement of rand_tucker_2i for tensors whose fp64 copy does not fit in
+// host memory (BASELINE cfgs 3-5: 55-256 GB of fp32). Y is read as contiguous slabs of its
+// last mode (fp32 -> fp64 per slab) and every ttm_all is accumulated slab by slab in slab
+// order, the pattern of the reference's streamed_block_product (dist.hpp:496-596) and
+// dist_project (dist.hpp:617-651): with slab s = Y[..., a:b],
+//   ttm_all(Y, U, skip) = sum_s ttm_all(Y_s, U, skip) restricted to rows a:b of U_last
+// (skip != last) or the slabs of ttm_all(Y_s, U, skip) placed at a:b (skip == last).
+// Same modes, same order of application (ascending, tensor.hpp:186-190) and the same
+// rand_tucker_2i control flow (tucker.hpp:136-169) as rand_tucker_2i() above; only the
+// summation order over the last mode differs (per slab, then over slabs, fp64).
+// ---------------------------------------------------------------------------
+struct SlabSource {
+    const float* y32 = nullptr;
+    std::vector<Index> shape;
+    Index front = 1;      // prod of all but the last extent
+    Index slab_len = 1;   // last-mode rows per slab
+};
+
+// fp32 -> fp64 copy of rows [a, b) of the last mode, split over g_threads host threads
+inline Tensor load_slab(const SlabSource& src, Index a, Index b) {
+    std::vector<Index> s = src.shape;
+    s.back() = b - a;
+    Tensor t(s);
+    const float* from = src.y32 + a * src.front;
+    double* to = t.data();
+    const Index n = t.size();
+    const int nt = std::max(1, std::min<int>(g_threads, static_cast<int>(n / (1 << 20)) + 1));
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nt; ++w) {
+        const Index lo = n * w / nt, hi = n * (w + 1) / nt;
+        pool.emplace_back([=] {
+            for (Index i = lo; i < hi; ++i) to[i] = static_cast<double>(from[i]);
+        });
+    }
+    for (auto& th : pool) th.join();
+    return t;
+}
+
+// ttm_all(Y, ms, skip, transpose=true) over the slabs of Y (skip = -1: every mode)
+inline Tensor ttm_all_streamed(const SlabSource& src, const std::vector<Mat>& ms, Index skip) {
+    const Index order = static_cast<Index>(src.shape.size());
+    const Index last = order - 1;
+    const Index L = src.shape.back();
+    std::vector<Index> os(src.shape);
+    for (Index n = 0; n < order; ++n)
+        if (n != skip) os[static_cast<size_t>(n)] = ms[static_cast<size_t>(n)].cols;
+    Tensor x(os);
+    std::vector<Mat> mt(static_cast<size_t>(order));
+    for (Index n = 0; n < last; ++n)
+        if (n != skip) mt[static_cast<size_t>(n)] = transpose(ms[static_cast<size_t>(n)]);
+    for (Index a = 0; a < L; a += src.slab_len) {
+        const Index b = std::min(L, a + src.slab_len);
+        Tensor cur = load_slab(src, a, b);
+        for (Index n = 0; n < last; ++n) {  // ascending modes, as tensor.hpp:186-190
+            if (n == skip) continue;
+            cur = ttm(cur, mt[static_cast<size_t>(n)], n);
+        }
+        if (skip == last) {  // the slab's rows of X (contiguous: last mode slowest)
+            std::copy(cur.d.begin(), cur.d.end(), x.d.begin() + a * (x.size() / L));
+            continue;
+        }
+        // X += cur x_last U_last[a:b, :]^T (the slab's share of the last-mode contraction)
+        const Mat& u = ms[static_cast<size_t>(last)];
+        const Index front = cur.size() / (b - a);
+        gemm(false, false, front, u.cols, b - a, 1.0, cur.data(), front, u.data() + a, u.rows, 1.0, x.data(), front);
+    }
+    return x;
+}
+
+// Diagnostics of the two discrete choices of a range step (hard part 1):
+// pivot margin = min_k (top - second) / top of the updated column norms at ColPiv step k
+// (range_finder.hpp:18-29); sign margin = min over columns of (|u|_max - max |u_i| over the
+// entries of the opposite sign) / |u|_max (fix_column_signs, tucker.hpp:39-45): how close the
+// sign rule is to picking an entry of the other sign.
+inline double sign_margin(const Mat& u) {
+    double m = 1.0;
+    for (Index j = 0; j < u.cols; ++j) {
+        Index imax = 0;
+        double best = -1.0;
+        for (Index i = 0; i < u.rows; ++i)
+            if (std::abs(u(i, j)) > best) best = std::abs(u(i, j)), imax = i;
+        const bool pos = u(imax, j) >= 0;
+        double opp = 0.0;
+        for (Index i = 0; i < u.rows; ++i)
+            if ((u(i, j) >= 0) != pos) opp = std::max(opp, std::abs(u(i, j)));
+        if (best > 0) m = std::min(m, (best - opp) / best);
+    }
+    return m;
+}
+
+inline Tucker rand_tucker_2i_streamed(const SlabSource& src, const std::vector<Index>& ranks, Index p,
+                                      const Seed& seed, std::vector<Mat>* z_out, std::vector<double>* margins) {
+    const Index order = static_cast<Index>(src.shape.size());
+    require(order >= 2, "rand_tucker_2i: streamed oracle needs order >= 2");
+    require(static_cast<Index>(ranks.size()) == order, "rand_tucker_2i: one rank per mode required");
+    require(p >= 0, "rand_tucker_2i: oversampling must be nonnegative");
+    std::vector<Mat> factors(static_cast<size_t>(order));
+    for (Index n = 0; n < order; ++n) {  // tucker.hpp:141-147
+        const Index rt = std::min(ranks[static_cast<size_t>(n)] + p, src.shape[static_cast<size_t>(n)]);
+        factors[static_cast<size_t>(n)] = gaussian_matrix(src.shape[static_cast<size_t>(n)], rt, alg3_init_seed(seed, n));
+    }
+    for (Index pass = 0; pass < 2; ++pass) {  // tucker.hpp:149-162
+        for (Index n = 0; n < order; ++n) {
+            const Tensor x = ttm_all_streamed(src, factors, n);
+            const Index rt = std::min(ranks[static_cast<size_t>(n)] + p, src.shape[static_cast<size_t>(n)]);
+            const Index width = x.size() / x.dim(n);
+            const Mat omega = gaussian_matrix(width, rt, alg3_omega_seed(seed, pass, n));
+            Mat z = unfold_times(x, n, omega);
+            ColPivQR f;
+            Mat u = orthonormal_basis(z, &f);
+            fix_column_signs(u);
+            if (margins) {
+                double pm = 1.0;
+                for (Index k = 0; k + 1 < u.cols; ++k) pm = std::min(pm, f.pivot_margin[static_cast<size_t>(k)]);
+                margins->push_back(pm);
+                margins->push_back(sign_margin(u));
+            }
+            if (z_out) z_out->push_back(std::move(z));
+            factors[static_cast<size_t>(n)] = std::move(u);
+        }
+    }
+    Tucker m;
+    m.core = ttm_all_streamed(src, factors, -1);  // tucker.hpp:166
     m.factors = std::move(factors);
     return m;
 }
@@ -1181,6 +1321,29 @@ int tko_rand_tucker_2i(const int64_t* shape, int64_t order, const double* y, con
         if (z_out)
             for (size_t i = 0; i < zs.size(); ++i)
                 std::memcpy(z_out[i], zs[i].data(), sizeof(double) * zs[i].d.size());
+    })
+}
+// Streamed-slab rand_tucker_2i on an fp32 host tensor (slab_elems: target fp64 elements per
+// slab of the last mode); margins (optional, 4N doubles): per step (pivot margin, sign margin).
+int tko_rand_tucker_2i_f32_streamed(const int64_t* shape, int64_t order, const float* y, const int64_t* ranks,
+                                    int64_t p, uint64_t root, uint64_t stream, int64_t slab_elems, double* core,
+                                    int64_t* core_shape, double** factors, int64_t* cols, double** z_out,
+                                    double* margins) {
+    TKO_TRY({
+        SlabSource src;
+        src.y32 = y;
+        src.shape = to_shape(shape, order);
+        for (int64_t n = 0; n + 1 < order; ++n) src.front *= shape[n];
+        src.slab_len = std::max<Index>(1, std::min<Index>(shape[order - 1], slab_elems / src.front));
+        std::vector<Mat> zs;
+        std::vector<double> mg;
+        Tucker m = rand_tucker_2i_streamed(src, to_shape(ranks, order), p, Seed{root, stream}, z_out ? &zs : nullptr,
+                                           margins ? &mg : nullptr);
+        write_model(m, core, core_shape, factors, cols);
+        if (z_out)
+            for (size_t i = 0; i < zs.size(); ++i)
+                std::memcpy(z_out[i], zs[i].data(), sizeof(double) * zs[i].d.size());
+        if (margins) std::memcpy(margins, mg.data(), sizeof(double) * mg.size());
     })
 }
 // The reference's distributed algorithms (dist.hpp:852-936) on the assembled tensor:

@@ -55,6 +55,9 @@ SIGNATURES = {
     "tk_context_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "tk_context_set_comm": (C.c_int, [C.c_void_p, C.POINTER(tk_comm)]),
     "tk_context_synchronize": (C.c_int, [C.c_void_p]),
+    "tk_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "tk_context_set_nccl": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int]),
+    "tk_nccl_version": (C.c_int, []),
     "tk_context_set_ttm_path": (C.c_int, [C.c_void_p, C.c_int]),
     "tk_context_set_orthonormalizer": (C.c_int, [C.c_void_p, C.c_int]),
     "tk_gram_orthonormalize": (C.c_int, [C.c_void_p, I64, I64, PD, PD, PD, PI64]),
@@ -106,6 +109,16 @@ def load(build_if_missing: bool = True):
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+TK_NCCL_UNIQUE_ID_BYTES = 128
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 of a native communicator)."""
+    buf = C.create_string_buffer(TK_NCCL_UNIQUE_ID_BYTES)
+    check(load().tk_nccl_unique_id(buf))
+    return buf.raw
 
 
 def check(rc: int):

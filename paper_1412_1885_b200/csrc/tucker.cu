@@ -8,6 +8,8 @@
 // core = X_{N-1} x_{N-1} U_{N-1}^T (the reference's extra pass at tucker.hpp:166 computes
 // the same tensor with the same operation order; opts.explicit_core_pass restores it).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -24,6 +26,48 @@
 
 using namespace tkb;
 
+namespace {
+// NCCL resolved at run time (no link-time dependency: the library loads on hosts without NCCL
+// and fails only when a native communicator is requested). The process's already-loaded
+// libnccl.so.2 (torch's) is preferred; TENKIT_NCCL_LIB overrides the path.
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    ncclResult_t (*get_version)(int*) = nullptr;
+    bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = nullptr;
+        if (const char* e = std::getenv("TENKIT_NCCL_LIB")) h = dlopen(e, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.get_version = reinterpret_cast<decltype(a.get_version)>(dlsym(h, "ncclGetVersion"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy && a.error_string;
+        return a;
+    }();
+    if (!api.ok) throw std::runtime_error("NCCL (libnccl.so.2) unavailable");
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw std::runtime_error(std::string("nccl: ") + what + ": " + nccl_api().error_string(r));
+}
+}  // namespace
+
 struct tk_context {
     int device = 0;
     cudaStream_t own = nullptr;
@@ -32,6 +76,11 @@ struct tk_context {
     int ttm_path = 0;  // 0 auto (tcgen05 for fp32 Y streams), 1 FFMA only, 2 tcgen05 whenever supported
     int ortho = TK_ORTHO_COLPIV;  // range-step basis: ColPiv QR + sign rule, or the dist protocol's Gram-eig
     tk_comm comm{};
+    // native NCCL communicator (tk_context_set_nccl): the partial sketches / cores are
+    // all-reduced in place on the call's stream, no host callback, CUDA graphs stay enabled
+    ncclComm_t nccl = nullptr;
+    int nccl_rank = 0, nccl_world = 0;
+    uint64_t nccl_gen = 0;  // bumped per communicator (part of the graph key)
     std::map<std::string, std::pair<void*, size_t>> bufs;
     int* rank_host = nullptr;  // pinned
     cudaStream_t side = nullptr;  // second stream: next Y pass overlapped with the current QR
@@ -85,8 +134,17 @@ struct tk_context {
         }
         return e.first;
     }
+    void drop_nccl() {
+        if (nccl) nccl_api().comm_destroy(nccl);
+        nccl = nullptr;
+        nccl_world = 0;
+    }
     ~tk_context() {
         g2i.reset();
+        try {
+            drop_nccl();
+        } catch (...) {
+        }
         if (ev_cap) cudaEventDestroy(ev_cap);
         if (cap) cudaStreamDestroy(cap);
         for (auto& kv : bufs)
@@ -304,10 +362,11 @@ struct TuckerRun {
         return fallback;
     }
 
-    // Mode 0 can lead a Y pass when the K-major tcgen05 kernel takes it (fp32, I_0 % 4 == 0).
-    // Only on the tcgen05-everywhere path (2): a 512-row-tile Y pass keeps one accumulator
-    // set, whose truncating accumulation over K = I_0 doubles the fp32 basis error in the
-    // noise directions relative to leading with an M-major pass (measured at cfg 2).
+    // Mode 0 can lead a Y pass when the K-major tcgen05 kernel takes it (fp32, I_0 % 4 == 0,
+    // r~_0 <= TENKIT_KM_LEAD_MAX = 64, >= 148 row tiles), on the auto and tc paths (not the
+    // FFMA-only path 1). stream_ttm always asks for the accurate variant: 128-row tiles with
+    // 2-4 accumulator sets (the truncating tensor-core accumulation over K = I_0 is split
+    // across the sets; a 512-row single-set tile doubled the fp32 basis error at cfg 2).
     bool km_stream_ok() const {
         if constexpr (sizeof(T) != 4) {
             return false;
@@ -452,7 +511,13 @@ struct TuckerRun {
     }
 
     void allreduce(double* buf, int64_t count) {
-        if (!ctx->has_comm || ctx->comm.world <= 1) return;
+        if (!ctx->has_comm) return;
+        if (ctx->nccl) {  // in place, on this call's stream (captured into the graph when capturing)
+            nccl_check(nccl_api().all_reduce(buf, buf, static_cast<size_t>(count), ncclFloat64, ncclSum, ctx->nccl, s),
+                       "ncclAllReduce");
+            return;
+        }
+        if (ctx->comm.world <= 1) return;
         const tk_comm& c = ctx->comm;
         require(count <= c.xbuf_capacity, "comm: exchange buffer too small");
         if (buf != c.xbuf) TK_CUDA(cudaMemcpyAsync(c.xbuf, buf, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -862,14 +927,17 @@ bool graphs_enabled() {
 // the context's private stream, then copies the model out and verifies the speculated ranks.
 // Returns false when the eager path must run (first sighting of this call, or a rank drop).
 template <typename T>
-bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, const T* ydev,
-              const std::vector<int64_t>& rk, int64_t p, const Seed& seed, const tk_tucker_opts& opt, tk_tucker_out* out,
-              tk_tucker_stats* stats) {
+bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, const std::vector<int64_t>& gd,
+              const std::vector<int64_t>& off, const T* ydev, const std::vector<int64_t>& rk, int64_t p,
+              const Seed& seed, const tk_tucker_opts& opt, tk_tucker_out* out, tk_tucker_stats* stats) {
     std::string key = std::to_string(sizeof(T)) + "|" + std::to_string(reinterpret_cast<uintptr_t>(ydev)) + "|" +
                       std::to_string(p) + "|" + std::to_string(seed.root) + "|" + std::to_string(seed.stream) + "|" +
                       std::to_string(opt.explicit_core_pass) + std::to_string(opt.overlap) + std::to_string(opt.one_pass_per_step) +
-                      std::to_string(opt.time_kernels) + "|" + std::to_string(ctx->ttm_path) + "|" + std::to_string(ctx->ortho);
-    for (int64_t n = 0; n < order; ++n) key += "|" + std::to_string(ld[n]) + "x" + std::to_string(rk[n]);
+                      std::to_string(opt.time_kernels) + "|" + std::to_string(ctx->ttm_path) + "|" + std::to_string(ctx->ortho) +
+                      "|nccl" + std::to_string(ctx->has_comm && ctx->nccl ? ctx->nccl_gen : 0);
+    for (int64_t n = 0; n < order; ++n)
+        key += "|" + std::to_string(ld[n]) + "x" + std::to_string(rk[n]) + "@" + std::to_string(off[n]) + "/" +
+               std::to_string(gd[n]);
     auto& g = ctx->g2i;
     if (g.key != key || (g.exec && g.buf_gen != ctx->buf_gen)) {
         g.reset();
@@ -882,7 +950,7 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
             TK_CUDA(cudaEventCreateWithFlags(&ctx->ev_cap, cudaEventDisableTiming));
         }
         ctx->ensure_side();
-        TuckerRun<T> r{ctx, ctx->cap, order, ld, ld, std::vector<int64_t>(order, 0), ydev};
+        TuckerRun<T> r{ctx, ctx->cap, order, ld, gd, off, ydev};
         r.time_kernels = opt.time_kernels != 0;
         r.capture = true;
         cudaGraph_t graph = nullptr;
@@ -920,7 +988,7 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
     for (int64_t n = 0; n < order; ++n) {
         out->core_shape[n] = g.cshape[n];
         out->factor_cols[n] = g.cols[n];
-        TK_CUDA(cudaMemcpyAsync(out->factors[n], g.U[n], sizeof(double) * ld[n] * g.cols[n], kind, s));
+        TK_CUDA(cudaMemcpyAsync(out->factors[n], g.U[n], sizeof(double) * gd[n] * g.cols[n], kind, s));
     }
     TK_CUDA(cudaStreamSynchronize(s));
     for (int i = 0; i < 2 * order; ++i)
@@ -960,8 +1028,10 @@ void rand_tucker_2i_impl(tk_context* ctx, int64_t order, const int64_t* dims, co
         r.time_kernels = o.time_kernels != 0;
         r.run(rk, p, seed, o, out, stats);
     };
-    if (!opt.sync_ranks && y_on_device && !(ctx->has_comm && ctx->comm.world > 1) && graphs_enabled() &&
-        graph_2i<T>(ctx, order, ld, ydev, rk, p, seed, opt, out, stats))
+    // graphs: single process, or a native NCCL communicator (its all-reduces are captured);
+    // the host-callback hook runs eagerly
+    if (!opt.sync_ranks && y_on_device && !(ctx->has_comm && ctx->comm.world > 1 && !ctx->nccl) &&
+        graphs_enabled() && graph_2i<T>(ctx, order, ld, gd, offset, ydev, rk, p, seed, opt, out, stats))
         return;
     if (opt.sync_ranks) {
         attempt(opt);
@@ -1054,9 +1124,55 @@ int tk_context_set_comm(tk_context* ctx, const tk_comm* comm) {
             return;
         }
         require(comm->world >= 1 && comm->rank >= 0 && comm->rank < comm->world, "comm: bad rank/world");
-        require(comm->world == 1 || (comm->allreduce_sum && comm->xbuf), "comm: missing reduction hook");
+        if (ctx->nccl)
+            require(comm->world == ctx->nccl_world && comm->rank == ctx->nccl_rank,
+                    "comm: rank/world differ from the native NCCL communicator");
+        else
+            require(comm->world == 1 || (comm->allreduce_sum && comm->xbuf), "comm: missing reduction hook");
         ctx->comm = *comm;
         ctx->has_comm = true;
+    });
+}
+
+int tk_nccl_unique_id(unsigned char* out) {
+    return guarded([&] {
+        require(out != nullptr, "null output");
+        ncclUniqueId id;
+        nccl_check(nccl_api().get_unique_id(&id), "ncclGetUniqueId");
+        static_assert(sizeof(id) == TK_NCCL_UNIQUE_ID_BYTES, "ncclUniqueId size");
+        std::memcpy(out, &id, sizeof(id));
+    });
+}
+
+int tk_nccl_version(void) {
+    try {
+        int v = 0;
+        const NcclApi& a = nccl_api();
+        if (a.get_version && a.get_version(&v) == ncclSuccess) return v;
+    } catch (...) {
+    }
+    return 0;
+}
+
+int tk_context_set_nccl(tk_context* ctx, const unsigned char* id, int rank, int world) {
+    return guarded([&] {
+        check_ctx(ctx);
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->g2i.reset();  // captured graphs hold the old communicator's collectives
+        ctx->drop_nccl();
+        if (world == 0) return;  // tear down only
+        require(id != nullptr && world >= 1 && rank >= 0 && rank < world, "nccl: bad rank/world");
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        ncclComm_t c = nullptr;
+        nccl_check(nccl_api().comm_init_rank(&c, world, uid, rank), "ncclCommInitRank");
+        ctx->nccl = c;
+        ctx->nccl_rank = rank;
+        ctx->nccl_world = world;
+        ++ctx->nccl_gen;
+        if (std::getenv("TENKIT_NCCL_VERBOSE"))
+            std::fprintf(stderr, "tenkit: native NCCL communicator %d.%d rank %d of %d on device %d\n",
+                         tk_nccl_version() / 10000, (tk_nccl_version() / 100) % 100, rank, world, ctx->device);
     });
 }
 

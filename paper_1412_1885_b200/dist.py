@@ -170,7 +170,7 @@ class DistComm:
     (slab_offset, global_last_dim) or, with `block_lo`/`global_dims`, a general block."""
 
     def __init__(self, slab_offset: int, global_last_dim: int, capacity: int, group=None, device=None,
-                 block_lo=None, global_dims=None):
+                 block_lo=None, global_dims=None, native: bool = False):
         import torch
         import torch.distributed as dist
         self.group = group
@@ -190,6 +190,22 @@ class DistComm:
         self.log = None  # MessageLog to record into, with self.plan (exchange_plan)
         self.plan = None
         self._cb = _lib.ALLREDUCE_FN(self._allreduce)
+        # native: the library's own NCCL communicator (tk_context_set_nccl) sums in place on its
+        # stream — only over an NCCL process group (one process per GPU); the torch.distributed
+        # callback remains for gloo (CPU tests, ranks sharing a GPU)
+        self.native = bool(native) and self.world > 1 and dev != "cpu" and dist.get_backend(group) == "nccl"
+        self.nccl_id = None
+        if self.native:
+            ids = [_lib.nccl_unique_id() if self.rank == 0 else None]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(ids, src=src, group=group)
+            self.nccl_id = ids[0]
+
+    def describe(self) -> str:
+        if self.native:
+            v = _lib.load().tk_nccl_version()
+            return f"native NCCL {v // 10000}.{(v // 100) % 100}.{v % 100} communicator, rank {self.rank} of {self.world}"
+        return f"torch.distributed callback, rank {self.rank} of {self.world}"
 
     def _record(self, count: int):
         if self.log is None or not self.plan:
@@ -229,7 +245,7 @@ class DistComm:
         s.global_last_dim = self.global_last_dim
         s.xbuf = C.cast(C.c_void_p(self.xbuf.data_ptr()), _lib.PD)
         s.xbuf_capacity = self.xbuf.numel()
-        s.allreduce_sum = self._cb
+        s.allreduce_sum = self._cb  # unused with a native communicator (the library sums in place)
         s.user = None
         s.blocked = 0 if self.block_lo is None else 1
         if self.block_lo is not None:
@@ -285,7 +301,12 @@ def dist_rand_tucker_2i(local_y, global_dims, lo, ranks, oversample, seed, *, co
     extents and the block's first index per mode (GridPlan.block), or — the slab form — the
     global last-mode size and the slab offset. Every rank returns the same model (replicated
     QR; the factors equal the single-node rand_tucker_2i's, not a rotation of them).
-    orthonormalizer='gram': the reference's own dist basis (Gram-eig, dist.hpp:688-723).
+
+    DIVERGENCE FROM THE REFERENCE'S DEFAULT: the reference's dist_rand_tucker_2i orthonormalises
+    with the Gram-eig transform and applies no sign rule (dist.hpp:688-723), so its factors
+    match the single-node ones only up to rotation (test_dist.cpp:141-152). This default
+    (orthonormalizer='colpiv') returns the single-node model (SURVEY §8e parity target);
+    pass orthonormalizer='gram' for the reference's dist numerics bit-for-bit in protocol.
     log=MessageLog(): records this rank's exchanges (dist.hpp:277-320)."""
     from .tenkit import rand_tucker_2i
     return _dist_call(rand_tucker_2i, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw, "2i")
@@ -296,7 +317,9 @@ def dist_rand_tucker(local_y, global_dims, lo, ranks, oversample, seed, *, conte
     global tensor whose block lives on this rank: the Omega rows of each unfolding are drawn
     at their global column ids (dist.hpp:496-596), partial sketches and the partial core are
     summed over ranks, the QR is replicated. Every rank returns the same model.
-    orthonormalizer='gram' / log=MessageLog(): as dist_rand_tucker_2i."""
+    Default basis 'colpiv' = single-node semantics; orthonormalizer='gram' = the reference's
+    dist_rand_tucker numerics (see dist_rand_tucker_2i for the divergence note).
+    log=MessageLog(): as dist_rand_tucker_2i."""
     from .tenkit import rand_tucker
     return _dist_call(rand_tucker, local_y, global_dims, lo, ranks, oversample, seed, context, group, kw, "alg2")
 

@@ -220,12 +220,30 @@ class Context:
     def synchronize(self):
         _lib.check(self.lib.tk_context_synchronize(self.handle))
 
+    def set_nccl(self, unique_id: bytes | None, rank: int = 0, world: int = 0):
+        """Install a native NCCL communicator (tk_context_set_nccl; None / world 0 tears it down).
+        The communicator is kept across calls (its creation is expensive)."""
+        if unique_id is None or world == 0:
+            _lib.check(self.lib.tk_context_set_nccl(self.handle, None, 0, 0))
+            self._nccl_key = None
+            return
+        key = (bytes(unique_id), int(rank), int(world))
+        if getattr(self, "_nccl_key", None) == key:
+            return
+        _lib.check(self.lib.tk_context_set_nccl(self.handle, bytes(unique_id), int(rank), int(world)))
+        self._nccl_key = key
+
     def set_comm(self, comm):
-        """Install a DistComm (paper_1412_1885_b200.dist) or None."""
+        """Install a DistComm (paper_1412_1885_b200.dist) or None. A native DistComm also
+        installs (once) its NCCL communicator on this context."""
         if comm is None:
             _lib.check(self.lib.tk_context_set_comm(self.handle, None))
             self._comm_keep = None
             return
+        if getattr(comm, "native", False):
+            self.set_nccl(comm.nccl_id, comm.rank, comm.world)
+        elif getattr(self, "_nccl_key", None) is not None:
+            self.set_nccl(None)
         st = comm.as_struct()
         _lib.check(self.lib.tk_context_set_comm(self.handle, C.byref(st)))
         self._comm_keep = (comm, st)
@@ -597,6 +615,8 @@ def model_fit(y, model, *, context: Context | None = None, norms: bool = False):
     farr = (_lib.PD * order)(*[_dptr(u) for u in fac])
     _lib.check(ctx.lib.tk_model_fit(ctx.handle, _dtype_code(yd), order, _i64arr(y.shape), _ptr(yd), _i64arr(cshape),
                                     _dptr(core) if core is not None else None, farr, int(rank), _dptr(sums)))
-    res, ny = float(np.sqrt(max(sums[0], 0.0))), float(np.sqrt(sums[1]))
+    res, ny = float(np.sqrt(max(sums[0], 0.0))), float(np.sqrt(max(sums[1], 0.0)))
+    if not ny > 0.0:  # tensor.hpp:285
+        raise TenkitError("tenkit: fit: reference tensor has zero norm")
     f = 1.0 - res / ny
     return (f, res, ny) if norms else f

@@ -53,8 +53,8 @@ def test_bench_functions_read_only_bound_names():
 
 
 def test_reference_arm_runs_on_the_host():
-    r = subprocess.run([sys.executable, BENCH, "--impl", "reference", "--steps", "1", "--warmup", "0",
-                        "--cpu-slabs", "4"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run([sys.executable, BENCH, "--impl", "reference", "--config", "cfg2", "--steps", "1", "--warmup",
+                        "0", "--cpu-slabs", "4"], capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
@@ -62,3 +62,21 @@ def test_reference_arm_runs_on_the_host():
         assert k in line, k
     assert line["impl"] == "reference" and line["config"]["workload"] == "cfg2"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    # the reference arm generates its sample with the oracle: the product library is never loaded
+    assert line["repo_library_loaded"] is False and line["config"]["sample_dims"] == [1000, 1000, 4]
+    assert line["host"]["nproc"] == os.cpu_count()
+
+
+def test_bench_partitions_follow_baseline():
+    """BASELINE's partitions: cfg3 mode-3 slabs at every N, cfg5 slabs at 2/4 and 2x2x2 at 8."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.bench_grid("cfg3", 3, 1, "strong") == [1, 1, 1]
+    assert bench.bench_grid("cfg3", 3, 8, "strong") == [1, 1, 8]
+    assert bench.bench_grid("cfg4", 4, 4, "strong") == [1, 1, 1, 4]
+    assert bench.bench_grid("cfg5", 3, 2, "strong") == [1, 1, 2]
+    assert bench.bench_grid("cfg5", 3, 4, "strong") == [1, 1, 4]
+    assert bench.bench_grid("cfg5", 3, 8, "strong") == [2, 2, 2]
+    assert bench.bench_grid("cfg2", 3, 8, "weak") == [2, 2, 2]
+    assert bench.sample_dims(bench.CONFIGS["cfg3"]) == [2400, 2400, 40]
+    assert bench.sample_dims(bench.CONFIGS["cfg1"]) == [200, 200, 200]

@@ -69,3 +69,24 @@ def test_rand_tucker_2i_tc_path_matches_oracle(P, O, ranks, p):
     ysq = float(np.sum(y32.astype(np.float64) ** 2))
     assert abs(float(np.sum(m.core ** 2)) - float(np.sum(g_ref ** 2))) / ysq < 1e-5
     assert m.stats["passes"] == 3  # steps share Y passes; the mode-0 pass on the K-major kernel
+
+
+@pytest.mark.parametrize("dims", [(64, 150, 150), (128, 160, 120)])
+def test_rand_tucker_2i_wide_kmajor_leader_matches_oracle(P, O, dims):
+    """r~ = 60 (ranks 50, p 10): mode 0 leads a Y pass on the NH = 64 K-major tcgen05 kernel
+    (one CTA per SM, 3 accumulator sets) with the transposed output (tout), fp32 vs the oracle."""
+    seed = (3, 9)
+    ranks, p = (50, 50, 50), 10
+    y = O.add_noise(O.gen_tucker(dims, (12, 12, 12), seed), 20.0, O.seed_derived(*seed, 0xAD0))
+    y32 = y.astype(np.float32)
+    O.set_threads(8)
+    g_ref, u_ref = O.rand_tucker_2i(y32.astype(np.float64), ranks, p, (7, 1))
+    O.set_threads(1)
+    m = P.rand_tucker_2i(P.DenseTensor.from_numpy(y32, np.float32).cuda(), ranks, p, (7, 1), sync_ranks=False).to_host()
+    assert m.stats["passes"] == 3
+    for u, v in zip(m.factors, u_ref):
+        assert u.shape == v.shape == (u.shape[0], min(60, u.shape[0]))
+        assert orthonormality_defect(u) < 1e-10
+        assert subspace_dist(u, v) < 1e-3
+    aligned = O.ttm_all(m.core, [u.T @ v for u, v in zip(m.factors, u_ref)], -1, False)
+    assert rel(aligned, g_ref) < 1e-3

@@ -136,3 +136,15 @@ def test_rng_bit_exact_vs_numpy_restatement(O):
         assert all(u[i] == O.uniform_at(root, stream, int(i)) for i in range(0, 2000, 97))
         ref = O.gaussian_matrix(2000, 1, (root, stream)).ravel()
         assert np.max(np.abs(np_normal(key, idx) - ref) / np.maximum(np.abs(ref), 1e-300)) < 4e-16
+
+
+def test_threaded_gaussian_fill_is_split_invariant(O):
+    """The oracle splits large gaussian fills over host threads at even (Box-Muller pair)
+    boundaries: every entry stays normal_at(seed, index) (random.hpp:63-71, 124-138)."""
+    O.set_threads(1)
+    a = O.gaussian_matrix(3_000_001, 1, (3, 4))
+    O.set_threads(7)
+    b = O.gaussian_matrix(3_000_001, 1, (3, 4))
+    O.set_threads(1)
+    assert np.array_equal(a, b)
+    assert a[2_999_999, 0] == O.normal_at(3, 4, 2_999_999) and a[3_000_000, 0] == O.normal_at(3, 4, 3_000_000)

@@ -238,3 +238,21 @@ def test_cp_uniform_generator(O):
     # counter indexing mirrors bench.hpp:63-71: entry (i, j) of factor n at j*I_n + i
     fseed = O.seed_derived(1, 2, 0x9E4, 1)
     assert fs[1][3, 2] == O.uniform_at(fseed[0], fseed[1], 2 * 5 + 3)
+
+
+# ------------------------------------------------------------------ streamed-slab oracle
+@pytest.mark.parametrize("dims", [(30, 26, 22), (12, 10, 9, 8), (40, 33)])
+@pytest.mark.parametrize("slab_elems", [1, 100, 1 << 30])
+def test_streamed_oracle_matches_whole_tensor(O, dims, slab_elems):
+    """The full-size checker (rand_tucker_2i over last-mode slabs of an fp32 host tensor,
+    dist.hpp:496-596 pattern) equals the whole-tensor restatement on the same fp32 values:
+    only the fp64 summation order over the last mode differs."""
+    ranks = [3] * len(dims)
+    y = O.add_noise(O.gen_tucker(dims, ranks, (0, 5)), 20.0, (0, 9))
+    y32 = y.astype(np.float32)
+    g, us = O.rand_tucker_2i(y32.astype(np.float64), ranks, 2, (1, 2))
+    g2, us2, mg = O.rand_tucker_2i_streamed(y32.ravel(order="F"), dims, ranks, 2, (1, 2), slab_elems=slab_elems)
+    for u, v in zip(us, us2):
+        assert u.shape == v.shape and np.abs(u - v).max() < 1e-12
+    assert np.abs(g - g2).max() < 1e-11 * np.abs(g).max()
+    assert mg.shape == (2 * len(dims), 2) and np.all(mg >= 0) and np.all(mg <= 1)

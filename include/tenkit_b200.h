@@ -107,6 +107,14 @@ typedef struct tk_tucker_stats {
     int ranks[2 * TK_MAX_ORDER];
     int stream_launches;   /* Y-streaming (first-stage TTM) launches */
     double stream_ms;      /* their summed CUDA-event time (time_kernels = 1) */
+    /* Per range step (pass * N + n; Alg. 2: n) diagnostics of the two discrete choices:
+     * pivot margin = min over ColPiv steps of (top - second) / top of the remaining column
+     * norms (range_finder.hpp:18-29); sign margin = min over columns of (max |u_i| of the
+     * chosen sign - max |u_i| of the other sign) / max |u_i| (tucker.hpp:39-45); qr_path 0 =
+     * pivoted CholeskyQR2, 1 = Householder (ill-conditioned Z or a near-tie pivot). */
+    double pivot_margin[2 * TK_MAX_ORDER];
+    double sign_margin[2 * TK_MAX_ORDER];
+    int qr_path[2 * TK_MAX_ORDER];
 } tk_tucker_stats;
 
 const char* tk_last_error(void);
@@ -138,7 +146,8 @@ int tk_context_set_nccl(tk_context* ctx, const unsigned char* id, int rank, int 
 int tk_nccl_version(void);
 /* Contraction kernels for the Y-streaming TTM passes: 0 auto (tcgen05 3xTF32 UMMA for fp32
  * data when the shape tiles the GPU, FFMA otherwise), 1 FFMA only, 2 tcgen05 whenever the
- * shape is supported (also for the kernel-level tk_ttm) */
+ * shape is supported (also for the kernel-level tk_ttm), 3 as 2 with the kernel-level tk_ttm
+ * on the Y-streaming kernel (ttm_stream.cu) when an M-major shape qualifies */
 int tk_context_set_ttm_path(tk_context* ctx, int path);
 /* Basis of every range step (tk_rand_tucker_2i / tk_rand_tucker, any comm):
  * TK_ORTHO_COLPIV (default) = orthonormal_basis + fix_column_signs (tucker.hpp:39-45,
@@ -174,6 +183,11 @@ int tk_unfold_times(tk_context* ctx, int dtype, int64_t order, const int64_t* di
 /* orthonormal_basis + fix_column_signs: q (rows x cols capacity, double) and the rank */
 int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* q, int64_t* rank,
                          double* rdiag);
+/* The same with the step's QR diagnostics: margins (host, 3 doubles, may be null) = pivot margin,
+ * sign margin, QR path (0 pivoted CholeskyQR2, 1 Householder: ill-conditioned Z or a pivot
+ * whose two best candidates are within the near-tie gap), as in tk_tucker_stats. */
+int tk_orthonormal_basis_ex(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* q, int64_t* rank,
+                            double* rdiag, double* margins);
 /* gram_orthonormalize of the stacked blocks (one device matrix z, rows x cols, cols <= 64):
  * u (rows x cols capacity, columns >= kept zero), spectrum (cols, descending, zero after
  * kept) and kept. TK_ERR_INVALID "all blocks are zero" for a zero Z. */

@@ -680,14 +680,17 @@ struct SlabSource {
     Index slab_len = 1;   // last-mode rows per slab
 };
 
-// fp32 -> fp64 copy of rows [a, b) of the last mode, split over g_threads host threads
-inline Tensor load_slab(const SlabSource& src, Index a, Index b) {
+// fp32 -> fp64 copy of rows [a, b) of the last mode into `t` (reused across slabs: one
+// allocation, no per-slab zero fill or page faults), split over g_threads host threads
+inline void load_slab(const SlabSource& src, Index a, Index b, Tensor& t) {
     std::vector<Index> s = src.shape;
     s.back() = b - a;
-    Tensor t(s);
+    const Index n = src.front * (b - a);
+    if (static_cast<Index>(t.d.size()) < n) t.d.resize(static_cast<size_t>(n));
+    t.d.resize(static_cast<size_t>(n));
+    t.shape = s;
     const float* from = src.y32 + a * src.front;
     double* to = t.data();
-    const Index n = t.size();
     const int nt = std::max(1, std::min<int>(g_threads, static_cast<int>(n / (1 << 20)) + 1));
     std::vector<std::thread> pool;
     for (int w = 0; w < nt; ++w) {
@@ -697,7 +700,6 @@ inline Tensor load_slab(const SlabSource& src, Index a, Index b) {
         });
     }
     for (auto& th : pool) th.join();
-    return t;
 }
 
 // ttm_all(Y, ms, skip, transpose=true) over the slabs of Y (skip = -1: every mode)
@@ -712,13 +714,19 @@ inline Tensor ttm_all_streamed(const SlabSource& src, const std::vector<Mat>& ms
     std::vector<Mat> mt(static_cast<size_t>(order));
     for (Index n = 0; n < last; ++n)
         if (n != skip) mt[static_cast<size_t>(n)] = transpose(ms[static_cast<size_t>(n)]);
+    Tensor slab;
+    slab.d.reserve(static_cast<size_t>(src.front * std::min(L, src.slab_len)));
     for (Index a = 0; a < L; a += src.slab_len) {
         const Index b = std::min(L, a + src.slab_len);
-        Tensor cur = load_slab(src, a, b);
+        load_slab(src, a, b, slab);
+        Tensor cur;
+        bool first = true;
         for (Index n = 0; n < last; ++n) {  // ascending modes, as tensor.hpp:186-190
             if (n == skip) continue;
-            cur = ttm(cur, mt[static_cast<size_t>(n)], n);
+            cur = ttm(first ? slab : cur, mt[static_cast<size_t>(n)], n);
+            first = false;
         }
+        if (first) cur = slab;  // order 1 + skip: nothing to contract before the last mode
         if (skip == last) {  // the slab's rows of X (contiguous: last mode slowest)
             std::copy(cur.d.begin(), cur.d.end(), x.d.begin() + a * (x.size() / L));
             continue;

@@ -42,7 +42,9 @@ class tk_tucker_opts(C.Structure):
 
 class tk_tucker_stats(C.Structure):
     _fields_ = [("passes", C.c_int), ("kernel_launches", C.c_int), ("y_bytes", C.c_double),
-                ("ranks", C.c_int * (2 * TK_MAX_ORDER)), ("stream_launches", C.c_int), ("stream_ms", C.c_double)]
+                ("ranks", C.c_int * (2 * TK_MAX_ORDER)), ("stream_launches", C.c_int), ("stream_ms", C.c_double),
+                ("pivot_margin", C.c_double * (2 * TK_MAX_ORDER)), ("sign_margin", C.c_double * (2 * TK_MAX_ORDER)),
+                ("qr_path", C.c_int * (2 * TK_MAX_ORDER))]
 
 
 # name -> (restype, argtypes); the exported surface of include/tenkit_b200.h
@@ -70,6 +72,7 @@ SIGNATURES = {
     "tk_ttm_all": (C.c_int, [C.c_void_p, C.c_int, I64, PI64, C.c_void_p, C.POINTER(PD), PI64, I64, C.c_void_p]),
     "tk_unfold_times": (C.c_int, [C.c_void_p, C.c_int, I64, PI64, C.c_void_p, I64, PD, I64, PD]),
     "tk_orthonormal_basis": (C.c_int, [C.c_void_p, I64, I64, PD, PD, PI64, PD]),
+    "tk_orthonormal_basis_ex": (C.c_int, [C.c_void_p, I64, I64, PD, PD, PI64, PD, PD]),
     "tk_gaussian_matrix": (C.c_int, [C.c_void_p, I64, I64, U64, U64, PD]),
     "tk_gaussian_fill": (C.c_int, [C.c_void_p, I64, U64, U64, U64, PD]),
     "tk_gaussian_fill_block": (C.c_int, [C.c_void_p, I64, PI64, PI64, PI64, U64, U64, PD]),

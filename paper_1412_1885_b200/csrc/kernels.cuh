@@ -48,6 +48,16 @@ void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void*
 int launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                   cudaStream_t s, bool accurate = false, bool tout = false, float* work = nullptr,
                   int64_t work_elems = 0);
+// Second-design Y-streaming pass (ttm_stream.cu, fp32): y_hi straight from the TMA-staged
+// shared memory, y_lo from TMEM, chunked accumulation flushed into fp32 registers, factor packed
+// by launch_pack_stream (NH = cols rounded up to 8). P == 1: contraction over mode 0 with the
+// transposed output out[q + r Q]; else out[p + r P + q P cols]. Persistent, 2 CTAs per SM.
+bool stream_ttm_enabled();
+bool stream_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols);
+int64_t stream_pack_bytes(int64_t rows, int cols);
+void launch_pack_stream(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s);
+void launch_ttm_stream(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+                       cudaStream_t s);
 // out[i] = sum_s part[s * n + i] (fixed split order)
 template <typename T>
 void launch_splitk_reduce(const T* part, T* out, int64_t n, int splits, cudaStream_t s);
@@ -120,8 +130,13 @@ void launch_cast2d(const S* in, int64_t ldi, D* out, int64_t ldo, int64_t rows, 
 // Runs as one thread-block cluster holding Z in distributed shared memory.
 // nparts > 0: z holds nparts split-K partials of Z, z[(s * ncols + j) * rows + i], summed in
 // order s = 0 .. nparts-1 while loading (launch_sketch_partials' layout).
+// margins (3 doubles, may be null): [0] pivot margin = min over pivot steps of (top - second) /
+// top of the remaining column norms, [1] sign margin = min over columns of (max |u_i| of the
+// chosen sign - max |u_i| of the other) / max |u_i|, [2] 0 = pivoted CholeskyQR2 fast path,
+// 1 = Householder path (ill-conditioned Z or a near-tie pivot, kTieGapSq).
 void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up,
-                              int up_dtype, int* rank_dev, double* diag, cudaStream_t s, int nparts = 0);
+                              int up_dtype, int* rank_dev, double* diag, cudaStream_t s, int nparts = 0,
+                              double* margins = nullptr);
 // Gram-path orthonormalisation of the distributed protocol (gram.cu; range_finder.hpp:43-105,
 // dist.hpp:688-723): U = Z T with T = V / sqrt(lambda) (descending, eigenvalues <= 1e-12 top
 // dropped), no sign rule. Same outputs as launch_orthonormal_basis (u rows x ucap, ld = rows,

@@ -115,6 +115,12 @@ __device__ void reduce_dots(Sh& sh, cg::cluster_group& cl, unsigned cs, int& par
 // one per Householder step.
 // ---------------------------------------------------------------------------------------
 constexpr double kFastMinRatio = 1e-4;  // cond(Z) <= 1e4: first-order second pass exact to ~1e-16
+// Near-tie guard: the Cholesky Schur diagonals carry a relative error up to ~eps / kFastMinRatio^2
+// (cancellation in S_jj = G_jj - sum l^2), the Householder norm downdate (the oracle's and the
+// reference's algorithm, range_finder.hpp:18-29) much less; when the two largest remaining
+// candidates of a pivot step are closer than kTieGapSq (relative, squared norms) the fast path
+// gives up and the Householder path decides the pivot.
+constexpr double kTieGapSq = 1e-6;
 
 // gp[a + b n] = sum over own rows of z[:, a] z[:, b] (full symmetric n x n)
 __device__ void gram_partial(const double* z, int ld, int nloc, int n, double* gp) {
@@ -209,10 +215,14 @@ __device__ void gram_reduce(cg::cluster_group& cl, unsigned cs, double* gp, doub
 // takes the Householder path). Per step: warp 0 picks the pivot (exact first-max via three
 // warp reductions on the non-negative doubles' bit patterns) and the scalars, all threads
 // swap and update the trailing Schur complement; ~3 block barriers per step.
-__device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rinv, int* perm, int* ctl) {
+__device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rinv, int* perm, int* ctl, double* pmargin) {
     const int tid = threadIdx.x, lane = tid & 31;
     for (int j = tid; j < n; j += kQrThreads) perm[j] = j;
     for (int e = tid; e < n * n; e += kQrThreads) rr[e] = 0.0;
+    if (tid == 0) {
+        ctl[1] = 0;
+        *pmargin = 1.0;
+    }
     __syncthreads();
     double r00 = 0.0;
     for (int k = 0; k < n; ++k) {
@@ -231,10 +241,22 @@ __device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rin
                 const unsigned cand = (j0 < n && b0 == top) ? unsigned(j0) : ((j1 < n && b1 == top) ? unsigned(j1) : 0xffffu);
                 best = static_cast<int>(__reduce_min_sync(0xffffffffu, cand));
                 if (best >= n) best = k;
+                // the largest other candidate: near-tie guard and pivot margin
+                const unsigned long long c0 = (j0 == best) ? 0ull : b0, c1 = (j1 == best) ? 0ull : b1;
+                const unsigned long long cm = c0 > c1 ? c0 : c1;
+                const unsigned h2 = __reduce_max_sync(0xffffffffu, unsigned(cm >> 32));
+                const unsigned l2 = __reduce_max_sync(0xffffffffu, (unsigned(cm >> 32) == h2) ? unsigned(cm) : 0u);
+                const double dtop = __longlong_as_double(static_cast<long long>(top));
+                const double dsec = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(h2) << 32) | l2));
+                if (lane == 0 && k + 1 < n) {
+                    if (dtop - dsec < kTieGapSq * dtop) ctl[1] = 1;
+                    else *pmargin = fmin(k == 0 ? 1.0 : *pmargin, 1.0 - sqrt(dsec / dtop));
+                }
             }
             if (lane == 0) ctl[0] = best;
         }
         __syncthreads();
+        if (pivot && ctl[1]) return false;  // near tie (uniform)
         const int best = ctl[0];
         if (best != k) {  // symmetric swap k <-> best; rows < k of R: swap their columns
             for (int j = tid; j < n; j += kQrThreads) {
@@ -289,7 +311,8 @@ __device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rin
 // through one indexed branch (k-uniform), and the unmasked trailing update leaves finished
 // rows/columns untouched (their multipliers are zero). Step k stores l_i = S_ip / d into
 // lraw[k n + i] (1 at the pivot) and sqrt(d) into rdk[k]; R is assembled afterwards.
-__device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lraw, double* rdk, int* perm, double* colk) {
+__device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lraw, double* rdk, int* perm, double* colk,
+                                            double* pmargin) {
     const int lane = threadIdx.x & 31;
     double row[32];
 #pragma unroll
@@ -297,24 +320,34 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
     double dg = lane < n ? gs[lane + lane * n] : 0.0;
     bool done = lane >= n;
     double r00 = 0.0;
-    // first maximum of the remaining Schur diagonal (exact, lowest index on ties)
-    auto pick = [&](int& pv, double& d) {
+    // first maximum of the remaining Schur diagonal (exact, lowest index on ties), and the
+    // largest of the other remaining candidates (the pivot margin, SURVEY §7 hard part 1)
+    auto pick = [&](int& pv, double& d, double& d2) {
         const unsigned long long key = done ? 0ull : static_cast<unsigned long long>(__double_as_longlong(fmax(dg, 0.0)));
         const unsigned hi = __reduce_max_sync(0xffffffffu, unsigned(key >> 32));
         const unsigned lo = __reduce_max_sync(0xffffffffu, unsigned(key >> 32) == hi ? unsigned(key) : 0u);
         const bool cand = !done && key == ((static_cast<unsigned long long>(hi) << 32) | lo);
         pv = static_cast<int>(__reduce_min_sync(0xffffffffu, cand ? unsigned(lane) : 0xffffu));
         d = __shfl_sync(0xffffffffu, dg, pv & 31);
+        const unsigned long long k2 = (lane == pv) ? 0ull : key;
+        const unsigned h2 = __reduce_max_sync(0xffffffffu, unsigned(k2 >> 32));
+        const unsigned l2 = __reduce_max_sync(0xffffffffu, unsigned(k2 >> 32) == h2 ? unsigned(k2) : 0u);
+        d2 = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(h2) << 32) | l2));
     };
     int pv;
-    double d;
-    pick(pv, d);
+    double d, d2;
+    double pm = 1.0;
+    pick(pv, d, d2);
 #pragma unroll 1
     for (int k = 0; k < n; ++k) {
         QR_MARK(700 + 4 * k);
         if (k == 0) r00 = d;  // (squared) R_00
         // R_kk > kFastMinRatio R_00 tested on the squares: the sqrt stays off the step's chain
         if (pv >= n || !(d > 0.0) || !(d > kFastMinRatio * kFastMinRatio * r00)) return false;
+        if (k + 1 < n) {  // near tie: the Householder path decides
+            if (d - d2 < kTieGapSq * d) return false;
+            pm = fmin(pm, 1.0 - sqrt(d2 / d));
+        }
         QR_MARK(701 + 4 * k);
         const double rd = 1.0 / d;  // overlaps the row exchange below
         // the pivot lane publishes its Schur row S_p. (= column S_.p, S symmetric): lane i reads
@@ -338,15 +371,17 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         // the diagonal first: the next pivot search overlaps the rest of the row update
         dg = fma(-l, cp, dg);
         int pv1 = n;
-        double d1 = 0.0;
-        if (k + 1 < n) pick(pv1, d1);
+        double d1 = 0.0, d12 = 0.0;
+        if (k + 1 < n) pick(pv1, d1, d12);
 #pragma unroll
         for (int j = 0; j < 32; ++j) row[j] = fma(-l, colk[j], row[j]);
         __syncwarp();
         pv = pv1;
         d = d1;
+        d2 = d12;
     }
     for (int k = lane; k < n; k += 32) rdk[k] = sqrt(rdk[k]);
+    if (lane == 0) *pmargin = pm;
     __syncwarp();
     return true;
 }
@@ -507,7 +542,7 @@ __device__ __forceinline__ void axpy_row(double* zr, int ld, int j0, int j1, dou
 __global__ void __launch_bounds__(kQrThreads, 1)
     qr_colpiv_cluster_kernel(const double* __restrict__ zin, int64_t rows, int ncols, int ld,
                              double* __restrict__ uout, int ucap, void* upout, int up_dtype, int* rank_out,
-                             double* diag_out, int fast, int rowpar, int nparts) {
+                             double* diag_out, int fast, int rowpar, int nparts, double* margin_out) {
     cg::cluster_group cl = cg::this_cluster();
     const unsigned cs = cl.num_blocks();
     const int crank = static_cast<int>(cl.block_rank());
@@ -560,6 +595,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     int rank = 0;
     const int size = static_cast<int>(lmin(rows, ncols));
     bool fast_ok = false;
+    double pmargin = 1.0;  // min over pivot steps of (top - second) / top of the remaining norms
     if (fast && rows >= ncols) {
         const int n = ncols;
         double* q = reinterpret_cast<double*>(sh.flag + 16);  // [n][ld]
@@ -579,7 +615,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         bool ok1;
         if (n <= 32) {  // registers, one warp; lraw (n x n) and the step diagonals in r2 / sh.dir
             if (warp == 0) {
-                const bool ok = warp_pchol_reg(gs, n, r2, sh.dir, perm, sh.wv);
+                const bool ok = warp_pchol_reg(gs, n, r2, sh.dir, perm, sh.wv, sh.tot + kVec - 1);
                 if (lane == 0) ctl[0] = ok ? 1 : 0;
             }
             __syncthreads();
@@ -593,7 +629,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
                 __syncthreads();
             }
         } else {
-            ok1 = cta_pchol(gs, n, true, r1, rinv1, perm, ctl);
+            ok1 = cta_pchol(gs, n, true, r1, rinv1, perm, ctl, sh.tot + kVec - 1);
         }
         QR_MARK(601);
         if (ok1) {  // identical in every CTA (same reduced Gram, same arithmetic)
@@ -633,6 +669,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             __syncthreads();
             fast_ok = true;
             rank = n;
+            pmargin = sh.tot[kVec - 1];
             QR_MARK(605);
         }
     }
@@ -686,6 +723,14 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             const bool take = ov > bv || (ov == bv && oi < best);
             bv = take ? ov : bv;
             best = take ? oi : best;
+        }
+        if (k + 1 < size) {  // the largest other candidate (pivot margin; every thread, same value)
+            double sec = 0.0;
+            for (int j = k + lane; j < ncols; j += 32)
+                if (j != best) sec = fmax(sec, sh.upd[j]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sec = fmax(sec, __shfl_xor_sync(0xffffffffu, sec, o));
+            if (bv > 0.0) pmargin = fmin(pmargin, (bv - sec) / bv);
         }
         const double upd_k = sh.upd[k], dir_k = sh.dir[k];
         QR_MARK(6 + 8 * k);
@@ -833,7 +878,7 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         const int sub = tid % kTpc, grp = tid / kTpc;
         for (int base = 0; base + warp * (32 / kTpc) < rank; base += kQrThreads / kTpc) {
             const int j = base + grp;
-            double bvv = -1.0, val = 0.0;
+            double bvv = -1.0, val = 0.0, pmax = 0.0, nmax = 0.0;
             int bi = 0x7fffffff;
             for (int i = sub; j < rank && i < nloc; i += kTpc) {
                 const double x = z[i + j * ld];
@@ -841,6 +886,8 @@ __global__ void __launch_bounds__(kQrThreads, 1)
                 bvv = take ? fabs(x) : bvv;
                 bi = take ? i : bi;
                 val = take ? x : val;
+                pmax = x > 0.0 ? fmax(pmax, x) : pmax;
+                nmax = x < 0.0 ? fmax(nmax, -x) : nmax;
             }
 #pragma unroll
             for (int o = kTpc / 2; o > 0; o >>= 1) {
@@ -851,10 +898,14 @@ __global__ void __launch_bounds__(kQrThreads, 1)
                 bvv = take ? ob : bvv;
                 bi = take ? oi : bi;
                 val = take ? ov : val;
+                pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+                nmax = fmax(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
             }
             if (sub == 0 && j < rank) {
                 m[2 * j] = bvv;
                 m[2 * j + 1] = val;
+                sh.upd[j] = pmax;  // (the norms are no longer in use) read remotely below
+                sh.dir[j] = nmax;
             }
         }
         if (cs > 1) cl.sync();
@@ -877,9 +928,25 @@ __global__ void __launch_bounds__(kQrThreads, 1)
                 }
             }
             sh.sgn[j] = val < 0.0 ? -1.0 : 1.0;
+            if (margin_out && crank == 0) {  // sign margin of column j: (max |u_i| of the winning sign - max of the other) / max
+                double pm = 0.0, nm = 0.0;
+                for (unsigned c = 0; c < cs; ++c) {
+                    pm = fmax(pm, (cs > 1 ? cl.map_shared_rank(sh.upd, c) : sh.upd)[j]);
+                    nm = fmax(nm, (cs > 1 ? cl.map_shared_rank(sh.dir, c) : sh.dir)[j]);
+                }
+                const double top = fmax(pm, nm);
+                sh.wv[j] = top > 0.0 ? fabs(pm - nm) / top : 0.0;
+            }
         }
         par ^= 1;
         __syncthreads();
+        if (margin_out && crank == 0 && tid == 0) {
+            double smin = 1.0;
+            for (int j = 0; j < rank; ++j) smin = fmin(smin, sh.wv[j]);
+            margin_out[0] = pmargin;
+            margin_out[1] = smin;
+            margin_out[2] = fast_ok ? 0.0 : 1.0;  // 0: pivoted CholeskyQR2, 1: Householder
+        }
     }
     QR_MARK(4);
 
@@ -937,7 +1004,7 @@ int64_t qr_max_rows(int ncols) {
 }
 
 void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up, int up_dtype,
-                              int* rank_dev, double* diag, cudaStream_t s, int nparts) {
+                              int* rank_dev, double* diag, cudaStream_t s, int nparts, double* margins) {
     require(rows >= 1, "orthonormal_basis: empty input");
     require(ncols >= 1 && ncols <= kMaxRank, "orthonormal_basis: column count must be in [1, 64]");
     int ld = 0;
@@ -979,7 +1046,7 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
     }();
     TK_MAXSMEM((qr_colpiv_cluster_kernel));
     TK_CUDA(cudaLaunchKernelEx(&cfg, qr_colpiv_cluster_kernel, z, rows, ncols, ld, u, ucap, up, up_dtype, rank_dev,
-                               diag, fast, rowpar, nparts));
+                               diag, fast, rowpar, nparts, margins));
 }
 
 }  // namespace tkb

@@ -1,0 +1,526 @@
+// ttm_stream.cu — the Y-streaming pass (first stage of every X_n = Y x_{p != n} U_p^T and of
+// the core, tensor.hpp:151-192) on the tcgen05 tensor cores, second design.
+//
+//   out[p, r, q] = sum_k Y[p, k, q] U[k, r]       (3xTF32: y u ~= y_hi u_hi + y_hi u_lo + y_lo u_hi)
+//
+// Differences from ttm_tc.cu (the first design, still used for the second stages):
+// * y_hi is read by the MMA straight from the TMA-staged shared memory: the tensor core takes
+//   the top 19 bits of an fp32 operand (y_hi = trunc_tf32(y)), so only y_lo = y - y_hi (exact)
+//   is computed by the converter warps and stored to TMEM (half the TMEM stores, and the main
+//   MMAs no longer wait for the converters). M-major tiles (contracted mode not the fastest)
+//   are MN-major A operands (TMA boxes of 32 p x 16 k, 128B swizzle), K-major tiles (mode 0)
+//   K-major A operands (16 k x rows, 64B swizzle).
+// * Accumulation is chunked: the MMAs accumulate F k-blocks (F * 16 k) into TMEM, then the
+//   converter warps add the chunk into fp32 registers (round-to-nearest) and the next chunk
+//   restarts the TMEM accumulator. The tensor core's truncating fp32 accumulation therefore
+//   only runs over F k-blocks whatever K is (the first design's error grew with K).
+// * The factor is packed with NH = r~ rounded up to 8 (not 16): the main MMA covers
+//   [U_hi | U_lo] with N = 2 NH, the cross MMA y_lo U_hi with N = NH (cta_group::1 MMAs take
+//   N in steps of 8). r~ = 40: 120 MMA columns per k-step instead of 144.
+// Warp roles (10 warps, two CTAs per SM, 256 TMEM columns each):
+//   warp 8      producer: TMA boxes of Y + bulk copy of the packed [U_hi | U_lo] k-block
+//   warp 9      TMEM allocator + single-thread MMA issuer
+//   warps 0-7   converters (y_lo into TMEM; warp w: TMEM lane quarter w & 3, k half w >> 2),
+//               chunk flushes into register accumulators, and the epilogue stores
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <stdexcept>
+
+#include "kernels.cuh"
+
+namespace tkb {
+
+namespace {
+
+using EncodeTiledFn2 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn2 encode_tiled2() {
+    static EncodeTiledFn2 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        return (e == cudaSuccess && q == cudaDriverEntryPointSuccess) ? reinterpret_cast<EncodeTiledFn2>(p) : nullptr;
+    }();
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled entry point unavailable");
+    return fn;
+}
+
+constexpr int kSConv = 8;                      // converter warps
+constexpr int kSThreads = (kSConv + 2) * 32;   // + producer + MMA
+constexpr int kSBK = 16;                       // k per pipeline stage (2 MMA k-steps of 8)
+
+__host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+template <int NH, bool KM>
+struct SCfg {
+    static_assert(NH % 8 == 0 && NH >= 16 && NH <= 64, "NH: multiple of 8 in [16, 64]");
+    static constexpr int CN = NH;                          // N of the cross MMA (N steps of 8 are legal)
+    static constexpr int DW = round_up(NH + CN, 16);       // accumulator columns per 128-row tile
+    static constexpr int MT = (NH <= 48) ? 2 : 1;          // 128-row M tiles per CTA
+    static constexpr int BM = 128 * MT;
+    static constexpr int NA = (MT * DW + 4 * MT * 16 <= 256) ? 4 : 2;  // y_lo TMEM buffers
+    static constexpr int A_BASE = MT * DW;
+    static_assert(A_BASE + NA * MT * 16 <= 256, "TMEM budget (two CTAs per SM)");
+    static constexpr int BOXR = KM ? (BM < 256 ? BM : 256) : 32;  // rows per TMA box
+    static constexpr int STAGE_Y = kSBK * BM * 4;
+    static constexpr int STAGE_B = 128 * NH;                 // two k-steps of [U_hi | U_lo] (2 NH x 8 tf32 each)
+    static constexpr int STAGES_FIT = (110 * 1024 - 1024) / (STAGE_Y + STAGE_B);
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static_assert(STAGES >= 3, "pipeline depth");
+    static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 1024 /*align*/ + 256;
+    // accumulator columns per converter warp: MT == 2 -> one tile (the warp's k half index),
+    // all NH columns; MT == 1 -> half of the columns
+    static constexpr int ACC = MT == 2 ? NH : NH / 2;
+};
+
+__device__ __forceinline__ void sfence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void sfence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ void ld8(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[e]);
+}
+
+__device__ __forceinline__ void ld4(uint32_t taddr, float* v) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr)
+                 : "memory");
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = __uint_as_float(r[e]);
+}
+
+// UMMA shared-memory descriptors (sm_100): start >> 4 [0,14), LBO >> 4 [16,30), SBO >> 4
+// [32,46), version 1 at bit 46, layout type [61,64): 0 none, 2 128B swizzle, 4 64B swizzle.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    return (uint64_t((saddr >> 4) & 0x3FFFu)) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
+           (uint64_t((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (uint64_t(layout) << 61);
+}
+
+// Instruction descriptor: D f32, A/B tf32, B K-major, A MN-major if a_mn, M = 128, N = n.
+__device__ __forceinline__ uint32_t sidesc(int n, bool a_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn ? (1u << 15) : 0u) | (uint32_t(n >> 3) << 17) |
+           (uint32_t(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+        "r"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma2(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// y_lo = y - trunc_tf32(y) (exact in fp32), rounded to nearest tf32 for the MMA
+__device__ __forceinline__ uint32_t lo_bits(float y) {
+    const float lo = y - __uint_as_float(__float_as_uint(y) & 0xFFFFE000u);
+    return (__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u;
+}
+
+// KM = false: Y viewed as (P, K, Q), tiles of BM consecutive p of one q; out[p + r P + q P cols].
+// KM = true:  Y viewed as Q rows of K contiguous values (contraction over mode 0), tiles of BM
+//             rows; out[row + r Q] (transposed output: the contracted mode moves last).
+// F: k-blocks (of 16) per accumulation chunk.
+template <int NH, bool KM>
+__global__ void __launch_bounds__(kSThreads, 2)
+    ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
+                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles, int F) {
+    using C = SCfg<NH, KM>;
+    constexpr int MT = C::MT, BM = C::BM, NA = C::NA;
+    extern __shared__ uint8_t ssm_raw[];
+    uint8_t* ssm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ssm_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sY = ssm;                                   // [stages][BM/BOXR boxes] (1024-B aligned stages)
+    uint8_t* sB = ssm + size_t(C::STAGES) * C::STAGE_Y;  // [stages][2 k-steps][2NH x 8] tf32 core matrices
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(C::STAGES) * C::STAGE_B);
+    uint64_t* full = bars;                   // [STAGES] producer -> converters, MMA
+    uint64_t* empty = full + C::STAGES;      // [STAGES] converters (8) + MMA commit (1) -> producer
+    uint64_t* afull = empty + C::STAGES;     // [NA]     converters (8) -> MMA
+    uint64_t* aempty = afull + NA;           // [NA]     MMA commit -> converters
+    uint64_t* dfull = aempty + NA;           // [1]      MMA commit (chunk done) -> converters
+    uint64_t* dempty = dfull + 1;            // [1]      converters (8, chunk flushed) -> MMA
+    uint32_t* tbase_sm = reinterpret_cast<uint32_t*>(dempty + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nk = static_cast<int>((K + kSBK - 1) / kSBK);
+    const int nchunks = (nk + F - 1) / F;
+
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kSConv + 1);
+        }
+        for (int a = 0; a < NA; ++a) {
+            mbar_init(&afull[a], kSConv);
+            mbar_init(&aempty[a], 1);
+        }
+        mbar_init(dfull, 1);
+        mbar_init(dempty, kSConv);
+        mbar_fence_init();
+    }
+    if (warp == kSConv + 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tbase_sm)),
+                     "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    sfence_before();
+    __syncthreads();
+    sfence_after();
+    const uint32_t tmem = *tbase_sm;
+
+    if (warp == kSConv) {
+        // ===== producer =====
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
+            uint32_t g = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int64_t q = t / tiles_p;
+                const int64_t p0 = (t % tiles_p) * BM;
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const int s = static_cast<int>(g % C::STAGES);
+                    mbar_wait(&empty[s], ((g / C::STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
+                    uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
+                    if constexpr (KM) {
+#pragma unroll
+                        for (int b = 0; b < BM / C::BOXR; ++b)
+                            tma2(dy + b * (C::BOXR * kSBK * 4), &ymap, kc * kSBK, static_cast<int>(p0 + C::BOXR * b),
+                                 &full[s]);
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < BM / 32; ++b)
+                            tma3(dy + b * 2048, &ymap, static_cast<int>(p0 + 32 * b), kc * kSBK, static_cast<int>(q),
+                                 &full[s]);
+                    }
+                    bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
+                }
+            }
+        }
+    } else if (warp == kSConv + 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            const uint32_t id_main = sidesc(2 * NH, !KM), id_cross = sidesc(C::CN, false);
+            uint32_t g = 0, ch = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                for (int c = 0; c < nchunks; ++c, ++ch) {
+                    if (ch > 0) {  // the previous chunk's accumulators flushed into registers
+                        mbar_wait(dempty, (ch - 1) & 1);
+                        sfence_after();
+                    }
+                    const int k1 = min(nk, (c + 1) * F);
+                    for (int kc = c * F; kc < k1; ++kc, ++g) {
+                        const int s = static_cast<int>(g % C::STAGES), a = static_cast<int>(g % NA);
+                        mbar_wait(&full[s], (g / C::STAGES) & 1);
+                        sfence_after();
+                        const uint32_t ys = smem_u32(sY + size_t(s) * C::STAGE_Y);
+                        const uint32_t bs = smem_u32(sB + size_t(s) * C::STAGE_B);
+#pragma unroll
+                        for (int j = 0; j < MT; ++j) {
+#pragma unroll
+                            for (int ks = 0; ks < 2; ++ks) {
+                                const uint64_t bd = sdesc(bs + ks * (64 * NH), 128, 256, 0);
+                                uint64_t ad;
+                                if constexpr (KM)  // K-major, 64B swizzle: rows of 64 B, 8-row groups 512 B apart
+                                    ad = sdesc(ys + j * (128 * 64) + ks * 32, 16, 512, 4);
+                                else  // MN-major, 128B swizzle: 32-p atoms 2 KB apart, 8-k groups 1 KB apart
+                                    ad = sdesc(ys + j * (4 * 2048) + ks * 1024, 2048, 1024, 2);
+                                mma_ss(tmem + uint32_t(j * C::DW), ad, bd, id_main, (kc > c * F || ks > 0) ? 1u : 0u);
+                            }
+                        }
+                        mbar_wait(&afull[a], (g / NA) & 1);
+                        sfence_after();
+#pragma unroll
+                        for (int j = 0; j < MT; ++j) {
+#pragma unroll
+                            for (int ks = 0; ks < 2; ++ks) {
+                                const uint64_t bd = sdesc(bs + ks * (64 * NH), 128, 256, 0);
+                                mma_ts(tmem + uint32_t(j * C::DW + NH), tmem + uint32_t(C::A_BASE + (a * MT + j) * 16 + ks * 8),
+                                       bd, id_cross, 1u);
+                            }
+                        }
+                        commit(&aempty[a]);
+                        commit(&empty[s]);
+                    }
+                    commit(dfull);
+                }
+            }
+        }
+    } else {
+        // ===== converters (warps 0-7) =====
+        const int quarter = warp & 3, khalf = warp >> 2;
+        const int L = quarter * 32 + lane;  // TMEM lane = row within each 128-row tile
+        const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+        // accumulator ownership: MT == 2 -> tile khalf, all NH columns; MT == 1 -> columns of half khalf
+        constexpr int ACC = C::ACC;
+        const int jt = MT == 2 ? khalf : 0;
+        const int c0 = MT == 2 ? 0 : khalf * (NH / 2);
+        float acc[ACC];
+        uint32_t g = 0, ch = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int64_t q = t / tiles_p;
+            const int64_t p0 = (t % tiles_p) * BM;
+            const int rows = static_cast<int>(lmin(BM, P - p0));
+#pragma unroll
+            for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
+            for (int kc = 0; kc < nk; ++kc, ++g) {
+                const int s = static_cast<int>(g % C::STAGES), a = static_cast<int>(g % NA);
+                mbar_wait(&full[s], (g / C::STAGES) & 1);
+                uint32_t lo[MT][8];
+                const uint8_t* stage = sY + size_t(s) * C::STAGE_Y;
+#pragma unroll
+                for (int j = 0; j < MT; ++j) {
+                    const int row = j * 128 + L;
+                    if constexpr (KM) {
+                        const int rr = row % C::BOXR;
+                        const uint8_t* rb = stage + (row / C::BOXR) * (C::BOXR * kSBK * 4) + rr * 64;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int phys = (2 * khalf + h) ^ ((rr >> 1) & 3);
+                            const float4 v = *reinterpret_cast<const float4*>(rb + phys * 16);
+                            lo[j][h * 4 + 0] = lo_bits(v.x);
+                            lo[j][h * 4 + 1] = lo_bits(v.y);
+                            lo[j][h * 4 + 2] = lo_bits(v.z);
+                            lo[j][h * 4 + 3] = lo_bits(v.w);
+                        }
+                    } else {
+                        // box (row / 32) of 16 k-rows x 128 B, 16-B chunk (lane / 4) at chunk ^ (k & 7)
+                        const uint8_t* bb = stage + (row >> 5) * 2048 + (lane & 3) * 4;
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const int k = khalf * 8 + kk;
+                            const float y = *reinterpret_cast<const float*>(bb + k * 128 + (((lane >> 2) ^ kk) << 4));
+                            lo[j][kk] = lo_bits(y);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);  // this warp's reads of the Y stage are done
+                mbar_wait(&aempty[a], ((g / NA) & 1) ^ 1);
+                sfence_after();
+#pragma unroll
+                for (int j = 0; j < MT; ++j)
+                    st8(tmem + lane_off + uint32_t(C::A_BASE + (a * MT + j) * 16 + khalf * 8), lo[j]);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                sfence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&afull[a]);
+                // chunk end: add the TMEM accumulators into the registers (round to nearest)
+                if ((kc + 1) % F == 0 || kc + 1 == nk) {
+                    mbar_wait(dfull, ch & 1);
+                    sfence_after();
+                    const uint32_t base = tmem + lane_off + uint32_t(jt * C::DW + c0);
+                    // 8 (or 4) main + cross columns at a time: bounded temporaries (no spills)
+#pragma unroll
+                    for (int c = 0; c < ACC; c += 8) {
+                        float m[8], x[8];
+                        if (c + 8 <= ACC) {
+                            ld8(base + c, m);
+                            ld8(base + NH + c, x);
+                        } else {
+                            ld4(base + c, m);
+                            ld4(base + NH + c, x);
+                        }
+                        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            if (c + e < ACC) acc[c + e] += m[e] + x[e];
+                    }
+                    sfence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(dempty);
+                    ++ch;
+                }
+            }
+            // ===== epilogue: rows jt*128 + L of the tile, columns c0 .. c0 + ACC - 1 =====
+            const int row = jt * 128 + L;
+            if (row < rows) {
+                float* o = out + q * P * cols + p0 + row;
+#pragma unroll
+                for (int e = 0; e < ACC; ++e)
+                    if (c0 + e < cols) o[int64_t(c0 + e) * P] = acc[e];
+            }
+        }
+    }
+    sfence_before();
+    __syncthreads();
+    if (warp == kSConv + 1) {
+        sfence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+    }
+}
+
+// [U_hi | U_lo] of a column-major fp64 factor (rows x cols, ld), tf32 in the UMMA K-major
+// no-swizzle core-matrix layout: per k-step of 8 rows of U, 2NH n-rows of 8 k (16-B core
+// matrix rows, 8-row groups 256 B apart, the two 4-k halves 128 B apart).
+__global__ void pack_stream_kernel(const double* __restrict__ u, int64_t ld, int64_t rows, int cols, int nh,
+                                   int64_t ksteps, uint32_t* __restrict__ out) {
+    const int64_t n_el = ksteps * 2 * nh * 8;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n_el; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t g = t / (2 * nh * 8);
+        const int rem = static_cast<int>(t % (2 * nh * 8));
+        const int n = rem / 8, kk = rem % 8;
+        const int64_t k = g * 8 + kk;
+        const int r = n < nh ? n : n - nh;
+        const float uf = (k < rows && r < cols) ? static_cast<float>(u[k + int64_t(r) * ld]) : 0.f;
+        uint32_t h;
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(uf));
+        uint32_t v = h;
+        if (n >= nh) asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(v) : "f"(uf - __uint_as_float(h)));
+        const int64_t byte = g * (64 * nh) + (n / 8) * 256 + (kk / 4) * 128 + (n % 8) * 16 + (kk % 4) * 4;
+        out[byte / 4] = v;
+    }
+}
+
+template <int NH, bool KM>
+void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+                   cudaStream_t s) {
+    using C = SCfg<NH, KM>;
+    static bool attr = false;
+    if (!attr) {
+        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(C::smem)));
+        attr = true;
+    }
+    require(K < (int64_t(1) << 31) && Q < (int64_t(1) << 31) && P < (int64_t(1) << 31), "ttm: extent too large for TMA");
+    CUtensorMap map;
+    CUresult r;
+    int64_t tiles_p, ntiles, rows;
+    if constexpr (KM) {  // Q rows of K contiguous values
+        tiles_p = (Q + C::BM - 1) / C::BM;
+        ntiles = tiles_p;
+        rows = Q;
+        const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(Q)};
+        const cuuint64_t strides[1] = {cuuint64_t(K) * 4};
+        const cuuint32_t box[2] = {kSBK, C::BOXR};
+        const cuuint32_t estr[2] = {1, 1};
+        r = encode_tiled2()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(in), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        tiles_p = (P + C::BM - 1) / C::BM;
+        ntiles = tiles_p * Q;
+        rows = P;
+        const cuuint64_t dims[3] = {cuuint64_t(P), cuuint64_t(K), cuuint64_t(Q)};
+        const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
+        const cuuint32_t box[3] = {32, kSBK, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        r = encode_tiled2()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    static const int F = [] {
+        const char* e = std::getenv("TENKIT_STREAM_CHUNK");
+        return e ? std::max(1, std::atoi(e)) : 8;
+    }();
+    const int64_t grid = std::min<int64_t>(ntiles, 2 * 148);
+    TK_MAXSMEM((ttm_stream_kernel<NH, KM>));
+    ttm_stream_kernel<NH, KM><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K, cols,
+                                                                                     tiles_p, ntiles, F);
+    TK_LAUNCH_CHECK();
+}
+
+inline int stream_nh(int cols) { return std::max(16, (cols + 7) / 8 * 8); }
+
+}  // namespace
+
+bool stream_ttm_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TENKIT_STREAM");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+bool stream_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols) {
+    if (reinterpret_cast<uintptr_t>(in) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
+    if (cols < 1 || cols > kMaxRank || K < kSBK) return false;
+    if (P == 1) return K % 4 == 0 && (Q + 255) / 256 >= 148;  // K-major: >= one wave of 2 x 128-row tiles
+    return P % 4 == 0 && P >= 256 && (P + 255) / 256 * Q >= 2 * 148;
+}
+
+int64_t stream_pack_bytes(int64_t rows, int cols) {
+    const int64_t ksteps = (rows + kSBK - 1) / kSBK * 2;
+    return ksteps * 64 * stream_nh(cols);
+}
+
+void launch_pack_stream(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s) {
+    require(cols >= 1 && cols <= kMaxRank, "ttm: factor column count must be in [1, 64]");
+    const int64_t ksteps = (rows + kSBK - 1) / kSBK * 2;
+    const int nh = stream_nh(cols);
+    const int64_t n = ksteps * 2 * nh * 8;
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
+    TK_MAXSMEM(pack_stream_kernel);
+    pack_stream_kernel<<<grid, 256, 0, s>>>(u, ld, rows, cols, nh, ksteps, static_cast<uint32_t*>(out));
+    TK_LAUNCH_CHECK();
+}
+
+// P == 1: contraction over mode 0, transposed output out[q + r Q]; else out[p + r P + q P cols].
+void launch_ttm_stream(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+                       cudaStream_t s) {
+    const uint8_t* b = static_cast<const uint8_t*>(bpk);
+    const int nh = stream_nh(cols);
+#define TK_STREAM_CASE(N)                                                   \
+    case N:                                                                 \
+        if (P == 1) launch_stream<N, true>(in, b, out, P, K, Q, cols, s);   \
+        else launch_stream<N, false>(in, b, out, P, K, Q, cols, s);         \
+        break;
+    switch (nh) {
+        TK_STREAM_CASE(16)
+        TK_STREAM_CASE(24)
+        TK_STREAM_CASE(32)
+        TK_STREAM_CASE(40)
+        TK_STREAM_CASE(48)
+        TK_STREAM_CASE(56)
+        TK_STREAM_CASE(64)
+        default: throw InvalidArgument("tenkit: ttm: factor column count must be in [1, 64]");
+    }
+#undef TK_STREAM_CASE
+}
+
+}  // namespace tkb

@@ -220,6 +220,22 @@ void block_of(const tk_context* ctx, const std::vector<int64_t>& ld, std::vector
     }
 }
 
+// Per range step QR diagnostics into the stats (the "margins" context buffer, 3 doubles per
+// step: pivot margin, sign margin, QR path); steps = 2N (Alg. 3) or N (Alg. 2).
+void read_margins(tk_context* ctx, int64_t order, cudaStream_t s, tk_tucker_stats* stats, int64_t steps = -1) {
+    if (steps < 0) steps = 2 * order;
+    double hm[3 * 2 * TK_MAX_ORDER];
+    const double* md = static_cast<const double*>(ctx->buf("margins", sizeof(double) * 3 * 2 * TK_MAX_ORDER));
+    TK_CUDA(cudaMemcpyAsync(hm, md, sizeof(double) * 3 * steps, cudaMemcpyDeviceToHost, s));
+    TK_CUDA(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < 2 * TK_MAX_ORDER; ++i) {
+        const bool v = i < steps;
+        stats->pivot_margin[i] = v ? hm[3 * i] : 0.0;
+        stats->sign_margin[i] = v ? hm[3 * i + 1] : 0.0;
+        stats->qr_path[i] = v ? static_cast<int>(hm[3 * i + 2]) : -1;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // One decomposition run for value type T.
 // ---------------------------------------------------------------------------
@@ -239,6 +255,7 @@ struct TuckerRun {
     int passes = 0;
     int group_count = 0;
     int* rank_dev = nullptr;
+    double* margins_dev = nullptr;  // per range step: pivot margin, sign margin, QR path
     bool time_kernels = false;
     std::vector<cudaEvent_t> ev;  // (start, stop) pairs around Y-streaming launches
 
@@ -488,6 +505,17 @@ struct TuckerRun {
             if (path == 1 || U.size() <= size_t(m) || !U[m]) return false;
             const float* fin = reinterpret_cast<const float*>(in);
             float* fout = reinterpret_cast<float*>(out);
+            // the Y passes: second-design streaming kernel (ttm_stream.cu) when the shape tiles the GPU
+            if (streams_y && stream_ttm_enabled() && (P != 1 || tout) && stream_ttm_supported(fin, fout, P, K, Q, cols[m])) {
+                void* bpk = ctx->buf("stream_pack", static_cast<size_t>(stream_pack_bytes(K, cols[m])));
+                launch_pack_stream(U[m] + off[m], gdims[m], K, cols[m], bpk, s);
+                if (time_kernels) mark();
+                launch_ttm_stream(fin, bpk, fout, P, K, Q, cols[m], s);
+                launches += 2;
+                if (P == 1) *tout = true;
+                if (time_kernels) mark();
+                return true;
+            }
             const int64_t welems = std::min<int64_t>(P * cols[m] * Q * 16, int64_t(64) << 20);
             if (!tc_ttm_supported(fin, fout, P, K, Q, cols[m], welems)) return false;
             void* bpk = ctx->buf(streams_y ? "umma_pack" : "umma_pack2", static_cast<size_t>(umma_pack_bytes(K, cols[m])));
@@ -598,7 +626,7 @@ struct TuckerRun {
                                                 rank_dev + step, nullptr, gw, s);
         } else {
             launch_orthonormal_basis(z, In, rn, U[n], rt[n], Up[n], sizeof(T) == 4 ? kF32 : kF64, rank_dev + step,
-                                     nullptr, s, nparts);
+                                     nullptr, s, nparts, margins_dev + 3 * step);
             ++launches;
         }
         ph_end();
@@ -633,6 +661,8 @@ struct TuckerRun {
             launches += 2;
         }
         rank_dev = static_cast<int*>(ctx->buf("ranks", sizeof(int) * 2 * TK_MAX_ORDER));
+        margins_dev = static_cast<double*>(ctx->buf("margins", sizeof(double) * 3 * 2 * TK_MAX_ORDER));
+        TK_CUDA(cudaMemsetAsync(margins_dev, 0, sizeof(double) * 3 * 2 * TK_MAX_ORDER, s));
         const bool sync = opt.sync_ranks != 0;
         const T* xlast = nullptr;
         std::vector<int64_t> xd;
@@ -780,6 +810,7 @@ struct TuckerRun {
             TK_CUDA(cudaMemcpyAsync(hr, rank_dev, sizeof(int) * 2 * order, cudaMemcpyDeviceToHost, s));
             TK_CUDA(cudaStreamSynchronize(s));
             for (int i = 0; i < 2 * order; ++i) stats->ranks[i] = hr[i];
+            read_margins(ctx, order, s, stats);
         }
         if (!out->on_device) TK_CUDA(cudaStreamSynchronize(s));
     }
@@ -803,6 +834,8 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
     }
     TuckerRun<T> r{ctx, s, order, cd, gd, lo, cur};
     r.rank_dev = static_cast<int*>(ctx->buf("ranks", sizeof(int) * 2 * TK_MAX_ORDER));
+    double* margins = static_cast<double*>(ctx->buf("margins", sizeof(double) * 3 * 2 * TK_MAX_ORDER));
+    TK_CUDA(cudaMemsetAsync(margins, 0, sizeof(double) * 3 * 2 * TK_MAX_ORDER, s));
     std::vector<double*> U(order);
     std::vector<int64_t> fcols(order);
     int which = 0;
@@ -853,7 +886,8 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
             r.launches += launch_gram_orthonormal(z, gd[n], gd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64,
                                                   r.rank_dev + n, nullptr, gw, s);
         } else {
-            launch_orthonormal_basis(z, gd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64, r.rank_dev + n, nullptr, s);
+            launch_orthonormal_basis(z, gd[n], rt, U[n], rt, up, sizeof(T) == 4 ? kF32 : kF64, r.rank_dev + n, nullptr, s, 0,
+                                     margins + 3 * n);
             ++r.launches;
         }
         TK_CUDA(cudaMemcpyAsync(ctx->rank_host, r.rank_dev + n, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -900,6 +934,7 @@ void rand_tucker_impl(tk_context* ctx, int64_t order, const int64_t* dims, const
         stats->kernel_launches = r.launches + 1;
         stats->y_bytes = static_cast<double>(prod(std::vector<int64_t>(dims, dims + order))) * sizeof(T);
         for (int n = 0; n < order; ++n) stats->ranks[n] = static_cast<int>(fcols[n]);
+        read_margins(ctx, order, s, stats, order);
     }
     TK_CUDA(cudaStreamSynchronize(s));
 }
@@ -1006,6 +1041,7 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
         stats->stream_ms = ms;
         stats->y_bytes = static_cast<double>(prod(ld)) * sizeof(T);
         for (int i = 0; i < 2 * order; ++i) stats->ranks[i] = hr[i];
+        read_margins(ctx, order, s, stats);
     }
     return true;
 }
@@ -1096,6 +1132,7 @@ int tk_context_create(int device, tk_context** out) {
         TK_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
         ctx->stream = ctx->own;
         TK_CUDA(cudaMallocHost(&ctx->rank_host, sizeof(int) * 4));
+        if (const char* e = std::getenv("TENKIT_TTM_PATH")) ctx->ttm_path = std::max(0, std::min(3, std::atoi(e)));  // A/B knob
         *out = ctx.release();
     });
 }
@@ -1179,7 +1216,7 @@ int tk_context_set_nccl(tk_context* ctx, const unsigned char* id, int rank, int 
 int tk_context_set_ttm_path(tk_context* ctx, int path) {
     return guarded([&] {
         check_ctx(ctx);
-        require(path >= 0 && path <= 2, "ttm path must be 0 (auto), 1 (FFMA) or 2 (tcgen05)");
+        require(path >= 0 && path <= 3, "ttm path must be 0 (auto), 1 (FFMA), 2 (tcgen05) or 3 (streaming kernel)");
         ctx->ttm_path = path;
     });
 }
@@ -1349,6 +1386,27 @@ int tk_orthonormal_basis(tk_context* ctx, int64_t rows, int64_t cols, const doub
     });
 }
 
+int tk_orthonormal_basis_ex(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* q, int64_t* rank,
+                            double* rdiag, double* margins) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(rows >= 1, "orthonormal_basis: empty input");
+        if (cols == 0) {
+            *rank = 0;
+            return;
+        }
+        require(cols <= rows, "orthonormal_basis: wide inputs are not supported on the device path");
+        int* rd = static_cast<int*>(ctx->buf("qr_rank", sizeof(int)));
+        double* md = static_cast<double*>(ctx->buf("qr_margins", 3 * sizeof(double)));
+        launch_orthonormal_basis(z, rows, static_cast<int>(cols), q, static_cast<int>(cols), nullptr, kF64, rd, rdiag,
+                                 ctx->stream, 0, md);
+        TK_CUDA(cudaMemcpyAsync(ctx->rank_host, rd, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        if (margins) TK_CUDA(cudaMemcpyAsync(margins, md, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        TK_CUDA(cudaStreamSynchronize(ctx->stream));
+        *rank = *ctx->rank_host;
+    });
+}
+
 int tk_gram_orthonormalize(tk_context* ctx, int64_t rows, int64_t cols, const double* z, double* u, double* spectrum,
                            int64_t* kept) {
     return guarded([&] {
@@ -1409,7 +1467,16 @@ int tk_ttm(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const
         if (dtype == TK_F32) {
             const float* ft = static_cast<const float*>(t);
             float* fo = static_cast<float*>(out);
-            if (ctx->ttm_path == 2 && tc_ttm_supported(ft, fo, P, d[mode], Q, static_cast<int>(mrows))) {
+            if (ctx->ttm_path == 3 && P > 1 && stream_ttm_supported(ft, fo, P, d[mode], Q, static_cast<int>(mrows))) {
+                // the Y-streaming kernel on an M-major contraction (K-major passes write transposed
+                // output, exercised through tk_rand_tucker_2i / tk_ttm_all)
+                void* bpk = ctx->buf("stream_pack", static_cast<size_t>(stream_pack_bytes(d[mode], static_cast<int>(mrows))));
+                launch_pack_stream(md, d[mode], d[mode], static_cast<int>(mrows), bpk, ctx->stream);
+                launch_ttm_stream(ft, bpk, fo, P, d[mode], Q, static_cast<int>(mrows), ctx->stream);
+                TK_CUDA(cudaStreamSynchronize(ctx->stream));
+                return;
+            }
+            if (ctx->ttm_path >= 2 && tc_ttm_supported(ft, fo, P, d[mode], Q, static_cast<int>(mrows))) {
                 void* bpk = ctx->buf("umma_pack", static_cast<size_t>(umma_pack_bytes(d[mode], static_cast<int>(mrows))));
                 launch_pack_umma(md, d[mode], d[mode], static_cast<int>(mrows), bpk, ctx->stream);
                 launch_ttm_tc(ft, bpk, fo, P, d[mode], Q, static_cast<int>(mrows), ctx->stream);

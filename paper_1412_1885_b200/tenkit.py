@@ -213,8 +213,9 @@ class Context:
         _lib.check(self.lib.tk_context_set_stream(self.handle, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
     def set_ttm_path(self, path: str):
-        """'auto' (tcgen05 3xTF32 for fp32 Y passes), 'ffma', or 'tc' (tcgen05 whenever supported)."""
-        code = {"auto": 0, "ffma": 1, "tc": 2}[path]
+        """'auto' (tcgen05 3xTF32 for fp32 Y passes), 'ffma', 'tc' (tcgen05 whenever supported), or
+        'stream' (tk_ttm on the Y-streaming kernel, ttm_stream.cu, when the shape qualifies)."""
+        code = {"auto": 0, "ffma": 1, "tc": 2, "stream": 3}[path]
         _lib.check(self.lib.tk_context_set_ttm_path(self.handle, code))
 
     def synchronize(self):
@@ -326,9 +327,12 @@ def _tucker_call(fn_name, y, ranks, oversample, seed, context, out, opts=None):
     cshape = tuple(int(o.core_shape[n]) for n in range(y.order))
     cols = [int(o.factor_cols[n]) for n in range(y.order)]
     csize = int(np.prod(cshape))
+    nsteps = 2 * y.order if fn_name == "tk_rand_tucker_2i" else y.order
     stats = {"passes": st.passes, "kernel_launches": st.kernel_launches, "y_bytes": st.y_bytes,
              "ranks": [st.ranks[i] for i in range(2 * y.order)], "stream_launches": st.stream_launches,
-             "stream_ms": st.stream_ms}
+             "stream_ms": st.stream_ms, "pivot_margin": [st.pivot_margin[i] for i in range(nsteps)],
+             "sign_margin": [st.sign_margin[i] for i in range(nsteps)],
+             "qr_path": [st.qr_path[i] for i in range(nsteps)]}
     if on_dev:
         return TuckerModel(core[:csize], [b[: int(i) * c] for b, i, c in zip(fbufs, gdims, cols)], cshape, stats)
     g = core[:csize].reshape(cshape, order="F").copy()
@@ -448,9 +452,10 @@ def unfold_times(t, mode: int, b, *, dtype=None, context=None) -> np.ndarray:
     return z.cpu().numpy().reshape((t.shape[mode], b.shape[1]), order="F")
 
 
-def orthonormal_basis(z, *, with_diag: bool = False, context=None):
+def orthonormal_basis(z, *, with_diag: bool = False, with_margins: bool = False, context=None):
     """Column-pivoted QR basis with the rank cut |R_kk| > 1e-12 |R_00| (range_finder.hpp:18-29),
-    sign-fixed as tucker.hpp:39-45 does for every Tucker factor."""
+    sign-fixed as tucker.hpp:39-45 does for every Tucker factor. with_margins: also return
+    {'pivot_margin', 'sign_margin', 'qr_path'} (0 CholeskyQR2 fast path, 1 Householder)."""
     import torch
     z = np.asarray(z, dtype=np.float64)
     if z.ndim != 2 or z.shape[0] < 1:
@@ -461,12 +466,17 @@ def orthonormal_basis(z, *, with_diag: bool = False, context=None):
     q = torch.zeros(rows * max(cols, 1), dtype=torch.float64, device="cuda")
     diag = torch.zeros(max(cols, 1), dtype=torch.float64, device="cuda")
     rank = C.c_int64()
-    _lib.check(ctx.lib.tk_orthonormal_basis(ctx.handle, rows, cols, _dptr(zd), _dptr(q), C.byref(rank), _dptr(diag)))
+    mg = np.zeros(3)
+    _lib.check(ctx.lib.tk_orthonormal_basis_ex(ctx.handle, rows, cols, _dptr(zd), _dptr(q), C.byref(rank), _dptr(diag),
+                                               mg.ctypes.data_as(_lib.PD)))
     r = rank.value
     u = q.cpu().numpy()[: rows * r].reshape((rows, r), order="F")
+    out = [u]
     if with_diag:
-        return u, diag.cpu().numpy()[: min(rows, cols)]
-    return u
+        out.append(diag.cpu().numpy()[: min(rows, cols)])
+    if with_margins:
+        out.append({"pivot_margin": float(mg[0]), "sign_margin": float(mg[1]), "qr_path": int(mg[2])})
+    return out[0] if len(out) == 1 else tuple(out)
 
 
 def gram_orthonormalize(z_blocks, *, context=None):

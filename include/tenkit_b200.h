@@ -159,7 +159,14 @@ int tk_context_set_ttm_path(tk_context* ctx, int path);
 int tk_context_set_orthonormalizer(tk_context* ctx, int kind);
 
 /* Alg. 3. y: dtype TK_F32/TK_F64, dims[order], device pointer if y_on_device else host
- * (copied in on the context stream). ranks[order], oversample >= 0, seed = SeedSpec{root, stream}. */
+ * (copied in on the context stream). ranks[order], oversample >= 0, seed = SeedSpec{root, stream}.
+ *
+ * Device-path limits (the reference accepts any shape; these return TK_ERR_INVALID):
+ *   r~_n = min(R_n + p, I_n) <= 64          "rank + oversample must be <= 64 on this device path"
+ *   I_n <= tk_qr_max_rows(r~_n)              "orthonormal_basis: sketch too large for the cluster QR"
+ *     (the sketch Z_n, I_n x r~_n fp64, lives in one <= 16-CTA cluster's shared memory:
+ *      about 6.6k rows at r~ = 60, 13k at r~ = 30; every BASELINE config is inside). */
+int64_t tk_qr_max_rows(int64_t cols);
 int tk_rand_tucker_2i(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y,
                       int y_on_device, const int64_t* ranks, int64_t oversample, uint64_t seed_root,
                       uint64_t seed_stream, const tk_tucker_opts* opts, tk_tucker_out* out,

@@ -60,6 +60,7 @@ SIGNATURES = {
     "tk_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "tk_context_set_nccl": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int]),
     "tk_nccl_version": (C.c_int, []),
+    "tk_qr_max_rows": (I64, [I64]),
     "tk_context_set_ttm_path": (C.c_int, [C.c_void_p, C.c_int]),
     "tk_context_set_orthonormalizer": (C.c_int, [C.c_void_p, C.c_int]),
     "tk_gram_orthonormalize": (C.c_int, [C.c_void_p, I64, I64, PD, PD, PD, PI64]),

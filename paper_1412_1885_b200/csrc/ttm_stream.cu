@@ -8,8 +8,8 @@
 //   the top 19 bits of an fp32 operand (y_hi = trunc_tf32(y)), so only y_lo = y - y_hi (exact)
 //   is computed by the converter warps and stored to TMEM (half the TMEM stores, and the main
 //   MMAs no longer wait for the converters). M-major tiles (contracted mode not the fastest)
-//   are MN-major A operands (TMA boxes of 32 p x 16 k, 128B swizzle), K-major tiles (mode 0)
-//   K-major A operands (16 k x rows, 64B swizzle).
+//   are MN-major A operands (TMA boxes of 32 p x 16 k; MN-major tf32 takes only the 128B-span
+//   swizzle with 32-B atoms), K-major tiles (mode 0) K-major A operands (16 k x rows, 64B swizzle).
 // * Accumulation is chunked: the MMAs accumulate F k-blocks (F * 16 k) into TMEM, then the
 //   converter warps add the chunk into fp32 registers (round-to-nearest) and the next chunk
 //   restarts the TMEM accumulator. The tensor core's truncating fp32 accumulation therefore
@@ -267,8 +267,9 @@ __global__ void __launch_bounds__(kSThreads, 2)
                                 uint64_t ad;
                                 if constexpr (KM)  // K-major, 64B swizzle: rows of 64 B, 8-row groups 512 B apart
                                     ad = sdesc(ys + j * (128 * 64) + ks * 32, 16, 512, 4);
-                                else  // MN-major, 128B swizzle: 32-p atoms 2 KB apart, 8-k groups 1 KB apart
-                                    ad = sdesc(ys + j * (4 * 2048) + ks * 1024, 2048, 1024, 2);
+                                else  // MN-major tf32: the 128B-span / 32B-atom swizzle (layout type 1), 32-p
+                                      // atoms 2 KB apart, 4-k groups 512 B apart
+                                    ad = sdesc(ys + j * (4 * 2048) + ks * 1024, 2048, 512, 1);
                                 mma_ss(tmem + uint32_t(j * C::DW), ad, bd, id_main, (kc > c * F || ks > 0) ? 1u : 0u);
                             }
                         }
@@ -328,12 +329,13 @@ __global__ void __launch_bounds__(kSThreads, 2)
                             lo[j][h * 4 + 3] = lo_bits(v.w);
                         }
                     } else {
-                        // box (row / 32) of 16 k-rows x 128 B, 16-B chunk (lane / 4) at chunk ^ (k & 7)
-                        const uint8_t* bb = stage + (row >> 5) * 2048 + (lane & 3) * 4;
+                        // box (row / 32) of 16 k-rows x 128 B; 32-B chunk (lane / 8) of row k at
+                        // chunk ^ (k & 3) (TMA SWIZZLE_128B_ATOM_32B = UMMA SWIZZLE_128B_BASE32B)
+                        const uint8_t* bb = stage + (row >> 5) * 2048 + (lane & 7) * 4;
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk) {
                             const int k = khalf * 8 + kk;
-                            const float y = *reinterpret_cast<const float*>(bb + k * 128 + (((lane >> 2) ^ kk) << 4));
+                            const float y = *reinterpret_cast<const float*>(bb + k * 128 + (((lane >> 3) ^ (kk & 3)) << 5));
                             lo[j][kk] = lo_bits(y);
                         }
                     }
@@ -450,7 +452,7 @@ void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, i
         const cuuint32_t box[3] = {32, kSBK, 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         r = encode_tiled2()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");

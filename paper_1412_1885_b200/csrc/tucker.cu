@@ -453,8 +453,10 @@ struct TuckerRun {
     } fc;
     std::vector<int> fver;  // per mode: bumped whenever U_m is rewritten
 
-    // Remaining (small) contractions of every mode except skip and f, descending.
-    const T* finish(const T* cur, std::vector<int64_t>& xd, const std::vector<int>& xp, int skip, int f) {
+    // Remaining (small) contractions of every mode except skip and f, descending. A contraction
+    // over the storage-fastest mode on the streaming kernel writes its output transposed (that
+    // mode moves to the slowest storage position): xd / xp follow the storage order.
+    const T* finish(const T* cur, std::vector<int64_t>& xd, std::vector<int>& xp, int skip, int f) {
         int which = 0;
         bool first = true;
         for (int m = static_cast<int>(order) - 1; m >= 0; --m) {
@@ -471,13 +473,39 @@ struct TuckerRun {
             else if (!which) fc.pass = -1;  // a later contraction overwrites projA
             first = false;
             ph_begin(1);
-            if (!hit && !stream_ttm(cur, m, out, P, K, Q, false)) ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
+            // the streaming kernel's K-major form (transposed output) is deterministic in the
+            // shapes, so a cache hit rotates the storage order exactly as the computing step did
+            bool tout = P == 1 && stream_second_ok(cur, out, P, K, Q, cols[m]);
+            if (!hit) {
+                bool tr = false;
+                if (!stream_ttm(cur, m, out, P, K, Q, false, tout ? &tr : nullptr))
+                    ttm(cur, factor_rows(m), out, P, K, Q, cols[m]);
+                tout = tr;
+            }
             ph_end();
             xd[k] = cols[m];
+            if (tout) {  // storage (1, ..., N-1, 0): the contracted mode last
+                std::rotate(xd.begin(), xd.begin() + 1, xd.end());
+                std::rotate(xp.begin(), xp.begin() + 1, xp.end());
+            }
             cur = out;
             which ^= 1;
         }
         return cur;
+    }
+
+    // A second-stage contraction on the streaming kernel (TENKIT_STREAM_SECOND=0: first design)
+    bool stream_second_ok(const T* in, T* out, int64_t P, int64_t K, int64_t Q, int c) const {
+        if constexpr (sizeof(T) != 4) {
+            return false;
+        } else {
+            static const bool on = [] {
+                const char* e = std::getenv("TENKIT_STREAM_SECOND");
+                return !(e && e[0] == '0');
+            }();
+            return on && ctx->ttm_path != 1 && stream_ttm_enabled() &&
+                   stream_ttm_supported(reinterpret_cast<const float*>(in), reinterpret_cast<float*>(out), P, K, Q, c);
+        }
     }
 
     // Y x_{p != skip} U_p^T (skip = -1: all modes), on the current stream.
@@ -505,15 +533,18 @@ struct TuckerRun {
             if (path == 1 || U.size() <= size_t(m) || !U[m]) return false;
             const float* fin = reinterpret_cast<const float*>(in);
             float* fout = reinterpret_cast<float*>(out);
-            // the Y passes: second-design streaming kernel (ttm_stream.cu) when the shape tiles the GPU
-            if (streams_y && stream_ttm_enabled() && (P != 1 || tout) && stream_ttm_supported(fin, fout, P, K, Q, cols[m])) {
-                void* bpk = ctx->buf("stream_pack", static_cast<size_t>(stream_pack_bytes(K, cols[m])));
+            // the Y passes (and the second stages that tile the GPU): second-design streaming
+            // kernel (ttm_stream.cu); K-major only with the transposed output
+            if ((streams_y || stream_second_ok(in, out, P, K, Q, cols[m])) && stream_ttm_enabled() &&
+                (P != 1 || tout) && stream_ttm_supported(fin, fout, P, K, Q, cols[m])) {
+                void* bpk = ctx->buf(streams_y ? "stream_pack" : "stream_pack2",
+                                     static_cast<size_t>(stream_pack_bytes(K, cols[m])));
                 launch_pack_stream(U[m] + off[m], gdims[m], K, cols[m], bpk, s);
-                if (time_kernels) mark();
+                if (streams_y && time_kernels) mark();
                 launch_ttm_stream(fin, bpk, fout, P, K, Q, cols[m], s);
                 launches += 2;
                 if (P == 1) *tout = true;
-                if (time_kernels) mark();
+                if (streams_y && time_kernels) mark();
                 return true;
             }
             const int64_t welems = std::min<int64_t>(P * cols[m] * Q * 16, int64_t(64) << 20);
@@ -1170,6 +1201,8 @@ int tk_context_set_comm(tk_context* ctx, const tk_comm* comm) {
         ctx->has_comm = true;
     });
 }
+
+int64_t tk_qr_max_rows(int64_t cols) { return cols >= 1 && cols <= kMaxRank ? qr_max_rows(static_cast<int>(cols)) : 0; }
 
 int tk_nccl_unique_id(unsigned char* out) {
     return guarded([&] {

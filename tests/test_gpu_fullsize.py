@@ -81,7 +81,8 @@ def test_full_size_config(P, O, name, capture_tol):
     ranks, p = list(cfg["ranks"]), int(cfg["p"])
     runs = [P.rand_tucker_2i(yd, ranks, p, alg, sync_ranks=False, out="device") for _ in range(3)]
     a, b = runs[1].to_host(), runs[2].to_host()  # runs[2] replays the graph captured by runs[1]
-    assert a.stats["passes"] == 3  # r~ = 60 too: the K-major tcgen05 pass (NH = 64) leads over mode 0
+    if os.environ.get("TENKIT_TTM_PATH", "0") != "1":  # (the FFMA-only A/B path cannot lead a pass with mode 0)
+        assert a.stats["passes"] == 3  # r~ = 60 too: the K-major tcgen05 pass leads over mode 0
     np.testing.assert_array_equal(a.core, b.core)
     for u, v in zip(a.factors, b.factors):
         np.testing.assert_array_equal(u, v)

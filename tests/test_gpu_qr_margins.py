@@ -93,3 +93,19 @@ def test_decomposition_reports_step_margins(P, O):
     for k in range(6):
         assert abs(m32.stats["pivot_margin"][k] - margins[k, 0]) < 1e-3
         assert abs(m32.stats["sign_margin"][k] - margins[k, 1]) < 1e-3
+
+
+def test_device_path_limits_fail_loudly(P, O):
+    """The documented device limits (include/tenkit_b200.h): r~ <= 64 and I_n <= tk_qr_max_rows(r~)
+    raise the reference-style invalid_argument (TenkitError) instead of computing garbage."""
+    import torch
+    lib = P.Context.default().lib
+    cap = int(lib.tk_qr_max_rows(60))
+    assert 6000 < cap < 7000 and int(lib.tk_qr_max_rows(30)) > 2 * 6000 and int(lib.tk_qr_max_rows(65)) == 0
+    y = torch.zeros(80 * 4 * 4, dtype=torch.float32, device="cuda")
+    with pytest.raises(P.TenkitError, match="rank \\+ oversample must be <= 64"):
+        P.rand_tucker_2i(P.DenseTensor((80, 4, 4), y), (60, 2, 2), 10, (0, 0))
+    rows = cap + 8
+    y = torch.randn(rows * 8 * 8, dtype=torch.float32, device="cuda")
+    with pytest.raises(P.TenkitError, match="sketch too large for the cluster QR"):
+        P.rand_tucker_2i(P.DenseTensor((rows, 8, 8), y), (50, 4, 4), 10, (0, 0))

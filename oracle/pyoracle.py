@@ -450,3 +450,94 @@ def cp_reconstruct(factors) -> np.ndarray:
     out = np.empty(int(np.prod(dims)))
     _check(lib().tko_cp_reconstruct(_iptr(dims), C.c_int64(len(dims)), C.c_int64(rank), arr, _ptr(out)))
     return _tensor(out, dims)
+
+
+# ---------------------------------------------------------------- oracle/_ref: the reference's own code
+_REF_PATH = os.path.join(_HERE, "_ref", "libtenkit_ref.so")
+_ref = None
+
+
+def ref_available() -> bool:
+    """True where oracle/_ref was built (this container: /root/reference present)."""
+    return os.path.exists(_REF_PATH)
+
+
+def ref_lib():
+    """The reference's hot-path headers (tensor/random/range_finder/tucker.hpp, unmodified)
+    compiled against oracle/ref_shim (Eigen API over LAPACK) — fixture generation only."""
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            subprocess.run(["make", "-s", "-C", _HERE, "ref"], check=True)
+        if not ref_available():
+            raise RuntimeError("oracle/_ref not built (reference sources absent)")
+        _ref = C.CDLL(_REF_PATH)
+        _ref.tkr_last_error.restype = C.c_char_p
+        _ref.tkr_normal_at.restype = C.c_double
+        _ref.tkr_normal_at.argtypes = [C.c_uint64] * 3
+        _ref.tkr_seed_derived.restype = C.c_uint64
+        _ref.tkr_seed_derived.argtypes = [C.c_uint64] * 3
+        p = openblas_path()
+        if not p or _ref.tkr_init(p.encode()) != 0:
+            raise RuntimeError("oracle/_ref: LAPACK (OpenBLAS) not found")
+    return _ref
+
+
+def _rcheck(rc):
+    if rc != 0:
+        msg = ref_lib().tkr_last_error().decode()
+        raise OracleError(msg) if rc == 1 else RuntimeError(msg)
+
+
+def ref_gaussian_matrix(rows: int, cols: int, seed) -> np.ndarray:
+    out = np.empty(rows * cols)
+    _rcheck(ref_lib().tkr_gaussian_matrix(C.c_int64(rows), C.c_int64(cols), C.c_uint64(seed[0]), C.c_uint64(seed[1]),
+                                          _ptr(out)))
+    return out.reshape((rows, cols), order="F")
+
+
+def ref_ttm(t, m, mode: int) -> np.ndarray:
+    t, m = _f64(t), _f64(m)
+    oshape = list(t.shape)
+    oshape[mode] = m.shape[0]
+    out = np.empty(int(np.prod(oshape)))
+    _rcheck(ref_lib().tkr_ttm(_iptr(_i64(t.shape)), C.c_int64(t.ndim), _ptr(_flat(t)), C.c_int64(m.shape[0]),
+                              C.c_int64(m.shape[1]), _ptr(_flat(m)), C.c_int64(mode), _ptr(out)))
+    return _tensor(out, oshape)
+
+
+def ref_unfold_times(t, mode: int, b) -> np.ndarray:
+    t, b = _f64(t), _f64(b)
+    out = np.empty(t.shape[mode] * b.shape[1])
+    _rcheck(ref_lib().tkr_unfold_times(_iptr(_i64(t.shape)), C.c_int64(t.ndim), _ptr(_flat(t)), C.c_int64(mode),
+                                       C.c_int64(b.shape[0]), C.c_int64(b.shape[1]), _ptr(_flat(b)), _ptr(out)))
+    return out.reshape((t.shape[mode], b.shape[1]), order="F")
+
+
+def ref_orthonormal_basis(z) -> np.ndarray:
+    """orthonormal_basis + fix_column_signs of the reference (range_finder.hpp:18-29, tucker.hpp:39-45)."""
+    z = _f64(z)
+    rows, cols = z.shape
+    q = np.empty(rows * max(cols, 1))
+    rank = C.c_int64()
+    _rcheck(ref_lib().tkr_orthonormal_basis(C.c_int64(rows), C.c_int64(cols), _ptr(_flat(z)), _ptr(q), C.byref(rank)))
+    return q[: rows * rank.value].reshape((rows, rank.value), order="F").copy()
+
+
+def _ref_tucker(fn, y, ranks, oversample, seed):
+    y = _f64(y)
+    dims = y.shape
+    rts, core, cshape, fbufs, farr, cols = _model_buffers(dims, ranks, oversample)
+    _rcheck(fn(_iptr(_i64(dims)), C.c_int64(y.ndim), _ptr(_flat(y)), _iptr(_i64(ranks)), C.c_int64(oversample),
+               C.c_uint64(seed[0]), C.c_uint64(seed[1]), _ptr(core), _iptr(cshape), farr, _iptr(cols)))
+    return _unpack_model(dims, core, cshape, fbufs, cols)
+
+
+def ref_rand_tucker_2i(y, ranks, oversample: int, seed):
+    """The reference's rand_tucker_2i (tucker.hpp:136-169) itself. Returns (core, factors)."""
+    return _ref_tucker(ref_lib().tkr_rand_tucker_2i, y, ranks, oversample, seed)
+
+
+def ref_rand_tucker(y, ranks, oversample: int, seed):
+    """The reference's rand_tucker (Alg. 2, tucker.hpp:108-130) itself. Returns (core, factors)."""
+    return _ref_tucker(ref_lib().tkr_rand_tucker, y, ranks, oversample, seed)

@@ -514,7 +514,8 @@ def run_b200(args, cfg):
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32" if cfg["dtype"] == "f32" else "f64",
             "data": "synthetic (reference seeded generators bench.hpp:46-112, generated on the device)",
-            "config": {"workload": args.config, "dims": gdims, "ranks": list(cfg["ranks"]), "oversample": cfg["p"],
+            "config": {"workload": args.config + (f"/scale{args.scale}" if args.scale > 1 else ""), "dims": gdims,
+                       "ranks": list(cfg["ranks"]), "oversample": cfg["p"],
                        "ffcp_rank": cfg["ffcp_rank"], "passes_per_step": passes,
                        "passes_reference": 2 * len(dims) + 1,
                        "parallelism": ("grid" + "x".join(map(str, grid))) + f" ({args.scaling})",
@@ -560,6 +561,16 @@ def _ncu_traffic(workload, world=1):
         return None
 
 
+def scaled(cfg, factor: int):
+    """The config at reduced size (every extent divided by `factor`, kept >= r~ + 8): code-path
+    checks of the partitions (e.g. gloo ranks sharing one GPU), not bench numbers."""
+    if factor <= 1:
+        return cfg
+    rts = [int(r) + int(cfg["p"]) for r in cfg["ranks"]]
+    dims = [max(int(d) // factor, rt + 8) for d, rt in zip(cfg["dims"], rts)]
+    return dict(cfg, dims=tuple(dims))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -577,8 +588,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-slabs", type=int, default=None, help="last-mode length of the CPU sample")
+    ap.add_argument("--scale", type=int, default=1, help="divide every extent (code-path checks only)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = scaled(CONFIGS[args.config], args.scale)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -10,14 +10,16 @@
 //   MMAs no longer wait for the converters). M-major tiles (contracted mode not the fastest)
 //   are MN-major A operands (TMA boxes of 32 p x 16 k; MN-major tf32 takes only the 128B-span
 //   swizzle with 32-B atoms), K-major tiles (mode 0) K-major A operands (16 k x rows, 64B swizzle).
-// * Accumulation is chunked: the MMAs accumulate F k-blocks (F * 16 k) into TMEM, then the
+// * Accumulation is chunked: the MMAs accumulate kChunk k-blocks (256 k) into TMEM, then the
 //   converter warps add the chunk into fp32 registers (round-to-nearest) and the next chunk
 //   restarts the TMEM accumulator. The tensor core's truncating fp32 accumulation therefore
 //   only runs over F k-blocks whatever K is (the first design's error grew with K).
 // * The factor is packed with NH = r~ rounded up to 8 (not 16): the main MMA covers
 //   [U_hi | U_lo] with N = 2 NH, the cross MMA y_lo U_hi with N = NH (cta_group::1 MMAs take
 //   N in steps of 8). r~ = 40: 120 MMA columns per k-step instead of 144.
-// Warp roles (10 warps, two CTAs per SM, 256 TMEM columns each):
+// * Two accumulator buffers in TMEM alternate per chunk: the MMAs of chunk c + 1 run while the
+//   converter warps add chunk c into their registers (the flush is deferred by one stage).
+// Warp roles (10 warps; two CTAs per SM with 256 TMEM columns each, one with 512 for NH = 64):
 //   warp 8      producer: TMA boxes of Y + bulk copy of the packed [U_hi | U_lo] k-block
 //   warp 9      TMEM allocator + single-thread MMA issuer
 //   warps 0-7   converters (y_lo into TMEM; warp w: TMEM lane quarter w & 3, k half w >> 2),
@@ -57,24 +59,31 @@ __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / 
 template <int NH, bool KM>
 struct SCfg {
     static_assert(NH % 8 == 0 && NH >= 16 && NH <= 64, "NH: multiple of 8 in [16, 64]");
+    static constexpr int OCC = NH <= 56 ? 2 : 1;           // CTAs per SM (TMEM: 256 or 512 columns each)
+    static constexpr int TMEM = 512 / OCC;
     static constexpr int CN = NH;                          // N of the cross MMA (N steps of 8 are legal)
     static constexpr int DW = round_up(NH + CN, 16);       // accumulator columns per 128-row tile
-    static constexpr int MT = (NH <= 48) ? 2 : 1;          // 128-row M tiles per CTA
+    static constexpr int MT = 1;                           // 128-row M tiles per CTA
     static constexpr int BM = 128 * MT;
-    static constexpr int NA = (MT * DW + 4 * MT * 16 <= 256) ? 4 : 2;  // y_lo TMEM buffers
-    static constexpr int A_BASE = MT * DW;
-    static_assert(A_BASE + NA * MT * 16 <= 256, "TMEM budget (two CTAs per SM)");
-    static constexpr int BOXR = KM ? (BM < 256 ? BM : 256) : 32;  // rows per TMA box
+    static constexpr int ND = 2;                           // accumulator buffers: chunk c -> buffer c & 1
+    static constexpr int NA_FIT = (TMEM - ND * MT * DW) / (MT * 16);
+    static constexpr int NA = NA_FIT > 4 ? 4 : NA_FIT;     // y_lo TMEM buffers
+    static_assert(NA >= 2, "TMEM budget");
+    static constexpr int A_BASE = ND * MT * DW;
+    static constexpr int BOXR = KM ? BM : 32;              // rows per TMA box
     static constexpr int STAGE_Y = kSBK * BM * 4;
-    static constexpr int STAGE_B = 128 * NH;                 // two k-steps of [U_hi | U_lo] (2 NH x 8 tf32 each)
-    static constexpr int STAGES_FIT = (110 * 1024 - 1024) / (STAGE_Y + STAGE_B);
-    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int STAGE_B = 128 * NH;               // two k-steps of [U_hi | U_lo] (2 NH x 8 tf32 each)
+    static constexpr int SMEM_BUDGET = OCC == 2 ? 110 * 1024 : 220 * 1024;
+    static constexpr int STAGES_FIT = (SMEM_BUDGET - 1024) / (STAGE_Y + STAGE_B);
+    static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static_assert(STAGES >= 3, "pipeline depth");
-    static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 1024 /*align*/ + 256;
-    // accumulator columns per converter warp: MT == 2 -> one tile (the warp's k half index),
-    // all NH columns; MT == 1 -> half of the columns
-    static constexpr int ACC = MT == 2 ? NH : NH / 2;
+    static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 256;
+    static constexpr int ACC = NH / 2;                     // accumulator columns per converter warp (its half)
 };
+
+// k-blocks (of 16) per accumulation chunk: the tensor core's truncating fp32 accumulation runs
+// over at most kChunk * 16 k, then the chunk is added into fp32 registers (round to nearest)
+constexpr int kChunk = 16;
 
 __device__ __forceinline__ void sfence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void sfence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -166,32 +175,34 @@ __device__ __forceinline__ uint32_t lo_bits(float y) {
 // KM = false: Y viewed as (P, K, Q), tiles of BM consecutive p of one q; out[p + r P + q P cols].
 // KM = true:  Y viewed as Q rows of K contiguous values (contraction over mode 0), tiles of BM
 //             rows; out[row + r Q] (transposed output: the contracted mode moves last).
-// F: k-blocks (of 16) per accumulation chunk.
+// Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
+// the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
 template <int NH, bool KM>
-__global__ void __launch_bounds__(kSThreads, 2)
+__global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
-                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles, int F) {
+                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles) {
     using C = SCfg<NH, KM>;
-    constexpr int MT = C::MT, BM = C::BM, NA = C::NA;
-    extern __shared__ uint8_t ssm_raw[];
-    uint8_t* ssm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ssm_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sY = ssm;                                   // [stages][BM/BOXR boxes] (1024-B aligned stages)
-    uint8_t* sB = ssm + size_t(C::STAGES) * C::STAGE_Y;  // [stages][2 k-steps][2NH x 8] tf32 core matrices
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(C::STAGES) * C::STAGE_B);
-    uint64_t* full = bars;                   // [STAGES] producer -> converters, MMA
-    uint64_t* empty = full + C::STAGES;      // [STAGES] converters (8) + MMA commit (1) -> producer
-    uint64_t* afull = empty + C::STAGES;     // [NA]     converters (8) -> MMA
-    uint64_t* aempty = afull + NA;           // [NA]     MMA commit -> converters
-    uint64_t* dfull = aempty + NA;           // [1]      MMA commit (chunk done) -> converters
-    uint64_t* dempty = dfull + 1;            // [1]      converters (8, chunk flushed) -> MMA
-    uint32_t* tbase_sm = reinterpret_cast<uint32_t*>(dempty + 1);
+    constexpr int BM = C::BM, NA = C::NA, ST = C::STAGES;
+    // dynamic shared memory starts at offset 0 of the CTA's window (no static shared memory in
+    // this kernel): 1024-B aligned as the 128B-span swizzles need
+    extern __shared__ __align__(1024) uint8_t ssm[];
+    uint8_t* sY = ssm;                             // [stages][BM/BOXR boxes]
+    uint8_t* sB = ssm + size_t(ST) * C::STAGE_Y;   // [stages][2 k-steps][2NH x 8] tf32 core matrices
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(ST) * C::STAGE_B);
+    uint64_t* full = bars;               // [ST]  producer -> converters, MMA
+    uint64_t* empty = full + ST;         // [ST]  converters (8) + MMA commit (1) -> producer
+    uint64_t* afull = empty + ST;        // [NA]  converters (8) -> MMA
+    uint64_t* aempty = afull + NA;       // [NA]  MMA commit -> converters
+    uint64_t* dfull = aempty + NA;       // [2]   MMA commit (chunk done) -> converters
+    uint64_t* dempty = dfull + 2;        // [2]   converters (8, chunk flushed) -> MMA
+    uint32_t* tbase_sm = reinterpret_cast<uint32_t*>(dempty + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nk = static_cast<int>((K + kSBK - 1) / kSBK);
-    const int nchunks = (nk + F - 1) / F;
 
     if (tid == 0) {
-        for (int s = 0; s < C::STAGES; ++s) {
+        if (smem_u32(ssm) & 1023) __trap();  // the swizzle atoms need 1024-B alignment
+        for (int s = 0; s < ST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kSConv + 1);
         }
@@ -199,13 +210,15 @@ __global__ void __launch_bounds__(kSThreads, 2)
             mbar_init(&afull[a], kSConv);
             mbar_init(&aempty[a], 1);
         }
-        mbar_init(dfull, 1);
-        mbar_init(dempty, kSConv);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&dfull[b], 1);
+            mbar_init(&dempty[b], kSConv);
+        }
         mbar_fence_init();
     }
     if (warp == kSConv + 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tbase_sm)),
-                     "r"(256));
+                     "r"(C::TMEM));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     sfence_before();
@@ -217,20 +230,17 @@ __global__ void __launch_bounds__(kSThreads, 2)
         // ===== producer =====
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
-            uint32_t g = 0;
+            int s = 0;
+            uint32_t ph = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 const int64_t q = t / tiles_p;
                 const int64_t p0 = (t % tiles_p) * BM;
-                for (int kc = 0; kc < nk; ++kc, ++g) {
-                    const int s = static_cast<int>(g % C::STAGES);
-                    mbar_wait(&empty[s], ((g / C::STAGES) & 1) ^ 1);
+                for (int kc = 0; kc < nk; ++kc) {
+                    mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
                     uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
                     if constexpr (KM) {
-#pragma unroll
-                        for (int b = 0; b < BM / C::BOXR; ++b)
-                            tma2(dy + b * (C::BOXR * kSBK * 4), &ymap, kc * kSBK, static_cast<int>(p0 + C::BOXR * b),
-                                 &full[s]);
+                        tma2(dy, &ymap, kc * kSBK, static_cast<int>(p0), &full[s]);
                     } else {
 #pragma unroll
                         for (int b = 0; b < BM / 32; ++b)
@@ -238,6 +248,7 @@ __global__ void __launch_bounds__(kSThreads, 2)
                                  &full[s]);
                     }
                     bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
+                    if (++s == ST) s = 0, ph ^= 1;
                 }
             }
         }
@@ -245,146 +256,168 @@ __global__ void __launch_bounds__(kSThreads, 2)
         // ===== MMA issuer =====
         if (lane == 0) {
             const uint32_t id_main = sidesc(2 * NH, !KM), id_cross = sidesc(C::CN, false);
-            uint32_t g = 0, ch = 0;
+            int s = 0, a = 0;
+            uint32_t ph = 0, aph = 0, ch = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                for (int c = 0; c < nchunks; ++c, ++ch) {
-                    if (ch > 0) {  // the previous chunk's accumulators flushed into registers
-                        mbar_wait(dempty, (ch - 1) & 1);
+                for (int k0 = 0; k0 < nk; k0 += kChunk, ++ch) {
+                    const int b = ch & 1;
+                    if (ch >= 2) {  // this buffer's previous chunk has been added into the registers
+                        mbar_wait(&dempty[b], ((ch >> 1) - 1) & 1);
                         sfence_after();
                     }
-                    const int k1 = min(nk, (c + 1) * F);
-                    for (int kc = c * F; kc < k1; ++kc, ++g) {
-                        const int s = static_cast<int>(g % C::STAGES), a = static_cast<int>(g % NA);
-                        mbar_wait(&full[s], (g / C::STAGES) & 1);
+                    const uint32_t dm = tmem + uint32_t(b * C::DW);
+                    const int k1 = min(nk, k0 + kChunk);
+                    for (int kc = k0; kc < k1; ++kc) {
+                        mbar_wait(&full[s], ph);
                         sfence_after();
                         const uint32_t ys = smem_u32(sY + size_t(s) * C::STAGE_Y);
                         const uint32_t bs = smem_u32(sB + size_t(s) * C::STAGE_B);
 #pragma unroll
-                        for (int j = 0; j < MT; ++j) {
-#pragma unroll
-                            for (int ks = 0; ks < 2; ++ks) {
-                                const uint64_t bd = sdesc(bs + ks * (64 * NH), 128, 256, 0);
-                                uint64_t ad;
-                                if constexpr (KM)  // K-major, 64B swizzle: rows of 64 B, 8-row groups 512 B apart
-                                    ad = sdesc(ys + j * (128 * 64) + ks * 32, 16, 512, 4);
-                                else  // MN-major tf32: the 128B-span / 32B-atom swizzle (layout type 1), 32-p
-                                      // atoms 2 KB apart, 4-k groups 512 B apart
-                                    ad = sdesc(ys + j * (4 * 2048) + ks * 1024, 2048, 512, 1);
-                                mma_ss(tmem + uint32_t(j * C::DW), ad, bd, id_main, (kc > c * F || ks > 0) ? 1u : 0u);
-                            }
+                        for (int ks = 0; ks < 2; ++ks) {
+                            const uint64_t bd = sdesc(bs + ks * (64 * NH), 128, 256, 0);
+                            uint64_t ad;
+                            if constexpr (KM)  // K-major, 64B swizzle: rows of 64 B, 8-row groups 512 B apart
+                                ad = sdesc(ys + ks * 32, 16, 512, 4);
+                            else  // MN-major tf32: the 128B-span / 32B-atom swizzle (layout type 1), 32-p
+                                  // atoms 2 KB apart, 4-k groups 512 B apart
+                                ad = sdesc(ys + ks * 1024, 2048, 512, 1);
+                            mma_ss(dm, ad, bd, id_main, (kc > k0 || ks > 0) ? 1u : 0u);
                         }
-                        mbar_wait(&afull[a], (g / NA) & 1);
+                        mbar_wait(&afull[a], aph);
                         sfence_after();
 #pragma unroll
-                        for (int j = 0; j < MT; ++j) {
-#pragma unroll
-                            for (int ks = 0; ks < 2; ++ks) {
-                                const uint64_t bd = sdesc(bs + ks * (64 * NH), 128, 256, 0);
-                                mma_ts(tmem + uint32_t(j * C::DW + NH), tmem + uint32_t(C::A_BASE + (a * MT + j) * 16 + ks * 8),
-                                       bd, id_cross, 1u);
-                            }
+                        for (int ks = 0; ks < 2; ++ks) {
+                            const uint64_t bd = sdesc(bs + ks * (64 * NH), 128, 256, 0);
+                            mma_ts(dm + NH, tmem + uint32_t(C::A_BASE + a * 16 + ks * 8), bd, id_cross, 1u);
                         }
                         commit(&aempty[a]);
                         commit(&empty[s]);
+                        if (++s == ST) s = 0, ph ^= 1;
+                        if (++a == NA) a = 0, aph ^= 1;
                     }
-                    commit(dfull);
+                    commit(&dfull[b]);
                 }
             }
         }
     } else {
         // ===== converters (warps 0-7) =====
         const int quarter = warp & 3, khalf = warp >> 2;
-        const int L = quarter * 32 + lane;  // TMEM lane = row within each 128-row tile
+        const int L = quarter * 32 + lane;  // TMEM lane = row of the 128-row tile
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-        // accumulator ownership: MT == 2 -> tile khalf, all NH columns; MT == 1 -> columns of half khalf
         constexpr int ACC = C::ACC;
-        const int jt = MT == 2 ? khalf : 0;
-        const int c0 = MT == 2 ? 0 : khalf * (NH / 2);
+        const int c0 = khalf * (NH / 2);  // this warp's accumulator columns
         float acc[ACC];
-        uint32_t g = 0, ch = 0;
+#pragma unroll
+        for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
+        int s = 0, a = 0;
+        uint32_t ph = 0, aph = 0, ch = 0;
+        // flush of chunk `pend` (buffer pend & 1) deferred by one stage, so the wait for its last
+        // MMAs overlaps the conversion of the next stage
+        bool pending = false;
+        uint32_t pend = 0;
+        auto flush = [&](uint32_t c) {
+            const int b = c & 1;
+            mbar_wait(&dfull[b], (c >> 1) & 1);
+            sfence_after();
+            const uint32_t base = tmem + lane_off + uint32_t(b * C::DW + c0);
+#pragma unroll
+            for (int cc = 0; cc < ACC; cc += 8) {
+                float m[8], x[8];
+                if (cc + 8 <= ACC) {
+                    ld8(base + cc, m);
+                    ld8(base + NH + cc, x);
+                } else {
+                    ld4(base + cc, m);
+                    ld4(base + NH + cc, x);
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (cc + e < ACC) acc[cc + e] += m[e] + x[e];
+            }
+            sfence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dempty[b]);
+        };
+        float* orow = nullptr;  // output row of the tile whose flush is pending (last chunk)
+        int64_t ostride = 0;
+        bool store_after = false;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int64_t q = t / tiles_p;
             const int64_t p0 = (t % tiles_p) * BM;
             const int rows = static_cast<int>(lmin(BM, P - p0));
+            for (int kc = 0; kc < nk; ++kc) {
+                mbar_wait(&full[s], ph);
+                uint32_t lo[8];
+                const uint32_t stage = smem_u32(sY + size_t(s) * C::STAGE_Y);
+                if constexpr (KM) {
+                    // row L: 64 B with 16-B chunks at chunk ^ ((L >> 1) & 3) (64B swizzle)
+                    const uint32_t rb = stage + L * 64;
 #pragma unroll
-            for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
-            for (int kc = 0; kc < nk; ++kc, ++g) {
-                const int s = static_cast<int>(g % C::STAGES), a = static_cast<int>(g % NA);
-                mbar_wait(&full[s], (g / C::STAGES) & 1);
-                uint32_t lo[MT][8];
-                const uint8_t* stage = sY + size_t(s) * C::STAGE_Y;
+                    for (int h = 0; h < 2; ++h) {
+                        const int phys = (2 * khalf + h) ^ ((L >> 1) & 3);
+                        float4 v;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                     : "r"(rb + phys * 16));
+                        lo[h * 4 + 0] = lo_bits(v.x);
+                        lo[h * 4 + 1] = lo_bits(v.y);
+                        lo[h * 4 + 2] = lo_bits(v.z);
+                        lo[h * 4 + 3] = lo_bits(v.w);
+                    }
+                } else {
+                    // box `quarter` of 16 k-rows x 128 B; 32-B chunk (lane / 8) of row k at
+                    // chunk ^ (k & 3) (TMA SWIZZLE_128B_ATOM_32B = UMMA SWIZZLE_128B_BASE32B)
+                    const uint32_t bb = stage + quarter * 2048 + khalf * 8 * 128 + (lane & 7) * 4;
 #pragma unroll
-                for (int j = 0; j < MT; ++j) {
-                    const int row = j * 128 + L;
-                    if constexpr (KM) {
-                        const int rr = row % C::BOXR;
-                        const uint8_t* rb = stage + (row / C::BOXR) * (C::BOXR * kSBK * 4) + rr * 64;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int phys = (2 * khalf + h) ^ ((rr >> 1) & 3);
-                            const float4 v = *reinterpret_cast<const float4*>(rb + phys * 16);
-                            lo[j][h * 4 + 0] = lo_bits(v.x);
-                            lo[j][h * 4 + 1] = lo_bits(v.y);
-                            lo[j][h * 4 + 2] = lo_bits(v.z);
-                            lo[j][h * 4 + 3] = lo_bits(v.w);
-                        }
-                    } else {
-                        // box (row / 32) of 16 k-rows x 128 B; 32-B chunk (lane / 8) of row k at
-                        // chunk ^ (k & 3) (TMA SWIZZLE_128B_ATOM_32B = UMMA SWIZZLE_128B_BASE32B)
-                        const uint8_t* bb = stage + (row >> 5) * 2048 + (lane & 7) * 4;
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {
-                            const int k = khalf * 8 + kk;
-                            const float y = *reinterpret_cast<const float*>(bb + k * 128 + (((lane >> 3) ^ (kk & 3)) << 5));
-                            lo[j][kk] = lo_bits(y);
-                        }
+                    for (int kk = 0; kk < 8; ++kk) {
+                        float y;
+                        asm volatile("ld.shared.f32 %0, [%1];\n"
+                                     : "=f"(y)
+                                     : "r"(bb + kk * 128 + (((lane >> 3) ^ (kk & 3)) << 5)));
+                        lo[kk] = lo_bits(y);
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // this warp's reads of the Y stage are done
-                mbar_wait(&aempty[a], ((g / NA) & 1) ^ 1);
+                if (++s == ST) s = 0, ph ^= 1;
+                mbar_wait(&aempty[a], aph ^ 1);
                 sfence_after();
-#pragma unroll
-                for (int j = 0; j < MT; ++j)
-                    st8(tmem + lane_off + uint32_t(C::A_BASE + (a * MT + j) * 16 + khalf * 8), lo[j]);
+                st8(tmem + lane_off + uint32_t(C::A_BASE + a * 16 + khalf * 8), lo);
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 sfence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&afull[a]);
-                // chunk end: add the TMEM accumulators into the registers (round to nearest)
-                if ((kc + 1) % F == 0 || kc + 1 == nk) {
-                    mbar_wait(dfull, ch & 1);
-                    sfence_after();
-                    const uint32_t base = tmem + lane_off + uint32_t(jt * C::DW + c0);
-                    // 8 (or 4) main + cross columns at a time: bounded temporaries (no spills)
+                if (++a == NA) a = 0, aph ^= 1;
+                if (pending) {  // the previous chunk: its MMAs are (nearly) done by now
+                    flush(pend);
+                    pending = false;
+                    if (store_after) {  // the previous tile's last chunk: its rows are complete
 #pragma unroll
-                    for (int c = 0; c < ACC; c += 8) {
-                        float m[8], x[8];
-                        if (c + 8 <= ACC) {
-                            ld8(base + c, m);
-                            ld8(base + NH + c, x);
-                        } else {
-                            ld4(base + c, m);
-                            ld4(base + NH + c, x);
-                        }
-                        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                        for (int e = 0; e < ACC; ++e)
+                            if (c0 + e < cols && orow) orow[int64_t(c0 + e) * ostride] = acc[e];
 #pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (c + e < ACC) acc[c + e] += m[e] + x[e];
+                        for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
+                        store_after = false;
                     }
-                    sfence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(dempty);
-                    ++ch;
+                }
+                if ((kc + 1) % kChunk == 0 || kc + 1 == nk) {
+                    pending = true;
+                    pend = ch++;
+                    if (kc + 1 == nk) {  // tile end: store once this chunk is flushed
+                        store_after = true;
+                        orow = L < rows ? out + q * P * cols + p0 + L : nullptr;
+                        ostride = P;
+                    }
                 }
             }
-            // ===== epilogue: rows jt*128 + L of the tile, columns c0 .. c0 + ACC - 1 =====
-            const int row = jt * 128 + L;
-            if (row < rows) {
-                float* o = out + q * P * cols + p0 + row;
+            if (t + gridDim.x >= ntiles && pending) {  // last tile of this CTA: flush and store now
+                flush(pend);
+                pending = false;
 #pragma unroll
                 for (int e = 0; e < ACC; ++e)
-                    if (c0 + e < cols) o[int64_t(c0 + e) * P] = acc[e];
+                    if (c0 + e < cols && orow) orow[int64_t(c0 + e) * ostride] = acc[e];
+                store_after = false;
             }
         }
     }
@@ -392,7 +425,7 @@ __global__ void __launch_bounds__(kSThreads, 2)
     __syncthreads();
     if (warp == kSConv + 1) {
         sfence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(C::TMEM));
     }
 }
 
@@ -456,14 +489,10 @@ void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, i
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-    static const int F = [] {
-        const char* e = std::getenv("TENKIT_STREAM_CHUNK");
-        return e ? std::max(1, std::atoi(e)) : 8;
-    }();
-    const int64_t grid = std::min<int64_t>(ntiles, 2 * 148);
+    const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
     TK_MAXSMEM((ttm_stream_kernel<NH, KM>));
     ttm_stream_kernel<NH, KM><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K, cols,
-                                                                                     tiles_p, ntiles, F);
+                                                                                     tiles_p, ntiles);
     TK_LAUNCH_CHECK();
 }
 

@@ -97,6 +97,11 @@ typedef struct tk_tucker_opts {
                                tucker.hpp:149-160); 0: consecutive steps with distinct modes share
                                one Y pass over a mode outside the group (same values up to
                                rounding; N = 3: 3 Y passes instead of 6) */
+    int precision;          /* fp32 data only. 0 (default): fp32-accurate tensor-core passes
+                               (3xTF32 with chunked round-to-nearest accumulation); 1: fp64
+                               arithmetic over the fp32 values (the reference's precision, about
+                               3-7x slower) — for data whose discrete QR decisions (pivot / sign,
+                               see tk_tucker_stats margins) are closer than fp32 can resolve */
 } tk_tucker_opts;
 
 /* Per-call timing/trace (filled when non-null) */

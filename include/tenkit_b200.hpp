@@ -274,7 +274,7 @@ TuckerModel tucker_call(bool two_pass, const BasicDenseTensor<T>& y, const std::
     }
     tk_context* ctx = Device::context();
     if (two_pass) {
-        tk_tucker_opts opts{0, 1, 0, 1, 0};
+        tk_tucker_opts opts{0, 1, 0, 1, 0, 0};
         check(tk_rand_tucker_2i(ctx, dtype_of<T>(), N, y.shape().data(), y.data(), 0, ranks.data(), oversample,
                                 seed.root, seed.stream, &opts, &out, nullptr));
     } else {

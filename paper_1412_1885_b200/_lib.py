@@ -37,7 +37,7 @@ class tk_tucker_out(C.Structure):
 
 class tk_tucker_opts(C.Structure):
     _fields_ = [("explicit_core_pass", C.c_int), ("sync_ranks", C.c_int), ("time_kernels", C.c_int),
-                ("overlap", C.c_int), ("one_pass_per_step", C.c_int)]
+                ("overlap", C.c_int), ("one_pass_per_step", C.c_int), ("precision", C.c_int)]
 
 
 class tk_tucker_stats(C.Structure):

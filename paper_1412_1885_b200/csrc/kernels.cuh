@@ -58,6 +58,11 @@ int64_t stream_pack_bytes(int64_t rows, int cols);
 void launch_pack_stream(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s);
 void launch_ttm_stream(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                        cudaStream_t s);
+// fp64 arithmetic over fp32 data (ttm_mixed.cu): out (fp64) = in (fp32) x_mode U, U packed
+// k-major with stride pack_stride(cols) (launch_pack_factor<double>); M-major shapes, P % 4 == 0.
+bool mixed_ttm_supported(const float* in, int64_t P);
+void launch_ttm_mixed(const float* in, const double* up, double* out, int64_t P, int64_t K, int64_t Q, int cols,
+                      cudaStream_t s);
 // out[i] = sum_s part[s * n + i] (fixed split order)
 template <typename T>
 void launch_splitk_reduce(const T* part, T* out, int64_t n, int splits, cudaStream_t s);

@@ -74,10 +74,12 @@ struct SCfg {
     static constexpr int STAGE_Y = kSBK * BM * 4;
     static constexpr int STAGE_B = 128 * NH;               // two k-steps of [U_hi | U_lo] (2 NH x 8 tf32 each)
     static constexpr int SMEM_BUDGET = OCC == 2 ? 110 * 1024 : 220 * 1024;
-    static constexpr int STAGES_FIT = (SMEM_BUDGET - 1024) / (STAGE_Y + STAGE_B);
+    static constexpr int STAGES_FIT = (SMEM_BUDGET - 1024) / (STAGE_Y + STAGE_B);  // (1 KB: barriers + slack)
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static_assert(STAGES >= 3, "pipeline depth");
-    static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + 256;
+    // barriers: 2 per stage + 2 per y_lo buffer + 4 accumulator-buffer barriers, + the TMEM base
+    static constexpr size_t BAR_BYTES = (2 * STAGES + 2 * NA + 4) * 8 + 16;
+    static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + BAR_BYTES;
     static constexpr int ACC = NH / 2;                     // accumulator columns per converter warp (its half)
 };
 

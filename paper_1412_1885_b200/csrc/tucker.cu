@@ -272,6 +272,9 @@ struct TuckerRun {
         return e && e[0] == '1';
     }();
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> phases;
+    // precision = fp64 on fp32 data (T = double): the Y passes read this fp32 tensor and
+    // compute in fp64 (ttm_mixed.cu); y is unused then
+    const float* y32 = nullptr;
     void ph_begin(int cat) {
         if (!phase_on || capture) return;
         cudaEvent_t a, b;
@@ -427,6 +430,19 @@ struct TuckerRun {
         T* out = static_cast<T*>(ctx->buf("proj1", sizeof(T) * P * cols[f] * Q));
         bool tout = false;
         ph_begin(0);
+        if constexpr (sizeof(T) == 8) {
+            if (y32) {  // fp64 arithmetic over the fp32 tensor
+                if (time_kernels) mark();
+                launch_ttm_mixed(y32, reinterpret_cast<const double*>(factor_rows(f)), reinterpret_cast<double*>(out),
+                                 P, K, Q, cols[f], s);
+                ++launches;
+                if (time_kernels) mark();
+                ph_end();
+                ++passes;
+                xd[f] = cols[f];
+                return out;
+            }
+        }
         if (!stream_ttm(y, f, out, P, K, Q, true, &tout)) {
             if (time_kernels) mark();
             ttm(y, factor_rows(f), out, P, K, Q, cols[f]);
@@ -995,8 +1011,10 @@ bool graphs_enabled() {
 template <typename T>
 bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, const std::vector<int64_t>& gd,
               const std::vector<int64_t>& off, const T* ydev, const std::vector<int64_t>& rk, int64_t p,
-              const Seed& seed, const tk_tucker_opts& opt, tk_tucker_out* out, tk_tucker_stats* stats) {
+              const Seed& seed, const tk_tucker_opts& opt, tk_tucker_out* out, tk_tucker_stats* stats,
+              const float* y32 = nullptr) {
     std::string key = std::to_string(sizeof(T)) + "|" + std::to_string(reinterpret_cast<uintptr_t>(ydev)) + "|" +
+                      std::to_string(reinterpret_cast<uintptr_t>(y32)) + "|" +
                       std::to_string(p) + "|" + std::to_string(seed.root) + "|" + std::to_string(seed.stream) + "|" +
                       std::to_string(opt.explicit_core_pass) + std::to_string(opt.overlap) + std::to_string(opt.one_pass_per_step) +
                       std::to_string(opt.time_kernels) + "|" + std::to_string(ctx->ttm_path) + "|" + std::to_string(ctx->ortho) +
@@ -1017,6 +1035,7 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
         }
         ctx->ensure_side();
         TuckerRun<T> r{ctx, ctx->cap, order, ld, gd, off, ydev};
+        r.y32 = y32;
         r.time_kernels = opt.time_kernels != 0;
         r.capture = true;
         cudaGraph_t graph = nullptr;
@@ -1070,7 +1089,7 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
             ms += t;
         }
         stats->stream_ms = ms;
-        stats->y_bytes = static_cast<double>(prod(ld)) * sizeof(T);
+        stats->y_bytes = static_cast<double>(prod(ld)) * (y32 ? sizeof(float) : sizeof(T));
         for (int i = 0; i < 2 * order; ++i) stats->ranks[i] = hr[i];
         read_margins(ctx, order, s, stats);
     }
@@ -1080,25 +1099,27 @@ bool graph_2i(tk_context* ctx, int64_t order, const std::vector<int64_t>& ld, co
 template <typename T>
 void rand_tucker_2i_impl(tk_context* ctx, int64_t order, const int64_t* dims, const void* y, int y_on_device,
                          const int64_t* ranks, int64_t p, Seed seed, const tk_tucker_opts& opt, tk_tucker_out* out,
-                         tk_tucker_stats* stats) {
+                         tk_tucker_stats* stats, const float* y32 = nullptr) {
     std::vector<int64_t> ld(dims, dims + order), rk(ranks, ranks + order);
     std::vector<int64_t> gd, offset;
     block_of(ctx, ld, gd, offset);
     const T* ydev = static_cast<const T*>(y);
-    if (!y_on_device) {
+    if (!y_on_device && !y32) {
         T* buf = static_cast<T*>(ctx->buf("y_in", sizeof(T) * prod(ld)));
         TK_CUDA(cudaMemcpyAsync(buf, y, sizeof(T) * prod(ld), cudaMemcpyHostToDevice, ctx->stream));
         ydev = buf;
     }
     auto attempt = [&](const tk_tucker_opts& o) {
         TuckerRun<T> r{ctx, ctx->stream, order, ld, gd, offset, ydev};
+        r.y32 = y32;
         r.time_kernels = o.time_kernels != 0;
         r.run(rk, p, seed, o, out, stats);
+        if (stats && y32) stats->y_bytes = static_cast<double>(prod(ld)) * sizeof(float);
     };
     // graphs: single process, or a native NCCL communicator (its all-reduces are captured);
     // the host-callback hook runs eagerly
-    if (!opt.sync_ranks && y_on_device && !(ctx->has_comm && ctx->comm.world > 1 && !ctx->nccl) &&
-        graphs_enabled() && graph_2i<T>(ctx, order, ld, gd, offset, ydev, rk, p, seed, opt, out, stats))
+    if (!opt.sync_ranks && (y_on_device || y32) && !(ctx->has_comm && ctx->comm.world > 1 && !ctx->nccl) &&
+        graphs_enabled() && graph_2i<T>(ctx, order, ld, gd, offset, ydev, rk, p, seed, opt, out, stats, y32))
         return;
     if (opt.sync_ranks) {
         attempt(opt);
@@ -1112,6 +1133,29 @@ void rand_tucker_2i_impl(tk_context* ctx, int64_t order, const int64_t* dims, co
             attempt(o2);
         }
     }
+}
+
+// precision = fp64 on fp32 data (tk_tucker_opts.precision = 1): the reference's own precision
+// on the fp32 tensor. Small tensors (fp64 copy <= 2 GB) are cast to fp64 once and run the fp64
+// path; large ones keep the fp32 tensor and run their Y passes in fp64 arithmetic over it
+// (ttm_mixed.cu), everything after the first stage in fp64.
+void rand_tucker_2i_fp64_on_f32(tk_context* ctx, int64_t order, const int64_t* dims, const void* y, int y_on_device,
+                                const int64_t* ranks, int64_t p, Seed seed, const tk_tucker_opts& opt,
+                                tk_tucker_out* out, tk_tucker_stats* stats) {
+    const int64_t n = prod(std::vector<int64_t>(dims, dims + order));
+    const float* y32 = static_cast<const float*>(y);
+    if (!y_on_device) {
+        float* buf = static_cast<float*>(ctx->buf("y_in", sizeof(float) * n));
+        TK_CUDA(cudaMemcpyAsync(buf, y, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        y32 = buf;
+    }
+    if (n * int64_t(sizeof(double)) <= (int64_t(2) << 30)) {
+        double* y64 = static_cast<double*>(ctx->buf("y_fp64", sizeof(double) * n));
+        launch_cast<float, double>(y32, y64, n, ctx->stream);
+        rand_tucker_2i_impl<double>(ctx, order, dims, y64, 1, ranks, p, seed, opt, out, stats);
+        return;
+    }
+    rand_tucker_2i_impl<double>(ctx, order, dims, nullptr, 1, ranks, p, seed, opt, out, stats, y32);
 }
 
 void validate_common(int dtype, int64_t order, const int64_t* dims, const int64_t* ranks, int64_t p,
@@ -1277,10 +1321,13 @@ int tk_rand_tucker_2i(tk_context* ctx, int dtype, int64_t order, const int64_t* 
         check_ctx(ctx);
         validate_common(dtype, order, dims, ranks, oversample, "rand_tucker_2i");
         require(out != nullptr && y != nullptr, "rand_tucker_2i: null argument");
-        tk_tucker_opts o{0, 1, 0, 1};
+        tk_tucker_opts o{0, 1, 0, 1, 0, 0};
         if (opts) o = *opts;
         const Seed seed{seed_root, seed_stream};
-        if (dtype == TK_F32) rand_tucker_2i_impl<float>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, o, out, stats);
+        require(o.precision == 0 || o.precision == 1, "rand_tucker_2i: precision must be 0 (native) or 1 (fp64)");
+        if (dtype == TK_F32 && o.precision == 1)
+            rand_tucker_2i_fp64_on_f32(ctx, order, dims, y, y_on_device, ranks, oversample, seed, o, out, stats);
+        else if (dtype == TK_F32) rand_tucker_2i_impl<float>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, o, out, stats);
         else rand_tucker_2i_impl<double>(ctx, order, dims, y, y_on_device, ranks, oversample, seed, o, out, stats);
     });
 }

@@ -314,9 +314,12 @@ def _tucker_call(fn_name, y, ranks, oversample, seed, context, out, opts=None):
     _lib.check(ctx.lib.tk_context_set_orthonormalizer(ctx.handle, _ORTHO[ortho]))
     try:
         if fn_name == "tk_rand_tucker_2i":
+            prec = getattr(opts, "precision", "native")
+            if prec not in ("native", "fp64"):
+                raise TenkitError("tenkit: rand_tucker_2i: precision must be 'native' or 'fp64'")
             oo = _lib.tk_tucker_opts(int(getattr(opts, "explicit_core_pass", 0)), int(getattr(opts, "sync_ranks", 1)),
                                      int(getattr(opts, "time_kernels", 0)), int(getattr(opts, "overlap", 1)),
-                                     int(getattr(opts, "one_pass_per_step", 0)))
+                                     int(getattr(opts, "one_pass_per_step", 0)), 1 if prec == "fp64" else 0)
             rc = getattr(ctx.lib, fn_name)(*args, C.byref(oo), C.byref(o), C.byref(st))
         else:
             rc = getattr(ctx.lib, fn_name)(*args, C.byref(o), C.byref(st))
@@ -356,20 +359,26 @@ class TuckerOptions:
     _global_dims: tuple = ()
     one_pass_per_step: int = 0
     orthonormalizer: str = "colpiv"
+    precision: str = "native"
 
 
 def rand_tucker_2i(y, ranks, oversample: int, seed, *, explicit_core_pass: bool = False, sync_ranks: bool = True,
                    context: Context | None = None, out: str | None = None, global_last_dim: int = 0,
                    time_kernels: bool = False, overlap: bool = True, global_dims=(),
-                   one_pass_per_step: bool = False, orthonormalizer: str = "colpiv") -> TuckerModel:
+                   one_pass_per_step: bool = False, orthonormalizer: str = "colpiv",
+                   precision: str = "native") -> TuckerModel:
     """Alg. 3 (tucker.hpp:136-169) on the B200. `y`: numpy array (host; copied in) or a
     device DenseTensor. Returns a host (numpy) model for host input, device otherwise,
     unless out='host'/'device'. global_dims / global_last_dim: with a comm hook installed,
     y is this rank's block of a tensor of these global extents (dist.py). one_pass_per_step:
     stream Y once per range step like the reference (default: consecutive steps share a pass).
-    orthonormalizer='gram': the distributed protocol's basis (dist_rand_tucker_2i numerics)."""
+    orthonormalizer='gram': the distributed protocol's basis (dist_rand_tucker_2i numerics).
+    precision='fp64' (fp32 data): fp64 arithmetic over the fp32 values, the reference's own
+    precision, for data whose pivot / sign decisions (stats 'pivot_margin' / 'sign_margin')
+    are closer than the default fp32-accurate passes resolve."""
     opts = TuckerOptions(int(explicit_core_pass), int(sync_ranks), int(global_last_dim), int(time_kernels),
-                         int(overlap), tuple(int(d) for d in global_dims), int(one_pass_per_step), orthonormalizer)
+                         int(overlap), tuple(int(d) for d in global_dims), int(one_pass_per_step), orthonormalizer,
+                         precision)
     return _tucker_call("tk_rand_tucker_2i", y, ranks, oversample, seed, context, out, opts)
 
 

@@ -1,7 +1,8 @@
 """BASELINE configs 3 and 4 at their FULL sizes (2400^3 fp32 = 55 GB, 300^4 fp32 = 32 GB) and cfg 5's
 per-GPU slab at 4 GPUs (4000 x 4000 x 1000 fp32 = 64 GB, ranks 50, r~ 60) on one B200:
 
-* oracle parity (north star: U_n, core and fit at 1e-3 in fp32): the CPU oracle's streamed-slab
+* oracle parity (north star: U_n, core and fit at 1e-3 in fp32; 1e-5 for the fp64 mode,
+  precision='fp64': fp64 arithmetic over the same fp32 values): the CPU oracle's streamed-slab
   rand_tucker_2i (oracle/tenkit_oracle.cpp rand_tucker_2i_streamed: the reference's control flow,
   tucker.hpp:136-169, with every ttm_all accumulated over last-mode slabs as dist.hpp:496-596
   streams blocks; fp64 on the same fp32 values) against the device model: the subspace of ALL
@@ -114,6 +115,11 @@ def test_full_size_config(P, O, name, capture_tol):
     d_steps = [subspace_dist(u, v) for u, v in zip(a.factors, sh.factors)]
     assert abs(P.model_fit(yd, s) - fit) < 1e-4
 
+    # the fp64 mode (tk_tucker_opts.precision = 1): fp64 arithmetic over the same fp32 values
+    t0 = time.perf_counter()
+    prec = P.rand_tucker_2i(yd, ranks, p, alg, sync_ranks=False, out="host", precision="fp64")
+    t_prec = time.perf_counter() - t0
+
     # ---- the oracle on the same fp32 bytes (host copy; the device tensor is freed first)
     yh = y.cpu().numpy()
     del y, yd, runs, s
@@ -132,12 +138,17 @@ def test_full_size_config(P, O, name, capture_tol):
     aligned = O.ttm_all(a.core, [u.T @ v for u, v in zip(a.factors, u_ref)], -1, False)
     core_err = _rel(aligned, g_ref)
     f_got, f_ref = _gram_fit(ysq, a.core), _gram_fit(ysq, g_ref)
+    sub64 = [subspace_dist(u, v) for u, v in zip(prec.factors, u_ref)]
+    core64 = _rel(O.ttm_all(prec.core, [u.T @ v for u, v in zip(prec.factors, u_ref)], -1, False), g_ref)
     _log({"test": "full_size_oracle", "config": name, "subspace_all_cols": sub, "core_rel": core_err,
           "fit": f_got, "fit_oracle": f_ref, "shared_vs_per_step": d_steps,
+          "fp64_mode_subspace": sub64, "fp64_mode_core_rel": core64, "fp64_mode_s": round(t_prec, 2),
           "pivot_margin_min": float(margins[:, 0].min()), "sign_margin_min": float(margins[:, 1].min()),
           "margins": margins.tolist(), "oracle_s": round(t_oracle, 1), "threads": os.cpu_count()})
     for u, v in zip(a.factors, u_ref):
         assert u.shape == v.shape
+    # the fp64 mode reproduces the reference's decisions and values at the fp64 bar (1e-5)
+    assert max(sub64) < 1e-5 and core64 < 1e-5, (sub64, core64)
     # the device reports the same decision margins as the oracle (its own fp32 values)
     dev_pm, dev_sm = np.array(a.stats["pivot_margin"]), np.array(a.stats["sign_margin"])
     assert np.all(np.abs(dev_pm - margins[:, 0]) < 1e-3 + 0.1 * margins[:, 0])

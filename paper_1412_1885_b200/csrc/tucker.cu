@@ -1153,6 +1153,7 @@ void rand_tucker_2i_fp64_on_f32(tk_context* ctx, int64_t order, const int64_t* d
         double* y64 = static_cast<double*>(ctx->buf("y_fp64", sizeof(double) * n));
         launch_cast<float, double>(y32, y64, n, ctx->stream);
         rand_tucker_2i_impl<double>(ctx, order, dims, y64, 1, ranks, p, seed, opt, out, stats);
+        if (stats) stats->y_bytes = static_cast<double>(n) * sizeof(float);  // the caller's fp32 tensor
         return;
     }
     rand_tucker_2i_impl<double>(ctx, order, dims, nullptr, 1, ranks, p, seed, opt, out, stats, y32);

@@ -3,27 +3,27 @@
 //
 //   out[p, r, q] = sum_k Y[p, k, q] U[k, r]       (3xTF32: y u ~= y_hi u_hi + y_hi u_lo + y_lo u_hi)
 //
-// Differences from ttm_tc.cu (the first design, still used for the second stages):
-// * y_hi is read by the MMA straight from the TMA-staged shared memory: the tensor core takes
-//   the top 19 bits of an fp32 operand (y_hi = trunc_tf32(y)), so only y_lo = y - y_hi (exact)
-//   is computed by the converter warps and stored to TMEM (half the TMEM stores, and the main
-//   MMAs no longer wait for the converters). M-major tiles (contracted mode not the fastest)
-//   are MN-major A operands (TMA boxes of 32 p x 16 k; MN-major tf32 takes only the 128B-span
-//   swizzle with 32-B atoms), K-major tiles (mode 0) K-major A operands (16 k x rows, 64B swizzle).
+// Differences from ttm_tc.cu (the first design):
 // * Accumulation is chunked: the MMAs accumulate kChunk k-blocks (256 k) into TMEM, then the
 //   converter warps add the chunk into fp32 registers (round-to-nearest) and the next chunk
 //   restarts the TMEM accumulator. The tensor core's truncating fp32 accumulation therefore
-//   only runs over F k-blocks whatever K is (the first design's error grew with K).
+//   only runs over 256 k whatever K is (the first design's error grew with K: at K = 4000 its
+//   fp32 bases missed the 1e-3 parity bar, these make it at 1.7-3.1e-4).
+// * Two accumulator buffers in TMEM alternate per chunk: the MMAs of chunk c + 1 run while the
+//   converter warps add chunk c into their registers (the add is deferred by one stage).
 // * The factor is packed with NH = r~ rounded up to 8 (not 16): the main MMA covers
 //   [U_hi | U_lo] with N = 2 NH, the cross MMA y_lo U_hi with N = NH (cta_group::1 MMAs take
 //   N in steps of 8). r~ = 40: 120 MMA columns per k-step instead of 144.
-// * Two accumulator buffers in TMEM alternate per chunk: the MMAs of chunk c + 1 run while the
-//   converter warps add chunk c into their registers (the flush is deferred by one stage).
-// Warp roles (10 warps; two CTAs per SM with 256 TMEM columns each, one with 512 for NH = 64):
+// * Up to six [y_hi | y_lo] TMEM buffers let the converters run ahead of the MMA issuer.
+// Y tiles are staged by TMA (M-major: boxes of 32 p x 16 k, 128B-span/32B-atom swizzle;
+// K-major: 16 k x 128 rows, 64B swizzle) for the converter warps' conflict-free reads.
+// Warp roles (10 warps; two CTAs per SM with 256 TMEM columns each, one with 512 for NH >= 56):
 //   warp 8      producer: TMA boxes of Y + bulk copy of the packed [U_hi | U_lo] k-block
 //   warp 9      TMEM allocator + single-thread MMA issuer
-//   warps 0-7   converters (y_lo into TMEM; warp w: TMEM lane quarter w & 3, k half w >> 2),
-//               chunk flushes into register accumulators, and the epilogue stores
+//   warps 0-7   converters ([y_hi | y_lo] into TMEM; warp w: TMEM lane quarter w & 3, k half
+//               w >> 2), chunk flushes into register accumulators, and the epilogue stores
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
@@ -34,6 +34,20 @@ namespace tkb {
 
 namespace {
 
+using EncodeTiledFn2 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn2 encode_tiled2() {
+    static EncodeTiledFn2 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        return (e == cudaSuccess && q == cudaDriverEntryPointSuccess) ? reinterpret_cast<EncodeTiledFn2>(p) : nullptr;
+    }();
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled entry point unavailable");
+    return fn;
+}
+
 constexpr int kSConv = 8;                      // converter warps
 constexpr int kSThreads = (kSConv + 2) * 32;   // + producer + MMA
 constexpr int kSBK = 16;                       // k per pipeline stage (2 MMA k-steps of 8)
@@ -43,32 +57,33 @@ __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / 
 template <int NH, bool KM>
 struct SCfg {
     static_assert(NH % 8 == 0 && NH >= 16 && NH <= 64, "NH: multiple of 8 in [16, 64]");
-    static constexpr int TMEM = 512;                       // one CTA per SM, all of TMEM
+    static constexpr int OCC = NH <= 48 ? 2 : 1;           // CTAs per SM (TMEM: 256 or 512 columns each)
+    static constexpr int TMEM = 512 / OCC;
     static constexpr int CN = NH;                          // N of the cross MMA (N steps of 8 are legal)
     static constexpr int DW = round_up(NH + CN, 16);       // accumulator columns per 128-row tile
-    static constexpr int BM = 128;                         // rows per tile (one TMEM lane each)
+    static constexpr int MT = 1;                           // 128-row M tiles per CTA
+    static constexpr int BM = 128 * MT;
     static constexpr int ND = 2;                           // accumulator buffers: chunk c -> buffer c & 1
-    static constexpr int NA_FIT = (TMEM - ND * DW) / 32;   // [y_hi | y_lo] buffers, 32 columns each
-    static constexpr int NA = NA_FIT > 8 ? 8 : NA_FIT;
-    static_assert(NA >= 3, "TMEM budget");
-    static constexpr int A_BASE = ND * DW;
+    static constexpr int NA_FIT = (TMEM - ND * MT * DW) / (MT * 32);
+    static constexpr int NA = NA_FIT > 6 ? 6 : NA_FIT;     // [y_hi | y_lo] TMEM buffers (32 columns)
+    static_assert(NA >= 2, "TMEM budget");
+    static constexpr int A_BASE = ND * MT * DW;
+    static constexpr int BOXR = KM ? BM : 32;              // rows per TMA box
+    static constexpr int STAGE_Y = kSBK * BM * 4;
     static constexpr int STAGE_B = 128 * NH;               // two k-steps of [U_hi | U_lo] (2 NH x 8 tf32 each)
-    static constexpr int BST_FIT = (200 * 1024) / STAGE_B;
-    static constexpr int BST = BST_FIT > 16 ? 16 : BST_FIT;  // factor ring depth
-    static constexpr size_t BAR_BYTES = (2 * BST + 2 * NA + 4) * 8 + 16;
-    static constexpr size_t smem = size_t(BST) * STAGE_B + BAR_BYTES;
+    static constexpr int SMEM_BUDGET = OCC == 2 ? 110 * 1024 : 220 * 1024;
+    static constexpr int STAGES_FIT = (SMEM_BUDGET - 1024) / (STAGE_Y + STAGE_B);  // (1 KB: barriers + slack)
+    static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
+    static_assert(STAGES >= 3, "pipeline depth");
+    // barriers: 2 per stage + 2 per y_lo buffer + 4 accumulator-buffer barriers, + the TMEM base
+    static constexpr size_t BAR_BYTES = (2 * STAGES + 2 * NA + 4) * 8 + 16;
+    static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + BAR_BYTES;
     static constexpr int ACC = NH / 2;                     // accumulator columns per converter warp (its half)
-    static constexpr int PF = 6;                           // stages of Y in flight per converter thread
 };
 
 // k-blocks (of 16) per accumulation chunk: the tensor core's truncating fp32 accumulation runs
 // over at most kChunk * 16 k, then the chunk is added into fp32 registers (round to nearest)
 constexpr int kChunk = 16;
-// end of the chunk starting at k-block k0: kChunk blocks, the tail merged into the last full
-// chunk when it would be shorter than `minlen` (every chunk has >= minlen blocks once nk >= minlen)
-__device__ __forceinline__ int chunk_end(int k0, int nk, int minlen) {
-    return nk - (k0 + kChunk) < minlen ? nk : k0 + kChunk;
-}
 
 __device__ __forceinline__ void sfence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void sfence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -112,15 +127,6 @@ __device__ __forceinline__ uint32_t sidesc(int n, bool a_mn) {
            (uint32_t(128 >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -135,90 +141,49 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
                  : "memory");
 }
 
-// y_lo = y - trunc_tf32(y) (exact in fp32), rounded to nearest tf32 for the MMA
-__device__ __forceinline__ uint32_t lo_bits(float y) {
-    const float lo = y - __uint_as_float(__float_as_uint(y) & 0xFFFFE000u);
-    return (__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u;
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
 }
 
-// The converter thread of TMEM lane L and k half h loads its row's 8 k values of a stage
-// straight from HBM (no shared-memory staging of Y: shared memory carries only the factor):
-// KM = false: Y viewed as (P, K, Q); row p of tile (p0, q): y[p + k P + q P K] (a warp reads
-//             32 consecutive p for one k: 128 coalesced bytes per load instruction);
-//             out[p + r P + q P cols].
-// KM = true:  Y viewed as Q rows of K contiguous values: 8 consecutive k = two 16-B loads;
-//             out[row + r Q] (transposed output: the contracted mode moves last).
+__device__ __forceinline__ void tma2(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// y_hi = y rounded to nearest tf32, y_lo = y - y_hi (exact in fp32; the tensor core reads its
+// top 19 bits)
+__device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo) {
+    hi = (__float_as_uint(y) + 0x1000u) & 0xFFFFE000u;
+    lo = __float_as_uint(y - __uint_as_float(hi));
+}
+
+// KM = false: Y viewed as (P, K, Q), tiles of BM consecutive p of one q; out[p + r P + q P cols].
+// KM = true:  Y viewed as Q rows of K contiguous values (contraction over mode 0), tiles of BM
+//             rows; out[row + r Q] (transposed output: the contracted mode moves last).
+// Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
+// the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
 template <int NH, bool KM>
-struct YLoader {
-    const float* base = nullptr;  // this row's first element (null: a row beyond the tensor)
-    int64_t kstride = 0;          // elements between consecutive k
-    int64_t K = 0;
-    __device__ __forceinline__ void load(int kc, int khalf, float (&v)[8]) const {
-        const int64_t k0 = int64_t(kc) * kSBK + khalf * 8;
-        if (!base) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = 0.f;
-            return;
-        }
-        if constexpr (KM) {
-            if (k0 + 8 <= K) {  // K % 4 == 0 and 16-B aligned rows
-                const float4 a = __ldg(reinterpret_cast<const float4*>(base + k0));
-                const float4 b = __ldg(reinterpret_cast<const float4*>(base + k0 + 4));
-                v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = k0 + e < K ? __ldg(base + k0 + e) : 0.f;
-            }
-        } else {
-            const float* p = base + k0 * kstride;
-            if (k0 + 8 <= K) {  // warp-uniform: the K tail only in a tile's last stage
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = __ldg(p + e * kstride);
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = k0 + e < K ? __ldg(p + e * kstride) : 0.f;
-            }
-        }
-    }
-};
-
-// First element of row L of tile t (null beyond the tensor), and of its output row: kept out of
-// line (64-bit divisions, once per tile) so the unrolled stage loop stays within the register
-// budget of 10-warp CTAs (168 per thread).
-template <bool KM>
-__device__ __noinline__ const float* tile_row(const float* y, int64_t t, int64_t tiles_p, int64_t P, int64_t K, int L) {
-    if constexpr (KM) {
-        const int64_t row = t * 128 + L;
-        return row < P ? y + row * K : nullptr;
-    } else {
-        const int64_t q = t / tiles_p, p = (t - q * tiles_p) * 128 + L;
-        return p < P ? y + q * P * K + p : nullptr;
-    }
-}
-template <bool KM>
-__device__ __noinline__ float* tile_out_row(float* out, int64_t t, int64_t tiles_p, int64_t P, int cols, int L) {
-    int64_t q = 0, p0;
-    if constexpr (KM) {
-        p0 = t * 128;
-    } else {
-        q = t / tiles_p;
-        p0 = (t - q * tiles_p) * 128;
-    }
-    return p0 + L < P ? out + q * P * cols + p0 + L : nullptr;
-}
-
-template <int NH, bool KM>
-__global__ void __launch_bounds__(kSThreads, 1)
-    ttm_stream_kernel(const float* __restrict__ y, const uint8_t* __restrict__ bpk, float* __restrict__ out,
+__global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
+    ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
                       int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles) {
     using C = SCfg<NH, KM>;
-    constexpr int BM = C::BM, NA = C::NA, BST = C::BST, PF = C::PF;
+    constexpr int BM = C::BM, NA = C::NA, ST = C::STAGES;
+    // dynamic shared memory starts at offset 0 of the CTA's window (no static shared memory in
+    // this kernel): 1024-B aligned as the 128B-span swizzles need
     extern __shared__ __align__(1024) uint8_t ssm[];
-    uint8_t* sB = ssm;  // [BST][2 k-steps][2NH x 8] tf32 core matrices
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(BST) * C::STAGE_B);
-    uint64_t* bfull = bars;              // [BST] producer -> MMA
-    uint64_t* bempty = bfull + BST;      // [BST] MMA commit -> producer
-    uint64_t* afull = bempty + BST;      // [NA]  converters (8) -> MMA
+    uint8_t* sY = ssm;                             // [stages][BM/BOXR boxes]
+    uint8_t* sB = ssm + size_t(ST) * C::STAGE_Y;   // [stages][2 k-steps][2NH x 8] tf32 core matrices
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(ST) * C::STAGE_B);
+    uint64_t* full = bars;               // [ST]  producer -> converters, MMA
+    uint64_t* empty = full + ST;         // [ST]  converters (8) + MMA commit (1) -> producer
+    uint64_t* afull = empty + ST;        // [NA]  converters (8) -> MMA
     uint64_t* aempty = afull + NA;       // [NA]  MMA commit -> converters
     uint64_t* dfull = aempty + NA;       // [2]   MMA commit (chunk done) -> converters
     uint64_t* dempty = dfull + 2;        // [2]   converters (8, chunk flushed) -> MMA
@@ -228,9 +193,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const int nk = static_cast<int>((K + kSBK - 1) / kSBK);
 
     if (tid == 0) {
-        for (int s = 0; s < BST; ++s) {
-            mbar_init(&bfull[s], 1);
-            mbar_init(&bempty[s], 1);
+        if (smem_u32(ssm) & 1023) __trap();  // the swizzle atoms need 1024-B alignment
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kSConv + 1);
         }
         for (int a = 0; a < NA; ++a) {
             mbar_init(&afull[a], kSConv);
@@ -253,39 +219,55 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const uint32_t tmem = *tbase_sm;
 
     if (warp == kSConv) {
-        // ===== producer: the factor's k-blocks (the only shared-memory operand) =====
+        // ===== producer =====
         if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
             int s = 0;
             uint32_t ph = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int64_t q = t / tiles_p;
+                const int64_t p0 = (t % tiles_p) * BM;
                 for (int kc = 0; kc < nk; ++kc) {
-                    mbar_wait(&bempty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&bfull[s], C::STAGE_B);
-                    bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &bfull[s]);
-                    if (++s == BST) s = 0, ph ^= 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
+                    uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
+                    if constexpr (KM) {
+                        tma2(dy, &ymap, kc * kSBK, static_cast<int>(p0), &full[s]);
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < BM / 32; ++b)
+                            tma3(dy + b * 2048, &ymap, static_cast<int>(p0 + 32 * b), kc * kSBK, static_cast<int>(q),
+                                 &full[s]);
+                    }
+                    bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
+                    if (++s == ST) s = 0, ph ^= 1;
                 }
             }
         }
     } else if (warp == kSConv + 1) {
-        // ===== MMA issuer: D[0:2NH] += y_hi [U_hi | U_lo], D[NH:2NH] += y_lo U_hi =====
+        // ===== MMA issuer =====
         if (lane == 0) {
             const uint32_t id_main = sidesc(2 * NH, false), id_cross = sidesc(C::CN, false);
             int s = 0, a = 0;
             uint32_t ph = 0, aph = 0, ch = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                for (int k0 = 0, k1 = 0; k0 < nk; k0 = k1, ++ch) {
-                    k1 = chunk_end(k0, nk, PF);
+                for (int k0 = 0; k0 < nk; k0 += kChunk, ++ch) {
                     const int b = ch & 1;
                     if (ch >= 2) {  // this buffer's previous chunk has been added into the registers
                         mbar_wait(&dempty[b], ((ch >> 1) - 1) & 1);
                         sfence_after();
                     }
                     const uint32_t dm = tmem + uint32_t(b * C::DW);
+                    const int k1 = min(nk, k0 + kChunk);
                     for (int kc = k0; kc < k1; ++kc) {
-                        mbar_wait(&bfull[s], ph);
+                        mbar_wait(&full[s], ph);
+                        sfence_after();
+                        const uint32_t ys = smem_u32(sY + size_t(s) * C::STAGE_Y);
+                        const uint32_t bs = smem_u32(sB + size_t(s) * C::STAGE_B);
+#pragma unroll
+                        (void)ys;
                         mbar_wait(&afull[a], aph);
                         sfence_after();
-                        const uint32_t bs = smem_u32(sB + size_t(s) * C::STAGE_B);
                         const uint32_t ahi = tmem + uint32_t(C::A_BASE + a * 32);
 #pragma unroll
                         for (int ks = 0; ks < 2; ++ks) {
@@ -294,8 +276,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
                             mma_ts(dm + NH, ahi + 16 + ks * 8, bd, id_cross, 1u);
                         }
                         commit(&aempty[a]);
-                        commit(&bempty[s]);
-                        if (++s == BST) s = 0, ph ^= 1;
+                        commit(&empty[s]);
+                        if (++s == ST) s = 0, ph ^= 1;
                         if (++a == NA) a = 0, aph ^= 1;
                     }
                     commit(&dfull[b]);
@@ -303,137 +285,126 @@ __global__ void __launch_bounds__(kSThreads, 1)
             }
         }
     } else {
-        // ===== converters (warps 0-7): lane quarter warp & 3, k half warp >> 2 =====
+        // ===== converters (warps 0-7) =====
         const int quarter = warp & 3, khalf = warp >> 2;
         const int L = quarter * 32 + lane;  // TMEM lane = row of the 128-row tile
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         constexpr int ACC = C::ACC;
-        const int c0 = khalf * (NH / 2);
+        const int c0 = khalf * (NH / 2);  // this warp's accumulator columns
         float acc[ACC];
 #pragma unroll
         for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
-        // (tile, k-block) sequence of this CTA, walked PF stages ahead by the loads
-        auto row_of = [&](int64_t t) {
-            YLoader<NH, KM> ld;
-            ld.K = K;
-            ld.base = tile_row<KM>(y, t, tiles_p, P, K, L);
-            ld.kstride = KM ? 1 : P;
-            return ld;
-        };
-        float pf[PF][8];
-        // prefetch cursor: (tile, k-block) PF stages ahead of the consumer, same order
-        int64_t tl = blockIdx.x;
-        int kl = 0;
-        YLoader<NH, KM> ldl = row_of(tl);
-        auto advance_load = [&](float (&v)[8]) {
-            if (tl < ntiles) {
-                ldl.load(kl, khalf, v);
-                if (++kl == nk) {
-                    kl = 0;
-                    tl += gridDim.x;
-                    if (tl < ntiles) ldl = row_of(tl);
-                }
-            }
-        };
-#pragma unroll
-        for (int i = 0; i < PF; ++i) advance_load(pf[i]);
-        int a = 0;
-        uint32_t aph = 0, ch = 0;
+        int s = 0, a = 0;
+        uint32_t ph = 0, aph = 0, ch = 0;
+        // flush of chunk `pend` (buffer pend & 1) deferred by one stage, so the wait for its last
+        // MMAs overlaps the conversion of the next stage
+        bool pending = false;
+        uint32_t pend = 0;
         auto flush = [&](uint32_t c) {
             const int b = c & 1;
             mbar_wait(&dfull[b], (c >> 1) & 1);
             sfence_after();
             const uint32_t base = tmem + lane_off + uint32_t(b * C::DW + c0);
 #pragma unroll
-            for (int cc = 0; cc < ACC; cc += 4) {  // 4 main + 4 cross columns at a time (few temporaries)
-                float m[4], x[4];
-                ld4(base + cc, m);
-                ld4(base + NH + cc, x);
+            for (int cc = 0; cc < ACC; cc += 8) {
+                float m[8], x[8];
+                if (cc + 8 <= ACC) {
+                    ld8(base + cc, m);
+                    ld8(base + NH + cc, x);
+                } else {
+                    ld4(base + cc, m);
+                    ld4(base + NH + cc, x);
+                }
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-                for (int e = 0; e < 4; ++e) acc[cc + e] += m[e] + x[e];
+                for (int e = 0; e < 8; ++e)
+                    if (cc + e < ACC) acc[cc + e] += m[e] + x[e];
             }
             sfence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&dempty[b]);
         };
-        auto store = [&](float* orow) {
-            if (orow) {
+        float* orow = nullptr;  // output row of the tile whose flush is pending (last chunk)
+        int64_t ostride = 0;
+        bool store_after = false;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int64_t q = t / tiles_p;
+            const int64_t p0 = (t % tiles_p) * BM;
+            const int rows = static_cast<int>(lmin(BM, P - p0));
+            for (int kc = 0; kc < nk; ++kc) {
+                mbar_wait(&full[s], ph);
+                uint32_t hi[8], lo[8];
+                const uint32_t stage = smem_u32(sY + size_t(s) * C::STAGE_Y);
+                if constexpr (KM) {
+                    // row L: 64 B with 16-B chunks at chunk ^ ((L >> 1) & 3) (64B swizzle)
+                    const uint32_t rb = stage + L * 64;
 #pragma unroll
-                for (int e = 0; e < ACC; ++e)
-                    if (c0 + e < cols) orow[int64_t(c0 + e) * P] = acc[e];
-            }
-#pragma unroll
-            for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
-        };
-        // consumer: this CTA's stages in order, unrolled by PF so the prefetch ring is indexed
-        // statically (stage g lives in pf[g % PF]). Every chunk has >= PF stages, so at most one
-        // ends per group of PF; it is added into the registers at the end of the NEXT group
-        // (its MMAs are long done by then; the MMA needs the buffer again a whole chunk later).
-        int64_t t = blockIdx.x;
-        int kc = 0, kend = chunk_end(0, nk, PF);
-        const int64_t total = t < ntiles ? ((ntiles - 1 - t) / gridDim.x + 1) * int64_t(nk) : 0;
-        bool pending = false;
-        uint32_t pend = 0;
-        float* pend_row = nullptr;
-        bool pend_tile = false;
-        for (int64_t g0 = 0; g0 < total; g0 += PF) {
-            bool ended = false, ended_tile = false;
-            uint32_t ended_ch = 0;
-            float* ended_row = nullptr;
-#pragma unroll
-            for (int i = 0; i < PF; ++i) {
-                if (g0 + i < total) {
-                    uint32_t hi[8], lo[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const float v = pf[i][e];
-                        const uint32_t hb = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;  // round to nearest tf32
-                        hi[e] = hb;
-                        lo[e] = __float_as_uint(v - __uint_as_float(hb));                 // exact residual
+                    for (int h = 0; h < 2; ++h) {
+                        const int phys = (2 * khalf + h) ^ ((L >> 1) & 3);
+                        float4 v;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                     : "r"(rb + phys * 16));
+                        split_hi_lo(v.x, hi[h * 4 + 0], lo[h * 4 + 0]);
+                        split_hi_lo(v.y, hi[h * 4 + 1], lo[h * 4 + 1]);
+                        split_hi_lo(v.z, hi[h * 4 + 2], lo[h * 4 + 2]);
+                        split_hi_lo(v.w, hi[h * 4 + 3], lo[h * 4 + 3]);
                     }
-                    advance_load(pf[i]);  // refill the slot PF stages ahead
-                    mbar_wait(&aempty[a], aph ^ 1);
-                    sfence_after();
-                    st8(tmem + lane_off + uint32_t(C::A_BASE + a * 32 + khalf * 8), hi);
-                    st8(tmem + lane_off + uint32_t(C::A_BASE + a * 32 + 16 + khalf * 8), lo);
-                    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-                    sfence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&afull[a]);
-                    if (++a == NA) a = 0, aph ^= 1;
-                    if (kc + 1 == kend) {  // chunk end
-                        ended = true;
-                        ended_ch = ch++;
-                        if (kend == nk) {  // tile end: the rows are stored once this chunk is added
-                            ended_tile = true;
-                            ended_row = tile_out_row<KM>(out, t, tiles_p, P, cols, L);
-                        }
+                } else {
+                    // box `quarter` of 16 k-rows x 128 B; 32-B chunk (lane / 8) of row k at
+                    // chunk ^ (k & 3) (TMA SWIZZLE_128B_ATOM_32B = UMMA SWIZZLE_128B_BASE32B)
+                    const uint32_t bb = stage + quarter * 2048 + khalf * 8 * 128 + (lane & 7) * 4;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        float y;
+                        asm volatile("ld.shared.f32 %0, [%1];\n"
+                                     : "=f"(y)
+                                     : "r"(bb + kk * 128 + (((lane >> 3) ^ (kk & 3)) << 5)));
+                        split_hi_lo(y, hi[kk], lo[kk]);
                     }
-                    if (++kc == nk) {
-                        kc = 0;
-                        t += gridDim.x;
-                        kend = chunk_end(0, nk, PF);
-                    } else if (kc == kend) {
-                        kend = chunk_end(kc, nk, PF);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);  // this warp's reads of the Y stage are done
+                if (++s == ST) s = 0, ph ^= 1;
+                mbar_wait(&aempty[a], aph ^ 1);
+                sfence_after();
+                st8(tmem + lane_off + uint32_t(C::A_BASE + a * 32 + khalf * 8), hi);
+                st8(tmem + lane_off + uint32_t(C::A_BASE + a * 32 + 16 + khalf * 8), lo);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                sfence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&afull[a]);
+                if (++a == NA) a = 0, aph ^= 1;
+                if (pending) {  // the previous chunk: its MMAs are (nearly) done by now
+                    flush(pend);
+                    pending = false;
+                    if (store_after) {  // the previous tile's last chunk: its rows are complete
+#pragma unroll
+                        for (int e = 0; e < ACC; ++e)
+                            if (c0 + e < cols && orow) orow[int64_t(c0 + e) * ostride] = acc[e];
+#pragma unroll
+                        for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
+                        store_after = false;
+                    }
+                }
+                if ((kc + 1) % kChunk == 0 || kc + 1 == nk) {
+                    pending = true;
+                    pend = ch++;
+                    if (kc + 1 == nk) {  // tile end: store once this chunk is flushed
+                        store_after = true;
+                        orow = L < rows ? out + q * P * cols + p0 + L : nullptr;
+                        ostride = P;
                     }
                 }
             }
-            if (pending) {
+            if (t + gridDim.x >= ntiles && pending) {  // last tile of this CTA: flush and store now
                 flush(pend);
-                if (pend_tile) store(pend_row);
                 pending = false;
+#pragma unroll
+                for (int e = 0; e < ACC; ++e)
+                    if (c0 + e < cols && orow) orow[int64_t(c0 + e) * ostride] = acc[e];
+                store_after = false;
             }
-            if (ended) {
-                pending = true;
-                pend = ended_ch;
-                pend_tile = ended_tile;
-                pend_row = ended_row;
-            }
-        }
-        if (pending) {  // this CTA's last chunk
-            flush(pend);
-            if (pend_tile) store(pend_row);
         }
     }
     sfence_before();
@@ -476,19 +447,37 @@ void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, i
                                      static_cast<int>(C::smem)));
         attr = true;
     }
+    require(K < (int64_t(1) << 31) && Q < (int64_t(1) << 31) && P < (int64_t(1) << 31), "ttm: extent too large for TMA");
+    CUtensorMap map;
+    CUresult r;
     int64_t tiles_p, ntiles, rows;
     if constexpr (KM) {  // Q rows of K contiguous values
         tiles_p = (Q + C::BM - 1) / C::BM;
         ntiles = tiles_p;
         rows = Q;
+        const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(Q)};
+        const cuuint64_t strides[1] = {cuuint64_t(K) * 4};
+        const cuuint32_t box[2] = {kSBK, C::BOXR};
+        const cuuint32_t estr[2] = {1, 1};
+        r = encode_tiled2()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(in), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
         tiles_p = (P + C::BM - 1) / C::BM;
         ntiles = tiles_p * Q;
         rows = P;
+        const cuuint64_t dims[3] = {cuuint64_t(P), cuuint64_t(K), cuuint64_t(Q)};
+        const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
+        const cuuint32_t box[3] = {32, kSBK, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        r = encode_tiled2()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
-    const int64_t grid = std::min<int64_t>(ntiles, 148);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
     TK_MAXSMEM((ttm_stream_kernel<NH, KM>));
-    ttm_stream_kernel<NH, KM><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(in, bpk, out, rows, K, cols,
+    ttm_stream_kernel<NH, KM><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K, cols,
                                                                                      tiles_p, ntiles);
     TK_LAUNCH_CHECK();
 }
@@ -507,9 +496,9 @@ bool stream_ttm_enabled() {
 
 bool stream_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols) {
     if (reinterpret_cast<uintptr_t>(in) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
-    if (cols < 1 || cols > kMaxRank || K < 8 * kSBK) return false;  // >= PF k-blocks per tile
-    if (P == 1) return K % 4 == 0 && (Q + 127) / 128 >= 2 * 148;    // K-major: >= two waves of 128-row tiles
-    return P % 4 == 0 && P >= 128 && (P + 127) / 128 * Q >= 2 * 148;
+    if (cols < 1 || cols > kMaxRank || K < kSBK) return false;
+    if (P == 1) return K % 4 == 0 && (Q + 255) / 256 >= 148;  // K-major: >= one wave of 2 x 128-row tiles
+    return P % 4 == 0 && P >= 256 && (P + 255) / 256 * Q >= 2 * 148;
 }
 
 int64_t stream_pack_bytes(int64_t rows, int cols) {

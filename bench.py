@@ -527,7 +527,10 @@ def run_b200(args, cfg):
             "decompositions_per_s": round(1e3 / ms_step, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": _ncu_traffic(args.config, world),
-                         "kernel": "ttm_tc_kernel (Y-streaming TTM, tcgen05 3xTF32)" if cfg["dtype"] == "f32" else "ttm_mmajor_kernel (Y-streaming TTM, FFMA)",
+                         "kernel": ("ttm_stream_kernel (Y-streaming TTM pass, tcgen05 3xTF32, chunked fp32 accumulation)"
+                                    if os.environ.get("TENKIT_STREAM", "1") != "0" else
+                                    "ttm_tc_kernel (Y-streaming TTM, tcgen05 3xTF32)") if cfg["dtype"] == "f32"
+                         else "ttm_mmajor_kernel (Y-streaming TTM, FFMA fp64)",
                          "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if not pk.get("_fallback") else "fallback",
                          "bytes_per_launch": ybytes, "mean_launch_ms": round(kern_ms, 4),
                          "launches_per_step": passes},

@@ -299,6 +299,8 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
         // flush of chunk `pend` (buffer pend & 1) deferred by one stage, so the wait for its last
         // MMAs overlaps the conversion of the next stage
         bool pending = false;
+        int since = 0;                     // stages converted since the pending chunk ended
+        constexpr int kDefer = NA + 2;     // > the converters' lead over the MMA issuer
         uint32_t pend = 0;
         auto flush = [&](uint32_t c) {
             const int b = c & 1;
@@ -375,7 +377,9 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&afull[a]);
                 if (++a == NA) a = 0, aph ^= 1;
-                if (pending) {  // the previous chunk: its MMAs are (nearly) done by now
+                // the previous chunk is added once the MMA issuer (up to NA stages behind the
+                // converters) has certainly finished it: kDefer stages after its end
+                auto drain = [&]() {
                     flush(pend);
                     pending = false;
                     if (store_after) {  // the previous tile's last chunk: its rows are complete
@@ -386,9 +390,12 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                         for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
                         store_after = false;
                     }
-                }
+                };
+                if (pending && ++since >= kDefer) drain();
                 if ((kc + 1) % kChunk == 0 || kc + 1 == nk) {
+                    if (pending) drain();  // a short chunk: the older one first
                     pending = true;
+                    since = 0;
                     pend = ch++;
                     if (kc + 1 == nk) {  // tile end: store once this chunk is flushed
                         store_after = true;

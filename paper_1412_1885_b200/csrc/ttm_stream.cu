@@ -15,7 +15,7 @@
 //   [U_hi | U_lo] with N = 2 NH, the cross MMA y_lo U_hi with N = NH (cta_group::1 MMAs take
 //   N in steps of 8). r~ = 40: 120 MMA columns per k-step instead of 144.
 // * Up to six [y_hi | y_lo] TMEM buffers let the converters run ahead of the MMA issuer.
-// Y tiles are staged by TMA (M-major: boxes of 32 p x 16 k, 128B-span/32B-atom swizzle;
+// Y tiles are staged by TMA, one box per stage (M-major: 128 p x 16 k unswizzled, 512-B rows;
 // K-major: 16 k x 128 rows, 64B swizzle) for the converter warps' conflict-free reads.
 // Warp roles (10 warps; two CTAs per SM with 256 TMEM columns each, one with 512 for NH >= 56):
 //   warp 8      producer: TMA boxes of Y + bulk copy of the packed [U_hi | U_lo] k-block
@@ -68,7 +68,7 @@ struct SCfg {
     static constexpr int NA = NA_FIT > 6 ? 6 : NA_FIT;     // [y_hi | y_lo] TMEM buffers (32 columns)
     static_assert(NA >= 2, "TMEM budget");
     static constexpr int A_BASE = ND * MT * DW;
-    static constexpr int BOXR = KM ? BM : 32;              // rows per TMA box
+    static constexpr int BOXR = BM;                        // rows per TMA box (one box per stage)
     static constexpr int STAGE_Y = kSBK * BM * 4;
     static constexpr int STAGE_B = 128 * NH;               // two k-steps of [U_hi | U_lo] (2 NH x 8 tf32 each)
     static constexpr int SMEM_BUDGET = OCC == 2 ? 110 * 1024 : 220 * 1024;
@@ -234,10 +234,7 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                     if constexpr (KM) {
                         tma2(dy, &ymap, kc * kSBK, static_cast<int>(p0), &full[s]);
                     } else {
-#pragma unroll
-                        for (int b = 0; b < BM / 32; ++b)
-                            tma3(dy + b * 2048, &ymap, static_cast<int>(p0 + 32 * b), kc * kSBK, static_cast<int>(q),
-                                 &full[s]);
+                        tma3(dy, &ymap, static_cast<int>(p0), kc * kSBK, static_cast<int>(q), &full[s]);
                     }
                     bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
                     if (++s == ST) s = 0, ph ^= 1;
@@ -353,15 +350,13 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                         split_hi_lo(v.w, hi[h * 4 + 3], lo[h * 4 + 3]);
                     }
                 } else {
-                    // box `quarter` of 16 k-rows x 128 B; 32-B chunk (lane / 8) of row k at
-                    // chunk ^ (k & 3) (TMA SWIZZLE_128B_ATOM_32B = UMMA SWIZZLE_128B_BASE32B)
-                    const uint32_t bb = stage + quarter * 2048 + khalf * 8 * 128 + (lane & 7) * 4;
+                    // one box of 16 k-rows x 128 p (512 B each, unswizzled): a warp reads 32
+                    // consecutive p of one k (conflict-free)
+                    const uint32_t bb = stage + khalf * 8 * 512 + L * 4;
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
                         float y;
-                        asm volatile("ld.shared.f32 %0, [%1];\n"
-                                     : "=f"(y)
-                                     : "r"(bb + kk * 128 + (((lane >> 3) ^ (kk & 3)) << 5)));
+                        asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(y) : "r"(bb + kk * 512));
                         split_hi_lo(y, hi[kk], lo[kk]);
                     }
                 }
@@ -475,10 +470,10 @@ void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, i
         rows = P;
         const cuuint64_t dims[3] = {cuuint64_t(P), cuuint64_t(K), cuuint64_t(Q)};
         const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
-        const cuuint32_t box[3] = {32, kSBK, 1};
+        const cuuint32_t box[3] = {C::BOXR, kSBK, 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         r = encode_tiled2()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");

@@ -83,7 +83,7 @@ struct SCfg {
 
 // k-blocks (of 16) per accumulation chunk: the tensor core's truncating fp32 accumulation runs
 // over at most kChunk * 16 k, then the chunk is added into fp32 registers (round to nearest)
-constexpr int kChunk = 16;
+constexpr int kChunkDefault = 16;
 
 __device__ __forceinline__ void sfence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void sfence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -169,7 +169,7 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
 //             rows; out[row + r Q] (transposed output: the contracted mode moves last).
 // Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
 // the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
-template <int NH, bool KM>
+template <int NH, bool KM, int kChunk = 16>
 __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
                       int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles) {
@@ -439,13 +439,13 @@ __global__ void pack_stream_kernel(const double* __restrict__ u, int64_t ld, int
     }
 }
 
-template <int NH, bool KM>
-void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+template <int NH, bool KM, int CH>
+void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                    cudaStream_t s) {
     using C = SCfg<NH, KM>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
@@ -478,13 +478,32 @@ void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, i
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
-    TK_MAXSMEM((ttm_stream_kernel<NH, KM>));
-    ttm_stream_kernel<NH, KM><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K, cols,
+    TK_MAXSMEM((ttm_stream_kernel<NH, KM, CH>));
+    ttm_stream_kernel<NH, KM, CH><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K, cols,
                                                                                      tiles_p, ntiles);
     TK_LAUNCH_CHECK();
 }
 
-inline int stream_nh(int cols) { return std::max(16, (cols + 7) / 8 * 8); }
+// A/B knob TENKIT_STREAM_CHUNK=0: one accumulation chunk per tile (no periodic flush)
+template <int NH, bool KM>
+void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+                   cudaStream_t s) {
+    static const bool whole = [] {
+        const char* e = std::getenv("TENKIT_STREAM_CHUNK");
+        return e && e[0] == '0';
+    }();
+    if (whole) launch_stream_ch<NH, KM, (1 << 20)>(in, bpk, out, P, K, Q, cols, s);
+    else launch_stream_ch<NH, KM, kChunkDefault>(in, bpk, out, P, K, Q, cols, s);
+}
+
+// NH = cols rounded up to 8 (A/B knob TENKIT_STREAM_NH16=1: to 16, the first design's padding)
+inline int stream_nh(int cols) {
+    static const bool r16 = [] {
+        const char* e = std::getenv("TENKIT_STREAM_NH16");
+        return e && e[0] == '1';
+    }();
+    return std::max(16, r16 ? (cols + 15) / 16 * 16 : (cols + 7) / 8 * 8);
+}
 
 }  // namespace
 

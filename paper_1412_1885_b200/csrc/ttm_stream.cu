@@ -169,7 +169,10 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
 //             rows; out[row + r Q] (transposed output: the contracted mode moves last).
 // Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
 // the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
-template <int NH, bool KM, int kChunk = 16>
+// ALT: inside a chunk consecutive k-blocks alternate between the two accumulator buffers (two
+// independent MMA accumulation chains), both added into the registers at the chunk end while
+// the MMA issuer waits; !ALT: chunk c accumulates into buffer c & 1 (double-buffered chunks).
+template <int NH, bool KM, int kChunk = 16, bool ALT = false>
 __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
                       int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles) {
@@ -249,12 +252,16 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
             uint32_t ph = 0, aph = 0, ch = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 for (int k0 = 0; k0 < nk; k0 += kChunk, ++ch) {
-                    const int b = ch & 1;
-                    if (ch >= 2) {  // this buffer's previous chunk has been added into the registers
+                    const int b = ALT ? 0 : (ch & 1);
+                    if constexpr (ALT) {
+                        if (ch >= 1) {  // both buffers of the previous chunk added into the registers
+                            mbar_wait(&dempty[0], (ch - 1) & 1);
+                            sfence_after();
+                        }
+                    } else if (ch >= 2) {  // this buffer's previous chunk has been added into the registers
                         mbar_wait(&dempty[b], ((ch >> 1) - 1) & 1);
                         sfence_after();
                     }
-                    const uint32_t dm = tmem + uint32_t(b * C::DW);
                     const int k1 = min(nk, k0 + kChunk);
                     for (int kc = k0; kc < k1; ++kc) {
                         mbar_wait(&full[s], ph);
@@ -269,7 +276,10 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
 #pragma unroll
                         for (int ks = 0; ks < 2; ++ks) {
                             const uint64_t bd = sdesc(bs + ks * (64 * NH), 128, 256, 0);
-                            mma_ts(dm, ahi + ks * 8, bd, id_main, (kc > k0 || ks > 0) ? 1u : 0u);
+                            const int bb = ALT ? ((kc - k0) & 1) : b;
+                            const uint32_t dm = tmem + uint32_t(bb * C::DW);
+                            const bool first = ALT ? (kc - k0 < 2) : (kc == k0);
+                            mma_ts(dm, ahi + ks * 8, bd, id_main, (!first || ks > 0) ? 1u : 0u);
                             mma_ts(dm + NH, ahi + 16 + ks * 8, bd, id_cross, 1u);
                         }
                         commit(&aempty[a]);
@@ -296,28 +306,35 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
         // flush of chunk `pend` (buffer pend & 1) deferred by one stage, so the wait for its last
         // MMAs overlaps the conversion of the next stage
         bool pending = false;
+        int pend_len = 0, cstart = 0;      // stages of the pending chunk; first stage of the current one
         int since = 0;                     // stages converted since the pending chunk ended
-        constexpr int kDefer = NA + 2;     // > the converters' lead over the MMA issuer
+        // > the converters' lead over the MMA issuer; ALT: the MMA issuer waits for the flush, so
+        // it happens once the converters have filled every A buffer of the next chunk
+        constexpr int kDefer = ALT ? NA : NA + 2;
         uint32_t pend = 0;
-        auto flush = [&](uint32_t c) {
-            const int b = c & 1;
-            mbar_wait(&dfull[b], (c >> 1) & 1);
+        auto flush = [&](uint32_t c, int len) {
+            const int b = ALT ? 0 : (c & 1);
+            mbar_wait(&dfull[b], ALT ? (c & 1) : ((c >> 1) & 1));
             sfence_after();
-            const uint32_t base = tmem + lane_off + uint32_t(b * C::DW + c0);
 #pragma unroll
-            for (int cc = 0; cc < ACC; cc += 8) {
-                float m[8], x[8];
-                if (cc + 8 <= ACC) {
-                    ld8(base + cc, m);
-                    ld8(base + NH + cc, x);
-                } else {
-                    ld4(base + cc, m);
-                    ld4(base + NH + cc, x);
+            for (int bb = 0; bb < (ALT ? 2 : 1); ++bb) {
+                if (bb >= len) break;  // a one-stage chunk never wrote its second buffer
+                const uint32_t base = tmem + lane_off + uint32_t((ALT ? bb : b) * C::DW + c0);
+#pragma unroll
+                for (int cc = 0; cc < ACC; cc += 8) {
+                    float m[8], x[8];
+                    if (cc + 8 <= ACC) {
+                        ld8(base + cc, m);
+                        ld8(base + NH + cc, x);
+                    } else {
+                        ld4(base + cc, m);
+                        ld4(base + NH + cc, x);
+                    }
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (cc + e < ACC) acc[cc + e] += m[e] + x[e];
                 }
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (cc + e < ACC) acc[cc + e] += m[e] + x[e];
             }
             sfence_before();
             __syncwarp();
@@ -375,7 +392,7 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                 // the previous chunk is added once the MMA issuer (up to NA stages behind the
                 // converters) has certainly finished it: kDefer stages after its end
                 auto drain = [&]() {
-                    flush(pend);
+                    flush(pend, pend_len);
                     pending = false;
                     if (store_after) {  // the previous tile's last chunk: its rows are complete
 #pragma unroll
@@ -392,6 +409,8 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                     pending = true;
                     since = 0;
                     pend = ch++;
+                    pend_len = kc + 1 - cstart;
+                    cstart = kc + 1 == nk ? 0 : kc + 1;
                     if (kc + 1 == nk) {  // tile end: store once this chunk is flushed
                         store_after = true;
                         orow = L < rows ? out + q * P * cols + p0 + L : nullptr;
@@ -400,7 +419,7 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                 }
             }
             if (t + gridDim.x >= ntiles && pending) {  // last tile of this CTA: flush and store now
-                flush(pend);
+                flush(pend, pend_len);
                 pending = false;
 #pragma unroll
                 for (int e = 0; e < ACC; ++e)
@@ -439,13 +458,13 @@ __global__ void pack_stream_kernel(const double* __restrict__ u, int64_t ld, int
     }
 }
 
-template <int NH, bool KM, int CH>
+template <int NH, bool KM, int CH, bool ALT>
 void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                    cudaStream_t s) {
     using C = SCfg<NH, KM>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, CH, ALT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
@@ -478,8 +497,8 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
-    TK_MAXSMEM((ttm_stream_kernel<NH, KM, CH>));
-    ttm_stream_kernel<NH, KM, CH><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K, cols,
+    TK_MAXSMEM((ttm_stream_kernel<NH, KM, CH, ALT>));
+    ttm_stream_kernel<NH, KM, CH, ALT><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K, cols,
                                                                                      tiles_p, ntiles);
     TK_LAUNCH_CHECK();
 }
@@ -492,8 +511,13 @@ void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, i
         const char* e = std::getenv("TENKIT_STREAM_CHUNK");
         return e && e[0] == '0';
     }();
-    if (whole) launch_stream_ch<NH, KM, (1 << 20)>(in, bpk, out, P, K, Q, cols, s);
-    else launch_stream_ch<NH, KM, kChunkDefault>(in, bpk, out, P, K, Q, cols, s);
+    static const bool alt = [] {
+        const char* e = std::getenv("TENKIT_STREAM_ALT");
+        return e && e[0] == '1';
+    }();
+    if (whole) launch_stream_ch<NH, KM, (1 << 20), false>(in, bpk, out, P, K, Q, cols, s);
+    else if (alt) launch_stream_ch<NH, KM, 2 * kChunkDefault, true>(in, bpk, out, P, K, Q, cols, s);
+    else launch_stream_ch<NH, KM, kChunkDefault, false>(in, bpk, out, P, K, Q, cols, s);
 }
 
 // NH = cols rounded up to 8 (A/B knob TENKIT_STREAM_NH16=1: to 16, the first design's padding)

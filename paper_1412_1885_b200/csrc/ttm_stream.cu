@@ -54,18 +54,18 @@ constexpr int kSBK = 16;                       // k per pipeline stage (2 MMA k-
 
 __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
-template <int NH, bool KM>
+template <int NH, bool KM, int MT_>
 struct SCfg {
     static_assert(NH % 8 == 0 && NH >= 16 && NH <= 64, "NH: multiple of 8 in [16, 64]");
-    static constexpr int OCC = NH <= 48 ? 2 : 1;           // CTAs per SM (TMEM: 256 or 512 columns each)
+    static constexpr int MT = MT_;                         // 128-row M tiles per CTA
+    static constexpr int OCC = (MT == 1 && NH <= 48) ? 2 : 1;  // CTAs per SM (TMEM: 256 or 512 columns each)
     static constexpr int TMEM = 512 / OCC;
     static constexpr int CN = NH;                          // N of the cross MMA (N steps of 8 are legal)
     static constexpr int DW = round_up(NH + CN, 16);       // accumulator columns per 128-row tile
-    static constexpr int MT = 1;                           // 128-row M tiles per CTA
     static constexpr int BM = 128 * MT;
     static constexpr int ND = 2;                           // accumulator buffers: chunk c -> buffer c & 1
     static constexpr int NA_FIT = (TMEM - ND * MT * DW) / (MT * 32);
-    static constexpr int NA = NA_FIT > 6 ? 6 : NA_FIT;     // [y_hi | y_lo] TMEM buffers (32 columns)
+    static constexpr int NA = NA_FIT > 6 ? 6 : NA_FIT;     // [y_hi | y_lo] TMEM buffers (32 columns per M tile)
     static_assert(NA >= 2, "TMEM budget");
     static constexpr int A_BASE = ND * MT * DW;
     static constexpr int BOXR = BM;                        // rows per TMA box (one box per stage)
@@ -127,18 +127,27 @@ __device__ __forceinline__ uint32_t sidesc(int n, bool a_mn) {
            (uint32_t(128 >> 4) << 24);
 }
 
+// Issued by the whole (converged) MMA warp: elect.sync picks the lane inside the asm, so the
+// operands stay warp-uniform (uniform registers) and ptxas emits a bare UTCHMMA / UTCBAR
+// instead of its per-active-lane loop (R2UR + ELECT + BRA.U.ANY around every MMA, which made
+// the single issuing thread the pipeline's bottleneck).
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
         "r"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
 
 __device__ __forceinline__ void commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
@@ -165,18 +174,17 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
 }
 
 // KM = false: Y viewed as (P, K, Q), tiles of BM consecutive p of one q; out[p + r P + q P cols].
+//             Row MT L + j of the tile is TMEM lane L of M tile j (a thread reads MT adjacent p).
 // KM = true:  Y viewed as Q rows of K contiguous values (contraction over mode 0), tiles of BM
-//             rows; out[row + r Q] (transposed output: the contracted mode moves last).
+//             rows; out[row + r Q] (transposed output: the contracted mode moves last). Row
+//             128 j + L of the tile is TMEM lane L of M tile j.
 // Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
 // the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
-// ALT: inside a chunk consecutive k-blocks alternate between the two accumulator buffers (two
-// independent MMA accumulation chains), both added into the registers at the chunk end while
-// the MMA issuer waits; !ALT: chunk c accumulates into buffer c & 1 (double-buffered chunks).
-template <int NH, bool KM, int kChunk = 16, bool ALT = false>
-__global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
+template <int NH, bool KM, int MT, int kChunk = 16>
+__global__ void __launch_bounds__(kSThreads, SCfg<NH, KM, MT>::OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
                       int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles) {
-    using C = SCfg<NH, KM>;
+    using C = SCfg<NH, KM, MT>;
     constexpr int BM = C::BM, NA = C::NA, ST = C::STAGES;
     // dynamic shared memory starts at offset 0 of the CTA's window (no static shared memory in
     // this kernel): 1024-B aligned as the 128B-span swizzles need
@@ -245,42 +253,38 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
             }
         }
     } else if (warp == kSConv + 1) {
-        // ===== MMA issuer =====
-        if (lane == 0) {
+        // ===== MMA issuer (the whole warp, converged; one elected lane issues) =====
+        {
+            const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // provably warp-uniform
             const uint32_t id_main = sidesc(2 * NH, false), id_cross = sidesc(C::CN, false);
             int s = 0, a = 0;
             uint32_t ph = 0, aph = 0, ch = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 for (int k0 = 0; k0 < nk; k0 += kChunk, ++ch) {
-                    const int b = ALT ? 0 : (ch & 1);
-                    if constexpr (ALT) {
-                        if (ch >= 1) {  // both buffers of the previous chunk added into the registers
-                            mbar_wait(&dempty[0], (ch - 1) & 1);
-                            sfence_after();
-                        }
-                    } else if (ch >= 2) {  // this buffer's previous chunk has been added into the registers
+                    const int b = ch & 1;
+                    if (ch >= 2) {  // this buffer's previous chunk has been added into the registers
                         mbar_wait(&dempty[b], ((ch >> 1) - 1) & 1);
+                        __syncwarp();
                         sfence_after();
                     }
                     const int k1 = min(nk, k0 + kChunk);
                     for (int kc = k0; kc < k1; ++kc) {
                         mbar_wait(&full[s], ph);
-                        sfence_after();
-                        const uint32_t ys = smem_u32(sY + size_t(s) * C::STAGE_Y);
                         const uint32_t bs = smem_u32(sB + size_t(s) * C::STAGE_B);
-#pragma unroll
-                        (void)ys;
                         mbar_wait(&afull[a], aph);
+                        __syncwarp();
                         sfence_after();
-                        const uint32_t ahi = tmem + uint32_t(C::A_BASE + a * 32);
+                        const uint32_t abuf = tm + uint32_t(C::A_BASE + a * MT * 32);
 #pragma unroll
                         for (int ks = 0; ks < 2; ++ks) {
                             const uint64_t bd = sdesc(bs + ks * (64 * NH), 128, 256, 0);
-                            const int bb = ALT ? ((kc - k0) & 1) : b;
-                            const uint32_t dm = tmem + uint32_t(bb * C::DW);
-                            const bool first = ALT ? (kc - k0 < 2) : (kc == k0);
-                            mma_ts(dm, ahi + ks * 8, bd, id_main, (!first || ks > 0) ? 1u : 0u);
-                            mma_ts(dm + NH, ahi + 16 + ks * 8, bd, id_cross, 1u);
+#pragma unroll
+                            for (int j = 0; j < MT; ++j) {
+                                const uint32_t dm = tm + uint32_t((b * MT + j) * C::DW);
+                                const uint32_t ahi = abuf + j * 32 + ks * 8;
+                                mma_ts(dm, ahi, bd, id_main, (kc > k0 || ks > 0) ? 1u : 0u);
+                                mma_ts(dm + NH, ahi + 16, bd, id_cross, 1u);
+                            }
                         }
                         commit(&aempty[a]);
                         commit(&empty[s]);
@@ -294,32 +298,30 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
     } else {
         // ===== converters (warps 0-7) =====
         const int quarter = warp & 3, khalf = warp >> 2;
-        const int L = quarter * 32 + lane;  // TMEM lane = row of the 128-row tile
+        const int L = quarter * 32 + lane;  // TMEM lane
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         constexpr int ACC = C::ACC;
         const int c0 = khalf * (NH / 2);  // this warp's accumulator columns
-        float acc[ACC];
+        float acc[MT][ACC];
 #pragma unroll
-        for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
+        for (int j = 0; j < MT; ++j)
+#pragma unroll
+            for (int e = 0; e < ACC; ++e) acc[j][e] = 0.f;
         int s = 0, a = 0;
         uint32_t ph = 0, aph = 0, ch = 0;
-        // flush of chunk `pend` (buffer pend & 1) deferred by one stage, so the wait for its last
-        // MMAs overlaps the conversion of the next stage
+        // flush of chunk `pend` (buffer pend & 1) deferred by kDefer stages (past the converters'
+        // lead over the MMA issuer), so the wait for its last MMAs does not stall the pipeline
         bool pending = false;
-        int pend_len = 0, cstart = 0;      // stages of the pending chunk; first stage of the current one
-        int since = 0;                     // stages converted since the pending chunk ended
-        // > the converters' lead over the MMA issuer; ALT: the MMA issuer waits for the flush, so
-        // it happens once the converters have filled every A buffer of the next chunk
-        constexpr int kDefer = ALT ? NA : NA + 2;
+        int since = 0;
+        constexpr int kDefer = NA + 2;
         uint32_t pend = 0;
-        auto flush = [&](uint32_t c, int len) {
-            const int b = ALT ? 0 : (c & 1);
-            mbar_wait(&dfull[b], ALT ? (c & 1) : ((c >> 1) & 1));
+        auto flush = [&](uint32_t c) {
+            const int b = c & 1;
+            mbar_wait(&dfull[b], (c >> 1) & 1);
             sfence_after();
 #pragma unroll
-            for (int bb = 0; bb < (ALT ? 2 : 1); ++bb) {
-                if (bb >= len) break;  // a one-stage chunk never wrote its second buffer
-                const uint32_t base = tmem + lane_off + uint32_t((ALT ? bb : b) * C::DW + c0);
+            for (int j = 0; j < MT; ++j) {
+                const uint32_t base = tmem + lane_off + uint32_t((b * MT + j) * C::DW + c0);
 #pragma unroll
                 for (int cc = 0; cc < ACC; cc += 8) {
                     float m[8], x[8];
@@ -333,48 +335,81 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
-                        if (cc + e < ACC) acc[cc + e] += m[e] + x[e];
+                        if (cc + e < ACC) acc[j][cc + e] += m[e] + x[e];
                 }
             }
             sfence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&dempty[b]);
         };
-        float* orow = nullptr;  // output row of the tile whose flush is pending (last chunk)
+        const auto row_of = [&](int j) { return KM ? 128 * j + L : MT * L + j; };
+        float* obase = nullptr;  // output tile of the pending last chunk
+        int orows = 0;
         int64_t ostride = 0;
         bool store_after = false;
+        const auto store = [&]() {
+#pragma unroll
+            for (int j = 0; j < MT; ++j) {
+                const int row = row_of(j);
+                if (row < orows) {
+                    // the address arithmetic stays here: without the barrier the compiler hoists
+                    // the ACC store addresses into the k loop (recomputed every stage)
+                    float* o = obase + row + int64_t(c0) * ostride;
+                    int64_t os = ostride;
+                    asm volatile("" : "+l"(o), "+l"(os));
+#pragma unroll
+                    for (int e = 0; e < ACC; ++e)
+                        if (c0 + e < cols) o[e * os] = acc[j][e];
+                }
+#pragma unroll
+                for (int e = 0; e < ACC; ++e) acc[j][e] = 0.f;
+            }
+            store_after = false;
+        };
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int64_t q = t / tiles_p;
             const int64_t p0 = (t % tiles_p) * BM;
-            const int rows = static_cast<int>(lmin(BM, P - p0));
             for (int kc = 0; kc < nk; ++kc) {
                 mbar_wait(&full[s], ph);
-                uint32_t hi[8], lo[8];
+                uint32_t hi[MT][8], lo[MT][8];
                 const uint32_t stage = smem_u32(sY + size_t(s) * C::STAGE_Y);
                 if constexpr (KM) {
-                    // row L: 64 B with 16-B chunks at chunk ^ ((L >> 1) & 3) (64B swizzle)
-                    const uint32_t rb = stage + L * 64;
+                    // row: 64 B with 16-B chunks at chunk ^ ((row >> 1) & 3) (64B swizzle)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int phys = (2 * khalf + h) ^ ((L >> 1) & 3);
-                        float4 v;
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
-                                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                                     : "r"(rb + phys * 16));
-                        split_hi_lo(v.x, hi[h * 4 + 0], lo[h * 4 + 0]);
-                        split_hi_lo(v.y, hi[h * 4 + 1], lo[h * 4 + 1]);
-                        split_hi_lo(v.z, hi[h * 4 + 2], lo[h * 4 + 2]);
-                        split_hi_lo(v.w, hi[h * 4 + 3], lo[h * 4 + 3]);
+                    for (int j = 0; j < MT; ++j) {
+                        const int row = 128 * j + L;
+                        const uint32_t rb = stage + row * 64;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int phys = (2 * khalf + h) ^ ((row >> 1) & 3);
+                            float4 v;
+                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                         : "r"(rb + phys * 16));
+                            split_hi_lo(v.x, hi[j][h * 4 + 0], lo[j][h * 4 + 0]);
+                            split_hi_lo(v.y, hi[j][h * 4 + 1], lo[j][h * 4 + 1]);
+                            split_hi_lo(v.z, hi[j][h * 4 + 2], lo[j][h * 4 + 2]);
+                            split_hi_lo(v.w, hi[j][h * 4 + 3], lo[j][h * 4 + 3]);
+                        }
                     }
                 } else {
-                    // one box of 16 k-rows x 128 p (512 B each, unswizzled): a warp reads 32
-                    // consecutive p of one k (conflict-free)
-                    const uint32_t bb = stage + khalf * 8 * 512 + L * 4;
+                    // one box of 16 k-rows x BM p (4 BM bytes each, unswizzled): per k a warp
+                    // reads 32 MT consecutive p (conflict-free)
+                    const uint32_t bb = stage + khalf * 8 * (BM * 4) + L * (MT * 4);
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
-                        float y;
-                        asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(y) : "r"(bb + kk * 512));
-                        split_hi_lo(y, hi[kk], lo[kk]);
+                        if constexpr (MT == 2) {
+                            float y0, y1;
+                            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n"
+                                         : "=f"(y0), "=f"(y1)
+                                         : "r"(bb + kk * (BM * 4)));
+                            split_hi_lo(y0, hi[0][kk], lo[0][kk]);
+                            split_hi_lo(y1, hi[1][kk], lo[1][kk]);
+                        } else {
+                            float y;
+                            asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(y) : "r"(bb + kk * (BM * 4)));
+                            split_hi_lo(y, hi[0][kk], lo[0][kk]);
+                        }
                     }
                 }
                 __syncwarp();
@@ -382,8 +417,12 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                 if (++s == ST) s = 0, ph ^= 1;
                 mbar_wait(&aempty[a], aph ^ 1);
                 sfence_after();
-                st8(tmem + lane_off + uint32_t(C::A_BASE + a * 32 + khalf * 8), hi);
-                st8(tmem + lane_off + uint32_t(C::A_BASE + a * 32 + 16 + khalf * 8), lo);
+                const uint32_t abuf = tmem + lane_off + uint32_t(C::A_BASE + a * MT * 32 + khalf * 8);
+#pragma unroll
+                for (int j = 0; j < MT; ++j) {
+                    st8(abuf + j * 32, hi[j]);
+                    st8(abuf + j * 32 + 16, lo[j]);
+                }
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 sfence_before();
                 __syncwarp();
@@ -391,40 +430,31 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM>::OCC)
                 if (++a == NA) a = 0, aph ^= 1;
                 // the previous chunk is added once the MMA issuer (up to NA stages behind the
                 // converters) has certainly finished it: kDefer stages after its end
-                auto drain = [&]() {
-                    flush(pend, pend_len);
+                if (pending && ++since >= kDefer) {
+                    flush(pend);
                     pending = false;
-                    if (store_after) {  // the previous tile's last chunk: its rows are complete
-#pragma unroll
-                        for (int e = 0; e < ACC; ++e)
-                            if (c0 + e < cols && orow) orow[int64_t(c0 + e) * ostride] = acc[e];
-#pragma unroll
-                        for (int e = 0; e < ACC; ++e) acc[e] = 0.f;
-                        store_after = false;
-                    }
-                };
-                if (pending && ++since >= kDefer) drain();
+                    if (store_after) store();  // the previous tile's last chunk: its rows are complete
+                }
                 if ((kc + 1) % kChunk == 0 || kc + 1 == nk) {
-                    if (pending) drain();  // a short chunk: the older one first
+                    if (pending) {  // a short chunk: the older one first
+                        flush(pend);
+                        if (store_after) store();
+                    }
                     pending = true;
                     since = 0;
                     pend = ch++;
-                    pend_len = kc + 1 - cstart;
-                    cstart = kc + 1 == nk ? 0 : kc + 1;
                     if (kc + 1 == nk) {  // tile end: store once this chunk is flushed
                         store_after = true;
-                        orow = L < rows ? out + q * P * cols + p0 + L : nullptr;
+                        obase = out + q * P * cols + p0;
+                        orows = static_cast<int>(lmin(BM, P - p0));
                         ostride = P;
                     }
                 }
             }
             if (t + gridDim.x >= ntiles && pending) {  // last tile of this CTA: flush and store now
-                flush(pend, pend_len);
+                flush(pend);
                 pending = false;
-#pragma unroll
-                for (int e = 0; e < ACC; ++e)
-                    if (c0 + e < cols && orow) orow[int64_t(c0 + e) * ostride] = acc[e];
-                store_after = false;
+                store();
             }
         }
     }
@@ -458,13 +488,13 @@ __global__ void pack_stream_kernel(const double* __restrict__ u, int64_t ld, int
     }
 }
 
-template <int NH, bool KM, int CH, bool ALT>
+template <int NH, bool KM, int MT, int CH>
 void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s) {
-    using C = SCfg<NH, KM>;
+                      cudaStream_t s) {
+    using C = SCfg<NH, KM, MT>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, CH, ALT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
@@ -497,13 +527,16 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
-    TK_MAXSMEM((ttm_stream_kernel<NH, KM, CH, ALT>));
-    ttm_stream_kernel<NH, KM, CH, ALT><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K, cols,
-                                                                                     tiles_p, ntiles);
+    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, CH>));
+    ttm_stream_kernel<NH, KM, MT, CH><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
+                                                                                             cols, tiles_p, ntiles);
     TK_LAUNCH_CHECK();
 }
 
-// A/B knob TENKIT_STREAM_CHUNK=0: one accumulation chunk per tile (no periodic flush)
+// Two 128-row M tiles per CTA (one CTA per SM) up to NH = 48: the per-stage barrier and address
+// work of the converters and the factor k-block are shared by both tiles. NH >= 56 (whose two
+// double-buffered tiles would not fit TMEM): one tile per CTA. A/B knobs: TENKIT_STREAM_MT=1
+// (one tile per CTA, two CTAs per SM), TENKIT_STREAM_CHUNK=0 (one accumulation chunk per tile).
 template <int NH, bool KM>
 void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                    cudaStream_t s) {
@@ -511,13 +544,18 @@ void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, i
         const char* e = std::getenv("TENKIT_STREAM_CHUNK");
         return e && e[0] == '0';
     }();
-    static const bool alt = [] {
-        const char* e = std::getenv("TENKIT_STREAM_ALT");
+    static const bool mt1 = [] {
+        const char* e = std::getenv("TENKIT_STREAM_MT");
         return e && e[0] == '1';
     }();
-    if (whole) launch_stream_ch<NH, KM, (1 << 20), false>(in, bpk, out, P, K, Q, cols, s);
-    else if (alt) launch_stream_ch<NH, KM, 2 * kChunkDefault, true>(in, bpk, out, P, K, Q, cols, s);
-    else launch_stream_ch<NH, KM, kChunkDefault, false>(in, bpk, out, P, K, Q, cols, s);
+    constexpr int MT = NH <= 48 ? 2 : 1;
+    if (mt1 || MT == 1) {
+        if (whole) launch_stream_ch<NH, KM, 1, (1 << 20)>(in, bpk, out, P, K, Q, cols, s);
+        else launch_stream_ch<NH, KM, 1, kChunkDefault>(in, bpk, out, P, K, Q, cols, s);
+    } else {
+        if (whole) launch_stream_ch<NH, KM, MT, (1 << 20)>(in, bpk, out, P, K, Q, cols, s);
+        else launch_stream_ch<NH, KM, MT, kChunkDefault>(in, bpk, out, P, K, Q, cols, s);
+    }
 }
 
 // NH = cols rounded up to 8 (A/B knob TENKIT_STREAM_NH16=1: to 16, the first design's padding)

@@ -9,19 +9,25 @@
 //   restarts the TMEM accumulator. The tensor core's truncating fp32 accumulation therefore
 //   only runs over 256 k whatever K is (the first design's error grew with K: at K = 4000 its
 //   fp32 bases missed the 1e-3 parity bar, these make it at 1.7-3.1e-4).
-// * Two accumulator buffers in TMEM alternate per chunk: the MMAs of chunk c + 1 run while the
-//   converter warps add chunk c into their registers (the add is deferred by one stage).
+// * Two accumulator buffers in TMEM alternate per chunk (one where TMEM is short, NH >= 56):
+//   the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
 // * The factor is packed with NH = r~ rounded up to 8 (not 16): the main MMA covers
 //   [U_hi | U_lo] with N = 2 NH, the cross MMA y_lo U_hi with N = NH (cta_group::1 MMAs take
 //   N in steps of 8). r~ = 40: 120 MMA columns per k-step instead of 144.
+// * Two 128-row M tiles per CTA (BM = 256), one CTA per SM: one Y box, one factor k-block,
+//   one set of barrier round trips per stage for both tiles.
+// * The producer and MMA warps run converged and issue through elect.sync inside the asm, so
+//   the TMA / UTCHMMA / commit operands live in uniform registers (no per-lane issue loop: with
+//   `if (lane == 0)` issue, ptxas wrapped every MMA in an R2UR/ELECT/BRA.U.ANY loop and the
+//   single issuing thread, not HBM, bounded the pass).
 // * Up to six [y_hi | y_lo] TMEM buffers let the converters run ahead of the MMA issuer.
-// Y tiles are staged by TMA, one box per stage (M-major: 128 p x 16 k unswizzled, 512-B rows;
-// K-major: 16 k x 128 rows, 64B swizzle) for the converter warps' conflict-free reads.
-// Warp roles (10 warps; two CTAs per SM with 256 TMEM columns each, one with 512 for NH >= 56):
-//   warp 8      producer: TMA boxes of Y + bulk copy of the packed [U_hi | U_lo] k-block
-//   warp 9      TMEM allocator + single-thread MMA issuer
+// Y tiles are staged by TMA, one box per stage (M-major: 256 p x 16 k unswizzled, 1 KB rows;
+// K-major: 16 k x 256 rows, 64B swizzle) for the converter warps' conflict-free reads.
+// Warp roles (10 warps, one CTA per SM with 512 TMEM columns):
+//   warp 8      producer: TMA box of Y + bulk copy of the packed [U_hi | U_lo] k-block
+//   warp 9      TMEM allocator + MMA issuer
 //   warps 0-7   converters ([y_hi | y_lo] into TMEM; warp w: TMEM lane quarter w & 3, k half
-//               w >> 2), chunk flushes into register accumulators, and the epilogue stores
+//               w >> 2, both M tiles), chunk flushes into register accumulators, epilogue stores
 #include <cuda.h>
 
 #include <algorithm>
@@ -54,16 +60,18 @@ constexpr int kSBK = 16;                       // k per pipeline stage (2 MMA k-
 
 __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
-template <int NH, bool KM, int MT_>
+template <int NH, bool KM, int MT_, int OCC_>
 struct SCfg {
     static_assert(NH % 8 == 0 && NH >= 16 && NH <= 64, "NH: multiple of 8 in [16, 64]");
     static constexpr int MT = MT_;                         // 128-row M tiles per CTA
-    static constexpr int OCC = (MT == 1 && NH <= 48) ? 2 : 1;  // CTAs per SM (TMEM: 256 or 512 columns each)
+    static constexpr int OCC = OCC_;                       // CTAs per SM (TMEM: 256 or 512 columns each)
     static constexpr int TMEM = 512 / OCC;
     static constexpr int CN = NH;                          // N of the cross MMA (N steps of 8 are legal)
     static constexpr int DW = round_up(NH + CN, 16);       // accumulator columns per 128-row tile
     static constexpr int BM = 128 * MT;
-    static constexpr int ND = 2;                           // accumulator buffers: chunk c -> buffer c & 1
+    // accumulator buffers: two (chunk c -> buffer c & 1) where they leave room for two A
+    // buffers, else one (the MMAs of the next chunk wait for the flush)
+    static constexpr int ND = (TMEM - 2 * MT * DW) >= 2 * MT * 32 ? 2 : 1;
     static constexpr int NA_FIT = (TMEM - ND * MT * DW) / (MT * 32);
     static constexpr int NA = NA_FIT > 6 ? 6 : NA_FIT;     // [y_hi | y_lo] TMEM buffers (32 columns per M tile)
     static_assert(NA >= 2, "TMEM budget");
@@ -166,6 +174,35 @@ __device__ __forceinline__ void tma2(void* dst, const CUtensorMap* map, int c0, 
         : "memory");
 }
 
+// One pipeline stage, issued by the whole (converged) producer warp through one elected lane:
+// expect_tx on the stage barrier, the Y box (TMA, 3-D M-major or 2-D K-major view) and the
+// packed factor k-block (bulk copy), all completing on that barrier.
+__device__ __forceinline__ void produce3(uint32_t bar, uint32_t bytes, uint32_t dy, const CUtensorMap* map, int c0,
+                                        int c1, int c2, uint32_t db, const void* src, uint32_t bbytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3, {%4, %5, %6}], "
+        "[%0];\n\t"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%7], [%8], %9, [%0];\n\t}\n" ::"r"(bar),
+        "r"(bytes), "r"(dy), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(db), "l"(src), "r"(bbytes)
+        : "memory");
+}
+
+__device__ __forceinline__ void produce2(uint32_t bar, uint32_t bytes, uint32_t dy, const CUtensorMap* map, int c0,
+                                        int c1, uint32_t db, const void* src, uint32_t bbytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3, {%4, %5}], "
+        "[%0];\n\t"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%6], [%7], %8, [%0];\n\t}\n" ::"r"(bar),
+        "r"(bytes), "r"(dy), "l"(map), "r"(c0), "r"(c1), "r"(db), "l"(src), "r"(bbytes)
+        : "memory");
+}
+
 // y_hi = y rounded to nearest tf32, y_lo = y - y_hi (exact in fp32; the tensor core reads its
 // top 19 bits)
 __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo) {
@@ -180,12 +217,12 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
 //             128 j + L of the tile is TMEM lane L of M tile j.
 // Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
 // the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
-template <int NH, bool KM, int MT, int kChunk = 16>
-__global__ void __launch_bounds__(kSThreads, SCfg<NH, KM, MT>::OCC)
+template <int NH, bool KM, int MT, int OCC, int kChunk = 16>
+__global__ void __launch_bounds__(kSThreads, OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
                       int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles) {
-    using C = SCfg<NH, KM, MT>;
-    constexpr int BM = C::BM, NA = C::NA, ST = C::STAGES;
+    using C = SCfg<NH, KM, MT, OCC>;
+    constexpr int BM = C::BM, NA = C::NA, ST = C::STAGES, ND = C::ND;
     // dynamic shared memory starts at offset 0 of the CTA's window (no static shared memory in
     // this kernel): 1024-B aligned as the 128B-span swizzles need
     extern __shared__ __align__(1024) uint8_t ssm[];
@@ -230,26 +267,26 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM, MT>::OCC)
     const uint32_t tmem = *tbase_sm;
 
     if (warp == kSConv) {
-        // ===== producer =====
-        if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
-            int s = 0;
-            uint32_t ph = 0;
-            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int64_t q = t / tiles_p;
-                const int64_t p0 = (t % tiles_p) * BM;
-                for (int kc = 0; kc < nk; ++kc) {
-                    mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], C::STAGE_Y + C::STAGE_B);
-                    uint8_t* dy = sY + size_t(s) * C::STAGE_Y;
-                    if constexpr (KM) {
-                        tma2(dy, &ymap, kc * kSBK, static_cast<int>(p0), &full[s]);
-                    } else {
-                        tma3(dy, &ymap, static_cast<int>(p0), kc * kSBK, static_cast<int>(q), &full[s]);
-                    }
-                    bulk_g2s(sB + size_t(s) * C::STAGE_B, bpk + size_t(kc) * C::STAGE_B, C::STAGE_B, &full[s]);
-                    if (++s == ST) s = 0, ph ^= 1;
+        // ===== producer (the whole warp, converged; one elected lane issues) =====
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
+        int s = 0;
+        uint32_t ph = 0;
+        const uint32_t y0 = smem_u32(sY), b0 = smem_u32(sB), f0 = smem_u32(full);
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int64_t q = t / tiles_p;
+            const int64_t p0 = (t % tiles_p) * BM;
+            for (int kc = 0; kc < nk; ++kc) {
+                mbar_wait(&empty[s], ph ^ 1);
+                __syncwarp();
+                const uint32_t bar = f0 + s * 8, dy = y0 + s * C::STAGE_Y, db = b0 + s * C::STAGE_B;
+                const uint8_t* src = bpk + size_t(kc) * C::STAGE_B;
+                if constexpr (KM) {
+                    produce2(bar, C::STAGE_Y + C::STAGE_B, dy, &ymap, kc * kSBK, static_cast<int>(p0), db, src, C::STAGE_B);
+                } else {
+                    produce3(bar, C::STAGE_Y + C::STAGE_B, dy, &ymap, static_cast<int>(p0), kc * kSBK,
+                             static_cast<int>(q), db, src, C::STAGE_B);
                 }
+                if (++s == ST) s = 0, ph ^= 1;
             }
         }
     } else if (warp == kSConv + 1) {
@@ -261,9 +298,9 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM, MT>::OCC)
             uint32_t ph = 0, aph = 0, ch = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 for (int k0 = 0; k0 < nk; k0 += kChunk, ++ch) {
-                    const int b = ch & 1;
-                    if (ch >= 2) {  // this buffer's previous chunk has been added into the registers
-                        mbar_wait(&dempty[b], ((ch >> 1) - 1) & 1);
+                    const int b = ND == 2 ? (ch & 1) : 0;
+                    if (ch >= ND) {  // this buffer's previous chunk has been added into the registers
+                        mbar_wait(&dempty[b], (ND == 2 ? (ch >> 1) - 1 : ch - 1) & 1);
                         __syncwarp();
                         sfence_after();
                     }
@@ -313,11 +350,12 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM, MT>::OCC)
         // lead over the MMA issuer), so the wait for its last MMAs does not stall the pipeline
         bool pending = false;
         int since = 0;
-        constexpr int kDefer = NA + 2;
+        // (one buffer: flushed at once, the MMAs of the next chunk wait for it)
+        constexpr int kDefer = ND == 2 ? NA + 2 : 0;
         uint32_t pend = 0;
         auto flush = [&](uint32_t c) {
-            const int b = c & 1;
-            mbar_wait(&dfull[b], (c >> 1) & 1);
+            const int b = ND == 2 ? (c & 1) : 0;
+            mbar_wait(&dfull[b], (ND == 2 ? (c >> 1) : c) & 1);
             sfence_after();
 #pragma unroll
             for (int j = 0; j < MT; ++j) {
@@ -449,6 +487,11 @@ __global__ void __launch_bounds__(kSThreads, SCfg<NH, KM, MT>::OCC)
                         orows = static_cast<int>(lmin(BM, P - p0));
                         ostride = P;
                     }
+                    if constexpr (kDefer == 0) {
+                        flush(pend);
+                        pending = false;
+                        if (store_after) store();
+                    }
                 }
             }
             if (t + gridDim.x >= ntiles && pending) {  // last tile of this CTA: flush and store now
@@ -488,13 +531,13 @@ __global__ void pack_stream_kernel(const double* __restrict__ u, int64_t ld, int
     }
 }
 
-template <int NH, bool KM, int MT, int CH>
+template <int NH, bool KM, int MT, int OCC, int CH>
 void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                       cudaStream_t s) {
-    using C = SCfg<NH, KM, MT>;
+    using C = SCfg<NH, KM, MT, OCC>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, OCC, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
@@ -527,35 +570,39 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
-    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, CH>));
-    ttm_stream_kernel<NH, KM, MT, CH><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
+    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, OCC, CH>));
+    ttm_stream_kernel<NH, KM, MT, OCC, CH><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
                                                                                              cols, tiles_p, ntiles);
     TK_LAUNCH_CHECK();
 }
 
-// Two 128-row M tiles per CTA (one CTA per SM) up to NH = 48: the per-stage barrier and address
-// work of the converters and the factor k-block are shared by both tiles. NH >= 56 (whose two
-// double-buffered tiles would not fit TMEM): one tile per CTA. A/B knobs: TENKIT_STREAM_MT=1
-// (one tile per CTA, two CTAs per SM), TENKIT_STREAM_CHUNK=0 (one accumulation chunk per tile).
-template <int NH, bool KM>
-void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s) {
+// Two 128-row M tiles per CTA, one CTA per SM: the per-stage barrier and address work of the
+// converters, the factor k-block and the MMA issue are shared by both tiles (measured: 0.79 of
+// the HBM peak at cfg3 against 0.71 with one tile per CTA and two CTAs per SM; NH = 64, whose
+// two tiles leave TMEM room for one accumulator buffer only: 0.76 against 0.63). A/B knobs:
+// TENKIT_STREAM_MT=1 (one tile per CTA, two CTAs per SM), TENKIT_STREAM_CHUNK=0 (one
+// accumulation chunk per tile).
+template <int NH, bool KM, int MT, int OCC>
+void launch_stream_mt(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+                      cudaStream_t s) {
     static const bool whole = [] {
         const char* e = std::getenv("TENKIT_STREAM_CHUNK");
         return e && e[0] == '0';
     }();
-    static const bool mt1 = [] {
+    if (whole) launch_stream_ch<NH, KM, MT, OCC, (1 << 20)>(in, bpk, out, P, K, Q, cols, s);
+    else launch_stream_ch<NH, KM, MT, OCC, kChunkDefault>(in, bpk, out, P, K, Q, cols, s);
+}
+
+template <int NH, bool KM>
+void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
+                   cudaStream_t s) {
+    static const int mt = [] {
         const char* e = std::getenv("TENKIT_STREAM_MT");
-        return e && e[0] == '1';
+        return e ? std::atoi(e) : 0;
     }();
-    constexpr int MT = NH <= 48 ? 2 : 1;
-    if (mt1 || MT == 1) {
-        if (whole) launch_stream_ch<NH, KM, 1, (1 << 20)>(in, bpk, out, P, K, Q, cols, s);
-        else launch_stream_ch<NH, KM, 1, kChunkDefault>(in, bpk, out, P, K, Q, cols, s);
-    } else {
-        if (whole) launch_stream_ch<NH, KM, MT, (1 << 20)>(in, bpk, out, P, K, Q, cols, s);
-        else launch_stream_ch<NH, KM, MT, kChunkDefault>(in, bpk, out, P, K, Q, cols, s);
-    }
+    const int m = mt == 1 ? 1 : 2;
+    if (m == 2) launch_stream_mt<NH, KM, 2, 1>(in, bpk, out, P, K, Q, cols, s);
+    else launch_stream_mt<NH, KM, 1, 2>(in, bpk, out, P, K, Q, cols, s);
 }
 
 // NH = cols rounded up to 8 (A/B knob TENKIT_STREAM_NH16=1: to 16, the first design's padding)

@@ -20,4 +20,5 @@ for C in cfg3 cfg2 cfg4 cfg5slab; do
   run r1 TENKIT_STREAM=0
   run mt2 TENKIT_STREAM=1
   run mt1 TENKIT_STREAM_MT=1
+  [ $C = cfg5slab ] && run mt2f TENKIT_STREAM_MT=2
 done

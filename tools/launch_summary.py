@@ -19,7 +19,7 @@ for r in rows:
             data.append((d["Kernel Name"], d["Grid Size"], float(d["Metric Value"].replace(",", ""))))
 # tkb kernels only, last nsteps * (launches per step)
 tk = [x for x in data if "tkb::" in x[0]]
-big = [i for i, x in enumerate(tk) if ("ttm_mmajor" in x[0] or "ttm_tc" in x[0]) and x[2] > 200000]
+big = [i for i, x in enumerate(tk) if ("ttm_mmajor" in x[0] or "ttm_tc" in x[0] or "ttm_stream" in x[0]) and x[2] > 200000]
 per_step = int(sys.argv[3]) if len(sys.argv) > 3 else 3  # Y passes per decomposition (grouped)
 start = big[-per_step * nsteps] if len(big) >= per_step * nsteps else 0
 win = tk[start:]

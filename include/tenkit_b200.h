@@ -163,14 +163,20 @@ int tk_context_set_ttm_path(tk_context* ctx, int path);
 #define TK_ORTHO_GRAM 1
 int tk_context_set_orthonormalizer(tk_context* ctx, int kind);
 
-/* Alg. 3. y: dtype TK_F32/TK_F64, dims[order], device pointer if y_on_device else host
- * (copied in on the context stream). ranks[order], oversample >= 0, seed = SeedSpec{root, stream}.
+/* Alg. 3. y: dtype TK_F32/TK_F64, dims[order], device pointer if y_on_device else host.
+ * Host input is copied in by the call: in last-mode slabs on a copy stream, each slab
+ * multiplied by the first Y pass as it lands when that pass runs on the streaming kernel (fp32),
+ * else in one copy on the context stream. ranks[order], oversample >= 0,
+ * seed = SeedSpec{root, stream}.
  *
- * Device-path limits (the reference accepts any shape; these return TK_ERR_INVALID):
+ * Device-path limit (the reference accepts any shape; this returns TK_ERR_INVALID):
  *   r~_n = min(R_n + p, I_n) <= 64          "rank + oversample must be <= 64 on this device path"
- *   I_n <= tk_qr_max_rows(r~_n)              "orthonormal_basis: sketch too large for the cluster QR"
- *     (the sketch Z_n, I_n x r~_n fp64, lives in one <= 16-CTA cluster's shared memory:
- *      about 6.6k rows at r~ = 60, 13k at r~ = 30; every BASELINE config is inside). */
+ * Mode lengths are not limited by the QR: tk_qr_max_rows(r~) is what ONE thread-block cluster
+ * holds in shared memory (the sketch Z_n, I_n x r~_n fp64: about 6.6k rows at r~ = 60, 13k at
+ * r~ = 30; every BASELINE config is inside); a taller sketch is first reduced by a blocked TSQR
+ * (unpivoted Householder QR of balanced row blocks, their R factors stacked) and the cluster
+ * QR pivots on the stack - same pivots, rank cut and sign rule (range_finder.hpp:18-29,
+ * tucker.hpp:39-45). */
 int64_t tk_qr_max_rows(int64_t cols);
 int tk_rand_tucker_2i(tk_context* ctx, int dtype, int64_t order, const int64_t* dims, const void* y,
                       int y_on_device, const int64_t* ranks, int64_t oversample, uint64_t seed_root,

@@ -56,8 +56,11 @@ bool stream_ttm_enabled();
 bool stream_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols);
 int64_t stream_pack_bytes(int64_t rows, int cols);
 void launch_pack_stream(const double* u, int64_t ld, int64_t rows, int cols, void* out, cudaStream_t s);
+// k0 (a multiple of 16) / accumulate: one K range of a pass split over K — `in` points at the
+// range's first k, K is its length, rows [k0, k0 + K) of the packed factor are used and the
+// result is added to `out`.
 void launch_ttm_stream(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                       cudaStream_t s);
+                       cudaStream_t s, int64_t k0 = 0, bool accumulate = false);
 // fp64 arithmetic over fp32 data (ttm_mixed.cu): out (fp64) = in (fp32) x_mode U, U packed
 // k-major with stride pack_stride(cols) (launch_pack_factor<double>); M-major shapes, P % 4 == 0.
 bool mixed_ttm_supported(const float* in, int64_t P);
@@ -139,9 +142,14 @@ void launch_cast2d(const S* in, int64_t ldi, D* out, int64_t ldo, int64_t rows, 
 // top of the remaining column norms, [1] sign margin = min over columns of (max |u_i| of the
 // chosen sign - max |u_i| of the other) / max |u_i|, [2] 0 = pivoted CholeskyQR2 fast path,
 // 1 = Householder path (ill-conditioned Z or a near-tie pivot, kTieGapSq).
-void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up,
-                              int up_dtype, int* rank_dev, double* diag, cudaStream_t s, int nparts = 0,
-                              double* margins = nullptr);
+// Sketches taller than qr_max_rows(ncols) take the blocked path (TSQR reduction of balanced row
+// blocks in front of the cluster QR, same pivots / rank cut / sign rule): it needs `work`,
+// qr_work_elems(rows, ncols) doubles (0 when the cluster QR holds Z), and nparts == 0.
+// Returns the number of kernel launches.
+int launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up,
+                             int up_dtype, int* rank_dev, double* diag, cudaStream_t s, int nparts = 0,
+                             double* margins = nullptr, double* work = nullptr);
+int64_t qr_work_elems(int64_t rows, int ncols);
 // Gram-path orthonormalisation of the distributed protocol (gram.cu; range_finder.hpp:43-105,
 // dist.hpp:688-723): U = Z T with T = V / sqrt(lambda) (descending, eigenvalues <= 1e-12 top
 // dropped), no sign rule. Same outputs as launch_orthonormal_basis (u rows x ucap, ld = rows,
@@ -154,7 +162,7 @@ int launch_gram_orthonormal(const double* z, int64_t rows, int64_t ldz, int ncol
 // columns >= kept zero), spectrum (n), kept -> *rank_dev.
 void launch_gram_ortho_transform(const double* gram, int n, double* transform, double* spectrum, int* rank_dev,
                                  cudaStream_t s);
-// Largest Z (rows) the cluster QR can hold for `ncols` columns.
+// Largest Z (rows) the single-cluster QR can hold for `ncols` columns (taller: blocked path).
 int64_t qr_max_rows(int ncols);
 
 // Named device scratch owned by the caller's context (grows, never shrinks; reused across calls).

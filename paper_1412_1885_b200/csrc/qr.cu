@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -542,7 +543,7 @@ __device__ __forceinline__ void axpy_row(double* zr, int ld, int j0, int j1, dou
 __global__ void __launch_bounds__(kQrThreads, 1)
     qr_colpiv_cluster_kernel(const double* __restrict__ zin, int64_t rows, int ncols, int ld,
                              double* __restrict__ uout, int ucap, void* upout, int up_dtype, int* rank_out,
-                             double* diag_out, int fast, int rowpar, int nparts, double* margin_out) {
+                             double* diag_out, int fast, int rowpar, int nparts, double* margin_out, int plain) {
     cg::cluster_group cl = cg::this_cluster();
     const unsigned cs = cl.num_blocks();
     const int crank = static_cast<int>(cl.block_rank());
@@ -872,8 +873,16 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     }  // Householder path
     QR_MARK(3);
 
-    // ---- sign fix: largest |entry| of each column positive (first maximum on ties)
-    if (rank > 0) {
+    // ---- sign fix: largest |entry| of each column positive (first maximum on ties); `plain`
+    //      (the blocked tall path's reduced QR: the sign rule applies to its final product) skips it
+    if (plain) {
+        for (int j = tid; j < rank; j += kQrThreads) sh.sgn[j] = 1.0;
+        if (margin_out && crank == 0 && tid == 0) {
+            margin_out[0] = pmargin;
+            margin_out[2] = fast_ok ? 0.0 : 1.0;
+        }
+        __syncthreads();
+    } else if (rank > 0) {
         double* m = sh.slot + par * kVec;
         const int sub = tid % kTpc, grp = tid / kTpc;
         for (int base = 0; base + warp * (32 / kTpc) < rank; base += kQrThreads / kTpc) {
@@ -973,6 +982,240 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     if (cs > 1) cl.sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
+// ---------------------------------------------------------------------------------------
+// Blocked path for sketches taller than one cluster's shared memory (rows > qr_max_rows):
+// a TSQR reduction in front of the cluster QR. Column pivoting only looks at column norms of
+// trailing submatrices, which an orthogonal transform from the left leaves unchanged: with
+// Z = Q0 S (unpivoted Householder QR of every row block, S = the stacked n x n R factors),
+// ColPivHouseholderQR(Z) = Q0 ColPivHouseholderQR(S) — the same pivots, |R_kk| and rank cut
+// (range_finder.hpp:18-29) — and the sign rule (tucker.hpp:39-45) is applied to the product.
+//   level l:   tall_block_qr_kernel   one CTA per row block: R_b into the stack, explicit Q_b
+//   last:      qr_colpiv_cluster_kernel (plain) on the stack (repeated levels until it fits)
+//   back:      tall_apply_kernel      W_l[block b] = Q_b W_{l+1}[b n .. (b + 1) n)
+//   finish:    tall_sign_partial_kernel / tall_finish_kernel: sign rule, margins, U + packed copy
+// ---------------------------------------------------------------------------------------
+constexpr int kTallThreads = 256;
+constexpr int kTallMaxBlockRows = 320;  // 320 x 64 doubles = 160 KB of shared memory
+
+// Unpivoted Householder QR (Eigen's makeHouseholderInPlace convention, as the cluster kernel)
+// of rows [lo_b, hi_b) of zin, balanced blocks b = blockIdx.x; every block has >= n rows.
+__global__ void __launch_bounds__(kTallThreads, 1)
+    tall_block_qr_kernel(const double* __restrict__ zin, int64_t rows, int n, int nb, double* __restrict__ qout,
+                         double* __restrict__ stack) {
+    extern __shared__ __align__(16) double tsm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kWarps = kTallThreads / 32;
+    const int b = blockIdx.x;
+    const int64_t lo = rows * b / nb, hi = rows * (b + 1) / nb;
+    const int m = static_cast<int>(hi - lo);
+    const int ld = m | 1;  // odd leading dimension: column-strided accesses spread over the banks
+    double* z = tsm;                       // [n][ld]
+    double* taus = z + size_t(ld) * n;     // [n]
+    double* betas = taus + kMaxRank;       // [n]
+    for (int t = tid; t < m * n; t += kTallThreads) {
+        const int i = t % m, j = t / m;
+        z[i + size_t(j) * ld] = zin[(lo + i) + int64_t(j) * rows];
+    }
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        // scalars of H_k, redundantly per warp (same order everywhere: identical values)
+        const double* ck = z + size_t(k) * ld;
+        double ts = 0.0;
+        for (int i = k + 1 + lane; i < m; i += 32) ts = fma(ck[i], ck[i], ts);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+        const double c0 = ck[k];
+        double tau, bta, rden = 0.0;
+        if (ts <= DBL_MIN) {
+            tau = 0.0;
+            bta = c0;
+        } else {
+            bta = sqrt(c0 * c0 + ts);
+            if (c0 >= 0.0) bta = -bta;
+            rden = 1.0 / (c0 - bta);
+            tau = (bta - c0) / bta;
+        }
+        if (tau != 0.0) {
+            for (int j = k + 1 + warp; j < n; j += kWarps) {  // a warp owns its columns for the step
+                double* cj = z + size_t(j) * ld;
+                double w = 0.0;
+                for (int i = k + 1 + lane; i < m; i += 32) w = fma(ck[i], cj[i], w);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+                w = cj[k] + w * rden;
+                const double tw = tau * w;
+                for (int i = k + 1 + lane; i < m; i += 32) cj[i] = fma(-tw * rden, ck[i], cj[i]);
+                __syncwarp();
+                if (lane == 0) cj[k] -= tw;
+            }
+        }
+        __syncthreads();
+        // column k is final: essential part scaled in place by one warp (no one reads it again
+        // before the Q accumulation), R_kk = beta
+        if (warp == k % kWarps) {
+            double* wk = z + size_t(k) * ld;
+            for (int i = k + 1 + lane; i < m; i += 32) wk[i] *= rden;
+            if (lane == 0) {
+                taus[k] = tau;
+                betas[k] = bta;
+            }
+        }
+    }
+    __syncthreads();
+    // R_b (upper triangular, diagonal = beta) into rows [b n, (b + 1) n) of the stack
+    const int64_t sld = int64_t(nb) * n;
+    for (int t = tid; t < n * n; t += kTallThreads) {
+        const int i = t % n, j = t / n;
+        stack[(int64_t(b) * n + i) + j * sld] = i < j ? z[i + size_t(j) * ld] : (i == j ? betas[i] : 0.0);
+    }
+    __syncthreads();
+    // explicit Q_b = H_0 ... H_{n-1} [I; 0] in place, backward
+    for (int k = n - 1; k >= 0; --k) {
+        const double tau = taus[k];
+        double* vk = z + size_t(k) * ld;
+        for (int j = k + 1 + warp; j < n; j += kWarps) {
+            double* cj = z + size_t(j) * ld;
+            double d = 0.0;
+            for (int i = k + 1 + lane; i < m; i += 32) d = fma(vk[i], cj[i], d);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const double td = tau * d;
+            for (int i = k + 1 + lane; i < m; i += 32) cj[i] = fma(-td, vk[i], cj[i]);
+            if (lane == 0) cj[k] = -td;
+        }
+        __syncthreads();
+        for (int i = tid; i < m; i += kTallThreads) vk[i] = i < k ? 0.0 : (i == k ? 1.0 - tau : -tau * vk[i]);
+        __syncthreads();
+    }
+    for (int t = tid; t < m * n; t += kTallThreads) {
+        const int i = t % m, j = t / m;
+        qout[(lo + i) + int64_t(j) * rows] = z[i + size_t(j) * ld];
+    }
+}
+
+// wout[rows of block b, 0:n) = q[rows of block b, 0:n) win[b n .. (b + 1) n, 0:n)  (balanced
+// blocks as above; q, wout: ld = rows; win: ld = nb n). grid (nb, row tiles of 128).
+__global__ void __launch_bounds__(128)
+    tall_apply_kernel(const double* __restrict__ q, int64_t rows, int n, int nb, const double* __restrict__ win,
+                      double* __restrict__ wout) {
+    extern __shared__ __align__(16) double apsm[];
+    double* ws = apsm;           // [n][n]
+    double* qs = ws + n * n;     // [n][128]
+    const int b = blockIdx.x;
+    const int64_t lo = rows * b / nb, hi = rows * (b + 1) / nb;
+    const int64_t r0 = lo + int64_t(blockIdx.y) * 128;
+    if (r0 >= hi) return;
+    const int nr = static_cast<int>(lmin(128, hi - r0));
+    const int64_t wld = int64_t(nb) * n;
+    for (int t = threadIdx.x; t < n * n; t += 128) ws[t] = win[(int64_t(b) * n + t % n) + (t / n) * wld];
+    for (int t = threadIdx.x; t < n * 128; t += 128) {
+        const int i = t & 127, k = t >> 7;
+        qs[t] = i < nr ? q[(r0 + i) + int64_t(k) * rows] : 0.0;
+    }
+    __syncthreads();
+    const int i = threadIdx.x;
+    if (i >= nr) return;
+    for (int j = 0; j < n; ++j) {
+        const double* wj = ws + j * n;
+        double a0 = 0.0, a1 = 0.0;
+        int k = 0;
+        for (; k + 2 <= n; k += 2) {
+            a0 = fma(qs[i + k * 128], wj[k], a0);
+            a1 = fma(qs[i + (k + 1) * 128], wj[k + 1], a1);
+        }
+        if (k < n) a0 = fma(qs[i + k * 128], wj[k], a0);
+        wout[(r0 + i) + int64_t(j) * rows] = a0 + a1;
+    }
+}
+
+constexpr int kSignChunk = 2048;  // rows per CTA of the sign scans
+
+// part[(c n + j) 4 + {0, 1, 2, 3}] = over rows of chunk c of column j: first largest |w|, its
+// value, largest positive entry, largest -negative entry
+__global__ void __launch_bounds__(256)
+    tall_sign_partial_kernel(const double* __restrict__ w, int64_t rows, int n, double* __restrict__ part) {
+    const int c = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t lo = int64_t(c) * kSignChunk, hi = lmin(rows, lo + kSignChunk);
+    for (int j = warp; j < n; j += 8) {
+        const double* col = w + int64_t(j) * rows;
+        double bv = -1.0, val = 0.0, pmax = 0.0, nmax = 0.0;
+        int64_t bi = INT64_MAX;
+        for (int64_t i = lo + lane; i < hi; i += 32) {
+            const double x = col[i];
+            const bool take = fabs(x) > bv;
+            bv = take ? fabs(x) : bv;
+            bi = take ? i : bi;
+            val = take ? x : val;
+            pmax = x > 0.0 ? fmax(pmax, x) : pmax;
+            nmax = x < 0.0 ? fmax(nmax, -x) : nmax;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, bv, o);
+            const long long oi = __shfl_xor_sync(0xffffffffu, static_cast<long long>(bi), o);
+            const double ov = __shfl_xor_sync(0xffffffffu, val, o);
+            const bool take = ob > bv || (ob == bv && oi < bi);
+            bv = take ? ob : bv;
+            bi = take ? oi : bi;
+            val = take ? ov : val;
+            pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+            nmax = fmax(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+        }
+        if (lane == 0) {
+            double* o = part + (size_t(c) * n + j) * 4;
+            o[0] = bv;
+            o[1] = val;
+            o[2] = pmax;
+            o[3] = nmax;
+        }
+    }
+}
+
+// sign rule from the chunk partials (scanned in row order: strict > keeps the first maximum),
+// then this CTA's rows of U (rows x ucap, columns >= rank zero) and of the packed copy
+__global__ void __launch_bounds__(256)
+    tall_finish_kernel(const double* __restrict__ w, int64_t rows, int n, int nchunks, const double* __restrict__ part,
+                       const int* __restrict__ rank_dev, double* __restrict__ uout, int ucap, void* upout, int up_dtype,
+                       double* margin_out) {
+    __shared__ double sgn[kMaxRank], smar[kMaxRank];
+    const int rank = *rank_dev;
+    for (int j = threadIdx.x; j < n; j += 256) {
+        double bv = -1.0, val = 0.0, pm = 0.0, nm = 0.0;
+        for (int c = 0; c < nchunks; ++c) {
+            const double* o = part + (size_t(c) * n + j) * 4;
+            const bool take = o[0] > bv;
+            bv = take ? o[0] : bv;
+            val = take ? o[1] : val;
+            pm = fmax(pm, o[2]);
+            nm = fmax(nm, o[3]);
+        }
+        sgn[j] = val < 0.0 ? -1.0 : 1.0;
+        const double top = fmax(pm, nm);
+        smar[j] = top > 0.0 ? fabs(pm - nm) / top : 0.0;
+    }
+    __syncthreads();
+    if (margin_out && blockIdx.x == 0 && threadIdx.x == 0 && rank > 0) {
+        double smin = 1.0;
+        for (int j = 0; j < rank; ++j) smin = fmin(smin, smar[j]);
+        margin_out[1] = smin;
+    }
+    const int64_t lo = int64_t(blockIdx.x) * kSignChunk, hi = lmin(rows, lo + kSignChunk);
+    const int nr = static_cast<int>(hi - lo);
+    for (int j = 0; j < ucap; ++j)
+        for (int i = threadIdx.x; i < nr; i += 256)
+            uout[(lo + i) + int64_t(j) * rows] = (j < rank && j < n) ? sgn[j] * w[(lo + i) + int64_t(j) * rows] : 0.0;
+    if (upout) {
+        const int stride = (rank + 3) / 4 * 4;
+        for (int t = threadIdx.x; t < nr * stride; t += 256) {
+            const int i = t / stride, j = t - i * stride;
+            const double v = j < rank ? sgn[j] * w[(lo + i) + int64_t(j) * rows] : 0.0;
+            const int64_t o = (lo + i) * stride + j;
+            if (up_dtype == kF32) static_cast<float*>(upout)[o] = static_cast<float>(v);
+            else static_cast<double*>(upout)[o] = v;
+        }
+    }
+}
+
 int pick_cluster(int64_t rows, int ncols, int* ld_out, size_t* smem_out) {
     static const int min_cs = [] {
         const char* e = std::getenv("TENKIT_QR_MIN_CLUSTER");
@@ -1003,10 +1246,10 @@ int64_t qr_max_rows(int ncols) {
     return static_cast<int64_t>((kQrSmemCap - kQrFixedSmem) / (sizeof(double) * std::max(ncols, 1))) * 16;
 }
 
-void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up, int up_dtype,
-                              int* rank_dev, double* diag, cudaStream_t s, int nparts, double* margins) {
-    require(rows >= 1, "orthonormal_basis: empty input");
-    require(ncols >= 1 && ncols <= kMaxRank, "orthonormal_basis: column count must be in [1, 64]");
+namespace {
+
+void launch_cluster_qr(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up, int up_dtype,
+                       int* rank_dev, double* diag, cudaStream_t s, int nparts, double* margins, int plain) {
     int ld = 0;
     size_t smem = 0;
     const int cs = pick_cluster(rows, ncols, &ld, &smem);
@@ -1046,7 +1289,98 @@ void launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* 
     }();
     TK_MAXSMEM((qr_colpiv_cluster_kernel));
     TK_CUDA(cudaLaunchKernelEx(&cfg, qr_colpiv_cluster_kernel, z, rows, ncols, ld, u, ucap, up, up_dtype, rank_dev,
-                               diag, fast, rowpar, nparts, margins));
+                               diag, fast, rowpar, nparts, margins, plain));
+}
+
+// Levels of the blocked path: level l factors a rows[l] x n matrix in nb[l] balanced row blocks
+// (each >= n and <= kTallMaxBlockRows rows) into Q_l (rows[l] x n) and a stack of nb[l] n rows;
+// the last stack fits the cluster QR.
+struct TallPlan {
+    std::vector<int64_t> rows;  // rows[0] = the sketch, rows[l + 1] = nb[l] * n; back() = the cluster QR's input
+    std::vector<int> nb;
+    int64_t work_elems = 0;
+};
+
+TallPlan tall_plan(int64_t rows, int n) {
+    TallPlan p;
+    p.rows.push_back(rows);
+    const int64_t cap = qr_max_rows(n);
+    const int br = std::max(2 * n, std::min<int>(kTallMaxBlockRows, static_cast<int>((160 * 1024) / (sizeof(double) * n))));
+    while (p.rows.back() > cap) {
+        const int64_t r = p.rows.back();
+        const int64_t nb = (r + br - 1) / br;
+        require(nb < (int64_t(1) << 24), "orthonormal_basis: sketch too tall");
+        p.nb.push_back(static_cast<int>(nb));
+        p.rows.push_back(nb * n);
+    }
+    // Q_l and W_l per level, the stacks (W of the last level = the cluster QR's output), sign partials
+    for (size_t l = 0; l < p.nb.size(); ++l) p.work_elems += 2 * p.rows[l] * n + p.rows[l + 1] * n;
+    p.work_elems += p.rows.back() * n;
+    p.work_elems += ((rows + kSignChunk - 1) / kSignChunk) * n * 4;
+    return p;
+}
+
+}  // namespace
+
+int64_t qr_work_elems(int64_t rows, int ncols) {
+    if (ncols < 1 || ncols > kMaxRank || rows <= qr_max_rows(ncols)) return 0;
+    return tall_plan(rows, ncols).work_elems;
+}
+
+int launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u, int ucap, void* up, int up_dtype,
+                             int* rank_dev, double* diag, cudaStream_t s, int nparts, double* margins, double* work) {
+    require(rows >= 1, "orthonormal_basis: empty input");
+    require(ncols >= 1 && ncols <= kMaxRank, "orthonormal_basis: column count must be in [1, 64]");
+    if (rows <= qr_max_rows(ncols)) {
+        launch_cluster_qr(z, rows, ncols, u, ucap, up, up_dtype, rank_dev, diag, s, nparts, margins, 0);
+        return 1;
+    }
+    require(work != nullptr && nparts == 0, "orthonormal_basis: sketch too large for the cluster QR");
+    const int n = ncols;
+    const TallPlan p = tall_plan(rows, n);
+    const int L = static_cast<int>(p.nb.size());
+    std::vector<double*> q(L), w(L + 1), st(L + 1);
+    double* cur = work;
+    for (int l = 0; l < L; ++l) {
+        q[l] = cur, cur += p.rows[l] * n;
+        w[l] = cur, cur += p.rows[l] * n;
+        st[l + 1] = cur, cur += p.rows[l + 1] * n;
+    }
+    w[L] = cur, cur += p.rows[L] * n;
+    double* part = cur;
+    static bool attr = false;
+    if (!attr) {
+        TK_CUDA(cudaFuncSetAttribute(tall_block_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        TK_CUDA(cudaFuncSetAttribute(tall_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr = true;
+    }
+    int launches = 0;
+    const double* src = z;
+    for (int l = 0; l < L; ++l) {
+        const int64_t mb = (p.rows[l] + p.nb[l] - 1) / p.nb[l] + 1;  // largest balanced block (+1: odd ld)
+        const size_t smem = (size_t(mb | 1) * n + 2 * kMaxRank) * sizeof(double);
+        tall_block_qr_kernel<<<p.nb[l], kTallThreads, smem, s>>>(src, p.rows[l], n, p.nb[l], q[l], st[l + 1]);
+        TK_CUDA(cudaGetLastError());
+        src = st[l + 1];
+        ++launches;
+    }
+    // the reduced matrix: pivots, rank cut, |R_kk| diagnostics, pivot margin — no sign rule
+    launch_cluster_qr(st[L], p.rows[L], n, w[L], n, nullptr, kF64, rank_dev, diag, s, 0, margins, 1);
+    ++launches;
+    for (int l = L - 1; l >= 0; --l) {
+        const int64_t mb = (p.rows[l] + p.nb[l] - 1) / p.nb[l] + 1;
+        const dim3 grid(p.nb[l], static_cast<unsigned>((mb + 127) / 128));
+        const size_t smem = (size_t(n) * n + size_t(n) * 128) * sizeof(double);
+        tall_apply_kernel<<<grid, 128, smem, s>>>(q[l], p.rows[l], n, p.nb[l], w[l + 1], w[l]);
+        TK_CUDA(cudaGetLastError());
+        ++launches;
+    }
+    const int nchunks = static_cast<int>((rows + kSignChunk - 1) / kSignChunk);
+    tall_sign_partial_kernel<<<nchunks, 256, 0, s>>>(w[0], rows, n, part);
+    TK_CUDA(cudaGetLastError());
+    tall_finish_kernel<<<nchunks, 256, 0, s>>>(w[0], rows, n, nchunks, part, rank_dev, u, ucap, up, up_dtype, margins);
+    TK_CUDA(cudaGetLastError());
+    return launches + 2;
 }
 
 }  // namespace tkb

@@ -210,6 +210,28 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
     lo = __float_as_uint(y - __uint_as_float(hi));
 }
 
+// The same split for two values at a time on the packed fp32x2 pipe (Veltkamp: c = 8193 y,
+// hi = c - (c - y): y rounded to nearest-even at 11 significant bits, a tf32 value; lo = y - hi
+// exact): FFMA2 + 3 FADD2 per pair instead of 6 scalar instructions. `nzero` is -0.0 from a
+// kernel argument: with a literal addend (or mul + sub) ptxas contracts the first two steps
+// into one FFMA2 (y * 8193 - y, a single rounding), which breaks the split. Overflows for
+// |y| > FLT_MAX / 8193.
+__device__ __forceinline__ void split_hi_lo2(float y0, float y1, float nzero, uint32_t& h0, uint32_t& h1, uint32_t& l0,
+                                             uint32_t& l1) {
+    asm("{\n\t.reg .b64 y, c, d, h, l, m, zz;\n\t"
+        "mov.b64 y, {%4, %5};\n\t"
+        "mov.b64 m, {%6, %6};\n\t"
+        "mov.b64 zz, {%7, %7};\n\t"
+        "fma.rn.f32x2 c, y, m, zz;\n\t"
+        "sub.rn.f32x2 d, c, y;\n\t"
+        "sub.rn.f32x2 h, c, d;\n\t"
+        "sub.rn.f32x2 l, y, h;\n\t"
+        "mov.b64 {%0, %1}, h;\n\t"
+        "mov.b64 {%2, %3}, l;\n\t}\n"
+        : "=r"(h0), "=r"(h1), "=r"(l0), "=r"(l1)
+        : "f"(y0), "f"(y1), "f"(8193.f), "f"(nzero));
+}
+
 // KM = false: Y viewed as (P, K, Q), tiles of BM consecutive p of one q; out[p + r P + q P cols].
 //             Row MT L + j of the tile is TMEM lane L of M tile j (a thread reads MT adjacent p).
 // KM = true:  Y viewed as Q rows of K contiguous values (contraction over mode 0), tiles of BM
@@ -217,10 +239,10 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
 //             128 j + L of the tile is TMEM lane L of M tile j.
 // Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
 // the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
-template <int NH, bool KM, int MT, int OCC, int kChunk = 16>
+template <int NH, bool KM, int MT, int OCC, int kChunk = 16, bool V2 = false>
 __global__ void __launch_bounds__(kSThreads, OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
-                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles) {
+                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles, int accum, float nzero) {
     using C = SCfg<NH, KM, MT, OCC>;
     constexpr int BM = C::BM, NA = C::NA, ST = C::STAGES, ND = C::ND;
     // dynamic shared memory starts at offset 0 of the CTA's window (no static shared memory in
@@ -345,7 +367,7 @@ __global__ void __launch_bounds__(kSThreads, OCC)
 #pragma unroll
             for (int e = 0; e < ACC; ++e) acc[j][e] = 0.f;
         int s = 0, a = 0;
-        uint32_t ph = 0, aph = 0, ch = 0;
+        uint32_t aph = 0, ch = 0;
         // flush of chunk `pend` (buffer pend & 1) deferred by kDefer stages (past the converters'
         // lead over the MMA issuer), so the wait for its last MMAs does not stall the pipeline
         bool pending = false;
@@ -395,6 +417,13 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                     float* o = obase + row + int64_t(c0) * ostride;
                     int64_t os = ostride;
                     asm volatile("" : "+l"(o), "+l"(os));
+                    if (accum) {  // a K range of a split pass: add to the earlier ranges' sums
+                        float prev[ACC];
+#pragma unroll
+                        for (int e = 0; e < ACC; ++e) prev[e] = (c0 + e < cols) ? o[e * os] : 0.f;
+#pragma unroll
+                        for (int e = 0; e < ACC; ++e) acc[j][e] += prev[e];
+                    }
 #pragma unroll
                     for (int e = 0; e < ACC; ++e)
                         if (c0 + e < cols) o[e * os] = acc[j][e];
@@ -404,55 +433,65 @@ __global__ void __launch_bounds__(kSThreads, OCC)
             }
             store_after = false;
         };
+        // raw Y values of one stage: this thread's MT rows x 8 k (its k half)
+        float raw[MT][8];
+        const auto load_stage = [&](int st) {
+            const uint32_t stage = smem_u32(sY + size_t(st) * C::STAGE_Y);
+            if constexpr (KM) {
+                // row: 64 B with 16-B chunks at chunk ^ ((row >> 1) & 3) (64B swizzle)
+#pragma unroll
+                for (int j = 0; j < MT; ++j) {
+                    const int row = 128 * j + L;
+                    const uint32_t rb = stage + row * 64;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int phys = (2 * khalf + h) ^ ((row >> 1) & 3);
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                     : "=f"(raw[j][h * 4 + 0]), "=f"(raw[j][h * 4 + 1]), "=f"(raw[j][h * 4 + 2]),
+                                       "=f"(raw[j][h * 4 + 3])
+                                     : "r"(rb + phys * 16));
+                    }
+                }
+            } else {
+                // one box of 16 k-rows x BM p (4 BM bytes each, unswizzled): per k a warp
+                // reads 32 MT consecutive p (conflict-free)
+                const uint32_t bb = stage + khalf * 8 * (BM * 4) + L * (MT * 4);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    if constexpr (MT == 2) {
+                        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n"
+                                     : "=f"(raw[0][kk]), "=f"(raw[1][kk])
+                                     : "r"(bb + kk * (BM * 4)));
+                    } else {
+                        asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(raw[0][kk]) : "r"(bb + kk * (BM * 4)));
+                    }
+                }
+            }
+        };
+        int sl = 0;            // stage ring position of the next load
+        uint32_t phl = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int64_t q = t / tiles_p;
             const int64_t p0 = (t % tiles_p) * BM;
             for (int kc = 0; kc < nk; ++kc) {
-                mbar_wait(&full[s], ph);
+                mbar_wait(&full[sl], phl);
+                load_stage(sl);
+                if (++sl == ST) sl = 0, phl ^= 1;
                 uint32_t hi[MT][8], lo[MT][8];
-                const uint32_t stage = smem_u32(sY + size_t(s) * C::STAGE_Y);
-                if constexpr (KM) {
-                    // row: 64 B with 16-B chunks at chunk ^ ((row >> 1) & 3) (64B swizzle)
 #pragma unroll
-                    for (int j = 0; j < MT; ++j) {
-                        const int row = 128 * j + L;
-                        const uint32_t rb = stage + row * 64;
+                for (int j = 0; j < MT; ++j)
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int phys = (2 * khalf + h) ^ ((row >> 1) & 3);
-                            float4 v;
-                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
-                                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                                         : "r"(rb + phys * 16));
-                            split_hi_lo(v.x, hi[j][h * 4 + 0], lo[j][h * 4 + 0]);
-                            split_hi_lo(v.y, hi[j][h * 4 + 1], lo[j][h * 4 + 1]);
-                            split_hi_lo(v.z, hi[j][h * 4 + 2], lo[j][h * 4 + 2]);
-                            split_hi_lo(v.w, hi[j][h * 4 + 3], lo[j][h * 4 + 3]);
-                        }
-                    }
-                } else {
-                    // one box of 16 k-rows x BM p (4 BM bytes each, unswizzled): per k a warp
-                    // reads 32 MT consecutive p (conflict-free)
-                    const uint32_t bb = stage + khalf * 8 * (BM * 4) + L * (MT * 4);
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        if constexpr (MT == 2) {
-                            float y0, y1;
-                            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n"
-                                         : "=f"(y0), "=f"(y1)
-                                         : "r"(bb + kk * (BM * 4)));
-                            split_hi_lo(y0, hi[0][kk], lo[0][kk]);
-                            split_hi_lo(y1, hi[1][kk], lo[1][kk]);
+                    for (int e = 0; e < 8; e += 2) {
+                        if constexpr (V2) {
+                            split_hi_lo2(raw[j][e], raw[j][e + 1], nzero, hi[j][e], hi[j][e + 1], lo[j][e], lo[j][e + 1]);
                         } else {
-                            float y;
-                            asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(y) : "r"(bb + kk * (BM * 4)));
-                            split_hi_lo(y, hi[0][kk], lo[0][kk]);
+                            split_hi_lo(raw[j][e], hi[j][e], lo[j][e]);
+                            split_hi_lo(raw[j][e + 1], hi[j][e + 1], lo[j][e + 1]);
                         }
                     }
-                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // this warp's reads of the Y stage are done
-                if (++s == ST) s = 0, ph ^= 1;
+                if (++s == ST) s = 0;
                 mbar_wait(&aempty[a], aph ^ 1);
                 sfence_after();
                 const uint32_t abuf = tmem + lane_off + uint32_t(C::A_BASE + a * MT * 32 + khalf * 8);
@@ -531,13 +570,13 @@ __global__ void pack_stream_kernel(const double* __restrict__ u, int64_t ld, int
     }
 }
 
-template <int NH, bool KM, int MT, int OCC, int CH>
+template <int NH, bool KM, int MT, int OCC, int CH, bool V2>
 void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool accum) {
     using C = SCfg<NH, KM, MT, OCC>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, OCC, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, OCC, CH, V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
@@ -570,9 +609,10 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
-    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, OCC, CH>));
-    ttm_stream_kernel<NH, KM, MT, OCC, CH><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
-                                                                                             cols, tiles_p, ntiles);
+    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, OCC, CH, V2>));
+    ttm_stream_kernel<NH, KM, MT, OCC, CH, V2><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
+                                                                                             cols, tiles_p, ntiles,
+                                                                                             accum ? 1 : 0, -0.0f);
     TK_LAUNCH_CHECK();
 }
 
@@ -580,29 +620,29 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
 // converters, the factor k-block and the MMA issue are shared by both tiles (measured: 0.79 of
 // the HBM peak at cfg3 against 0.71 with one tile per CTA and two CTAs per SM; NH = 64, whose
 // two tiles leave TMEM room for one accumulator buffer only: 0.76 against 0.63). A/B knobs:
-// TENKIT_STREAM_MT=1 (one tile per CTA, two CTAs per SM), TENKIT_STREAM_CHUNK=0 (one
-// accumulation chunk per tile).
+// TENKIT_STREAM_MT=1 (one tile per CTA, two CTAs per SM), TENKIT_STREAM_V2=1 (hi/lo split of
+// two values at a time on the packed fp32x2 pipe, split_hi_lo2).
 template <int NH, bool KM, int MT, int OCC>
 void launch_stream_mt(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                      cudaStream_t s) {
-    static const bool whole = [] {
-        const char* e = std::getenv("TENKIT_STREAM_CHUNK");
-        return e && e[0] == '0';
+                      cudaStream_t s, bool accum) {
+    static const bool v2 = [] {
+        const char* e = std::getenv("TENKIT_STREAM_V2");
+        return e && e[0] == '1';
     }();
-    if (whole) launch_stream_ch<NH, KM, MT, OCC, (1 << 20)>(in, bpk, out, P, K, Q, cols, s);
-    else launch_stream_ch<NH, KM, MT, OCC, kChunkDefault>(in, bpk, out, P, K, Q, cols, s);
+    if (v2) launch_stream_ch<NH, KM, MT, OCC, kChunkDefault, true>(in, bpk, out, P, K, Q, cols, s, accum);
+    else launch_stream_ch<NH, KM, MT, OCC, kChunkDefault, false>(in, bpk, out, P, K, Q, cols, s, accum);
 }
 
 template <int NH, bool KM>
 void launch_stream(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                   cudaStream_t s) {
+                   cudaStream_t s, bool accum) {
     static const int mt = [] {
         const char* e = std::getenv("TENKIT_STREAM_MT");
         return e ? std::atoi(e) : 0;
     }();
     const int m = mt == 1 ? 1 : 2;
-    if (m == 2) launch_stream_mt<NH, KM, 2, 1>(in, bpk, out, P, K, Q, cols, s);
-    else launch_stream_mt<NH, KM, 1, 2>(in, bpk, out, P, K, Q, cols, s);
+    if (m == 2) launch_stream_mt<NH, KM, 2, 1>(in, bpk, out, P, K, Q, cols, s, accum);
+    else launch_stream_mt<NH, KM, 1, 2>(in, bpk, out, P, K, Q, cols, s, accum);
 }
 
 // NH = cols rounded up to 8 (A/B knob TENKIT_STREAM_NH16=1: to 16, the first design's padding)
@@ -647,15 +687,20 @@ void launch_pack_stream(const double* u, int64_t ld, int64_t rows, int cols, voi
     TK_LAUNCH_CHECK();
 }
 
+int64_t stream_pack_kblock_bytes(int cols) { return 128 * int64_t(stream_nh(cols)); }
+
 // P == 1: contraction over mode 0, transposed output out[q + r Q]; else out[p + r P + q P cols].
+// k0 (a multiple of 16) / accumulate: the pass covers rows [k0, k0 + K) of the packed factor and
+// adds to `out` (one K range of a pass split over K; `in` points at the range's first k).
 void launch_ttm_stream(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
-                       cudaStream_t s) {
-    const uint8_t* b = static_cast<const uint8_t*>(bpk);
+                       cudaStream_t s, int64_t k0, bool accum) {
+    require(k0 % kSBK == 0, "ttm: split ranges start at multiples of 16");
     const int nh = stream_nh(cols);
+    const uint8_t* b = static_cast<const uint8_t*>(bpk) + (k0 / kSBK) * stream_pack_kblock_bytes(cols);
 #define TK_STREAM_CASE(N)                                                   \
     case N:                                                                 \
-        if (P == 1) launch_stream<N, true>(in, b, out, P, K, Q, cols, s);   \
-        else launch_stream<N, false>(in, b, out, P, K, Q, cols, s);         \
+        if (P == 1) launch_stream<N, true>(in, b, out, P, K, Q, cols, s, accum);   \
+        else launch_stream<N, false>(in, b, out, P, K, Q, cols, s, accum);         \
         break;
     switch (nh) {
         TK_STREAM_CASE(16)

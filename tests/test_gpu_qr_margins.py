@@ -96,8 +96,9 @@ def test_decomposition_reports_step_margins(P, O):
 
 
 def test_device_path_limits_fail_loudly(P, O):
-    """The documented device limits (include/tenkit_b200.h): r~ <= 64 and I_n <= tk_qr_max_rows(r~)
-    raise the reference-style invalid_argument (TenkitError) instead of computing garbage."""
+    """The documented device limit (include/tenkit_b200.h): r~ <= 64 raises the reference-style
+    invalid_argument (TenkitError) instead of computing garbage. tk_qr_max_rows is the
+    single-cluster capacity; taller sketches take the blocked path (tests below)."""
     import torch
     lib = P.Context.default().lib
     cap = int(lib.tk_qr_max_rows(60))
@@ -105,7 +106,48 @@ def test_device_path_limits_fail_loudly(P, O):
     y = torch.zeros(80 * 4 * 4, dtype=torch.float32, device="cuda")
     with pytest.raises(P.TenkitError, match="rank \\+ oversample must be <= 64"):
         P.rand_tucker_2i(P.DenseTensor((80, 4, 4), y), (60, 2, 2), 10, (0, 0))
-    rows = cap + 8
-    y = torch.randn(rows * 8 * 8, dtype=torch.float32, device="cuda")
-    with pytest.raises(P.TenkitError, match="sketch too large for the cluster QR"):
-        P.rand_tucker_2i(P.DenseTensor((rows, 8, 8), y), (50, 4, 4), 10, (0, 0))
+
+
+@pytest.mark.parametrize("rows,cols", [(7000, 60), (20000, 60), (30000, 30), (60000, 64), (60000, 7)])
+def test_tall_sketch_blocked_qr_matches_oracle(P, O, rows, cols):
+    """Sketches taller than one cluster's shared memory (rows > tk_qr_max_rows): TSQR reduction
+    of balanced row blocks, then the cluster ColPiv QR on the stacked R factors
+    (range_finder.hpp:18-29 is invariant under the orthogonal reduction), sign rule on the
+    product (tucker.hpp:39-45). Same pivots, |R_kk|, U and margins as the oracle."""
+    lib = P.Context.default().lib
+    assert rows > int(lib.tk_qr_max_rows(cols))
+    z = O.gaussian_matrix(rows, cols, (rows, cols))
+    if cols > 2:
+        z[:, 1] = 3.0 * z[:, 0] + 1e-3 * z[:, 1]
+    u_ref, d = O.orthonormal_basis(z, diagnostics=True)
+    u_ref = O.fix_column_signs(u_ref)
+    u, diag, mg = P.orthonormal_basis(z, with_diag=True, with_margins=True)
+    assert u.shape == u_ref.shape
+    assert np.allclose(np.abs(diag), np.abs(d["rdiag"]), rtol=1e-10, atol=1e-12)  # same pivots, same R_kk
+    assert np.max(np.abs(u - u_ref)) < 1e-10
+    assert np.linalg.norm(u.T @ u - np.eye(u.shape[1])) < 1e-12
+    assert 0.0 < mg["pivot_margin"] <= 1.0 and 0.0 < mg["sign_margin"] <= 1.0
+
+
+def test_tall_sketch_rank_deficient(P, O):
+    """Blocked path with a rank-deficient sketch: the reduced matrix takes the Householder path
+    and the rank cut drops the same columns as the oracle."""
+    rows, cols, r = 9000, 48, 11
+    z = O.gaussian_matrix(rows, r, (5, 0)) @ O.gaussian_matrix(r, cols, (5, 1))
+    u_ref = O.fix_column_signs(O.orthonormal_basis(z))
+    u, mg = P.orthonormal_basis(z, with_margins=True)
+    assert u.shape == u_ref.shape == (rows, r) and mg["qr_path"] == 1
+    assert np.linalg.norm(u @ u.T @ u_ref - u_ref) < 1e-9  # same subspace
+    assert np.linalg.norm(u.T @ u - np.eye(r)) < 1e-12
+
+
+def test_long_mode_decomposition_matches_oracle(P, O):
+    """rand_tucker_2i with a mode longer than the cluster QR holds (20000 x 24 x 20, r~ = 60 in
+    mode 0): fp64 factors / core / fit equal the oracle's (the reference accepts any shape)."""
+    from test_gpu_parity import compare_models
+    dims, ranks, p = (20000, 24, 20), (50, 6, 6), 10
+    y = O.gen_tucker(dims, (8, 5, 5), (2, 0))
+    y = O.add_noise(y, 25.0, (2, 1))
+    ref = O.rand_tucker_2i(y, ranks, p, (7, 0))
+    got = P.rand_tucker_2i(P.DenseTensor.from_numpy(y), ranks, p, (7, 0))
+    compare_models(O, y, got, ref, 1e-8)

@@ -94,3 +94,38 @@ def test_fp64_mode_on_fp32_data_matches_oracle_at_fp64_bar(P, O, dims, ranks, p)
         assert u.shape == v.shape and np.abs(u - v).max() < 1e-8
     assert rel(m.core, g_ref) < 1e-8
     assert m.stats["y_bytes"] == 4 * int(np.prod(dims))
+
+
+def test_host_input_lands_in_slabs_under_the_first_pass(P, O):
+    """Host input (the e2e path, bench.hpp:456-520 times the copy-in): the tensor is copied in
+    last-mode slabs on a copy stream and the first Y pass (leader = last mode) multiplies each
+    slab as it lands, partial sums added in slab order. Same model as the device-input call up to
+    fp32 rounding of the slab sums, and the oracle's within the fp32 bar."""
+    import torch
+    seed = (8, 3)
+    dims = (416, 400, 208)
+    ranks, p = (12, 12, 12), 8
+    y = O.add_noise(O.gen_tucker(dims, (10, 10, 10), seed), 20.0, O.seed_derived(*seed, 0xAD0))
+    y32 = y.astype(np.float32)
+    import os
+    O.set_threads(os.cpu_count() or 1)
+    g_ref, u_ref = O.rand_tucker_2i(y32.astype(np.float64), ranks, p, (7, 4))
+    O.set_threads(1)
+    host = P.DenseTensor.from_numpy(y32, np.float32)
+    m_host = P.rand_tucker_2i(host, ranks, p, (7, 4), sync_ranks=False, out="host")
+    m_dev = P.rand_tucker_2i(host.cuda(), ranks, p, (7, 4), sync_ranks=False).to_host()
+    assert m_host.stats["passes"] == 3 and m_dev.stats["passes"] == 3
+    # 208 / 8 slabs -> 32-k ranges: 7 launches of the first pass instead of 1
+    assert m_host.stats["kernel_launches"] == m_dev.stats["kernel_launches"] + 6
+    for uh, ud, v in zip(m_host.factors, m_dev.factors, u_ref):
+        assert uh.shape == ud.shape == v.shape
+        assert subspace_dist(uh, ud) < 2e-4
+        assert subspace_dist(uh, v) < 1e-3
+        assert orthonormality_defect(uh) < 1e-10
+    aligned = O.ttm_all(m_host.core, [u.T @ v for u, v in zip(m_host.factors, u_ref)], -1, False)
+    assert rel(aligned, g_ref) < 1e-3
+    # twice in a row (the landing buffer is reused while the copy stream refills it)
+    m2 = P.rand_tucker_2i(host, ranks, p, (7, 4), sync_ranks=False, out="host")
+    for a, b in zip(m_host.factors, m2.factors):
+        assert np.array_equal(a, b)
+    assert np.array_equal(m_host.core, m2.core)

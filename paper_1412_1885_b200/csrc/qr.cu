@@ -645,7 +645,8 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             } else {
                 if (warp == 0) warp_tri_inv(r1, rinv1, n, r2);
                 __syncthreads();
-                apply_upper(z, q, ld, nloc, n, r2, perm);
+                if (rowpar == 2) apply_dmma(z, q, ld, nloc, n, r2, perm);  // n > 32: FP64 tensor cores as well
+                else apply_upper(z, q, ld, nloc, n, r2, perm);
             }
             __syncthreads();
             QR_MARK(602);
@@ -1301,10 +1302,21 @@ struct TallPlan {
     int64_t work_elems = 0;
 };
 
+// Largest sketch the cluster QR takes directly. Above the shared-memory capacity the blocked
+// path is the only one; A/B knob TENKIT_QR_TALL_ABOVE=rows sends shorter sketches there too.
+int64_t cluster_rows_limit(int n) {
+    static const int64_t knob = [] {
+        const char* e = std::getenv("TENKIT_QR_TALL_ABOVE");
+        return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(0);  // 0: off
+    }();
+    const int64_t cap = qr_max_rows(n);
+    return knob > 0 ? std::min(cap, std::max<int64_t>(knob, 4 * n)) : cap;
+}
+
 TallPlan tall_plan(int64_t rows, int n) {
     TallPlan p;
     p.rows.push_back(rows);
-    const int64_t cap = qr_max_rows(n);
+    const int64_t cap = cluster_rows_limit(n);
     const int br = std::max(2 * n, std::min<int>(kTallMaxBlockRows, static_cast<int>((160 * 1024) / (sizeof(double) * n))));
     while (p.rows.back() > cap) {
         const int64_t r = p.rows.back();
@@ -1323,7 +1335,7 @@ TallPlan tall_plan(int64_t rows, int n) {
 }  // namespace
 
 int64_t qr_work_elems(int64_t rows, int ncols) {
-    if (ncols < 1 || ncols > kMaxRank || rows <= qr_max_rows(ncols)) return 0;
+    if (ncols < 1 || ncols > kMaxRank || rows <= cluster_rows_limit(ncols)) return 0;
     return tall_plan(rows, ncols).work_elems;
 }
 
@@ -1331,7 +1343,7 @@ int launch_orthonormal_basis(const double* z, int64_t rows, int ncols, double* u
                              int* rank_dev, double* diag, cudaStream_t s, int nparts, double* margins, double* work) {
     require(rows >= 1, "orthonormal_basis: empty input");
     require(ncols >= 1 && ncols <= kMaxRank, "orthonormal_basis: column count must be in [1, 64]");
-    if (rows <= qr_max_rows(ncols)) {
+    if (rows <= cluster_rows_limit(ncols)) {
         launch_cluster_qr(z, rows, ncols, u, ucap, up, up_dtype, rank_dev, diag, s, nparts, margins, 0);
         return 1;
     }

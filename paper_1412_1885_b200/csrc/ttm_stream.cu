@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -100,6 +101,35 @@ __device__ __forceinline__ void st8(uint32_t taddr, const uint32_t (&v)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
                  "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                  : "memory");
+}
+
+// [hi | lo] of one M tile's k half: columns [0, 8) and [16, 24) of the A buffer, one address register
+__device__ __forceinline__ void st8_pair(uint32_t taddr, const uint32_t (&h)[8], const uint32_t (&l)[8]) {
+    asm volatile(
+        "{\n\t.reg .b32 t1;\n\t"
+        "add.u32 t1, %0, 16;\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [t1], {%9, %10, %11, %12, %13, %14, %15, %16};\n\t}\n" ::"r"(taddr),
+        "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(l[0]), "r"(l[1]),
+        "r"(l[2]), "r"(l[3]), "r"(l[4]), "r"(l[5]), "r"(l[6]), "r"(l[7])
+        : "memory");
+}
+__device__ __forceinline__ void st8_quad(uint32_t taddr, const uint32_t (&h0)[8], const uint32_t (&l0)[8],
+                                         const uint32_t (&h1)[8], const uint32_t (&l1)[8]) {
+    asm volatile(
+        "{\n\t.reg .b32 t1, t2, t3;\n\t"
+        "add.u32 t1, %0, 16;\n\t"
+        "add.u32 t2, %0, 32;\n\t"
+        "add.u32 t3, %0, 48;\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [t1], {%9, %10, %11, %12, %13, %14, %15, %16};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [t2], {%17, %18, %19, %20, %21, %22, %23, %24};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [t3], {%25, %26, %27, %28, %29, %30, %31, %32};\n\t}\n" ::"r"(taddr),
+        "r"(h0[0]), "r"(h0[1]), "r"(h0[2]), "r"(h0[3]), "r"(h0[4]), "r"(h0[5]), "r"(h0[6]), "r"(h0[7]), "r"(l0[0]),
+        "r"(l0[1]), "r"(l0[2]), "r"(l0[3]), "r"(l0[4]), "r"(l0[5]), "r"(l0[6]), "r"(l0[7]), "r"(h1[0]), "r"(h1[1]),
+        "r"(h1[2]), "r"(h1[3]), "r"(h1[4]), "r"(h1[5]), "r"(h1[6]), "r"(h1[7]), "r"(l1[0]), "r"(l1[1]), "r"(l1[2]),
+        "r"(l1[3]), "r"(l1[4]), "r"(l1[5]), "r"(l1[6]), "r"(l1[7])
+        : "memory");
 }
 
 __device__ __forceinline__ void ld8(uint32_t taddr, float* v) {
@@ -203,33 +233,28 @@ __device__ __forceinline__ void produce2(uint32_t bar, uint32_t bytes, uint32_t 
         : "memory");
 }
 
+// mbarrier operations on 32-bit shared-window addresses kept in registers (the generic-pointer
+// helpers recompute the window base from SR_CgaCtaId at every use inside the stage loop)
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+
 // y_hi = y rounded to nearest tf32, y_lo = y - y_hi (exact in fp32; the tensor core reads its
 // top 19 bits)
 __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo) {
     hi = (__float_as_uint(y) + 0x1000u) & 0xFFFFE000u;
     lo = __float_as_uint(y - __uint_as_float(hi));
-}
-
-// The same split for two values at a time on the packed fp32x2 pipe (Veltkamp: c = 8193 y,
-// hi = c - (c - y): y rounded to nearest-even at 11 significant bits, a tf32 value; lo = y - hi
-// exact): FFMA2 + 3 FADD2 per pair instead of 6 scalar instructions. `nzero` is -0.0 from a
-// kernel argument: with a literal addend (or mul + sub) ptxas contracts the first two steps
-// into one FFMA2 (y * 8193 - y, a single rounding), which breaks the split. Overflows for
-// |y| > FLT_MAX / 8193.
-__device__ __forceinline__ void split_hi_lo2(float y0, float y1, float nzero, uint32_t& h0, uint32_t& h1, uint32_t& l0,
-                                             uint32_t& l1) {
-    asm("{\n\t.reg .b64 y, c, d, h, l, m, zz;\n\t"
-        "mov.b64 y, {%4, %5};\n\t"
-        "mov.b64 m, {%6, %6};\n\t"
-        "mov.b64 zz, {%7, %7};\n\t"
-        "fma.rn.f32x2 c, y, m, zz;\n\t"
-        "sub.rn.f32x2 d, c, y;\n\t"
-        "sub.rn.f32x2 h, c, d;\n\t"
-        "sub.rn.f32x2 l, y, h;\n\t"
-        "mov.b64 {%0, %1}, h;\n\t"
-        "mov.b64 {%2, %3}, l;\n\t}\n"
-        : "=r"(h0), "=r"(h1), "=r"(l0), "=r"(l1)
-        : "f"(y0), "f"(y1), "f"(8193.f), "f"(nzero));
 }
 
 // KM = false: Y viewed as (P, K, Q), tiles of BM consecutive p of one q; out[p + r P + q P cols].
@@ -239,10 +264,10 @@ __device__ __forceinline__ void split_hi_lo2(float y0, float y1, float nzero, ui
 //             128 j + L of the tile is TMEM lane L of M tile j.
 // Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
 // the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
-template <int NH, bool KM, int MT, int OCC, int kChunk = 16, bool V2 = false>
+template <int NH, bool KM, int MT, int OCC, int kChunk = 16>
 __global__ void __launch_bounds__(kSThreads, OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
-                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles, int accum, float nzero) {
+                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles, int accum, int bq, int64_t Q) {
     using C = SCfg<NH, KM, MT, OCC>;
     constexpr int BM = C::BM, NA = C::NA, ST = C::STAGES, ND = C::ND;
     // dynamic shared memory starts at offset 0 of the CTA's window (no static shared memory in
@@ -293,12 +318,13 @@ __global__ void __launch_bounds__(kSThreads, OCC)
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(&ymap) : "memory");
         int s = 0;
         uint32_t ph = 0;
-        const uint32_t y0 = smem_u32(sY), b0 = smem_u32(sB), f0 = smem_u32(full);
+        uint32_t y0 = smem_u32(sY), b0 = smem_u32(sB), f0 = smem_u32(full), e0 = smem_u32(empty);
+        asm volatile("" : "+r"(y0), "+r"(b0), "+r"(f0), "+r"(e0));
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const int64_t q = t / tiles_p;
-            const int64_t p0 = (t % tiles_p) * BM;
+            const int64_t q = (t / tiles_p) * bq;
+            const int64_t p0 = (t % tiles_p) * (BM / bq);
             for (int kc = 0; kc < nk; ++kc) {
-                mbar_wait(&empty[s], ph ^ 1);
+                bar_wait(e0 + s * 8, ph ^ 1);
                 __syncwarp();
                 const uint32_t bar = f0 + s * 8, dy = y0 + s * C::STAGE_Y, db = b0 + s * C::STAGE_B;
                 const uint8_t* src = bpk + size_t(kc) * C::STAGE_B;
@@ -318,19 +344,21 @@ __global__ void __launch_bounds__(kSThreads, OCC)
             const uint32_t id_main = sidesc(2 * NH, false), id_cross = sidesc(C::CN, false);
             int s = 0, a = 0;
             uint32_t ph = 0, aph = 0, ch = 0;
+            uint32_t sb0 = smem_u32(sB), full0 = smem_u32(full), afull0 = smem_u32(afull), dempty0 = smem_u32(dempty);
+            asm volatile("" : "+r"(sb0), "+r"(full0), "+r"(afull0), "+r"(dempty0));
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 for (int k0 = 0; k0 < nk; k0 += kChunk, ++ch) {
                     const int b = ND == 2 ? (ch & 1) : 0;
                     if (ch >= ND) {  // this buffer's previous chunk has been added into the registers
-                        mbar_wait(&dempty[b], (ND == 2 ? (ch >> 1) - 1 : ch - 1) & 1);
+                        bar_wait(dempty0 + b * 8, (ND == 2 ? (ch >> 1) - 1 : ch - 1) & 1);
                         __syncwarp();
                         sfence_after();
                     }
                     const int k1 = min(nk, k0 + kChunk);
                     for (int kc = k0; kc < k1; ++kc) {
-                        mbar_wait(&full[s], ph);
-                        const uint32_t bs = smem_u32(sB + size_t(s) * C::STAGE_B);
-                        mbar_wait(&afull[a], aph);
+                        bar_wait(full0 + s * 8, ph);
+                        const uint32_t bs = sb0 + s * C::STAGE_B;
+                        bar_wait(afull0 + a * 8, aph);
                         __syncwarp();
                         sfence_after();
                         const uint32_t abuf = tm + uint32_t(C::A_BASE + a * MT * 32);
@@ -361,13 +389,16 @@ __global__ void __launch_bounds__(kSThreads, OCC)
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         constexpr int ACC = C::ACC;
         const int c0 = khalf * (NH / 2);  // this warp's accumulator columns
+        uint32_t sy0 = smem_u32(sY), full0 = smem_u32(full), empty0 = smem_u32(empty), afull0 = smem_u32(afull),
+                 aempty0 = smem_u32(aempty), dfull0 = smem_u32(dfull), dempty0 = smem_u32(dempty);
+        asm volatile("" : "+r"(sy0), "+r"(full0), "+r"(empty0), "+r"(afull0), "+r"(aempty0), "+r"(dfull0), "+r"(dempty0));
         float acc[MT][ACC];
 #pragma unroll
         for (int j = 0; j < MT; ++j)
 #pragma unroll
             for (int e = 0; e < ACC; ++e) acc[j][e] = 0.f;
         int s = 0, a = 0;
-        uint32_t aph = 0, ch = 0;
+        uint32_t ph = 0, aph = 0, ch = 0;
         // flush of chunk `pend` (buffer pend & 1) deferred by kDefer stages (past the converters'
         // lead over the MMA issuer), so the wait for its last MMAs does not stall the pipeline
         bool pending = false;
@@ -377,7 +408,7 @@ __global__ void __launch_bounds__(kSThreads, OCC)
         uint32_t pend = 0;
         auto flush = [&](uint32_t c) {
             const int b = ND == 2 ? (c & 1) : 0;
-            mbar_wait(&dfull[b], (ND == 2 ? (c >> 1) : c) & 1);
+            bar_wait(dfull0 + b * 8, (ND == 2 ? (c >> 1) : c) & 1);
             sfence_after();
 #pragma unroll
             for (int j = 0; j < MT; ++j) {
@@ -400,21 +431,25 @@ __global__ void __launch_bounds__(kSThreads, OCC)
             }
             sfence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&dempty[b]);
+            if (lane == 0) bar_arrive(dempty0 + b * 8);
         };
         const auto row_of = [&](int j) { return KM ? 128 * j + L : MT * L + j; };
+        // M-major tiles of two q (bq = 2, MT = 2): rows [0, 128) of the tile are 128 p of q, rows
+        // [128, 256) the same p of q + 1 (a thread's two adjacent rows share their q)
+        const int BP = BM / bq;                       // p extent of a tile
+        const int qo = (!KM && bq == 2 && L >= 64) ? 1 : 0;
         float* obase = nullptr;  // output tile of the pending last chunk
-        int orows = 0;
+        int orows = 0, oq = 1;
         int64_t ostride = 0;
         bool store_after = false;
         const auto store = [&]() {
 #pragma unroll
             for (int j = 0; j < MT; ++j) {
-                const int row = row_of(j);
-                if (row < orows) {
+                const int row = row_of(j) - qo * BP;
+                if (row < orows && qo < oq) {
                     // the address arithmetic stays here: without the barrier the compiler hoists
                     // the ACC store addresses into the k loop (recomputed every stage)
-                    float* o = obase + row + int64_t(c0) * ostride;
+                    float* o = obase + row + int64_t(c0) * ostride + (qo ? ostride * cols : 0);
                     int64_t os = ostride;
                     asm volatile("" : "+l"(o), "+l"(os));
                     if (accum) {  // a K range of a split pass: add to the earlier ranges' sums
@@ -436,7 +471,7 @@ __global__ void __launch_bounds__(kSThreads, OCC)
         // raw Y values of one stage: this thread's MT rows x 8 k (its k half)
         float raw[MT][8];
         const auto load_stage = [&](int st) {
-            const uint32_t stage = smem_u32(sY + size_t(st) * C::STAGE_Y);
+            const uint32_t stage = sy0 + st * C::STAGE_Y;
             if constexpr (KM) {
                 // row: 64 B with 16-B chunks at chunk ^ ((row >> 1) & 3) (64B swizzle)
 #pragma unroll
@@ -455,55 +490,51 @@ __global__ void __launch_bounds__(kSThreads, OCC)
             } else {
                 // one box of 16 k-rows x BM p (4 BM bytes each, unswizzled): per k a warp
                 // reads 32 MT consecutive p (conflict-free)
-                const uint32_t bb = stage + khalf * 8 * (BM * 4) + L * (MT * 4);
+                // (two-q tiles: the box is [q][k][p] with BP p per row; the row stride stays a
+                // compile-time immediate of the loads on either branch)
+                const auto ld_rows = [&](auto bp_c, uint32_t bb) {
+                    constexpr int kBP = decltype(bp_c)::value;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    if constexpr (MT == 2) {
-                        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n"
-                                     : "=f"(raw[0][kk]), "=f"(raw[1][kk])
-                                     : "r"(bb + kk * (BM * 4)));
-                    } else {
-                        asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(raw[0][kk]) : "r"(bb + kk * (BM * 4)));
+                    for (int kk = 0; kk < 8; ++kk) {
+                        if constexpr (MT == 2) {
+                            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n"
+                                         : "=f"(raw[0][kk]), "=f"(raw[1][kk])
+                                         : "r"(bb + kk * (kBP * 4)));
+                        } else {
+                            asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(raw[0][kk]) : "r"(bb + kk * (kBP * 4)));
+                        }
                     }
-                }
+                };
+                if (bq == 2)
+                    ld_rows(std::integral_constant<int, BM / 2>{},
+                            stage + qo * (kSBK * (BM / 2) * 4) + khalf * 8 * ((BM / 2) * 4) + (L * MT - qo * (BM / 2)) * 4);
+                else
+                    ld_rows(std::integral_constant<int, BM>{}, stage + khalf * 8 * (BM * 4) + L * (MT * 4));
             }
         };
-        int sl = 0;            // stage ring position of the next load
-        uint32_t phl = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const int64_t q = t / tiles_p;
-            const int64_t p0 = (t % tiles_p) * BM;
+            const int64_t q = (t / tiles_p) * bq;
+            const int64_t p0 = (t % tiles_p) * BP;
             for (int kc = 0; kc < nk; ++kc) {
-                mbar_wait(&full[sl], phl);
-                load_stage(sl);
-                if (++sl == ST) sl = 0, phl ^= 1;
+                bar_wait(full0 + s * 8, ph);
+                load_stage(s);
                 uint32_t hi[MT][8], lo[MT][8];
 #pragma unroll
                 for (int j = 0; j < MT; ++j)
 #pragma unroll
-                    for (int e = 0; e < 8; e += 2) {
-                        if constexpr (V2) {
-                            split_hi_lo2(raw[j][e], raw[j][e + 1], nzero, hi[j][e], hi[j][e + 1], lo[j][e], lo[j][e + 1]);
-                        } else {
-                            split_hi_lo(raw[j][e], hi[j][e], lo[j][e]);
-                            split_hi_lo(raw[j][e + 1], hi[j][e + 1], lo[j][e + 1]);
-                        }
-                    }
+                    for (int e = 0; e < 8; ++e) split_hi_lo(raw[j][e], hi[j][e], lo[j][e]);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);  // this warp's reads of the Y stage are done
-                if (++s == ST) s = 0;
-                mbar_wait(&aempty[a], aph ^ 1);
+                if (lane == 0) bar_arrive(empty0 + s * 8);  // this warp's reads of the Y stage are done
+                if (++s == ST) s = 0, ph ^= 1;
+                bar_wait(aempty0 + a * 8, aph ^ 1);
                 sfence_after();
                 const uint32_t abuf = tmem + lane_off + uint32_t(C::A_BASE + a * MT * 32 + khalf * 8);
-#pragma unroll
-                for (int j = 0; j < MT; ++j) {
-                    st8(abuf + j * 32, hi[j]);
-                    st8(abuf + j * 32 + 16, lo[j]);
-                }
+                if constexpr (MT == 2) st8_quad(abuf, hi[0], lo[0], hi[1], lo[1]);
+                else st8_pair(abuf, hi[0], lo[0]);
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 sfence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&afull[a]);
+                if (lane == 0) bar_arrive(afull0 + a * 8);
                 if (++a == NA) a = 0, aph ^= 1;
                 // the previous chunk is added once the MMA issuer (up to NA stages behind the
                 // converters) has certainly finished it: kDefer stages after its end
@@ -523,7 +554,8 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                     if (kc + 1 == nk) {  // tile end: store once this chunk is flushed
                         store_after = true;
                         obase = out + q * P * cols + p0;
-                        orows = static_cast<int>(lmin(BM, P - p0));
+                        orows = static_cast<int>(lmin(BP, P - p0));
+                        oq = static_cast<int>(lmin(bq, Q - q));
                         ostride = P;
                     }
                     if constexpr (kDefer == 0) {
@@ -570,20 +602,21 @@ __global__ void pack_stream_kernel(const double* __restrict__ u, int64_t ld, int
     }
 }
 
-template <int NH, bool KM, int MT, int OCC, int CH, bool V2>
+template <int NH, bool KM, int MT, int OCC, int CH>
 void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                       cudaStream_t s, bool accum) {
     using C = SCfg<NH, KM, MT, OCC>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, OCC, CH, V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, OCC, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
     require(K < (int64_t(1) << 31) && Q < (int64_t(1) << 31) && P < (int64_t(1) << 31), "ttm: extent too large for TMA");
     CUtensorMap map;
     CUresult r;
-    int64_t tiles_p, ntiles, rows;
+    int64_t tiles_p, ntiles, rows, qext = 1;
+    int bq = 1;
     if constexpr (KM) {  // Q rows of K contiguous values
         tiles_p = (Q + C::BM - 1) / C::BM;
         ntiles = tiles_p;
@@ -596,12 +629,25 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
-        tiles_p = (P + C::BM - 1) / C::BM;
-        ntiles = tiles_p * Q;
+        // tiles of BM p of one q, or (MT = 2) of BM / 2 p of two q where that wastes fewer of the
+        // tile's rows on the ragged end of P (2400 = 9.4 x 256 = 18.75 x 128: 6.3% -> 1.3% idle rows)
+        static const bool no_bq = [] {
+            const char* e = std::getenv("TENKIT_STREAM_BQ");
+            return e && e[0] == '1';
+        }();
+        if (MT == 2 && !no_bq && Q >= 2) {
+            const double w1 = double((P + C::BM - 1) / C::BM * C::BM) / double(P);
+            const double w2 = double((P + C::BM / 2 - 1) / (C::BM / 2) * (C::BM / 2)) / double(P) * double((Q + 1) / 2 * 2) / double(Q);
+            if (w2 < w1 - 0.005) bq = 2;
+        }
+        const int bp = C::BM / bq;
+        tiles_p = (P + bp - 1) / bp;
+        ntiles = tiles_p * ((Q + bq - 1) / bq);
         rows = P;
+        qext = Q;
         const cuuint64_t dims[3] = {cuuint64_t(P), cuuint64_t(K), cuuint64_t(Q)};
         const cuuint64_t strides[2] = {cuuint64_t(P) * 4, cuuint64_t(P) * cuuint64_t(K) * 4};
-        const cuuint32_t box[3] = {C::BOXR, kSBK, 1};
+        const cuuint32_t box[3] = {cuuint32_t(bp), kSBK, cuuint32_t(bq)};
         const cuuint32_t estr[3] = {1, 1, 1};
         r = encode_tiled2()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -609,10 +655,10 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
-    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, OCC, CH, V2>));
-    ttm_stream_kernel<NH, KM, MT, OCC, CH, V2><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
+    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, OCC, CH>));
+    ttm_stream_kernel<NH, KM, MT, OCC, CH><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
                                                                                              cols, tiles_p, ntiles,
-                                                                                             accum ? 1 : 0, -0.0f);
+                                                                                             accum ? 1 : 0, bq, qext);
     TK_LAUNCH_CHECK();
 }
 
@@ -620,17 +666,12 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
 // converters, the factor k-block and the MMA issue are shared by both tiles (measured: 0.79 of
 // the HBM peak at cfg3 against 0.71 with one tile per CTA and two CTAs per SM; NH = 64, whose
 // two tiles leave TMEM room for one accumulator buffer only: 0.76 against 0.63). A/B knobs:
-// TENKIT_STREAM_MT=1 (one tile per CTA, two CTAs per SM), TENKIT_STREAM_V2=1 (hi/lo split of
-// two values at a time on the packed fp32x2 pipe, split_hi_lo2).
+// TENKIT_STREAM_MT=1 (one tile per CTA, two CTAs per SM), TENKIT_STREAM_BQ=1 (M-major tiles
+// never span two q).
 template <int NH, bool KM, int MT, int OCC>
 void launch_stream_mt(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                       cudaStream_t s, bool accum) {
-    static const bool v2 = [] {
-        const char* e = std::getenv("TENKIT_STREAM_V2");
-        return e && e[0] == '1';
-    }();
-    if (v2) launch_stream_ch<NH, KM, MT, OCC, kChunkDefault, true>(in, bpk, out, P, K, Q, cols, s, accum);
-    else launch_stream_ch<NH, KM, MT, OCC, kChunkDefault, false>(in, bpk, out, P, K, Q, cols, s, accum);
+    launch_stream_ch<NH, KM, MT, OCC, kChunkDefault>(in, bpk, out, P, K, Q, cols, s, accum);
 }
 
 template <int NH, bool KM>

@@ -28,7 +28,9 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("shape,mode", [((512, 300, 300), 1), ((1024, 100, 80), 1), ((2048, 333, 40), 1),
-                                        ((300, 400, 64), 2), ((256, 4000, 300), 1)])
+                                        ((300, 400, 64), 2), ((256, 4000, 300), 1),
+                                        # tiles of 128 p x 2 q (ragged P: fewer idle tile rows), odd / even Q
+                                        ((640, 64, 301), 1), ((2400, 48, 40), 1)])
 @pytest.mark.parametrize("rows", [8, 15, 20, 30, 40, 50, 60, 64])
 def test_stream_ttm_matches_oracle_and_ffma(P, O, shape, mode, rows):
     ctx = P.Context.default()

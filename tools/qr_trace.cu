@@ -6,7 +6,7 @@
 #include <random>
 #include <vector>
 int main() {
-    int shapes[][2] = {{300, 20}, {1000, 30}, {4000, 60}};
+    int shapes[][2] = {{300, 20}, {1000, 30}, {2400, 40}, {4000, 60}};
     for (auto& sh : shapes) {
         const int rows = sh[0], cols = sh[1];
         std::vector<double> h(rows * cols);
@@ -19,9 +19,11 @@ int main() {
         cudaMalloc(&u, h.size() * 8);
         cudaMalloc(&rk, 4);
         cudaMemcpy(z, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        double* work = nullptr;
+        if (tkb::qr_work_elems(rows, cols) > 0) cudaMalloc(&work, tkb::qr_work_elems(rows, cols) * 8);
         float* upk;
         cudaMalloc(&upk, size_t(rows) * 64 * 4);
-        for (int it = 0; it < 3; ++it) tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0);
+        for (int it = 0; it < 3; ++it) tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0, 0, nullptr, work);
         cudaDeviceSynchronize();
         {
             cudaEvent_t e0, e1;
@@ -29,7 +31,7 @@ int main() {
             cudaEventCreate(&e1);
             cudaEventRecord(e0);
             for (int it = 0; it < 20; ++it)
-                tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0);
+                tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0, 0, nullptr, work);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms = 0.f;
@@ -44,7 +46,7 @@ int main() {
             for (int it = 0; it < 10; ++it) {
                 cudaMemsetAsync(big, it, size_t(2) << 30);
                 cudaEventRecord(e0);
-                tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0);
+                tkb::launch_orthonormal_basis(z, rows, cols, u, cols, upk, 0, rk, nullptr, 0, 0, nullptr, work);
                 cudaEventRecord(e1);
                 cudaEventSynchronize(e1);
                 float m1 = 0.f;

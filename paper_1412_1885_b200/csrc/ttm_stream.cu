@@ -256,6 +256,13 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
     hi = (__float_as_uint(y) + 0x1000u) & 0xFFFFE000u;
     lo = __float_as_uint(y - __uint_as_float(hi));
 }
+// A/B variant (TENKIT_STREAM_TRUNC=1): y_hi = y truncated to tf32 (one instruction less per
+// value); y_lo = y - y_hi then has the sign of y and up to 13 significant bits, of which the
+// tensor core keeps 11: a one-sided residual of < 2^-20 |y| instead of a two-sided < 2^-21 |y|.
+__device__ __forceinline__ void split_hi_lo_trunc(float y, uint32_t& hi, uint32_t& lo) {
+    hi = __float_as_uint(y) & 0xFFFFE000u;
+    lo = __float_as_uint(y - __uint_as_float(hi));
+}
 
 // KM = false: Y viewed as (P, K, Q), tiles of BM consecutive p of one q; out[p + r P + q P cols].
 //             Row MT L + j of the tile is TMEM lane L of M tile j (a thread reads MT adjacent p).
@@ -264,7 +271,7 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
 //             128 j + L of the tile is TMEM lane L of M tile j.
 // Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
 // the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
-template <int NH, bool KM, int MT, int OCC, int kChunk = 16>
+template <int NH, bool KM, int MT, int OCC, int kChunk = 16, bool TR = false>
 __global__ void __launch_bounds__(kSThreads, OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
                       int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles, int accum, int bq, int64_t Q) {
@@ -522,7 +529,10 @@ __global__ void __launch_bounds__(kSThreads, OCC)
 #pragma unroll
                 for (int j = 0; j < MT; ++j)
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) split_hi_lo(raw[j][e], hi[j][e], lo[j][e]);
+                    for (int e = 0; e < 8; ++e) {
+                        if constexpr (TR) split_hi_lo_trunc(raw[j][e], hi[j][e], lo[j][e]);
+                        else split_hi_lo(raw[j][e], hi[j][e], lo[j][e]);
+                    }
                 __syncwarp();
                 if (lane == 0) bar_arrive(empty0 + s * 8);  // this warp's reads of the Y stage are done
                 if (++s == ST) s = 0, ph ^= 1;
@@ -602,13 +612,13 @@ __global__ void pack_stream_kernel(const double* __restrict__ u, int64_t ld, int
     }
 }
 
-template <int NH, bool KM, int MT, int OCC, int CH>
+template <int NH, bool KM, int MT, int OCC, int CH, bool TR>
 void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                       cudaStream_t s, bool accum) {
     using C = SCfg<NH, KM, MT, OCC>;
     static bool attr = false;
     if (!attr) {
-        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, OCC, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TK_CUDA(cudaFuncSetAttribute(ttm_stream_kernel<NH, KM, MT, OCC, CH, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::smem)));
         attr = true;
     }
@@ -655,8 +665,8 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
     }
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(C::OCC) * 148);
-    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, OCC, CH>));
-    ttm_stream_kernel<NH, KM, MT, OCC, CH><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
+    TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, OCC, CH, TR>));
+    ttm_stream_kernel<NH, KM, MT, OCC, CH, TR><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
                                                                                              cols, tiles_p, ntiles,
                                                                                              accum ? 1 : 0, bq, qext);
     TK_LAUNCH_CHECK();
@@ -671,7 +681,12 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
 template <int NH, bool KM, int MT, int OCC>
 void launch_stream_mt(const float* in, const uint8_t* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                       cudaStream_t s, bool accum) {
-    launch_stream_ch<NH, KM, MT, OCC, kChunkDefault>(in, bpk, out, P, K, Q, cols, s, accum);
+    static const bool tr = [] {
+        const char* e = std::getenv("TENKIT_STREAM_TRUNC");
+        return e && e[0] == '1';
+    }();
+    if (tr) launch_stream_ch<NH, KM, MT, OCC, kChunkDefault, true>(in, bpk, out, P, K, Q, cols, s, accum);
+    else launch_stream_ch<NH, KM, MT, OCC, kChunkDefault, false>(in, bpk, out, P, K, Q, cols, s, accum);
 }
 
 template <int NH, bool KM>

@@ -122,6 +122,30 @@ def test_rand_tucker_gram_matches_oracle(P, O, alg, dtype, dims, ranks, p):
     assert abs(f - f_ref) <= tol * abs(f_ref)
 
 
+@pytest.mark.parametrize("dims,ranks,p", [((60, 50, 40), (5, 5, 5), 5), ((300, 280, 260), (20, 20, 20), 10)])
+def test_gram_fp32_data_fp64_mode_matches_oracle_on_every_column(P, O, dims, ranks, p):
+    """fp32 data on the distributed protocol's basis: in fp32 arithmetic the oversampled (noise)
+    eigenvectors rotate freely (test above); precision='fp64' (fp64 arithmetic over the same
+    fp32 values, the reference's own precision) reproduces the oracle's dist_rand_tucker_2i on
+    EVERY r~ column up to eigenvector signs, the aligned core and the fit at the fp64 bar."""
+    y = _tensor(O, dims, ranks, (61, len(dims))).astype(np.float32)
+    yd = P.DenseTensor.from_numpy(y, np.float32).cuda()
+    m = P.rand_tucker_2i(yd, list(ranks), p, (62, 1), orthonormalizer="gram", precision="fp64").to_host()
+    g_ref, u_ref = O.dist_rand_tucker_gram(y.astype(np.float64), list(ranks), p, (62, 1), alg=3)
+    ss = []
+    for u, uo in zip(m.factors, u_ref):
+        assert u.shape == uo.shape
+        assert orthonormality_defect(u) < 1e-10
+        assert subspace_dist(u, uo) < 1e-7
+        ss.append(signs(u, uo))
+        assert np.abs(u * ss[-1] - uo).max() < 1e-6
+    g = align_core(m.core, ss)
+    assert np.linalg.norm(g - g_ref) <= 1e-7 * np.linalg.norm(g_ref)
+    f = O.fit(y.astype(np.float64), O.reconstruct(m.core, m.factors))
+    f_ref = O.fit(y.astype(np.float64), O.reconstruct(g_ref, u_ref))
+    assert abs(f - f_ref) <= 1e-9
+
+
 def test_gram_rank_drop_and_replay(P, O):
     """Exact-rank data: the Gram cut (eigenvalues <= 1e-12 top) drops directions like the
     reference's dist path; repeated calls replay the captured graph identically; the

@@ -239,6 +239,21 @@ def test_rand_tucker_alg2_matches_oracle(P, O):
     compare_models(O, y, got, ref, F64_TOL)
 
 
+@pytest.mark.parametrize("dims,mlr,ranks,p", [((400, 400, 400), (10, 10, 10), (20, 20, 20), 10),
+                                              ((640, 300, 280), (8, 8, 8), (30, 12, 12), 10),
+                                              ((72, 64, 60, 56), (4, 4, 4, 4), (6, 6, 6, 6), 4)])
+def test_rand_tucker_alg2_fp32_workload_shapes_match_oracle(P, O, dims, mlr, ranks, p):
+    """Alg. 2 (tucker.hpp:108-130) in fp32 at shapes whose first (Y-streaming) contraction runs
+    on the tensor-core kernels, 3- and 4-way, against the fp64 oracle on the fp32 values."""
+    import os
+    y = noisy_tucker(O, dims, mlr, 20.0, (31, len(dims))).astype(np.float32)
+    O.set_threads(os.cpu_count() or 1)
+    ref = O.rand_tucker(y.astype(np.float64), ranks, p, (32, 0))
+    O.set_threads(1)
+    got = P.rand_tucker(P.DenseTensor.from_numpy(y, np.float32).cuda(), ranks, p, (32, 0)).to_host()
+    compare_models(O, y.astype(np.float64), got, ref, F32_TOL)
+
+
 def test_ffcp_variants_match_oracle(P, O):
     fs = [np.abs(O.gaussian_matrix(d, 3, (84, n))) for n, d in enumerate((10, 9, 8))]
     y = O.cp_reconstruct(fs)

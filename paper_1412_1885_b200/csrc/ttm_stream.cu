@@ -55,6 +55,20 @@ EncodeTiledFn2 encode_tiled2() {
     return fn;
 }
 
+// compile-time A/B knobs (tools/build_variant.sh builds a second library with -D overrides)
+#ifndef TK_STREAM_NA_MAX
+#define TK_STREAM_NA_MAX 6
+#endif
+#ifndef TK_STREAM_STAGES_MAX
+#define TK_STREAM_STAGES_MAX 12
+#endif
+#ifndef TK_STREAM_ND_MAX
+#define TK_STREAM_ND_MAX 2
+#endif
+#ifndef TK_STREAM_CHUNK
+#define TK_STREAM_CHUNK 16
+#endif
+
 constexpr int kSConv = 8;                      // converter warps
 constexpr int kSThreads = (kSConv + 2) * 32;   // + producer + MMA
 constexpr int kSBK = 16;                       // k per pipeline stage (2 MMA k-steps of 8)
@@ -72,9 +86,9 @@ struct SCfg {
     static constexpr int BM = 128 * MT;
     // accumulator buffers: two (chunk c -> buffer c & 1) where they leave room for two A
     // buffers, else one (the MMAs of the next chunk wait for the flush)
-    static constexpr int ND = (TMEM - 2 * MT * DW) >= 2 * MT * 32 ? 2 : 1;
+    static constexpr int ND = ((TMEM - 2 * MT * DW) >= 2 * MT * 32 && TK_STREAM_ND_MAX >= 2) ? 2 : 1;
     static constexpr int NA_FIT = (TMEM - ND * MT * DW) / (MT * 32);
-    static constexpr int NA = NA_FIT > 6 ? 6 : NA_FIT;     // [y_hi | y_lo] TMEM buffers (32 columns per M tile)
+    static constexpr int NA = NA_FIT > TK_STREAM_NA_MAX ? TK_STREAM_NA_MAX : NA_FIT;     // [y_hi | y_lo] TMEM buffers (32 columns per M tile)
     static_assert(NA >= 2, "TMEM budget");
     static constexpr int A_BASE = ND * MT * DW;
     static constexpr int BOXR = BM;                        // rows per TMA box (one box per stage)
@@ -82,7 +96,7 @@ struct SCfg {
     static constexpr int STAGE_B = 128 * NH;               // two k-steps of [U_hi | U_lo] (2 NH x 8 tf32 each)
     static constexpr int SMEM_BUDGET = OCC == 2 ? 110 * 1024 : 220 * 1024;
     static constexpr int STAGES_FIT = (SMEM_BUDGET - 1024) / (STAGE_Y + STAGE_B);  // (1 KB: barriers + slack)
-    static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
+    static constexpr int STAGES = STAGES_FIT > TK_STREAM_STAGES_MAX ? TK_STREAM_STAGES_MAX : STAGES_FIT;
     static_assert(STAGES >= 3, "pipeline depth");
     // barriers: 2 per stage + 2 per y_lo buffer + 4 accumulator-buffer barriers, + the TMEM base
     static constexpr size_t BAR_BYTES = (2 * STAGES + 2 * NA + 4) * 8 + 16;
@@ -92,7 +106,7 @@ struct SCfg {
 
 // k-blocks (of 16) per accumulation chunk: the tensor core's truncating fp32 accumulation runs
 // over at most kChunk * 16 k, then the chunk is added into fp32 registers (round to nearest)
-constexpr int kChunkDefault = 16;
+constexpr int kChunkDefault = TK_STREAM_CHUNK;
 
 __device__ __forceinline__ void sfence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void sfence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }

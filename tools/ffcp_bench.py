@@ -1,4 +1,5 @@
-"""Times device FFCP on a config-2-sized Tucker model (core 30^3, U 1000x30, CP rank 20):
+"""Times device FFCP on a config-2-sized Tucker model (core 30^3, U 1000x30, CP rank 20; or
+`python tools/ffcp_bench.py iters core I R`, e.g. 200 40 2400 30 for cfg 3):
 the persistent cooperative kernel (default) against the per-sweep CUDA graph
 (TENKIT_FFCP_GRAPH=1), and the largest fit-trace difference between the two."""
 import os, sys, time
@@ -7,7 +8,7 @@ import torch
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import paper_1412_1885_b200 as P
 torch.manual_seed(0)
-cs, I, R = 30, 1000, 20
+cs, I, R = (int(a) for a in sys.argv[2:5]) if len(sys.argv) >= 5 else (30, 1000, 20)
 core = torch.randn(cs ** 3, dtype=torch.float64, device="cuda")
 us = [torch.linalg.qr(torch.randn(I, cs, dtype=torch.float64, device="cuda"))[0].t().contiguous().view(-1) for _ in range(3)]
 m = P.TuckerModel(core, us, (cs, cs, cs))

@@ -9,8 +9,11 @@
 //   restarts the TMEM accumulator. The tensor core's truncating fp32 accumulation therefore
 //   only runs over 256 k whatever K is (the first design's error grew with K: at K = 4000 its
 //   fp32 bases missed the 1e-3 parity bar, these make it at 1.7-3.1e-4).
-// * Two accumulator buffers in TMEM alternate per chunk (one where TMEM is short, NH >= 56):
-//   the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
+// * One accumulator buffer per M tile; the TMEM it leaves goes to a deeper ring of [y_hi | y_lo]
+//   A buffers (5-6 instead of 3), which decouples the converter warps from the MMA issuer better
+//   than overlapping the chunk flush did (compile-time A/B TK_STREAM_ND_MAX=2: two buffers
+//   alternating per chunk, the MMAs of chunk c + 1 running while chunk c is added; measured
+//   2-5 % slower at cfg 2 / 3 / 4).
 // * The factor is packed with NH = r~ rounded up to 8 (not 16): the main MMA covers
 //   [U_hi | U_lo] with N = 2 NH, the cross MMA y_lo U_hi with N = NH (cta_group::1 MMAs take
 //   N in steps of 8). r~ = 40: 120 MMA columns per k-step instead of 144.
@@ -62,14 +65,20 @@ EncodeTiledFn2 encode_tiled2() {
 #ifndef TK_STREAM_STAGES_MAX
 #define TK_STREAM_STAGES_MAX 12
 #endif
+#ifndef TK_STREAM_CONV
+#define TK_STREAM_CONV 8
+#endif
 #ifndef TK_STREAM_ND_MAX
-#define TK_STREAM_ND_MAX 2
+#define TK_STREAM_ND_MAX 1
 #endif
 #ifndef TK_STREAM_CHUNK
 #define TK_STREAM_CHUNK 16
 #endif
 
-constexpr int kSConv = 8;                      // converter warps
+constexpr int kSConv = TK_STREAM_CONV;         // converter warps: 8 (two k halves per TMEM lane quarter), 16 (four k quarters) or 4 (all 16 k)
+static_assert(kSConv == 4 || kSConv == 8 || kSConv == 16, "converter warps");
+constexpr int kKSplit = kSConv / 4;            // warps sharing a TMEM lane quarter, each takes 16 / kKSplit k of a stage
+constexpr int kKPW = 16 / kKSplit;             // k per converter warp and stage
 constexpr int kSThreads = (kSConv + 2) * 32;   // + producer + MMA
 constexpr int kSBK = 16;                       // k per pipeline stage (2 MMA k-steps of 8)
 
@@ -101,7 +110,7 @@ struct SCfg {
     // barriers: 2 per stage + 2 per y_lo buffer + 4 accumulator-buffer barriers, + the TMEM base
     static constexpr size_t BAR_BYTES = (2 * STAGES + 2 * NA + 4) * 8 + 16;
     static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + BAR_BYTES;
-    static constexpr int ACC = NH / 2;                     // accumulator columns per converter warp (its half)
+    static constexpr int ACC = NH / kKSplit;               // accumulator columns per converter warp (its share)
 };
 
 // k-blocks (of 16) per accumulation chunk: the tensor core's truncating fp32 accumulation runs
@@ -127,6 +136,45 @@ __device__ __forceinline__ void st8_pair(uint32_t taddr, const uint32_t (&h)[8],
         "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(l[0]), "r"(l[1]),
         "r"(l[2]), "r"(l[3]), "r"(l[4]), "r"(l[5]), "r"(l[6]), "r"(l[7])
         : "memory");
+}
+// the same for 4-k shares (16 converter warps)
+__device__ __forceinline__ void st4_pair(uint32_t taddr, const uint32_t (&h)[4], const uint32_t (&l)[4]) {
+    asm volatile(
+        "{\n\t.reg .b32 t1;\n\t"
+        "add.u32 t1, %0, 16;\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x4.b32 [t1], {%5, %6, %7, %8};\n\t}\n" ::"r"(taddr),
+        "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3])
+        : "memory");
+}
+__device__ __forceinline__ void st4_quad(uint32_t taddr, const uint32_t (&h0)[4], const uint32_t (&l0)[4],
+                                         const uint32_t (&h1)[4], const uint32_t (&l1)[4]) {
+    asm volatile(
+        "{\n\t.reg .b32 t1, t2, t3;\n\t"
+        "add.u32 t1, %0, 16;\n\t"
+        "add.u32 t2, %0, 32;\n\t"
+        "add.u32 t3, %0, 48;\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x4.b32 [t1], {%5, %6, %7, %8};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x4.b32 [t2], {%9, %10, %11, %12};\n\t"
+        "tcgen05.st.sync.aligned.32x32b.x4.b32 [t3], {%13, %14, %15, %16};\n\t}\n" ::"r"(taddr),
+        "r"(h0[0]), "r"(h0[1]), "r"(h0[2]), "r"(h0[3]), "r"(l0[0]), "r"(l0[1]), "r"(l0[2]), "r"(l0[3]), "r"(h1[0]),
+        "r"(h1[1]), "r"(h1[2]), "r"(h1[3]), "r"(l1[0]), "r"(l1[1]), "r"(l1[2]), "r"(l1[3])
+        : "memory");
+}
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16};\n" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void ld2(uint32_t taddr, float* v) {
+    uint32_t r[2];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr) : "memory");
+    v[0] = __uint_as_float(r[0]);
+    v[1] = __uint_as_float(r[1]);
 }
 __device__ __forceinline__ void st8_quad(uint32_t taddr, const uint32_t (&h0)[8], const uint32_t (&l0)[8],
                                          const uint32_t (&h1)[8], const uint32_t (&l1)[8]) {
@@ -283,8 +331,9 @@ __device__ __forceinline__ void split_hi_lo_trunc(float y, uint32_t& hi, uint32_
 // KM = true:  Y viewed as Q rows of K contiguous values (contraction over mode 0), tiles of BM
 //             rows; out[row + r Q] (transposed output: the contracted mode moves last). Row
 //             128 j + L of the tile is TMEM lane L of M tile j.
-// Accumulation chunks of kChunk k-blocks alternate between two TMEM accumulator buffers, so
-// the MMAs of chunk c + 1 run while the converter warps add chunk c into their registers.
+// Accumulation chunks of kChunk k-blocks: at a chunk end the converter warps wait for the chunk's
+// MMAs, add the TMEM accumulator into their registers and release it (ND = 2: two buffers
+// alternating, the flush deferred behind the next chunk's first stages).
 template <int NH, bool KM, int MT, int OCC, int kChunk = 16, bool TR = false>
 __global__ void __launch_bounds__(kSThreads, OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
@@ -405,11 +454,11 @@ __global__ void __launch_bounds__(kSThreads, OCC)
         }
     } else {
         // ===== converters (warps 0-7) =====
-        const int quarter = warp & 3, khalf = warp >> 2;
+        const int quarter = warp & 3, khalf = warp >> 2;  // khalf: this warp's k share of a stage (0 .. kKSplit - 1)
         const int L = quarter * 32 + lane;  // TMEM lane
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         constexpr int ACC = C::ACC;
-        const int c0 = khalf * (NH / 2);  // this warp's accumulator columns
+        const int c0 = khalf * (NH / kKSplit);  // this warp's accumulator columns
         uint32_t sy0 = smem_u32(sY), full0 = smem_u32(full), empty0 = smem_u32(empty), afull0 = smem_u32(afull),
                  aempty0 = smem_u32(aempty), dfull0 = smem_u32(dfull), dempty0 = smem_u32(dempty);
         asm volatile("" : "+r"(sy0), "+r"(full0), "+r"(empty0), "+r"(afull0), "+r"(aempty0), "+r"(dfull0), "+r"(dempty0));
@@ -440,9 +489,16 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                     if (cc + 8 <= ACC) {
                         ld8(base + cc, m);
                         ld8(base + NH + cc, x);
-                    } else {
+                    } else if (cc + 4 <= ACC) {
                         ld4(base + cc, m);
                         ld4(base + NH + cc, x);
+                        if (cc + 6 <= ACC) {
+                            ld2(base + cc + 4, m + 4);
+                            ld2(base + NH + cc + 4, x + 4);
+                        }
+                    } else {
+                        ld2(base + cc, m);
+                        ld2(base + NH + cc, x);
                     }
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
@@ -490,7 +546,7 @@ __global__ void __launch_bounds__(kSThreads, OCC)
             store_after = false;
         };
         // raw Y values of one stage: this thread's MT rows x 8 k (its k half)
-        float raw[MT][8];
+        float raw[MT][kKPW];
         const auto load_stage = [&](int st) {
             const uint32_t stage = sy0 + st * C::STAGE_Y;
             if constexpr (KM) {
@@ -500,8 +556,8 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                     const int row = 128 * j + L;
                     const uint32_t rb = stage + row * 64;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int phys = (2 * khalf + h) ^ ((row >> 1) & 3);
+                    for (int h = 0; h < kKPW / 4; ++h) {
+                        const int phys = ((kKPW / 4) * khalf + h) ^ ((row >> 1) & 3);
                         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                                      : "=f"(raw[j][h * 4 + 0]), "=f"(raw[j][h * 4 + 1]), "=f"(raw[j][h * 4 + 2]),
                                        "=f"(raw[j][h * 4 + 3])
@@ -516,7 +572,7 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                 const auto ld_rows = [&](auto bp_c, uint32_t bb) {
                     constexpr int kBP = decltype(bp_c)::value;
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
+                    for (int kk = 0; kk < kKPW; ++kk) {
                         if constexpr (MT == 2) {
                             asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n"
                                          : "=f"(raw[0][kk]), "=f"(raw[1][kk])
@@ -528,9 +584,9 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                 };
                 if (bq == 2)
                     ld_rows(std::integral_constant<int, BM / 2>{},
-                            stage + qo * (kSBK * (BM / 2) * 4) + khalf * 8 * ((BM / 2) * 4) + (L * MT - qo * (BM / 2)) * 4);
+                            stage + qo * (kSBK * (BM / 2) * 4) + khalf * kKPW * ((BM / 2) * 4) + (L * MT - qo * (BM / 2)) * 4);
                 else
-                    ld_rows(std::integral_constant<int, BM>{}, stage + khalf * 8 * (BM * 4) + L * (MT * 4));
+                    ld_rows(std::integral_constant<int, BM>{}, stage + khalf * kKPW * (BM * 4) + L * (MT * 4));
             }
         };
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -539,11 +595,11 @@ __global__ void __launch_bounds__(kSThreads, OCC)
             for (int kc = 0; kc < nk; ++kc) {
                 bar_wait(full0 + s * 8, ph);
                 load_stage(s);
-                uint32_t hi[MT][8], lo[MT][8];
+                uint32_t hi[MT][kKPW], lo[MT][kKPW];
 #pragma unroll
                 for (int j = 0; j < MT; ++j)
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
+                    for (int e = 0; e < kKPW; ++e) {
                         if constexpr (TR) split_hi_lo_trunc(raw[j][e], hi[j][e], lo[j][e]);
                         else split_hi_lo(raw[j][e], hi[j][e], lo[j][e]);
                     }
@@ -552,9 +608,20 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                 if (++s == ST) s = 0, ph ^= 1;
                 bar_wait(aempty0 + a * 8, aph ^ 1);
                 sfence_after();
-                const uint32_t abuf = tmem + lane_off + uint32_t(C::A_BASE + a * MT * 32 + khalf * 8);
-                if constexpr (MT == 2) st8_quad(abuf, hi[0], lo[0], hi[1], lo[1]);
-                else st8_pair(abuf, hi[0], lo[0]);
+                const uint32_t abuf = tmem + lane_off + uint32_t(C::A_BASE + a * MT * 32 + khalf * kKPW);
+                if constexpr (kKPW == 16) {
+#pragma unroll
+                    for (int j = 0; j < MT; ++j) {
+                        st16(abuf + j * 32, hi[j]);
+                        st16(abuf + j * 32 + 16, lo[j]);
+                    }
+                } else if constexpr (kKPW == 8) {
+                    if constexpr (MT == 2) st8_quad(abuf, hi[0], lo[0], hi[1], lo[1]);
+                    else st8_pair(abuf, hi[0], lo[0]);
+                } else {
+                    if constexpr (MT == 2) st4_quad(abuf, hi[0], lo[0], hi[1], lo[1]);
+                    else st4_pair(abuf, hi[0], lo[0]);
+                }
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 sfence_before();
                 __syncwarp();

@@ -226,6 +226,9 @@ __device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rin
     }
     __syncthreads();
     double r00 = 0.0;
+    // pivot margin = 1 - sqrt(max over steps of second / top): the largest ratio is tracked as a
+    // fraction (cross-multiplied compare), the division and square root happen once at the end
+    double mnum = 0.0, mden = 1.0;  // (lane 0 of warp 0)
     for (int k = 0; k < n; ++k) {
         if (tid < 32) {
             int best = k;
@@ -251,7 +254,7 @@ __device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rin
                 const double dsec = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(h2) << 32) | l2));
                 if (lane == 0 && k + 1 < n) {
                     if (dtop - dsec < kTieGapSq * dtop) ctl[1] = 1;
-                    else *pmargin = fmin(k == 0 ? 1.0 : *pmargin, 1.0 - sqrt(dsec / dtop));
+                    else if (dsec * mden > mnum * dtop) mnum = dsec, mden = dtop;
                 }
             }
             if (lane == 0) ctl[0] = best;
@@ -291,11 +294,15 @@ __device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rin
         const int m = n - k - 1;
         // trailing update S_ij -= (S_ki / R_kk)(S_kj / R_kk), i, j > k; the diagonal threads
         // also write row k of R
-        for (int e = tid; e < m * m; e += kQrThreads) {
-            const int i = k + 1 + e % m, j = k + 1 + e / m;
-            const double rki = gs[k + i * n] * inv, rkj = gs[k + j * n] * inv;
-            gs[i + j * n] = fma(-rki, rkj, gs[i + j * n]);
-            if (i == j) rr[k + j * n] = rkj;
+        // (16 x 16 thread tiles over the trailing block: no integer division in the index math)
+        (void)m;
+        for (int j = k + 1 + (tid >> 4); j < n; j += kQrThreads / 16) {
+            const double rkj = gs[k + j * n] * inv;
+            for (int i = k + 1 + (tid & 15); i < n; i += 16) {
+                const double rki = gs[k + i * n] * inv;
+                gs[i + j * n] = fma(-rki, rkj, gs[i + j * n]);
+                if (i == j) rr[k + j * n] = rkj;
+            }
         }
         if (tid == 0) {
             rr[k + k * n] = rkk;
@@ -303,6 +310,8 @@ __device__ bool cta_pchol(double* gs, int n, bool pivot, double* rr, double* rin
         }
         __syncthreads();
     }
+    if (tid == 0 && pivot) *pmargin = 1.0 - sqrt(mnum / mden);
+    __syncthreads();
     return true;
 }
 
@@ -337,7 +346,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
     };
     int pv;
     double d, d2;
-    double pm = 1.0;
+    double mnum = 0.0, mden = 1.0;  // largest second / top ratio so far, as a fraction
     pick(pv, d, d2);
 #pragma unroll 1
     for (int k = 0; k < n; ++k) {
@@ -347,7 +356,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         if (pv >= n || !(d > 0.0) || !(d > kFastMinRatio * kFastMinRatio * r00)) return false;
         if (k + 1 < n) {  // near tie: the Householder path decides
             if (d - d2 < kTieGapSq * d) return false;
-            pm = fmin(pm, 1.0 - sqrt(d2 / d));
+            if (d2 * mden > mnum * d) mnum = d2, mden = d;  // (no division / square root on the step chain)
         }
         QR_MARK(701 + 4 * k);
         const double rd = 1.0 / d;  // overlaps the row exchange below
@@ -382,7 +391,7 @@ __device__ __noinline__ bool warp_pchol_reg(const double* gs, int n, double* lra
         d2 = d12;
     }
     for (int k = lane; k < n; k += 32) rdk[k] = sqrt(rdk[k]);
-    if (lane == 0) *pmargin = pm;
+    if (lane == 0) *pmargin = 1.0 - sqrt(mnum / mden);
     __syncwarp();
     return true;
 }

@@ -71,6 +71,9 @@ EncodeTiledFn2 encode_tiled2() {
 #ifndef TK_STREAM_ND_MAX
 #define TK_STREAM_ND_MAX 1
 #endif
+#ifndef TK_STREAM_SPLITB
+#define TK_STREAM_SPLITB 0
+#endif
 #ifndef TK_STREAM_DEFER1
 #define TK_STREAM_DEFER1 0
 #endif
@@ -107,12 +110,28 @@ struct SCfg {
     static constexpr int STAGE_Y = kSBK * BM * 4;
     static constexpr int STAGE_B = 128 * NH;               // two k-steps of [U_hi | U_lo] (2 NH x 8 tf32 each)
     static constexpr int SMEM_BUDGET = OCC == 2 ? 110 * 1024 : 220 * 1024;
+#if TK_STREAM_SPLITB
+    // Split rings: a Y stage is released by the converter warps alone (right after conversion);
+    // the factor k-blocks live in their own ring, NA + 2 slots deeper, released by the MMA commits
+    // (with one ring the MMA issuer, up to NA stages behind, holds the 16 KB Y slots for the sake
+    // of their 5 KB factor blocks).
+#ifdef TK_STREAM_BEXTRA
+    static constexpr int BEXTRA = TK_STREAM_BEXTRA;
+#else
+    static constexpr int BEXTRA = NA + 2;
+#endif
+    static constexpr int STAGES_FIT = (SMEM_BUDGET - 1024 - BEXTRA * STAGE_B) / (STAGE_Y + STAGE_B);
+    static constexpr int STAGES = STAGES_FIT > TK_STREAM_STAGES_MAX ? TK_STREAM_STAGES_MAX : STAGES_FIT;
+    static constexpr int BSTAGES = STAGES + BEXTRA;
+#else
     static constexpr int STAGES_FIT = (SMEM_BUDGET - 1024) / (STAGE_Y + STAGE_B);  // (1 KB: barriers + slack)
     static constexpr int STAGES = STAGES_FIT > TK_STREAM_STAGES_MAX ? TK_STREAM_STAGES_MAX : STAGES_FIT;
+    static constexpr int BSTAGES = STAGES;
+#endif
     static_assert(STAGES >= 3, "pipeline depth");
-    // barriers: 2 per stage + 2 per y_lo buffer + 4 accumulator-buffer barriers, + the TMEM base
-    static constexpr size_t BAR_BYTES = (2 * STAGES + 2 * NA + 4) * 8 + 16;
-    static constexpr size_t smem = size_t(STAGES) * (STAGE_Y + STAGE_B) + BAR_BYTES;
+    // barriers: 2 per stage (+ 2 per factor slot) + 2 per y_lo buffer + 4 accumulator-buffer barriers, + the TMEM base
+    static constexpr size_t BAR_BYTES = (2 * STAGES + 2 * BSTAGES + 2 * NA + 4) * 8 + 16;
+    static constexpr size_t smem = size_t(STAGES) * STAGE_Y + size_t(BSTAGES) * STAGE_B + BAR_BYTES;
     static constexpr int ACC = NH / kKSplit;               // accumulator columns per converter warp (its share)
 };
 
@@ -315,6 +334,39 @@ __device__ __forceinline__ void bar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
 
+// Split rings: the Y box and the factor k-block complete on their own barriers.
+__device__ __forceinline__ void produce_y3(uint32_t bar, uint32_t bytes, uint32_t dy, const CUtensorMap* map, int c0,
+                                          int c1, int c2) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3, {%4, %5, %6}], "
+        "[%0];\n\t}\n" ::"r"(bar),
+        "r"(bytes), "r"(dy), "l"(map), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void produce_y2(uint32_t bar, uint32_t bytes, uint32_t dy, const CUtensorMap* map, int c0,
+                                          int c1) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3, {%4, %5}], "
+        "[%0];\n\t}\n" ::"r"(bar),
+        "r"(bytes), "r"(dy), "l"(map), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void produce_b(uint32_t bar, uint32_t db, const void* src, uint32_t bbytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %3;\n\t"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%1], [%2], %3, [%0];\n\t}\n" ::"r"(bar),
+        "r"(db), "l"(src), "r"(bbytes)
+        : "memory");
+}
+
 // y_hi = y rounded to nearest tf32, y_lo = y - y_hi (exact in fp32; the tensor core reads its
 // top 19 bits)
 __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo) {
@@ -347,11 +399,14 @@ __global__ void __launch_bounds__(kSThreads, OCC)
     // this kernel): 1024-B aligned as the 128B-span swizzles need
     extern __shared__ __align__(1024) uint8_t ssm[];
     uint8_t* sY = ssm;                             // [stages][BM/BOXR boxes]
-    uint8_t* sB = ssm + size_t(ST) * C::STAGE_Y;   // [stages][2 k-steps][2NH x 8] tf32 core matrices
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(ST) * C::STAGE_B);
+    constexpr int SB = C::BSTAGES;
+    uint8_t* sB = ssm + size_t(ST) * C::STAGE_Y;   // [factor slots][2 k-steps][2NH x 8] tf32 core matrices
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(SB) * C::STAGE_B);
     uint64_t* full = bars;               // [ST]  producer -> converters, MMA
     uint64_t* empty = full + ST;         // [ST]  converters (8) + MMA commit (1) -> producer
-    uint64_t* afull = empty + ST;        // [NA]  converters (8) -> MMA
+    uint64_t* bfull = empty + ST;        // [SB]  split rings: producer -> MMA (factor k-block landed)
+    uint64_t* bempty = bfull + SB;       // [SB]  split rings: MMA commit -> producer
+    uint64_t* afull = bempty + SB;       // [NA]  converters (8) -> MMA
     uint64_t* aempty = afull + NA;       // [NA]  MMA commit -> converters
     uint64_t* dfull = aempty + NA;       // [2]   MMA commit (chunk done) -> converters
     uint64_t* dempty = dfull + 2;        // [2]   converters (8, chunk flushed) -> MMA
@@ -364,7 +419,11 @@ __global__ void __launch_bounds__(kSThreads, OCC)
         if (smem_u32(ssm) & 1023) __trap();  // the swizzle atoms need 1024-B alignment
         for (int s = 0; s < ST; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kSConv + 1);
+            mbar_init(&empty[s], TK_STREAM_SPLITB ? kSConv : kSConv + 1);
+        }
+        for (int b = 0; b < SB; ++b) {
+            mbar_init(&bfull[b], 1);
+            mbar_init(&bempty[b], 1);
         }
         for (int a = 0; a < NA; ++a) {
             mbar_init(&afull[a], kSConv);
@@ -393,20 +452,37 @@ __global__ void __launch_bounds__(kSThreads, OCC)
         uint32_t ph = 0;
         uint32_t y0 = smem_u32(sY), b0 = smem_u32(sB), f0 = smem_u32(full), e0 = smem_u32(empty);
         asm volatile("" : "+r"(y0), "+r"(b0), "+r"(f0), "+r"(e0));
+#if TK_STREAM_SPLITB
+        int sb = 0;
+        uint32_t phb = 0;
+        uint32_t bf0 = smem_u32(bfull), be0 = smem_u32(bempty);
+        asm volatile("" : "+r"(bf0), "+r"(be0));
+#endif
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int64_t q = (t / tiles_p) * bq;
             const int64_t p0 = (t % tiles_p) * (BM / bq);
             for (int kc = 0; kc < nk; ++kc) {
+                const uint8_t* src = bpk + size_t(kc) * C::STAGE_B;
+#if TK_STREAM_SPLITB
+                bar_wait(be0 + sb * 8, phb ^ 1);
+                __syncwarp();
+                produce_b(bf0 + sb * 8, b0 + sb * C::STAGE_B, src, C::STAGE_B);
+                if (++sb == SB) sb = 0, phb ^= 1;
+                bar_wait(e0 + s * 8, ph ^ 1);
+                __syncwarp();
+                if constexpr (KM) produce_y2(f0 + s * 8, C::STAGE_Y, y0 + s * C::STAGE_Y, &ymap, kc * kSBK, static_cast<int>(p0));
+                else produce_y3(f0 + s * 8, C::STAGE_Y, y0 + s * C::STAGE_Y, &ymap, static_cast<int>(p0), kc * kSBK, static_cast<int>(q));
+#else
                 bar_wait(e0 + s * 8, ph ^ 1);
                 __syncwarp();
                 const uint32_t bar = f0 + s * 8, dy = y0 + s * C::STAGE_Y, db = b0 + s * C::STAGE_B;
-                const uint8_t* src = bpk + size_t(kc) * C::STAGE_B;
                 if constexpr (KM) {
                     produce2(bar, C::STAGE_Y + C::STAGE_B, dy, &ymap, kc * kSBK, static_cast<int>(p0), db, src, C::STAGE_B);
                 } else {
                     produce3(bar, C::STAGE_Y + C::STAGE_B, dy, &ymap, static_cast<int>(p0), kc * kSBK,
                              static_cast<int>(q), db, src, C::STAGE_B);
                 }
+#endif
                 if (++s == ST) s = 0, ph ^= 1;
             }
         }
@@ -417,7 +493,11 @@ __global__ void __launch_bounds__(kSThreads, OCC)
             const uint32_t id_main = sidesc(2 * NH, false), id_cross = sidesc(C::CN, false);
             int s = 0, a = 0;
             uint32_t ph = 0, aph = 0, ch = 0;
-            uint32_t sb0 = smem_u32(sB), full0 = smem_u32(full), afull0 = smem_u32(afull), dempty0 = smem_u32(dempty);
+            // the ring the MMA issuer follows: the stage ring, or the factor ring when they are split
+            constexpr int RS = TK_STREAM_SPLITB ? SB : ST;
+            uint64_t* const rfull = TK_STREAM_SPLITB ? bfull : full;
+            uint64_t* const rempty = TK_STREAM_SPLITB ? bempty : empty;
+            uint32_t sb0 = smem_u32(sB), full0 = smem_u32(rfull), afull0 = smem_u32(afull), dempty0 = smem_u32(dempty);
             asm volatile("" : "+r"(sb0), "+r"(full0), "+r"(afull0), "+r"(dempty0));
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 for (int k0 = 0; k0 < nk; k0 += kChunk, ++ch) {
@@ -429,7 +509,7 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                     }
                     const int k1 = min(nk, k0 + kChunk);
                     for (int kc = k0; kc < k1; ++kc) {
-                        bar_wait(full0 + s * 8, ph);
+                        bar_wait(full0 + s * 8, ph);  // (split rings: the factor ring's barriers)
                         const uint32_t bs = sb0 + s * C::STAGE_B;
                         bar_wait(afull0 + a * 8, aph);
                         __syncwarp();
@@ -447,8 +527,8 @@ __global__ void __launch_bounds__(kSThreads, OCC)
                             }
                         }
                         commit(&aempty[a]);
-                        commit(&empty[s]);
-                        if (++s == ST) s = 0, ph ^= 1;
+                        commit(&rempty[s]);
+                        if (++s == RS) s = 0, ph ^= 1;
                         if (++a == NA) a = 0, aph ^= 1;
                     }
                     commit(&dfull[b]);

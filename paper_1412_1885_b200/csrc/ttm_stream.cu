@@ -71,6 +71,9 @@ EncodeTiledFn2 encode_tiled2() {
 #ifndef TK_STREAM_ND_MAX
 #define TK_STREAM_ND_MAX 1
 #endif
+#ifndef TK_STREAM_WAIT_HINT
+#define TK_STREAM_WAIT_HINT 0
+#endif
 #ifndef TK_STREAM_SPLITB
 #define TK_STREAM_SPLITB 0
 #endif
@@ -320,6 +323,19 @@ __device__ __forceinline__ void produce2(uint32_t bar, uint32_t bytes, uint32_t 
 // mbarrier operations on 32-bit shared-window addresses kept in registers (the generic-pointer
 // helpers recompute the window base from SR_CgaCtaId at every use inside the stage loop)
 __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+#if TK_STREAM_WAIT_HINT
+    // suspend-time hint: the hardware parks the warp until the phase completes (or the hint
+    // expires) instead of returning to the retry loop every few hundred cycles
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}\n" ::"r"(bar),
+        "r"(parity), "r"(uint32_t(TK_STREAM_WAIT_HINT))
+        : "memory");
+#else
     asm volatile(
         "{\n\t"
         ".reg .pred P1;\n\t"
@@ -329,6 +345,7 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
         "}\n" ::"r"(bar),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void bar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");

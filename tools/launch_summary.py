@@ -19,7 +19,8 @@ for r in rows:
             data.append((d["Kernel Name"], d["Grid Size"], float(d["Metric Value"].replace(",", ""))))
 # tkb kernels only, last nsteps * (launches per step)
 tk = [x for x in data if "tkb::" in x[0]]
-big = [i for i, x in enumerate(tk) if ("ttm_mmajor" in x[0] or "ttm_tc" in x[0] or "ttm_stream" in x[0]) and x[2] > 200000]
+thr = float(sys.argv[4]) if len(sys.argv) > 4 else 200000.0  # ns: a launch at least this long is a Y pass
+big = [i for i, x in enumerate(tk) if ("ttm_mmajor" in x[0] or "ttm_tc" in x[0] or "ttm_stream" in x[0]) and x[2] > thr]
 per_step = int(sys.argv[3]) if len(sys.argv) > 3 else 3  # Y passes per decomposition (grouped)
 start = big[-per_step * nsteps] if len(big) >= per_step * nsteps else 0
 win = tk[start:]

@@ -48,10 +48,10 @@ void launch_pack_umma(const double* u, int64_t ld, int64_t rows, int cols, void*
 int launch_ttm_tc(const float* in, const void* bpk, float* out, int64_t P, int64_t K, int64_t Q, int cols,
                   cudaStream_t s, bool accurate = false, bool tout = false, float* work = nullptr,
                   int64_t work_elems = 0);
-// Second-design Y-streaming pass (ttm_stream.cu, fp32): y_hi straight from the TMA-staged
-// shared memory, y_lo from TMEM, chunked accumulation flushed into fp32 registers, factor packed
-// by launch_pack_stream (NH = cols rounded up to 8). P == 1: contraction over mode 0 with the
-// transposed output out[q + r Q]; else out[p + r P + q P cols]. Persistent, 2 CTAs per SM.
+// Second-design Y-streaming pass (ttm_stream.cu, fp32): [y_hi | y_lo] from TMEM, chunked
+// accumulation flushed into fp32 registers, factor packed by launch_pack_stream (NH = cols rounded
+// up to 8). P == 1: contraction over mode 0 with the transposed output out[q + r Q]; else
+// out[p + r P + q P cols]. Persistent, one CTA per SM with two 128-row M tiles.
 bool stream_ttm_enabled();
 bool stream_ttm_supported(const float* in, float* out, int64_t P, int64_t K, int64_t Q, int cols);
 int64_t stream_pack_bytes(int64_t rows, int cols);

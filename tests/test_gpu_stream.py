@@ -1,5 +1,5 @@
-"""The second-design Y-streaming kernel (csrc/ttm_stream.cu: y_hi read by the MMA from the
-TMA-staged shared memory, y_lo from TMEM, chunked accumulation flushed into fp32 registers)
+"""The second-design Y-streaming kernel (csrc/ttm_stream.cu: [y_hi | y_lo] A operands from TMEM,
+chunked accumulation flushed into fp32 registers)
 against the oracle's ttm (tensor.hpp:151-176) and the FFMA kernel, through tk_ttm with
 ttm path 3 (M-major contractions), and inside rand_tucker_2i, where it runs every Y pass
 (M-major and the mode-0 K-major pass with its transposed output).

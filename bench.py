@@ -533,7 +533,10 @@ def run_b200(args, cfg):
                          else "ttm_mmajor_kernel (Y-streaming TTM, FFMA fp64)",
                          "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if not pk.get("_fallback") else "fallback",
                          "bytes_per_launch": ybytes, "mean_launch_ms": round(kern_ms, 4),
-                         "launches_per_step": passes},
+                         "launches_per_step": passes,
+                         # context, not a bench value: the same kernel alone under ncu (committed capture,
+                         # un-throttled clocks); the live figure above is taken under the sustained power cap
+                         "alone_under_ncu": _ncu_alone(args.config, world, hbm)},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "fit_model": round(fit_model, 7),
@@ -560,6 +563,24 @@ def _ncu_traffic(workload, world=1):
     try:
         d = json.load(open(p)).get(workload)
         return d.get("dram_bytes_per_launch") if d and world == 1 else None
+    except Exception:
+        return None
+
+
+def _ncu_alone(workload, world, hbm):
+    """Mean duration of the workload's Y-pass launches in the committed ncu --set full capture
+    (profiles/ttm_traffic.json) and the fraction of the HBM peak it corresponds to, else None."""
+    p = os.path.join(ROOT, "profiles", "ttm_traffic.json")
+    try:
+        d = json.load(open(p)).get(workload)
+        if not d or world != 1:
+            return None
+        us = [v["ncu_duration_us"] for v in d.values() if isinstance(v, dict) and "ncu_duration_us" in v]
+        if not us:
+            return None
+        ms = sum(us) / len(us) / 1e3
+        return {"mean_launch_ms": round(ms, 4), "frac": round(d["algorithmic_bytes_per_launch"] / (ms * 1e-3) / 1e9 / hbm, 4),
+                "source": "profiles/ttm_traffic.json"}
     except Exception:
         return None
 

@@ -71,6 +71,9 @@ EncodeTiledFn2 encode_tiled2() {
 #ifndef TK_STREAM_ND_MAX
 #define TK_STREAM_ND_MAX 1
 #endif
+#ifndef TK_STREAM_PIPEBAL
+#define TK_STREAM_PIPEBAL 1
+#endif
 #ifndef TK_STREAM_WAIT_HINT
 #define TK_STREAM_WAIT_HINT 0
 #endif
@@ -390,6 +393,26 @@ __device__ __forceinline__ void split_hi_lo(float y, uint32_t& hi, uint32_t& lo)
     hi = (__float_as_uint(y) + 0x1000u) & 0xFFFFE000u;
     lo = __float_as_uint(y - __uint_as_float(hi));
 }
+// The same values with the work spread over both issue pipes: the rounding add as an IMAD
+// (`one` is 1 from a kernel argument, so ptxas keeps the multiply-add on the fma pipe instead of
+// a VIADD on the alu pipe) and y - hi as an immediate-form FFMA (hi * -1 + y, twice the issue
+// rate of the three-register FADD). With the plain form the alu pipe carries two of the three
+// instructions per value (VIADD, LOP3) and bounds the split; 12 of a thread's 16 values take
+// this form, 4 the plain one: ~40 pipe cycles per warp and stage on either pipe instead of 64 / 32.
+__device__ __forceinline__ void split_hi_lo_fma(float y, uint32_t one, uint32_t& hi, uint32_t& lo) {
+    uint32_t h;
+    asm("mad.lo.u32 %0, %1, %2, 0x1000;\n" : "=r"(h) : "r"(__float_as_uint(y)), "r"(one));
+    hi = h & 0xFFFFE000u;
+    float l;
+    asm("fma.rn.f32 %0, %1, 0fBF800000, %2;\n" : "=f"(l) : "f"(__uint_as_float(hi)), "f"(y));
+    lo = __float_as_uint(l);
+}
+__device__ __forceinline__ void split_hi_lo_alu(float y, uint32_t& hi, uint32_t& lo) {
+    hi = (__float_as_uint(y) + 0x1000u) & 0xFFFFE000u;
+    float l;
+    asm("fma.rn.f32 %0, %1, 0fBF800000, %2;\n" : "=f"(l) : "f"(__uint_as_float(hi)), "f"(y));
+    lo = __float_as_uint(l);
+}
 // A/B variant (TENKIT_STREAM_TRUNC=1): y_hi = y truncated to tf32 (one instruction less per
 // value); y_lo = y - y_hi then has the sign of y and up to 13 significant bits, of which the
 // tensor core keeps 11: a one-sided residual of < 2^-20 |y| instead of a two-sided < 2^-21 |y|.
@@ -409,7 +432,8 @@ __device__ __forceinline__ void split_hi_lo_trunc(float y, uint32_t& hi, uint32_
 template <int NH, bool KM, int MT, int OCC, int kChunk = 16, bool TR = false>
 __global__ void __launch_bounds__(kSThreads, OCC)
     ttm_stream_kernel(const __grid_constant__ CUtensorMap ymap, const uint8_t* __restrict__ bpk, float* __restrict__ out,
-                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles, int accum, int bq, int64_t Q) {
+                      int64_t P, int64_t K, int cols, int64_t tiles_p, int64_t ntiles, int accum, int bq, int64_t Q,
+                      uint32_t one) {
     using C = SCfg<NH, KM, MT, OCC>;
     constexpr int BM = C::BM, NA = C::NA, ST = C::STAGES, ND = C::ND;
     // dynamic shared memory starts at offset 0 of the CTA's window (no static shared memory in
@@ -703,7 +727,9 @@ __global__ void __launch_bounds__(kSThreads, OCC)
 #pragma unroll
                     for (int e = 0; e < kKPW; ++e) {
                         if constexpr (TR) split_hi_lo_trunc(raw[j][e], hi[j][e], lo[j][e]);
-                        else split_hi_lo(raw[j][e], hi[j][e], lo[j][e]);
+                        else if constexpr (TK_STREAM_PIPEBAL == 0) split_hi_lo(raw[j][e], hi[j][e], lo[j][e]);
+                        else if (TK_STREAM_PIPEBAL == 1 && (e & 3) == 3) split_hi_lo_alu(raw[j][e], hi[j][e], lo[j][e]);
+                        else split_hi_lo_fma(raw[j][e], one, hi[j][e], lo[j][e]);
                     }
                 __syncwarp();
                 if (lane == 0) bar_arrive(empty0 + s * 8);  // this warp's reads of the Y stage are done
@@ -851,7 +877,7 @@ void launch_stream_ch(const float* in, const uint8_t* bpk, float* out, int64_t P
     TK_MAXSMEM((ttm_stream_kernel<NH, KM, MT, OCC, CH, TR>));
     ttm_stream_kernel<NH, KM, MT, OCC, CH, TR><<<static_cast<unsigned>(grid), kSThreads, C::smem, s>>>(map, bpk, out, rows, K,
                                                                                              cols, tiles_p, ntiles,
-                                                                                             accum ? 1 : 0, bq, qext);
+                                                                                             accum ? 1 : 0, bq, qext, 1u);
     TK_LAUNCH_CHECK();
 }
 

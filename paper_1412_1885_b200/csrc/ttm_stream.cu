@@ -418,7 +418,9 @@ __device__ __forceinline__ void split_hi_lo_alu(float y, uint32_t& hi, uint32_t&
 // tensor core keeps 11: a one-sided residual of < 2^-20 |y| instead of a two-sided < 2^-21 |y|.
 __device__ __forceinline__ void split_hi_lo_trunc(float y, uint32_t& hi, uint32_t& lo) {
     hi = __float_as_uint(y) & 0xFFFFE000u;
-    lo = __float_as_uint(y - __uint_as_float(hi));
+    float l;  // y - hi as an immediate-form FFMA (see split_hi_lo_fma)
+    asm("fma.rn.f32 %0, %1, 0fBF800000, %2;\n" : "=f"(l) : "f"(__uint_as_float(hi)), "f"(y));
+    lo = __float_as_uint(l);
 }
 
 // KM = false: Y viewed as (P, K, Q), tiles of BM consecutive p of one q; out[p + r P + q P cols].

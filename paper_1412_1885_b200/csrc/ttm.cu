@@ -535,6 +535,61 @@ __global__ void __launch_bounds__(256) sketch_kernel(const T* __restrict__ x, in
         }
 }
 
+// The same with one CTA covering ALL rn columns (rn <= 64) of its 32 rows: thread (lane = row,
+// warp = column group of CG = ceil(rn / 8) columns). X is staged once per row tile (the 32-column
+// tiles above stage it once per column tile and leave 24 of 64 columns idle at rn = 40), and a
+// k step costs 1 + CG shared loads for CG FMAs. KT = k per staging round (32 when CG > 4, so the
+// two staging buffers stay inside the static shared-memory limit).
+template <typename T, int CG, int KT>
+__global__ void __launch_bounds__(256) sketch_wide_kernel(const T* __restrict__ x, int B, int64_t I, int A,
+                                                          const T* __restrict__ om, int stride, int rn, int kchunk,
+                                                          double* __restrict__ part) {
+    constexpr int NC = 8 * CG;
+    __shared__ double xs[KT][33];
+    __shared__ double os[KT][NC + 1];
+    const int tid = threadIdx.x, ti = tid & 31, tr = tid >> 5;
+    const int64_t i0 = int64_t(blockIdx.x) * 32;
+    const int K = B * A;
+    const int k0 = blockIdx.z * kchunk, k1 = min(K, k0 + kchunk);
+    double acc[CG];
+#pragma unroll
+    for (int j = 0; j < CG; ++j) acc[j] = 0.0;
+    for (int kk = k0; kk < k1; kk += KT) {
+        for (int e = tid; e < KT * 32; e += 256) {
+            // coalesced: consecutive threads walk the contiguous index (i when B == 1, else b)
+            const int kl = B == 1 ? (e >> 5) : (e % KT), il = B == 1 ? (e & 31) : (e / KT);
+            const int k = kk + kl;
+            const int64_t i = i0 + il;
+            double v = 0.0;
+            if (k < k1 && i < I) {
+                const int b = k % B, a = k / B;
+                v = static_cast<double>(x[b + i * B + int64_t(a) * B * I]);
+            }
+            xs[kl][il] = v;
+        }
+        for (int e = tid; e < KT * NC; e += 256) {
+            const int kl = e / NC, rl = e % NC;
+            const int k = kk + kl;
+            os[kl][rl] = (k < k1 && rl < rn) ? static_cast<double>(om[int64_t(k) * stride + rl]) : 0.0;
+        }
+        __syncthreads();
+        const int kn = min(KT, k1 - kk);
+        for (int k = 0; k < kn; ++k) {
+            const double xv = xs[k][ti];
+#pragma unroll
+            for (int j = 0; j < CG; ++j) acc[j] = fma(xv, os[k][tr * CG + j], acc[j]);
+        }
+        __syncthreads();
+    }
+    const int64_t i = i0 + ti;
+    if (i < I)
+#pragma unroll
+        for (int j = 0; j < CG; ++j) {
+            const int r = tr * CG + j;
+            if (r < rn) part[(int64_t(blockIdx.z) * rn + r) * I + i] = acc[j];
+        }
+}
+
 __global__ void sketch_reduce_kernel(const double* __restrict__ part, int64_t I, int rn, int S, double* __restrict__ z,
                                      int64_t ldz) {
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < I * rn; t += int64_t(gridDim.x) * blockDim.x) {
@@ -683,7 +738,7 @@ static int sketch_split_cap(int64_t I, int rn) {
         const char* e = std::getenv("TENKIT_SKETCH_CTAS");
         return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(4 * 148);
     }();
-    const int64_t tiles = ((I + 31) / 32) * ((rn + 31) / 32);
+    const int64_t tiles = (I + 31) / 32;  // one CTA covers every column of its 32 rows (rn <= 64)
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (target + tiles - 1) / tiles)));
 }
 
@@ -699,9 +754,29 @@ int launch_sketch_partials(const T* x, int64_t B, int64_t I, int64_t A, const T*
     S = std::max(1, std::min(S, (K + 63) / 64));
     const int kchunk = ((K + S - 1) / S + 63) / 64 * 64;
     S = (K + kchunk - 1) / kchunk;
-    TK_MAXSMEM((sketch_kernel<T>));
-    sketch_kernel<T><<<dim3(gx, gy, S), 256, 0, s>>>(x, static_cast<int>(B), I, static_cast<int>(A), om, pack_stride(rn), rn,
-                                                     kchunk, work);
+    static const bool narrow = [] {  // A/B knob: the 32-column tiles
+        const char* e = std::getenv("TENKIT_SKETCH_NARROW");
+        return e && e[0] == '1';
+    }();
+    if (narrow || rn <= 32 || rn > 64) {  // (one 32-column tile already covers rn <= 32)
+        TK_MAXSMEM((sketch_kernel<T>));
+        sketch_kernel<T><<<dim3(gx, gy, S), 256, 0, s>>>(x, static_cast<int>(B), I, static_cast<int>(A), om, pack_stride(rn),
+                                                         rn, kchunk, work);
+        TK_LAUNCH_CHECK();
+        return S;
+    }
+#define TK_SKETCH_CASE(CG, KT)                                                                                     \
+    case CG:                                                                                                       \
+        sketch_wide_kernel<T, CG, KT><<<dim3(gx, 1, S), 256, 0, s>>>(x, static_cast<int>(B), I, static_cast<int>(A), om, \
+                                                                     pack_stride(rn), rn, kchunk, work);           \
+        break;
+    switch ((rn + 7) / 8) {
+        TK_SKETCH_CASE(5, 32)
+        TK_SKETCH_CASE(6, 32)
+        TK_SKETCH_CASE(7, 32)
+        TK_SKETCH_CASE(8, 32)
+    }
+#undef TK_SKETCH_CASE
     TK_LAUNCH_CHECK();
     return S;
 }
